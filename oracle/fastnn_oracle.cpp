@@ -1,0 +1,649 @@
+// fastnn_oracle.cpp -- CPU restatement of the reference training step (TEST INFRASTRUCTURE ONLY).
+//
+// This file is the parity CHECKER for the B200 path, never the product: only tests/,
+// __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may load it.
+// It restates, in plain scalar C++, the arithmetic of the reference `fastnn` headers
+// (/root/reference/proj/include/fastnn/*.hpp) for the hot path named by BASELINE.json:
+//   train_minibatch (network.hpp:463-472) over dense / conv / 2x2 max-pool / sigmoid / relu /
+//   softmax nodes, softmax_cross_entropy (network.hpp:410-437), sgd_momentum_step
+//   (optim.hpp:69-80), and the RBM cd_k_update (energy.hpp:131-171).
+// Accumulation orders follow the reference's AVX2 kernels so results agree bit-for-bit where the
+// reference is deterministic:
+//   * NT gemm  = mm_dot_rows (gemm.hpp:81-125): 8 fma lanes over k, then the fixed hsum8 tree
+//     (simd.hpp:25-34);
+//   * NN / TN  = mm_axpy_rows (gemm.hpp:30-78): one sequential fma chain over k per output;
+//   * conv     = add_corr_map(_fixed) / im2col (conv.hpp:62-119, :215-273): one fma chain over
+//     (c, di, dj) per output, the same order for both backends;
+//   * conv bwd = padded-valid full conv with flipped, channel-transposed kernels
+//     (layers.hpp:152-193, conv.hpp:337-345) and add_corr_map for the kernel gradient.
+// Pinned against the reference itself: tests/golden/*.npz were produced by oracle/_ref (the
+// reference headers compiled by oracle/Makefile) through tests/golden/make_golden.py.
+//
+// The padded (pad=1) conv backward used by the ImageNet-shaped config is NOT runnable in the
+// reference (layers.hpp:159 throws); here it is the composite of reference primitives described in
+// dx = crop(conv_full(dy, kt)), gk = sum_img corr(pad(x), dy).
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <string>
+#include <vector>
+
+namespace {
+
+// ---------------------------------------------------------------------------- gemm kernels
+
+// hsum8 fixed tree (simd.hpp:25-34): (0+4,1+5,2+6,3+7) -> (s0+s2, s1+s3) -> t0+t1
+inline float hsum8(const float* v) {
+    float s0 = v[0] + v[4], s1 = v[1] + v[5], s2 = v[2] + v[6], s3 = v[3] + v[7];
+    float t0 = s0 + s2, t1 = s1 + s3;
+    return t0 + t1;
+}
+
+// C[i][j] = dot(A.row(i), B.row(j)), gemm.hpp:81-125 order
+void gemm_nt(const float* A, size_t lda, const float* B, size_t ldb, float* C, size_t ldc, size_t M, size_t N,
+             size_t K) {
+    const size_t kt = K / 8 * 8;
+    for (size_t i = 0; i < M; ++i)
+        for (size_t j = 0; j < N; ++j) {
+            float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            const float* a = A + i * lda;
+            const float* b = B + j * ldb;
+            for (size_t k = 0; k < kt; k += 8)
+                for (int l = 0; l < 8; ++l) acc[l] = std::fmaf(a[k + l], b[k + l], acc[l]);
+            for (size_t k = kt; k < K; ++k) acc[k - kt] = std::fmaf(a[k], b[k], acc[k - kt]);
+            C[i * ldc + j] = hsum8(acc);
+        }
+}
+
+// C = op(A) . B with op(A) = A (NN) or A^T (TN): gemm.hpp:30-78, sequential fma over k
+void gemm_axpy(bool a_t, const float* A, size_t lda, const float* B, size_t ldb, float* C, size_t ldc, size_t M,
+               size_t N, size_t K) {
+    for (size_t i = 0; i < M; ++i)
+        for (size_t j = 0; j < N; ++j) {
+            float acc = 0.0f;
+            for (size_t k = 0; k < K; ++k) acc = std::fmaf(a_t ? A[k * lda + i] : A[i * lda + k], B[k * ldb + j], acc);
+            C[i * ldc + j] = acc;
+        }
+}
+
+inline float sigmoidf_ref(float v) { return 1.0f / (1.0f + std::exp(-v)); }  // layers.hpp:279, energy.hpp:36
+
+// ---------------------------------------------------------------------------- conv kernels
+struct Shape4 {
+    size_t n, c, h, w;
+};
+
+// valid cross-correlation with zero padding `pad`; acc chain over (c, di, dj) (conv.hpp:180-273)
+void conv_fwd(const float* x, const Shape4& xs, const float* ker, size_t k, size_t kh, size_t kw, size_t pad,
+              float* y /* n,k,oh,ow */) {
+    const size_t oh = xs.h + 2 * pad - kh + 1, ow = xs.w + 2 * pad - kw + 1;
+    for (size_t b = 0; b < xs.n; ++b)
+        for (size_t f = 0; f < k; ++f)
+            for (size_t oy = 0; oy < oh; ++oy)
+                for (size_t ox = 0; ox < ow; ++ox) {
+                    float acc = 0.0f;
+                    for (size_t c = 0; c < xs.c; ++c)
+                        for (size_t di = 0; di < kh; ++di)
+                            for (size_t dj = 0; dj < kw; ++dj) {
+                                const long long iy = (long long)(oy + di) - (long long)pad;
+                                const long long ix = (long long)(ox + dj) - (long long)pad;
+                                const float v = (iy < 0 || ix < 0 || iy >= (long long)xs.h || ix >= (long long)xs.w)
+                                                    ? 0.0f
+                                                    : x[((b * xs.c + c) * xs.h + iy) * xs.w + ix];
+                                acc = std::fmaf(ker[((f * xs.c + c) * kh + di) * kw + dj], v, acc);
+                            }
+                    y[((b * k + f) * oh + oy) * ow + ox] = acc;
+                }
+}
+
+// dx = crop_pad(full-conv(dy, kt)) via padded-valid with flipped kernels (layers.hpp:161-174,
+// conv.hpp:337-345): dx[b,c,iy,ix] = sum_f sum_{di,dj} dy_pad[b,f,iy+pad+di,ix+pad+dj] * K[f,c,kh-1-di,kw-1-dj]
+// where dy_pad has a (kh-1) zero border. With pad>0 this is the SURVEY 8(c) composite (crop p per border).
+void conv_bwd_data(const float* dy, size_t n, size_t k, size_t oh, size_t ow, const float* ker, size_t c_in,
+                   size_t kh, size_t kw, size_t pad, size_t h, size_t w, float* dx) {
+    for (size_t b = 0; b < n; ++b)
+        for (size_t c = 0; c < c_in; ++c)
+            for (size_t iy = 0; iy < h; ++iy)
+                for (size_t ix = 0; ix < w; ++ix) {
+                    float acc = 0.0f;
+                    for (size_t f = 0; f < k; ++f)
+                        for (size_t di = 0; di < kh; ++di)
+                            for (size_t dj = 0; dj < kw; ++dj) {
+                                // position in the (kh-1)-padded dy
+                                const long long py = (long long)(iy + pad + di) - (long long)(kh - 1);
+                                const long long px = (long long)(ix + pad + dj) - (long long)(kw - 1);
+                                const float v = (py < 0 || px < 0 || py >= (long long)oh || px >= (long long)ow)
+                                                    ? 0.0f
+                                                    : dy[((b * k + f) * oh + py) * ow + px];
+                                acc = std::fmaf(v, ker[((f * c_in + c) * kh + (kh - 1 - di)) * kw + (kw - 1 - dj)], acc);
+                            }
+                    dx[((b * c_in + c) * h + iy) * w + ix] = acc;
+                }
+}
+
+// gk[f,c] += sum_img corr(x[img,c] (padded), dy[img,f]) (layers.hpp:176-184, add_corr_map conv.hpp:62-89)
+void conv_bwd_filter(const float* x, const Shape4& xs, const float* dy, size_t k, size_t oh, size_t ow, size_t kh,
+                     size_t kw, size_t pad, float* gk, float* gb) {
+    for (size_t f = 0; f < k; ++f)
+        for (size_t c = 0; c < xs.c; ++c)
+            for (size_t img = 0; img < xs.n; ++img)
+                for (size_t oy = 0; oy < kh; ++oy)
+                    for (size_t ox = 0; ox < kw; ++ox) {
+                        float acc = gk[((f * xs.c + c) * kh + oy) * kw + ox];
+                        for (size_t di = 0; di < oh; ++di)
+                            for (size_t dj = 0; dj < ow; ++dj) {
+                                const long long iy = (long long)(oy + di) - (long long)pad;
+                                const long long ix = (long long)(ox + dj) - (long long)pad;
+                                const float v = (iy < 0 || ix < 0 || iy >= (long long)xs.h || ix >= (long long)xs.w)
+                                                    ? 0.0f
+                                                    : x[((img * xs.c + c) * xs.h + iy) * xs.w + ix];
+                                acc = std::fmaf(dy[((img * k + f) * oh + di) * ow + dj], v, acc);
+                            }
+                        gk[((f * xs.c + c) * kh + oy) * kw + ox] = acc;
+                    }
+    for (size_t img = 0; img < xs.n; ++img)  // layers.hpp:185-191, serial
+        for (size_t f = 0; f < k; ++f)
+            for (size_t p = 0; p < oh * ow; ++p) gb[f] += dy[(img * k + f) * oh * ow + p];
+}
+
+// ---------------------------------------------------------------------------- network
+enum Kind { Dense = 0, Conv = 1, MaxPool = 2, Sigmoid = 3, Relu = 4, Softmax = 5, Dropout = 6, BatchNorm = 7, Flatten = 8 };
+
+struct Layer {
+    int kind = Dense;
+    // extents of one sample at the input / output of this node
+    std::vector<size_t> in_shape, out_shape;
+    // dense: w (out,in), conv: kernels (k,c,kh,kw); b per unit
+    size_t out = 0, in = 0, k = 0, c = 0, kh = 0, kw = 0, h = 0, w = 0, pad = 0;
+    std::vector<float> wv, bv, gw, gb, vw, vb;
+    std::vector<float> x_cache, y_cache, argmax;
+};
+
+size_t numel(const std::vector<size_t>& s) {
+    size_t n = 1;
+    for (size_t e : s) n *= e;
+    return n;
+}
+
+struct Net {
+    std::vector<Layer> layers;
+    std::vector<size_t> input;
+    float lr = 0.1f, mom = 0.9f, wd = 0.0f;
+    std::string err;
+};
+
+// glorot_fill (layers.hpp:40-48): U(+-sqrt(6/(fan_in+fan_out))), row-major draws
+void glorot(std::vector<float>& t, size_t fan_in, size_t fan_out, std::mt19937& rng) {
+    const float limit = std::sqrt(6.0f / static_cast<float>(fan_in + fan_out));
+    std::uniform_real_distribution<float> dist(-limit, limit);
+    for (float& v : t) v = dist(rng);
+}
+
+std::vector<float> forward(Net& net, const float* x, size_t B) {
+    std::vector<float> cur(x, x + B * numel(net.input));
+    for (Layer& L : net.layers) {
+        const size_t per_in = numel(L.in_shape), per_out = numel(L.out_shape);
+        std::vector<float> y(B * per_out, 0.0f);
+        switch (L.kind) {
+            case Dense: {  // dense_forward layers.hpp:74-89
+                L.x_cache = cur;
+                gemm_nt(cur.data(), L.in, L.wv.data(), L.in, y.data(), L.out, B, L.out, L.in);
+                for (size_t r = 0; r < B; ++r)
+                    for (size_t j = 0; j < L.out; ++j) y[r * L.out + j] += L.bv[j];
+                break;
+            }
+            case Conv: {  // conv_forward layers.hpp:132-148
+                L.x_cache = cur;
+                conv_fwd(cur.data(), {B, L.c, L.h, L.w}, L.wv.data(), L.k, L.kh, L.kw, L.pad, y.data());
+                const size_t plane = L.out_shape[1] * L.out_shape[2];
+                for (size_t m = 0; m < B * L.k; ++m)
+                    for (size_t p = 0; p < plane; ++p) y[m * plane + p] += L.bv[m % L.k];
+                break;
+            }
+            case MaxPool: {  // pool_forward layers.hpp:205-238 (ties keep the first index)
+                const size_t ch = L.in_shape[0], h = L.in_shape[1], w = L.in_shape[2], oh = h / 2, ow = w / 2;
+                L.argmax.assign(B * per_out, 0.0f);
+                for (size_t m = 0; m < B * ch; ++m)
+                    for (size_t oy = 0; oy < oh; ++oy)
+                        for (size_t ox = 0; ox < ow; ++ox) {
+                            const float* r0 = &cur[(m * h + 2 * oy) * w];
+                            const float* r1 = &cur[(m * h + 2 * oy + 1) * w];
+                            const float v[4] = {r0[2 * ox], r0[2 * ox + 1], r1[2 * ox], r1[2 * ox + 1]};
+                            int best = 0;
+                            for (int i = 1; i < 4; ++i)
+                                if (v[i] > v[best]) best = i;
+                            y[(m * oh + oy) * ow + ox] = v[best];
+                            L.argmax[(m * oh + oy) * ow + ox] = (float)best;
+                        }
+                break;
+            }
+            case Sigmoid:
+                for (size_t i = 0; i < y.size(); ++i) y[i] = sigmoidf_ref(cur[i]);
+                L.y_cache = y;
+                break;
+            case Relu:
+                for (size_t i = 0; i < y.size(); ++i) y[i] = cur[i] > 0.0f ? cur[i] : 0.0f;
+                L.y_cache = y;
+                break;
+            case Softmax: {  // softmax layers.hpp:301-320
+                const size_t cols = per_in;
+                for (size_t r = 0; r < B; ++r) {
+                    const float* p = &cur[r * cols];
+                    float* q = &y[r * cols];
+                    float m = p[0];
+                    for (size_t j = 1; j < cols; ++j) m = std::max(m, p[j]);
+                    float sum = 0.0f;
+                    for (size_t j = 0; j < cols; ++j) {
+                        q[j] = std::exp(p[j] - m);
+                        sum += q[j];
+                    }
+                    for (size_t j = 0; j < cols; ++j) q[j] /= sum;
+                }
+                break;
+            }
+            case Flatten:  // NCHW rows repacked contiguously: identity on dense storage (network.hpp:43-53)
+                y = cur;
+                break;
+            default:
+                break;
+        }
+        (void)per_in;
+        cur.swap(y);
+    }
+    return cur;
+}
+
+// backward pass + gradient accumulation (network.hpp:463-467); dlogits scaled by B_global
+double backward(Net& net, const std::vector<float>& pred, const int* labels, size_t B, size_t B_global) {
+    const size_t C = numel(net.layers.back().out_shape);
+    // softmax_cross_entropy network.hpp:410-437 (dlogits = (p - y)/B, loss in double)
+    std::vector<float> g(B * C);
+    double loss = 0.0;
+    for (size_t r = 0; r < B; ++r) {
+        for (size_t j = 0; j < C; ++j) {
+            const float yv = (size_t)labels[r] == j ? 1.0f : 0.0f;
+            g[r * C + j] = (pred[r * C + j] - yv) / (float)B_global;
+        }
+        loss -= std::log(std::max((double)pred[r * C + labels[r]], 1e-300));
+    }
+    for (size_t li = net.layers.size(); li-- > 0;) {
+        Layer& L = net.layers[li];
+        const size_t per_in = numel(L.in_shape);
+        std::vector<float> dx(B * per_in, 0.0f);
+        switch (L.kind) {
+            case Dense: {  // dense_backward layers.hpp:92-107
+                gemm_axpy(false, g.data(), L.out, L.wv.data(), L.in, dx.data(), L.in, B, L.in, L.out);
+                std::vector<float> step(L.out * L.in);
+                gemm_axpy(true, g.data(), L.out, L.x_cache.data(), L.in, step.data(), L.in, L.out, L.in, B);
+                for (size_t i = 0; i < step.size(); ++i) L.gw[i] += 1.0f * step[i];
+                for (size_t r = 0; r < B; ++r)
+                    for (size_t j = 0; j < L.out; ++j) L.gb[j] += g[r * L.out + j];
+                break;
+            }
+            case Conv: {  // conv_backward layers.hpp:152-193
+                const size_t oh = L.out_shape[1], ow = L.out_shape[2];
+                conv_bwd_data(g.data(), B, L.k, oh, ow, L.wv.data(), L.c, L.kh, L.kw, L.pad, L.h, L.w, dx.data());
+                conv_bwd_filter(L.x_cache.data(), {B, L.c, L.h, L.w}, g.data(), L.k, oh, ow, L.kh, L.kw, L.pad,
+                                L.gw.data(), L.gb.data());
+                break;
+            }
+            case MaxPool: {  // pool_backward layers.hpp:240-271
+                const size_t ch = L.in_shape[0], h = L.in_shape[1], w = L.in_shape[2], oh = h / 2, ow = w / 2;
+                for (size_t m = 0; m < B * ch; ++m)
+                    for (size_t oy = 0; oy < oh; ++oy)
+                        for (size_t ox = 0; ox < ow; ++ox) {
+                            const int best = (int)L.argmax[(m * oh + oy) * ow + ox];
+                            dx[(m * h + 2 * oy + best / 2) * w + 2 * ox + best % 2] = g[(m * oh + oy) * ow + ox];
+                        }
+                break;
+            }
+            case Sigmoid:  // activation_gradient layers.hpp:284-298
+                for (size_t i = 0; i < dx.size(); ++i) dx[i] = g[i] * L.y_cache[i] * (1.0f - L.y_cache[i]);
+                break;
+            case Relu:
+                for (size_t i = 0; i < dx.size(); ++i) dx[i] = L.y_cache[i] > 0.0f ? g[i] : 0.0f;
+                break;
+            case Softmax:  // pass-through (network.hpp:139-144)
+            case Flatten:
+                dx = g;
+                break;
+            default:
+                break;
+        }
+        g.swap(dx);
+    }
+    return loss / (double)B_global;
+}
+
+// sgd_momentum_step optim.hpp:69-80
+void sgd(std::vector<float>& p, std::vector<float>& v, const std::vector<float>& grad, float lr, float mom, float wd) {
+    for (size_t i = 0; i < p.size(); ++i) {
+        const float g = grad[i] + wd * p[i];
+        v[i] = mom * v[i] - lr * g;
+        p[i] += v[i];
+    }
+}
+
+void apply(Net& net) {  // network.hpp:468-470
+    if (net.lr != 0.0f)
+        for (Layer& L : net.layers)
+            if (L.kind == Dense || L.kind == Conv) {
+                sgd(L.wv, L.vw, L.gw, net.lr, net.mom, net.wd);
+                sgd(L.bv, L.vb, L.gb, net.lr, net.mom, net.wd);
+            }
+    for (Layer& L : net.layers) {
+        std::fill(L.gw.begin(), L.gw.end(), 0.0f);
+        std::fill(L.gb.begin(), L.gb.end(), 0.0f);
+    }
+}
+
+struct ParamSlot {
+    std::vector<float>* val;
+    std::vector<float>* grad;
+    std::vector<float>* vel;
+};
+
+std::vector<ParamSlot> params(Net& net) {  // trainable() order: w then b per layer (network.hpp:83, :100, :244-249)
+    std::vector<ParamSlot> out;
+    for (Layer& L : net.layers)
+        if (L.kind == Dense || L.kind == Conv) {
+            out.push_back({&L.wv, &L.gw, &L.vw});
+            out.push_back({&L.bv, &L.gb, &L.vb});
+        }
+    return out;
+}
+
+}  // namespace
+
+extern "C" {
+
+struct orc_layer {
+    int kind;
+    long long in, out, k, kh, kw, pad;
+    float p;
+};
+
+// build_network (network.hpp:284-375) restricted to the hot-path node kinds, plus a conv pad
+// (the reference's LayerDesc cannot express it; SURVEY 8(c) composite for config 5).
+void* orc_net_create(int input_rank, const long long* input, const orc_layer* descs, int n_layers, float lr, float mom,
+                     float wd, unsigned seed, char* err, int errlen) {
+    auto fail = [&](const std::string& m) -> void* {
+        if (err && errlen > 0) {
+            std::strncpy(err, m.c_str(), (size_t)errlen - 1);
+            err[errlen - 1] = 0;
+        }
+        return nullptr;
+    };
+    if (n_layers < 1) return fail("network spec has no layers");
+    if (input_rank != 1 && input_rank != 3) return fail("network spec input must have 1 or 3 extents");
+    auto net = std::make_unique<Net>();
+    net->lr = lr;
+    net->mom = mom;
+    net->wd = wd;
+    for (int i = 0; i < input_rank; ++i) net->input.push_back((size_t)input[i]);
+    std::vector<size_t> cur = net->input;
+    for (int i = 0; i < n_layers; ++i) {
+        const orc_layer& d = descs[i];
+        Layer L;
+        L.kind = d.kind;
+        if (d.kind == Dense && cur.size() == 3) {  // implicit flatten (network.hpp:309-312)
+            Layer F;
+            F.kind = Flatten;
+            F.in_shape = cur;
+            F.out_shape = {numel(cur)};
+            net->layers.push_back(F);
+            cur = F.out_shape;
+        }
+        L.in_shape = cur;
+        switch (d.kind) {
+            case Dense:
+                if ((long long)cur[0] != d.in) return fail("dense input extent mismatch");
+                L.in = (size_t)d.in;
+                L.out = (size_t)d.out;
+                L.wv.assign(L.out * L.in, 0.0f);
+                L.bv.assign(L.out, 0.0f);
+                cur = {L.out};
+                break;
+            case Conv:
+                if (cur.size() != 3) return fail("conv needs (c,h,w)");
+                L.c = cur[0];
+                L.h = cur[1];
+                L.w = cur[2];
+                L.k = (size_t)d.k;
+                L.kh = (size_t)d.kh;
+                L.kw = (size_t)d.kw;
+                L.pad = (size_t)d.pad;
+                L.wv.assign(L.k * L.c * L.kh * L.kw, 0.0f);
+                L.bv.assign(L.k, 0.0f);
+                cur = {L.k, L.h + 2 * L.pad - L.kh + 1, L.w + 2 * L.pad - L.kw + 1};
+                break;
+            case MaxPool:
+                if (cur.size() != 3 || cur[1] % 2 || cur[2] % 2) return fail("maxpool needs even (c,h,w)");
+                cur = {cur[0], cur[1] / 2, cur[2] / 2};
+                break;
+            case Sigmoid:
+            case Relu:
+                break;
+            case Softmax:
+                if (cur.size() != 1 || i + 1 != n_layers) return fail("softmax must be the final flat layer");
+                break;
+            case Flatten:
+                cur = {numel(cur)};
+                break;
+            default:
+                return fail("layer kind not on the hot path (dropout/batchnorm)");
+        }
+        L.out_shape = cur;
+        L.gw.assign(L.wv.size(), 0.0f);
+        L.gb.assign(L.bv.size(), 0.0f);
+        L.vw.assign(L.wv.size(), 0.0f);
+        L.vb.assign(L.bv.size(), 0.0f);
+        net->layers.push_back(std::move(L));
+    }
+    std::mt19937 init_rng(seed);  // network.hpp:369-373: dense and conv, in layer order
+    for (Layer& L : net->layers) {
+        if (L.kind == Dense) glorot(L.wv, L.in, L.out, init_rng);
+        if (L.kind == Conv) glorot(L.wv, L.c * L.kh * L.kw, L.k * L.kh * L.kw, init_rng);
+    }
+    return net.release();
+}
+
+void orc_net_destroy(void* h) { delete static_cast<Net*>(h); }
+
+int orc_net_num_params(void* h) { return (int)params(*static_cast<Net*>(h)).size(); }
+
+long long orc_net_param_size(void* h, int idx) { return (long long)params(*static_cast<Net*>(h))[idx].val->size(); }
+
+// which: 0 value, 1 grad, 2 velocity
+void orc_net_get(void* h, int idx, int which, float* out) {
+    ParamSlot s = params(*static_cast<Net*>(h))[idx];
+    const std::vector<float>* v = which == 0 ? s.val : which == 1 ? s.grad : s.vel;
+    std::memcpy(out, v->data(), v->size() * sizeof(float));
+}
+
+void orc_net_set(void* h, int idx, int which, const float* in) {
+    ParamSlot s = params(*static_cast<Net*>(h))[idx];
+    std::vector<float>* v = which == 0 ? s.val : which == 1 ? s.grad : s.vel;
+    std::memcpy(v->data(), in, v->size() * sizeof(float));
+}
+
+void orc_net_set_hparams(void* h, float lr, float mom, float wd) {
+    Net* n = static_cast<Net*>(h);
+    n->lr = lr;
+    n->mom = mom;
+    n->wd = wd;
+}
+
+// forward (training) + backward with gradients accumulated; dlogits scaled by 1/B_global so a
+// data-parallel shard's gradients sum to the full-batch gradient. Returns the shard's loss share.
+double orc_net_forward_backward(void* h, const float* x, const int* labels, long long B, long long B_global,
+                                float* probs_out) {
+    Net& net = *static_cast<Net*>(h);
+    std::vector<float> pred = forward(net, x, (size_t)B);
+    if (probs_out) std::memcpy(probs_out, pred.data(), pred.size() * sizeof(float));
+    return backward(net, pred, labels, (size_t)B, (size_t)B_global);
+}
+
+void orc_net_apply(void* h) { apply(*static_cast<Net*>(h)); }
+
+// train_minibatch network.hpp:463-472
+double orc_net_train_minibatch(void* h, const float* x, const int* labels, long long B) {
+    const double loss = orc_net_forward_backward(h, x, labels, B, B, nullptr);
+    orc_net_apply(h);
+    return loss;
+}
+
+// forward_batch + argmax_row (network.hpp:66-72, :402): first maximum wins
+void orc_net_forward(void* h, const float* x, long long B, float* probs, int* argmax) {
+    Net& net = *static_cast<Net*>(h);
+    std::vector<float> pred = forward(net, x, (size_t)B);
+    const size_t C = pred.size() / (size_t)B;
+    if (probs) std::memcpy(probs, pred.data(), pred.size() * sizeof(float));
+    if (argmax)
+        for (long long r = 0; r < B; ++r) {
+            size_t best = 0;
+            for (size_t j = 1; j < C; ++j)
+                if (pred[r * C + j] > pred[r * C + best]) best = j;
+            argmax[r] = (int)best;
+        }
+}
+
+// ---------------------------------------------------------------------------- op level
+// gemm (gemm.hpp:225-229): C = op(A) . op(B), dense row-major operands
+void orc_gemm(int ta, int tb, const float* A, const float* B, float* C, long long M, long long N, long long K) {
+    if (ta && tb) {  // gemm_blocked transposes A first (gemm.hpp:199), then NT
+        std::vector<float> at((size_t)(M * K));
+        for (long long i = 0; i < M; ++i)
+            for (long long k = 0; k < K; ++k) at[(size_t)(i * K + k)] = A[k * M + i];
+        gemm_nt(at.data(), (size_t)K, B, (size_t)K, C, (size_t)N, (size_t)M, (size_t)N, (size_t)K);
+    } else if (tb) {
+        gemm_nt(A, (size_t)K, B, (size_t)K, C, (size_t)N, (size_t)M, (size_t)N, (size_t)K);
+    } else {
+        gemm_axpy(ta != 0, A, ta ? (size_t)M : (size_t)K, B, (size_t)N, C, (size_t)N, (size_t)M, (size_t)N,
+                  (size_t)K);
+    }
+}
+
+void orc_conv_forward(const float* x, long long n, long long c, long long h, long long w, const float* ker,
+                      const float* bias, long long k, long long kh, long long kw, long long pad, float* y) {
+    conv_fwd(x, {(size_t)n, (size_t)c, (size_t)h, (size_t)w}, ker, (size_t)k, (size_t)kh, (size_t)kw, (size_t)pad, y);
+    const size_t plane = (size_t)((h + 2 * pad - kh + 1) * (w + 2 * pad - kw + 1));
+    if (bias)
+        for (size_t m = 0; m < (size_t)(n * k); ++m)
+            for (size_t p = 0; p < plane; ++p) y[m * plane + p] += bias[m % (size_t)k];
+}
+
+void orc_conv_backward(const float* x, long long n, long long c, long long h, long long w, const float* ker,
+                       long long k, long long kh, long long kw, long long pad, const float* dy, float* dx, float* gk,
+                       float* gb) {
+    const size_t oh = (size_t)(h + 2 * pad - kh + 1), ow = (size_t)(w + 2 * pad - kw + 1);
+    if (dx)
+        conv_bwd_data(dy, (size_t)n, (size_t)k, oh, ow, ker, (size_t)c, (size_t)kh, (size_t)kw, (size_t)pad, (size_t)h,
+                      (size_t)w, dx);
+    if (gk && gb)
+        conv_bwd_filter(x, {(size_t)n, (size_t)c, (size_t)h, (size_t)w}, dy, (size_t)k, oh, ow, (size_t)kh, (size_t)kw,
+                        (size_t)pad, gk, gb);
+}
+
+void orc_sgd_momentum_step(float* p, float* v, const float* g, long long n, float lr, float mom, float wd) {
+    for (long long i = 0; i < n; ++i) {
+        const float gg = g[i] + wd * p[i];
+        v[i] = mom * v[i] - lr * gg;
+        p[i] += v[i];
+    }
+}
+
+// ---------------------------------------------------------------------------- RBM CD-1
+// cd_k_update (energy.hpp:131-171) for binary units with k = 1 and the Bernoulli draws supplied:
+// h_s = (u < (double)sigmoid(a)) is exactly bernoulli_distribution(p)(mt19937) when u is the
+// generate_canonical<double,53> stream (random.h:3741-3749). Shard form: statistics over the local
+// rows, scaled by lr / B_global. If d* outputs are given, the deltas are written instead of applied.
+double orc_rbm_cd1(long long H, long long V, float* W, float* bv, float* bh, const float* v0, long long B,
+                   long long B_global, float lr, const double* u, float* h0_out, float* hs_out, float* v1_out,
+                   float* h1_out, float* dW, float* dbh, float* dbv) {
+    const size_t h = (size_t)H, vis = (size_t)V, b = (size_t)B;
+    std::vector<float> h0(b * h), hs(b * h), v1(b * vis), h1(b * h);
+    // rbm_hidden_given_visible (energy.hpp:101-110): NT gemm, row bias, unit rule
+    gemm_nt(v0, vis, W, vis, h0.data(), h, b, h, vis);
+    for (size_t r = 0; r < b; ++r)
+        for (size_t j = 0; j < h; ++j) {
+            const float a = h0[r * h + j] + bh[j];
+            const float p = sigmoidf_ref(a);
+            h0[r * h + j] = p;
+            hs[r * h + j] = (u[r * h + j] < (double)p) ? 1.0f : 0.0f;
+        }
+    // rbm_visible_given_hidden (energy.hpp:112-120): NN gemm
+    gemm_axpy(false, hs.data(), h, W, vis, v1.data(), vis, b, vis, h);
+    for (size_t r = 0; r < b; ++r)
+        for (size_t j = 0; j < vis; ++j) v1[r * vis + j] = sigmoidf_ref(v1[r * vis + j] + bv[j]);
+    double recon = 0.0;  // sq_diff_per_row energy.hpp:84-96
+    for (size_t i = 0; i < b * vis; ++i) {
+        const double d = double(v0[i]) - double(v1[i]);
+        recon += d * d;
+    }
+    gemm_nt(v1.data(), vis, W, vis, h1.data(), h, b, h, vis);
+    for (size_t r = 0; r < b; ++r)
+        for (size_t j = 0; j < h; ++j) h1[r * h + j] = sigmoidf_ref(h1[r * h + j] + bh[j]);
+    std::vector<float> pos(h * vis), neg(h * vis);
+    gemm_axpy(true, h0.data(), h, v0, vis, pos.data(), vis, h, vis, b);
+    gemm_axpy(true, h1.data(), h, v1.data(), vis, neg.data(), vis, h, vis, b);
+    const float scale = lr / static_cast<float>(B_global);
+    if (dW) {
+        for (size_t i = 0; i < h * vis; ++i) dW[i] = scale * (pos[i] - neg[i]);
+        for (size_t j = 0; j < h; ++j) dbh[j] = 0.0f;
+        for (size_t j = 0; j < vis; ++j) dbv[j] = 0.0f;
+        for (size_t r = 0; r < b; ++r)
+            for (size_t j = 0; j < h; ++j) dbh[j] += scale * (h0[r * h + j] - h1[r * h + j]);
+        for (size_t r = 0; r < b; ++r)
+            for (size_t j = 0; j < vis; ++j) dbv[j] += scale * (v0[r * vis + j] - v1[r * vis + j]);
+    } else {
+        for (size_t i = 0; i < h * vis; ++i) W[i] += scale * (pos[i] - neg[i]);
+        for (size_t r = 0; r < b; ++r)
+            for (size_t j = 0; j < h; ++j) bh[j] += scale * (h0[r * h + j] - h1[r * h + j]);
+        for (size_t r = 0; r < b; ++r)
+            for (size_t j = 0; j < vis; ++j) bv[j] += scale * (v0[r * vis + j] - v1[r * vis + j]);
+    }
+    if (h0_out) std::memcpy(h0_out, h0.data(), h0.size() * sizeof(float));
+    if (hs_out) std::memcpy(hs_out, hs.data(), hs.size() * sizeof(float));
+    if (v1_out) std::memcpy(v1_out, v1.data(), v1.size() * sizeof(float));
+    if (h1_out) std::memcpy(h1_out, h1.data(), h1.size() * sizeof(float));
+    return recon / double(B_global);
+}
+
+// Rbm::init (energy.hpp:31): glorot on w only, biases zero
+void orc_rbm_init(long long H, long long V, unsigned seed, float* W) {
+    std::mt19937 rng(seed);
+    std::vector<float> w((size_t)(H * V));
+    glorot(w, (size_t)V, (size_t)H, rng);
+    std::memcpy(W, w.data(), w.size() * sizeof(float));
+}
+
+// ---------------------------------------------------------------------------- synthetic inputs
+// The exact libstdc++ distributions the reference's tests and BASELINE.md use.
+void orc_uniform_f32(unsigned seed, float lo, float hi, long long n, float* out) {
+    std::mt19937 rng(seed);
+    std::uniform_real_distribution<float> d(lo, hi);
+    for (long long i = 0; i < n; ++i) out[i] = d(rng);
+}
+
+void orc_canonical_f64(unsigned seed, long long n, double* out) {
+    std::mt19937 rng(seed);
+    for (long long i = 0; i < n; ++i) out[i] = std::generate_canonical<double, 53>(rng);
+}
+
+void orc_bernoulli_f32(unsigned seed, double p, long long n, float* out) {
+    std::mt19937 rng(seed);
+    std::bernoulli_distribution d(p);
+    for (long long i = 0; i < n; ++i) out[i] = d(rng) ? 1.0f : 0.0f;
+}
+
+void orc_uniform_int(unsigned seed, int lo, int hi, long long n, int* out) {
+    std::mt19937 rng(seed);
+    std::uniform_int_distribution<int> d(lo, hi);
+    for (long long i = 0; i < n; ++i) out[i] = d(rng);
+}
+
+}  // extern "C"
