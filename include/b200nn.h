@@ -1,0 +1,164 @@
+/* b200nn.h -- C ABI of the B200-native training step (libb200nn.so).
+ *
+ * The drop-in boundary for the reference's hot path. The reference (fastnn) is header-only C++
+ * with no C ABI; each entry point below replaces the reference interface cited beside it, with
+ * plain pointers and sizes (no C++ or torch types). Host-side C++ mirroring fastnn's API
+ * (include/b200nn.hpp) and the Python binding (paper_1804_04512_b200/_lib.py) sit on top.
+ *
+ * Conventions
+ *  - Every call returns a status; 0 = B2N_OK. On failure b2n_last_error() gives the message
+ *    (thread-local). Status codes map one-to-one onto fastnn's typed exceptions
+ *    (config.hpp:11-57), which the C++ wrapper rethrows.
+ *  - "host" pointers are ordinary (ideally pinned) CPU memory; "dev" pointers are CUDA device
+ *    memory on the object's device. Dense row-major layouts, fastnn logical order
+ *    (NCHW for images, (out, in) for dense weights, (k, c, kh, kw) for conv kernels).
+ *  - Objects are single-thread affine (fastnn layers are not re-entrant).
+ */
+#ifndef B200NN_H
+#define B200NN_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes == fastnn error types */
+enum {
+    B2N_OK = 0,
+    B2N_ESHAPE = 1,  /* ShapeError   */
+    B2N_EPARAM = 2,  /* ParamError   */
+    B2N_ELABEL = 3,  /* LabelError   */
+    B2N_ECUDA = 4,   /* CUDA runtime / driver failure */
+    B2N_ENCCL = 5,   /* NCCL failure */
+    B2N_EOOM = 6,    /* device allocation failure */
+    B2N_ESPEC = 7,   /* SpecError    */
+    B2N_EBOUNDS = 8, /* BoundsError  */
+    B2N_EINTERNAL = 9
+};
+
+/* fastnn::LayerDesc::Kind numbering (network.hpp:195) */
+enum {
+    B2N_DENSE = 0,
+    B2N_CONV = 1,
+    B2N_MAXPOOL = 2,
+    B2N_SIGMOID = 3,
+    B2N_RELU = 4,
+    B2N_SOFTMAX = 5,
+    B2N_DROPOUT = 6,
+    B2N_BATCHNORM = 7,
+    B2N_FLATTEN = 8
+};
+
+/* tensor-core precision policy: 3xTF32 (split hi/lo, ~fp32; default) or 1xTF32 (fast) */
+enum { B2N_TF32X3 = 0, B2N_TF32 = 1 };
+
+/* parameter views for get/set */
+enum { B2N_VALUE = 0, B2N_GRAD = 1, B2N_VELOCITY = 2 };
+
+/* == fastnn::LayerDesc (network.hpp:194-223) plus a conv zero-padding field (`pad`) that the
+ *    reference's ConvShape has (conv.hpp:21) but its LayerDesc cannot set. */
+typedef struct b2n_layer_desc {
+    int kind;
+    long long in, out;    /* dense extents */
+    long long k, kh, kw;  /* conv extents */
+    long long pad;        /* conv zero padding */
+    float p;              /* dropout probability (dropout is outside the hot path: ESPEC) */
+} b2n_layer_desc;
+
+/* == fastnn::NetworkSpec (network.hpp:225-234) */
+typedef struct b2n_network_spec {
+    int input_rank; /* 1: {features}, 3: {c, h, w} */
+    long long input[3];
+    const b2n_layer_desc* layers;
+    int n_layers;
+    int optimizer; /* 0 = SgdMomentum (optim.hpp:11); others ESPEC */
+    float lr, momentum, weight_decay;
+    long long batch_size;
+    unsigned seed;
+} b2n_network_spec;
+
+typedef struct b2n_net b2n_net;
+typedef struct b2n_rbm b2n_rbm;
+
+const char* b2n_last_error(void);
+int b2n_version(void);
+int b2n_device_count(int* n);
+
+/* ---- network: replaces build_network / train_minibatch / forward_batch (network.hpp:284-484) ---- */
+
+/* build_network (network.hpp:284-375): same validation (ESPEC), same seeded Glorot init
+ * (layers.hpp:40-48, identical std::mt19937 draws), parameters resident on `device`. */
+int b2n_build_network(const b2n_network_spec* spec, int device, int precision, b2n_net** out);
+int b2n_net_destroy(b2n_net* net);
+
+/* Network::trainable() order (network.hpp:244-249): w then b per dense / conv layer */
+int b2n_net_num_params(b2n_net* net, int* n);
+int b2n_net_param_shape(b2n_net* net, int idx, int* rank, long long dims[4]);
+int b2n_net_get_param(b2n_net* net, int idx, int which, float* host);
+int b2n_net_set_param(b2n_net* net, int idx, int which, const float* host);
+int b2n_net_set_hparams(b2n_net* net, float lr, float momentum, float weight_decay);
+
+/* train_minibatch (network.hpp:463-472): forward, softmax-xent, backward, SGD-momentum step
+ * (skipped when lr == 0), gradients cleared. y_onehot is validated like network.hpp:423-432
+ * (ELABEL). Host buffers; returns the mean loss. */
+int b2n_train_minibatch(b2n_net* net, const float* x_host, const float* y_onehot_host, long long batch,
+                        double* loss);
+/* same with int class ids (the shim's one-hot -> id conversion skipped) */
+int b2n_train_minibatch_labels(b2n_net* net, const float* x_host, const int* labels_host, long long batch,
+                               double* loss);
+/* forward_batch + argmax_row (network.hpp:66-72, :402): probs (batch x classes) and first-max ids */
+int b2n_forward_batch(b2n_net* net, const float* x_host, long long batch, float* probs_host, int* argmax_host);
+
+/* Data-parallel pieces. forward_backward leaves the full-batch-scaled gradient
+ * (dlogits / batch_global) in the packed gradient buffer without touching parameters;
+ * apply_update runs the SGD-momentum kernel over the packed buffers. With b2n_net_dp_init the
+ * step allreduces the gradient over NCCL between the two. */
+int b2n_net_forward_backward(b2n_net* net, const float* x_host, const int* labels_host, long long batch,
+                             long long batch_global, double* loss_share);
+int b2n_net_apply_update(b2n_net* net);
+int b2n_net_grad_buffer(b2n_net* net, float** dev_ptr, long long* n_floats);
+int b2n_nccl_unique_id(char id_out[128]);
+int b2n_net_dp_init(b2n_net* net, const char id[128], int rank, int world);
+
+/* Device-resident stepping (throughput measurement): stage a batch into the net's device input
+ * buffers once, then run `steps` whole training steps as CUDA-graph launches on the net's
+ * stream without host synchronisation. b2n_net_loss waits and returns the last step's loss. */
+int b2n_net_stage(b2n_net* net, const float* x_host, const int* labels_host, long long batch);
+int b2n_net_run_staged(b2n_net* net, int steps, long long batch_global);
+int b2n_net_loss(b2n_net* net, double* loss);
+int b2n_net_stream(b2n_net* net, void** cuda_stream);
+int b2n_net_kernels_per_step(b2n_net* net, long long batch, int* n);
+
+/* ---- RBM: replaces Rbm (energy.hpp:16-32) and cd_k_update (energy.hpp:131-171) ---- */
+int b2n_rbm_create(long long hidden, long long visible, int device, int precision, b2n_rbm** out);
+int b2n_rbm_destroy(b2n_rbm* rbm);
+/* Rbm::init (energy.hpp:31): Glorot on w with std::mt19937(seed), zero biases */
+int b2n_rbm_init(b2n_rbm* rbm, unsigned seed);
+int b2n_rbm_set(b2n_rbm* rbm, const float* w_host, const float* bv_host, const float* bh_host);
+int b2n_rbm_get(b2n_rbm* rbm, float* w_host, float* bv_host, float* bh_host);
+/* cd_k_update for binary units. uniforms_host holds the k*batch*hidden draws
+ * std::bernoulli_distribution would consume (generate_canonical<double,53>, row-major per Gibbs
+ * step): h = (u < p) is then bit-exact with the reference's sampling given the same p.
+ * batch_global > batch makes this a data-parallel shard (lr / batch_global scaling). */
+int b2n_cd_k_update(b2n_rbm* rbm, const float* v0_host, long long batch, int k, float lr,
+                    const double* uniforms_host, long long batch_global, double* recon);
+/* the chain states of the last update (h0 mean, h sample, v1 mean, h1 mean), batch-major */
+int b2n_rbm_last_states(b2n_rbm* rbm, float* h0, float* hs, float* v1, float* h1);
+int b2n_rbm_dp_init(b2n_rbm* rbm, const char id[128], int rank, int world);
+int b2n_rbm_stage(b2n_rbm* rbm, const float* v0_host, const double* uniforms_host, long long batch);
+int b2n_rbm_run_staged(b2n_rbm* rbm, int steps, float lr, long long batch_global);
+int b2n_rbm_recon(b2n_rbm* rbm, double* recon);
+int b2n_rbm_stream(b2n_rbm* rbm, void** cuda_stream);
+
+/* ---- op level (device pointers, async on `stream`; NULL = default stream) ---- */
+/* gemm (gemm.hpp:225-229): C = op(A) . op(B); lda/ldb/ldc are row pitches in floats (multiples
+ * of 4, 16-byte aligned bases -- every fastnn tensor satisfies this, tensor.hpp:142) */
+int b2n_gemm(const float* A, long long lda, int transpose_a, const float* B, long long ldb, int transpose_b,
+             float* C, long long ldc, long long M, long long N, long long K, int precision, void* stream);
+/* sgd_momentum_step (optim.hpp:69-80) over n contiguous floats (n % 4 == 0, 16-byte aligned) */
+int b2n_sgd_momentum_step(float* p, float* v, const float* g, long long n, float lr, float momentum,
+                          float weight_decay, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B200NN_H */

@@ -1,0 +1,248 @@
+// b200nn.cu -- the C ABI (include/b200nn.h): status codes + thread-local messages around the
+// device runtime (network.cuh, rbm.cuh, conv.cuh, gemm_tc.cuh). Built by
+// paper_1804_04512_b200/build.py into paper_1804_04512_b200/_build/libb200nn.so for sm_100a.
+#include <cstdio>
+#include <new>
+
+#include "../../include/b200nn.h"
+#include "network.cuh"
+#include "probe.cuh"
+#include "rbm.cuh"
+#include "runtime.cuh"
+
+struct b2n_net {
+    b2n::Net impl;
+    template <class... A>
+    explicit b2n_net(A&&... a) : impl(std::forward<A>(a)...) {}
+};
+struct b2n_rbm {
+    b2n::Rbm impl;
+    template <class... A>
+    explicit b2n_rbm(A&&... a) : impl(std::forward<A>(a)...) {}
+};
+
+namespace {
+thread_local std::string g_last_error;
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        g_last_error.clear();
+        return B2N_OK;
+    } catch (const b2n::Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return B2N_EOOM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return B2N_EINTERNAL;
+    }
+}
+
+#define B2N_REQUIRE(cond, code, msg) \
+    do {                             \
+        if (!(cond)) throw b2n::Error(code, msg); \
+    } while (0)
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+}  // namespace
+
+extern "C" {
+
+const char* b2n_last_error(void) { return g_last_error.c_str(); }
+int b2n_version(void) { return 1; }
+int b2n_device_count(int* n) {
+    return guard([&] { B2N_CUDA(cudaGetDeviceCount(n)); });
+}
+
+// ------------------------------------------------------------------ network
+int b2n_build_network(const b2n_network_spec* spec, int device, int precision, b2n_net** out) {
+    return guard([&] {
+        B2N_REQUIRE(spec && out, B2N_EPARAM, "null argument");
+        *out = new b2n_net(*spec, device, precision);
+    });
+}
+int b2n_net_destroy(b2n_net* net) {
+    return guard([&] { delete net; });
+}
+int b2n_net_num_params(b2n_net* net, int* n) {
+    return guard([&] { *n = net->impl.num_params(); });
+}
+int b2n_net_param_shape(b2n_net* net, int idx, int* rank, long long dims[4]) {
+    return guard([&] {
+        B2N_REQUIRE(idx >= 0 && idx < net->impl.num_params(), B2N_EBOUNDS, "param index out of range");
+        const auto& v = net->impl.param(idx);
+        *rank = (int)v.dims.size();
+        for (size_t i = 0; i < v.dims.size(); ++i) dims[i] = v.dims[i];
+    });
+}
+int b2n_net_get_param(b2n_net* net, int idx, int which, float* host) {
+    return guard([&] { net->impl.get_param(idx, which, host); });
+}
+int b2n_net_set_param(b2n_net* net, int idx, int which, const float* host) {
+    return guard([&] { net->impl.set_param(idx, which, host); });
+}
+int b2n_net_set_hparams(b2n_net* net, float lr, float momentum, float weight_decay) {
+    return guard([&] { net->impl.set_hparams(lr, momentum, weight_decay); });
+}
+
+int b2n_train_minibatch(b2n_net* net, const float* x, const float* y_onehot, long long batch, double* loss) {
+    return guard([&] {
+        // one-hot contract of softmax_cross_entropy (network.hpp:423-432) checked on the host
+        long long C = 0;
+        int rank;
+        long long dims[4];
+        int np = net->impl.num_params();
+        b2n_net_param_shape(net, np - 1, &rank, dims);
+        C = dims[0];
+        std::vector<int> labels((size_t)batch);
+        for (long long r = 0; r < batch; ++r) {
+            long long ones = 0, truth = 0;
+            for (long long j = 0; j < C; ++j) {
+                const float y = y_onehot[r * C + j];
+                if (y == 1.0f) {
+                    ++ones;
+                    truth = j;
+                } else if (y != 0.0f) {
+                    throw b2n::Error(B2N_ELABEL, "softmax_cross_entropy: labels must be one-hot; row " + std::to_string(r));
+                }
+            }
+            if (ones != 1)
+                throw b2n::Error(B2N_ELABEL, "softmax_cross_entropy: labels must be one-hot; row " + std::to_string(r));
+            labels[(size_t)r] = (int)truth;
+        }
+        *loss = net->impl.train(x, labels.data(), batch);
+    });
+}
+int b2n_train_minibatch_labels(b2n_net* net, const float* x, const int* labels, long long batch, double* loss) {
+    return guard([&] { *loss = net->impl.train(x, labels, batch); });
+}
+int b2n_forward_batch(b2n_net* net, const float* x, long long batch, float* probs, int* argmax) {
+    return guard([&] { net->impl.forward(x, batch, probs, argmax); });
+}
+int b2n_net_forward_backward(b2n_net* net, const float* x, const int* labels, long long batch, long long batch_global,
+                             double* loss_share) {
+    return guard([&] { *loss_share = net->impl.forward_backward(x, labels, batch, batch_global); });
+}
+int b2n_net_apply_update(b2n_net* net) {
+    return guard([&] { net->impl.apply_update(); });
+}
+int b2n_net_grad_buffer(b2n_net* net, float** dev_ptr, long long* n) {
+    return guard([&] {
+        *dev_ptr = net->impl.grad_buffer();
+        *n = net->impl.packed_floats();
+    });
+}
+int b2n_nccl_unique_id(char id_out[128]) {
+    return guard([&] {
+        ncclUniqueId uid;
+        b2n::nccl_check(b2n::nccl().getUniqueId(&uid), "ncclGetUniqueId");
+        std::memcpy(id_out, uid.internal, 128);
+    });
+}
+int b2n_net_dp_init(b2n_net* net, const char id[128], int rank, int world) {
+    return guard([&] { net->impl.dp_init(id, rank, world); });
+}
+int b2n_net_stage(b2n_net* net, const float* x, const int* labels, long long batch) {
+    return guard([&] { net->impl.stage(x, labels, batch); });
+}
+int b2n_net_run_staged(b2n_net* net, int steps, long long batch_global) {
+    return guard([&] { net->impl.run_staged(steps, batch_global); });
+}
+int b2n_net_loss(b2n_net* net, double* loss) {
+    return guard([&] { *loss = net->impl.loss(); });
+}
+int b2n_net_stream(b2n_net* net, void** s) {
+    return guard([&] { *s = net->impl.stream(); });
+}
+int b2n_net_kernels_per_step(b2n_net* net, long long batch, int* n) {
+    return guard([&] { *n = net->impl.kernels_per_step(batch); });
+}
+
+// ------------------------------------------------------------------ RBM
+int b2n_rbm_create(long long hidden, long long visible, int device, int precision, b2n_rbm** out) {
+    return guard([&] { *out = new b2n_rbm(hidden, visible, device, precision); });
+}
+int b2n_rbm_destroy(b2n_rbm* r) {
+    return guard([&] { delete r; });
+}
+int b2n_rbm_init(b2n_rbm* r, unsigned seed) {
+    return guard([&] { r->impl.init(seed); });
+}
+int b2n_rbm_set(b2n_rbm* r, const float* w, const float* bv, const float* bh) {
+    return guard([&] { r->impl.set(w, bv, bh); });
+}
+int b2n_rbm_get(b2n_rbm* r, float* w, float* bv, float* bh) {
+    return guard([&] { r->impl.get(w, bv, bh); });
+}
+int b2n_cd_k_update(b2n_rbm* r, const float* v0, long long batch, int k, float lr, const double* u,
+                    long long batch_global, double* recon) {
+    return guard([&] { *recon = r->impl.cd_k(v0, batch, k, lr, u, batch_global ? batch_global : batch); });
+}
+int b2n_rbm_last_states(b2n_rbm* r, float* h0, float* hs, float* v1, float* h1) {
+    return guard([&] { r->impl.last_states(h0, hs, v1, h1); });
+}
+int b2n_rbm_dp_init(b2n_rbm* r, const char id[128], int rank, int world) {
+    return guard([&] { r->impl.dp_init(id, rank, world); });
+}
+int b2n_rbm_stage(b2n_rbm* r, const float* v0, const double* u, long long batch) {
+    return guard([&] { r->impl.stage(v0, u, batch, 1); });
+}
+int b2n_rbm_run_staged(b2n_rbm* r, int steps, float lr, long long batch_global) {
+    return guard([&] { r->impl.run_staged(steps, lr, batch_global); });
+}
+int b2n_rbm_recon(b2n_rbm* r, double* recon) {
+    return guard([&] { *recon = r->impl.recon(); });
+}
+int b2n_rbm_stream(b2n_rbm* r, void** s) {
+    return guard([&] { *s = r->impl.stream(); });
+}
+
+// ------------------------------------------------------------------ op level
+int b2n_gemm(const float* A, long long lda, int ta, const float* B, long long ldb, int tb, float* C, long long ldc,
+             long long M, long long N, long long K, int precision, void* stream) {
+    return guard([&] {
+        B2N_REQUIRE(M > 0 && N > 0 && K > 0, B2N_ESHAPE, "gemm extents must be positive");
+        b2n::EpiParams e = b2n::epi_default();
+        e.C = C;
+        e.ldc = ldc;
+        // op(A) = A (K-major rows of M) or A^T (A stored K x M: MN-major)
+        // op(B) = B^T (B stored N x K: K-major) or B (stored K x N: MN-major)
+        b2n::GemmLaunch g = b2n::plan_gemm((int)M, (int)N, (int)K, {A, lda, ta != 0}, {B, ldb, tb == 0}, b2n::EPI_STORE,
+                                           e, precision == B2N_TF32X3);
+        g.run(as_stream(stream));
+    });
+}
+
+int b2n_sgd_momentum_step(float* p, float* v, const float* g, long long n, float lr, float momentum, float wd,
+                          void* stream) {
+    return guard([&] {
+        B2N_REQUIRE(n % 4 == 0, B2N_ESHAPE, "sgd: n must be a multiple of 4");
+        B2N_REQUIRE(lr > 0.0f, B2N_EPARAM, "optimizer step: lr must be > 0");
+        B2N_REQUIRE(momentum >= 0.0f && momentum < 1.0f, B2N_EPARAM, "optimizer step: momentum must be in [0, 1)");
+        b2n::sgd_packed_kernel<<<b2n::grid_for(n / 4), 256, 0, as_stream(stream)>>>(
+            reinterpret_cast<float4*>(p), reinterpret_cast<float4*>(v), reinterpret_cast<const float4*>(g), n / 4, lr,
+            momentum, wd);
+        B2N_CUDA(cudaGetLastError());
+    });
+}
+
+// bring-up probe (not part of the documented ABI): A is 128 x 32 (K-major, lda) or 32 x 128
+// (MN-major), B is 32 x 32 (K-major rows of N, or MN-major). smem_out: 5120 floats, d_out: 128x32.
+int b2n_debug_probe(const float* A, long long lda, int a_mn, const float* B, long long ldb, int b_mn, float* smem_out,
+                    float* d_out) {
+    return guard([&] {
+        CUtensorMap ma = a_mn ? b2n::make_map_2d(A, 128, 32, lda, 32, 32, true) : b2n::make_map_2d(A, 32, 128, lda, 32, 128);
+        CUtensorMap mb = b_mn ? b2n::make_map_2d(B, 32, 32, ldb, 32, 32, true) : b2n::make_map_2d(B, 32, 32, ldb, 32, 32);
+        const int smem = 16384 + 4096 + 1024 + 256;
+        B2N_CUDA(cudaFuncSetAttribute(b2n::probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        b2n::probe_kernel<<<1, 192, smem>>>(ma, mb, a_mn, b_mn, smem_out, d_out);
+        B2N_CUDA(cudaGetLastError());
+        B2N_CUDA(cudaDeviceSynchronize());
+    });
+}
+
+}  // extern "C"

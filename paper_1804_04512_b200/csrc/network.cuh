@@ -1,0 +1,736 @@
+// network.cuh -- device-resident replacement of fastnn::Network / train_minibatch
+// (network.hpp:236-472). The layer list is planned once per (batch, global batch) into a fixed
+// launch sequence, captured as one CUDA graph:
+//
+//   dense + activation       -> 1 tcgen05 GEMM, bias+act epilogue            (dense_forward+activation_apply)
+//   last dense + softmax     -> 1 tcgen05 GEMM, softmax-xent epilogue         (+softmax_cross_entropy, argmax)
+//   backward, per dense l    -> dX GEMM with act' epilogue (skipped for l=0: its dX is dead)
+//                               dW GEMM over [X | 1] with the SGD-momentum epilogue (gradient of w and b
+//                               in one GEMM: the ones column yields the bias gradient)
+//   conv + act + maxpool     -> conv.cuh implicit-GEMM kernels
+//
+// Parameters live in one packed buffer: a dense layer is W_aug (out x ldw) with b in column `in`,
+// so the forward bias and the SGD update of b ride on the W tiles. Velocity and gradient buffers
+// mirror that layout, which makes the data-parallel allreduce a single NCCL call and the optimizer
+// one vectorised pass.
+#pragma once
+#include <functional>
+#include <map>
+#include <memory>
+#include <random>
+
+#include "conv.cuh"
+#include "nccl_dyn.cuh"
+#include "runtime.cuh"
+
+namespace b2n {
+
+struct DevMem {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void alloc(size_t n) {
+        release();
+        if (n == 0) return;
+        cudaError_t e = cudaMalloc(&p, n);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            throw Error(e == cudaErrorMemoryAllocation ? B2N_EOOM : B2N_ECUDA,
+                        std::string("cudaMalloc(") + std::to_string(n) + "): " + cudaGetErrorString(e));
+        }
+        bytes = n;
+        // zero-fill, then wait for it: the objects' streams are non-blocking and do not order
+        // against the legacy stream cudaMemset runs on
+        B2N_CUDA(cudaMemset(p, 0, n));
+        B2N_CUDA(cudaDeviceSynchronize());
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    ~DevMem() { release(); }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct HostPinned {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void alloc(size_t n) {
+        release();
+        B2N_CUDA(cudaMallocHost(&p, std::max<size_t>(n, 64)));
+        bytes = n;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+    }
+    ~HostPinned() { release(); }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+using Op = std::function<void(cudaStream_t)>;
+
+struct ParamView {  // one fastnn ParamRef (w or b of a layer) inside the packed buffers
+    std::vector<long long> dims;
+    long long off;      // float offset of element (0,0) in the packed buffers
+    long long rows, cols, pitch;  // 2-D view: rows x cols with row pitch (floats)
+};
+
+inline long long numel(const std::vector<long long>& s) {
+    long long n = 1;
+    for (long long e : s) n *= e;
+    return n;
+}
+
+class Net {
+  public:
+    struct Layer {
+        int kind = B2N_DENSE;
+        std::vector<long long> in_shape, out_shape;
+        // dense
+        long long in = 0, out = 0, ldw = 0, off = 0;
+        // conv (+ fused act + pool)
+        ConvGeom g;
+        long long kern_off = 0, bias_off = 0;
+        // fused epilogue choices
+        int act = ACT_NONE;
+        bool pool_after = false;
+        bool softmax_after = false;
+        // activations (device)
+        float* Ain = nullptr;
+        long long ld_in = 0;
+        float* Aout = nullptr;
+        long long ld_out = 0;
+        float* D = nullptr;  // gradient w.r.t. this layer's (pre-activation / pooled) output
+        long long ldd = 0;
+        uint8_t* arg = nullptr;  // pool argmax codes
+        float* Dx = nullptr;     // gradient w.r.t. this layer's input (conv dgrad output)
+    };
+
+    Net(const b2n_network_spec& spec, int device, int precision);
+    ~Net();
+
+    int num_params() const { return (int)params_.size(); }
+    const ParamView& param(int i) const { return params_.at(i); }
+    void get_param(int idx, int which, float* host);
+    void set_param(int idx, int which, const float* host);
+    void set_hparams(float lr, float mom, float wd) {
+        lr_ = lr;
+        mom_ = mom;
+        wd_ = wd;
+        invalidate_plans();
+    }
+
+    double train(const float* x, const int* labels, long long B);
+    double forward_backward(const float* x, const int* labels, long long B, long long Bg);
+    void apply_update();
+    void forward(const float* x, long long B, float* probs, int* argmax);
+    void stage(const float* x, const int* labels, long long B);
+    void run_staged(int steps, long long Bg);
+    double loss();
+    int kernels_per_step(long long B);
+    void dp_init(const char id[128], int rank, int world) {
+        dp_ = std::make_unique<DpComm>();
+        dp_->init(id, rank, world);
+        invalidate_plans();
+    }
+    cudaStream_t stream() const { return stream_; }
+    float* grad_buffer() const { return G_.as<float>(); }
+    long long packed_floats() const { return n_packed_; }
+
+  private:
+    enum Mode { FUSED = 0, SPLIT = 1, FWD = 2, SPLIT_APPLY = 3 };
+    struct Plan {
+        long long B = 0, Bg = 0;
+        std::vector<Op> ops[4];
+        cudaGraphExec_t graph[4] = {nullptr, nullptr, nullptr, nullptr};
+        int nkernels[4] = {0, 0, 0, 0};
+        ~Plan() {
+            for (auto& g : graph)
+                if (g) cudaGraphExecDestroy(g);
+        }
+    };
+
+    void ensure_capacity(long long B);
+    void alloc_activations();
+    Plan& plan_for(long long B, long long Bg);
+    void build_plan(Plan& pl);
+    void launch(Plan& pl, int mode);
+    void stage_inputs(const float* x, const int* labels, long long B);
+    double read_loss(long long B);
+    void invalidate_plans() { plans_.clear(); }
+    void check_train_params() const;
+
+    int device_;
+    bool x3_;
+    cudaStream_t stream_ = nullptr;
+    std::vector<long long> input_;
+    std::vector<Layer> layers_;
+    std::vector<ParamView> params_;
+    long long n_packed_ = 0;
+    long long classes_ = 0;
+    float lr_, mom_, wd_;
+    long long cap_ = 0;
+    DevMem P_, V_, G_;
+    DevMem act_;
+    float* X_ = nullptr;  // network input (augmented with a ones column for a first dense layer)
+    long long ldx_ = 0;
+    int* labels_ = nullptr;
+    double* row_loss_ = nullptr;
+    int* argmax_ = nullptr;
+    float* probs_ = nullptr;
+    float* logits_ = nullptr;  // only when classes > 256 (standalone softmax kernel)
+    long long ldlog_ = 0;
+    HostPinned h_loss_;
+    long long last_B_ = 0, last_Bg_ = 0;
+    std::map<std::pair<long long, long long>, std::unique_ptr<Plan>> plans_;
+    std::unique_ptr<DpComm> dp_;
+    DevMem loss_sum_;  // dp: double partial loss
+};
+
+// --------------------------------------------------------------------------- construction
+inline Net::Net(const b2n_network_spec& spec, int device, int precision)
+    : device_(device), x3_(precision == B2N_TF32X3), lr_(spec.lr), mom_(spec.momentum), wd_(spec.weight_decay) {
+    // validation mirrors build_network (network.hpp:285-300, :303-367)
+    if (spec.n_layers < 1 || !spec.layers) throw Error(B2N_ESPEC, "network spec has no layers");
+    if (spec.input_rank != 1 && spec.input_rank != 3)
+        throw Error(B2N_ESPEC, "network spec input must have 1 or 3 extents; got " + std::to_string(spec.input_rank));
+    for (int i = 0; i < spec.input_rank; ++i)
+        if (spec.input[i] < 1) throw Error(B2N_ESPEC, "network spec input extents must be positive");
+    if (spec.batch_size < 1) throw Error(B2N_ESPEC, "network spec batch_size must be >= 1");
+    if (spec.optimizer != 0) throw Error(B2N_ESPEC, "b200nn: only the SGD-momentum optimizer is on the B200 path");
+    B2N_CUDA(cudaSetDevice(device));
+    B2N_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+    input_.assign(spec.input, spec.input + spec.input_rank);
+
+    auto shape_str = [](const std::vector<long long>& s) {
+        std::string o = "(";
+        for (size_t i = 0; i < s.size(); ++i) o += (i ? "x" : "") + std::to_string(s[i]);
+        return o + ")";
+    };
+    auto mismatch = [&](int idx, const std::vector<long long>& got, const std::string& need) {
+        throw Error(B2N_ESPEC, "network spec: " + (idx == 1 ? std::string("input") : "layer " + std::to_string(idx - 1)) +
+                                   " produces " + shape_str(got) + " but layer " + std::to_string(idx) + " expects " +
+                                   need);
+    };
+    std::vector<long long> cur = input_;
+    for (int i = 0; i < spec.n_layers; ++i) {
+        const b2n_layer_desc& d = spec.layers[i];
+        const int idx = i + 1;
+        switch (d.kind) {
+            case B2N_DENSE: {
+                if (cur.size() == 3) cur = {cur[0] * cur[1] * cur[2]};  // implicit flatten (network.hpp:309-312)
+                if (cur[0] != d.in) mismatch(idx, cur, "dense input extent " + std::to_string(d.in));
+                if (d.out < 1) throw Error(B2N_ESPEC, "dense output extent must be positive");
+                Layer L;
+                L.kind = B2N_DENSE;
+                L.in_shape = cur;
+                L.in = d.in;
+                L.out = d.out;
+                L.ldw = round_up(d.in + 1, 8);
+                cur = {d.out};
+                L.out_shape = cur;
+                layers_.push_back(L);
+                break;
+            }
+            case B2N_CONV: {
+                if (cur.size() != 3) mismatch(idx, cur, "feature maps (c, h, w) for conv");
+                if (d.kh > cur[1] + 2 * d.pad || d.kw > cur[2] + 2 * d.pad)
+                    mismatch(idx, cur, "extents >= the " + std::to_string(d.kh) + "x" + std::to_string(d.kw) + " kernel");
+                if (d.k < 1 || d.kh < 1 || d.kw < 1 || d.pad < 0) throw Error(B2N_ESPEC, "bad conv extents");
+                Layer L;
+                L.kind = B2N_CONV;
+                L.in_shape = cur;
+                L.g.c = (int)cur[0];
+                L.g.h = (int)cur[1];
+                L.g.w = (int)cur[2];
+                L.g.k = (int)d.k;
+                L.g.kh = (int)d.kh;
+                L.g.kw = (int)d.kw;
+                L.g.pad = (int)d.pad;
+                L.g.oh = L.g.h + 2 * L.g.pad - L.g.kh + 1;
+                L.g.ow = L.g.w + 2 * L.g.pad - L.g.kw + 1;
+                cur = {d.k, L.g.oh, L.g.ow};
+                L.out_shape = cur;
+                layers_.push_back(L);
+                break;
+            }
+            case B2N_MAXPOOL: {
+                if (cur.size() != 3) mismatch(idx, cur, "feature maps (c, h, w) for maxpool");
+                if (cur[1] % 2 || cur[2] % 2) mismatch(idx, cur, "even spatial extents for 2x2 pooling");
+                if (layers_.empty() || layers_.back().kind != B2N_CONV || layers_.back().pool_after)
+                    throw Error(B2N_ESPEC, "b200nn: maxpool must follow a conv (+activation) to fuse into its epilogue");
+                layers_.back().pool_after = true;
+                cur = {cur[0], cur[1] / 2, cur[2] / 2};
+                layers_.back().out_shape = cur;
+                break;
+            }
+            case B2N_SIGMOID:
+            case B2N_RELU: {
+                const int a = d.kind == B2N_SIGMOID ? ACT_SIGMOID : ACT_RELU;
+                if (layers_.empty() || layers_.back().act != ACT_NONE || layers_.back().pool_after)
+                    throw Error(B2N_ESPEC, "b200nn: an activation must directly follow a dense or conv layer");
+                layers_.back().act = a;
+                break;
+            }
+            case B2N_SOFTMAX:
+                if (cur.size() != 1) mismatch(idx, cur, "a flat vector for softmax");
+                if (i + 1 != spec.n_layers)
+                    throw Error(B2N_ESPEC, "network spec: softmax (layer " + std::to_string(idx) + ") must be the final layer");
+                if (layers_.empty() || layers_.back().kind != B2N_DENSE || layers_.back().act != ACT_NONE)
+                    throw Error(B2N_ESPEC, "b200nn: softmax must follow a dense layer");
+                layers_.back().softmax_after = true;
+                break;
+            case B2N_FLATTEN:
+                if (cur.size() != 3) mismatch(idx, cur, "feature maps (c, h, w) for flatten");
+                cur = {cur[0] * cur[1] * cur[2]};
+                break;
+            case B2N_DROPOUT:
+            case B2N_BATCHNORM:
+                throw Error(B2N_ESPEC, "b200nn: dropout / batchnorm are outside the B200 hot path (SURVEY 2.1 #9)");
+            default: throw Error(B2N_ESPEC, "unknown layer kind " + std::to_string(d.kind));
+        }
+    }
+    if (!layers_.back().softmax_after || layers_.back().kind != B2N_DENSE)
+        throw Error(B2N_ESPEC, "b200nn: the training step needs a dense + softmax output (network.hpp:465)");
+    for (const Layer& L : layers_)
+        if (L.kind == B2N_CONV && L.pool_after && (L.g.oh % 2 || L.g.ow % 2))
+            throw Error(B2N_ESPEC, "maxpool needs even extents");
+    classes_ = layers_.back().out;
+
+    // packed parameter layout, trainable() order
+    long long off = 0;
+    auto take = [&](long long n) {
+        const long long o = off;
+        off = round_up(off + n, 32);
+        return o;
+    };
+    for (Layer& L : layers_) {
+        if (L.kind == B2N_DENSE) {
+            L.off = take(L.out * L.ldw);
+            params_.push_back({{L.out, L.in}, L.off, L.out, L.in, L.ldw});
+            params_.push_back({{L.out}, L.off + L.in, L.out, 1, L.ldw});
+        } else {
+            const long long kn = (long long)L.g.k * L.g.c * L.g.kh * L.g.kw;
+            L.kern_off = take(kn);
+            L.bias_off = take(L.g.k);
+            params_.push_back({{L.g.k, L.g.c, L.g.kh, L.g.kw}, L.kern_off, 1, kn, kn});
+            params_.push_back({{L.g.k}, L.bias_off, 1, L.g.k, L.g.k});
+        }
+    }
+    n_packed_ = round_up(off, 32);
+    P_.alloc(n_packed_ * 4);
+    V_.alloc(n_packed_ * 4);
+    G_.alloc(n_packed_ * 4);
+    loss_sum_.alloc(64);
+    // seeded Glorot init in layer order (network.hpp:369-373, layers.hpp:40-48), same draws
+    std::mt19937 rng(spec.seed);
+    std::vector<float> host(n_packed_, 0.0f);
+    for (Layer& L : layers_) {
+        long long fan_in, fan_out, rows, cols, pitch, base;
+        if (L.kind == B2N_DENSE) {
+            fan_in = L.in, fan_out = L.out, rows = L.out, cols = L.in, pitch = L.ldw, base = L.off;
+        } else {
+            fan_in = (long long)L.g.c * L.g.kh * L.g.kw, fan_out = (long long)L.g.k * L.g.kh * L.g.kw;
+            rows = 1, cols = (long long)L.g.k * fan_in, pitch = cols, base = L.kern_off;
+        }
+        const float limit = std::sqrt(6.0f / static_cast<float>(fan_in + fan_out));
+        UniformF32 dist(-limit, limit);
+        for (long long r = 0; r < rows; ++r)
+            for (long long j = 0; j < cols; ++j) host[base + r * pitch + j] = dist(rng);
+    }
+    B2N_CUDA(cudaMemcpyAsync(P_.p, host.data(), n_packed_ * 4, cudaMemcpyHostToDevice, stream_));
+    B2N_CUDA(cudaStreamSynchronize(stream_));
+    h_loss_.alloc(sizeof(double) * 4096);
+    ensure_capacity(spec.batch_size);
+}
+
+inline Net::~Net() {
+    plans_.clear();
+    if (stream_) cudaStreamDestroy(stream_);
+}
+
+inline void Net::ensure_capacity(long long B) {
+    if (B <= cap_) return;
+    cap_ = std::max(B, cap_);
+    invalidate_plans();
+    alloc_activations();
+}
+
+inline void Net::alloc_activations() {
+    // one allocation, carved per layer; 256 B alignment per buffer
+    struct Req {
+        void** dst;
+        size_t bytes;
+    };
+    std::vector<Req> reqs;
+    const long long cap = cap_;
+    auto req = [&](void** dst, size_t bytes) { reqs.push_back({dst, (bytes + 255) / 256 * 256}); };
+    const Layer& first = layers_.front();
+    const long long in0 = numel(input_);
+    ldx_ = first.kind == B2N_DENSE ? round_up(in0 + 1, 8) : in0;
+    req((void**)&X_, cap * ldx_ * 4);
+    for (size_t i = 0; i < layers_.size(); ++i) {
+        Layer& L = layers_[i];
+        const bool last = i + 1 == layers_.size();
+        const bool next_dense = !last && layers_[i + 1].kind == B2N_DENSE;
+        if (L.kind == B2N_DENSE) {
+            L.ld_out = round_up(L.out + (next_dense ? 1 : 0), 8);
+            if (!last) req((void**)&L.Aout, cap * L.ld_out * 4);
+            L.ldd = round_up(L.out, 8);
+            req((void**)&L.D, cap * L.ldd * 4);
+        } else {
+            const long long per = numel(L.out_shape);
+            // pooled (or plain) conv output; an augmented row when a dense layer consumes it
+            L.ld_out = next_dense ? round_up(per + 1, 8) : per;
+            req((void**)&L.Aout, cap * L.ld_out * 4);
+            L.ldd = next_dense ? round_up(per, 8) : per;
+            req((void**)&L.D, cap * L.ldd * 4);
+            if (L.pool_after) req((void**)&L.arg, cap * per);
+        }
+    }
+    if (classes_ > 256) {
+        ldlog_ = round_up(classes_ + 1, 8);
+        req((void**)&logits_, cap * ldlog_ * 4);
+    }
+    req((void**)&labels_, cap * 4);
+    req((void**)&row_loss_, cap * 8);
+    req((void**)&argmax_, cap * 4);
+    req((void**)&probs_, cap * classes_ * 4);
+    size_t total = 0;
+    for (auto& r : reqs) total += r.bytes;
+    act_.alloc(total);
+    size_t o = 0;
+    for (auto& r : reqs) {
+        *r.dst = static_cast<char*>(act_.p) + o;
+        o += r.bytes;
+    }
+    // wire inputs and ones columns
+    float* prev = X_;
+    long long ld_prev = ldx_;
+    for (size_t i = 0; i < layers_.size(); ++i) {
+        Layer& L = layers_[i];
+        L.Ain = prev;
+        L.ld_in = ld_prev;
+        if (L.kind == B2N_DENSE) {
+            set_column_kernel<<<grid_for(cap), 256, 0, stream_>>>(L.Ain, cap, L.ld_in, L.in, 1.0f);
+            B2N_CUDA(cudaGetLastError());
+        }
+        prev = L.Aout;
+        ld_prev = L.ld_out;
+    }
+    // conv dgrad targets: the D buffer of the previous layer
+    for (size_t i = 1; i < layers_.size(); ++i) layers_[i].Dx = layers_[i - 1].D;
+    B2N_CUDA(cudaStreamSynchronize(stream_));
+}
+
+inline void Net::check_train_params() const {  // optim.hpp:51-55, only reached when lr != 0 (network.hpp:468)
+    if (lr_ != 0.0f) {
+        if (!(lr_ > 0.0f)) throw Error(B2N_EPARAM, "optimizer step: lr must be > 0");
+        if (mom_ < 0.0f || mom_ >= 1.0f) throw Error(B2N_EPARAM, "optimizer step: momentum must be in [0, 1)");
+    }
+}
+
+// --------------------------------------------------------------------------- planning
+inline Net::Plan& Net::plan_for(long long B, long long Bg) {
+    auto key = std::make_pair(B, Bg);
+    auto it = plans_.find(key);
+    if (it != plans_.end()) return *it->second;
+    auto pl = std::make_unique<Plan>();
+    pl->B = B;
+    pl->Bg = Bg;
+    build_plan(*pl);
+    Plan& ref = *pl;
+    plans_[key] = std::move(pl);
+    return ref;
+}
+
+inline void Net::build_plan(Plan& pl) {
+    const int B = (int)pl.B;
+    float* P = P_.as<float>();
+    float* Vv = V_.as<float>();
+    float* G = G_.as<float>();
+    std::vector<Op> fwd, bwd_fused, bwd_split;
+    int nk_fwd = 0, nk_fused = 0, nk_split = 0;
+    const size_t nl = layers_.size();
+
+    // ---------------- forward
+    for (size_t i = 0; i < nl; ++i) {
+        Layer& L = layers_[i];
+        if (L.kind == B2N_DENSE) {
+            EpiParams e = epi_default();
+            e.bias = P + L.off + L.in;
+            e.bias_stride = L.ldw;
+            const bool fused_softmax = L.softmax_after && L.out <= 256;
+            if (fused_softmax) {
+                e.C = L.D;
+                e.ldc = L.ldd;
+                e.labels = labels_;
+                e.batch_div = (float)pl.Bg;
+                e.row_loss = row_loss_;
+                e.argmax = argmax_;
+                e.probs = probs_;
+                e.ld_probs = classes_;
+            } else if (L.softmax_after) {
+                e.C = logits_;
+                e.ldc = ldlog_;
+                e.act = ACT_NONE;
+            } else {
+                e.C = L.Aout;
+                e.ldc = L.ld_out;
+                e.act = L.act;
+            }
+            GemmLaunch g = plan_gemm(B, (int)L.out, (int)L.in, {L.Ain, L.ld_in, false}, {P + L.off, L.ldw, false},
+                                     fused_softmax ? EPI_SOFTMAX_XENT : EPI_BIAS_ACT, e, x3_);
+            fwd.push_back([g](cudaStream_t s) { g.run(s); });
+            ++nk_fwd;
+            if (L.softmax_after && !fused_softmax) {
+                float* lg = logits_;
+                long long ldl = ldlog_, C = classes_;
+                float* D = L.D;
+                long long ldd = L.ldd;
+                int* lab = labels_;
+                double* rl = row_loss_;
+                int* am = argmax_;
+                float* pr = probs_;
+                float bd = (float)pl.Bg;
+                fwd.push_back([=](cudaStream_t s) {
+                    softmax_xent_rows_kernel<<<(B * 32 + 255) / 256, 256, 0, s>>>(lg, ldl, B, (int)C, lab, bd, D, ldd,
+                                                                                   rl, am, pr, C);
+                });
+                ++nk_fwd;
+                if (ldd < C + 1) throw Error(B2N_EINTERNAL, "dlogits pitch");
+            }
+        } else {
+            ConvFwdLaunch c = plan_conv_fwd(L.g, B, L.Ain, L.ld_in, P + L.kern_off, P + L.bias_off, L.act, L.pool_after,
+                                            L.Aout, L.ld_out, L.arg, x3_);
+            fwd.push_back([c](cudaStream_t s) { c.run(s); });
+            ++nk_fwd;
+        }
+    }
+    // ---------------- backward
+    for (size_t ii = nl; ii-- > 0;) {
+        Layer& L = layers_[ii];
+        if (L.kind == B2N_DENSE) {
+            if (ii > 0) {  // dX with the previous layer's activation derivative fused
+                Layer& Prev = layers_[ii - 1];
+                if (Prev.kind == B2N_DENSE) {
+                    EpiParams e = epi_default();
+                    e.C = Prev.D;
+                    e.ldc = Prev.ldd;
+                    e.aux = Prev.Aout;
+                    e.ld_aux = Prev.ld_out;
+                    e.act = Prev.act;
+                    GemmLaunch g = plan_gemm(B, (int)L.in, (int)L.out, {L.D, L.ldd, false}, {P + L.off, L.ldw, true},
+                                             Prev.act == ACT_NONE ? EPI_STORE : EPI_DACT, e, x3_);
+                    bwd_fused.push_back([g](cudaStream_t s) { g.run(s); });
+                    bwd_split.push_back([g](cudaStream_t s) { g.run(s); });
+                } else {  // conv below: plain dX into the pooled-gradient buffer (act' applied by the conv gather)
+                    EpiParams e = epi_default();
+                    e.C = Prev.D;
+                    e.ldc = Prev.ldd;
+                    GemmLaunch g = plan_gemm(B, (int)L.in, (int)L.out, {L.D, L.ldd, false}, {P + L.off, L.ldw, true},
+                                             EPI_STORE, e, x3_);
+                    bwd_fused.push_back([g](cudaStream_t s) { g.run(s); });
+                    bwd_split.push_back([g](cudaStream_t s) { g.run(s); });
+                }
+                ++nk_fused;
+                ++nk_split;
+            }
+            // dW (+ db through the ones column): M = out, N = in + 1, K = batch
+            EpiParams ef = epi_default();
+            ef.C = P + L.off;
+            ef.ldc = L.ldw;
+            ef.V = Vv + L.off;
+            ef.ldv = L.ldw;
+            ef.lr = lr_;
+            ef.mom = mom_;
+            ef.wd = wd_;
+            GemmLaunch gf = plan_gemm((int)L.out, (int)L.in + 1, B, {L.D, L.ldd, true}, {L.Ain, L.ld_in, true},
+                                      EPI_SGD, ef, x3_);
+            EpiParams es = epi_default();
+            es.C = G + L.off;
+            es.ldc = L.ldw;
+            GemmLaunch gs = plan_gemm((int)L.out, (int)L.in + 1, B, {L.D, L.ldd, true}, {L.Ain, L.ld_in, true},
+                                      EPI_STORE, es, x3_);
+            bwd_fused.push_back([gf](cudaStream_t s) { gf.run(s); });
+            bwd_split.push_back([gs](cudaStream_t s) { gs.run(s); });
+            ++nk_fused;
+            ++nk_split;
+        } else {
+            // conv: dgrad (unless first layer), then wgrad (+ fused SGD on the reduce)
+            const bool first = ii == 0;
+            ConvBwdLaunch cb = plan_conv_bwd(L.g, B, L.Ain, L.ld_in, P + L.kern_off, P + L.bias_off, L.act,
+                                             L.pool_after, L.Aout, L.ld_out, L.arg, L.D, L.ldd,
+                                             first ? nullptr : layers_[ii - 1].D, first ? 0 : layers_[ii - 1].ldd,
+                                             P + L.kern_off, Vv + L.kern_off, P + L.bias_off, Vv + L.bias_off,
+                                             G + L.kern_off, G + L.bias_off, lr_, mom_, wd_, x3_);
+            bwd_fused.push_back([cb](cudaStream_t s) { cb.run(s, true); });
+            bwd_split.push_back([cb](cudaStream_t s) { cb.run(s, false); });
+            nk_fused += cb.kernels();
+            nk_split += cb.kernels();
+        }
+    }
+    pl.ops[FWD] = fwd;
+    pl.nkernels[FWD] = nk_fwd;
+    pl.ops[FUSED] = fwd;
+    pl.ops[FUSED].insert(pl.ops[FUSED].end(), bwd_fused.begin(), bwd_fused.end());
+    pl.nkernels[FUSED] = nk_fwd + nk_fused;
+    pl.ops[SPLIT] = fwd;
+    pl.ops[SPLIT].insert(pl.ops[SPLIT].end(), bwd_split.begin(), bwd_split.end());
+    pl.nkernels[SPLIT] = nk_fwd + nk_split;
+    // data-parallel apply: allreduce(G) then the packed SGD pass
+    float* Pp = P;
+    long long n4 = n_packed_ / 4;
+    float lr = lr_, mom = mom_, wd = wd_;
+    DpComm* dp = dp_.get();
+    long long npk = n_packed_;
+    pl.ops[SPLIT_APPLY].push_back([=](cudaStream_t s) {
+        if (dp) dp->allreduce_f32(G, (size_t)npk, s);
+        sgd_packed_kernel<<<grid_for(n4), 256, 0, s>>>(reinterpret_cast<float4*>(Pp), reinterpret_cast<float4*>(Vv),
+                                                       reinterpret_cast<const float4*>(G), n4, lr, mom, wd);
+    });
+    pl.nkernels[SPLIT_APPLY] = 1;
+}
+
+inline void Net::launch(Plan& pl, int mode) {
+    if (!pl.graph[mode]) {
+        cudaGraph_t graph;
+        B2N_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+        try {
+            for (auto& op : pl.ops[mode]) op(stream_);
+        } catch (...) {
+            cudaStreamEndCapture(stream_, &graph);
+            throw;
+        }
+        B2N_CUDA(cudaStreamEndCapture(stream_, &graph));
+        B2N_CUDA(cudaGraphInstantiate(&pl.graph[mode], graph, 0));
+        cudaGraphDestroy(graph);
+    }
+    B2N_CUDA(cudaGraphLaunch(pl.graph[mode], stream_));
+}
+
+// --------------------------------------------------------------------------- stepping
+inline void Net::stage_inputs(const float* x, const int* labels, long long B) {
+    const long long in0 = numel(input_);
+    B2N_CUDA(cudaMemcpy2DAsync(X_, ldx_ * 4, x, in0 * 4, in0 * 4, B, cudaMemcpyHostToDevice, stream_));
+    if (labels) {
+        for (long long r = 0; r < B; ++r)
+            if (labels[r] < 0 || labels[r] >= classes_)
+                throw Error(B2N_ELABEL, "softmax_cross_entropy: labels must be one-hot; row " + std::to_string(r));
+        B2N_CUDA(cudaMemcpyAsync(labels_, labels, B * 4, cudaMemcpyHostToDevice, stream_));
+    } else {
+        B2N_CUDA(cudaMemsetAsync(labels_, 0, B * 4, stream_));
+    }
+}
+
+inline double Net::read_loss(long long B) {
+    B2N_CUDA(cudaMemcpyAsync(h_loss_.p, row_loss_, B * 8, cudaMemcpyDeviceToHost, stream_));
+    B2N_CUDA(cudaStreamSynchronize(stream_));
+    double loss = 0.0;  // network.hpp:433-435: sequential over rows, then / batch
+    const double* rl = h_loss_.as<double>();
+    for (long long r = 0; r < B; ++r) loss += rl[r];
+    return loss;
+}
+
+inline double Net::train(const float* x, const int* labels, long long B) {
+    if (B < 1) throw Error(B2N_ESHAPE, "network input expects (batch >= 1, ...)");
+    check_train_params();
+    ensure_capacity(B);
+    if (B > 4096) h_loss_.alloc(B * 8);
+    stage_inputs(x, labels, B);
+    if (dp_) {
+        throw Error(B2N_EPARAM, "data-parallel nets step through forward_backward + apply_update");
+    }
+    Plan& pl = plan_for(B, B);
+    launch(pl, lr_ != 0.0f ? FUSED : SPLIT);
+    last_B_ = B;
+    last_Bg_ = B;
+    return read_loss(B) / (double)B;
+}
+
+inline double Net::forward_backward(const float* x, const int* labels, long long B, long long Bg) {
+    if (B < 1 || Bg < B) throw Error(B2N_ESHAPE, "forward_backward: need 1 <= batch <= batch_global");
+    ensure_capacity(B);
+    stage_inputs(x, labels, B);
+    Plan& pl = plan_for(B, Bg);
+    launch(pl, SPLIT);
+    last_B_ = B;
+    last_Bg_ = Bg;
+    return read_loss(B) / (double)Bg;
+}
+
+inline void Net::apply_update() {
+    check_train_params();
+    if (!last_B_) throw Error(B2N_EPARAM, "apply_update before forward_backward");
+    Plan& pl = plan_for(last_B_, last_Bg_);
+    if (lr_ != 0.0f) launch(pl, SPLIT_APPLY);
+    B2N_CUDA(cudaStreamSynchronize(stream_));
+}
+
+inline void Net::forward(const float* x, long long B, float* probs, int* argmax) {
+    if (B < 1) throw Error(B2N_ESHAPE, "forward_batch: batch must be >= 1");
+    ensure_capacity(B);
+    stage_inputs(x, nullptr, B);
+    Plan& pl = plan_for(B, B);
+    launch(pl, FWD);
+    if (probs) B2N_CUDA(cudaMemcpyAsync(probs, probs_, B * classes_ * 4, cudaMemcpyDeviceToHost, stream_));
+    if (argmax) B2N_CUDA(cudaMemcpyAsync(argmax, argmax_, B * 4, cudaMemcpyDeviceToHost, stream_));
+    B2N_CUDA(cudaStreamSynchronize(stream_));
+}
+
+inline void Net::stage(const float* x, const int* labels, long long B) {
+    ensure_capacity(B);
+    stage_inputs(x, labels, B);
+    B2N_CUDA(cudaStreamSynchronize(stream_));
+    last_B_ = B;
+}
+
+inline void Net::run_staged(int steps, long long Bg) {
+    if (!last_B_) throw Error(B2N_EPARAM, "run_staged before stage");
+    check_train_params();
+    Plan& pl = plan_for(last_B_, Bg ? Bg : last_B_);
+    last_Bg_ = pl.Bg;
+    for (int s = 0; s < steps; ++s) {
+        if (dp_) {
+            launch(pl, SPLIT);
+            launch(pl, SPLIT_APPLY);
+        } else {
+            launch(pl, lr_ != 0.0f ? FUSED : SPLIT);
+        }
+    }
+}
+
+inline double Net::loss() { return read_loss(last_B_) / (double)(last_Bg_ ? last_Bg_ : last_B_); }
+
+inline int Net::kernels_per_step(long long B) {
+    Plan& pl = plan_for(B, B);
+    return dp_ ? pl.nkernels[SPLIT] + pl.nkernels[SPLIT_APPLY] : pl.nkernels[lr_ != 0.0f ? FUSED : SPLIT];
+}
+
+// --------------------------------------------------------------------------- params
+inline void Net::get_param(int idx, int which, float* host) {
+    if (idx < 0 || idx >= num_params()) throw Error(B2N_EBOUNDS, "param index out of range");
+    const ParamView& v = params_[idx];
+    const float* base = (which == B2N_VALUE ? P_ : which == B2N_GRAD ? G_ : V_).as<float>() + v.off;
+    B2N_CUDA(cudaMemcpy2DAsync(host, v.cols * 4, base, v.pitch * 4, v.cols * 4, v.rows, cudaMemcpyDeviceToHost,
+                               stream_));
+    B2N_CUDA(cudaStreamSynchronize(stream_));
+}
+
+inline void Net::set_param(int idx, int which, const float* host) {
+    if (idx < 0 || idx >= num_params()) throw Error(B2N_EBOUNDS, "param index out of range");
+    const ParamView& v = params_[idx];
+    float* base = (which == B2N_VALUE ? P_ : which == B2N_GRAD ? G_ : V_).as<float>() + v.off;
+    B2N_CUDA(cudaMemcpy2DAsync(base, v.pitch * 4, host, v.cols * 4, v.cols * 4, v.rows, cudaMemcpyHostToDevice,
+                               stream_));
+    B2N_CUDA(cudaStreamSynchronize(stream_));
+}
+
+}  // namespace b2n

@@ -1,0 +1,292 @@
+// rbm.cuh -- device-resident replacement of fastnn::Rbm + cd_k_update (energy.hpp:16-32, :131-171)
+// for binary units. One CD-k step is k*2 + 2 tcgen05 GEMM launches (4 for CD-1):
+//
+//   h0/hs : Vcat[0:B] . W^T, epilogue sigmoid(+bh) -> h0 (into Hcat[0:B]) and hs = (u < h0)
+//   v1    : hs . W,          epilogue sigmoid(+bv) -> Vcat[B:2B], row partials of (v0 - v1)^2
+//   h1    : Vcat[B:2B] . W^T, epilogue -sigmoid(+bh) -> Hcat[B:2B]
+//   dW    : Hcat^T . Vcat over K = 2B  ->  W_aug += lr/B * acc
+//
+// W_aug is (H+1) x ldw: W in [0:H, 0:V], bh in column V, bv in row H. Hcat carries a +1 / -1
+// column and Vcat a ones column, so the single concatenated-K GEMM yields
+//   [0:H, 0:V] = pos - neg,  [0:H, V] = sum(h0 - h1),  [H, 0:V] = sum(v0 - v1)
+// i.e. the reference's weight update and both bias updates (energy.hpp:148-169) in one pass.
+#pragma once
+#include <random>
+
+#include "nccl_dyn.cuh"
+#include "network.cuh"
+
+namespace b2n {
+
+class Rbm {
+  public:
+    Rbm(long long H, long long V, int device, int precision)
+        : H_(H), V_(V), device_(device), x3_(precision == B2N_TF32X3) {
+        if (H < 1 || V < 1) throw Error(B2N_ESHAPE, "rbm extents must be positive");
+        B2N_CUDA(cudaSetDevice(device));
+        B2N_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+        ldw_ = round_up(V + 1, 8);
+        nW_ = round_up((H + 1) * ldw_, 32);
+        W_.alloc(nW_ * 4);
+        G_.alloc(nW_ * 4);
+        h_recon_.alloc(8 * 1024);
+    }
+    ~Rbm() {
+        plans_.clear();
+        if (stream_) cudaStreamDestroy(stream_);
+    }
+
+    void init(unsigned seed) {  // energy.hpp:31 -> glorot_fill(w, visible, hidden)
+        std::mt19937 rng(seed);
+        const float limit = std::sqrt(6.0f / static_cast<float>(V_ + H_));
+        UniformF32 dist(-limit, limit);
+        std::vector<float> w((size_t)(H_ * V_));
+        for (float& v : w) v = dist(rng);
+        std::vector<float> zh((size_t)H_, 0.0f), zv((size_t)V_, 0.0f);
+        set(w.data(), zv.data(), zh.data());
+    }
+    void set(const float* w, const float* bv, const float* bh) {
+        float* W = W_.as<float>();
+        B2N_CUDA(cudaMemsetAsync(W, 0, nW_ * 4, stream_));
+        B2N_CUDA(cudaMemcpy2DAsync(W, ldw_ * 4, w, V_ * 4, V_ * 4, H_, cudaMemcpyHostToDevice, stream_));
+        B2N_CUDA(cudaMemcpy2DAsync(W + V_, ldw_ * 4, bh, 4, 4, H_, cudaMemcpyHostToDevice, stream_));
+        B2N_CUDA(cudaMemcpyAsync(W + H_ * ldw_, bv, V_ * 4, cudaMemcpyHostToDevice, stream_));
+        B2N_CUDA(cudaStreamSynchronize(stream_));
+    }
+    void get(float* w, float* bv, float* bh) {
+        const float* W = W_.as<float>();
+        if (w) B2N_CUDA(cudaMemcpy2DAsync(w, V_ * 4, W, ldw_ * 4, V_ * 4, H_, cudaMemcpyDeviceToHost, stream_));
+        if (bh) B2N_CUDA(cudaMemcpy2DAsync(bh, 4, W + V_, ldw_ * 4, 4, H_, cudaMemcpyDeviceToHost, stream_));
+        if (bv) B2N_CUDA(cudaMemcpyAsync(bv, W + H_ * ldw_, V_ * 4, cudaMemcpyDeviceToHost, stream_));
+        B2N_CUDA(cudaStreamSynchronize(stream_));
+    }
+
+    double cd_k(const float* v0, long long B, int k, float lr, const double* u, long long Bg) {
+        if (k < 1) throw Error(B2N_EPARAM, "cd_k_update: k must be >= 1, got " + std::to_string(k));
+        if (B < 1 || Bg < B) throw Error(B2N_ESHAPE, "cd_k_update: need 1 <= batch <= batch_global");
+        stage(v0, u, B, k);
+        Plan& pl = plan_for(B, k, lr, Bg);
+        launch(pl);
+        if (dp_) throw Error(B2N_EPARAM, "data-parallel RBM steps through run_staged");
+        last_B_ = B;
+        last_Bg_ = Bg;
+        return recon();
+    }
+    void stage(const float* v0, const double* u, long long B, int k = 1) {
+        ensure_capacity(B, k);
+        float* Vc = Vcat_.as<float>();
+        B2N_CUDA(cudaMemcpy2DAsync(Vc, ldv_ * 4, v0, V_ * 4, V_ * 4, B, cudaMemcpyHostToDevice, stream_));
+        B2N_CUDA(cudaMemcpyAsync(U_.p, u, (size_t)k * B * H_ * 8, cudaMemcpyHostToDevice, stream_));
+        staged_B_ = B;
+        staged_k_ = k;
+    }
+    void run_staged(int steps, float lr, long long Bg) {
+        if (!staged_B_) throw Error(B2N_EPARAM, "run_staged before stage");
+        Plan& pl = plan_for(staged_B_, staged_k_, lr, Bg ? Bg : staged_B_);
+        for (int s = 0; s < steps; ++s) launch(pl);
+        last_B_ = staged_B_;
+        last_Bg_ = pl.Bg;
+    }
+    double recon() {  // sum of the per-(tile,row) partials / batch_global
+        const long long nt = recon_tiles_;
+        B2N_CUDA(cudaMemcpyAsync(h_recon_.p, recon_.p, nt * last_B_ * 8, cudaMemcpyDeviceToHost, stream_));
+        B2N_CUDA(cudaStreamSynchronize(stream_));
+        const double* r = h_recon_.as<double>();
+        double acc = 0.0;
+        for (long long b = 0; b < last_B_; ++b)
+            for (long long t = 0; t < nt; ++t) acc += r[t * cap_ + b];
+        return acc / (double)last_Bg_;
+    }
+    void last_states(float* h0, float* hs, float* v1, float* h1) {
+        const long long B = last_B_;
+        const float* Hc = Hcat_.as<float>();
+        const float* Vc = Vcat_.as<float>();
+        const auto D2H = cudaMemcpyDeviceToHost;
+        if (h0) B2N_CUDA(cudaMemcpy2DAsync(h0, H_ * 4, Hc, ldh_ * 4, H_ * 4, B, D2H, stream_));
+        if (hs) B2N_CUDA(cudaMemcpy2DAsync(hs, H_ * 4, HS_.p, ldhs_ * 4, H_ * 4, B, D2H, stream_));
+        if (v1) B2N_CUDA(cudaMemcpy2DAsync(v1, V_ * 4, Vc + B * ldv_, ldv_ * 4, V_ * 4, B, D2H, stream_));
+        if (h1) B2N_CUDA(cudaMemcpy2DAsync(h1, H_ * 4, Hc + B * ldh_, ldh_ * 4, H_ * 4, B, D2H, stream_));
+        B2N_CUDA(cudaStreamSynchronize(stream_));
+        if (h1) {
+            for (long long i = 0; i < B * H_; ++i) h1[i] = -h1[i];  // stored negated for the dW GEMM
+        }
+    }
+    void dp_init(const char id[128], int rank, int world) {
+        dp_ = std::make_unique<DpComm>();
+        dp_->init(id, rank, world);
+        plans_.clear();
+    }
+    cudaStream_t stream() const { return stream_; }
+    int kernels_per_step() const { return last_kernels_; }
+
+  private:
+    struct Plan {
+        long long B, Bg;
+        int k;
+        float lr;
+        std::vector<Op> ops;
+        int nk = 0;
+        int recon_tiles = 1;
+        cudaGraphExec_t graph = nullptr;
+        ~Plan() {
+            if (graph) cudaGraphExecDestroy(graph);
+        }
+    };
+
+
+    void ensure_capacity(long long B, int k) {
+        if (B <= cap_ && k <= kcap_) return;
+        cap_ = std::max(cap_, B);
+        kcap_ = std::max(kcap_, k);
+        plans_.clear();
+        hcol_B_ = -1;
+        ldv_ = round_up(V_ + 1, 8);
+        ldh_ = round_up(H_ + 1, 8);
+        ldhs_ = round_up(H_, 8);
+        Vcat_.alloc(2 * cap_ * ldv_ * 4);
+        Hcat_.alloc(2 * cap_ * ldh_ * 4);
+        HS_.alloc(cap_ * ldhs_ * 4);
+        U_.alloc((size_t)kcap_ * cap_ * H_ * 8);
+        recon_.alloc((size_t)cap_ * 64 * 8);
+        if (h_recon_.bytes < (size_t)cap_ * 64 * 8) h_recon_.alloc((size_t)cap_ * 64 * 8);
+        set_column_kernel<<<grid_for(2 * cap_), 256, 0, stream_>>>(Vcat_.as<float>(), 2 * cap_, ldv_, V_, 1.0f);
+        B2N_CUDA(cudaGetLastError());
+        B2N_CUDA(cudaStreamSynchronize(stream_));
+    }
+
+    Plan& plan_for(long long B, int k, float lr, long long Bg) {
+        for (auto& p : plans_)
+            if (p->B == B && p->k == k && p->lr == lr && p->Bg == Bg) return *p;
+        auto pl = std::make_unique<Plan>();
+        pl->B = B;
+        pl->k = k;
+        pl->lr = lr;
+        pl->Bg = Bg;
+        build(*pl);
+        plans_.push_back(std::move(pl));
+        return *plans_.back();
+    }
+
+    void build(Plan& pl) {
+        const int B = (int)pl.B;
+        float* W = W_.as<float>();
+        float* G = G_.as<float>();
+        float* Vc = Vcat_.as<float>();
+        float* Hc = Hcat_.as<float>();
+        float* HSp = HS_.as<float>();
+        double* U = U_.as<double>();
+        const int H = (int)H_, V = (int)V_;
+        auto hidden = [&](const float* vin, int epi, float* out, long long ldo, const double* u) {
+            EpiParams e = epi_default();
+            e.C = out;
+            e.ldc = ldo;
+            e.bias = W + V;
+            e.bias_stride = ldw_;
+            e.u = u;
+            e.ldu = H;
+            e.C2 = HSp;
+            e.ldc2 = ldhs_;
+            GemmLaunch g = plan_gemm(B, H, V, {vin, ldv_, false}, {W, ldw_, false}, epi, e, x3_);
+            pl.ops.push_back([g](cudaStream_t s) { g.run(s); });
+            ++pl.nk;
+        };
+        auto visible = [&](double* recon_rows) {
+            EpiParams e = epi_default();
+            e.C = Vc + (long long)B * ldv_;
+            e.ldc = ldv_;
+            e.bias = W + (long long)H * ldw_;
+            e.bias_stride = 1;
+            e.aux = Vc;
+            e.ld_aux = ldv_;
+            e.row_part = recon_rows;
+            e.ld_part = cap_;
+            GemmLaunch g = plan_gemm(B, V, H, {HSp, ldhs_, false}, {W, ldw_, true}, EPI_RBM_VIS, e, x3_);
+            pl.recon_tiles = (int)g.grid.x;
+            pl.ops.push_back([g](cudaStream_t s) { g.run(s); });
+            ++pl.nk;
+        };
+        // CD-k chain (energy.hpp:137-146): h0 mean + first sample share one GEMM
+        hidden(Vc, EPI_RBM_HID, Hc, ldh_, U);
+        for (int step = 1; step <= pl.k; ++step) {
+            visible(step == 1 ? recon_.as<double>() : recon_.as<double>() + (size_t)cap_ * 32);
+            if (step < pl.k) {
+                // resample hidden from v_step into HS (h mean scratch: Hcat[B:2B], overwritten below)
+                hidden(Vc + (long long)B * ldv_, EPI_RBM_HID, Hc + (long long)B * ldh_, ldh_,
+                       U + (size_t)step * B * H);
+            }
+        }
+        hidden(Vc + (long long)B * ldv_, EPI_RBM_NEGHID, Hc + (long long)B * ldh_, ldh_, nullptr);
+        // dW / dbh / dbv in one GEMM over K = 2B
+        const float scale = pl.lr / static_cast<float>(pl.Bg);
+        EpiParams e = epi_default();
+        if (dp_) {
+            e.C = G;
+            e.ldc = ldw_;
+            e.alpha = 1.0f;
+        } else {
+            e.C = W;
+            e.ldc = ldw_;
+            e.alpha = scale;
+        }
+        GemmLaunch g = plan_gemm(H + 1, V + 1, 2 * B, {Hc, ldh_, true}, {Vc, ldv_, true}, dp_ ? EPI_STORE : EPI_AXPY, e,
+                                 x3_);
+        pl.ops.push_back([g](cudaStream_t s) { g.run(s); });
+        ++pl.nk;
+        if (dp_) {
+            DpComm* dp = dp_.get();
+            long long n = nW_;
+            pl.ops.push_back([=](cudaStream_t s) {
+                dp->allreduce_f32(G, (size_t)n, s);
+                axpy_kernel<<<grid_for(n / 4), 256, 0, s>>>(reinterpret_cast<float4*>(W),
+                                                            reinterpret_cast<const float4*>(G), n / 4, scale);
+            });
+            ++pl.nk;
+        }
+        last_kernels_ = pl.nk;
+    }
+
+    void launch(Plan& pl) {
+        if (hcol_B_ != pl.B) {  // the +1 / -1 column of Hcat for this batch split
+            float* Hc = Hcat_.as<float>();
+            const long long B = pl.B;
+            set_column_kernel<<<grid_for(B), 256, 0, stream_>>>(Hc, B, ldh_, H_, 1.0f);
+            set_column_kernel<<<grid_for(B), 256, 0, stream_>>>(Hc + B * ldh_, B, ldh_, H_, -1.0f);
+            B2N_CUDA(cudaGetLastError());
+            hcol_B_ = pl.B;
+        }
+        recon_tiles_ = pl.recon_tiles;
+        if (!pl.graph) {
+            cudaGraph_t graph;
+            B2N_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+            try {
+                for (auto& op : pl.ops) op(stream_);
+            } catch (...) {
+                cudaStreamEndCapture(stream_, &graph);
+                throw;
+            }
+            B2N_CUDA(cudaStreamEndCapture(stream_, &graph));
+            B2N_CUDA(cudaGraphInstantiate(&pl.graph, graph, 0));
+            cudaGraphDestroy(graph);
+        }
+        B2N_CUDA(cudaGraphLaunch(pl.graph, stream_));
+    }
+
+    long long H_, V_;
+    int device_;
+    bool x3_;
+    cudaStream_t stream_ = nullptr;
+    long long ldw_ = 0, nW_ = 0, ldv_ = 0, ldh_ = 0, ldhs_ = 0;
+    long long cap_ = 0;
+    int kcap_ = 0;
+    DevMem W_, G_, Vcat_, Hcat_, HS_, U_, recon_;
+    HostPinned h_recon_;
+    long long staged_B_ = 0, last_B_ = 0, last_Bg_ = 0;
+    int staged_k_ = 1;
+    int last_kernels_ = 0;
+    int recon_tiles_ = 1;
+    long long hcol_B_ = -1;
+    std::vector<std::unique_ptr<Plan>> plans_;
+    std::unique_ptr<DpComm> dp_;
+};
+
+}  // namespace b2n

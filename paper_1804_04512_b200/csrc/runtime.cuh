@@ -1,0 +1,286 @@
+// runtime.cuh -- host-side plumbing shared by every op: typed errors (mirroring fastnn's
+// config.hpp:11-57 hierarchy as status codes), TMA descriptor encoding, GEMM planning / launch,
+// and the bandwidth-bound kernels that are not GEMM epilogues (SGD over packed buffers,
+// standalone softmax-xent for classes > 256, fills).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <limits>
+#include <random>
+#include <cstdint>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/b200nn.h"
+#include "gemm_tc.cuh"
+
+namespace b2n {
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define B2N_CUDA(x)                                                                                        \
+    do {                                                                                                   \
+        cudaError_t e_ = (x);                                                                              \
+        if (e_ != cudaSuccess)                                                                             \
+            throw ::b2n::Error(B2N_ECUDA, std::string(#x) + " failed: " + cudaGetErrorString(e_) + " (" + \
+                                              __FILE__ + ":" + std::to_string(__LINE__) + ")");            \
+    } while (0)
+
+inline long long round_up(long long n, long long m) { return (n + m - 1) / m * m; }
+
+// std::uniform_real_distribution<float>(a, b) as libstdc++ evaluates it (random.h:1907-1909:
+// generate_canonical<float, 24>(urng) * (b - a) + a) with the multiply-add fused, which is what the
+// reference's -march=native build emits (-ffp-contract=fast); spelled out so the init is
+// bit-identical to fastnn::glorot_fill (layers.hpp:40-48) whatever flags compile this file.
+struct UniformF32 {
+    float a, b;
+    UniformF32(float lo, float hi) : a(lo), b(hi) {}
+    template <class R>
+    float operator()(R& rng) {
+        const float u = std::generate_canonical<float, std::numeric_limits<float>::digits>(rng);
+        return std::fma(u, b - a, a);
+    }
+};
+
+// ------------------------------------------------------------------ TMA descriptors
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+inline EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        B2N_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) throw Error(B2N_ECUDA, "cuTensorMapEncodeTiled unavailable");
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// 2-D fp32 map over a row-major matrix of `outer` rows x `inner` logical columns with row pitch
+// `ld` elements; 128 B-swizzled boxes of box_inner (32) x box_outer (16 B atoms for K-major operands,
+// 32 B atoms for MN-major ones); out-of-bounds reads fill zero.
+inline CUtensorMap make_map_2d(const float* base, uint64_t inner, uint64_t outer, uint64_t ld, uint32_t box_inner,
+                               uint32_t box_outer, bool mn_major = false) {
+    if ((reinterpret_cast<uintptr_t>(base) & 15) || ((ld * 4) & 15))
+        throw Error(B2N_ESHAPE, "tensor-core operand needs a 16-byte aligned base and a row pitch that is a "
+                                "multiple of 4 floats (fastnn pads rows to 8, tensor.hpp:142)");
+    CUtensorMap m;
+    cuuint64_t dims[2] = {inner, std::max<uint64_t>(outer, 1)};
+    cuuint64_t strides[1] = {ld * 4};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, es,
+                             CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Error(B2N_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return m;
+}
+
+// ------------------------------------------------------------------ GEMM plan
+// One operand of D = op(A) . op(B). K-major: row-major [rows][K] (fastnn NT side);
+// MN-major: row-major [K][rows] (the transposed side).
+struct Operand {
+    const float* ptr;
+    long long ld;
+    bool mn_major;
+};
+
+struct GemmLaunch {
+    CUtensorMap ma, mb;
+    GemmParams p;
+    int bn = 64;
+    bool x3 = true;
+    dim3 grid;
+    size_t smem = 0;
+    void run(cudaStream_t st) const;
+};
+
+template <int BN, bool X3>
+void launch_gemm_inst(const GemmLaunch& g, cudaStream_t st) {
+    using Cfg = GemmCfg<BN, X3>;
+    static bool attr = [] {
+        B2N_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, X3>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+        return true;
+    }();
+    (void)attr;
+    gemm_tc_kernel<BN, X3><<<g.grid, kThreads, Cfg::SMEM, st>>>(g.ma, g.mb, g.p);
+    B2N_CUDA(cudaGetLastError());
+}
+
+inline void GemmLaunch::run(cudaStream_t st) const {
+#define B2N_G(BNV)                                     \
+    case BNV:                                          \
+        if (x3)                                        \
+            launch_gemm_inst<BNV, true>(*this, st);    \
+        else                                           \
+            launch_gemm_inst<BNV, false>(*this, st);   \
+        break;
+    switch (bn) {
+        B2N_G(16)
+        B2N_G(32)
+        B2N_G(64)
+        B2N_G(128)
+        B2N_G(256)
+        default: throw Error(B2N_ESHAPE, "bad BN");
+    }
+#undef B2N_G
+}
+
+inline int pick_bn(int M, int N, bool b_mn, int epi) {
+    if (epi == EPI_SOFTMAX_XENT) {
+        int bn = N <= 16 ? 16 : N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+        if (b_mn && bn < 32) bn = 32;
+        return bn;
+    }
+    if (N <= 16 && !b_mn) return 16;
+    const int mt = (M + kBM - 1) / kBM;
+    for (int bn : {128, 64}) {
+        if ((long long)mt * ((N + bn - 1) / bn) >= 120) return bn;
+    }
+    return 32;
+}
+
+inline GemmLaunch plan_gemm(int M, int N, int K, Operand A, Operand B, int epi, const EpiParams& ep, bool x3,
+                            int bn = 0) {
+    if (M <= 0 || N <= 0 || K <= 0) throw Error(B2N_ESHAPE, "gemm extents must be positive");
+    GemmLaunch g;
+    g.bn = bn ? bn : pick_bn(M, N, B.mn_major, epi);
+    if (epi == EPI_SOFTMAX_XENT && N > g.bn) throw Error(B2N_ESHAPE, "fused softmax needs classes <= 256");
+    if (B.mn_major && g.bn < 32) g.bn = 32;
+    g.x3 = x3;
+    g.ma = A.mn_major ? make_map_2d(A.ptr, M, K, A.ld, 32, 32, true) : make_map_2d(A.ptr, K, M, A.ld, 32, kBM);
+    g.mb = B.mn_major ? make_map_2d(B.ptr, N, K, B.ld, 32, 32, true) : make_map_2d(B.ptr, K, N, B.ld, 32, g.bn);
+    g.p.M = M;
+    g.p.N = N;
+    g.p.K = K;
+    g.p.a_mn = A.mn_major;
+    g.p.b_mn = B.mn_major;
+    g.p.epi = epi;
+    g.p.ep = ep;
+    g.grid = dim3((N + g.bn - 1) / g.bn, (M + kBM - 1) / kBM, 1);
+    return g;
+}
+
+inline EpiParams epi_default() {
+    EpiParams e;
+    std::memset(&e, 0, sizeof(e));
+    e.alpha = 1.0f;
+    e.batch_div = 1.0f;
+    return e;
+}
+
+// ------------------------------------------------------------------ bandwidth kernels
+// sgd_momentum_step (optim.hpp:69-80) over one packed parameter / velocity / gradient buffer:
+// float4-vectorised, grid-stride, 16 B per thread per access.
+__global__ void sgd_packed_kernel(float4* __restrict__ p, float4* __restrict__ v, const float4* __restrict__ g,
+                                  long long n4, float lr, float mom, float wd) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+        float4 pp = p[i], vv = v[i];
+        const float4 gg = g[i];
+        float gx = gg.x + wd * pp.x, gy = gg.y + wd * pp.y, gz = gg.z + wd * pp.z, gw = gg.w + wd * pp.w;
+        vv.x = mom * vv.x - lr * gx;
+        vv.y = mom * vv.y - lr * gy;
+        vv.z = mom * vv.z - lr * gz;
+        vv.w = mom * vv.w - lr * gw;
+        pp.x += vv.x;
+        pp.y += vv.y;
+        pp.z += vv.z;
+        pp.w += vv.w;
+        p[i] = pp;
+        v[i] = vv;
+    }
+}
+
+__global__ void fill_kernel(float* __restrict__ p, long long n, float v) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
+// ones column of an augmented activation matrix (the bias trick: [X | 1] . [W | b]^T)
+__global__ void set_column_kernel(float* __restrict__ p, long long rows, long long ld, long long col, float v) {
+    long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (r < rows) p[r * ld + col] = v;
+}
+
+// W += alpha * D over a packed buffer (data-parallel RBM update after the allreduce)
+__global__ void axpy_kernel(float4* __restrict__ w, const float4* __restrict__ d, long long n4, float alpha) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+        float4 a = w[i];
+        const float4 b = d[i];
+        a.x += alpha * b.x;
+        a.y += alpha * b.y;
+        a.z += alpha * b.z;
+        a.w += alpha * b.w;
+        w[i] = a;
+    }
+}
+
+// softmax + softmax_cross_entropy for class counts beyond one tensor-core tile: one warp per row,
+// the max / exp-sum / normalise passes run in the reference's sequential order by lane 0 after a
+// warp-parallel max (max is order-independent), so dlogits and loss follow network.hpp:410-437.
+__global__ void softmax_xent_rows_kernel(const float* __restrict__ logits, long long ld, int rows, int cols,
+                                         const int* __restrict__ labels, float batch_div, float* __restrict__ dlogits,
+                                         long long ldd, double* __restrict__ row_loss, int* __restrict__ argmax,
+                                         float* __restrict__ probs, long long ldp) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (warp >= rows) return;
+    const float* z = logits + (long long)warp * ld;
+    float mx = -INFINITY;
+    for (int j = lane; j < cols; j += 32) mx = fmaxf(mx, z[j]);
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    // exp terms in parallel, then the sequential sum (layers.hpp:312-315 order)
+    float* dl = dlogits + (long long)warp * ldd;
+    for (int j = lane; j < cols; j += 32) dl[j] = expf(z[j] - mx);
+    __syncwarp();
+    if (lane == 0) {
+        float sum = 0.0f;
+        for (int j = 0; j < cols; ++j) sum += dl[j];
+        dl[cols] = sum;  // ldd >= cols + 1 guaranteed by the planner
+    }
+    __syncwarp();
+    const float sum = dl[cols];
+    const int label = labels[warp];
+    float bestp = -1.0f;
+    int best = 0;
+    for (int j = lane; j < cols; j += 32) {
+        const float q = dl[j] / sum;
+        if (q > bestp) {
+            bestp = q;
+            best = j;
+        }
+        if (probs) probs[(long long)warp * ldp + j] = q;
+        if (j == label) row_loss[warp] = -log(fmax((double)q, 1e-300));
+        dl[j] = (q - (j == label ? 1.0f : 0.0f)) / batch_div;
+    }
+    for (int o = 16; o; o >>= 1) {  // first-max argmax across lanes
+        const float bp = __shfl_xor_sync(0xffffffffu, bestp, o);
+        const int bi = __shfl_xor_sync(0xffffffffu, best, o);
+        if (bp > bestp || (bp == bestp && bi < best)) {
+            bestp = bp;
+            best = bi;
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+        dl[cols] = 0.0f;
+        if (argmax) argmax[warp] = best;
+    }
+}
+
+inline int grid_for(long long n, int block = 256) {
+    long long g = (n + block - 1) / block;
+    return (int)std::min<long long>(std::max<long long>(g, 1), 148 * 8);
+}
+
+}  // namespace b2n

@@ -1,0 +1,389 @@
+"""Host-side mirror of the reference's hot-path API (fastnn, /root/reference/proj/include/fastnn).
+
+Same names, argument meaning and error types as the reference, backed by the B200 C ABI
+(include/b200nn.h). Tensors are numpy arrays in fastnn's logical layout (NCHW / (out, in) /
+(k, c, kh, kw)); parameters stay resident on the GPU between steps.
+
+    spec = NetworkSpec(input=[784], layers=[LayerDesc.dense(784, 500), LayerDesc.sigmoid(), ...])
+    net = build_network(spec)                      # network.hpp:284
+    loss = train_minibatch(net, x, y_onehot)       # network.hpp:463
+    probs = forward_batch(net, x)                  # network.hpp:402
+    acc = evaluate(net, images, labels)            # network.hpp:474
+    rbm = Rbm(500, 784); rbm.init(seed)            # energy.hpp:16-32
+    recon = cd_k_update(rbm, v0, 1, lr, uniforms)  # energy.hpp:131
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import (BoundsError, CudaError, Error, LabelError, NcclError, ParamError, ShapeError,  # noqa: F401
+                   SpecError)
+
+DENSE, CONV, MAXPOOL, SIGMOID, RELU, SOFTMAX, DROPOUT, BATCHNORM, FLATTEN = range(9)
+TF32X3, TF32 = 0, 1
+VALUE, GRAD, VELOCITY = 0, 1, 2
+
+
+def _f(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_float))
+
+
+def _d(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _i(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_int))
+
+
+@dataclass
+class LayerDesc:
+    """fastnn::LayerDesc (network.hpp:194-223) plus conv `pad`."""
+    kind: int = DENSE
+    in_: int = 0
+    out: int = 0
+    k: int = 0
+    kh: int = 0
+    kw: int = 0
+    pad: int = 0
+    p: float = 0.0
+
+    @staticmethod
+    def dense(i: int, o: int) -> "LayerDesc":
+        return LayerDesc(DENSE, in_=i, out=o)
+
+    @staticmethod
+    def conv(k: int, kh: int, kw: int, pad: int = 0) -> "LayerDesc":
+        return LayerDesc(CONV, k=k, kh=kh, kw=kw, pad=pad)
+
+    @staticmethod
+    def maxpool() -> "LayerDesc":
+        return LayerDesc(MAXPOOL)
+
+    @staticmethod
+    def sigmoid() -> "LayerDesc":
+        return LayerDesc(SIGMOID)
+
+    @staticmethod
+    def relu() -> "LayerDesc":
+        return LayerDesc(RELU)
+
+    @staticmethod
+    def softmax() -> "LayerDesc":
+        return LayerDesc(SOFTMAX)
+
+    @staticmethod
+    def flatten() -> "LayerDesc":
+        return LayerDesc(FLATTEN)
+
+    @staticmethod
+    def dropout(p: float) -> "LayerDesc":
+        return LayerDesc(DROPOUT, p=p)
+
+    @staticmethod
+    def from_dict(d: dict) -> "LayerDesc":
+        return LayerDesc(d["kind"], in_=d.get("in", 0), out=d.get("out", 0), k=d.get("k", 0), kh=d.get("kh", 0),
+                         kw=d.get("kw", 0), pad=d.get("pad", 0), p=d.get("p", 0.0))
+
+
+@dataclass
+class NetworkSpec:
+    """fastnn::NetworkSpec (network.hpp:225-234)."""
+    input: list = field(default_factory=list)
+    layers: list = field(default_factory=list)
+    optimizer: int = 0
+    lr: float = 0.1
+    momentum: float = 0.9
+    weight_decay: float = 0.0
+    batch_size: int = 100
+    seed: int = 42
+
+    @staticmethod
+    def from_dict(d: dict) -> "NetworkSpec":
+        return NetworkSpec(input=list(d["input"]), layers=[LayerDesc.from_dict(x) for x in d["layers"]],
+                           lr=d.get("lr", 0.1), momentum=d.get("momentum", 0.9),
+                           weight_decay=d.get("weight_decay", 0.0), batch_size=d.get("batch_size", 100),
+                           seed=d.get("seed", 42))
+
+
+class Network:
+    """Device-resident fastnn::Network. Build with build_network()."""
+
+    def __init__(self, spec: NetworkSpec, device: int = 0, precision: int = TF32X3):
+        if isinstance(spec, dict):
+            spec = NetworkSpec.from_dict(spec)
+        self.spec = spec
+        arr = (_lib.LayerDescC * max(len(spec.layers), 1))()
+        for i, d in enumerate(spec.layers):
+            arr[i].kind, arr[i].in_, arr[i].out = d.kind, d.in_, d.out
+            arr[i].k, arr[i].kh, arr[i].kw, arr[i].pad, arr[i].p = d.k, d.kh, d.kw, d.pad, d.p
+        cs = _lib.NetworkSpecC()
+        cs.input_rank = len(spec.input)
+        for i, e in enumerate(spec.input[:3]):
+            cs.input[i] = e
+        cs.layers = arr
+        cs.n_layers = len(spec.layers)
+        cs.optimizer = spec.optimizer
+        cs.lr, cs.momentum, cs.weight_decay = spec.lr, spec.momentum, spec.weight_decay
+        cs.batch_size = spec.batch_size
+        cs.seed = spec.seed
+        h = C.c_void_p()
+        _lib.call("b2n_build_network", C.byref(cs), device, precision, C.byref(h))
+        self._h = h
+        self.input = list(spec.input)
+        dense = [d for d in spec.layers if d.kind == DENSE]
+        self.classes = dense[-1].out if dense else 0
+        self.batch_size = spec.batch_size
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.load().b2n_net_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    # ---- fastnn::Network::trainable() surface
+    def num_params(self) -> int:
+        n = C.c_int()
+        _lib.call("b2n_net_num_params", self._h, C.byref(n))
+        return n.value
+
+    def param_shape(self, idx: int) -> tuple:
+        r = C.c_int()
+        dims = (C.c_longlong * 4)()
+        _lib.call("b2n_net_param_shape", self._h, idx, C.byref(r), dims)
+        return tuple(dims[i] for i in range(r.value))
+
+    def get_param(self, idx: int, which: int = VALUE) -> np.ndarray:
+        out = np.zeros(self.param_shape(idx), np.float32)
+        _lib.call("b2n_net_get_param", self._h, idx, which, _f(out))
+        return out
+
+    def set_param(self, idx: int, values, which: int = VALUE) -> None:
+        v = np.ascontiguousarray(values, np.float32).reshape(self.param_shape(idx))
+        _lib.call("b2n_net_set_param", self._h, idx, which, _f(v))
+
+    def params(self, which: int = VALUE) -> list:
+        return [self.get_param(i, which) for i in range(self.num_params())]
+
+    def set_hparams(self, lr: float, momentum: float, weight_decay: float = 0.0) -> None:
+        _lib.call("b2n_net_set_hparams", self._h, lr, momentum, weight_decay)
+
+    # ---- data-parallel pieces
+    def forward_backward(self, x, labels, batch_global: int | None = None) -> float:
+        x = np.ascontiguousarray(x, np.float32)
+        labels = np.ascontiguousarray(labels, np.int32)
+        out = C.c_double()
+        _lib.call("b2n_net_forward_backward", self._h, _f(x), _i(labels), labels.shape[0],
+                  batch_global or labels.shape[0], C.byref(out))
+        return out.value
+
+    def apply_update(self) -> None:
+        _lib.call("b2n_net_apply_update", self._h)
+
+    def dp_init(self, nccl_id: bytes, rank: int, world: int) -> None:
+        _lib.call("b2n_net_dp_init", self._h, nccl_id, rank, world)
+
+    # ---- device-resident stepping (bench)
+    def stage(self, x, labels) -> None:
+        x = np.ascontiguousarray(x, np.float32)
+        labels = np.ascontiguousarray(labels, np.int32)
+        _lib.call("b2n_net_stage", self._h, _f(x), _i(labels), labels.shape[0])
+
+    def run_staged(self, steps: int, batch_global: int = 0) -> None:
+        _lib.call("b2n_net_run_staged", self._h, steps, batch_global)
+
+    def loss(self) -> float:
+        out = C.c_double()
+        _lib.call("b2n_net_loss", self._h, C.byref(out))
+        return out.value
+
+    def stream_handle(self) -> int:
+        s = C.c_void_p()
+        _lib.call("b2n_net_stream", self._h, C.byref(s))
+        return s.value or 0
+
+    def kernels_per_step(self, batch: int) -> int:
+        n = C.c_int()
+        _lib.call("b2n_net_kernels_per_step", self._h, batch, C.byref(n))
+        return n.value
+
+
+def build_network(spec, device: int = 0, precision: int = TF32X3) -> Network:
+    """fastnn::build_network (network.hpp:284-375)."""
+    return Network(spec, device, precision)
+
+
+def _flat_batch(net: Network, x) -> np.ndarray:
+    x = np.ascontiguousarray(x, np.float32)
+    per = int(np.prod(net.input))
+    if x.ndim < 2 or int(np.prod(x.shape[1:])) != per:  # network.hpp:380-392 ingest
+        raise ShapeError("network input expects (batch, " + ", ".join(str(e) for e in net.input) + ")")
+    return x.reshape(x.shape[0], per)
+
+
+def train_minibatch(net: Network, x, y_onehot) -> float:
+    """fastnn::train_minibatch (network.hpp:463-472); y is one-hot (batch, classes)."""
+    xb = _flat_batch(net, x)
+    y = np.ascontiguousarray(y_onehot, np.float32)
+    if y.ndim != 2 or y.shape[0] != xb.shape[0] or y.shape[1] != net.classes:
+        raise ShapeError("softmax_cross_entropy: predictions and labels must both be (batch, classes)")
+    out = C.c_double()
+    _lib.call("b2n_train_minibatch", net.handle, _f(xb), _f(y), xb.shape[0], C.byref(out))
+    return out.value
+
+
+def train_minibatch_labels(net: Network, x, labels) -> float:
+    xb = _flat_batch(net, x)
+    lab = np.ascontiguousarray(labels, np.int32)
+    out = C.c_double()
+    _lib.call("b2n_train_minibatch_labels", net.handle, _f(xb), _i(lab), xb.shape[0], C.byref(out))
+    return out.value
+
+
+def forward_batch(net: Network, x, return_argmax: bool = False):
+    """fastnn::forward_batch (network.hpp:402); optional argmax_row ids (network.hpp:66-72)."""
+    xb = _flat_batch(net, x)
+    probs = np.zeros((xb.shape[0], net.classes), np.float32)
+    am = np.zeros(xb.shape[0], np.int32)
+    _lib.call("b2n_forward_batch", net.handle, _f(xb), xb.shape[0], _f(probs), _i(am))
+    return (probs, am) if return_argmax else probs
+
+
+def evaluate(net: Network, images, labels) -> float:
+    """fastnn::evaluate (network.hpp:474-484): batched inference, first-max argmax accuracy."""
+    images = np.asarray(images, np.float32)
+    labels = np.asarray(labels)
+    if images.shape[0] == 0:
+        raise Error("evaluate: empty dataset")
+    correct = 0
+    for lo in range(0, images.shape[0], net.batch_size):
+        hi = min(lo + net.batch_size, images.shape[0])
+        _, am = forward_batch(net, images[lo:hi], return_argmax=True)
+        correct += int((am == labels[lo:hi]).sum())
+    return correct / images.shape[0]
+
+
+class Rbm:
+    """fastnn::Rbm (energy.hpp:16-32), binary units, resident on the GPU."""
+
+    def __init__(self, hidden: int, visible: int, device: int = 0, precision: int = TF32X3):
+        h = C.c_void_p()
+        _lib.call("b2n_rbm_create", hidden, visible, device, precision, C.byref(h))
+        self._h = h
+        self.hidden, self.visible = hidden, visible
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.load().b2n_rbm_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    def init(self, seed: int) -> None:
+        _lib.call("b2n_rbm_init", self._h, seed)
+
+    def set(self, w, bv, bh) -> None:
+        w = np.ascontiguousarray(w, np.float32)
+        bv = np.ascontiguousarray(bv, np.float32)
+        bh = np.ascontiguousarray(bh, np.float32)
+        if w.shape != (self.hidden, self.visible) or bv.shape != (self.visible,) or bh.shape != (self.hidden,):
+            raise ShapeError("rbm parameter shapes")
+        _lib.call("b2n_rbm_set", self._h, _f(w), _f(bv), _f(bh))
+
+    def get(self):
+        w = np.zeros((self.hidden, self.visible), np.float32)
+        bv = np.zeros(self.visible, np.float32)
+        bh = np.zeros(self.hidden, np.float32)
+        _lib.call("b2n_rbm_get", self._h, _f(w), _f(bv), _f(bh))
+        return w, bv, bh
+
+    def last_states(self, batch: int):
+        h0 = np.zeros((batch, self.hidden), np.float32)
+        hs = np.zeros_like(h0)
+        v1 = np.zeros((batch, self.visible), np.float32)
+        h1 = np.zeros_like(h0)
+        _lib.call("b2n_rbm_last_states", self._h, _f(h0), _f(hs), _f(v1), _f(h1))
+        return h0, hs, v1, h1
+
+    def stage(self, v0, uniforms) -> None:
+        v0 = np.ascontiguousarray(v0, np.float32)
+        u = np.ascontiguousarray(uniforms, np.float64)
+        _lib.call("b2n_rbm_stage", self._h, _f(v0), _d(u), v0.shape[0])
+
+    def run_staged(self, steps: int, lr: float, batch_global: int = 0) -> None:
+        _lib.call("b2n_rbm_run_staged", self._h, steps, lr, batch_global)
+
+    def recon(self) -> float:
+        out = C.c_double()
+        _lib.call("b2n_rbm_recon", self._h, C.byref(out))
+        return out.value
+
+    def stream_handle(self) -> int:
+        s = C.c_void_p()
+        _lib.call("b2n_rbm_stream", self._h, C.byref(s))
+        return s.value or 0
+
+    def dp_init(self, nccl_id: bytes, rank: int, world: int) -> None:
+        _lib.call("b2n_rbm_dp_init", self._h, nccl_id, rank, world)
+
+
+def cd_k_update(rbm: Rbm, v0, k: int, lr: float, uniforms, batch_global: int | None = None) -> float:
+    """fastnn::cd_k_update (energy.hpp:131-171) with the Bernoulli uniforms supplied
+    (k * batch * hidden generate_canonical<double,53> draws, the stream std::bernoulli_distribution
+    consumes from the reference's std::mt19937)."""
+    if k < 1:
+        raise ParamError(f"cd_k_update: k must be >= 1, got {k}")
+    v0 = np.ascontiguousarray(v0, np.float32)
+    if v0.ndim != 2:
+        raise ShapeError("cd_k_update: expected a rank-2 tensor")
+    if v0.shape[1] != rbm.visible:
+        raise ShapeError("cd_k_update: visible extent mismatch")
+    u = np.ascontiguousarray(uniforms, np.float64).ravel()
+    if u.size < k * v0.shape[0] * rbm.hidden:
+        raise ShapeError("cd_k_update: need k * batch * hidden uniforms")
+    out = C.c_double()
+    _lib.call("b2n_cd_k_update", rbm.handle, _f(v0), v0.shape[0], k, lr, _d(u), batch_global or v0.shape[0],
+              C.byref(out))
+    return out.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _lib.call("b2n_nccl_unique_id", buf)
+    return buf.raw
+
+
+# ---- op level on device tensors (torch CUDA tensors: plumbing only)
+def gemm(a, b, transpose_a: bool = False, transpose_b: bool = False, precision: int = TF32X3):
+    """fastnn::gemm (gemm.hpp:225-229) on CUDA tensors: C = op(A) . op(B)."""
+    import torch
+    M = a.shape[1] if transpose_a else a.shape[0]
+    K = a.shape[0] if transpose_a else a.shape[1]
+    kb = b.shape[1] if transpose_b else b.shape[0]
+    N = b.shape[0] if transpose_b else b.shape[1]
+    if K != kb:
+        raise ShapeError(f"gemm inner extents disagree: {K} vs {kb}")
+    c = torch.empty((M, N), dtype=torch.float32, device=a.device)
+    stream = torch.cuda.current_stream(a.device).cuda_stream
+    _lib.call("b2n_gemm", a.data_ptr(), a.stride(0), int(transpose_a), b.data_ptr(), b.stride(0), int(transpose_b),
+              c.data_ptr(), c.stride(0), M, N, K, precision, stream)
+    return c
+
+
+def sgd_momentum_step(p, v, g, lr: float, momentum: float, weight_decay: float = 0.0) -> None:
+    """fastnn::sgd_momentum_step (optim.hpp:69-80) on contiguous CUDA tensors, in place."""
+    import torch
+    stream = torch.cuda.current_stream(p.device).cuda_stream
+    _lib.call("b2n_sgd_momentum_step", p.data_ptr(), v.data_ptr(), g.data_ptr(), p.numel(), lr, momentum,
+              weight_decay, stream)

@@ -1,0 +1,118 @@
+"""The MLP training step (config 1) on the B200 vs the oracle (bit-exact restatement of
+fastnn::train_minibatch, network.hpp:463-472) on identical seeded inputs and weights.
+Tolerance: 3xTF32 GEMMs with fp32 epilogues -> normalized error <= 1e-4 (north_star bar 1e-3)."""
+import numpy as np
+import pytest
+
+from conftest import norm_err
+from oracle import oracle as O
+from paper_1804_04512_b200 import configs as CF
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+def inputs(spec, B, seed=1):
+    per = int(np.prod(spec["input"]))
+    x = O.uniform_f32(seed, B * per).reshape([B] + spec["input"])
+    lab = O.uniform_int(seed + 1, 0, spec["layers"][-2]["out"] - 1, B)
+    return x, lab
+
+
+def test_init_matches_reference_build_network(gpu):
+    from paper_1804_04512_b200 import fastnn as F
+    spec = CF.mlp_spec()
+    net = F.build_network(spec)
+    orc = O.Net(spec)
+    for i in range(net.num_params()):
+        np.testing.assert_array_equal(net.get_param(i).ravel(), orc.get(i))
+
+
+@pytest.mark.parametrize("B", [100, 37, 1, 128, 200])
+def test_mlp_step(gpu, B):
+    from paper_1804_04512_b200 import fastnn as F
+    spec = CF.mlp_spec(B)
+    net = F.build_network(spec)
+    orc = O.Net(spec)
+    x, lab = inputs(spec, B)
+    y = np.zeros((B, 10), np.float32)
+    y[np.arange(B), lab] = 1
+    for step in range(3):
+        lg = F.train_minibatch(net, x, y)
+        lo = orc.train_minibatch(x, lab)
+        assert abs(lg - lo) / abs(lo) < TOL, (step, lg, lo)
+        for i in range(net.num_params()):
+            e = norm_err(net.get_param(i).ravel(), orc.get(i))
+            assert e < TOL, (step, i, e)
+            ev = norm_err(net.get_param(i, F.VELOCITY).ravel(), orc.get(i, 2))
+            assert ev < 1e-3, (step, i, ev)
+
+
+def test_mlp_grads_and_argmax(gpu):
+    from paper_1804_04512_b200 import fastnn as F
+    spec = CF.mlp_spec()
+    net = F.build_network(spec)
+    orc = O.Net(spec)
+    x, lab = inputs(spec, 100)
+    lg = net.forward_backward(x, lab)
+    lo = orc.forward_backward(x, lab)
+    assert abs(lg - lo) / lo < TOL
+    for i in range(net.num_params()):
+        assert norm_err(net.get_param(i, F.GRAD).ravel(), orc.get(i, 1)) < 1e-4
+    probs, am = F.forward_batch(net, x, return_argmax=True)
+    op, oa = orc.forward(x)
+    assert norm_err(probs, op) < 1e-5
+    # argmax bit-exact except where the top-2 probabilities are within float noise
+    top2 = np.sort(op, axis=1)[:, -2:]
+    near = (top2[:, 1] - top2[:, 0]) < 1e-5
+    assert np.array_equal(am[~near], oa[~near])
+
+
+def test_lr_zero_leaves_params(gpu):
+    """test_network.cpp:258-273: lr = 0 reports the loss, parameters untouched."""
+    from paper_1804_04512_b200 import fastnn as F
+    spec = CF.mlp_spec(20)
+    spec["lr"] = 0.0
+    net = F.build_network(spec)
+    before = net.params()
+    x, lab = inputs(spec, 20)
+    y = np.eye(10, dtype=np.float32)[lab]
+    loss = F.train_minibatch(net, x, y)
+    assert loss > 0
+    for a, b in zip(before, net.params()):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_label_and_param_errors(gpu):
+    from paper_1804_04512_b200 import fastnn as F
+    net = F.build_network(CF.mlp_spec(4))
+    x = np.zeros((4, 784), np.float32)
+    with pytest.raises(F.LabelError):
+        F.train_minibatch(net, x, np.full((4, 10), 0.1, np.float32))
+    with pytest.raises(F.ShapeError):
+        F.train_minibatch(net, np.zeros((4, 783), np.float32), np.eye(10, dtype=np.float32)[:4])
+    net.set_hparams(0.1, 1.0, 0.0)
+    with pytest.raises(F.ParamError):
+        F.train_minibatch(net, x, np.eye(10, dtype=np.float32)[:4])
+
+
+def test_data_parallel_shards_sum_to_full_batch(gpu):
+    """8(e): uneven contiguous shards (13,13,13,13,12,12,12,12) with dlogits / B_global; the
+    summed shard gradients equal the full-batch gradient."""
+    from paper_1804_04512_b200 import fastnn as F
+    from paper_1804_04512_b200.dp import shard_bounds
+    spec = CF.mlp_spec()
+    x, lab = inputs(spec, 100)
+    full = F.build_network(spec)
+    full.forward_backward(x, lab)
+    gfull = full.params(F.GRAD)
+    acc = None
+    loss = 0.0
+    for r in range(8):
+        lo, hi = shard_bounds(100, 8, r)
+        net = F.build_network(spec)
+        loss += net.forward_backward(x[lo:hi], lab[lo:hi], batch_global=100)
+        g = net.params(F.GRAD)
+        acc = g if acc is None else [a + b for a, b in zip(acc, g)]
+    for a, b in zip(acc, gfull):
+        assert norm_err(a, b) < 1e-5

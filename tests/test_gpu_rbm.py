@@ -1,0 +1,59 @@
+"""RBM CD-1 (config 2) on the B200 vs the oracle restatement of cd_k_update (energy.hpp:131-171).
+Sampling contract: hs == (u < h0) bit-exactly on the kernel's own h0; cross-implementation flips
+only where |u - p_ref| is within the probability error."""
+import numpy as np
+import pytest
+
+from conftest import norm_err
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("B,H,V", [(100, 500, 784), (10, 50, 78), (1, 8, 4), (130, 64, 100)])
+def test_cd1_step(gpu, B, H, V):
+    from paper_1804_04512_b200 import fastnn as F
+    rbm = F.Rbm(H, V)
+    rbm.init(42)
+    W = O.rbm_init(H, V, 42)
+    w0, bv0, bh0 = rbm.get()
+    np.testing.assert_array_equal(w0, W)
+    v0 = O.bernoulli_f32(3, 0.5, B * V).reshape(B, V)
+    u = O.canonical_f64(5, B * H).reshape(B, H)
+    bv = np.zeros(V, np.float32)
+    bh = np.zeros(H, np.float32)
+    recon_g = F.cd_k_update(rbm, v0, 1, 0.1, u)
+    h0, hs, v1, h1 = rbm.last_states(B)
+    # bit-exact sampling on the kernel's own probabilities
+    np.testing.assert_array_equal(hs, (u < h0.astype(np.float64)).astype(np.float32))
+    recon_o, Wo, bvo, bho, ex = O.rbm_cd1(W, bv, bh, v0, 0.1, u)
+    assert norm_err(h0, ex["h0"]) < 1e-5
+    flips = hs != ex["hs"]
+    dp = np.abs(h0 - ex["h0"]).max()
+    assert np.all(np.abs(u[flips] - ex["h0"][flips]) <= dp + 1e-7), "flip outside the probability error band"
+    if not flips.any():
+        assert norm_err(v1, ex["v1"]) < 1e-4
+        wg, bvg, bhg = rbm.get()
+        assert norm_err(wg - W, Wo - W) < 1e-3
+        assert norm_err(bvg, bvo) < 1e-3
+        assert norm_err(bhg, bho) < 1e-3
+        assert abs(recon_g - recon_o) / recon_o < 1e-5
+
+
+def test_cd1_zero_model_fixed_point(gpu):
+    """test_energy.cpp:120-131: v0 = 0.5 on the zero model gives a zero update."""
+    from paper_1804_04512_b200 import fastnn as F
+    rbm = F.Rbm(2, 3)
+    rbm.set(np.zeros((2, 3), np.float32), np.zeros(3, np.float32), np.zeros(2, np.float32))
+    v0 = np.full((4, 3), 0.5, np.float32)
+    u = O.canonical_f64(3, 8)
+    F.cd_k_update(rbm, v0, 1, 0.1, u)
+    w, bv, bh = rbm.get()
+    assert not w.any() and not bv.any() and not bh.any()
+
+
+def test_k_below_one(gpu):
+    from paper_1804_04512_b200 import fastnn as F
+    rbm = F.Rbm(2, 2)
+    with pytest.raises(F.ParamError):
+        F.cd_k_update(rbm, np.zeros((1, 2), np.float32), 0, 0.1, np.zeros(2))
