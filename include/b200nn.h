@@ -127,6 +127,11 @@ int b2n_net_run_staged(b2n_net* net, int steps, long long batch_global);
 int b2n_net_loss(b2n_net* net, double* loss);
 int b2n_net_stream(b2n_net* net, void** cuda_stream);
 int b2n_net_kernels_per_step(b2n_net* net, long long batch, int* n);
+/* Per-op device time of the planned step (un-graphed launches, CUDA events between ops), averaged
+ * over `steps`: stats[i*4 + {0,1,2,3}] = {ms, algorithmic FLOPs, algorithmic HBM bytes, kernels};
+ * names gets the op names, newline-separated. */
+int b2n_net_profile(b2n_net* net, long long batch, int steps, int max_ops, double* stats, char* names, int names_len,
+                    int* n_ops);
 
 /* ---- RBM: replaces Rbm (energy.hpp:16-32) and cd_k_update (energy.hpp:131-171) ---- */
 int b2n_rbm_create(long long hidden, long long visible, int device, int precision, b2n_rbm** out);
@@ -148,6 +153,9 @@ int b2n_rbm_stage(b2n_rbm* rbm, const float* v0_host, const double* uniforms_hos
 int b2n_rbm_run_staged(b2n_rbm* rbm, int steps, float lr, long long batch_global);
 int b2n_rbm_recon(b2n_rbm* rbm, double* recon);
 int b2n_rbm_stream(b2n_rbm* rbm, void** cuda_stream);
+int b2n_rbm_kernels_per_step(b2n_rbm* rbm, int* n);
+int b2n_rbm_profile(b2n_rbm* rbm, int steps, float lr, long long batch_global, int max_ops, double* stats, char* names,
+                    int names_len, int* n_ops);
 
 /* ---- op level (device pointers, async on `stream`; NULL = default stream) ---- */
 /* gemm (gemm.hpp:225-229): C = op(A) . op(B); lda/ldb/ldc are row pitches in floats (multiples

@@ -92,6 +92,9 @@ _SIGS = {
     "b2n_net_loss": ([_VP, _D], C.c_int),
     "b2n_net_stream": ([_VP, C.POINTER(_VP)], C.c_int),
     "b2n_net_kernels_per_step": ([_VP, C.c_longlong, _I], C.c_int),
+    "b2n_net_profile": ([_VP, C.c_longlong, C.c_int, C.c_int, _D, C.c_char_p, C.c_int, _I], C.c_int),
+    "b2n_rbm_profile": ([_VP, C.c_int, C.c_float, C.c_longlong, C.c_int, _D, C.c_char_p, C.c_int, _I], C.c_int),
+    "b2n_rbm_kernels_per_step": ([_VP, _I], C.c_int),
     "b2n_rbm_create": ([C.c_longlong, C.c_longlong, C.c_int, C.c_int, C.POINTER(_VP)], C.c_int),
     "b2n_rbm_destroy": ([_VP], C.c_int),
     "b2n_rbm_init": ([_VP, C.c_uint], C.c_int),

@@ -162,6 +162,31 @@ int b2n_net_kernels_per_step(b2n_net* net, long long batch, int* n) {
     return guard([&] { *n = net->impl.kernels_per_step(batch); });
 }
 
+namespace {
+void export_stats(const std::vector<b2n::OpStats>& st, int max_ops, double* stats, char* names, int names_len,
+                  int* n_ops) {
+    *n_ops = (int)st.size();
+    std::string joined;
+    for (size_t i = 0; i < st.size() && (int)i < max_ops; ++i) {
+        stats[i * 4 + 0] = st[i].ms;
+        stats[i * 4 + 1] = st[i].flops;
+        stats[i * 4 + 2] = st[i].bytes;
+        stats[i * 4 + 3] = st[i].kernels;
+        joined += st[i].name;
+        joined.push_back('\n');
+    }
+    if (names && names_len > 0) {
+        std::strncpy(names, joined.c_str(), (size_t)names_len - 1);
+        names[names_len - 1] = 0;
+    }
+}
+}  // namespace
+
+int b2n_net_profile(b2n_net* net, long long batch, int steps, int max_ops, double* stats, char* names, int names_len,
+                    int* n_ops) {
+    return guard([&] { export_stats(net->impl.profile(batch, steps), max_ops, stats, names, names_len, n_ops); });
+}
+
 // ------------------------------------------------------------------ RBM
 int b2n_rbm_create(long long hidden, long long visible, int device, int precision, b2n_rbm** out) {
     return guard([&] { *out = new b2n_rbm(hidden, visible, device, precision); });
@@ -196,6 +221,13 @@ int b2n_rbm_run_staged(b2n_rbm* r, int steps, float lr, long long batch_global) 
 }
 int b2n_rbm_recon(b2n_rbm* r, double* recon) {
     return guard([&] { *recon = r->impl.recon(); });
+}
+int b2n_rbm_profile(b2n_rbm* r, int steps, float lr, long long batch_global, int max_ops, double* stats, char* names,
+                    int names_len, int* n_ops) {
+    return guard([&] { export_stats(r->impl.profile(steps, lr, batch_global), max_ops, stats, names, names_len, n_ops); });
+}
+int b2n_rbm_kernels_per_step(b2n_rbm* r, int* n) {
+    return guard([&] { *n = r->impl.kernels_per_step(); });
 }
 int b2n_rbm_stream(b2n_rbm* r, void** s) {
     return guard([&] { *s = r->impl.stream(); });
@@ -242,6 +274,23 @@ int b2n_debug_probe(const float* A, long long lda, int a_mn, const float* B, lon
         b2n::probe_kernel<<<1, 192, smem>>>(ma, mb, a_mn, b_mn, smem_out, d_out);
         B2N_CUDA(cudaGetLastError());
         B2N_CUDA(cudaDeviceSynchronize());
+    });
+}
+
+// bring-up: time one GEMM with a per-CTA %globaltimer trace (trace: grid * 64 u64)
+int b2n_debug_gemm_trace(const float* A, long long lda, int ta, const float* B, long long ldb, int tb, float* C,
+                         long long ldc, long long M, long long N, long long K, int precision, int bn,
+                         unsigned long long* trace, int* grid_out) {
+    return guard([&] {
+        b2n::EpiParams e = b2n::epi_default();
+        e.C = C;
+        e.ldc = ldc;
+        b2n::GemmLaunch g = b2n::plan_gemm((int)M, (int)N, (int)K, {A, lda, ta != 0}, {B, ldb, tb == 0}, b2n::EPI_STORE,
+                                           e, precision == B2N_TF32X3, bn);
+        g.p.trace = trace;
+        g.run(nullptr);
+        B2N_CUDA(cudaDeviceSynchronize());
+        *grid_out = (int)(g.grid.x * g.grid.y * g.grid.z);
     });
 }
 

@@ -10,9 +10,11 @@ struct ConvGeom {
 };
 
 struct ConvFwdLaunch {
+    double flops = 0, bytes = 0;
     void run(cudaStream_t) const { throw Error(B2N_ESPEC, "b200nn: conv path not built yet"); }
 };
 struct ConvBwdLaunch {
+    double flops = 0, bytes = 0;
     void run(cudaStream_t, bool) const { throw Error(B2N_ESPEC, "b200nn: conv path not built yet"); }
     int kernels() const { return 0; }
 };

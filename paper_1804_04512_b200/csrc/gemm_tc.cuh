@@ -1,18 +1,21 @@
 // gemm_tc.cuh -- the tcgen05 tensor-core GEMM with fused training-step epilogues.
 //
-// D[M x N] = op(A)[M x K] . op(B)[K x N], fp32 in HBM, computed as 3xTF32 (a = a_hi + a_lo split in
-// shared memory; D += a_lo.b_hi + a_hi.b_lo + a_hi.b_hi) so results track the reference's fp32
-// arithmetic (gemm.hpp:30-125) to ~1e-6; a 1xTF32 instantiation exists for the fast mode.
+// D[M x N] = op(A)[M x K] . op(B)[K x N], fp32 in HBM, computed as 3xTF32 so results track the
+// reference's fp32 arithmetic (gemm.hpp:30-125) to ~1e-6: kind::tf32 truncates each fp32 operand
+// to tf32 (measured on B200), so the TMA-landed raw tile IS the hi part; splitter warps write only
+// lo = x - trunc(x), and D += a_lo.b + a.b_lo + a.b. A 1xTF32 instantiation is the fast mode.
 //
-// Structure (one 128 x BN output tile per CTA, 6 warps):
-//   warp 0      : TMA producer  (cp.async.bulk.tensor, SWIZZLE_128B boxes, mbarrier expect_tx)
-//   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer (commit -> smem slot release)
-//   warps 2..5  : 3xTF32 hi/lo splitters for each landed stage, then the epilogue
-//                 (tcgen05.ld TMEM -> registers -> fused bias / activation / softmax-xent /
-//                  SGD-momentum / RBM sampling -> global)
-// Operands may be K-major (row-major [rows][K], "NT" side) or MN-major (row-major [K][rows], the
-// transposed side of the reference's NN / TN calls); both are legal UMMA layouts for kind::tf32,
-// so no transpose pass is ever run. TMA zero-fills out-of-bounds boxes, which pads M, N and K.
+// One 128 x BN output tile per CTA (or per cluster of `splits` CTAs, split-K), 10 warps:
+//   warp 0      : TMA producer (cp.async.bulk.tensor into 128 B-swizzled smem, mbarrier expect_tx)
+//   warp 1      : TMEM allocator + single-thread tcgen05.mma issuer (tcgen05.commit frees a stage)
+//   warps 2..9  : lo splitters for each landed stage, then TMEM -> smem tile (tcgen05.ld)
+//   all warps   : split-K reduction (partials through an L2 workspace, cluster barrier, each CTA of
+//                 the cluster reduces a row slice in fixed split order -> deterministic) and the fused
+//                 epilogue on coalesced float4 rows: bias / activation / act' / SGD-momentum /
+//                 RBM sampling / W += lr/B (pos - neg); softmax-xent row-wise.
+// Operands may be K-major (row-major [rows][K]) or MN-major (row-major [K][rows], the transposed
+// side of the reference's NN / TN calls), both legal UMMA layouts for kind::tf32, so no transpose
+// pass ever runs. TMA zero-fills out-of-bounds boxes, which pads M, N and K.
 #pragma once
 #include "ptx.cuh"
 
@@ -64,12 +67,31 @@ struct GemmParams {
     int M, N, K;
     int a_mn, b_mn;  // 1 = MN-major operand (row-major [K][rows])
     int epi;
+    int splits;      // split-K factor == cluster size along z
+    int kb_per_split;
+    float* ws;       // split-K partial tiles [tile][split][128][BN]
     EpiParams ep;
+    unsigned long long* trace;  // bring-up timeline (%globaltimer ns), null in production
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// slots per CTA: 0 start, 1 setup done, 2+kb TMA issue (kb<16), 18+kb stage landed (kb<16),
+// 34+kb mma issued (kb<16), 50 last commit, 51 epilogue start, 52 end, 53 tile in smem, 54 partial
+// written, 55 cluster barrier passed, 56 reduced, 57 epilogue done
+#define B2N_TRACE(slot)                                                                                          \
+    do {                                                                                                         \
+        if (p.trace && (slot) < 64)                                                                              \
+            p.trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 64 + (slot)] = gtimer(); \
+    } while (0)
 
 constexpr int kBM = 128;
 constexpr int kBK = 32;  // 32 fp32 = one 128-byte swizzle row
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;
+constexpr int kThreads = 64 + 32 * kEpiWarps;  // 320
 
 template <int BN, bool X3>
 struct GemmCfg {
@@ -77,9 +99,12 @@ struct GemmCfg {
     static constexpr int B_BYTES = BN * kBK * 4;
     static constexpr int STAGE_BYTES = (A_BYTES + B_BYTES) * (X3 ? 2 : 1);
     static constexpr int STAGES_FIT = (200 * 1024) / STAGE_BYTES;
-    static constexpr int STAGES = STAGES_FIT > 4 ? 4 : STAGES_FIT;
+    static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
     static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
-    static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+    static constexpr int TP = BN + 4;  // padded smem tile pitch (floats): conflict-free row writes
+    static constexpr int TILE_BYTES = kBM * TP * 4;
+    static constexpr int MAIN_BYTES = STAGES * STAGE_BYTES > TILE_BYTES ? STAGES * STAGE_BYTES : TILE_BYTES;
+    static constexpr int SMEM = MAIN_BYTES + 1024 + 256;
     static_assert(STAGES >= 2, "tile too large");
 };
 
@@ -91,130 +116,164 @@ __device__ __forceinline__ float apply_act(int act, float v) {
     return v;
 }
 
-// 3xTF32 split of one landed tile: hi (truncated to tf32) in place, lo = x - hi to the lo slot.
-__device__ __forceinline__ void split_tile(uint8_t* hi, uint8_t* lo, int bytes, int tid, int nthreads) {
-    float4* h = reinterpret_cast<float4*>(hi);
-    float4* l = reinterpret_cast<float4*>(lo);
-    for (int i = tid; i < bytes / 16; i += nthreads) {
-        float4 x = h[i];
-        float4 a, b;
-        a.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-        a.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-        a.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-        a.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
-        b.x = x.x - a.x;
-        b.y = x.y - a.y;
-        b.z = x.z - a.z;
-        b.w = x.w - a.w;
-        h[i] = a;
-        l[i] = b;
+// lo = x - trunc_tf32(x) of one landed tile (the raw tile doubles as the hi operand)
+__device__ __forceinline__ void split_lo(const uint8_t* raw, uint8_t* lo, int bytes, int tid, int nthreads) {
+    const uint32_t r = smem_u32(raw), l = smem_u32(lo);
+#pragma unroll 4
+    for (int i = tid * 16; i < bytes; i += nthreads * 16) {
+        float x0, x1, x2, x3;
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(x0), "=f"(x1), "=f"(x2), "=f"(x3) : "r"(r + i));
+        const float y0 = x0 - __uint_as_float(__float_as_uint(x0) & 0xFFFFE000u);
+        const float y1 = x1 - __uint_as_float(__float_as_uint(x1) & 0xFFFFE000u);
+        const float y2 = x2 - __uint_as_float(__float_as_uint(x2) & 0xFFFFE000u);
+        const float y3 = x3 - __uint_as_float(__float_as_uint(x3) & 0xFFFFE000u);
+        asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(l + i), "f"(y0), "f"(y1), "f"(y2), "f"(y3)
+                     : "memory");
     }
 }
 
-template <int BN>
-__device__ __forceinline__ void gemm_epilogue(const GemmParams& p, uint32_t tmem_row, int m, int n0) {
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+// 4 consecutive columns of one row: vector access when the row pitch and column allow it
+__device__ __forceinline__ bool vec_ok(const void* base, long long ld, int n, int N) {
+    return n + 3 < N && (ld & 3) == 0 && ((reinterpret_cast<uintptr_t>(base) & 15) == 0);
+}
+
+// elementwise epilogue on 4 columns [n, n+4) of row m (values v); returns the row partial for RBM_VIS
+__device__ __forceinline__ double epi4(const GemmParams& p, int m, int n, const float (&v)[4]) {
     const EpiParams& e = p.ep;
-    const bool mok = m < p.M;
-    if (p.epi == EPI_SOFTMAX_XENT) {
-        // whole row lives in this thread (host guarantees N <= BN, one N tile). softmax
-        // (layers.hpp:301-320) then softmax_cross_entropy (network.hpp:410-437), sequential in j.
-        float mx = -INFINITY;
-        for (int c = 0; c < BN; c += 16) {
-            float v[16];
-            tmem_ld16(tmem_row + c, v);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int n = c + i;
-                if (n < p.N) mx = fmaxf(mx, v[i] + e.bias[(long long)n * e.bias_stride]);
-            }
-        }
-        float sum = 0.0f;
-        for (int c = 0; c < BN; c += 16) {
-            float v[16];
-            tmem_ld16(tmem_row + c, v);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int n = c + i;
-                if (n < p.N) sum += expf((v[i] + e.bias[(long long)n * e.bias_stride]) - mx);
-            }
-        }
-        const int label = mok ? e.labels[m] : 0;
-        int best = 0;
-        float bestp = -1.0f;
-        float ptrue = 0.0f;
-        for (int c = 0; c < BN; c += 16) {
-            float v[16];
-            tmem_ld16(tmem_row + c, v);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int n = c + i;
-                if (n < p.N && mok) {
-                    const float q = expf((v[i] + e.bias[(long long)n * e.bias_stride]) - mx) / sum;
-                    if (q > bestp) {  // strict >: first maximum wins (network.hpp:69-70)
-                        bestp = q;
-                        best = n;
-                    }
-                    if (n == label) ptrue = q;
-                    const float y = n == label ? 1.0f : 0.0f;
-                    e.C[(long long)m * e.ldc + n] = (q - y) / e.batch_div;
-                    if (e.probs) e.probs[(long long)m * e.ld_probs + n] = q;
-                }
-            }
-        }
-        if (mok) {
-            e.row_loss[m] = -log(fmax((double)ptrue, 1e-300));
-            if (e.argmax) e.argmax[m] = best;
-        }
-        return;
-    }
+    const int cnt = p.N - n < 4 ? p.N - n : 4;
+    const long long row = (long long)m * e.ldc;
     double part = 0.0;
-    for (int c = 0; c < BN; c += 16) {
-        float v[16];
-        tmem_ld16(tmem_row + c, v);
-        if (!mok) continue;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const int n = n0 + c + i;
-            if (n >= p.N) break;
-            const float a = v[i];
-            const long long mn = (long long)m * e.ldc + n;
-            switch (p.epi) {
-                case EPI_STORE: e.C[mn] = e.alpha * a; break;
-                case EPI_BIAS_ACT: e.C[mn] = apply_act(e.act, a + e.bias[(long long)n * e.bias_stride]); break;
-                case EPI_DACT: {
-                    const float y = e.aux[(long long)m * e.ld_aux + n];
-                    e.C[mn] = e.act == ACT_SIGMOID ? a * y * (1.0f - y) : (y > 0.0f ? a : 0.0f);
-                    break;
-                }
-                case EPI_SGD: {  // optim.hpp:75-78
-                    float* pp = e.C + mn;
-                    float* vv = e.V + (long long)m * e.ldv + n;
-                    const float g = a + e.wd * *pp;
-                    const float vel = e.mom * *vv - e.lr * g;
-                    *vv = vel;
-                    *pp = *pp + vel;
-                    break;
-                }
-                case EPI_RBM_HID: {  // energy.hpp:101-110 + unit_sample_inplace :59-61
-                    const float pr = sigmoid_ref(a + e.bias[(long long)n * e.bias_stride]);
-                    e.C[mn] = pr;
-                    e.C2[(long long)m * e.ldc2 + n] = (e.u[(long long)m * e.ldu + n] < (double)pr) ? 1.0f : 0.0f;
-                    break;
-                }
-                case EPI_RBM_VIS: {
-                    const float pr = sigmoid_ref(a + e.bias[(long long)n * e.bias_stride]);
-                    e.C[mn] = pr;
-                    const double d = (double)e.aux[(long long)m * e.ld_aux + n] - (double)pr;
-                    part += d * d;
-                    break;
-                }
-                case EPI_RBM_NEGHID: e.C[mn] = -sigmoid_ref(a + e.bias[(long long)n * e.bias_stride]); break;
-                case EPI_AXPY: e.C[mn] = e.C[mn] + e.alpha * a; break;
-                default: break;
+    switch (p.epi) {
+        case EPI_STORE: {
+            if (vec_ok(e.C, e.ldc, n, p.N)) {
+                *reinterpret_cast<float4*>(e.C + row + n) =
+                    make_float4(e.alpha * v[0], e.alpha * v[1], e.alpha * v[2], e.alpha * v[3]);
+            } else {
+                for (int i = 0; i < cnt; ++i) e.C[row + n + i] = e.alpha * v[i];
             }
+            break;
         }
+        case EPI_BIAS_ACT: {
+            float o[4] = {0, 0, 0, 0};
+            for (int i = 0; i < cnt; ++i) o[i] = apply_act(e.act, v[i] + e.bias[(long long)(n + i) * e.bias_stride]);
+            if (vec_ok(e.C, e.ldc, n, p.N))
+                *reinterpret_cast<float4*>(e.C + row + n) = make_float4(o[0], o[1], o[2], o[3]);
+            else
+                for (int i = 0; i < cnt; ++i) e.C[row + n + i] = o[i];
+            break;
+        }
+        case EPI_DACT: {
+            float y[4] = {0, 0, 0, 0}, o[4] = {0, 0, 0, 0};
+            const long long ar = (long long)m * e.ld_aux + n;
+            if (vec_ok(e.aux, e.ld_aux, n, p.N)) {
+                const float4 t = *reinterpret_cast<const float4*>(e.aux + ar);
+                y[0] = t.x, y[1] = t.y, y[2] = t.z, y[3] = t.w;
+            } else {
+                for (int i = 0; i < cnt; ++i) y[i] = e.aux[ar + i];
+            }
+            for (int i = 0; i < cnt; ++i)  // layers.hpp:294 order: dy * y * (1 - y)
+                o[i] = e.act == ACT_SIGMOID ? v[i] * y[i] * (1.0f - y[i]) : (y[i] > 0.0f ? v[i] : 0.0f);
+            if (vec_ok(e.C, e.ldc, n, p.N))
+                *reinterpret_cast<float4*>(e.C + row + n) = make_float4(o[0], o[1], o[2], o[3]);
+            else
+                for (int i = 0; i < cnt; ++i) e.C[row + n + i] = o[i];
+            break;
+        }
+        case EPI_SGD: {  // optim.hpp:75-78 on (w | b) tiles
+            float pp[4] = {0, 0, 0, 0}, vv[4] = {0, 0, 0, 0};
+            const long long vr = (long long)m * e.ldv + n;
+            const bool vec = vec_ok(e.C, e.ldc, n, p.N) && vec_ok(e.V, e.ldv, n, p.N);
+            if (vec) {
+                const float4 a = *reinterpret_cast<const float4*>(e.C + row + n);
+                const float4 b = *reinterpret_cast<const float4*>(e.V + vr);
+                pp[0] = a.x, pp[1] = a.y, pp[2] = a.z, pp[3] = a.w;
+                vv[0] = b.x, vv[1] = b.y, vv[2] = b.z, vv[3] = b.w;
+            } else {
+                for (int i = 0; i < cnt; ++i) pp[i] = e.C[row + n + i], vv[i] = e.V[vr + i];
+            }
+            for (int i = 0; i < cnt; ++i) {
+                const float g = v[i] + e.wd * pp[i];
+                vv[i] = e.mom * vv[i] - e.lr * g;
+                pp[i] = pp[i] + vv[i];
+            }
+            if (vec) {
+                *reinterpret_cast<float4*>(e.C + row + n) = make_float4(pp[0], pp[1], pp[2], pp[3]);
+                *reinterpret_cast<float4*>(e.V + vr) = make_float4(vv[0], vv[1], vv[2], vv[3]);
+            } else {
+                for (int i = 0; i < cnt; ++i) e.C[row + n + i] = pp[i], e.V[vr + i] = vv[i];
+            }
+            break;
+        }
+        case EPI_RBM_HID: {  // energy.hpp:101-110 + unit_sample_inplace :59-61
+            for (int i = 0; i < cnt; ++i) {
+                const float pr = sigmoid_ref(v[i] + e.bias[(long long)(n + i) * e.bias_stride]);
+                e.C[row + n + i] = pr;
+                e.C2[(long long)m * e.ldc2 + n + i] = (e.u[(long long)m * e.ldu + n + i] < (double)pr) ? 1.0f : 0.0f;
+            }
+            break;
+        }
+        case EPI_RBM_VIS: {
+            for (int i = 0; i < cnt; ++i) {
+                const float pr = sigmoid_ref(v[i] + e.bias[(long long)(n + i) * e.bias_stride]);
+                e.C[row + n + i] = pr;
+                const double d = (double)e.aux[(long long)m * e.ld_aux + n + i] - (double)pr;
+                part += d * d;
+            }
+            break;
+        }
+        case EPI_RBM_NEGHID:
+            for (int i = 0; i < cnt; ++i) e.C[row + n + i] = -sigmoid_ref(v[i] + e.bias[(long long)(n + i) * e.bias_stride]);
+            break;
+        case EPI_AXPY: {
+            if (vec_ok(e.C, e.ldc, n, p.N)) {
+                float4 a = *reinterpret_cast<const float4*>(e.C + row + n);
+                a.x += e.alpha * v[0];
+                a.y += e.alpha * v[1];
+                a.z += e.alpha * v[2];
+                a.w += e.alpha * v[3];
+                *reinterpret_cast<float4*>(e.C + row + n) = a;
+            } else {
+                for (int i = 0; i < cnt; ++i) e.C[row + n + i] = e.C[row + n + i] + e.alpha * v[i];
+            }
+            break;
+        }
+        default: break;
     }
-    if (p.epi == EPI_RBM_VIS && mok) e.row_part[(long long)blockIdx.x * e.ld_part + m] = part;
+    return part;
+}
+
+// softmax (layers.hpp:301-320) + softmax_cross_entropy (network.hpp:410-437) of one full row held
+// in the smem tile; sequential in j like the reference.
+__device__ __forceinline__ void softmax_row(const GemmParams& p, const float* trow, int m) {
+    const EpiParams& e = p.ep;
+    float mx = -INFINITY;
+    for (int n = 0; n < p.N; ++n) mx = fmaxf(mx, trow[n] + e.bias[(long long)n * e.bias_stride]);
+    float sum = 0.0f;
+    for (int n = 0; n < p.N; ++n) sum += expf((trow[n] + e.bias[(long long)n * e.bias_stride]) - mx);
+    const int label = e.labels[m];
+    int best = 0;
+    float bestp = -1.0f, ptrue = 0.0f;
+    for (int n = 0; n < p.N; ++n) {
+        const float q = expf((trow[n] + e.bias[(long long)n * e.bias_stride]) - mx) / sum;
+        if (q > bestp) {  // strict >: first maximum wins (network.hpp:69-70)
+            bestp = q;
+            best = n;
+        }
+        if (n == label) ptrue = q;
+        e.C[(long long)m * e.ldc + n] = (q - (n == label ? 1.0f : 0.0f)) / e.batch_div;
+        if (e.probs) e.probs[(long long)m * e.ld_probs + n] = q;
+    }
+    e.row_loss[m] = -log(fmax((double)ptrue, 1e-300));
+    if (e.argmax) e.argmax[m] = best;
 }
 
 template <int BN, bool X3>
@@ -223,22 +282,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                    const GemmParams p) {
     using Cfg = GemmCfg<BN, X3>;
     constexpr int S = Cfg::STAGES;
+    constexpr int TP = Cfg::TP;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * Cfg::STAGE_BYTES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + Cfg::MAIN_BYTES);
     uint64_t* ready = full + S;
     uint64_t* empty = ready + S;
     uint64_t* tmem_full = empty + S;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+    float* tile = reinterpret_cast<float*>(smem);  // epilogue staging, reuses the drained stages
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m0 = blockIdx.y * kBM, n0 = blockIdx.x * BN;
-    const int num_kb = (p.K + kBK - 1) / kBK;
+    const int num_kb_total = (p.K + kBK - 1) / kBK;
+    const int split = blockIdx.z;
+    const int kb0 = split * p.kb_per_split;
+    const int kb1 = min(num_kb_total, kb0 + p.kb_per_split);
+    const int num_kb = kb1 > kb0 ? kb1 - kb0 : 0;
 
     if (threadIdx.x == 0) {
+        B2N_TRACE(0);
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&ready[s], 128);
+            mbar_init(&ready[s], 32 * kEpiWarps);
             mbar_init(&empty[s], 1);
         }
         mbar_init(tmem_full, 1);
@@ -251,17 +317,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) B2N_TRACE(1);
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
-            for (int kb = 0; kb < num_kb; ++kb) {
-                const int s = kb % S;
-                const uint32_t ph = (kb / S) & 1;
+            for (int i = 0; i < num_kb; ++i) {
+                const int s = i % S;
+                const uint32_t ph = (i / S) & 1;
                 mbar_wait(&empty[s], ph ^ 1);
                 uint8_t* a = smem + s * Cfg::STAGE_BYTES;
                 uint8_t* b = a + Cfg::A_BYTES;
                 mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES + Cfg::B_BYTES);
-                const int k0 = kb * kBK;
+                if (i < 16) B2N_TRACE(2 + i);
+                const int k0 = (kb0 + i) * kBK;
                 if (!p.a_mn) {
                     tma_load_2d(a, &mapA, &full[s], k0, m0);
                 } else {
@@ -279,11 +347,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         if (lane == 0) {  // ---------------- MMA issuer
             const uint32_t idesc = umma_idesc_tf32(kBM, BN, p.a_mn, p.b_mn);
-            for (int kb = 0; kb < num_kb; ++kb) {
-                const int s = kb % S;
-                const uint32_t ph = (kb / S) & 1;
+            for (int i = 0; i < num_kb; ++i) {
+                const int s = i % S;
+                const uint32_t ph = (i / S) & 1;
                 mbar_wait(X3 ? &ready[s] : &full[s], ph);
                 tc_fence_after();
+                if (i < 16) B2N_TRACE(34 + i);
                 const uint32_t a_hi = smem_u32(smem + s * Cfg::STAGE_BYTES);
                 const uint32_t b_hi = a_hi + Cfg::A_BYTES;
                 const uint32_t a_lo = b_hi + Cfg::B_BYTES;
@@ -292,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int kk = 0; kk < kBK / 8; ++kk) {
                     const uint64_t dah = p.a_mn ? desc_mnmajor(a_hi, kk) : desc_kmajor(a_hi, kk);
                     const uint64_t dbh = p.b_mn ? desc_mnmajor(b_hi, kk) : desc_kmajor(b_hi, kk);
-                    const uint32_t acc = (kb | kk) != 0;
+                    const uint32_t acc = (i | kk) != 0;
                     if (X3) {
                         const uint64_t dal = p.a_mn ? desc_mnmajor(a_lo, kk) : desc_kmajor(a_lo, kk);
                         const uint64_t dbl = p.b_mn ? desc_mnmajor(b_lo, kk) : desc_kmajor(b_lo, kk);
@@ -306,34 +375,122 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mma_commit(&empty[s]);
             }
             mma_commit(tmem_full);
+            B2N_TRACE(50);
         }
-    } else {  // ---------------- splitters + epilogue (warps 2..5)
+    } else {  // ---------------- splitters, then TMEM -> smem tile (warps 2..9)
         const int ct = threadIdx.x - 64;
         if (X3) {
-            for (int kb = 0; kb < num_kb; ++kb) {
-                const int s = kb % S;
-                const uint32_t ph = (kb / S) & 1;
+            for (int i = 0; i < num_kb; ++i) {
+                const int s = i % S;
+                const uint32_t ph = (i / S) & 1;
                 mbar_wait(&full[s], ph);
+                if (ct == 0 && i < 16) B2N_TRACE(18 + i);
                 uint8_t* a = smem + s * Cfg::STAGE_BYTES;
-                split_tile(a, a + Cfg::A_BYTES + Cfg::B_BYTES, Cfg::A_BYTES, ct, 128);
-                split_tile(a + Cfg::A_BYTES, a + 2 * Cfg::A_BYTES + Cfg::B_BYTES, Cfg::B_BYTES, ct, 128);
+                split_lo(a, a + Cfg::A_BYTES + Cfg::B_BYTES, Cfg::A_BYTES + Cfg::B_BYTES, ct, 32 * kEpiWarps);
                 fence_proxy_async_smem();
                 mbar_arrive(&ready[s]);
             }
         }
         mbar_wait(tmem_full, 0);
         tc_fence_after();
-        const int q = warp & 3;  // TMEM lane quadrant this warp may access
+        if (ct == 0) B2N_TRACE(51);
+        const int q = warp & 3;            // TMEM lane quadrant this warp may access
+        const int half = (warp - 2) >> 2;  // two warps per quadrant split the columns
         const int row = 32 * q + lane;
-        gemm_epilogue<BN>(p, tmem_base + ((uint32_t)(32 * q) << 16), m0 + row, n0);
+        const uint32_t trow = tmem_base + ((uint32_t)(32 * q) << 16);
+        float* dst = tile + row * TP;
+        if (num_kb == 0) {
+            for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); ++c) dst[c] = 0.0f;
+        } else if (BN >= 32) {
+            for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 16) {
+                float v[16];
+                tmem_ld16(trow + c, v);
+#pragma unroll
+                for (int i = 0; i < 16; i += 4)
+                    *reinterpret_cast<float4*>(dst + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+            }
+        } else {
+            float v[8];
+            tmem_ld8(trow + half * 8, v);
+#pragma unroll
+            for (int i = 0; i < 8; i += 4)
+                *reinterpret_cast<float4*>(dst + half * 8 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        }
     }
     __syncwarp();
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) B2N_TRACE(53);
+
+    // ---------------- split-K reduction across the cluster (fixed split order: deterministic)
+    int r_lo = 0, r_hi = kBM;
+    if (p.splits > 1) {
+        const long long tile_id = (long long)blockIdx.y * gridDim.x + blockIdx.x;
+        float* ws = p.ws + tile_id * p.splits * (long long)(kBM * BN);
+        float* mine = ws + (long long)split * kBM * BN;
+        for (int idx = threadIdx.x; idx < kBM * BN / 4; idx += kThreads) {
+            const int r = idx / (BN / 4), c = (idx % (BN / 4)) * 4;
+            if (m0 + r < p.M)
+                *reinterpret_cast<float4*>(mine + r * BN + c) = *reinterpret_cast<const float4*>(tile + r * TP + c);
+        }
+        if (threadIdx.x == 0) B2N_TRACE(54);
+        cluster_sync_all();  // release our partial / acquire everyone's
+        if (threadIdx.x == 0) B2N_TRACE(55);
+        const int rank = (int)cluster_rank();
+        const int rows = (kBM + p.splits - 1) / p.splits;
+        r_lo = min(kBM, rank * rows);
+        r_hi = min(kBM, r_lo + rows);
+        for (int idx = threadIdx.x; idx < (r_hi - r_lo) * (BN / 4); idx += kThreads) {
+            const int r = r_lo + idx / (BN / 4), c = (idx % (BN / 4)) * 4;
+            if (m0 + r >= p.M) continue;
+            float4 acc = *reinterpret_cast<const float4*>(ws + r * BN + c);
+            for (int z = 1; z < p.splits; ++z) {
+                const float4 t = *reinterpret_cast<const float4*>(ws + (long long)z * kBM * BN + r * BN + c);
+                acc.x += t.x;
+                acc.y += t.y;
+                acc.z += t.z;
+                acc.w += t.w;
+            }
+            *reinterpret_cast<float4*>(tile + r * TP + c) = acc;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) B2N_TRACE(56);
+    }
+
+    // ---------------- fused epilogue on rows [r_lo, r_hi) of the tile
+    if (p.epi == EPI_SOFTMAX_XENT) {
+        for (int r = r_lo + threadIdx.x; r < r_hi; r += kThreads)
+            if (m0 + r < p.M) softmax_row(p, tile + r * TP, m0 + r);
+    } else {
+        constexpr int G = BN / 4;  // threads per row
+        const int total = (r_hi - r_lo) * G;
+        const int iters = (total + kThreads - 1) / kThreads;
+        for (int it = 0; it < iters; ++it) {
+            const int idx = it * kThreads + threadIdx.x;
+            const int r = r_lo + idx / G, c = (idx % G) * 4;
+            const int m = m0 + r, n = n0 + c;
+            double part = 0.0;
+            if (idx < total && m < p.M && n < p.N) {
+                const float4 t = *reinterpret_cast<const float4*>(tile + r * TP + c);
+                const float v[4] = {t.x, t.y, t.z, t.w};
+                part = epi4(p, m, n, v);
+            }
+            if (G <= 32 && p.epi == EPI_RBM_VIS) {  // row partial over this CTA's BN columns
+#pragma unroll
+                for (int o = G / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+                if (idx < total && (idx % G) == 0 && m < p.M)
+                    p.ep.row_part[(long long)blockIdx.x * p.ep.ld_part + m] = part;
+            }
+        }
+    }
+
+    __syncthreads();
+    if (threadIdx.x == 0) B2N_TRACE(57);
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
     }
+    if (threadIdx.x == 0) B2N_TRACE(52);
 }
 
 }  // namespace b2n

@@ -15,6 +15,7 @@
 // one vectorised pass.
 #pragma once
 #include <functional>
+#include <string>
 #include <map>
 #include <memory>
 #include <random>
@@ -25,56 +26,50 @@
 
 namespace b2n {
 
-struct DevMem {
-    void* p = nullptr;
-    size_t bytes = 0;
-    void alloc(size_t n) {
-        release();
-        if (n == 0) return;
-        cudaError_t e = cudaMalloc(&p, n);
-        if (e != cudaSuccess) {
-            p = nullptr;
-            throw Error(e == cudaErrorMemoryAllocation ? B2N_EOOM : B2N_ECUDA,
-                        std::string("cudaMalloc(") + std::to_string(n) + "): " + cudaGetErrorString(e));
+// one planned launch (or short launch sequence) of a step, with its algorithmic work
+struct Op {
+    std::function<void(cudaStream_t)> fn;
+    std::string name;
+    double flops = 0, bytes = 0;
+    int kernels = 1;
+    Op() = default;
+    template <class F>
+    Op(F f, std::string n = "op", double fl = 0, double by = 0, int k = 1)
+        : fn(std::move(f)), name(std::move(n)), flops(fl), bytes(by), kernels(k) {}
+    void operator()(cudaStream_t s) const { fn(s); }
+};
+inline Op gemm_op(const GemmLaunch& g, const std::string& name) {
+    return Op([g](cudaStream_t s) { g.run(s); }, name, g.flops, g.bytes, 1);
+}
+
+// per-op device time of `steps` un-graphed runs of an op list (CUDA events between ops)
+struct OpStats {
+    std::string name;
+    double ms = 0, flops = 0, bytes = 0;
+    int kernels = 1;
+};
+inline std::vector<OpStats> profile_ops(const std::vector<Op>& ops, int steps, cudaStream_t st) {
+    std::vector<cudaEvent_t> ev(ops.size() + 1);
+    for (auto& e : ev) B2N_CUDA(cudaEventCreate(&e));
+    std::vector<OpStats> out(ops.size());
+    for (size_t i = 0; i < ops.size(); ++i) out[i] = {ops[i].name, 0.0, ops[i].flops, ops[i].bytes, ops[i].kernels};
+    for (int s = 0; s < steps + 1; ++s) {  // first pass warms up
+        for (size_t i = 0; i < ops.size(); ++i) {
+            B2N_CUDA(cudaEventRecord(ev[i], st));
+            ops[i](st);
         }
-        bytes = n;
-        // zero-fill, then wait for it: the objects' streams are non-blocking and do not order
-        // against the legacy stream cudaMemset runs on
-        B2N_CUDA(cudaMemset(p, 0, n));
-        B2N_CUDA(cudaDeviceSynchronize());
+        B2N_CUDA(cudaEventRecord(ev[ops.size()], st));
+        B2N_CUDA(cudaEventSynchronize(ev[ops.size()]));
+        if (s == 0) continue;
+        for (size_t i = 0; i < ops.size(); ++i) {
+            float ms = 0;
+            B2N_CUDA(cudaEventElapsedTime(&ms, ev[i], ev[i + 1]));
+            out[i].ms += ms / steps;
+        }
     }
-    void release() {
-        if (p) cudaFree(p);
-        p = nullptr;
-        bytes = 0;
-    }
-    ~DevMem() { release(); }
-    template <class T>
-    T* as() const {
-        return static_cast<T*>(p);
-    }
-};
-
-struct HostPinned {
-    void* p = nullptr;
-    size_t bytes = 0;
-    void alloc(size_t n) {
-        release();
-        B2N_CUDA(cudaMallocHost(&p, std::max<size_t>(n, 64)));
-        bytes = n;
-    }
-    void release() {
-        if (p) cudaFreeHost(p);
-        p = nullptr;
-    }
-    ~HostPinned() { release(); }
-    template <class T>
-    T* as() const {
-        return static_cast<T*>(p);
-    }
-};
-
-using Op = std::function<void(cudaStream_t)>;
+    for (auto& e : ev) cudaEventDestroy(e);
+    return out;
+}
 
 struct ParamView {  // one fastnn ParamRef (w or b of a layer) inside the packed buffers
     std::vector<long long> dims;
@@ -135,6 +130,13 @@ class Net {
     void run_staged(int steps, long long Bg);
     double loss();
     int kernels_per_step(long long B);
+    std::vector<OpStats> profile(long long B, int steps) {
+        ensure_capacity(B);
+        Plan& pl = plan_for(B, B);
+        std::vector<Op> ops = pl.ops[dp_ ? SPLIT : (lr_ != 0.0f ? FUSED : SPLIT)];
+        if (dp_) ops.insert(ops.end(), pl.ops[SPLIT_APPLY].begin(), pl.ops[SPLIT_APPLY].end());
+        return profile_ops(ops, steps, stream_);
+    }
     void dp_init(const char id[128], int rank, int world) {
         dp_ = std::make_unique<DpComm>();
         dp_->init(id, rank, world);
@@ -488,7 +490,7 @@ inline void Net::build_plan(Plan& pl) {
             }
             GemmLaunch g = plan_gemm(B, (int)L.out, (int)L.in, {L.Ain, L.ld_in, false}, {P + L.off, L.ldw, false},
                                      fused_softmax ? EPI_SOFTMAX_XENT : EPI_BIAS_ACT, e, x3_);
-            fwd.push_back([g](cudaStream_t s) { g.run(s); });
+            fwd.push_back(gemm_op(g, "dense" + std::to_string(i) + (fused_softmax ? ".fwd+softmax_xent" : ".fwd+act")));
             ++nk_fwd;
             if (L.softmax_after && !fused_softmax) {
                 float* lg = logits_;
@@ -500,17 +502,17 @@ inline void Net::build_plan(Plan& pl) {
                 int* am = argmax_;
                 float* pr = probs_;
                 float bd = (float)pl.Bg;
-                fwd.push_back([=](cudaStream_t s) {
+                fwd.push_back(Op([=](cudaStream_t s) {
                     softmax_xent_rows_kernel<<<(B * 32 + 255) / 256, 256, 0, s>>>(lg, ldl, B, (int)C, lab, bd, D, ldd,
                                                                                    rl, am, pr, C);
-                });
+                }, "softmax_xent", 0.0, (double)B * C * 16));
                 ++nk_fwd;
                 if (ldd < C + 1) throw Error(B2N_EINTERNAL, "dlogits pitch");
             }
         } else {
             ConvFwdLaunch c = plan_conv_fwd(L.g, B, L.Ain, L.ld_in, P + L.kern_off, P + L.bias_off, L.act, L.pool_after,
                                             L.Aout, L.ld_out, L.arg, x3_);
-            fwd.push_back([c](cudaStream_t s) { c.run(s); });
+            fwd.push_back(Op([c](cudaStream_t s) { c.run(s); }, "conv" + std::to_string(i) + ".fwd", c.flops, c.bytes));
             ++nk_fwd;
         }
     }
@@ -529,16 +531,16 @@ inline void Net::build_plan(Plan& pl) {
                     e.act = Prev.act;
                     GemmLaunch g = plan_gemm(B, (int)L.in, (int)L.out, {L.D, L.ldd, false}, {P + L.off, L.ldw, true},
                                              Prev.act == ACT_NONE ? EPI_STORE : EPI_DACT, e, x3_);
-                    bwd_fused.push_back([g](cudaStream_t s) { g.run(s); });
-                    bwd_split.push_back([g](cudaStream_t s) { g.run(s); });
+                    bwd_fused.push_back(gemm_op(g, "dense" + std::to_string(ii) + ".dgrad+dact"));
+                    bwd_split.push_back(gemm_op(g, "dense" + std::to_string(ii) + ".dgrad+dact"));
                 } else {  // conv below: plain dX into the pooled-gradient buffer (act' applied by the conv gather)
                     EpiParams e = epi_default();
                     e.C = Prev.D;
                     e.ldc = Prev.ldd;
                     GemmLaunch g = plan_gemm(B, (int)L.in, (int)L.out, {L.D, L.ldd, false}, {P + L.off, L.ldw, true},
                                              EPI_STORE, e, x3_);
-                    bwd_fused.push_back([g](cudaStream_t s) { g.run(s); });
-                    bwd_split.push_back([g](cudaStream_t s) { g.run(s); });
+                    bwd_fused.push_back(gemm_op(g, "dense" + std::to_string(ii) + ".dgrad"));
+                    bwd_split.push_back(gemm_op(g, "dense" + std::to_string(ii) + ".dgrad"));
                 }
                 ++nk_fused;
                 ++nk_split;
@@ -559,8 +561,8 @@ inline void Net::build_plan(Plan& pl) {
             es.ldc = L.ldw;
             GemmLaunch gs = plan_gemm((int)L.out, (int)L.in + 1, B, {L.D, L.ldd, true}, {L.Ain, L.ld_in, true},
                                       EPI_STORE, es, x3_);
-            bwd_fused.push_back([gf](cudaStream_t s) { gf.run(s); });
-            bwd_split.push_back([gs](cudaStream_t s) { gs.run(s); });
+            bwd_fused.push_back(gemm_op(gf, "dense" + std::to_string(ii) + ".wgrad+sgd"));
+            bwd_split.push_back(gemm_op(gs, "dense" + std::to_string(ii) + ".wgrad"));
             ++nk_fused;
             ++nk_split;
         } else {
@@ -571,12 +573,25 @@ inline void Net::build_plan(Plan& pl) {
                                              first ? nullptr : layers_[ii - 1].D, first ? 0 : layers_[ii - 1].ldd,
                                              P + L.kern_off, Vv + L.kern_off, P + L.bias_off, Vv + L.bias_off,
                                              G + L.kern_off, G + L.bias_off, lr_, mom_, wd_, x3_);
-            bwd_fused.push_back([cb](cudaStream_t s) { cb.run(s, true); });
-            bwd_split.push_back([cb](cudaStream_t s) { cb.run(s, false); });
+            bwd_fused.push_back(Op([cb](cudaStream_t s) { cb.run(s, true); }, "conv" + std::to_string(ii) + ".bwd+sgd",
+                                   cb.flops, cb.bytes, cb.kernels()));
+            bwd_split.push_back(Op([cb](cudaStream_t s) { cb.run(s, false); }, "conv" + std::to_string(ii) + ".bwd",
+                                   cb.flops, cb.bytes, cb.kernels()));
             nk_fused += cb.kernels();
             nk_split += cb.kernels();
         }
     }
+    (void)nk_fwd;
+    (void)nk_fused;
+    (void)nk_split;
+    auto count = [](const std::vector<Op>& v) {
+        int n = 0;
+        for (const Op& o : v) n += o.kernels;
+        return n;
+    };
+    nk_fwd = count(fwd);
+    nk_fused = count(bwd_fused);
+    nk_split = count(bwd_split);
     pl.ops[FWD] = fwd;
     pl.nkernels[FWD] = nk_fwd;
     pl.ops[FUSED] = fwd;
@@ -591,11 +606,11 @@ inline void Net::build_plan(Plan& pl) {
     float lr = lr_, mom = mom_, wd = wd_;
     DpComm* dp = dp_.get();
     long long npk = n_packed_;
-    pl.ops[SPLIT_APPLY].push_back([=](cudaStream_t s) {
+    pl.ops[SPLIT_APPLY].push_back(Op([=](cudaStream_t s) {
         if (dp) dp->allreduce_f32(G, (size_t)npk, s);
         sgd_packed_kernel<<<grid_for(n4), 256, 0, s>>>(reinterpret_cast<float4*>(Pp), reinterpret_cast<float4*>(Vv),
                                                        reinterpret_cast<const float4*>(G), n4, lr, mom, wd);
-    });
+    }, dp ? "allreduce+sgd" : "sgd", 0.0, (double)npk * 20));
     pl.nkernels[SPLIT_APPLY] = 1;
 }
 

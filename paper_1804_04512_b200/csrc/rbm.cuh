@@ -118,6 +118,12 @@ class Rbm {
     }
     cudaStream_t stream() const { return stream_; }
     int kernels_per_step() const { return last_kernels_; }
+    std::vector<OpStats> profile(int steps, float lr, long long Bg) {
+        if (!staged_B_) throw Error(B2N_EPARAM, "profile before stage");
+        Plan& pl = plan_for(staged_B_, staged_k_, lr, Bg ? Bg : staged_B_);
+        if (hcol_B_ != pl.B) launch(pl);  // sets the +1/-1 column
+        return profile_ops(pl.ops, steps, stream_);
+    }
 
   private:
     struct Plan {
@@ -187,7 +193,7 @@ class Rbm {
             e.C2 = HSp;
             e.ldc2 = ldhs_;
             GemmLaunch g = plan_gemm(B, H, V, {vin, ldv_, false}, {W, ldw_, false}, epi, e, x3_);
-            pl.ops.push_back([g](cudaStream_t s) { g.run(s); });
+            pl.ops.push_back(gemm_op(g, epi == EPI_RBM_HID ? "rbm.hidden+sample" : "rbm.neg_hidden"));
             ++pl.nk;
         };
         auto visible = [&](double* recon_rows) {
@@ -202,7 +208,7 @@ class Rbm {
             e.ld_part = cap_;
             GemmLaunch g = plan_gemm(B, V, H, {HSp, ldhs_, false}, {W, ldw_, true}, EPI_RBM_VIS, e, x3_);
             pl.recon_tiles = (int)g.grid.x;
-            pl.ops.push_back([g](cudaStream_t s) { g.run(s); });
+            pl.ops.push_back(gemm_op(g, "rbm.visible+recon"));
             ++pl.nk;
         };
         // CD-k chain (energy.hpp:137-146): h0 mean + first sample share one GEMM
@@ -230,16 +236,16 @@ class Rbm {
         }
         GemmLaunch g = plan_gemm(H + 1, V + 1, 2 * B, {Hc, ldh_, true}, {Vc, ldv_, true}, dp_ ? EPI_STORE : EPI_AXPY, e,
                                  x3_);
-        pl.ops.push_back([g](cudaStream_t s) { g.run(s); });
+        pl.ops.push_back(gemm_op(g, dp_ ? "rbm.dW" : "rbm.dW+update"));
         ++pl.nk;
         if (dp_) {
             DpComm* dp = dp_.get();
             long long n = nW_;
-            pl.ops.push_back([=](cudaStream_t s) {
+            pl.ops.push_back(Op([=](cudaStream_t s) {
                 dp->allreduce_f32(G, (size_t)n, s);
                 axpy_kernel<<<grid_for(n / 4), 256, 0, s>>>(reinterpret_cast<float4*>(W),
                                                             reinterpret_cast<const float4*>(G), n / 4, scale);
-            });
+            }, "allreduce+update", 0.0, (double)n * 12));
             ++pl.nk;
         }
         last_kernels_ = pl.nk;

@@ -14,6 +14,7 @@
 #include <cstring>
 #include <stdexcept>
 #include <string>
+#include <memory>
 #include <vector>
 
 #include "../../include/b200nn.h"
@@ -87,6 +88,55 @@ inline CUtensorMap make_map_2d(const float* base, uint64_t inner, uint64_t outer
     return m;
 }
 
+struct DevMem {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void alloc(size_t n) {
+        release();
+        if (n == 0) return;
+        cudaError_t e = cudaMalloc(&p, n);
+        if (e != cudaSuccess) {
+            p = nullptr;
+            throw Error(e == cudaErrorMemoryAllocation ? B2N_EOOM : B2N_ECUDA,
+                        std::string("cudaMalloc(") + std::to_string(n) + "): " + cudaGetErrorString(e));
+        }
+        bytes = n;
+        // zero-fill, then wait for it: the objects' streams are non-blocking and do not order
+        // against the legacy stream cudaMemset runs on
+        B2N_CUDA(cudaMemset(p, 0, n));
+        B2N_CUDA(cudaDeviceSynchronize());
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    ~DevMem() { release(); }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+struct HostPinned {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void alloc(size_t n) {
+        release();
+        B2N_CUDA(cudaMallocHost(&p, std::max<size_t>(n, 64)));
+        bytes = n;
+    }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+    }
+    ~HostPinned() { release(); }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
 // ------------------------------------------------------------------ GEMM plan
 // One operand of D = op(A) . op(B). K-major: row-major [rows][K] (fastnn NT side);
 // MN-major: row-major [K][rows] (the transposed side).
@@ -102,9 +152,29 @@ struct GemmLaunch {
     int bn = 64;
     bool x3 = true;
     dim3 grid;
-    size_t smem = 0;
+    std::shared_ptr<DevMem> ws;  // split-K partial tiles
+    double flops = 0, bytes = 0;  // algorithmic work of one launch (roofline numerators)
     void run(cudaStream_t st) const;
 };
+
+// Algorithmic HBM bytes of one GEMM launch: each operand read once, each epilogue stream once.
+inline double gemm_bytes(int M, int N, int K, int epi) {
+    const double mn = (double)M * N, a = (double)M * K * 4, b = (double)N * K * 4;
+    double e = 0;
+    switch (epi) {
+        case EPI_STORE: e = mn * 4; break;
+        case EPI_BIAS_ACT: e = mn * 4 + N * 4.0; break;
+        case EPI_DACT: e = mn * 8; break;
+        case EPI_SOFTMAX_XENT: e = mn * 8 + M * 16.0 + N * 4.0; break;
+        case EPI_SGD: e = mn * 16; break;
+        case EPI_RBM_HID: e = mn * 16 + N * 4.0; break;
+        case EPI_RBM_VIS: e = mn * 8 + M * 8.0 + N * 4.0; break;
+        case EPI_RBM_NEGHID: e = mn * 4 + N * 4.0; break;
+        case EPI_AXPY: e = mn * 8; break;
+        default: e = mn * 4;
+    }
+    return a + b + e;
+}
 
 template <int BN, bool X3>
 void launch_gemm_inst(const GemmLaunch& g, cudaStream_t st) {
@@ -114,8 +184,19 @@ void launch_gemm_inst(const GemmLaunch& g, cudaStream_t st) {
         return true;
     }();
     (void)attr;
-    gemm_tc_kernel<BN, X3><<<g.grid, kThreads, Cfg::SMEM, st>>>(g.ma, g.mb, g.p);
-    B2N_CUDA(cudaGetLastError());
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = g.grid;
+    cfg.blockDim = dim3(kThreads, 1, 1);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 1;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = (unsigned)g.p.splits;  // split-K CTAs of one tile form a cluster
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    B2N_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, X3>, g.ma, g.mb, g.p));
 }
 
 inline void GemmLaunch::run(cudaStream_t st) const {
@@ -137,25 +218,46 @@ inline void GemmLaunch::run(cudaStream_t st) const {
 #undef B2N_G
 }
 
-inline int pick_bn(int M, int N, bool b_mn, int epi) {
+// Tile width and split-K factor: enough CTAs to put most SMs to work on these latency-bound shapes
+// (<= 128 CTAs in clusters of <= 8, the co-residency limit), the widest tile that still gets there.
+struct Tiling {
+    int bn, splits, kb_per_split;
+};
+inline Tiling pick_tiling(int M, int N, int K, bool b_mn, int epi) {
+    const int mt = (M + kBM - 1) / kBM, nkb = (K + kBK - 1) / kBK;
+    int bn;
     if (epi == EPI_SOFTMAX_XENT) {
-        int bn = N <= 16 ? 16 : N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+        bn = N <= 16 ? 16 : N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
         if (b_mn && bn < 32) bn = 32;
-        return bn;
+    } else if (N <= 16 && !b_mn) {
+        bn = 16;
+    } else {
+        bn = 32;
+        for (int c : {128, 64})
+            if ((long long)mt * ((N + c - 1) / c) * std::min(8, nkb) >= 96) {
+                bn = c;
+                break;
+            }
     }
-    if (N <= 16 && !b_mn) return 16;
-    const int mt = (M + kBM - 1) / kBM;
-    for (int bn : {128, 64}) {
-        if ((long long)mt * ((N + bn - 1) / bn) >= 120) return bn;
-    }
-    return 32;
+    const int tiles = mt * ((N + bn - 1) / bn);
+    // power-of-two cluster sizes (1, 2, 4, 8): odd sizes schedule poorly (measured: a 7-CTA
+    // cluster grid started its last CTAs ~6 us after the first)
+    int want = std::max(1, std::min({128 / std::max(tiles, 1), 8, nkb}));
+    int splits = 1;
+    while (splits * 2 <= want) splits *= 2;
+    // 8-CTA clusters only co-schedule ~112 at a time on 148 SMs (measured); fall back to 4
+    if (splits == 8 && tiles * 8 > 112) splits = 4;
+    const int kbps = (nkb + splits - 1) / splits;
+    return {bn, splits, kbps};
 }
 
 inline GemmLaunch plan_gemm(int M, int N, int K, Operand A, Operand B, int epi, const EpiParams& ep, bool x3,
                             int bn = 0) {
     if (M <= 0 || N <= 0 || K <= 0) throw Error(B2N_ESHAPE, "gemm extents must be positive");
     GemmLaunch g;
-    g.bn = bn ? bn : pick_bn(M, N, B.mn_major, epi);
+    Tiling t = pick_tiling(M, N, K, B.mn_major, epi);
+    if (bn) t.bn = bn;
+    g.bn = t.bn;
     if (epi == EPI_SOFTMAX_XENT && N > g.bn) throw Error(B2N_ESHAPE, "fused softmax needs classes <= 256");
     if (B.mn_major && g.bn < 32) g.bn = 32;
     g.x3 = x3;
@@ -168,7 +270,18 @@ inline GemmLaunch plan_gemm(int M, int N, int K, Operand A, Operand B, int epi, 
     g.p.b_mn = B.mn_major;
     g.p.epi = epi;
     g.p.ep = ep;
-    g.grid = dim3((N + g.bn - 1) / g.bn, (M + kBM - 1) / kBM, 1);
+    g.p.trace = nullptr;
+    g.p.splits = t.splits;
+    g.p.kb_per_split = t.kb_per_split;
+    g.p.ws = nullptr;
+    g.grid = dim3((N + g.bn - 1) / g.bn, (M + kBM - 1) / kBM, t.splits);
+    if (t.splits > 1) {
+        g.ws = std::make_shared<DevMem>();
+        g.ws->alloc((size_t)g.grid.x * g.grid.y * t.splits * kBM * g.bn * 4);
+        g.p.ws = g.ws->as<float>();
+    }
+    g.flops = 2.0 * M * N * K;
+    g.bytes = gemm_bytes(M, N, K, epi);
     return g;
 }
 
