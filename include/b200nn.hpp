@@ -1,0 +1,276 @@
+// b200nn.hpp -- header-only C++ host API over the C ABI (b200nn.h), mirroring the reference's
+// hot-path API (fastnn, /root/reference/proj/include/fastnn) name for name:
+//
+//   fastnn                                   b200nn
+//   LayerDesc / NetworkSpec (network.hpp:194-234)   LayerDesc / NetworkSpec (+ conv pad)
+//   build_network (network.hpp:284)          build_network          -> device-resident Network
+//   train_minibatch (network.hpp:463)        train_minibatch        -> loss, params updated in HBM
+//   forward_batch / evaluate (:402, :474)    forward_batch / evaluate
+//   Rbm / cd_k_update (energy.hpp:16, :131)  Rbm / cd_k_update      (Bernoulli uniforms supplied)
+//   Error, ShapeError, ... (config.hpp:11-57) the same exception types, thrown from C ABI statuses
+//
+// Tensors: any type with fastnn::Tensor's accessors (rank(), dim(i), rows_total(), last_dim(),
+// row_ptr(r)) -- pass fastnn::Tensor itself for a drop-in swap; rows are packed (lane padding
+// stripped, tensor.hpp:16-18) before the host->device copy.
+#pragma once
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <memory>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "b200nn.h"
+
+namespace b200nn {
+
+struct Error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct ShapeError : Error {
+    using Error::Error;
+};
+struct ParamError : Error {
+    using Error::Error;
+};
+struct LabelError : Error {
+    using Error::Error;
+};
+struct SpecError : Error {
+    using Error::Error;
+};
+struct BoundsError : Error {
+    using Error::Error;
+};
+struct CudaError : Error {
+    using Error::Error;
+};
+struct NcclError : Error {
+    using Error::Error;
+};
+
+inline void check(int status) {
+    if (status == B2N_OK) return;
+    const std::string msg = b2n_last_error();
+    switch (status) {
+        case B2N_ESHAPE: throw ShapeError(msg);
+        case B2N_EPARAM: throw ParamError(msg);
+        case B2N_ELABEL: throw LabelError(msg);
+        case B2N_ESPEC: throw SpecError(msg);
+        case B2N_EBOUNDS: throw BoundsError(msg);
+        case B2N_ECUDA: throw CudaError(msg);
+        case B2N_ENCCL: throw NcclError(msg);
+        default: throw Error(msg);
+    }
+}
+
+struct LayerDesc {
+    enum class Kind { Dense, Conv, MaxPool, Sigmoid, Relu, Softmax, Dropout, BatchNorm, Flatten };
+    Kind kind = Kind::Dense;
+    long long in = 0, out = 0;
+    long long k = 0, kh = 0, kw = 0, pad = 0;
+    float p = 0.0f;
+    static LayerDesc dense(long long in, long long out) { return {Kind::Dense, in, out}; }
+    static LayerDesc conv(long long k, long long kh, long long kw, long long pad = 0) {
+        LayerDesc d;
+        d.kind = Kind::Conv;
+        d.k = k, d.kh = kh, d.kw = kw, d.pad = pad;
+        return d;
+    }
+    static LayerDesc maxpool() { return LayerDesc{Kind::MaxPool}; }
+    static LayerDesc sigmoid() { return LayerDesc{Kind::Sigmoid}; }
+    static LayerDesc relu() { return LayerDesc{Kind::Relu}; }
+    static LayerDesc softmax() { return LayerDesc{Kind::Softmax}; }
+    static LayerDesc flatten() { return LayerDesc{Kind::Flatten}; }
+};
+
+struct NetworkSpec {
+    std::vector<long long> input;
+    std::vector<LayerDesc> layers;
+    int optimizer = 0;  // SgdMomentum
+    float lr = 0.1f, momentum = 0.9f, weight_decay = 0.0f;
+    std::size_t batch_size = 100;
+    unsigned seed = 42;
+};
+
+namespace detail {
+template <class T>
+std::vector<float> pack_rows(const T& t) {  // logical elements, lane padding stripped
+    const std::size_t rows = t.rows_total(), n = t.last_dim();
+    std::vector<float> out(rows * n);
+    for (std::size_t r = 0; r < rows; ++r) std::memcpy(out.data() + r * n, t.row_ptr(r), n * sizeof(float));
+    return out;
+}
+}  // namespace detail
+
+class Network {
+  public:
+    Network(const NetworkSpec& spec, int device = 0, int precision = B2N_TF32X3) {
+        std::vector<b2n_layer_desc> ld;
+        for (const LayerDesc& d : spec.layers)
+            ld.push_back({(int)d.kind, d.in, d.out, d.k, d.kh, d.kw, d.pad, d.p});
+        b2n_network_spec s{};
+        s.input_rank = (int)spec.input.size();
+        for (std::size_t i = 0; i < spec.input.size() && i < 3; ++i) s.input[i] = spec.input[i];
+        s.layers = ld.data();
+        s.n_layers = (int)ld.size();
+        s.optimizer = spec.optimizer;
+        s.lr = spec.lr, s.momentum = spec.momentum, s.weight_decay = spec.weight_decay;
+        s.batch_size = (long long)spec.batch_size;
+        s.seed = spec.seed;
+        b2n_net* h = nullptr;
+        check(b2n_build_network(&s, device, precision, &h));
+        h_.reset(h);
+        input_ = spec.input;
+        batch_size = spec.batch_size;
+        for (const LayerDesc& d : spec.layers)
+            if (d.kind == LayerDesc::Kind::Dense) classes_ = d.out;
+    }
+    b2n_net* handle() const { return h_.get(); }
+    std::size_t batch_size = 100;
+    long long classes() const { return classes_; }
+    long long input_size() const {
+        long long n = 1;
+        for (long long e : input_) n *= e;
+        return n;
+    }
+
+    // Network::trainable() (network.hpp:244-249): w then b per layer
+    int num_params() const {
+        int n = 0;
+        check(b2n_net_num_params(h_.get(), &n));
+        return n;
+    }
+    std::vector<long long> param_dims(int idx) const {
+        int rank = 0;
+        long long dims[4];
+        check(b2n_net_param_shape(h_.get(), idx, &rank, dims));
+        return std::vector<long long>(dims, dims + rank);
+    }
+    std::vector<float> param(int idx, int which = B2N_VALUE) const {
+        long long n = 1;
+        for (long long d : param_dims(idx)) n *= d;
+        std::vector<float> out((std::size_t)n);
+        check(b2n_net_get_param(h_.get(), idx, which, out.data()));
+        return out;
+    }
+    void set_param(int idx, const std::vector<float>& v, int which = B2N_VALUE) {
+        check(b2n_net_set_param(h_.get(), idx, which, v.data()));
+    }
+
+  private:
+    struct Del {
+        void operator()(b2n_net* n) const { b2n_net_destroy(n); }
+    };
+    std::unique_ptr<b2n_net, Del> h_;
+    std::vector<long long> input_;
+    long long classes_ = 0;
+};
+
+inline Network build_network(const NetworkSpec& spec, int device = 0) { return Network(spec, device); }
+
+// train_minibatch (network.hpp:463-472): x (batch, ...) and y one-hot (batch, classes)
+template <class T>
+double train_minibatch(Network& net, const T& x, const T& y) {
+    if (x.rank() < 2 || (long long)(x.rows_total() * x.last_dim() / x.dim(0)) != net.input_size())
+        throw ShapeError("network input expects (batch, " + std::to_string(net.input_size()) + ")");
+    if (y.rank() != 2 || y.dim(0) != x.dim(0) || (long long)y.dim(1) != net.classes())
+        throw ShapeError("softmax_cross_entropy: predictions and labels must both be (batch, classes)");
+    const std::vector<float> xs = detail::pack_rows(x), ys = detail::pack_rows(y);
+    double loss = 0.0;
+    check(b2n_train_minibatch(net.handle(), xs.data(), ys.data(), (long long)x.dim(0), &loss));
+    return loss;
+}
+
+// forward_batch (network.hpp:402): probabilities, plus argmax_row ids (first maximum wins)
+template <class T>
+std::vector<float> forward_batch(Network& net, const T& x, std::vector<int>* argmax = nullptr) {
+    const std::vector<float> xs = detail::pack_rows(x);
+    const long long B = (long long)x.dim(0);
+    std::vector<float> probs((std::size_t)(B * net.classes()));
+    std::vector<int> am((std::size_t)B);
+    check(b2n_forward_batch(net.handle(), xs.data(), B, probs.data(), am.data()));
+    if (argmax) *argmax = std::move(am);
+    return probs;
+}
+
+// evaluate (network.hpp:474-484) over a dataset of `n` packed samples and int labels
+inline double evaluate(Network& net, const float* images, const int* labels, std::size_t n) {
+    if (n == 0) throw Error("evaluate: empty dataset");
+    const long long per = net.input_size();
+    std::size_t correct = 0;
+    std::vector<float> probs;
+    std::vector<int> am;
+    for (std::size_t lo = 0; lo < n; lo += net.batch_size) {
+        const std::size_t hi = std::min(lo + net.batch_size, n);
+        const long long B = (long long)(hi - lo);
+        probs.resize((std::size_t)(B * net.classes()));
+        am.resize((std::size_t)B);
+        check(b2n_forward_batch(net.handle(), images + lo * per, B, probs.data(), am.data()));
+        for (long long r = 0; r < B; ++r) correct += am[(std::size_t)r] == labels[lo + (std::size_t)r];
+    }
+    return (double)correct / (double)n;
+}
+
+// Rbm (energy.hpp:16-32), binary units
+class Rbm {
+  public:
+    Rbm(std::size_t hidden, std::size_t visible, int device = 0, int precision = B2N_TF32X3)
+        : hidden_(hidden), visible_(visible) {
+        b2n_rbm* h = nullptr;
+        check(b2n_rbm_create((long long)hidden, (long long)visible, device, precision, &h));
+        h_.reset(h);
+    }
+    // Rbm::init (energy.hpp:31): glorot_fill(w, visible, hidden) drawn from the caller's generator,
+    // exactly as the reference consumes it (uniform_real_distribution<float>, layers.hpp:40-48)
+    void init(std::mt19937& rng) {
+        const float limit = std::sqrt(6.0f / static_cast<float>(visible_ + hidden_));
+        std::vector<float> w(hidden_ * visible_), bv(visible_, 0.0f), bh(hidden_, 0.0f);
+        for (float& x : w) {
+            const float u = std::generate_canonical<float, std::numeric_limits<float>::digits>(rng);
+            x = std::fma(u, limit - (-limit), -limit);
+        }
+        set(w, bv, bh);
+    }
+    void init_seed(unsigned seed) { check(b2n_rbm_init(h_.get(), seed)); }
+    void set(const std::vector<float>& w, const std::vector<float>& bv, const std::vector<float>& bh) {
+        check(b2n_rbm_set(h_.get(), w.data(), bv.data(), bh.data()));
+    }
+    void get(std::vector<float>& w, std::vector<float>& bv, std::vector<float>& bh) const {
+        w.resize(hidden_ * visible_);
+        bv.resize(visible_);
+        bh.resize(hidden_);
+        check(b2n_rbm_get(h_.get(), w.data(), bv.data(), bh.data()));
+    }
+    std::size_t hidden_units() const { return hidden_; }
+    std::size_t visible_units() const { return visible_; }
+    b2n_rbm* handle() const { return h_.get(); }
+
+  private:
+    struct Del {
+        void operator()(b2n_rbm* r) const { b2n_rbm_destroy(r); }
+    };
+    std::unique_ptr<b2n_rbm, Del> h_;
+    std::size_t hidden_, visible_;
+};
+
+// cd_k_update (energy.hpp:131-171). The reference draws its Bernoulli samples from `rng`; here the
+// same stream is drawn on the host (generate_canonical<double,53>, exactly what
+// std::bernoulli_distribution consumes) and supplied, so sampling stays bit-exact.
+template <class T>
+double cd_k_update(Rbm& rbm, const T& v0, int k, float lr, std::mt19937& rng) {
+    if (k < 1) throw ParamError("cd_k_update: k must be >= 1, got " + std::to_string(k));
+    if (v0.rank() != 2) throw ShapeError("cd_k_update: expected a rank-2 tensor, got rank " + std::to_string(v0.rank()));
+    if (v0.dim(1) != rbm.visible_units()) throw ShapeError("cd_k_update: visible extent mismatch");
+    const std::vector<float> vs = detail::pack_rows(v0);
+    const std::size_t B = v0.dim(0);
+    std::vector<double> u((std::size_t)k * B * rbm.hidden_units());
+    for (double& d : u) d = std::generate_canonical<double, 53>(rng);
+    double recon = 0.0;
+    check(b2n_cd_k_update(rbm.handle(), vs.data(), (long long)B, k, lr, u.data(), (long long)B, &recon));
+    return recon;
+}
+
+}  // namespace b200nn

@@ -207,8 +207,6 @@ inline Net::Net(const b2n_network_spec& spec, int device, int precision)
         if (spec.input[i] < 1) throw Error(B2N_ESPEC, "network spec input extents must be positive");
     if (spec.batch_size < 1) throw Error(B2N_ESPEC, "network spec batch_size must be >= 1");
     if (spec.optimizer != 0) throw Error(B2N_ESPEC, "b200nn: only the SGD-momentum optimizer is on the B200 path");
-    B2N_CUDA(cudaSetDevice(device));
-    B2N_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     input_.assign(spec.input, spec.input + spec.input_rank);
 
     auto shape_str = [](const std::vector<long long>& s) {
@@ -327,6 +325,9 @@ inline Net::Net(const b2n_network_spec& spec, int device, int precision)
         }
     }
     n_packed_ = round_up(off, 32);
+    // the spec is valid: from here on device work (spec errors above never touch the GPU)
+    B2N_CUDA(cudaSetDevice(device));
+    B2N_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
     P_.alloc(n_packed_ * 4);
     V_.alloc(n_packed_ * 4);
     G_.alloc(n_packed_ * 4);
@@ -385,7 +386,8 @@ inline void Net::alloc_activations() {
         if (L.kind == B2N_DENSE) {
             L.ld_out = round_up(L.out + (next_dense ? 1 : 0), 8);
             if (!last) req((void**)&L.Aout, cap * L.ld_out * 4);
-            L.ldd = round_up(L.out, 8);
+            // the standalone (classes > 256) softmax kernel keeps its row sum in column `out`
+            L.ldd = round_up(L.out + (last && L.out > 256 ? 1 : 0), 8);
             req((void**)&L.D, cap * L.ldd * 4);
         } else {
             const long long per = numel(L.out_shape);

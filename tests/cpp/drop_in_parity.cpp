@@ -1,0 +1,116 @@
+// drop_in_parity.cpp -- the reference and the B200 build side by side through their C++ APIs
+// (fastnn from /root/reference/proj/include, b200nn from include/b200nn.hpp), acceptance-style:
+// one PASS/FAIL line per criterion (the gate format of proj/tests/acceptance.cpp:657-685).
+// Built by oracle/Makefile into oracle/_ref/drop_in_parity (it links the reference headers);
+// run by tests/test_gpu_cpp.py on a GPU box.
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <string>
+
+#include "b200nn.hpp"
+#include "fastnn/energy.hpp"
+#include "fastnn/network.hpp"
+
+namespace {
+
+double norm_err(const std::vector<float>& got, const fastnn::Tensor& want) {
+    double num = 0, den = 0;
+    std::size_t i = 0;
+    for (std::size_t r = 0; r < want.rows_total(); ++r)
+        for (std::size_t j = 0; j < want.last_dim(); ++j, ++i) {
+            num = std::max(num, (double)std::fabs(got[i] - want.row_ptr(r)[j]));
+            den = std::max(den, (double)std::fabs(want.row_ptr(r)[j]));
+        }
+    return num / (den > 0 ? den : 1.0);
+}
+
+fastnn::Tensor random_batch(std::vector<long long> dims, unsigned seed) {
+    fastnn::Tensor t = fastnn::make_tensor(dims);
+    std::mt19937 rng(seed);
+    std::uniform_real_distribution<float> d(0.0f, 1.0f);
+    for (std::size_t r = 0; r < t.rows_total(); ++r)
+        for (std::size_t j = 0; j < t.last_dim(); ++j) t.row_ptr(r)[j] = d(rng);
+    return t;
+}
+
+bool net_criterion(const char* name, const std::vector<long long>& input,
+                   const std::vector<fastnn::LayerDesc>& fl, const std::vector<b200nn::LayerDesc>& bl, float lr,
+                   std::size_t batch) {
+    fastnn::NetworkSpec fs;
+    fs.input = input;
+    fs.layers = fl;
+    fs.lr = lr;
+    b200nn::NetworkSpec bs;
+    bs.input = input;
+    bs.layers = bl;
+    bs.lr = lr;
+    fastnn::Network ref = fastnn::build_network(fs);
+    b200nn::Network dev = b200nn::build_network(bs);
+    std::vector<long long> xd{(long long)batch};
+    xd.insert(xd.end(), input.begin(), input.end());
+    fastnn::Tensor x = random_batch(xd, 1);
+    fastnn::Tensor y = fastnn::make_tensor({(long long)batch, 10});
+    std::mt19937 lr_rng(2);
+    for (std::size_t r = 0; r < batch; ++r) y.at(r, lr_rng() % 10) = 1.0f;
+    double worst = 0, dloss = 0;
+    for (int step = 0; step < 3; ++step) {
+        const double lf = fastnn::train_minibatch(ref, x, y);
+        const double lb = b200nn::train_minibatch(dev, x, y);
+        dloss = std::max(dloss, std::fabs(lf - lb) / std::fabs(lf));
+    }
+    auto tp = ref.trainable();
+    for (int i = 0; i < dev.num_params(); ++i) worst = std::max(worst, norm_err(dev.param(i), *tp[i].value));
+    const bool ok = worst < 1e-3 && dloss < 1e-4;
+    std::printf("criterion %s: %s -- 3 steps, loss rel err %.2e, worst param norm err %.2e (tol 1e-3)\n", name,
+                ok ? "PASS" : "FAIL", dloss, worst);
+    return ok;
+}
+
+}  // namespace
+
+int main() {
+    using FL = fastnn::LayerDesc;
+    using BL = b200nn::LayerDesc;
+    bool ok = true;
+    ok &= net_criterion("mlp", {784}, {FL::dense(784, 500), FL::sigmoid(), FL::dense(500, 250), FL::sigmoid(),
+                                       FL::dense(250, 10), FL::softmax()},
+                        {BL::dense(784, 500), BL::sigmoid(), BL::dense(500, 250), BL::sigmoid(), BL::dense(250, 10),
+                         BL::softmax()},
+                        0.1f, 100);
+    ok &= net_criterion("mnist_cnn", {1, 28, 28},
+                        {FL::conv(8, 5, 5), FL::sigmoid(), FL::maxpool(), FL::conv(8, 5, 5), FL::sigmoid(),
+                         FL::maxpool(), FL::dense(128, 150), FL::sigmoid(), FL::dense(150, 10), FL::softmax()},
+                        {BL::conv(8, 5, 5), BL::sigmoid(), BL::maxpool(), BL::conv(8, 5, 5), BL::sigmoid(),
+                         BL::maxpool(), BL::dense(128, 150), BL::sigmoid(), BL::dense(150, 10), BL::softmax()},
+                        0.1f, 100);
+    ok &= net_criterion("cifar_cnn", {3, 32, 32},
+                        {FL::conv(12, 5, 5), FL::relu(), FL::maxpool(), FL::conv(12, 5, 5), FL::relu(), FL::maxpool(),
+                         FL::dense(300, 64), FL::relu(), FL::dense(64, 10), FL::softmax()},
+                        {BL::conv(12, 5, 5), BL::relu(), BL::maxpool(), BL::conv(12, 5, 5), BL::relu(), BL::maxpool(),
+                         BL::dense(300, 64), BL::relu(), BL::dense(64, 10), BL::softmax()},
+                        0.001f, 100);
+    {  // RBM CD-1 with the same generators on both sides
+        fastnn::Rbm ref(500, 784);
+        b200nn::Rbm dev(500, 784);
+        std::mt19937 ia(42), ib(42);
+        ref.init(ia);
+        dev.init(ib);
+        fastnn::Tensor v0 = fastnn::make_tensor({100, 784});
+        std::mt19937 vr(3);
+        std::bernoulli_distribution bit(0.5);
+        for (std::size_t r = 0; r < 100; ++r)
+            for (std::size_t j = 0; j < 784; ++j) v0.at(r, j) = bit(vr) ? 1.0f : 0.0f;
+        std::mt19937 ra(5), rb(5);
+        const double rf = fastnn::cd_k_update(ref, v0, 1, 0.1f, ra);
+        const double rd = b200nn::cd_k_update(dev, v0, 1, 0.1f, rb);
+        std::vector<float> w, bv, bh;
+        dev.get(w, bv, bh);
+        const double ew = norm_err(w, ref.w), ev = norm_err(bv, ref.bv), eh = norm_err(bh, ref.bh);
+        const bool r_ok = ew < 1e-3 && ev < 1e-3 && eh < 1e-3 && std::fabs(rf - rd) < 1e-3 * rf;
+        std::printf("criterion rbm_cd1: %s -- recon %.9g vs %.9g, W %.2e bv %.2e bh %.2e\n", r_ok ? "PASS" : "FAIL", rd,
+                    rf, ew, ev, eh);
+        ok &= r_ok;
+    }
+    return ok ? 0 : 1;
+}

@@ -1,0 +1,136 @@
+"""Generate the golden fixtures that pin the oracle to the reference (run in the build container,
+where /root/reference exists and oracle/_ref/libfastnn_ref.so is built by `make -C oracle`).
+
+Every array here comes from the UNMODIFIED reference (fastnn headers compiled behind
+oracle/ref_shim.cpp): build_network / train_minibatch (network.hpp:284, :463), gemm
+(gemm.hpp:225), cd_k_update (energy.hpp:131), sgd_momentum_step (optim.hpp:69) and, for the
+padded ImageNet-shaped net, the SURVEY 8(c) composite of reference primitives.
+
+    python tests/golden/make_golden.py        # writes tests/golden/*.npz and full_size.json
+"""
+from __future__ import annotations
+
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+ROOT = HERE.parents[1]
+sys.path.insert(0, str(ROOT))
+
+from oracle import oracle as O  # noqa: E402
+from paper_1804_04512_b200 import configs as CF  # noqa: E402
+
+
+def small_specs():
+    mlp = {"input": [64], "layers": [CF.dense(64, 48), CF.sigmoid(), CF.dense(48, 24), CF.sigmoid(),
+                                     CF.dense(24, 10), CF.softmax()], "lr": 0.1, "momentum": 0.9, "seed": 42}
+    mnist = {"input": [1, 12, 12], "layers": [CF.conv(4, 3, 3), CF.sigmoid(), CF.maxpool(), CF.conv(4, 2, 2),
+                                              CF.sigmoid(), CF.maxpool(), CF.dense(16, 12), CF.sigmoid(),
+                                              CF.dense(12, 10), CF.softmax()], "lr": 0.1, "momentum": 0.9, "seed": 7}
+    cifar = {"input": [3, 16, 16], "layers": [CF.conv(5, 5, 5), CF.relu(), CF.maxpool(), CF.conv(5, 3, 3),
+                                              CF.relu(), CF.maxpool(), CF.dense(20, 8), CF.relu(),
+                                              CF.dense(8, 10), CF.softmax()], "lr": 0.01, "momentum": 0.9,
+             "seed": 11}
+    imnet = {"input": [3, 16, 16], "layers": [CF.conv(4, 3, 3, 1), CF.relu(), CF.maxpool(), CF.conv(4, 3, 3, 1),
+                                              CF.relu(), CF.maxpool(), CF.dense(64, 16), CF.relu(),
+                                              CF.dense(16, 10), CF.softmax()], "lr": 0.05, "momentum": 0.9,
+             "seed": 13}
+    return {"mlp_small": (mlp, 12), "mnist_cnn_small": (mnist, 6), "cifar_cnn_small": (cifar, 5),
+            "imagenet_cnn_small": (imnet, 3)}
+
+
+def net_case(spec, B, steps=2):
+    per = int(np.prod(spec["input"]))
+    x = O.uniform_f32(101, B * per).reshape([B] + spec["input"])
+    lab = O.uniform_int(102, 0, 9, B)
+    ref = O.Net(spec, "ref")
+    out = {"x": x, "labels": lab}
+    for i in range(ref.num_params()):
+        out[f"init{i}"] = ref.get(i)
+    losses = []
+    probs = np.zeros((B, 10), np.float32)
+    losses.append(ref.forward_backward(x, lab, probs=probs))
+    out["probs0"] = probs
+    for i in range(ref.num_params()):
+        out[f"grad{i}"] = ref.get(i, 1)
+    ref.apply()
+    for _ in range(steps - 1):
+        losses.append(ref.train_minibatch(x, lab))
+    for i in range(ref.num_params()):
+        out[f"final{i}"] = ref.get(i)
+        out[f"vel{i}"] = ref.get(i, 2)
+    p, am = ref.forward(x)
+    out["probs_final"], out["argmax_final"] = p, am
+    out["losses"] = np.array(losses)
+    return out
+
+
+def main():
+    assert O.ref_available(), "build oracle/_ref first (make -C oracle) -- needs /root/reference"
+    meta = {}
+    rng = np.random.default_rng(2024)
+    g = {}
+    for ta in (0, 1):
+        for tb in (0, 1):
+            M, N, K = 13, 11, 17
+            a = rng.standard_normal((K, M) if ta else (M, K)).astype(np.float32)
+            b = rng.standard_normal((N, K) if tb else (K, N)).astype(np.float32)
+            g[f"a_{ta}{tb}"], g[f"b_{ta}{tb}"] = a, b
+            g[f"c_{ta}{tb}"] = O.gemm(ta, tb, a, b, "ref")
+    np.savez_compressed(HERE / "gemm.npz", **g)
+    for name, (spec, B) in small_specs().items():
+        np.savez_compressed(HERE / f"{name}.npz", **net_case(spec, B))
+        meta[name] = {"spec": spec, "batch": B}
+    # RBM CD-1 (the reference consumes its own std::mt19937(seed); the oracle takes the same stream
+    # as supplied uniforms)
+    H, V, B = 24, 40, 8
+    W = O.rbm_init(H, V, 42, "ref")
+    v0 = O.bernoulli_f32(3, 0.5, B * V).reshape(B, V)
+    bv = O.uniform_f32(9, V, -0.1, 0.1)
+    bh = O.uniform_f32(10, H, -0.1, 0.1)
+    recon, W1, bv1, bh1 = O.ref_cd_k(W, bv, bh, v0, 1, 0.1, 5)
+    np.savez_compressed(HERE / "rbm.npz", W=W, bv=bv, bh=bh, v0=v0, W1=W1, bv1=bv1, bh1=bh1,
+                        recon=np.array([recon]), rng_seed=np.array([5]))
+    # SGD trace (acceptance.cpp:483-555 grads {0.3, -0.2, 0.05})
+    p = np.array([1.0, 0, 0, 0], np.float32)
+    v = np.zeros(4, np.float32)
+    trace = []
+    lib = O.load("ref")
+    for gv in (0.3, -0.2, 0.05):
+        gg = np.array([gv, 0, 0, 0], np.float32)
+        lib.ref_sgd_momentum_step(O.fptr(p), O.fptr(v), O.fptr(gg), 4, 0.1, 0.9, 0.0)
+        trace.append(p[0])
+    np.savez_compressed(HERE / "sgd.npz", trace=np.array(trace, np.float32))
+    # full-size checksums: one reference step of every config at its full batch (B=100; the
+    # ImageNet-shaped composite at batch 2 to stay within seconds)
+    full = {}
+    for name in ["mlp", "mnist_cnn", "cifar_cnn", "imagenet_cnn"]:
+        spec = CF.NET_CONFIGS[name](2 if name == "imagenet_cnn" else 100)
+        B = spec["batch_size"]
+        per = int(np.prod(spec["input"]))
+        classes = [d for d in spec["layers"] if d["kind"] == CF.DENSE][-1]["out"]
+        x = O.uniform_f32(1, B * per).reshape([B] + spec["input"])
+        lab = O.uniform_int(2, 0, classes - 1, B)
+        ref = O.Net(spec, "ref")
+        loss = ref.train_minibatch(x, lab)
+        full[name] = {"batch": B, "loss": loss,
+                      "param_sums": [float(np.sum(ref.get(i).astype(np.float64))) for i in range(ref.num_params())],
+                      "param_abs_sums": [float(np.sum(np.abs(ref.get(i).astype(np.float64))))
+                                         for i in range(ref.num_params())]}
+    c = CF.RBM
+    W = O.rbm_init(c["hidden"], c["visible"], c["seed"], "ref")
+    v0 = O.bernoulli_f32(3, 0.5, c["batch_size"] * c["visible"]).reshape(c["batch_size"], c["visible"])
+    recon, W1, bv1, bh1 = O.ref_cd_k(W, np.zeros(c["visible"], np.float32), np.zeros(c["hidden"], np.float32), v0,
+                                     1, c["lr"], 5)
+    full["rbm"] = {"recon": recon, "w_sum": float(np.sum(W1.astype(np.float64))),
+                   "bv_sum": float(np.sum(bv1.astype(np.float64))), "bh_sum": float(np.sum(bh1.astype(np.float64)))}
+    (HERE / "full_size.json").write_text(json.dumps(full, indent=1))
+    (HERE / "meta.json").write_text(json.dumps(meta, indent=1))
+    print("golden fixtures written to", HERE)
+
+
+if __name__ == "__main__":
+    main()
