@@ -7,16 +7,17 @@
 //           reference's first-index tie rule (layers.hpp:228-232) via lane shuffles, writes only the
 //           pooled activation and a 1-byte argmax code -- the full-resolution conv output never
 //           reaches HBM.
-//   DGRAD : M = input pixels, N = input channels, K = kernels*kh*kw; the A operand is dZ gathered on
-//           the fly from the pooled gradient, argmax code and pooled activation (act'), i.e.
-//           pool_backward + activation_gradient + the padded-valid full conv (conv.hpp:337-345) in
-//           one pass. Skipped for the first layer (its dx is dead).
+//   DGRAD : M = input pixels, N = input channels, K = kernels*kh*kw; the A operand is gathered from
+//           dZ (pool_backward + activation_gradient), i.e. the padded-valid full conv
+//           (conv.hpp:337-345) as an implicit GEMM. Skipped for the first layer (its dx is dead).
 //   WGRAD : M = patch index (c,di,dj) plus a ones row (-> bias gradient), N = kernels, K = output
 //           pixels split across CTAs; per-CTA partial tiles are reduced in fixed order by
 //           conv_wgrad_reduce_kernel, which also applies the SGD-momentum step (deterministic).
-// Roles (288 threads): warps 0-3 gather A (and per-block B) tiles into 128 B-swizzled smem with the
-// 3xTF32 lo split, warp 4 allocates TMEM and issues tcgen05.mma, warps 5-8 drain a double-buffered
-// TMEM accumulator through the epilogue.
+// Roles (416 threads): warps 0-7 gather A (and per-block B) tiles into 128 B-swizzled smem with the
+// 3xTF32 lo split (all loads of a thread issued before its 16 B smem stores), warp 8 allocates TMEM
+// and issues tcgen05.mma, warps 9-12 drain a double-buffered TMEM accumulator through the epilogue.
+// Backward first materialises dZ = unpool(dpool) * act' once (conv_dz_kernel) so the dgrad / wgrad
+// gathers are single loads.
 #pragma once
 #include "runtime.cuh"
 
@@ -47,6 +48,7 @@ struct ConvParams {
     float* dx;          // DGRAD output (previous layer's D)
     long long lddx;
     float* ws;          // WGRAD partials [item][128][32]
+    const float* dz;    // DGRAD / WGRAD: unpooled pre-activation gradient [B][K][OH][OW]
     // work decomposition
     int items;       // total work items
     int kblocks;     // K blocks per item
@@ -58,7 +60,8 @@ struct ConvParams {
     long long npix;  // rows of the GEMM view (pixels)
 };
 
-constexpr int kConvThreads = 288;
+constexpr int kGatherWarps = 8;
+constexpr int kConvThreads = 32 * (kGatherWarps + 1 + 4);  // gather | MMA | 4 epilogue warps = 416
 constexpr int kConvStages = 4;
 
 template <int NP, int MODE, bool X3>
@@ -84,43 +87,36 @@ __device__ __forceinline__ uint32_t mnmaj_off(int mn, int k) {
     return (mn >> 5) * 4096 + k * 128 + (((((mn & 31) >> 3) ^ (k & 3)) & 3) << 5) + (mn & 7) * 4;
 }
 
+__device__ __forceinline__ void sts4(uint8_t* base, uint32_t off, float a, float b, float c, float d) {
+    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(base) + off), "f"(a), "f"(b), "f"(c), "f"(d)
+                 : "memory");
+}
+
 __device__ __forceinline__ float act_grad(int act, float g, float y) {
     if (act == ACT_SIGMOID) return g * y * (1.0f - y);  // layers.hpp:294
     if (act == ACT_RELU) return y > 0.0f ? g : 0.0f;
     return g;
 }
 
-// dZ = gradient w.r.t. the conv's pre-activation output at (b, kk, oy, ox), from the pooled
-// gradient: pool_backward (layers.hpp:240-271) then activation_gradient (layers.hpp:284-298)
-__device__ __forceinline__ float conv_dz(const ConvParams& p, int b, int kk, int oy, int ox) {
-    if (p.pool) {
-        const int py = oy >> 1, px = ox >> 1;
-        const long long pi = ((long long)kk * p.ph + py) * p.pw + px;
-        const int code = p.arg[(long long)b * p.g.k * p.ph * p.pw + pi];
-        if (code != ((oy & 1) << 1) + (ox & 1)) return 0.0f;
-        return act_grad(p.act, p.dy[(long long)b * p.lddy + pi], p.y[(long long)b * p.ldy + pi]);
-    }
-    const long long pi = ((long long)kk * p.g.oh + oy) * p.g.ow + ox;
-    return act_grad(p.act, p.dy[(long long)b * p.lddy + pi], p.y[(long long)b * p.ldy + pi]);
-}
-
 // decode a GEMM row of the FWD view into an output pixel; pool order puts a window on 4 rows
 __device__ __forceinline__ bool fwd_pixel(const ConvParams& p, long long row, int& b, int& oy, int& ox) {
+    b = oy = ox = 0;
     if (row >= p.npix) return false;
     if (p.pool) {
         const long long win = row >> 2;
         const int w = (int)(row & 3);
-        const long long per = (long long)p.ph * p.pw;
+        const int per = p.ph * p.pw;
         b = (int)(win / per);
-        const int rem = (int)(win % per);
-        oy = 2 * (rem / p.pw) + (w >> 1);
-        ox = 2 * (rem % p.pw) + (w & 1);
+        const int rem = (int)(win - (long long)b * per);
+        const int py = rem / p.pw;
+        oy = 2 * py + (w >> 1);
+        ox = 2 * (rem - py * p.pw) + (w & 1);
     } else {
-        const long long per = (long long)p.g.oh * p.g.ow;
+        const int per = p.g.oh * p.g.ow;
         b = (int)(row / per);
-        const int rem = (int)(row % per);
+        const int rem = (int)(row - (long long)b * per);
         oy = rem / p.g.ow;
-        ox = rem % p.g.ow;
+        ox = rem - oy * p.g.ow;
     }
     return true;
 }
@@ -130,6 +126,8 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_tc_kernel(const ConvPara
     using Cfg = ConvCfg<NP, MODE, X3>;
     constexpr int S = kConvStages;
     constexpr int NPAD = Cfg::NPAD;
+    constexpr int MMA_WARP = kGatherWarps;
+    constexpr int NG = 32 * kGatherWarps;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* stages = smem;
@@ -143,11 +141,11 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_tc_kernel(const ConvPara
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const ConvGeom& g = p.g;
-    const int HW = g.h * g.w;
+    const int HW = g.h * g.w, OHW = g.oh * g.ow;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
-            mbar_init(&full[s], 128);
+            mbar_init(&full[s], NG);
             mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -156,21 +154,21 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_tc_kernel(const ConvPara
         }
         fence_barrier_init();
     }
-    if (warp == 4) tmem_alloc(tslot, Cfg::TMEM_COLS);
-    // per-k tables and the static weight operand (FWD: W[n][c,di,dj]; DGRAD: W[kk][n][di,dj] as [n][kk,di,dj])
+    if (warp == MMA_WARP) tmem_alloc(tslot, Cfg::TMEM_COLS);
+    // per-k gather offsets: FWD/WGRAD patch index (c,di,dj) -> c*H*W + di*W + dj;
+    // DGRAD (kk,di,dj) -> kk*OH*OW - di*OW - dj (relative to the (iy+pad, ix+pad) position of dZ)
     const int Kdim = MODE == CONV_DGRAD ? p.kkk : p.ckk;
     for (int k = threadIdx.x; k < Cfg::KMAX; k += blockDim.x) {
         int off = 0, didj = 0;
         if (k < Kdim) {
             const int khw = g.kh * g.kw;
             const int ch = k / khw, r = k % khw, di = r / g.kw, dj = r % g.kw;
-            off = MODE == CONV_DGRAD ? ch * p.ph * p.pw : ch * HW;  // (unused for dgrad)
+            off = MODE == CONV_DGRAD ? ch * OHW - di * g.ow - dj : ch * HW + di * g.w + dj;
             didj = (di << 16) | dj;
-            if (MODE == CONV_DGRAD) off = ch;
         }
         ktab[k] = make_int2(off, didj);
     }
-    if (MODE != CONV_WGRAD) {
+    if (MODE != CONV_WGRAD) {  // the static weight operand, K-major, hi and lo
         const int kb_total = (Kdim + 31) / 32;
         for (int idx = threadIdx.x; idx < NP * kb_total * 32; idx += blockDim.x) {
             const int n = idx / (kb_total * 32), k = idx % (kb_total * 32);
@@ -183,8 +181,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_tc_kernel(const ConvPara
                     v = p.wk[((long long)kk * g.c + n) * khw + r];
                 }
             }
-            const int kb = k >> 5;
-            uint8_t* blk = wb + kb * (NP * 128);
+            uint8_t* blk = wb + (k >> 5) * (NP * 128);
             *reinterpret_cast<float*>(blk + kmaj_off(n, k & 31)) = v;
             if (X3) *reinterpret_cast<float*>(blk + Cfg::WB_BYTES / 2 + kmaj_off(n, k & 31)) = split_lo1(v);
         }
@@ -195,91 +192,115 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_tc_kernel(const ConvPara
     tc_fence_after();
     const uint32_t tmem_base = *tslot;
 
-    if (warp < 4) {
-        // ===================== gather producers (128 threads)
+    if (warp < kGatherWarps) {
+        // ===================== gather producers (256 threads): loads first, then 16 B smem stores
         const int t = threadIdx.x;
         int it = 0;
         for (int item = blockIdx.x; item < p.items; item += gridDim.x) {
+            // per-item row decode (FWD / DGRAD: one GEMM row per thread pair)
+            const int r = t & 127, half = t >> 7;
+            int b = 0, oy = 0, ox = 0;
+            bool ok = false;
+            const float* base = p.x;
+            if (MODE == CONV_FWD) {
+                ok = fwd_pixel(p, (long long)item * 128 + r, b, oy, ox);
+                base = p.x + (long long)b * p.ldx + (long long)(oy - g.pad) * g.w + (ox - g.pad);
+            } else if (MODE == CONV_DGRAD) {
+                const long long row = (long long)item * 128 + r;
+                ok = row < p.npix;
+                if (ok) {
+                    b = (int)(row / HW);
+                    const int rem = (int)(row - (long long)b * HW);
+                    oy = rem / g.w;  // (iy, ix) of the input pixel
+                    ox = rem - oy * g.w;
+                }
+                base = p.dz + (long long)b * g.k * OHW + (long long)(oy + g.pad) * g.ow + (ox + g.pad);
+            }
             for (int kb = 0; kb < p.kblocks; ++kb, ++it) {
                 const int s = it % S;
                 mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
                 uint8_t* a = stages + s * Cfg::STAGE_BYTES;
                 uint8_t* alo = a + Cfg::A_BYTES + Cfg::B_BYTES;
-                if (MODE == CONV_FWD) {
-                    int b, oy, ox;
-                    const bool ok = fwd_pixel(p, (long long)item * 128 + t, b, oy, ox);
-                    const float* xb = p.x + (long long)b * p.ldx;
-#pragma unroll 4
-                    for (int kk = 0; kk < 32; ++kk) {
-                        const int k = kb * 32 + kk;
-                        float v = 0.0f;
-                        if (ok && k < p.ckk) {
-                            const int2 e = ktab[k];
-                            const int iy = oy + (e.y >> 16) - g.pad, ix = ox + (e.y & 0xFFFF) - g.pad;
-                            if (iy >= 0 && iy < g.h && ix >= 0 && ix < g.w) v = __ldg(xb + e.x + iy * g.w + ix);
+                if (MODE == CONV_FWD || MODE == CONV_DGRAD) {
+                    float v[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int k = kb * 32 + half * 16 + i;
+                        const int2 e = ktab[k];
+                        const int di = e.y >> 16, dj = e.y & 0xFFFF;
+                        bool in = ok && k < Kdim;
+                        if (MODE == CONV_FWD) {
+                            if (g.pad) in = in && (unsigned)(oy - g.pad + di) < (unsigned)g.h &&
+                                           (unsigned)(ox - g.pad + dj) < (unsigned)g.w;
+                        } else {
+                            in = in && (unsigned)(oy + g.pad - di) < (unsigned)g.oh &&
+                                 (unsigned)(ox + g.pad - dj) < (unsigned)g.ow;
                         }
-                        *reinterpret_cast<float*>(a + kmaj_off(t, kk)) = v;
-                        if (X3) *reinterpret_cast<float*>(alo + kmaj_off(t, kk)) = split_lo1(v);
+                        v[i] = in ? __ldg(base + e.x) : 0.0f;
                     }
-                } else if (MODE == CONV_DGRAD) {
-                    const long long row = (long long)item * 128 + t;
-                    const bool ok = row < p.npix;
-                    const int b = ok ? (int)(row / HW) : 0, rem = ok ? (int)(row % HW) : 0;
-                    const int iy = rem / g.w, ix = rem % g.w;
-#pragma unroll 4
-                    for (int kk = 0; kk < 32; ++kk) {
-                        const int k = kb * 32 + kk;
-                        float v = 0.0f;
-                        if (ok && k < p.kkk) {
-                            const int2 e = ktab[k];
-                            const int oy = iy + g.pad - (e.y >> 16), ox = ix + g.pad - (e.y & 0xFFFF);
-                            if (oy >= 0 && oy < g.oh && ox >= 0 && ox < g.ow) v = conv_dz(p, b, e.x, oy, ox);
-                        }
-                        *reinterpret_cast<float*>(a + kmaj_off(t, kk)) = v;
-                        if (X3) *reinterpret_cast<float*>(alo + kmaj_off(t, kk)) = split_lo1(v);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t o = kmaj_off(r, half * 16 + 4 * j);
+                        sts4(a, o, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                        if (X3)
+                            sts4(alo, o, split_lo1(v[4 * j]), split_lo1(v[4 * j + 1]), split_lo1(v[4 * j + 2]),
+                                 split_lo1(v[4 * j + 3]));
                     }
-                } else {  // WGRAD: A'[K'=pixel][M'=patch] and B'[K'=pixel][N'=kernel], MN-major
+                } else {  // WGRAD: A'[K'=pixel][M'=patch], B'[K'=pixel][N'=kernel], MN-major
                     const int mt = item / p.chunks, ch = item % p.chunks;
                     const int kp = t & 31, grp = t >> 5;
                     const long long px = (long long)ch * p.chunk_px + kb * 32 + kp;
-                    const bool ok = px < p.npix && kb * 32 + kp < p.chunk_px;
-                    const int per = g.oh * g.ow;
-                    const int b = ok ? (int)(px / per) : 0, rem = ok ? (int)(px % per) : 0;
-                    const int oy = rem / g.ow, ox = rem % g.ow;
-                    const float* xb = p.x + (long long)b * p.ldx;
-                    uint8_t* bb = a + Cfg::A_BYTES;
-                    uint8_t* blo = alo + Cfg::A_BYTES;
-#pragma unroll 4
-                    for (int jj = 0; jj < 32; ++jj) {
-                        const int j = mt * 128 + grp * 32 + jj;
-                        float v = 0.0f;
-                        if (ok) {
+                    const bool pok = px < p.npix && kb * 32 + kp < p.chunk_px;
+                    int pb = 0, py = 0, pxx = 0;
+                    if (pok) {
+                        pb = (int)(px / OHW);
+                        const int rem = (int)(px - (long long)pb * OHW);
+                        py = rem / g.ow;
+                        pxx = rem - py * g.ow;
+                    }
+                    const float* xb = p.x + (long long)pb * p.ldx + (long long)(py - g.pad) * g.w + (pxx - g.pad);
+                    float v[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int j = mt * 128 + grp * 16 + i;
+                        float val = 0.0f;
+                        if (pok) {
                             if (j < p.ckk) {
                                 const int2 e = ktab[j];
-                                const int iy = oy + (e.y >> 16) - g.pad, ix = ox + (e.y & 0xFFFF) - g.pad;
-                                if (iy >= 0 && iy < g.h && ix >= 0 && ix < g.w) v = __ldg(xb + e.x + iy * g.w + ix);
+                                const int di = e.y >> 16, dj = e.y & 0xFFFF;
+                                const bool in = !g.pad || ((unsigned)(py - g.pad + di) < (unsigned)g.h &&
+                                                          (unsigned)(pxx - g.pad + dj) < (unsigned)g.w);
+                                if (in) val = __ldg(xb + e.x);
                             } else if (j == p.ckk) {
-                                v = 1.0f;  // ones row: its product with dZ is the bias gradient
+                                val = 1.0f;  // ones row: its product with dZ is the bias gradient
                             }
                         }
-                        const uint32_t o = mnmaj_off(grp * 32 + jj, kp);
-                        *reinterpret_cast<float*>(a + o) = v;
-                        if (X3) *reinterpret_cast<float*>(alo + o) = split_lo1(v);
+                        v[i] = val;
+                    }
+                    const float* dzp = p.dz + (long long)pb * g.k * OHW + (long long)py * g.ow + pxx;
+                    float d[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const int n = grp * 4 + i;
+                        d[i] = (pok && n < g.k) ? __ldg(dzp + (long long)n * OHW) : 0.0f;
                     }
 #pragma unroll
-                    for (int nn = 0; nn < 8; ++nn) {
-                        const int n = grp * 8 + nn;
-                        const float v = (ok && n < g.k) ? conv_dz(p, b, n, oy, ox) : 0.0f;
-                        const uint32_t o = mnmaj_off(n, kp);
-                        *reinterpret_cast<float*>(bb + o) = v;
-                        if (X3) *reinterpret_cast<float*>(blo + o) = split_lo1(v);
+                    for (int j = 0; j < 4; ++j) {
+                        const uint32_t o = mnmaj_off(grp * 16 + 4 * j, kp);
+                        sts4(a, o, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                        if (X3)
+                            sts4(alo, o, split_lo1(v[4 * j]), split_lo1(v[4 * j + 1]), split_lo1(v[4 * j + 2]),
+                                 split_lo1(v[4 * j + 3]));
                     }
+                    const uint32_t ob = Cfg::A_BYTES + mnmaj_off(grp * 4, kp);
+                    sts4(a, ob, d[0], d[1], d[2], d[3]);
+                    if (X3) sts4(alo, ob, split_lo1(d[0]), split_lo1(d[1]), split_lo1(d[2]), split_lo1(d[3]));
                 }
                 fence_proxy_async_smem();
                 mbar_arrive(&full[s]);
             }
         }
-    } else if (warp == 4) {
+    } else if (warp == MMA_WARP) {
         // ===================== MMA issuer
         if (lane == 0) {
             const uint32_t idesc =
@@ -326,7 +347,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_tc_kernel(const ConvPara
             }
         }
     } else {
-        // ===================== epilogue (warps 5..8 -> TMEM quadrants 1,2,3,0)
+        // ===================== epilogue (4 warps -> TMEM quadrants warp%4)
         const int q = warp & 3;
         const int r = 32 * q + lane;
         int ai = 0;
@@ -392,40 +413,69 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_tc_kernel(const ConvPara
             } else {  // WGRAD partial tile: rows = patch index, cols = kernels
                 float* dst = p.ws + (long long)item * 128 * 32 + r * 32;
 #pragma unroll
-                for (int n = 0; n < 32; n += 4) *reinterpret_cast<float4*>(dst + n) = make_float4(v[n], v[n + 1], v[n + 2], v[n + 3]);
+                for (int n = 0; n < 32; n += 4)
+                    *reinterpret_cast<float4*>(dst + n) = make_float4(v[n], v[n + 1], v[n + 2], v[n + 3]);
             }
         }
     }
     __syncwarp();
     tc_fence_before();
     __syncthreads();
-    if (warp == 4) {
+    if (warp == MMA_WARP) {
         tc_fence_after();
         tmem_dealloc(tmem_base, Cfg::TMEM_COLS);
     }
 }
 
-// fixed-order reduction of the WGRAD partials + the optimizer step on kernels and bias
-// (sgd_momentum_step, optim.hpp:69-80) or a plain gradient store (data-parallel split mode)
+// dZ = unpool(dpool) * act'(y): pool_backward (layers.hpp:240-271) + activation_gradient
+// (layers.hpp:284-298) materialised once per layer (dense [B][K][OH][OW]) so the dgrad / wgrad
+// gathers read it with one load. One thread per pooled element, float2 stores.
+__global__ void conv_dz_kernel(const ConvParams p, float* __restrict__ dz) {
+    const long long per = (long long)p.g.k * p.ph * p.pw;
+    const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (idx >= (long long)p.B * per) return;
+    const long long b = idx / per, pi = idx - b * per;
+    const float gv = p.dy[b * p.lddy + pi], yv = p.y[b * p.ldy + pi];
+    const float d = act_grad(p.act, gv, yv);
+    if (p.pool) {
+        const int k = (int)(pi / (p.ph * p.pw)), rem = (int)(pi % (p.ph * p.pw));
+        const int py = rem / p.pw, px = rem % p.pw;
+        const int code = p.arg[b * per + pi];
+        float* o = dz + ((b * p.g.k + k) * p.g.oh + 2 * py) * (long long)p.g.ow + 2 * px;
+        *reinterpret_cast<float2*>(o) = make_float2(code == 0 ? d : 0.0f, code == 1 ? d : 0.0f);
+        *reinterpret_cast<float2*>(o + p.g.ow) = make_float2(code == 2 ? d : 0.0f, code == 3 ? d : 0.0f);
+    } else {
+        dz[b * per + pi] = d;
+    }
+}
+
+// fixed-order reduction of the WGRAD partials (chunk groups summed by 8 thread groups, then the 8
+// group sums in order) + the optimizer step on kernels and bias (sgd_momentum_step,
+// optim.hpp:69-80) or a plain gradient store (data-parallel split mode). One block per patch row.
 __global__ void conv_wgrad_reduce_kernel(const float* __restrict__ ws, int chunks, int ckk, int kout, int mtiles,
                                          float* kern, float* kvel, float* bias, float* bvel, float* gk, float* gb,
                                          int fused, float lr, float mom, float wd) {
-    const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // over kout * (ckk + 1)
-    if (idx >= kout * (ckk + 1)) return;
-    const int n = idx / (ckk + 1), j = idx % (ckk + 1);
+    const int j = blockIdx.x;  // patch row (c,di,dj) or the bias row ckk
     const int mt = j / 128, r = j % 128;
+    const int n = threadIdx.x & 31, grp = threadIdx.x >> 5;
+    __shared__ float part[8][32];
     float acc = 0.0f;
-    for (int ch = 0; ch < chunks; ++ch) acc += ws[((long long)(mt * chunks + ch) * 128 + r) * 32 + n];
+    for (int ch = grp; ch < chunks; ch += 8) acc += ws[((long long)(mt * chunks + ch) * 128 + r) * 32 + n];
+    part[grp][n] = acc;
+    __syncthreads();
+    if (grp != 0 || n >= kout) return;
+    float s = part[0][n];
+    for (int q = 1; q < 8; ++q) s += part[q][n];
     float* pp = j < ckk ? kern + (long long)n * ckk + j : bias + n;
     float* vv = j < ckk ? kvel + (long long)n * ckk + j : bvel + n;
     float* gg = j < ckk ? gk + (long long)n * ckk + j : gb + n;
     if (fused) {
-        const float gr = acc + wd * *pp;
+        const float gr = s + wd * *pp;
         const float vel = mom * *vv - lr * gr;
         *vv = vel;
         *pp = *pp + vel;
     } else {
-        *gg = acc;
+        *gg = s;
     }
     (void)mtiles;
 }
@@ -446,12 +496,12 @@ struct ConvBwdLaunch {
     int np_d = 8;
     bool x3 = true;
     int grid_d = 1, grid_w = 1;
-    std::shared_ptr<DevMem> ws;
+    std::shared_ptr<DevMem> ws, dz;
     float *kern, *kvel, *bias, *bvel, *gk, *gb;
     float lr, mom, wd;
     double flops = 0, bytes = 0;
     void run(cudaStream_t st, bool fused) const;
-    int kernels() const { return has_dgrad ? 3 : 2; }
+    int kernels() const { return has_dgrad ? 4 : 3; }
 };
 
 template <int NP, int MODE, bool X3>
@@ -484,11 +534,13 @@ inline void launch_conv(const ConvParams& p, int np, bool x3, int grid, cudaStre
 inline void ConvFwdLaunch::run(cudaStream_t st) const { launch_conv<CONV_FWD>(p, np, x3, grid, st); }
 
 inline void ConvBwdLaunch::run(cudaStream_t st, bool fused) const {
+    const long long npool = (long long)pw.B * pw.g.k * pw.ph * pw.pw;
+    conv_dz_kernel<<<(unsigned)((npool + 255) / 256), 256, 0, st>>>(pw, dz->as<float>());
+    B2N_CUDA(cudaGetLastError());
     if (has_dgrad) launch_conv<CONV_DGRAD>(pd, np_d, x3, grid_d, st);
     launch_conv<CONV_WGRAD>(pw, 32, x3, grid_w, st);
-    const int n = pw.g.k * (pw.ckk + 1);
-    conv_wgrad_reduce_kernel<<<(n + 127) / 128, 128, 0, st>>>(pw.ws, pw.chunks, pw.ckk, pw.g.k, pw.mtiles_w, kern,
-                                                              kvel, bias, bvel, gk, gb, fused ? 1 : 0, lr, mom, wd);
+    conv_wgrad_reduce_kernel<<<pw.ckk + 1, 256, 0, st>>>(pw.ws, pw.chunks, pw.ckk, pw.g.k, pw.mtiles_w, kern, kvel,
+                                                         bias, bvel, gk, gb, fused ? 1 : 0, lr, mom, wd);
     B2N_CUDA(cudaGetLastError());
 }
 
@@ -564,6 +616,9 @@ inline ConvBwdLaunch plan_conv_bwd(const ConvGeom& g, int B, const float* x, lon
     base.arg = const_cast<uint8_t*>(arg);
     base.dy = dy;
     base.lddy = lddy;
+    L.dz = std::make_shared<DevMem>();
+    L.dz->alloc((size_t)B * g.k * g.oh * g.ow * 4);
+    base.dz = L.dz->as<float>();
     L.x3 = x3;
     const double opix = (double)B * g.oh * g.ow, ipix = (double)B * g.h * g.w;
     const double pooled = (double)B * g.k * base.ph * base.pw;

@@ -1,0 +1,126 @@
+"""Summarise the ncu captures of profiles/capture.sh into committed evidence.
+
+    python profiles/summarize.py r1      # reads gpurun_out/r1_*, writes profiles/r1_*.md + ncu_traffic.json
+
+Per kernel: duration, DRAM read+write bytes (-> `traffic` in bench.py's roofline), achieved DRAM
+throughput, tensor-pipe activity, SM throughput, registers, and the SASS proof of tcgen05/TMA.
+"""
+from __future__ import annotations
+
+import csv
+import io
+import json
+import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parents[1]
+OUT = ROOT / "gpurun_out"
+PROF = ROOT / "profiles"
+
+METRICS = {
+    "dur_us": "gpu__time_duration.sum",
+    "dram_read": "dram__bytes_read.sum",
+    "dram_write": "dram__bytes_write.sum",
+    "dram_pct": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+    "tensor_pct": "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm_pct": "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "regs": "launch__registers_per_thread",
+    "grid": "launch__grid_size",
+}
+UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1, "nsecond": 1e-3, "msecond": 1e3}
+
+RBM_STEP = ["rbm.hidden+sample", "rbm.visible+recon", "rbm.neg_hidden", "rbm.dW+update"]
+CIFAR_CONV = None  # labelled from the template's mode argument
+
+
+def raw_rows(rep: Path):
+    txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(txt)))
+    head, units = rows[0], rows[1]
+    out = []
+    for r in rows[2:]:
+        d = {"kernel": r[head.index("Kernel Name")]}
+        for k, m in METRICS.items():
+            if m in head:
+                i = head.index(m)
+                try:
+                    v = float(r[i].replace(",", ""))
+                except ValueError:
+                    v = None
+                if v is not None:
+                    v *= UNIT_SCALE.get(units[i], 1)
+                d[k] = v
+        out.append(d)
+    return out
+
+
+def launch_share(csv_path: Path):
+    rows = [r for r in csv.reader(open(csv_path)) if r and not r[0].startswith("==")]
+    head = rows[0]
+    ki, vi, ui = head.index("Kernel Name"), head.index("Metric Value"), head.index("Metric Unit")
+    agg = {}
+    for r in rows[1:]:
+        v = float(r[vi].replace(",", ""))
+        t = v * {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(r[ui], 1.0)
+        name = r[ki].split("(")[0]
+        agg.setdefault(name, [0, 0.0])
+        agg[name][0] += 1
+        agg[name][1] += t
+    return agg
+
+
+def main(tag: str):
+    lines = [f"# ncu summary, round tag `{tag}` (B200, `--clock-control none`)", "",
+             "Captured with `profiles/capture.sh` under gpurun; numbers from single-kernel replay",
+             "(cold-cache, serialised): compare SHARES with bench.py's live CUDA-event timings, not absolutes.", ""]
+    traffic = {}
+    for rep, names, title in [(OUT / f"{tag}_rbm_full.ncu-rep", RBM_STEP, "RBM CD-1 step (headline), 4 GEMM launches"),
+                              (OUT / f"{tag}_cifar_conv_full.ncu-rep", CIFAR_CONV, "CIFAR CNN conv kernels")]:
+        if not rep.exists():
+            continue
+        rows = raw_rows(rep)
+        lines += [f"## {title}", "", "| op | kernel | us | DRAM rd+wr MB | DRAM % | tensor-pipe % | SM % | regs | grid |",
+                  "|---|---|---|---|---|---|---|---|---|"]
+        for i, d in enumerate(rows):
+            if names is None:
+                mode = d["kernel"].split("<")[1].split(",")[1].strip() if "<" in d["kernel"] else "?"
+                op = {"0": "conv.fwd+act+pool", "1": "conv.dgrad", "2": "conv.wgrad"}.get(mode, "?") + f" (grid {d.get('grid', 0):.0f})"
+            else:
+                op = names[i] if i < len(names) else "?"
+            tb = (d.get("dram_read") or 0) + (d.get("dram_write") or 0)
+            traffic.setdefault(op, tb)
+            lines.append(f"| {op} | `{d['kernel'][:60]}` | {d.get('dur_us', 0):.2f} | {tb / 1e6:.3f} | "
+                         f"{d.get('dram_pct', 0):.1f} | {d.get('tensor_pct', 0):.1f} | {d.get('sm_pct', 0):.1f} | "
+                         f"{d.get('regs', 0):.0f} | {d.get('grid', 0):.0f} |")
+        lines.append("")
+    for c in ["rbm", "mlp", "mnist_cnn", "cifar_cnn"]:
+        p = OUT / f"{tag}_launches_{c}.csv"
+        if not p.exists():
+            continue
+        agg = launch_share(p)
+        tot = sum(v[1] for v in agg.values())
+        lines += [f"## launch list: `bench.py --profile-only --config {c}`", "", "| kernel | launches | total us | share |",
+                  "|---|---|---|---|"]
+        for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+            lines.append(f"| `{k[:70]}` | {n} | {t:.1f} | {t / tot:.1%} |")
+        lines.append("")
+    lib = ROOT / "paper_1804_04512_b200" / "_build" / "libb200nn.so"
+    if lib.exists():
+        sass = subprocess.run(["cuobjdump", "-sass", str(lib)], capture_output=True, text=True).stdout
+        import re
+        counts = {m: len(re.findall(r"\b" + m + r"\b", sass)) for m in ["UTCHMMA", "UTMALDG", "LDTM", "UTCBAR", "HMMA"]}
+        lines += ["## SASS evidence (cuobjdump -sass libb200nn.so)", "",
+                  "| mnemonic | count | meaning |", "|---|---|---|",
+                  f"| UTCHMMA | {counts['UTCHMMA']} | tcgen05.mma (kind::tf32) |",
+                  f"| UTMALDG | {counts['UTMALDG']} | TMA tensor loads |",
+                  f"| LDTM | {counts['LDTM']} | tcgen05.ld (TMEM -> registers) |",
+                  f"| UTCBAR | {counts['UTCBAR']} | tcgen05.commit -> mbarrier |",
+                  f"| HMMA | {counts['HMMA']} | legacy mma.sync (none expected) |", ""]
+    (PROF / f"{tag}_ncu_summary.md").write_text("\n".join(lines) + "\n")
+    (PROF / "ncu_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "r1")
