@@ -155,6 +155,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_tc_kernel(const ConvPara
         fence_barrier_init();
     }
     if (warp == MMA_WARP) tmem_alloc(tslot, Cfg::TMEM_COLS);
+    pdl_wait();  // weights / inputs below are written by earlier kernels of the step
     // per-k gather offsets: FWD/WGRAD patch index (c,di,dj) -> c*H*W + di*W + dj;
     // DGRAD (kk,di,dj) -> kk*OH*OW - di*OW - dj (relative to the (iy+pad, ix+pad) position of dZ)
     const int Kdim = MODE == CONV_DGRAD ? p.kkk : p.ckk;
@@ -345,6 +346,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_tc_kernel(const ConvPara
                 }
                 mma_commit(&tfull[acc]);
             }
+            pdl_trigger();  // all MMAs issued: the next kernel may launch
         }
     } else {
         // ===================== epilogue (4 warps -> TMEM quadrants warp%4)
@@ -431,6 +433,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_tc_kernel(const ConvPara
 // (layers.hpp:284-298) materialised once per layer (dense [B][K][OH][OW]) so the dgrad / wgrad
 // gathers read it with one load. One thread per pooled element, float2 stores.
 __global__ void conv_dz_kernel(const ConvParams p, float* __restrict__ dz) {
+    pdl_wait();
     const long long per = (long long)p.g.k * p.ph * p.pw;
     const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (idx >= (long long)p.B * per) return;
@@ -455,6 +458,7 @@ __global__ void conv_dz_kernel(const ConvParams p, float* __restrict__ dz) {
 __global__ void conv_wgrad_reduce_kernel(const float* __restrict__ ws, int chunks, int ckk, int kout, int mtiles,
                                          float* kern, float* kvel, float* bias, float* bvel, float* gk, float* gb,
                                          int fused, float lr, float mom, float wd) {
+    pdl_wait();
     const int j = blockIdx.x;  // patch row (c,di,dj) or the bias row ckk
     const int mt = j / 128, r = j % 128;
     const int n = threadIdx.x & 31, grp = threadIdx.x >> 5;
@@ -513,8 +517,7 @@ inline void launch_conv_inst(const ConvParams& p, int grid, cudaStream_t st) {
         return true;
     }();
     (void)attr;
-    conv_tc_kernel<NP, MODE, X3><<<grid, kConvThreads, Cfg::SMEM, st>>>(p);
-    B2N_CUDA(cudaGetLastError());
+    launch_ex(conv_tc_kernel<NP, MODE, X3>, dim3(grid), dim3(kConvThreads), Cfg::SMEM, st, 1u, p);
 }
 
 template <int MODE>
@@ -535,13 +538,11 @@ inline void ConvFwdLaunch::run(cudaStream_t st) const { launch_conv<CONV_FWD>(p,
 
 inline void ConvBwdLaunch::run(cudaStream_t st, bool fused) const {
     const long long npool = (long long)pw.B * pw.g.k * pw.ph * pw.pw;
-    conv_dz_kernel<<<(unsigned)((npool + 255) / 256), 256, 0, st>>>(pw, dz->as<float>());
-    B2N_CUDA(cudaGetLastError());
+    launch_ex(conv_dz_kernel, dim3((unsigned)((npool + 255) / 256)), dim3(256), 0, st, 1u, pw, dz->as<float>());
     if (has_dgrad) launch_conv<CONV_DGRAD>(pd, np_d, x3, grid_d, st);
     launch_conv<CONV_WGRAD>(pw, 32, x3, grid_w, st);
-    conv_wgrad_reduce_kernel<<<pw.ckk + 1, 256, 0, st>>>(pw.ws, pw.chunks, pw.ckk, pw.g.k, pw.mtiles_w, kern, kvel,
-                                                         bias, bvel, gk, gb, fused ? 1 : 0, lr, mom, wd);
-    B2N_CUDA(cudaGetLastError());
+    launch_ex(conv_wgrad_reduce_kernel, dim3(pw.ckk + 1), dim3(256), 0, st, 1u, (const float*)pw.ws, pw.chunks, pw.ckk,
+              pw.g.k, pw.mtiles_w, kern, kvel, bias, bvel, gk, gb, fused ? 1 : 0, lr, mom, wd);
 }
 
 inline int conv_np(int n) {

@@ -318,6 +318,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (threadIdx.x == 0) B2N_TRACE(1);
+    pdl_wait();  // everything above overlapped the previous kernel's tail
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
@@ -393,7 +394,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_wait(tmem_full, 0);
         tc_fence_after();
-        if (ct == 0) B2N_TRACE(51);
+        if (ct == 0) {
+            B2N_TRACE(51);
+            pdl_trigger();  // main loop done: let the next kernel launch and run its prologue
+        }
         const int q = warp & 3;            // TMEM lane quadrant this warp may access
         const int half = (warp - 2) >> 2;  // two warps per quadrant split the columns
         const int row = 32 * q + lane;

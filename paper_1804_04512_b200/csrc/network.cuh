@@ -505,8 +505,8 @@ inline void Net::build_plan(Plan& pl) {
                 float* pr = probs_;
                 float bd = (float)pl.Bg;
                 fwd.push_back(Op([=](cudaStream_t s) {
-                    softmax_xent_rows_kernel<<<(B * 32 + 255) / 256, 256, 0, s>>>(lg, ldl, B, (int)C, lab, bd, D, ldd,
-                                                                                   rl, am, pr, C);
+                    launch_ex(softmax_xent_rows_kernel, dim3((B * 32 + 255) / 256), dim3(256), 0, s, 1u,
+                              (const float*)lg, ldl, B, (int)C, (const int*)lab, bd, D, ldd, rl, am, pr, C);
                 }, "softmax_xent", 0.0, (double)B * C * 16));
                 ++nk_fwd;
                 if (ldd < C + 1) throw Error(B2N_EINTERNAL, "dlogits pitch");
@@ -610,8 +610,8 @@ inline void Net::build_plan(Plan& pl) {
     long long npk = n_packed_;
     pl.ops[SPLIT_APPLY].push_back(Op([=](cudaStream_t s) {
         if (dp) dp->allreduce_f32(G, (size_t)npk, s);
-        sgd_packed_kernel<<<grid_for(n4), 256, 0, s>>>(reinterpret_cast<float4*>(Pp), reinterpret_cast<float4*>(Vv),
-                                                       reinterpret_cast<const float4*>(G), n4, lr, mom, wd);
+        launch_ex(sgd_packed_kernel, dim3(grid_for(n4)), dim3(256), 0, s, 1u, reinterpret_cast<float4*>(Pp),
+                  reinterpret_cast<float4*>(Vv), reinterpret_cast<const float4*>(G), n4, lr, mom, wd);
     }, dp ? "allreduce+sgd" : "sgd", 0.0, (double)npk * 20));
     pl.nkernels[SPLIT_APPLY] = 1;
 }

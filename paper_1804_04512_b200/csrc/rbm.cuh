@@ -243,8 +243,8 @@ class Rbm {
             long long n = nW_;
             pl.ops.push_back(Op([=](cudaStream_t s) {
                 dp->allreduce_f32(G, (size_t)n, s);
-                axpy_kernel<<<grid_for(n / 4), 256, 0, s>>>(reinterpret_cast<float4*>(W),
-                                                            reinterpret_cast<const float4*>(G), n / 4, scale);
+                launch_ex(axpy_kernel, dim3(grid_for(n / 4)), dim3(256), 0, s, 1u, reinterpret_cast<float4*>(W),
+                          reinterpret_cast<const float4*>(G), n / 4, scale);
             }, "allreduce+update", 0.0, (double)n * 12));
             ++pl.nk;
         }

@@ -11,6 +11,7 @@
 #include <limits>
 #include <random>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -137,6 +138,45 @@ struct HostPinned {
     }
 };
 
+// ------------------------------------------------------------------ launches
+// Every step kernel is launched with programmatic stream serialization (PDL): inside a captured
+// graph the edge becomes programmatic, so a kernel's launch + prologue overlap its predecessor's
+// tail; kernels call pdl_wait() before touching dependent data. B2N_PDL=0 disables it.
+inline bool pdl_enabled() {
+    static bool on = [] {
+        const char* e = std::getenv("B2N_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline void launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                      unsigned cluster_z, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    int n = 0;
+    if (pdl_enabled()) {
+        at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[n].val.programmaticStreamSerializationAllowed = 1;
+        ++n;
+    }
+    if (cluster_z > 1) {
+        at[n].id = cudaLaunchAttributeClusterDimension;
+        at[n].val.clusterDim.x = 1;
+        at[n].val.clusterDim.y = 1;
+        at[n].val.clusterDim.z = cluster_z;
+        ++n;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = n;
+    B2N_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 // ------------------------------------------------------------------ GEMM plan
 // One operand of D = op(A) . op(B). K-major: row-major [rows][K] (fastnn NT side);
 // MN-major: row-major [K][rows] (the transposed side).
@@ -184,19 +224,9 @@ void launch_gemm_inst(const GemmLaunch& g, cudaStream_t st) {
         return true;
     }();
     (void)attr;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = g.grid;
-    cfg.blockDim = dim3(kThreads, 1, 1);
-    cfg.dynamicSmemBytes = Cfg::SMEM;
-    cfg.stream = st;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 1;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = (unsigned)g.p.splits;  // split-K CTAs of one tile form a cluster
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    B2N_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, X3>, g.ma, g.mb, g.p));
+    // split-K CTAs of one tile form a cluster along z
+    launch_ex(gemm_tc_kernel<BN, X3>, g.grid, dim3(kThreads, 1, 1), Cfg::SMEM, st, (unsigned)g.p.splits, g.ma, g.mb,
+              g.p);
 }
 
 inline void GemmLaunch::run(cudaStream_t st) const {
@@ -298,6 +328,7 @@ inline EpiParams epi_default() {
 // float4-vectorised, grid-stride, 16 B per thread per access.
 __global__ void sgd_packed_kernel(float4* __restrict__ p, float4* __restrict__ v, const float4* __restrict__ g,
                                   long long n4, float lr, float mom, float wd) {
+    pdl_wait();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
         float4 pp = p[i], vv = v[i];
         const float4 gg = g[i];
@@ -316,18 +347,21 @@ __global__ void sgd_packed_kernel(float4* __restrict__ p, float4* __restrict__ v
 }
 
 __global__ void fill_kernel(float* __restrict__ p, long long n, float v) {
+    pdl_wait();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         p[i] = v;
 }
 
 // ones column of an augmented activation matrix (the bias trick: [X | 1] . [W | b]^T)
 __global__ void set_column_kernel(float* __restrict__ p, long long rows, long long ld, long long col, float v) {
+    pdl_wait();
     long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (r < rows) p[r * ld + col] = v;
 }
 
 // W += alpha * D over a packed buffer (data-parallel RBM update after the allreduce)
 __global__ void axpy_kernel(float4* __restrict__ w, const float4* __restrict__ d, long long n4, float alpha) {
+    pdl_wait();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
         float4 a = w[i];
         const float4 b = d[i];
@@ -346,6 +380,7 @@ __global__ void softmax_xent_rows_kernel(const float* __restrict__ logits, long 
                                          const int* __restrict__ labels, float batch_div, float* __restrict__ dlogits,
                                          long long ldd, double* __restrict__ row_loss, int* __restrict__ argmax,
                                          float* __restrict__ probs, long long ldp) {
+    pdl_wait();
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (warp >= rows) return;
     const float* z = logits + (long long)warp * ld;
