@@ -294,4 +294,16 @@ int b2n_debug_gemm_trace(const float* A, long long lda, int ta, const float* B, 
     });
 }
 
+// bring-up: copy the B2N_TRACE=1 registry (regions x 512 CTAs x 64 u64 stamps); returns regions used
+int b2n_debug_trace_read(unsigned long long* host, long long max_u64, int* regions) {
+    return guard([&] {
+        auto& r = b2n::TraceRegistry::get();
+        *regions = r.used;
+        if (!r.buf.p) return;
+        const size_t n = std::min<size_t>((size_t)max_u64, r.buf.bytes / 8);
+        B2N_CUDA(cudaDeviceSynchronize());
+        B2N_CUDA(cudaMemcpy(host, r.buf.p, n * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
 }  // extern "C"

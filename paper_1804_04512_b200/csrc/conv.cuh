@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_tc_kernel(const ConvPara
 // dZ = unpool(dpool) * act'(y): pool_backward (layers.hpp:240-271) + activation_gradient
 // (layers.hpp:284-298) materialised once per layer (dense [B][K][OH][OW]) so the dgrad / wgrad
 // gathers read it with one load. One thread per pooled element, float2 stores.
-__global__ void conv_dz_kernel(const ConvParams p, float* __restrict__ dz) {
+static __global__ void conv_dz_kernel(const ConvParams p, float* __restrict__ dz) {
     pdl_wait();
     const long long per = (long long)p.g.k * p.ph * p.pw;
     const long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -455,7 +455,7 @@ __global__ void conv_dz_kernel(const ConvParams p, float* __restrict__ dz) {
 // fixed-order reduction of the WGRAD partials (chunk groups summed by 8 thread groups, then the 8
 // group sums in order) + the optimizer step on kernels and bias (sgd_momentum_step,
 // optim.hpp:69-80) or a plain gradient store (data-parallel split mode). One block per patch row.
-__global__ void conv_wgrad_reduce_kernel(const float* __restrict__ ws, int chunks, int ckk, int kout, int mtiles,
+static __global__ void conv_wgrad_reduce_kernel(const float* __restrict__ ws, int chunks, int ckk, int kout, int mtiles,
                                          float* kern, float* kvel, float* bias, float* bvel, float* gk, float* gb,
                                          int fused, float lr, float mom, float wd) {
     pdl_wait();
@@ -521,7 +521,12 @@ inline void launch_conv_inst(const ConvParams& p, int grid, cudaStream_t st) {
 }
 
 template <int MODE>
-inline void launch_conv(const ConvParams& p, int np, bool x3, int grid, cudaStream_t st) {
+void launch_conv(const ConvParams& p, int np, bool x3, int grid, cudaStream_t st) {
+    if constexpr (MODE == CONV_WGRAD) {  // always 32 kernel columns (MN-major atom width)
+        if (x3) launch_conv_inst<32, MODE, true>(p, grid, st);
+        else launch_conv_inst<32, MODE, false>(p, grid, st);
+        return;
+    }
     if (np == 8) {
         if (x3) launch_conv_inst<8, MODE, true>(p, grid, st);
         else launch_conv_inst<8, MODE, false>(p, grid, st);
@@ -533,6 +538,12 @@ inline void launch_conv(const ConvParams& p, int np, bool x3, int grid, cudaStre
         else launch_conv_inst<32, MODE, false>(p, grid, st);
     }
 }
+// each mode is instantiated in its own translation unit (conv_fwd.cu / conv_dgrad.cu / conv_wgrad.cu)
+#ifndef B2N_CONV_INSTANTIATE
+extern template void launch_conv<CONV_FWD>(const ConvParams&, int, bool, int, cudaStream_t);
+extern template void launch_conv<CONV_DGRAD>(const ConvParams&, int, bool, int, cudaStream_t);
+extern template void launch_conv<CONV_WGRAD>(const ConvParams&, int, bool, int, cudaStream_t);
+#endif
 
 inline void ConvFwdLaunch::run(cudaStream_t st) const { launch_conv<CONV_FWD>(p, np, x3, grid, st); }
 

@@ -1,0 +1,8 @@
+// gemm_e7.cu -- instantiates the tcgen05 GEMM for the EPI_RBM_NEGHID epilogue (all tile widths, both
+// precisions) in its own translation unit; see runtime.cuh gemm_launch_epi.
+#define B2N_GEMM_INSTANTIATE
+#include "runtime.cuh"
+
+namespace b2n {
+template void gemm_launch_epi<EPI_RBM_NEGHID>(const GemmLaunch&, cudaStream_t);
+}  // namespace b2n

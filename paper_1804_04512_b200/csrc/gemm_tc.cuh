@@ -69,6 +69,7 @@ struct GemmParams {
     int epi;
     int splits;      // split-K factor == cluster size along z
     int kb_per_split;
+    int pre_a, pre_b;  // operand not written by the preceding kernel: TMA it before griddepcontrol.wait
     float* ws;       // split-K partial tiles [tile][split][128][BN]
     EpiParams ep;
     unsigned long long* trace;  // bring-up timeline (%globaltimer ns), null in production
@@ -147,12 +148,13 @@ __device__ __forceinline__ bool vec_ok(const void* base, long long ld, int n, in
 }
 
 // elementwise epilogue on 4 columns [n, n+4) of row m (values v); returns the row partial for RBM_VIS
+template <int EPI>
 __device__ __forceinline__ double epi4(const GemmParams& p, int m, int n, const float (&v)[4]) {
     const EpiParams& e = p.ep;
     const int cnt = p.N - n < 4 ? p.N - n : 4;
     const long long row = (long long)m * e.ldc;
     double part = 0.0;
-    switch (p.epi) {
+    switch (EPI) {
         case EPI_STORE: {
             if (vec_ok(e.C, e.ldc, n, p.N)) {
                 *reinterpret_cast<float4*>(e.C + row + n) =
@@ -276,7 +278,31 @@ __device__ __forceinline__ void softmax_row(const GemmParams& p, const float* tr
     if (e.argmax) e.argmax[m] = best;
 }
 
-template <int BN, bool X3>
+// L2 prefetch of the epilogue's input rows for this tile, issued while the main loop runs
+template <int BN, int EPI>
+__device__ __forceinline__ void epilogue_prefetch(const GemmParams& p, int m0, int n0, int ct) {
+    const EpiParams& e = p.ep;
+    const int rows = min(kBM, p.M - m0);
+    auto rowpf = [&](const void* base, long long ld, int es) {
+        if (!base) return;
+        const int lines = (BN * es + 127) / 128;
+        for (int idx = ct; idx < rows * lines; idx += 32 * kEpiWarps) {
+            const int r = idx / lines, l = idx % lines;
+            prefetch_l2(static_cast<const char*>(base) + ((long long)(m0 + r) * ld + n0) * es + l * 128);
+        }
+    };
+    switch (EPI) {
+        case EPI_DACT: rowpf(e.aux, e.ld_aux, 4); rowpf(e.C, e.ldc, 4); break;
+        case EPI_SGD: rowpf(e.C, e.ldc, 4); rowpf(e.V, e.ldv, 4); break;
+        case EPI_AXPY: rowpf(e.C, e.ldc, 4); break;
+        case EPI_RBM_HID: rowpf(e.u, e.ldu, 8); rowpf(e.C, e.ldc, 4); rowpf(e.C2, e.ldc2, 4); break;
+        case EPI_RBM_VIS: rowpf(e.aux, e.ld_aux, 4); rowpf(e.C, e.ldc, 4); break;
+        default: rowpf(e.C, e.ldc, 4); break;
+    }
+    if (e.bias && ct < BN && n0 + ct < p.N) prefetch_l2(e.bias + (long long)(n0 + ct) * e.bias_stride);
+}
+
+template <int BN, bool X3, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
                    const GemmParams p) {
@@ -318,31 +344,59 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     if (threadIdx.x == 0) B2N_TRACE(1);
-    pdl_wait();  // everything above overlapped the previous kernel's tail
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------- TMA producer
-            for (int i = 0; i < num_kb; ++i) {
+            auto load_a = [&](int i) {
+                uint8_t* a = smem + (i % S) * Cfg::STAGE_BYTES;
+                const int k0 = (kb0 + i) * kBK;
+                if (!p.a_mn) {
+                    tma_load_2d(a, &mapA, &full[i % S], k0, m0);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < kBM / 32; ++j) tma_load_2d(a + j * 4096, &mapA, &full[i % S], m0 + 32 * j, k0);
+                }
+            };
+            auto load_b = [&](int i) {
+                uint8_t* b = smem + (i % S) * Cfg::STAGE_BYTES + Cfg::A_BYTES;
+                const int k0 = (kb0 + i) * kBK;
+                if (!p.b_mn) {
+                    tma_load_2d(b, &mapB, &full[i % S], k0, n0);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < BN / 32; ++j) tma_load_2d(b + j * 4096, &mapB, &full[i % S], n0 + 32 * j, k0);
+                }
+            };
+            // pull every K block past the resident stages toward L2 now: after the step's L2 flush
+            // the loads would otherwise pay HBM latency one pipeline round at a time
+            for (int i = S; i < num_kb; ++i) {
+                const int k0 = (kb0 + i) * kBK;
+                if (!p.a_mn) tma_prefetch_2d(&mapA, k0, m0);
+                else for (int j = 0; j < kBM / 32; ++j) tma_prefetch_2d(&mapA, m0 + 32 * j, k0);
+                if (!p.b_mn) tma_prefetch_2d(&mapB, k0, n0);
+                else for (int j = 0; j < BN / 32; ++j) tma_prefetch_2d(&mapB, n0 + 32 * j, k0);
+            }
+            // operands independent of the preceding kernel stream in while it drains (PDL)
+            const int pre = min(num_kb, S);
+            for (int i = 0; i < pre; ++i) {
+                mbar_arrive_expect_tx(&full[i], Cfg::A_BYTES + Cfg::B_BYTES);
+                if (i < 16) B2N_TRACE(2 + i);
+                if (p.pre_a) load_a(i);
+                if (p.pre_b) load_b(i);
+            }
+            pdl_wait();
+            for (int i = 0; i < pre; ++i) {
+                if (!p.pre_a) load_a(i);
+                if (!p.pre_b) load_b(i);
+            }
+            for (int i = pre; i < num_kb; ++i) {
                 const int s = i % S;
                 const uint32_t ph = (i / S) & 1;
                 mbar_wait(&empty[s], ph ^ 1);
-                uint8_t* a = smem + s * Cfg::STAGE_BYTES;
-                uint8_t* b = a + Cfg::A_BYTES;
                 mbar_arrive_expect_tx(&full[s], Cfg::A_BYTES + Cfg::B_BYTES);
                 if (i < 16) B2N_TRACE(2 + i);
-                const int k0 = (kb0 + i) * kBK;
-                if (!p.a_mn) {
-                    tma_load_2d(a, &mapA, &full[s], k0, m0);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < kBM / 32; ++j) tma_load_2d(a + j * 4096, &mapA, &full[s], m0 + 32 * j, k0);
-                }
-                if (!p.b_mn) {
-                    tma_load_2d(b, &mapB, &full[s], k0, n0);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < BN / 32; ++j) tma_load_2d(b + j * 4096, &mapB, &full[s], n0 + 32 * j, k0);
-                }
+                load_a(i);
+                load_b(i);
             }
         }
     } else if (warp == 1) {
@@ -380,6 +434,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {  // ---------------- splitters, then TMEM -> smem tile (warps 2..9)
         const int ct = threadIdx.x - 64;
+        epilogue_prefetch<BN, EPI>(p, m0, n0, ct);
         if (X3) {
             for (int i = 0; i < num_kb; ++i) {
                 const int s = i % S;
@@ -424,6 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
     tc_fence_before();
     __syncthreads();
+    pdl_wait();  // global writes (and epilogue reads) only after the preceding kernel completed
     if (threadIdx.x == 0) B2N_TRACE(53);
 
     // ---------------- split-K reduction across the cluster (fixed split order: deterministic)
@@ -457,12 +513,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             *reinterpret_cast<float4*>(tile + r * TP + c) = acc;
         }
+        if (threadIdx.x == 0) B2N_TRACE(58);
         __syncthreads();
         if (threadIdx.x == 0) B2N_TRACE(56);
     }
 
     // ---------------- fused epilogue on rows [r_lo, r_hi) of the tile
-    if (p.epi == EPI_SOFTMAX_XENT) {
+    if (threadIdx.x == 0) B2N_TRACE(59);
+    if constexpr (EPI == EPI_SOFTMAX_XENT) {
         for (int r = r_lo + threadIdx.x; r < r_hi; r += kThreads)
             if (m0 + r < p.M) softmax_row(p, tile + r * TP, m0 + r);
     } else {
@@ -477,9 +535,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (idx < total && m < p.M && n < p.N) {
                 const float4 t = *reinterpret_cast<const float4*>(tile + r * TP + c);
                 const float v[4] = {t.x, t.y, t.z, t.w};
-                part = epi4(p, m, n, v);
+                part = epi4<EPI>(p, m, n, v);
             }
-            if (G <= 32 && p.epi == EPI_RBM_VIS) {  // row partial over this CTA's BN columns
+            if constexpr (G <= 32 && EPI == EPI_RBM_VIS) {  // row partial over this CTA's BN columns
 #pragma unroll
                 for (int o = G / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
                 if (idx < total && (idx % G) == 0 && m < p.M)
@@ -488,6 +546,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     }
 
+    if (threadIdx.x == 0) B2N_TRACE(60);
     __syncthreads();
     if (threadIdx.x == 0) B2N_TRACE(57);
     if (warp == 1) {

@@ -32,14 +32,52 @@ struct Op {
     std::string name;
     double flops = 0, bytes = 0;
     int kernels = 1;
+    bool is_gemm = false;
+    GemmLaunch gemm;  // when is_gemm: launched directly (its PDL prefetch flags are per op list)
     Op() = default;
     template <class F>
     Op(F f, std::string n = "op", double fl = 0, double by = 0, int k = 1)
         : fn(std::move(f)), name(std::move(n)), flops(fl), bytes(by), kernels(k) {}
-    void operator()(cudaStream_t s) const { fn(s); }
+    void operator()(cudaStream_t s) const {
+        if (is_gemm)
+            gemm.run(s);
+        else
+            fn(s);
+    }
 };
 inline Op gemm_op(const GemmLaunch& g, const std::string& name) {
-    return Op([g](cudaStream_t s) { g.run(s); }, name, g.flops, g.bytes, 1);
+    Op o;
+    o.name = name;
+    o.flops = g.flops;
+    o.bytes = g.bytes;
+    o.is_gemm = true;
+    o.gemm = g;
+    return o;
+}
+// PDL prefetch analysis over one captured op list: a GEMM operand may be loaded before
+// griddepcontrol.wait iff the immediately preceding op does not write it (kernel N-2 has always
+// completed when kernel N launches). Non-GEMM ops count as writing everything.
+inline void assign_prefetch(std::vector<Op>& ops) {
+    for (size_t i = 0; i < ops.size(); ++i) {
+        if (!ops[i].is_gemm) continue;
+        GemmLaunch& g = ops[i].gemm;
+        if (i == 0) {  // first node of a graph: no in-graph predecessor
+            g.p.pre_a = g.p.pre_b = 1;
+            continue;
+        }
+        const Op& prev = ops[i - 1];
+        if (!prev.is_gemm) {
+            g.p.pre_a = g.p.pre_b = 0;
+            continue;
+        }
+        bool wa = false, wb = false;
+        for (const auto& w : prev.gemm.writes) {
+            wa = wa || overlaps(w, g.a_rng);
+            wb = wb || overlaps(w, g.b_rng);
+        }
+        g.p.pre_a = !wa;
+        g.p.pre_b = !wb;
+    }
 }
 
 // per-op device time of `steps` un-graphed runs of an op list (CUDA events between ops)
@@ -602,6 +640,7 @@ inline void Net::build_plan(Plan& pl) {
     pl.ops[SPLIT] = fwd;
     pl.ops[SPLIT].insert(pl.ops[SPLIT].end(), bwd_split.begin(), bwd_split.end());
     pl.nkernels[SPLIT] = nk_fwd + nk_split;
+    for (int m : {FWD, FUSED, SPLIT}) assign_prefetch(pl.ops[m]);
     // data-parallel apply: allreduce(G) then the packed SGD pass
     float* Pp = P;
     long long n4 = n_packed_ / 4;

@@ -248,6 +248,7 @@ class Rbm {
             }, "allreduce+update", 0.0, (double)n * 12));
             ++pl.nk;
         }
+        assign_prefetch(pl.ops);
         last_kernels_ = pl.nk;
     }
 

@@ -194,8 +194,19 @@ struct GemmLaunch {
     dim3 grid;
     std::shared_ptr<DevMem> ws;  // split-K partial tiles
     double flops = 0, bytes = 0;  // algorithmic work of one launch (roofline numerators)
+    // address ranges for the PDL prefetch analysis: operands read, epilogue outputs written
+    std::pair<uintptr_t, uintptr_t> a_rng{0, 0}, b_rng{0, 0};
+    std::vector<std::pair<uintptr_t, uintptr_t>> writes;
     void run(cudaStream_t st) const;
 };
+
+inline std::pair<uintptr_t, uintptr_t> rng_of(const void* p, long long rows, long long ld, int elem = 4) {
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    return {a, a + (uintptr_t)std::max<long long>(rows, 0) * ld * elem};
+}
+inline bool overlaps(std::pair<uintptr_t, uintptr_t> x, std::pair<uintptr_t, uintptr_t> y) {
+    return x.first < y.second && y.first < x.second;
+}
 
 // Algorithmic HBM bytes of one GEMM launch: each operand read once, each epilogue stream once.
 inline double gemm_bytes(int M, int N, int K, int epi) {
@@ -216,36 +227,78 @@ inline double gemm_bytes(int M, int N, int K, int epi) {
     return a + b + e;
 }
 
-template <int BN, bool X3>
+template <int BN, bool X3, int EPI>
 void launch_gemm_inst(const GemmLaunch& g, cudaStream_t st) {
     using Cfg = GemmCfg<BN, X3>;
     static bool attr = [] {
-        B2N_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, X3>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+        B2N_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, X3, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Cfg::SMEM));
         return true;
     }();
     (void)attr;
     // split-K CTAs of one tile form a cluster along z
-    launch_ex(gemm_tc_kernel<BN, X3>, g.grid, dim3(kThreads, 1, 1), Cfg::SMEM, st, (unsigned)g.p.splits, g.ma, g.mb,
-              g.p);
+    launch_ex(gemm_tc_kernel<BN, X3, EPI>, g.grid, dim3(kThreads, 1, 1), Cfg::SMEM, st, (unsigned)g.p.splits, g.ma,
+              g.mb, g.p);
 }
 
-inline void GemmLaunch::run(cudaStream_t st) const {
-#define B2N_G(BNV)                                     \
-    case BNV:                                          \
-        if (x3)                                        \
-            launch_gemm_inst<BNV, true>(*this, st);    \
-        else                                           \
-            launch_gemm_inst<BNV, false>(*this, st);   \
-        break;
-    switch (bn) {
-        B2N_G(16)
-        B2N_G(32)
-        B2N_G(64)
-        B2N_G(128)
-        B2N_G(256)
+// per-epilogue launchers, each instantiated in its own translation unit (gemm_e<N>.cu): one
+// kernel per (BN, precision, epilogue) keeps each kernel's code small -- after the per-step L2
+// flush every first-executed instruction line comes from HBM
+// tile widths the planner can choose per epilogue: 16 only with a K-major B (N <= 16), 256 only for
+// a fused softmax over up to 256 classes
+constexpr bool bn_allowed(int epi, int bn) {
+    return bn == 16 ? (epi == EPI_STORE || epi == EPI_BIAS_ACT || epi == EPI_SOFTMAX_XENT)
+                    : bn == 256 ? epi == EPI_SOFTMAX_XENT : true;
+}
+
+template <int BN, int EPI>
+inline void launch_gemm_bn(const GemmLaunch& g, cudaStream_t st) {
+    if constexpr (bn_allowed(EPI, BN)) {
+        if (g.x3)
+            launch_gemm_inst<BN, true, EPI>(g, st);
+        else
+            launch_gemm_inst<BN, false, EPI>(g, st);
+    } else {
+        throw Error(B2N_EINTERNAL, "tile width not instantiated for this epilogue");
+    }
+}
+
+template <int EPI>
+void gemm_launch_epi(const GemmLaunch& g, cudaStream_t st) {
+    switch (g.bn) {
+        case 16: launch_gemm_bn<16, EPI>(g, st); break;
+        case 32: launch_gemm_bn<32, EPI>(g, st); break;
+        case 64: launch_gemm_bn<64, EPI>(g, st); break;
+        case 128: launch_gemm_bn<128, EPI>(g, st); break;
+        case 256: launch_gemm_bn<256, EPI>(g, st); break;
         default: throw Error(B2N_ESHAPE, "bad BN");
     }
-#undef B2N_G
+}
+#ifndef B2N_GEMM_INSTANTIATE
+extern template void gemm_launch_epi<EPI_STORE>(const GemmLaunch&, cudaStream_t);
+extern template void gemm_launch_epi<EPI_BIAS_ACT>(const GemmLaunch&, cudaStream_t);
+extern template void gemm_launch_epi<EPI_DACT>(const GemmLaunch&, cudaStream_t);
+extern template void gemm_launch_epi<EPI_SOFTMAX_XENT>(const GemmLaunch&, cudaStream_t);
+extern template void gemm_launch_epi<EPI_SGD>(const GemmLaunch&, cudaStream_t);
+extern template void gemm_launch_epi<EPI_RBM_HID>(const GemmLaunch&, cudaStream_t);
+extern template void gemm_launch_epi<EPI_RBM_VIS>(const GemmLaunch&, cudaStream_t);
+extern template void gemm_launch_epi<EPI_RBM_NEGHID>(const GemmLaunch&, cudaStream_t);
+extern template void gemm_launch_epi<EPI_AXPY>(const GemmLaunch&, cudaStream_t);
+#endif
+
+inline void GemmLaunch::run(cudaStream_t st) const {
+    switch (p.epi) {
+        case EPI_STORE: gemm_launch_epi<EPI_STORE>(*this, st); break;
+        case EPI_BIAS_ACT: gemm_launch_epi<EPI_BIAS_ACT>(*this, st); break;
+        case EPI_DACT: gemm_launch_epi<EPI_DACT>(*this, st); break;
+        case EPI_SOFTMAX_XENT: gemm_launch_epi<EPI_SOFTMAX_XENT>(*this, st); break;
+        case EPI_SGD: gemm_launch_epi<EPI_SGD>(*this, st); break;
+        case EPI_RBM_HID: gemm_launch_epi<EPI_RBM_HID>(*this, st); break;
+        case EPI_RBM_VIS: gemm_launch_epi<EPI_RBM_VIS>(*this, st); break;
+        case EPI_RBM_NEGHID: gemm_launch_epi<EPI_RBM_NEGHID>(*this, st); break;
+        case EPI_AXPY: gemm_launch_epi<EPI_AXPY>(*this, st); break;
+        default: throw Error(B2N_EINTERNAL, "bad epilogue");
+    }
 }
 
 // Tile width and split-K factor: enough CTAs to put most SMs to work on these latency-bound shapes
@@ -259,7 +312,7 @@ inline Tiling pick_tiling(int M, int N, int K, bool b_mn, int epi) {
     if (epi == EPI_SOFTMAX_XENT) {
         bn = N <= 16 ? 16 : N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
         if (b_mn && bn < 32) bn = 32;
-    } else if (N <= 16 && !b_mn) {
+    } else if (N <= 16 && !b_mn && bn_allowed(epi, 16)) {
         bn = 16;
     } else {
         bn = 32;
@@ -270,16 +323,47 @@ inline Tiling pick_tiling(int M, int N, int K, bool b_mn, int epi) {
             }
     }
     const int tiles = mt * ((N + bn - 1) / bn);
-    // power-of-two cluster sizes (1, 2, 4, 8): odd sizes schedule poorly (measured: a 7-CTA
-    // cluster grid started its last CTAs ~6 us after the first)
-    int want = std::max(1, std::min({128 / std::max(tiles, 1), 8, nkb}));
+    // split-K only where it pays: ~0.35 us per 3xTF32 K block vs ~1.3 us for the cluster reduction
+    // (measured, tests/_graph_trace.py); power-of-two clusters, <= 112 CTAs for clusters of 8
     int splits = 1;
-    while (splits * 2 <= want) splits *= 2;
-    // 8-CTA clusters only co-schedule ~112 at a time on 148 SMs (measured); fall back to 4
-    if (splits == 8 && tiles * 8 > 112) splits = 4;
+    double best = nkb * 0.35;
+    for (int sp = 2; sp <= 8 && sp <= nkb; sp *= 2) {
+        if (tiles * sp > (sp == 8 ? 112 : 148)) break;
+        const double t = ((nkb + sp - 1) / sp) * 0.35 + 1.3;
+        if (t < best - 1e-9) {
+            best = t;
+            splits = sp;
+        }
+    }
     const int kbps = (nkb + splits - 1) / splits;
     return {bn, splits, kbps};
 }
+
+// Bring-up tracing (B2N_TRACE=1): every planned GEMM gets a region of a global device buffer in
+// which each CTA records %globaltimer stamps (gemm_tc.cuh B2N_TRACE slots); b2n_debug_trace_read
+// copies it out. Off by default (null trace pointer, no cost).
+struct TraceRegistry {
+    static constexpr int kRegionCtas = 512;
+    static constexpr int kMaxRegions = 64;
+    DevMem buf;
+    int used = 0;
+    bool on = false;
+    static TraceRegistry& get() {
+        static TraceRegistry r = [] {
+            TraceRegistry t;
+            const char* e = std::getenv("B2N_TRACE");
+            t.on = e && e[0] == '1';
+            return t;
+        }();
+        return r;
+    }
+    unsigned long long* next() {
+        if (!on) return nullptr;
+        if (!buf.p) buf.alloc((size_t)kMaxRegions * kRegionCtas * 64 * 8);
+        if (used >= kMaxRegions) return nullptr;
+        return buf.as<unsigned long long>() + (size_t)(used++) * kRegionCtas * 64;
+    }
+};
 
 inline GemmLaunch plan_gemm(int M, int N, int K, Operand A, Operand B, int epi, const EpiParams& ep, bool x3,
                             int bn = 0) {
@@ -301,8 +385,12 @@ inline GemmLaunch plan_gemm(int M, int N, int K, Operand A, Operand B, int epi, 
     g.p.epi = epi;
     g.p.ep = ep;
     g.p.trace = nullptr;
+    if ((long long)((N + 31) / 32) * ((M + kBM - 1) / kBM) * 8 <= TraceRegistry::kRegionCtas)
+        g.p.trace = TraceRegistry::get().next();
     g.p.splits = t.splits;
     g.p.kb_per_split = t.kb_per_split;
+    g.p.pre_a = 0;
+    g.p.pre_b = 0;
     g.p.ws = nullptr;
     g.grid = dim3((N + g.bn - 1) / g.bn, (M + kBM - 1) / kBM, t.splits);
     if (t.splits > 1) {
@@ -312,6 +400,17 @@ inline GemmLaunch plan_gemm(int M, int N, int K, Operand A, Operand B, int epi, 
     }
     g.flops = 2.0 * M * N * K;
     g.bytes = gemm_bytes(M, N, K, epi);
+    g.a_rng = rng_of(A.ptr, A.mn_major ? K : M, A.ld);
+    g.b_rng = rng_of(B.ptr, B.mn_major ? K : N, B.ld);
+    if (ep.C) g.writes.push_back(rng_of(ep.C, M, ep.ldc));
+    if (epi == EPI_SGD && ep.V) g.writes.push_back(rng_of(ep.V, M, ep.ldv));
+    if (epi == EPI_RBM_HID && ep.C2) g.writes.push_back(rng_of(ep.C2, M, ep.ldc2));
+    if (epi == EPI_RBM_VIS && ep.row_part) g.writes.push_back(rng_of(ep.row_part, 64, ep.ld_part, 8));
+    if (epi == EPI_SOFTMAX_XENT) {
+        if (ep.probs) g.writes.push_back(rng_of(ep.probs, M, ep.ld_probs));
+        if (ep.row_loss) g.writes.push_back(rng_of(ep.row_loss, M, 1, 8));
+        if (ep.argmax) g.writes.push_back(rng_of(ep.argmax, M, 1, 4));
+    }
     return g;
 }
 
@@ -326,7 +425,7 @@ inline EpiParams epi_default() {
 // ------------------------------------------------------------------ bandwidth kernels
 // sgd_momentum_step (optim.hpp:69-80) over one packed parameter / velocity / gradient buffer:
 // float4-vectorised, grid-stride, 16 B per thread per access.
-__global__ void sgd_packed_kernel(float4* __restrict__ p, float4* __restrict__ v, const float4* __restrict__ g,
+static __global__ void sgd_packed_kernel(float4* __restrict__ p, float4* __restrict__ v, const float4* __restrict__ g,
                                   long long n4, float lr, float mom, float wd) {
     pdl_wait();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
@@ -346,21 +445,21 @@ __global__ void sgd_packed_kernel(float4* __restrict__ p, float4* __restrict__ v
     }
 }
 
-__global__ void fill_kernel(float* __restrict__ p, long long n, float v) {
+static __global__ void fill_kernel(float* __restrict__ p, long long n, float v) {
     pdl_wait();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
         p[i] = v;
 }
 
 // ones column of an augmented activation matrix (the bias trick: [X | 1] . [W | b]^T)
-__global__ void set_column_kernel(float* __restrict__ p, long long rows, long long ld, long long col, float v) {
+static __global__ void set_column_kernel(float* __restrict__ p, long long rows, long long ld, long long col, float v) {
     pdl_wait();
     long long r = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (r < rows) p[r * ld + col] = v;
 }
 
 // W += alpha * D over a packed buffer (data-parallel RBM update after the allreduce)
-__global__ void axpy_kernel(float4* __restrict__ w, const float4* __restrict__ d, long long n4, float alpha) {
+static __global__ void axpy_kernel(float4* __restrict__ w, const float4* __restrict__ d, long long n4, float alpha) {
     pdl_wait();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
         float4 a = w[i];
@@ -376,7 +475,7 @@ __global__ void axpy_kernel(float4* __restrict__ w, const float4* __restrict__ d
 // softmax + softmax_cross_entropy for class counts beyond one tensor-core tile: one warp per row,
 // the max / exp-sum / normalise passes run in the reference's sequential order by lane 0 after a
 // warp-parallel max (max is order-independent), so dlogits and loss follow network.hpp:410-437.
-__global__ void softmax_xent_rows_kernel(const float* __restrict__ logits, long long ld, int rows, int cols,
+static __global__ void softmax_xent_rows_kernel(const float* __restrict__ logits, long long ld, int rows, int cols,
                                          const int* __restrict__ labels, float batch_div, float* __restrict__ dlogits,
                                          long long ldd, double* __restrict__ row_loss, int* __restrict__ argmax,
                                          float* __restrict__ probs, long long ldp) {
