@@ -21,6 +21,7 @@
 #include <random>
 
 #include "conv.cuh"
+#include "convt.cuh"
 #include "nccl_dyn.cuh"
 #include "runtime.cuh"
 
@@ -144,6 +145,10 @@ class Net {
         long long ldd = 0;
         uint8_t* arg = nullptr;  // pool argmax codes
         float* Dx = nullptr;     // gradient w.r.t. this layer's input (conv dgrad output)
+        // halo-tile conv path (convt.cuh): output / D row-blocked when a conv consumes them
+        bool blocked_out = false;
+        long long codes_bstride = 0;
+        int codes_pw = 0;
     };
 
     Net(const b2n_network_spec& spec, int device, int precision);
@@ -232,6 +237,19 @@ class Net {
     std::map<std::pair<long long, long long>, std::unique_ptr<Plan>> plans_;
     std::unique_ptr<DpComm> dp_;
     DevMem loss_sum_;  // dp: double partial loss
+    bool tconv_ = false;     // conv layers on the halo-tile kernels (convt.cuh) instead of conv.cuh
+    float* Xb_ = nullptr;    // row-blocked copy of a conv network's input
+    long long xb_bstride_ = 0;
+    TLayout out_layout(const Layer& L, float* p, long long ld) const {
+        TLayout t;
+        t.p = p;
+        t.bstride = ld;
+        t.blocked = L.blocked_out ? 1 : 0;
+        t.C = (int)L.out_shape[0];
+        t.H = (int)L.out_shape[1];
+        t.W = (int)L.out_shape[2];
+        return t;
+    }
 };
 
 // --------------------------------------------------------------------------- construction
@@ -341,6 +359,13 @@ inline Net::Net(const b2n_network_spec& spec, int device, int precision)
         if (L.kind == B2N_CONV && L.pool_after && (L.g.oh % 2 || L.g.ow % 2))
             throw Error(B2N_ESPEC, "maxpool needs even extents");
     classes_ = layers_.back().out;
+    {  // the halo-tile conv kernels cover 3x3 / 5x5 filters with <= 32 channels and kernels
+        const char* e = std::getenv("B2N_CONV_LEGACY");
+        tconv_ = !(e && e[0] == '1');
+        for (const Layer& L : layers_)
+            if (L.kind == B2N_CONV && !(L.g.kh == L.g.kw && (L.g.kh == 3 || L.g.kh == 5) && L.g.k <= 32 && L.g.c <= 32))
+                tconv_ = false;
+    }
 
     // packed parameter layout, trainable() order
     long long off = 0;
@@ -429,13 +454,21 @@ inline void Net::alloc_activations() {
             req((void**)&L.D, cap * L.ldd * 4);
         } else {
             const long long per = numel(L.out_shape);
+            const long long kq = (L.g.k + 3) / 4, oh = L.out_shape[1], ow = L.out_shape[2];
+            L.blocked_out = tconv_ && !next_dense && !last;
             // pooled (or plain) conv output; an augmented row when a dense layer consumes it
-            L.ld_out = next_dense ? round_up(per + 1, 8) : per;
+            L.ld_out = next_dense ? round_up(per + 1, 8) : L.blocked_out ? oh * kq * ow * 4 : per;
             req((void**)&L.Aout, cap * L.ld_out * 4);
-            L.ldd = next_dense ? round_up(per, 8) : per;
+            L.ldd = next_dense ? round_up(per, 8) : L.blocked_out ? L.ld_out : per;
             req((void**)&L.D, cap * L.ldd * 4);
-            if (L.pool_after) req((void**)&L.arg, cap * per);
+            L.codes_pw = (int)round_up(ow, 4);
+            L.codes_bstride = tconv_ ? oh * kq * L.codes_pw * 4 : per;
+            if (L.pool_after) req((void**)&L.arg, cap * L.codes_bstride);
         }
+    }
+    if (tconv_ && first.kind == B2N_CONV) {
+        xb_bstride_ = (long long)first.g.h * ((first.g.c + 3) / 4) * first.g.w * 4;
+        req((void**)&Xb_, cap * xb_bstride_ * 4);
     }
     if (classes_ > 256) {
         ldlog_ = round_up(classes_ + 1, 8);
@@ -501,6 +534,7 @@ inline void Net::build_plan(Plan& pl) {
     std::vector<Op> fwd, bwd_fused, bwd_split;
     int nk_fwd = 0, nk_fused = 0, nk_split = 0;
     const size_t nl = layers_.size();
+    std::vector<ConvTLaunch> tfwd(nl);  // halo-tile conv forward plans (their tiles / X maps feed wgrad)
 
     // ---------------- forward
     for (size_t i = 0; i < nl; ++i) {
@@ -550,6 +584,43 @@ inline void Net::build_plan(Plan& pl) {
                 if (ldd < C + 1) throw Error(B2N_EINTERNAL, "dlogits pitch");
             }
         } else {
+            if (tconv_) {
+                const ConvGeom& g = L.g;
+                const int Cp = (g.c + 3) & ~3;
+                const float* in = L.Ain;
+                long long in_bs = L.ld_in;
+                if (i == 0) {  // network input NCHW -> row-blocked (channel quads)
+                    float* xs = X_;
+                    long long ldx = ldx_, xbs = xb_bstride_;
+                    float* xb = Xb_;
+                    const long long n = (long long)B * g.h * (Cp / 4) * g.w;
+                    fwd.push_back(Op([=](cudaStream_t s) {
+                        launch_ex(convt_repack_kernel, dim3(grid_for(n)), dim3(256), 0, s, 1u, (const float*)xs, ldx, B,
+                                  g.c, g.h, g.w, xb, xbs);
+                    }, "conv0.repack", 0.0, (double)B * g.h * g.w * (g.c + Cp) * 4));
+                    in = Xb_;
+                    in_bs = xb_bstride_;
+                }
+                ConvTLaunch f = plan_convt(CT_FWD, B, Cp, g.h, g.w, g.kh, g.kw, g.pad, g.k, x3_);
+                f.map = make_map_blocked(in, B, Cp / 4, g.h, g.w, in_bs, f.p.P, f.p.HR);
+                f.p.act = L.act;
+                f.p.pool = L.pool_after ? 1 : 0;
+                f.p.bias = P + L.bias_off;
+                f.p.out = out_layout(L, L.Aout, L.ld_out);
+                f.p.codes = L.arg;
+                f.p.codes_bstride = L.codes_bstride;
+                f.p.codes_pw = L.codes_pw;
+                f.p.wk = P + L.kern_off;
+                f.p.wk_K = g.k;
+                f.p.wk_C = g.c;
+                const double outn = (double)B * numel(L.out_shape);
+                f.bytes = (double)B * g.c * g.h * g.w * 4 + outn * (L.pool_after ? 5 : 4) + (double)g.k * (g.c * g.kh * g.kw + 1) * 4;
+                f.flops = 2.0 * B * g.oh * g.ow * g.k * (double)g.c * g.kh * g.kw;
+                tfwd[i] = f;
+                fwd.push_back(Op([f](cudaStream_t s) { f.run(s); }, "conv" + std::to_string(i) + ".fwd", f.flops, f.bytes));
+                ++nk_fwd;
+                continue;
+            }
             ConvFwdLaunch c = plan_conv_fwd(L.g, B, L.Ain, L.ld_in, P + L.kern_off, P + L.bias_off, L.act, L.pool_after,
                                             L.Aout, L.ld_out, L.arg, x3_);
             fwd.push_back(Op([c](cudaStream_t s) { c.run(s); }, "conv" + std::to_string(i) + ".fwd", c.flops, c.bytes));
@@ -605,6 +676,62 @@ inline void Net::build_plan(Plan& pl) {
             bwd_split.push_back(gemm_op(gs, "dense" + std::to_string(ii) + ".wgrad"));
             ++nk_fused;
             ++nk_split;
+        } else if (tconv_) {
+            const ConvGeom& g = L.g;
+            const int Kp = (g.k + 3) & ~3;
+            const TLayout dP = out_layout(L, L.D, L.ldd), Pv = out_layout(L, L.Aout, L.ld_out);
+            const bool has_d = ii > 0;
+            DZSrc z;
+            std::memset(&z, 0, sizeof(z));
+            z.dP = dP;
+            z.P = Pv;
+            z.codes = L.arg;
+            z.codes_bstride = L.codes_bstride;
+            z.PWc = L.codes_pw;
+            z.act = L.act;
+            z.pool = L.pool_after ? 1 : 0;
+            z.OHz = g.oh;
+            z.OWz = g.ow;
+            z.tma = L.blocked_out ? 1 : 0;
+            z.Kq = Kp / 4;
+            ConvTLaunch d;
+            if (has_d) {  // dX = the previous conv's pooled-output gradient (row-blocked)
+                const Layer& Prev = layers_[ii - 1];
+                d = plan_convt(CT_DGRAD, B, Kp, g.oh, g.ow, g.kh, g.kw, g.kh - 1 - g.pad, g.c, x3_, &z);
+                std::memset(&d.map, 0, sizeof(d.map));
+                d.p.out = out_layout(Prev, Prev.D, Prev.ldd);
+                d.p.wk = P + L.kern_off;
+                d.p.wk_K = g.k;
+                d.p.wk_C = g.c;
+                const double pooled = (double)B * numel(L.out_shape);
+                d.bytes = pooled * 9 + (double)B * g.c * g.h * g.w * 4;
+                d.flops = 2.0 * B * g.h * g.w * g.c * (double)g.k * g.kh * g.kw;
+            }
+            auto wplan = [&](bool fused) {
+                ConvTWLaunch w = plan_convt_wgrad(tfwd[ii], g.k, g.c, z);
+                w.kern = P + L.kern_off;
+                w.kvel = Vv + L.kern_off;
+                w.bias = P + L.bias_off;
+                w.bvel = Vv + L.bias_off;
+                w.gk = G + L.kern_off;
+                w.gb = G + L.bias_off;
+                w.lr = lr_;
+                w.mom = mom_;
+                w.wd = wd_;
+                (void)fused;
+                return w;
+            };
+            const ConvTWLaunch wf = wplan(true), wsp = wplan(false);
+            const double fl = wf.flops + (has_d ? d.flops : 0.0), by = wf.bytes + (has_d ? d.bytes : 0.0);
+            const int nk = has_d ? 3 : 2;
+            bwd_fused.push_back(Op([d, wf, has_d](cudaStream_t s) {
+                if (has_d) d.run(s);
+                wf.run(s, true);
+            }, "conv" + std::to_string(ii) + ".bwd+sgd", fl, by, nk));
+            bwd_split.push_back(Op([d, wsp, has_d](cudaStream_t s) {
+                if (has_d) d.run(s);
+                wsp.run(s, false);
+            }, "conv" + std::to_string(ii) + ".bwd", fl, by, nk));
         } else {
             // conv: dgrad (unless first layer), then wgrad (+ fused SGD on the reduce)
             const bool first = ii == 0;
