@@ -142,8 +142,12 @@ struct ConvTParams {
     int N;             // real output channels
     int R, Wt, P, HR;  // output rows / cols per tile, halo cols / rows
     int tiles_x, tiles_y, ntiles;
-    int ksteps, stages;
-    int halo_bytes, stage_bytes, w_bytes;  // smem carve-up (host-computed)
+    int ksteps, slots, stages;  // K steps per halo row, TMEM row slots per buffer
+    int halo_bytes;             // fp32 halo [HR][G][P][4]
+    int h_bytes;                // one halo buffer incl. the slack MMA rows past the tile read
+    int stage_bytes, w_bytes;       // smem carve-up (host-computed)
+    const float* x;     // FWD input, row-blocked [b][y][G][Win][4]
+    long long x_bstride;
     // epilogue
     int act, pool;
     const float* bias;  // FWD
@@ -157,36 +161,39 @@ struct ConvTParams {
     // DGRAD producer: dZ of the layer, staged + expanded on the fly (two staging slots)
     DZSrc z;
     int zslot_bytes;
+    unsigned long long* trace;  // bring-up: per-tile role timestamps of CTA 0 (clock64), null in production
 };
+#define CT_TRACE(it, ev)                                                                  \
+    do {                                                                                  \
+        if (p.trace && blockIdx.x == 0 && (it) < 64 && p.trace[(it) * 8 + (ev)] == 0)        \
+            p.trace[(it) * 8 + (ev)] = clock64();                                                \
+    } while (0)
 
-// K step s (8 tf32 = two 16-byte chunks kc) -> correlation input channel / tap of element j of chunk kc
-__device__ __forceinline__ bool ct_kdecode(const ConvTParams& p, int s, int kc, int j, int& cin, int& di, int& dj) {
+// K step s of a halo row (tf32, K = 8 = two 16-byte chunks kc of 4 channels) -> correlation input
+// channel / tap column of element j (0..3) of chunk kc. G >= 2 quads: s = (dj, quad pair), the two
+// chunks are quads 2gp and 2gp+1 (a plane apart); G == 1: s = tap pair, the second chunk is the same
+// quad one pixel on (tap dj + 1). The filter row di is not part of K: it is stacked along N.
+__device__ __forceinline__ bool ct_kdecode(const ConvTParams& p, int s, int kc, int j, int& cin, int& dj) {
     if (p.G >= 2) {
-        const int GP = (p.G + 1) >> 1, tap = s / GP, gp = s - tap * GP;
-        di = tap / p.kw;
-        dj = tap - di * p.kw;
-        const int q = 2 * gp + kc;
+        const int GP = (p.G + 1) >> 1;
+        dj = s / GP;
+        const int q = 2 * (s - dj * GP) + kc;
         cin = 4 * q + j;
         return q < p.G;
     }
-    const int DJP = (p.kw + 1) >> 1;
-    di = s / DJP;
-    dj = 2 * (s - di * DJP) + kc;
+    dj = 2 * s + kc;
     cin = j;
     return dj < p.kw;
 }
-// byte offset of K step s for output row r inside the halo, and the K-chunk stride (LBO)
-__device__ __forceinline__ uint32_t ct_aoff(const ConvTParams& p, int r, int s, uint32_t& lbo) {
+// byte offset of K step s inside a halo row, and the K-chunk stride (LBO)
+__device__ __forceinline__ uint32_t ct_aoff(const ConvTParams& p, int s, uint32_t& lbo) {
     if (p.G >= 2) {
-        const int GP = (p.G + 1) >> 1, tap = s / GP, gp = s - tap * GP;
-        const int di = tap / p.kw, dj = tap - di * p.kw;
+        const int GP = (p.G + 1) >> 1, dj = s / GP, gp = s - dj * GP;
         lbo = (uint32_t)p.P * 16;
-        return (uint32_t)((((r + di) * p.G + 2 * gp) * p.P + dj) * 16);
+        return (uint32_t)((2 * gp * p.P + dj) * 16);
     }
-    const int DJP = (p.kw + 1) >> 1;
-    const int di = s / DJP, djp = s - di * DJP;
     lbo = 16;  // the second K chunk is the same row one pixel on: tap dj + 1
-    return (uint32_t)(((r + di) * p.P + 2 * djp) * 16);
+    return (uint32_t)(2 * s * 16);
 }
 
 constexpr uint32_t kLayoutNone = 0;
@@ -201,6 +208,48 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, u
         : "memory");
 }
 
+// 1-D bulk copy global -> shared (sizes / addresses multiples of 16 B), completing on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+// Input halo rows [ys, ys + HR) x cols [xs, xs + P) of a row-blocked tensor [b][y][G][W][4] into smem
+// [HR][G][P][4]: one bulk copy per (row, quad) of the in-range columns (a ~P*16-byte contiguous run),
+// zeros for the padding. A whole warp calls it: lanes zero-fill, lane 0 arms `bar` and issues the
+// copies. (A 5-D TMA box would have a 16-byte innermost extent: thousands of tiny TMA lines.)
+__device__ __forceinline__ void halo_load_warp(const float* base, long long bstride, int G, int H, int W, int b, int ys,
+                                               int xs, int HR, int P, uint8_t* dst, uint64_t* bar, int lane) {
+    const int xa = max(xs, 0), xe = min(xs + P, W);
+    const int ncol = xe - xa;
+    const int lz = ncol > 0 ? xa - xs : P;            // zero columns on the left (all when no overlap)
+    const int rz = ncol > 0 ? xs + P - xe : 0;        // zero columns on the right
+    const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int row = lane; row < HR * G; row += 32) {
+        const int hr = row / G;
+        float4* d = reinterpret_cast<float4*>(dst + (long long)row * P * 16);
+        const int y = ys + hr;
+        if ((unsigned)y >= (unsigned)H || ncol <= 0) {
+            for (int c = 0; c < P; ++c) d[c] = z4;
+        } else {
+            for (int c = 0; c < lz; ++c) d[c] = z4;
+            for (int c = P - rz; c < P; ++c) d[c] = z4;
+        }
+    }
+    fence_proxy_async_smem();
+    __syncwarp();
+    if (lane == 0) {
+        const int y_lo = max(ys, 0), y_hi = min(ys + HR, H);
+        const int rows = ncol > 0 && y_hi > y_lo ? (y_hi - y_lo) * G : 0;
+        mbar_arrive_expect_tx(bar, (uint32_t)(rows * ncol * 16));
+        for (int y = y_lo; rows && y < y_hi; ++y)
+            for (int g = 0; g < G; ++g)
+                bulk_g2s(dst + ((long long)((y - ys) * G + g) * P + lz) * 16,
+                         base + (long long)b * bstride + (((long long)y * G + g) * W + xa) * 4, (uint32_t)ncol * 16, bar);
+    }
+}
+
 __device__ __forceinline__ void ct_tile(const ConvTParams& p, int t, int& b, int& y0, int& x0) {
     const int per = p.tiles_x * p.tiles_y;
     b = t / per;
@@ -212,12 +261,169 @@ __device__ __forceinline__ void ct_tile(const ConvTParams& p, int t, int& b, int
 
 template <int MODE, bool X3>
 struct CtRoles {
-    static constexpr int kEpi0 = 2;                               // warps 2..5: epilogue
-    static constexpr int kProd0 = 6;                              // warps 6..: lo split / dZ expansion
-    static constexpr int kProdWarps = MODE == CT_DGRAD ? 8 : (X3 ? 4 : 0);
+    static constexpr int kEpi0 = 2;                               // warps 2..9: epilogue
+    static constexpr int kProd0 = 10;                             // warps 10..: lo split / dZ expansion
+    static constexpr int kProdWarps = MODE == CT_DGRAD ? 8 : 4;
     static constexpr int kThreads = 32 * (kProd0 + kProdWarps);
 };
 
+// warp-converged MMA issue: the whole warp runs the loop, one elected lane issues (a lone divergent
+// issuing thread costs ~2x per tcgen05.mma, measured)
+__device__ __forceinline__ void mma_tf32_elect(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
+        "@p tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_elect(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\t"
+        "@p tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(smem_u32(bar))
+        : "memory");
+}
+// zero 16 consecutive TMEM columns of this warp's 32 lanes
+__device__ __forceinline__ void tmem_zero16(uint32_t taddr) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr),
+        "r"(0u)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_zero8(uint32_t taddr) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(0u)
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_zero4(uint32_t taddr) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%1,%1,%1};" ::"r"(taddr), "r"(0u) : "memory");
+}
+template <int N>
+__device__ __forceinline__ void tmem_zeron(uint32_t taddr) {
+    if constexpr (N == 4) tmem_zero4(taddr);
+    else if constexpr (N == 8) tmem_zero8(taddr);
+    else
+#pragma unroll
+        for (int c = 0; c < N; c += 16) tmem_zero16(taddr + c);
+}
+
+// Epilogue of one warp over all tiles of the CTA: TMEM lane quadrant q (pixels 32q..32q+31 of each
+// tile row), channels [hsel*NK/2, (hsel+1)*NK/2). Specialised on activation / pooling / output layout.
+// FWD: bias + act (layers.hpp:138-146, :278-282), then the 2x2 max with the reference's first-index
+// tie rule over window order (0,0) (0,1) (1,0) (1,1) (layers.hpp:228-232) -> pooled value + code byte.
+template <int NK, int ACT, bool POOL, bool BLOCKED, int MODE>
+__device__ __forceinline__ void ct_epilogue(const ConvTParams& p, uint32_t tmem_base, int bufcols, uint64_t* tfull,
+                                            uint64_t* tempty, int q, int hsel, int lane) {
+    constexpr int NH = NK / 2;   // channels of this warp
+    constexpr int NQ = (NH + 3) / 4;
+    const int c_lo = hsel * NH;
+    const int L = 32 * q + lane;
+    const uint32_t tq = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)c_lo;
+    // output row r of buffer buf accumulates in row slot HR-1-r (see convt_mma_kernel); zero the real
+    // slots of both buffers once, then after every drain
+    auto zero_rows = [&](int buf) {
+        for (int r = 0; r < p.R; ++r) tmem_zeron<NH>(tq + (uint32_t)(buf * bufcols + (p.HR - 1 - r) * NK));
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    };
+    zero_rows(0);
+    zero_rows(1);
+    tc_fence_before();
+    mbar_arrive(&tempty[0]);
+    mbar_arrive(&tempty[1]);
+    const int Kq = (p.out.C + 3) >> 2;  // channel quads actually stored
+    float bias_r[NH];
+#pragma unroll
+    for (int j = 0; j < NH; ++j) bias_r[j] = (MODE == CT_FWD && c_lo + j < p.N) ? __ldg(p.bias + c_lo + j) : 0.0f;
+    const long long plane = (long long)p.out.H * p.out.W;  // NCHW channel stride
+    const long long qstride = (long long)p.out.W * 4;      // blocked quad stride (floats)
+    int it = 0;
+    for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
+        const int buf = it & 1;
+        mbar_wait_sleep(&tfull[buf], (it >> 1) & 1);
+        tc_fence_after();
+        if (q == 0 && hsel == 0 && lane == 0) CT_TRACE(it, 5);
+        int b, y0, x0;
+        ct_tile(p, t, b, y0, x0);
+        const int x = x0 + L;
+        const bool xok = L < p.Wt && x < p.OW;
+        const uint32_t tcol = tq + (uint32_t)(buf * bufcols + (p.HR - 1) * NK);  // slot of row 0; row r at -r*NK
+        float* ob = p.out.p + (long long)b * p.out.bstride;
+        for (int r = 0; r < p.R; r += POOL ? 2 : 1) {
+            float v0[NH], v1[NH];
+            tmem_ldn<NH>(tcol - r * NK, v0);
+            if (POOL) tmem_ldn<NH>(tcol - (r + 1) * NK, v1);
+            const int y = y0 + r;
+#pragma unroll
+            for (int j = 0; j < NH; ++j) {
+                v0[j] = apply_act(ACT, v0[j] + bias_r[j]);
+                if (POOL) v1[j] = apply_act(ACT, v1[j] + bias_r[j]);
+            }
+            if (POOL) {
+                const bool writer = xok && y + 1 < p.OH && (lane & 1) == 0;
+                const int py = y >> 1, px = x >> 1;
+                float* orow = BLOCKED ? ob + (long long)py * Kq * qstride + (long long)px * 4 : ob + (long long)py * p.out.W + px;
+                uint8_t* crow = p.codes + (long long)b * p.codes_bstride + (((long long)py * Kq) * p.codes_pw + px) * 4;
+#pragma unroll
+                for (int g = 0; g < NQ; ++g) {
+                    float o[4];
+                    uint32_t cw = 0;
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
+                        const int j = 4 * g + jj;
+                        const float a1 = __shfl_xor_sync(0xffffffffu, v0[j], 1);
+                        const float a3 = __shfl_xor_sync(0xffffffffu, v1[j], 1);
+                        float best = v0[j];
+                        uint32_t code = 0;
+                        if (a1 > best) best = a1, code = 1;
+                        if (v1[j] > best) best = v1[j], code = 2;
+                        if (a3 > best) best = a3, code = 3;
+                        o[jj] = best;
+                        cw |= code << (8 * jj);
+                    }
+                    const int gq = (c_lo >> 2) + g;
+                    if (writer && gq < Kq) {
+                        if (BLOCKED) {
+                            *reinterpret_cast<float4*>(orow + gq * qstride) = make_float4(o[0], o[1], o[2], o[3]);
+                        } else {
+#pragma unroll
+                            for (int jj = 0; jj < 4; ++jj)
+                                if (4 * gq + jj < p.out.C) orow[(4 * gq + jj) * plane] = o[jj];
+                        }
+                        *reinterpret_cast<uint32_t*>(crow + (long long)gq * p.codes_pw * 4) = cw;
+                    }
+                }
+            } else if (xok && y < p.OH) {
+                float* orow = BLOCKED ? ob + (long long)y * Kq * qstride + (long long)x * 4 : ob + (long long)y * p.out.W + x;
+#pragma unroll
+                for (int g = 0; g < NQ; ++g) {
+                    const int gq = (c_lo >> 2) + g;
+                    if (gq >= Kq) break;
+                    if (BLOCKED) {
+                        *reinterpret_cast<float4*>(orow + gq * qstride) =
+                            make_float4(v0[4 * g], v0[4 * g + 1], v0[4 * g + 2], v0[4 * g + 3]);
+                    } else {
+#pragma unroll
+                        for (int jj = 0; jj < 4; ++jj)
+                            if (4 * gq + jj < p.out.C) orow[(4 * gq + jj) * plane] = v0[4 * g + jj];
+                    }
+                }
+            }
+        }
+        zero_rows(buf);
+        tc_fence_before();
+        if (q == 0 && hsel == 0 && lane == 0) CT_TRACE(it, 6);
+        mbar_arrive(&tempty[buf]);
+    }
+}
+
+// Correlation over row-blocked halo tiles on the tensor cores (3xTF32: a.b = ah.bh + ah.bl + al.bh with
+// the hardware's tf32 truncation making the raw value the hi part, fp32 accumulate, ~1e-7 relative). Per tile (R output rows x Wt columns) and per halo row
+// h, each MMA reads the halo row ONCE and multiplies it with all kh filter rows stacked along N
+// (N = kh * NK). Output row r's accumulator lives in TMEM row slot (HR - 1 - r), so the MMA of halo row h
+// lands its kh products on rows h, h-1, .., h-kh+1 -- exactly the rows that need them. Slots are zeroed
+// by the epilogue after it drains them, so every MMA accumulates.
+//   warp 0      : FWD halo producer (bulk copies + edge zeros) | DGRAD dP/P/codes staging (TMA)
+//   warp 1      : TMEM allocation + MMA issue (warp-converged, elect.sync)
+//   warps 2..9  : epilogue (two warps per TMEM lane quadrant, half the channels each)
+//   warps 10..  : FWD lo split of the landed halo | DGRAD dZ expansion into hi / lo halo planes
 template <int NK, int MODE, bool X3>
 __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
     convt_mma_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapZdP,
@@ -236,15 +442,15 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
     uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
     uint64_t* zfull = reinterpret_cast<uint64_t*>(tslot + 2);  // DGRAD staging slots
     uint64_t* zempty = zfull + 2;
-    uint64_t* dtab = zempty + 2;  // per K step: A descriptor (row 0, stage 0), B descriptor
+    uint64_t* dtab = zempty + 2;  // per K step: A descriptor (halo row 0, stage 0), B descriptor
     uint8_t* zst = reinterpret_cast<uint8_t*>(dtab + 2 * p.ksteps);  // 2 staging slots (DGRAD)
     zst = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(zst) + 127) & ~uintptr_t(127));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int S = p.stages;
-    const int acc_cols = p.R * NK;
+    const int bufcols = p.slots * NK;
     uint32_t tcols = 32;
-    while (tcols < (uint32_t)(2 * acc_cols)) tcols <<= 1;
+    while (tcols < (uint32_t)(2 * bufcols)) tcols <<= 1;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
@@ -254,63 +460,60 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 128);
+            mbar_init(&tempty[a], 256);
             mbar_init(&zfull[a], 1);
             mbar_init(&zempty[a], 32 * Roles::kProdWarps);
         }
         fence_barrier_init();
-        if (MODE == CT_FWD) tma_prefetch(&mapX);
     }
     if (warp == 1) tmem_alloc(tslot, tcols);
-    // zero the slack behind every halo buffer once (the MMA rows past the tile width read it)
-    for (int s = 0; s < S; ++s)
-        for (int h = 0; h < (X3 ? 2 : 1); ++h) {
-            float4* z = reinterpret_cast<float4*>(smem + s * p.stage_bytes + h * (p.stage_bytes / 2) + p.halo_bytes);
-            const int n = (X3 ? p.stage_bytes / 2 : p.stage_bytes) - p.halo_bytes;
-            for (int i = threadIdx.x; i < n / 16; i += blockDim.x) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+    // zero the halo buffers once: the slack behind them is read by MMA rows past the tile width
+    for (int i = threadIdx.x; i < S * p.stage_bytes / 16; i += blockDim.x)
+        reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
     pdl_wait();  // weights and inputs are written by earlier kernels of the step
-    {  // weights, K-major no-swizzle: [kstep][kc][n][4]
-        const int total = p.ksteps * 2 * NK * 4;
+    {  // weights, K-major no-swizzle: [kstep][kc][n = di*NK + k][4]
+        const int NN = p.kh * NK;
+        const int total = p.ksteps * 2 * NN * 4;
         for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
-            const int j = idx & 3, n = (idx >> 2) % NK, kc = (idx / (4 * NK)) & 1, s = idx / (8 * NK);
-            int cin, di, dj;
+            const int j = idx & 3, n = (idx >> 2) % NN, kc = (idx / (4 * NN)) & 1, s = idx / (8 * NN);
+            const int di = n / NK, nn = n - di * NK;
+            int cin, dj;
             float v = 0.0f;
-            if (ct_kdecode(p, s, kc, j, cin, di, dj) && n < p.N) {
+            if (ct_kdecode(p, s, kc, j, cin, dj) && nn < p.N) {
                 if (MODE == CT_FWD) {
-                    if (cin < p.wk_C) v = __ldg(p.wk + (((long long)n * p.wk_C + cin) * p.kh + di) * p.kw + dj);
+                    if (cin < p.wk_C) v = __ldg(p.wk + (((long long)nn * p.wk_C + cin) * p.kh + di) * p.kw + dj);
                 } else if (cin < p.wk_K) {  // flipped, transposed: Wf[n=c][k][di][dj] = W[k][c][kh-1-di][kw-1-dj]
-                    v = __ldg(p.wk + (((long long)cin * p.wk_C + n) * p.kh + (p.kh - 1 - di)) * p.kw + (p.kw - 1 - dj));
+                    v = __ldg(p.wk + (((long long)cin * p.wk_C + nn) * p.kh + (p.kh - 1 - di)) * p.kw + (p.kw - 1 - dj));
                 }
             }
-            const int off = s * (2 * NK * 16) + kc * (NK * 16) + n * 16 + j * 4;
+            const int off = s * (2 * NN * 16) + kc * (NN * 16) + n * 16 + j * 4;
             *reinterpret_cast<float*>(wsm + off) = v;
-            if (X3) *reinterpret_cast<float*>(wsm + p.w_bytes + off) = split_lo1(v);
+            *reinterpret_cast<float*>(wsm + p.w_bytes + off) = split_lo1(v);
         }
     }
     for (int ks = threadIdx.x; ks < p.ksteps; ks += blockDim.x) {  // descriptors, built once
         uint32_t lbo;
-        const uint32_t ao = ct_aoff(p, 0, ks, lbo);
+        const uint32_t ao = ct_aoff(p, ks, lbo);
         dtab[2 * ks] = desc_none(smem_u32(smem) + ao, lbo);
-        dtab[2 * ks + 1] = desc_none(smem_u32(wsm) + (uint32_t)(ks * (2 * NK * 16)), NK * 16);
+        dtab[2 * ks + 1] = desc_none(smem_u32(wsm) + (uint32_t)(ks * (2 * p.kh * NK * 16)), p.kh * NK * 16);
     }
     fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tslot;
-    const int half = X3 ? p.stage_bytes / 2 : 0;  // lo halo offset inside a stage
 
     if (warp == 0) {
-        if (MODE == CT_FWD && lane == 0) {  // ---------------- TMA producer
+        if (MODE == CT_FWD) {  // ---------------- halo producer (bulk copies + edge zeros)
             int it = 0;
             for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
                 const int s = it % S;
-                mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
+                mbar_wait_sleep(&empty[s], ((it / S) & 1) ^ 1);
+                if (lane == 0) CT_TRACE(it, 0);
                 int b, y0, x0;
                 ct_tile(p, t, b, y0, x0);
-                mbar_arrive_expect_tx(&full[s], (uint32_t)p.halo_bytes);
-                tma_load_5d(smem + s * p.stage_bytes, &mapX, &full[s], 0, x0 - p.pad, 0, y0 - p.pad, b);
+                halo_load_warp(p.x, p.x_bstride, p.G, p.Hin, p.Win, b, y0 - p.pad, x0 - p.pad, p.HR, p.P,
+                               smem + s * p.stage_bytes, &full[s], lane);
             }
         } else if (MODE == CT_DGRAD && lane == 0 && p.z.tma) {  // ---------------- dP / P / codes staging
             int it = 0;
@@ -325,58 +528,58 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
                          p.z.pool ? Y0 >> 1 : Y0, (p.z.pool ? X0 >> 1 : X0) & ~3);
             }
         }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer
-            // descriptor arithmetic only touches the 14-bit start-address field (smem < 256 KB)
-            const uint32_t idesc = umma_idesc_tf32(128, NK, 0, 0);
-            const uint64_t a_lo_add = (uint64_t)(half >> 4), b_lo_add = (uint64_t)(p.w_bytes >> 4);
-            const uint64_t row_add = (uint64_t)((p.G >= 2 ? p.G * p.P * 16 : p.P * 16) >> 4);
-            int it = 0;
-            for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
-                const int s = it % S, buf = it & 1;
-                mbar_wait(&tempty[buf], ((it >> 1) & 1) ^ 1);
-                mbar_wait((MODE == CT_FWD && X3) ? &ready[s] : &full[s], (it / S) & 1);
-                tc_fence_after();
-                uint64_t a_add = (uint64_t)((s * p.stage_bytes) >> 4);
-                for (int r = 0; r < p.R; ++r, a_add += row_add) {
-                    const uint32_t tacc = tmem_base + (uint32_t)(buf * acc_cols + r * NK);
-#pragma unroll 2
-                    for (int ks = 0; ks < p.ksteps; ++ks) {
-                        const uint64_t dah = dtab[2 * ks] + a_add, dbh = dtab[2 * ks + 1];
-                        if (X3) {
-                            mma_tf32(tacc, dah + a_lo_add, dbh, idesc, ks != 0);
-                            mma_tf32(tacc, dah, dbh + b_lo_add, idesc, 1);
-                            mma_tf32(tacc, dah, dbh, idesc, 1);
-                        } else {
-                            mma_tf32(tacc, dah, dbh, idesc, ks != 0);
-                        }
+    } else if (warp == 1) {  // ---------------- MMA issue (whole warp, elected lane)
+        // descriptor arithmetic only touches the 14-bit start-address field (smem < 256 KB)
+        const uint32_t idesc = umma_idesc_tf32(128, p.kh * NK, 0, 0);
+        const uint64_t a_lo_add = (uint64_t)(p.h_bytes >> 4), b_lo_add = (uint64_t)(p.w_bytes >> 4);
+        const uint64_t row_add = (uint64_t)((p.G * p.P * 16) >> 4);
+        int it = 0;
+        for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
+            const int s = it % S, buf = it & 1;
+            mbar_wait(&tempty[buf], (it >> 1) & 1);  // slots drained and re-zeroed
+            mbar_wait(MODE == CT_FWD ? &ready[s] : &full[s], (it / S) & 1);
+            tc_fence_after();
+            if (lane == 0) CT_TRACE(it, 3);
+            uint64_t a_add = (uint64_t)((s * p.stage_bytes) >> 4);
+            for (int h = 0; h < p.HR; ++h, a_add += row_add) {
+                // halo row h feeds output rows h - di (di = 0..kh-1) = row slots HR-1-h .. HR-1-h+kh-1
+                const uint32_t tacc = tmem_base + (uint32_t)(buf * bufcols + (p.HR - 1 - h) * NK);
+                for (int ks = 0; ks < p.ksteps; ++ks) {
+                    const uint64_t dah = dtab[2 * ks] + a_add, dbh = dtab[2 * ks + 1];
+                    if (X3) {
+                        mma_tf32_elect(tacc, dah + a_lo_add, dbh, idesc);
+                        mma_tf32_elect(tacc, dah, dbh + b_lo_add, idesc);
                     }
+                    mma_tf32_elect(tacc, dah, dbh, idesc);
                 }
-                mma_commit(&empty[s]);
-                mma_commit(&tfull[buf]);
             }
-            pdl_trigger();
+            if (lane == 0) CT_TRACE(it, 4);
+            mma_commit_elect(&empty[s]);
+            mma_commit_elect(&tfull[buf]);
         }
+        if (lane == 0) pdl_trigger();
     } else if (warp >= Roles::kProd0) {
         const int pt = threadIdx.x - 32 * Roles::kProd0;
         constexpr int NP = 32 * Roles::kProdWarps;
+        const int chunks = p.HR * p.G * p.P;  // 16-byte quads of one halo
         int it = 0;
         for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
             const int s = it % S;
             uint8_t* hi = smem + s * p.stage_bytes;
-            if (MODE == CT_FWD) {  // ---------------- lo split of the TMA-landed halo
-                mbar_wait(&full[s], (it / S) & 1);
-                const uint32_t src = smem_u32(hi), dst = src + half;
-                for (int i = pt * 16; i < p.halo_bytes; i += NP * 16) {
-                    float x0, x1, x2, x3;
-                    asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                                 : "=f"(x0), "=f"(x1), "=f"(x2), "=f"(x3)
-                                 : "r"(src + i));
-                    asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(dst + i), "f"(split_lo1(x0)),
-                                 "f"(split_lo1(x1)), "f"(split_lo1(x2)), "f"(split_lo1(x3))
-                                 : "memory");
+            uint8_t* lo = hi + p.h_bytes;
+            if (MODE == CT_FWD) {  // ---------------- lo = x - tf32(x) of the landed halo (the raw halo is hi)
+                mbar_wait_sleep(&full[s], (it / S) & 1);
+                if (pt == 0) CT_TRACE(it, 1);
+                if (X3) {
+                    const float4* src = reinterpret_cast<const float4*>(hi);
+                    for (int i = pt; i < chunks; i += NP) {
+                        const float4 a = src[i];
+                        reinterpret_cast<float4*>(lo)[i] =
+                            make_float4(split_lo1(a.x), split_lo1(a.y), split_lo1(a.z), split_lo1(a.w));
+                    }
                 }
                 fence_proxy_async_smem();
+                if (pt == 0) CT_TRACE(it, 2);
                 mbar_arrive(&ready[s]);
             } else {  // ---------------- dZ halo expansion (hi + lo) from the staged pooled tile
                 int b, y0, x0;
@@ -386,20 +589,19 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
                 const int zs = it & 1;
                 uint8_t* slot = zst + zs * p.zslot_bytes;
                 if (p.z.tma) {
-                    mbar_wait(&zfull[zs], (it >> 1) & 1);
+                    mbar_wait_sleep(&zfull[zs], (it >> 1) & 1);
                 } else {
                     zs_load_sync(p.z, slot, b, sy0, sx0, pt, NP);
                     asm volatile("bar.sync 1, %0;" ::"r"(NP) : "memory");
                 }
-                mbar_wait(&empty[s], ((it / S) & 1) ^ 1);
-                const int chunks = p.HR * p.G * p.P;
+                mbar_wait_sleep(&empty[s], ((it / S) & 1) ^ 1);
                 for (int i = pt; i < chunks; i += NP) {
                     const int row = i / (p.G * p.P), rem = i - row * (p.G * p.P);
                     const int q = rem / p.P, col = rem - q * p.P;
                     const float4 d = zs_dz(p.z, slot, sy0, sx0, q, Y0 + row, X0 + col);
-                    *reinterpret_cast<float4*>(hi + (long long)i * 16) = d;
+                    reinterpret_cast<float4*>(hi)[i] = d;
                     if (X3)
-                        *reinterpret_cast<float4*>(hi + half + (long long)i * 16) =
+                        reinterpret_cast<float4*>(lo)[i] =
                             make_float4(split_lo1(d.x), split_lo1(d.y), split_lo1(d.z), split_lo1(d.w));
                 }
                 fence_proxy_async_smem();
@@ -410,102 +612,28 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
                     asm volatile("bar.sync 1, %0;" ::"r"(NP) : "memory");
             }
         }
-    } else {  // ---------------- epilogue: warps 2..5 -> TMEM lane quadrant warp % 4
+    } else {  // ---------------- epilogue: warps 2..9, two per TMEM lane quadrant (warp % 4), half the channels each
         const int q = warp & 3;
-        const int L = 32 * q + lane;
-        const int Kq = (p.out.C + 3) >> 2;  // output channel quads actually stored
-        int it = 0;
-        for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
-            const int buf = it & 1;
-            mbar_wait(&tfull[buf], (it >> 1) & 1);
-            tc_fence_after();
-            int b, y0, x0;
-            ct_tile(p, t, b, y0, x0);
-            const int x = x0 + L;
-            const bool xok = L < p.Wt && x < p.OW;
-            const uint32_t trow = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * acc_cols);
-            const int step = p.pool ? 2 : 1;
-            for (int r = 0; r < p.R; r += step) {
-                float v0[NK], v1[NK];
-#pragma unroll
-                for (int c0 = 0; c0 < NK; c0 += 8) {
-                    float tt[8];
-                    tmem_ld8(trow + r * NK + c0, tt);
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) v0[c0 + i] = tt[i];
-                }
-                if (p.pool) {
-#pragma unroll
-                    for (int c0 = 0; c0 < NK; c0 += 8) {
-                        float tt[8];
-                        tmem_ld8(trow + (r + 1) * NK + c0, tt);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) v1[c0 + i] = tt[i];
-                    }
-                }
-                const int y = y0 + r;
-                if (MODE == CT_FWD) {
-#pragma unroll
-                    for (int n = 0; n < NK; ++n) {
-                        const float bn = n < p.N ? __ldg(p.bias + n) : 0.0f;
-                        v0[n] = n < p.N ? apply_act(p.act, v0[n] + bn) : 0.0f;  // layers.hpp:138-146 + act
-                        if (p.pool) v1[n] = n < p.N ? apply_act(p.act, v1[n] + bn) : 0.0f;
-                    }
-                }
-                if (p.pool) {
-                    // 2x2 window: (y, x) (y, x+1) (y+1, x) (y+1, x+1) = codes 0..3, first maximum wins
-                    const bool wok = xok && y + 1 < p.OH;
-                    const int py = y >> 1, px = x >> 1;
-                    const bool writer = wok && (lane & 1) == 0;
-#pragma unroll
-                    for (int g = 0; g < NK / 4; ++g) {
-                        float o[4];
-                        uint32_t cw = 0;
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const int n = 4 * g + j;
-                            const float a1 = __shfl_xor_sync(0xffffffffu, v0[n], 1);
-                            const float a3 = __shfl_xor_sync(0xffffffffu, v1[n], 1);
-                            float best = v0[n];
-                            uint32_t code = 0;
-                            if (a1 > best) best = a1, code = 1;
-                            if (v1[n] > best) best = v1[n], code = 2;
-                            if (a3 > best) best = a3, code = 3;
-                            o[j] = best;
-                            cw |= code << (8 * j);
-                        }
-                        if (writer && g < Kq) {
-                            if (p.out.blocked) {
-                                *reinterpret_cast<float4*>(p.out.p + tl_quad(p.out, b, g, py, px)) =
-                                    make_float4(o[0], o[1], o[2], o[3]);
-                            } else {
-                                float* base = p.out.p + (long long)b * p.out.bstride + (long long)py * p.out.W + px;
-#pragma unroll
-                                for (int j = 0; j < 4; ++j)
-                                    if (4 * g + j < p.out.C) base[(long long)(4 * g + j) * p.out.H * p.out.W] = o[j];
-                            }
-                            *reinterpret_cast<uint32_t*>(p.codes + (long long)b * p.codes_bstride +
-                                                         (((long long)py * Kq + g) * p.codes_pw + px) * 4) = cw;
-                        }
-                    }
-                } else if (xok && y < p.OH) {
-#pragma unroll
-                    for (int g = 0; g < NK / 4; ++g) {
-                        if (g >= Kq) break;
-                        if (p.out.blocked) {
-                            *reinterpret_cast<float4*>(p.out.p + tl_quad(p.out, b, g, y, x)) =
-                                make_float4(v0[4 * g], v0[4 * g + 1], v0[4 * g + 2], v0[4 * g + 3]);
-                        } else {
-                            float* base = p.out.p + (long long)b * p.out.bstride + (long long)y * p.out.W + x;
-#pragma unroll
-                            for (int j = 0; j < 4; ++j)
-                                if (4 * g + j < p.out.C) base[(long long)(4 * g + j) * p.out.H * p.out.W] = v0[4 * g + j];
-                        }
-                    }
-                }
+        const int hsel = (warp - Roles::kEpi0) >> 2;
+        if (MODE == CT_DGRAD) {
+            ct_epilogue<NK, ACT_NONE, false, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane);
+        } else {
+            const int sel = (p.act == ACT_SIGMOID ? 2 : p.act == ACT_RELU ? 1 : 0) * 4 + (p.pool ? 2 : 0) +
+                            (p.out.blocked ? 1 : 0);
+            switch (sel) {
+                case 3: ct_epilogue<NK, ACT_NONE, true, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
+                case 2: ct_epilogue<NK, ACT_NONE, true, false, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
+                case 7: ct_epilogue<NK, ACT_RELU, true, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
+                case 6: ct_epilogue<NK, ACT_RELU, true, false, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
+                case 11: ct_epilogue<NK, ACT_SIGMOID, true, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
+                case 10: ct_epilogue<NK, ACT_SIGMOID, true, false, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
+                case 1: ct_epilogue<NK, ACT_NONE, false, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
+                case 0: ct_epilogue<NK, ACT_NONE, false, false, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
+                case 5: ct_epilogue<NK, ACT_RELU, false, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
+                case 4: ct_epilogue<NK, ACT_RELU, false, false, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
+                case 9: ct_epilogue<NK, ACT_SIGMOID, false, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
+                default: ct_epilogue<NK, ACT_SIGMOID, false, false, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
             }
-            tc_fence_before();
-            mbar_arrive(&tempty[buf]);
         }
     }
     __syncwarp();
@@ -523,6 +651,8 @@ struct ConvTWParams {
     int K, Kp, C;                             // real kernels, padded, real channels
     int R, Wt, P, HR, tiles_x, tiles_y, ntiles;
     int halo_bytes, slot_bytes;               // X halo; one (halo | dZ staging) slot
+    const float* x;                           // layer input, row-blocked
+    long long x_bstride;
     DZSrc z;
     float* ws;  // per-CTA partials [cta][Kp*Cp*kh*kw + Kp]
     int ws_stride;
@@ -562,9 +692,9 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 #pragma unroll
         for (int i = 0; i < T; ++i) acc[j][i] = 0.0f;
 
-    if (threadIdx.x == 0) {
-        mbar_init(&full[0], 1);
-        mbar_init(&full[1], 1);
+    if (threadIdx.x == 0) {  // two arrivals per fill: the dZ staging arm and the halo arm
+        mbar_init(&full[0], p.z.tma ? 2 : 1);
+        mbar_init(&full[1], p.z.tma ? 2 : 1);
         fence_barrier_init();
         tma_prefetch(&mapX);
     }
@@ -577,16 +707,19 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         y0 = ty * p.R;
         x0 = (rem - ty * p.tiles_x) * p.Wt;
     };
-    auto issue = [&](int t, int sl) {
+    auto issue = [&](int t, int sl) {  // warp 0: X halo (bulk copies) + dZ staging (TMA) on full[sl]
         int b, y0, x0;
         tile_of(t, b, y0, x0);
-        mbar_arrive_expect_tx(&full[sl], (uint32_t)p.halo_bytes + (p.z.tma ? zs_tx_bytes(p.z) : 0u));
-        tma_load_5d(slots[sl], &mapX, &full[sl], 0, x0 - p.pad, 0, y0 - p.pad, b);
-        if (p.z.tma)
+        const int lane = threadIdx.x & 31;
+        if (lane == 0 && p.z.tma) {
+            mbar_arrive_expect_tx(&full[sl], zs_tx_bytes(p.z));
             zs_issue(p.z, &mapZdP, &mapZP, &mapZc, slots[sl] + hb, &full[sl], b, p.z.pool ? y0 >> 1 : y0,
                      (p.z.pool ? x0 >> 1 : x0) & ~3);
+        }
+        halo_load_warp(p.x, p.x_bstride, p.G, p.H, p.W, b, y0 - p.pad, x0 - p.pad, p.HR, p.P, slots[sl], &full[sl],
+                       lane);
     };
-    if (threadIdx.x == 0 && (int)blockIdx.x < p.ntiles) issue(blockIdx.x, 0);
+    if (threadIdx.x < 32 && (int)blockIdx.x < p.ntiles) issue(blockIdx.x, 0);
     int it = 0;
     for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
         const int sl = it & 1;
@@ -605,7 +738,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             reinterpret_cast<float4*>(dz)[i] = zs_dz(p.z, zslot, sy0, sx0, q, Y, X);
         }
         __syncthreads();  // dz ready; the other slot (previous tile) is free
-        if (threadIdx.x == 0 && t + (int)gridDim.x < p.ntiles) issue(t + gridDim.x, sl ^ 1);
+        if (threadIdx.x < 32 && t + (int)gridDim.x < p.ntiles) issue(t + gridDim.x, sl ^ 1);
         if (active) {
             const float* hx = reinterpret_cast<const float*>(slots[sl]);
             const int cq = c >> 2, cj = c & 3;
@@ -780,14 +913,15 @@ inline void dz_maps(const DZSrc& z, int B, CUtensorMap out[3]) {
 }
 
 // tile shape for an OH x OW correlation output: Wt <= 128 columns, R (even) rows, 2*R*NK TMEM columns <= 512
-inline void ct_tile_shape(int OH, int OW, int NK, int& R, int& Wt) {
+inline void ct_tile_shape(int OH, int OW, int NK, int kh, int& R, int& Wt) {
     Wt = std::min(OW, 128);
     if (Wt & 1) ++Wt;
     R = (128 + Wt - 1) / Wt;
     R = std::max(2, (R + 1) & ~1);
     const int ohe = (OH + 1) & ~1;
     R = std::min(R, std::max(2, ohe));
-    while (2 * R * NK > 512 && R > 2) R -= 2;
+    // two TMEM buffers of (R + 2(kh-1)) row slots of NK columns
+    while (2 * (R + 2 * (kh - 1)) * NK > 512 && R > 2) R -= 2;
 }
 
 inline int ct_nk(int n) {
@@ -827,19 +961,21 @@ inline ConvTLaunch plan_convt(int mode, int B, int Cp, int Hin, int Win, int kh,
     p.OH = Hin + 2 * pad - kh + 1;
     p.OW = Win + 2 * pad - kw + 1;
     p.N = N;
-    ct_tile_shape(p.OH, p.OW, L.nk, p.R, p.Wt);
+    if (kh * L.nk > 256) throw Error(B2N_ESHAPE, "b200nn conv: kh x kernels exceeds one MMA (N <= 256)");
+    if (2 * (2 + 2 * (kh - 1)) * L.nk > 512) throw Error(B2N_ESHAPE, "b200nn conv: accumulators exceed TMEM");
+    ct_tile_shape(p.OH, p.OW, L.nk, kh, p.R, p.Wt);
     p.P = p.Wt + kw - 1;
     p.HR = p.R + kh - 1;
+    p.slots = p.HR + kh - 1;
     p.tiles_x = (p.OW + p.Wt - 1) / p.Wt;
     p.tiles_y = (p.OH + p.R - 1) / p.R;
     p.ntiles = B * p.tiles_x * p.tiles_y;
-    p.ksteps = p.G >= 2 ? kh * kw * ((p.G + 1) / 2) : kh * ((kw + 1) / 2);
+    p.ksteps = p.G >= 2 ? kw * ((p.G + 1) / 2) : (kw + 1) / 2;
     p.halo_bytes = p.HR * p.G * p.P * 16;
     // MMA rows past the tile width read at most (kw + 128) * 16 bytes beyond the halo (ct_aoff)
-    const int slack = (kw + 129) * 16;
-    const int one = (p.halo_bytes + slack + 127) & ~127;
-    p.stage_bytes = one * (x3 ? 2 : 1);
-    p.w_bytes = p.ksteps * 2 * L.nk * 16;
+    p.h_bytes = (p.halo_bytes + (kw + 129) * 16 + 127) & ~127;
+    p.stage_bytes = 2 * p.h_bytes;
+    p.w_bytes = p.ksteps * 2 * kh * L.nk * 16;
     std::memset(L.zmaps, 0, sizeof(L.zmaps));
     if (z) {  // DGRAD: pooled window covering the dZ halo rows / cols of a tile
         p.z = *z;
@@ -849,12 +985,13 @@ inline ConvTLaunch plan_convt(int mode, int B, int Cp, int Hin, int Win, int kh,
         dz_maps(p.z, B, L.zmaps);
     }
     const int fixed = 2 * p.w_bytes + 1024 + 256 + p.ksteps * 16 + 128 + 2 * p.zslot_bytes;
-    const int budget = 220 * 1024;
+    const int budget = 227 * 1024;
     p.stages = std::min(4, (budget - fixed) / p.stage_bytes);
     if (p.stages < 2) throw Error(B2N_ESHAPE, "b200nn conv: halo tile does not fit shared memory");
     L.smem = p.stages * p.stage_bytes + fixed;
     L.grid = std::min(p.ntiles, sm_count());
     L.flops = 2.0 * B * p.OH * p.OW * N * (double)Cp * kh * kw;
+    p.trace = TraceRegistry::get().next();
     return L;
 }
 
@@ -932,6 +1069,8 @@ inline ConvTWLaunch plan_convt_wgrad(const ConvTLaunch& f, int K, int C, const D
     p.tiles_y = q.tiles_y;
     p.ntiles = q.ntiles;
     p.halo_bytes = q.halo_bytes;
+    p.x = q.x;
+    p.x_bstride = q.x_bstride;
     p.z = z0;
     p.z.bh = z0.pool ? q.R / 2 : q.R;
     p.z.bw = ((z0.pool ? q.Wt / 2 : q.Wt) + 6) & ~3;  // window start is aligned down to 4 (TMA: 16 B)

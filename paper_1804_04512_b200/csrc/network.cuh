@@ -603,6 +603,8 @@ inline void Net::build_plan(Plan& pl) {
                 }
                 ConvTLaunch f = plan_convt(CT_FWD, B, Cp, g.h, g.w, g.kh, g.kw, g.pad, g.k, x3_);
                 f.map = make_map_blocked(in, B, Cp / 4, g.h, g.w, in_bs, f.p.P, f.p.HR);
+                f.p.x = in;
+                f.p.x_bstride = in_bs;
                 f.p.act = L.act;
                 f.p.pool = L.pool_after ? 1 : 0;
                 f.p.bias = P + L.bias_off;

@@ -109,6 +109,52 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]);
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, float (&v)[4]) {
+    uint32_t r[4];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+        : "r"(taddr)
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(r[i]);
+}
+// N consecutive columns (N = 4, 8, 16) of this warp's 32 lanes
+template <int N>
+__device__ __forceinline__ void tmem_ldn(uint32_t taddr, float* v) {
+    if constexpr (N == 4) {
+        float t[4];
+        tmem_ld4(taddr, t);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) v[i] = t[i];
+    } else if constexpr (N == 8) {
+        float t[8];
+        tmem_ld8(taddr, t);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = t[i];
+    } else {
+#pragma unroll
+        for (int c = 0; c < N; c += 16) {
+            float t[16];
+            tmem_ld16(taddr + c, t);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[c + i] = t[i];
+        }
+    }
+}
+// mbarrier wait for long waits: the suspend-time hint lets the warp sleep until the phase completes
+// instead of re-polling (polling warps steal issue slots from the working ones)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "B2N_WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
+        "@!p bra B2N_WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
     uint32_t r[8];
     asm volatile(
