@@ -135,6 +135,7 @@ __device__ __forceinline__ float4 zs_dz(const DZSrc& z, const uint8_t* slot, int
 }
 
 enum ConvTMode : int { CT_FWD = 0, CT_DGRAD = 1 };
+constexpr int kCtMaxKSteps = 16;  // K steps per halo row: kw * ceil(quads / 2) (or ceil(kw / 2) for one quad)
 
 struct ConvTParams {
     // the correlation this launch computes: input Hin x Win, Cp = 4*G channels, kh x kw, pad
@@ -162,6 +163,7 @@ struct ConvTParams {
     DZSrc z;
     int zslot_bytes;
     unsigned long long* trace;  // bring-up: per-tile role timestamps of CTA 0 (clock64), null in production
+    int dbg;                    // bring-up bisection (B2N_CT_DBG): 1 no lo split, 2 no epilogue work, 4 no halo copy
 };
 #define CT_TRACE(it, ev)                                                                  \
     do {                                                                                  \
@@ -346,7 +348,7 @@ __device__ __forceinline__ void ct_epilogue(const ConvTParams& p, uint32_t tmem_
         const bool xok = L < p.Wt && x < p.OW;
         const uint32_t tcol = tq + (uint32_t)(buf * bufcols + (p.HR - 1) * NK);  // slot of row 0; row r at -r*NK
         float* ob = p.out.p + (long long)b * p.out.bstride;
-        for (int r = 0; r < p.R; r += POOL ? 2 : 1) {
+        for (int r = 0; r < (p.dbg & 2 ? 0 : p.R); r += POOL ? 2 : 1) {
             float v0[NH], v1[NH];
             tmem_ldn<NH>(tcol - r * NK, v0);
             if (POOL) tmem_ldn<NH>(tcol - (r + 1) * NK, v1);
@@ -407,7 +409,7 @@ __device__ __forceinline__ void ct_epilogue(const ConvTParams& p, uint32_t tmem_
                 }
             }
         }
-        zero_rows(buf);
+        if (!(p.dbg & 2)) zero_rows(buf);
         tc_fence_before();
         if (q == 0 && hsel == 0 && lane == 0) CT_TRACE(it, 6);
         mbar_arrive(&tempty[buf]);
@@ -491,12 +493,6 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
             *reinterpret_cast<float*>(wsm + p.w_bytes + off) = split_lo1(v);
         }
     }
-    for (int ks = threadIdx.x; ks < p.ksteps; ks += blockDim.x) {  // descriptors, built once
-        uint32_t lbo;
-        const uint32_t ao = ct_aoff(p, ks, lbo);
-        dtab[2 * ks] = desc_none(smem_u32(smem) + ao, lbo);
-        dtab[2 * ks + 1] = desc_none(smem_u32(wsm) + (uint32_t)(ks * (2 * p.kh * NK * 16)), p.kh * NK * 16);
-    }
     fence_proxy_async_smem();
     tc_fence_before();
     __syncthreads();
@@ -512,8 +508,12 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
                 if (lane == 0) CT_TRACE(it, 0);
                 int b, y0, x0;
                 ct_tile(p, t, b, y0, x0);
-                halo_load_warp(p.x, p.x_bstride, p.G, p.Hin, p.Win, b, y0 - p.pad, x0 - p.pad, p.HR, p.P,
-                               smem + s * p.stage_bytes, &full[s], lane);
+                if (p.dbg & 4) {
+                    if (lane == 0) mbar_arrive(&full[s]);
+                } else {
+                    halo_load_warp(p.x, p.x_bstride, p.G, p.Hin, p.Win, b, y0 - p.pad, x0 - p.pad, p.HR, p.P,
+                                   smem + s * p.stage_bytes, &full[s], lane);
+                }
             }
         } else if (MODE == CT_DGRAD && lane == 0 && p.z.tma) {  // ---------------- dP / P / codes staging
             int it = 0;
@@ -533,6 +533,9 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
         const uint32_t idesc = umma_idesc_tf32(128, p.kh * NK, 0, 0);
         const uint64_t a_lo_add = (uint64_t)(p.h_bytes >> 4), b_lo_add = (uint64_t)(p.w_bytes >> 4);
         const uint64_t row_add = (uint64_t)((p.G * p.P * 16) >> 4);
+        const uint64_t a_base = desc_none(smem_u32(smem), p.G >= 2 ? (uint32_t)p.P * 16 : 16u);
+        const uint64_t b_base = desc_none(smem_u32(wsm), (uint32_t)(p.kh * NK * 16));
+        const uint64_t b_step = (uint64_t)((2 * p.kh * NK * 16) >> 4);
         int it = 0;
         for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
             const int s = it % S, buf = it & 1;
@@ -540,17 +543,35 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
             mbar_wait(MODE == CT_FWD ? &ready[s] : &full[s], (it / S) & 1);
             tc_fence_after();
             if (lane == 0) CT_TRACE(it, 3);
-            uint64_t a_add = (uint64_t)((s * p.stage_bytes) >> 4);
-            for (int h = 0; h < p.HR; ++h, a_add += row_add) {
+            // descriptors by running adds on the start-address field (no per-MMA memory loads):
+            // K step (dj, quad pair gp) starts at (2*gp*P + dj) * 16 bytes into the halo row, or at
+            // 2*s*16 for a single quad (tap pairs); its weights at s * kh*NK*32 bytes
+            uint64_t a_row = a_base + (uint64_t)((s * p.stage_bytes) >> 4);
+            for (int h = 0; h < p.HR; ++h, a_row += row_add) {
                 // halo row h feeds output rows h - di (di = 0..kh-1) = row slots HR-1-h .. HR-1-h+kh-1
                 const uint32_t tacc = tmem_base + (uint32_t)(buf * bufcols + (p.HR - 1 - h) * NK);
-                for (int ks = 0; ks < p.ksteps; ++ks) {
-                    const uint64_t dah = dtab[2 * ks] + a_add, dbh = dtab[2 * ks + 1];
-                    if (X3) {
-                        mma_tf32_elect(tacc, dah + a_lo_add, dbh, idesc);
-                        mma_tf32_elect(tacc, dah, dbh + b_lo_add, idesc);
+                uint64_t dbh = b_base;
+                if (p.G >= 2) {
+                    const int GP = (p.G + 1) >> 1;
+                    for (int dj = 0; dj < p.kw; ++dj) {
+                        uint64_t dah = a_row + (uint64_t)dj;
+                        for (int gp = 0; gp < GP; ++gp, dah += (uint64_t)(2 * p.P), dbh += b_step) {
+                            if (X3) {
+                                mma_tf32_elect(tacc, dah + a_lo_add, dbh, idesc);
+                                mma_tf32_elect(tacc, dah, dbh + b_lo_add, idesc);
+                            }
+                            mma_tf32_elect(tacc, dah, dbh, idesc);
+                        }
                     }
-                    mma_tf32_elect(tacc, dah, dbh, idesc);
+                } else {
+                    uint64_t dah = a_row;
+                    for (int ks = 0; ks < p.ksteps; ++ks, dah += 2, dbh += b_step) {
+                        if (X3) {
+                            mma_tf32_elect(tacc, dah + a_lo_add, dbh, idesc);
+                            mma_tf32_elect(tacc, dah, dbh + b_lo_add, idesc);
+                        }
+                        mma_tf32_elect(tacc, dah, dbh, idesc);
+                    }
                 }
             }
             if (lane == 0) CT_TRACE(it, 4);
@@ -570,7 +591,7 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
             if (MODE == CT_FWD) {  // ---------------- lo = x - tf32(x) of the landed halo (the raw halo is hi)
                 mbar_wait_sleep(&full[s], (it / S) & 1);
                 if (pt == 0) CT_TRACE(it, 1);
-                if (X3) {
+                if (X3 && !(p.dbg & 1)) {
                     const float4* src = reinterpret_cast<const float4*>(hi);
                     for (int i = pt; i < chunks; i += NP) {
                         const float4 a = src[i];
@@ -971,6 +992,7 @@ inline ConvTLaunch plan_convt(int mode, int B, int Cp, int Hin, int Win, int kh,
     p.tiles_y = (p.OH + p.R - 1) / p.R;
     p.ntiles = B * p.tiles_x * p.tiles_y;
     p.ksteps = p.G >= 2 ? kw * ((p.G + 1) / 2) : (kw + 1) / 2;
+    if (p.ksteps > kCtMaxKSteps) throw Error(B2N_ESHAPE, "b200nn conv: filter width x channel quads too large");
     p.halo_bytes = p.HR * p.G * p.P * 16;
     // MMA rows past the tile width read at most (kw + 128) * 16 bytes beyond the halo (ct_aoff)
     p.h_bytes = (p.halo_bytes + (kw + 129) * 16 + 127) & ~127;
@@ -992,6 +1014,7 @@ inline ConvTLaunch plan_convt(int mode, int B, int Cp, int Hin, int Win, int kh,
     L.grid = std::min(p.ntiles, sm_count());
     L.flops = 2.0 * B * p.OH * p.OW * N * (double)Cp * kh * kw;
     p.trace = TraceRegistry::get().next();
+    if (const char* e = std::getenv("B2N_CT_DBG")) p.dbg = std::atoi(e);
     return L;
 }
 

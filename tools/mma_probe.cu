@@ -23,7 +23,8 @@ __global__ void probe(Cfg c, unsigned long long* out) {
     __shared__ uint64_t bar;
     __shared__ uint32_t tslot;
     uint8_t* s = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm) + 1023) & ~uintptr_t(1023));
-    for (int i = threadIdx.x; i < 160 * 1024 / 4; i += blockDim.x) reinterpret_cast<float*>(s)[i] = 0.0f;
+    for (int i = threadIdx.x; i < 160 * 1024 / 4; i += blockDim.x)
+        reinterpret_cast<float*>(s)[i] = c.a_step < 0 ? 0.0f : 0.001f * (float)((i * 2654435761u) >> 20) - 1.0f;
     if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
     if (threadIdx.x < 32) tmem_alloc(&tslot, 256);
     fence_proxy_async_smem();
@@ -31,7 +32,31 @@ __global__ void probe(Cfg c, unsigned long long* out) {
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tslot;
-    if (c.nacc == 3 && threadIdx.x < 32) {  // warp-converged issue, elect.sync per MMA
+    if (c.nacc == 4 && threadIdx.x < 32) {  // conv-kernel pattern: descriptors from an smem table + row adds
+        __shared__ uint64_t tab[16];
+        const uint32_t a0 = smem_u32(s), b0 = a0 + 96 * 1024;
+        if (threadIdx.x < 8) {
+            tab[2 * threadIdx.x] = umma_desc(a0 + threadIdx.x * c.a_step, c.lbo, c.sbo, c.layout);
+            tab[2 * threadIdx.x + 1] = umma_desc(b0 + threadIdx.x * 1536, 48 * 16, 128, c.layout);
+        }
+        __syncwarp();
+        const uint32_t idesc = umma_idesc_tf32(128, c.N, 0, 0);
+        const unsigned long long t0 = clock64();
+        uint64_t add = 0;
+        for (int i = 0; i < c.iters; i += 24, add = (add + 130) & 1023) {
+            for (int h = 0; h < 4; ++h) {
+                for (int ks = 0; ks < 2; ++ks) {
+                    const uint64_t da = tab[2 * ks] + add + h * 8, db = tab[2 * ks + 1];
+                    mma_tf32_elect(tmem + (3 - h) * 16, da + 520, db, idesc);
+                    mma_tf32_elect(tmem + (3 - h) * 16, da, db + 96, idesc);
+                    mma_tf32_elect(tmem + (3 - h) * 16, da, db, idesc);
+                }
+            }
+        }
+        if (threadIdx.x == 0) mma_commit(&bar);
+        mbar_wait(&bar, 0);
+        if (threadIdx.x == 0) out[blockIdx.x] = clock64() - t0;
+    } else if (c.nacc == 3 && threadIdx.x < 32) {  // warp-converged issue, elect.sync per MMA
         const uint32_t a0 = smem_u32(s), b0 = a0 + 96 * 1024;
         const uint32_t idesc = umma_idesc_tf32(128, c.N, 0, 0);
         const uint64_t da = umma_desc(a0, c.lbo, c.sbo, c.layout), db = umma_desc(b0, c.lbo, c.sbo, c.layout);
@@ -46,7 +71,7 @@ __global__ void probe(Cfg c, unsigned long long* out) {
         if (threadIdx.x == 0) mma_commit(&bar);
         mbar_wait(&bar, 0);
         if (threadIdx.x == 0) out[blockIdx.x] = clock64() - t0;
-    } else if (c.nacc != 3 && threadIdx.x == 0) {
+    } else if (c.nacc < 3 && threadIdx.x == 0) {
         const uint32_t a0 = smem_u32(s), b0 = a0 + 96 * 1024;
         uint32_t idesc;
         if (c.kind == 0) idesc = umma_idesc_tf32(128, c.N, 0, 0);
@@ -92,20 +117,18 @@ int main() {
     // layout codes: 0 = none (interleave), 2 = SW128, 4 = SW64, 6 = SW32
     const char* lname[8] = {"NONE", "SW128B32", "SW128", "?", "SW64", "?", "SW32", "?"};
     struct { int layout, lbo, sbo, a_step; } L[] = {{0, 2080, 128, 16}, {0, 128, 256, 0}, {2, 16, 1024, 32}, {6, 16, 256, 32}, {4, 16, 512, 32}};
-    for (int kind = 0; kind < 1; ++kind)
-        for (int li : {2})
-            for (int N : {16, 32, 64, 128, 256})
-                for (int nacc : {1, 2, 3}) {
-                    if (N * nacc > 256) continue;
-                    auto& l = L[li];
-                    Cfg c{kind, N, l.layout, l.lbo, l.sbo, l.a_step, 2048, nacc};
-                    probe<<<148, 128, 200 * 1024>>>(c, d);
-                    unsigned long long h[148];
-                    cudaError_t e = cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
-                    if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
-                    double avg = 0; for (int i = 0; i < 148; ++i) avg += h[i]; avg /= 148;
-                    printf("kind=%s layout=%-8s N=%3d variant=%d : %6.1f clk/MMA  (floor %d)\n", kind ? "bf16" : "tf32",
-                           lname[l.layout], N, nacc, avg / c.iters, N / 2);
-                }
+    struct { int layout, lbo, sbo, a_step; } P2[] = {{0, 16, 128, 32}, {0, 2080, 128, 16}, {0, 128, 256, 16}};
+    for (auto& l : P2)
+        for (int N : {16, 48, 96})
+            for (int var : {3, 4}) {
+                Cfg c{0, N, l.layout, l.lbo, l.sbo, l.a_step, 24 * 96, var};
+                probe<<<148, 128, 200 * 1024>>>(c, d);
+                unsigned long long h[148];
+                cudaError_t e = cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+                if (e != cudaSuccess) { printf("error %s\n", cudaGetErrorString(e)); return 1; }
+                double avg = 0; for (int i = 0; i < 148; ++i) avg += h[i]; avg /= 148;
+                printf("tf32 NONE lbo=%5d sbo=%4d N=%3d variant=%d : %6.1f clk/MMA (floor %d)\n", l.lbo, l.sbo, N, var,
+                       avg / c.iters, N / 2);
+            }
     return 0;
 }
