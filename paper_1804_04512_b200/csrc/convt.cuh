@@ -677,19 +677,29 @@ struct ConvTWParams {
     DZSrc z;
     float* ws;  // per-CTA partials [cta][Kp*Cp*kh*kw + Kp]
     int ws_stride;
+    int chunk;  // output columns per sliding-window run (enough runs per tile for every stream)
 };
 
-constexpr int kWgThreads = 256;
 constexpr int kWgChunk = 16;  // output columns per sliding-window run
-
-// Thread (stream st, channel c, kernel quad kq) owns dW[4kq..4kq+3][c][.][.] over the pixel runs of its
-// stream. Per tile the X halo and the pooled dP / P / codes arrive by TMA into a double-buffered slot
-// (the next tile's loads fly while this one computes); dZ is expanded from the slot into smem.
+// thread count / kernels per thread of the weight-gradient kernel for a filter size
 template <int KH, int KW>
-__global__ void __launch_bounds__(kWgThreads, 1)
+struct WgCfg {
+    static constexpr int KG = KH * KW <= 9 ? 8 : 4;           // kernels per thread (register accumulators)
+    static constexpr int NT = KH * KW <= 9 ? 512 : 256;       // threads
+};
+
+// Thread (stream st, channel c, kernel group kg) owns dW[KG*kg .. KG*kg+KG)[c][.][.] over the pixel runs
+// of its stream: per output pixel KH loads of the X window (sliding along the row) + KG/4 float4 loads
+// of dZ feed KG*KH*KW FMAs. Per tile the X halo and the pooled dP / P / codes arrive by bulk copy / TMA
+// into a double-buffered slot (the next tile's loads fly while this one computes); dZ is expanded from
+// the slot into smem, and the bias gradient (sum of dZ) is accumulated there, per thread in a fixed
+// quad, reduced in fixed order at the end.
+template <int KH, int KW>
+__global__ void __launch_bounds__(WgCfg<KH, KW>::NT, 1)
     convt_wgrad_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapZdP,
                        const __grid_constant__ CUtensorMap mapZP, const __grid_constant__ CUtensorMap mapZc,
                        const ConvTWParams p) {
+    constexpr int KG = WgCfg<KH, KW>::KG, NT = WgCfg<KH, KW>::NT, T = KH * KW;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* slots[2] = {smem, smem + p.slot_bytes};  // [X halo | dZ staging]
@@ -698,26 +708,27 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     const int Kq = p.Kp >> 2;
     const int dz_floats = p.R * p.Kp * p.Wt;
     uint64_t* full = reinterpret_cast<uint64_t*>(dz + dz_floats);
-    float* red = reinterpret_cast<float*>(full + 4);  // CTA reduction scratch
+    float* red = reinterpret_cast<float*>(smem);  // CTA reduction scratch, reuses the slots after the tile loop
 
-    const int TPS = p.C * Kq;
-    const int streams = kWgThreads / TPS;
+    const int ngrp = (p.Kp + KG - 1) / KG;  // kernel groups
+    const int TPS = p.C * ngrp;
+    const int streams = NT / TPS;
     const int st = threadIdx.x / TPS, w = threadIdx.x - st * TPS;
-    const int c = w % p.C, kq = w / p.C;
+    const int c = w % p.C, kg = w / p.C;
     const bool active = st < streams;
-    constexpr int T = KH * KW;
-    float acc[4][T];
-    float bacc[4] = {0.f, 0.f, 0.f, 0.f};
+    float acc[KG][T];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < KG; ++j)
 #pragma unroll
         for (int i = 0; i < T; ++i) acc[j][i] = 0.0f;
+    // bias: thread t always expands quad bq = t % Kq (fixed assignment -> deterministic order)
+    const int bq = threadIdx.x % Kq;
+    float4 bsum = make_float4(0.f, 0.f, 0.f, 0.f);
 
     if (threadIdx.x == 0) {  // two arrivals per fill: the dZ staging arm and the halo arm
         mbar_init(&full[0], p.z.tma ? 2 : 1);
         mbar_init(&full[1], p.z.tma ? 2 : 1);
         fence_barrier_init();
-        tma_prefetch(&mapX);
     }
     __syncthreads();
     pdl_wait();
@@ -741,6 +752,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                        lane);
     };
     if (threadIdx.x < 32 && (int)blockIdx.x < p.ntiles) issue(blockIdx.x, 0);
+    const int npx = p.R * p.Wt;
     int it = 0;
     for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
         const int sl = it & 1;
@@ -750,80 +762,88 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         uint8_t* zslot = slots[sl] + hb;
         mbar_wait(&full[sl], (it >> 1) & 1);
         if (!p.z.tma) {
-            zs_load_sync(p.z, zslot, b, sy0, sx0, threadIdx.x, kWgThreads);
+            zs_load_sync(p.z, zslot, b, sy0, sx0, threadIdx.x, NT);
             __syncthreads();
         }
-        for (int i = threadIdx.x; i < p.R * Kq * p.Wt; i += kWgThreads) {  // dZ of the tile
-            const int r = i / (Kq * p.Wt), rem = i - r * (Kq * p.Wt), q = rem / p.Wt, xx = rem - q * p.Wt;
-            const int Y = y0 + r, X = x0 + xx;
-            reinterpret_cast<float4*>(dz)[i] = zs_dz(p.z, zslot, sy0, sx0, q, Y, X);
-        }
+        if (threadIdx.x < (NT / Kq) * Kq)
+            for (int pi = threadIdx.x / Kq; pi < npx; pi += NT / Kq) {  // dZ of the tile, quad bq
+                const int r = pi / p.Wt, xx = pi - r * p.Wt;
+                const int Y = y0 + r, X = x0 + xx;
+                float4 d = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (Y < p.OH && X < p.OW) d = zs_dz(p.z, zslot, sy0, sx0, bq, Y, X);
+                reinterpret_cast<float4*>(dz)[(r * Kq + bq) * p.Wt + xx] = d;
+                bsum.x += d.x;
+                bsum.y += d.y;
+                bsum.z += d.z;
+                bsum.w += d.w;
+            }
         __syncthreads();  // dz ready; the other slot (previous tile) is free
         if (threadIdx.x < 32 && t + (int)gridDim.x < p.ntiles) issue(t + gridDim.x, sl ^ 1);
         if (active) {
             const float* hx = reinterpret_cast<const float*>(slots[sl]);
             const int cq = c >> 2, cj = c & 3;
-            const int runs_per_row = (p.Wt + kWgChunk - 1) / kWgChunk;
+            const int runs_per_row = (p.Wt + p.chunk - 1) / p.chunk;
             for (int u = st; u < p.R * runs_per_row; u += streams) {
-                const int r = u / runs_per_row, xb = (u - r * runs_per_row) * kWgChunk;
-                const int xe = min(min(p.Wt, xb + kWgChunk), p.OW - x0);
+                const int r = u / runs_per_row, xb = (u - r * runs_per_row) * p.chunk;
+                const int xe = min(min(p.Wt, xb + p.chunk), p.OW - x0);
                 if (y0 + r >= p.OH || xb >= xe) continue;
                 float win[KH][KW];
+                const float* hrow = hx + (((r * p.G + cq) * p.P + xb) * 4 + cj);
+                const int rstride = p.G * p.P * 4;
 #pragma unroll
                 for (int di = 0; di < KH; ++di)
 #pragma unroll
-                    for (int dj = 0; dj < KW - 1; ++dj)
-                        win[di][dj + 1] = hx[(((r + di) * p.G + cq) * p.P + xb + dj) * 4 + cj];
+                    for (int dj = 0; dj < KW - 1; ++dj) win[di][dj + 1] = hrow[di * rstride + dj * 4];
+                const float4* dzr = reinterpret_cast<const float4*>(dz) + (r * Kq + kg * (KG / 4)) * p.Wt;
                 for (int xx = xb; xx < xe; ++xx) {
+                    const float* hcol = hrow + (xx - xb + KW - 1) * 4;
 #pragma unroll
                     for (int di = 0; di < KH; ++di) {
 #pragma unroll
                         for (int dj = 0; dj < KW - 1; ++dj) win[di][dj] = win[di][dj + 1];
-                        win[di][KW - 1] = hx[(((r + di) * p.G + cq) * p.P + xx + KW - 1) * 4 + cj];
+                        win[di][KW - 1] = hcol[di * rstride];
                     }
-                    const float4 d4 = reinterpret_cast<const float4*>(dz)[(r * Kq + kq) * p.Wt + xx];
-                    const float dd[4] = {d4.x, d4.y, d4.z, d4.w};
+                    float dd[KG];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
+                    for (int g = 0; g < KG / 4; ++g) {
+                        const float4 d4 = dzr[g * p.Wt + xx];
+                        dd[4 * g] = d4.x, dd[4 * g + 1] = d4.y, dd[4 * g + 2] = d4.z, dd[4 * g + 3] = d4.w;
+                    }
+#pragma unroll
+                    for (int j = 0; j < KG; ++j)
 #pragma unroll
                         for (int di = 0; di < KH; ++di)
 #pragma unroll
                             for (int dj = 0; dj < KW; ++dj)
                                 acc[j][di * KW + dj] = fmaf(dd[j], win[di][dj], acc[j][di * KW + dj]);
-                        bacc[j] += dd[j];
-                    }
                 }
             }
         }
         __syncthreads();  // slot and dz consumed
     }
     pdl_trigger();
-    // fixed-order reduction over the streams of this CTA, then one partial row per CTA
-    const int nval = 4 * T + 4;
+    // fixed-order reductions: streams of the CTA, bias over the threads of each quad; one row per CTA
+    const int nval = KG * T;
     if (active)
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < KG; ++j)
             for (int i = 0; i < T; ++i) red[((long long)st * TPS + w) * nval + j * T + i] = acc[j][i];
-            red[((long long)st * TPS + w) * nval + 4 * T + j] = bacc[j];
-        }
+    float* bred = red + (long long)streams * TPS * nval;  // [NT][4]
+    reinterpret_cast<float4*>(bred)[threadIdx.x] = bsum;
     __syncthreads();
     float* out = p.ws + (long long)blockIdx.x * p.ws_stride;
     const int nk = p.Kp * p.Cp * T;
-    for (int idx = threadIdx.x; idx < nk + p.Kp; idx += kWgThreads) {
-        int ww = -1, slotv = 0;
+    for (int idx = threadIdx.x; idx < nk + p.Kp; idx += NT) {
+        float sum = 0.0f;
         if (idx < nk) {  // idx = ((k * Cp + c) * T + tap)
             const int k = idx / (p.Cp * T), rem = idx - k * (p.Cp * T), cc = rem / T, tap = rem - cc * T;
-            if (cc < p.C) {
-                ww = (k >> 2) * p.C + cc;
-                slotv = (k & 3) * T + tap;
+            if (cc < p.C && k / KG < ngrp) {
+                const int ww = (k / KG) * p.C + cc, slotv = (k % KG) * T + tap;
+                for (int q = 0; q < streams; ++q) sum += red[((long long)q * TPS + ww) * nval + slotv];
             }
-        } else {  // bias of kernel k: the c == 0 threads' dZ sums
-            const int k = idx - nk;
-            ww = (k >> 2) * p.C;
-            slotv = 4 * T + (k & 3);
+        } else {  // bias of kernel k: threads with bq == k / 4, in thread order
+            const int k = idx - nk, q4 = k >> 2, j = k & 3;
+            for (int tt = q4; tt < (NT / Kq) * Kq; tt += Kq) sum += bred[tt * 4 + j];
         }
-        float sum = 0.0f;
-        if (ww >= 0)
-            for (int q = 0; q < streams; ++q) sum += red[((long long)q * TPS + ww) * nval + slotv];
         out[idx] = sum;
     }
 }
@@ -1084,31 +1104,44 @@ inline ConvTWLaunch plan_convt_wgrad(const ConvTLaunch& f, int K, int C, const D
     p.K = K;
     p.Kp = (K + 3) & ~3;
     p.C = C;
-    p.R = q.R;
     p.Wt = q.Wt;
     p.P = q.P;
-    p.HR = q.HR;
     p.tiles_x = q.tiles_x;
-    p.tiles_y = q.tiles_y;
-    p.ntiles = q.ntiles;
-    p.halo_bytes = q.halo_bytes;
     p.x = q.x;
     p.x_bstride = q.x_bstride;
     p.z = z0;
-    p.z.bh = z0.pool ? q.R / 2 : q.R;
     p.z.bw = ((z0.pool ? q.Wt / 2 : q.Wt) + 6) & ~3;  // window start is aligned down to 4 (TMA: 16 B)
     if (!((p.kh == 3 && p.kw == 3) || (p.kh == 5 && p.kw == 5)))
         throw Error(B2N_EINTERNAL, "convt wgrad: only 3x3 and 5x5 filters are instantiated");
     const int T = p.kh * p.kw;
-    const int TPS = C * (p.Kp / 4);
-    if (TPS > kWgThreads) throw Error(B2N_ESHAPE, "convt wgrad: channels x kernel quads exceed one CTA");
-    const int streams = kWgThreads / TPS;
+    const int KG = T <= 9 ? 8 : 4, NT = T <= 9 ? 512 : 256;  // WgCfg
+    const int TPS = C * ((p.Kp + KG - 1) / KG);
+    if (TPS > NT) throw Error(B2N_ESHAPE, "convt wgrad: channels x kernel groups exceed one CTA");
+    const int streams = NT / TPS;
+    // its own tile height: as many output rows as fit (compute per tile must hide the next tile's loads)
+    const int red_bytes = streams * TPS * KG * T * 4 + NT * 16;
+    auto smem_for = [&](int R) {
+        DZSrc zz = p.z;
+        zz.bh = z0.pool ? R / 2 : R;
+        const int halo = (R + p.kh - 1) * p.G * p.P * 16;
+        const int slot = (((halo + 127) & ~127) + zs_bytes(zz) + 1023) & ~1023;
+        return 1024 + std::max(2 * slot + R * p.Kp * p.Wt * 4 + 64, red_bytes);
+    };
+    const int ohe = (p.OH + 1) & ~1;
+    p.R = std::min(std::max(2, ohe), 16);
+    while (p.R > 2 && smem_for(p.R) > 200 * 1024) p.R -= 2;
+    p.HR = p.R + p.kh - 1;
+    p.tiles_y = (p.OH + p.R - 1) / p.R;
+    p.ntiles = p.B * p.tiles_x * p.tiles_y;
+    p.halo_bytes = p.HR * p.G * p.P * 16;
+    p.z.bh = z0.pool ? p.R / 2 : p.R;
+    p.chunk = std::max(2, std::min(kWgChunk, (p.R * p.Wt + streams - 1) / streams));
     p.ws_stride = (p.Kp * p.Cp * T + p.Kp + 3) & ~3;
     p.slot_bytes = (((p.halo_bytes + 127) & ~127) + zs_bytes(p.z) + 1023) & ~1023;
     L.map = f.map;
     dz_maps(p.z, p.B, L.zmaps);
     L.grid = std::min(p.ntiles, sm_count());
-    L.smem = 1024 + 2 * p.slot_bytes + p.R * p.Kp * p.Wt * 4 + 64 + streams * TPS * (4 * T + 4) * 4;
+    L.smem = smem_for(p.R);
     if (L.smem > 227 * 1024) throw Error(B2N_ESHAPE, "convt wgrad: tile does not fit shared memory");
     L.ws = std::make_shared<DevMem>();
     L.ws->alloc((size_t)L.grid * p.ws_stride * 4);

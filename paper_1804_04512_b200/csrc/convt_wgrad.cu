@@ -11,7 +11,7 @@ static void launch_wg(const ConvTWLaunch& L, cudaStream_t st) {
         return true;
     }();
     (void)attr;
-    launch_ex(k, dim3(L.grid), dim3(kWgThreads), (size_t)L.smem, st, 1u, L.map, L.zmaps[0], L.zmaps[1], L.zmaps[2],
+    launch_ex(k, dim3(L.grid), dim3(WgCfg<KH, KW>::NT), (size_t)L.smem, st, 1u, L.map, L.zmaps[0], L.zmaps[1], L.zmaps[2],
               L.p);
 }
 
