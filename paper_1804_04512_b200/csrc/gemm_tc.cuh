@@ -399,39 +399,37 @@ __global__ void __launch_bounds__(kThreads, 1)
                 load_b(i);
             }
         }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ---------------- MMA issuer
-            const uint32_t idesc = umma_idesc_tf32(kBM, BN, p.a_mn, p.b_mn);
-            for (int i = 0; i < num_kb; ++i) {
-                const int s = i % S;
-                const uint32_t ph = (i / S) & 1;
-                mbar_wait(X3 ? &ready[s] : &full[s], ph);
-                tc_fence_after();
-                if (i < 16) B2N_TRACE(34 + i);
-                const uint32_t a_hi = smem_u32(smem + s * Cfg::STAGE_BYTES);
-                const uint32_t b_hi = a_hi + Cfg::A_BYTES;
-                const uint32_t a_lo = b_hi + Cfg::B_BYTES;
-                const uint32_t b_lo = a_lo + Cfg::A_BYTES;
+    } else if (warp == 1) {  // ---------------- MMA issue: whole warp, one elected lane per MMA
+        // descriptors advance by running adds on the 14-bit start-address field: a K-major kk step is
+        // 32 B (SW128 rows), an MN-major one 1024 B (8 K-rows of 128 B); stages STAGE_BYTES apart
+        const uint32_t idesc = umma_idesc_tf32(kBM, BN, p.a_mn, p.b_mn);
+        const uint32_t a0 = smem_u32(smem), b0 = a0 + Cfg::A_BYTES;
+        const uint64_t da0 = p.a_mn ? desc_mnmajor(a0, 0) : desc_kmajor(a0, 0);
+        const uint64_t db0 = p.b_mn ? desc_mnmajor(b0, 0) : desc_kmajor(b0, 0);
+        const uint64_t a_kk = p.a_mn ? 64 : 2, b_kk = p.b_mn ? 64 : 2;
+        constexpr uint64_t lo_add = (uint64_t)((Cfg::A_BYTES + Cfg::B_BYTES) >> 4);
+        for (int i = 0; i < num_kb; ++i) {
+            const int s = i % S;
+            const uint32_t ph = (i / S) & 1;
+            mbar_wait(X3 ? &ready[s] : &full[s], ph);
+            tc_fence_after();
+            if (i < 16 && lane == 0) B2N_TRACE(34 + i);
+            const uint64_t st = (uint64_t)((s * Cfg::STAGE_BYTES) >> 4);
+            uint64_t dah = da0 + st, dbh = db0 + st;
 #pragma unroll
-                for (int kk = 0; kk < kBK / 8; ++kk) {
-                    const uint64_t dah = p.a_mn ? desc_mnmajor(a_hi, kk) : desc_kmajor(a_hi, kk);
-                    const uint64_t dbh = p.b_mn ? desc_mnmajor(b_hi, kk) : desc_kmajor(b_hi, kk);
-                    const uint32_t acc = (i | kk) != 0;
-                    if (X3) {
-                        const uint64_t dal = p.a_mn ? desc_mnmajor(a_lo, kk) : desc_kmajor(a_lo, kk);
-                        const uint64_t dbl = p.b_mn ? desc_mnmajor(b_lo, kk) : desc_kmajor(b_lo, kk);
-                        mma_tf32(tmem_base, dal, dbh, idesc, acc);
-                        mma_tf32(tmem_base, dah, dbl, idesc, 1);
-                        mma_tf32(tmem_base, dah, dbh, idesc, 1);
-                    } else {
-                        mma_tf32(tmem_base, dah, dbh, idesc, acc);
-                    }
+            for (int kk = 0; kk < kBK / 8; ++kk, dah += a_kk, dbh += b_kk) {
+                if (X3) {
+                    mma_tf32_warp(tmem_base, dah + lo_add, dbh, idesc, (i | kk) != 0);
+                    mma_tf32_warp(tmem_base, dah, dbh + lo_add, idesc, 1);
+                    mma_tf32_warp(tmem_base, dah, dbh, idesc, 1);
+                } else {
+                    mma_tf32_warp(tmem_base, dah, dbh, idesc, (i | kk) != 0);
                 }
-                mma_commit(&empty[s]);
             }
-            mma_commit(tmem_full);
-            B2N_TRACE(50);
+            mma_commit_warp(&empty[s]);
         }
+        mma_commit_warp(tmem_full);
+        if (lane == 0) B2N_TRACE(50);
     } else {  // ---------------- splitters, then TMEM -> smem tile (warps 2..9)
         const int ct = threadIdx.x - 64;
         epilogue_prefetch<BN, EPI>(p, m0, n0, ct);
