@@ -954,15 +954,19 @@ inline void dz_maps(const DZSrc& z, int B, CUtensorMap out[3]) {
 }
 
 // tile shape for an OH x OW correlation output: Wt <= 128 columns, R (even) rows, 2*R*NK TMEM columns <= 512
-inline void ct_tile_shape(int OH, int OW, int NK, int kh, int& R, int& Wt) {
+inline void ct_tile_shape(int B, int OH, int OW, int NK, int kh, int& R, int& Wt) {
     Wt = std::min(OW, 128);
     if (Wt & 1) ++Wt;
-    R = (128 + Wt - 1) / Wt;
+    // >= 512 output pixels per tile: halo rows are re-read (R + kh - 1) / R times
+    R = (512 + Wt - 1) / Wt;
     R = std::max(2, (R + 1) & ~1);
     const int ohe = (OH + 1) & ~1;
     R = std::min(R, std::max(2, ohe));
     // two TMEM buffers of (R + 2(kh-1)) row slots of NK columns
     while (2 * (R + 2 * (kh - 1)) * NK > 512 && R > 2) R -= 2;
+    // small maps: keep >= 2 tiles per SM so every SM has a pipeline to run
+    const long long tx = (OW + Wt - 1) / Wt;
+    while (R > 2 && (long long)B * tx * ((OH + R - 1) / R) < 2LL * sm_count()) R -= 2;
 }
 
 inline int ct_nk(int n) {
@@ -1004,7 +1008,22 @@ inline ConvTLaunch plan_convt(int mode, int B, int Cp, int Hin, int Win, int kh,
     p.N = N;
     if (kh * L.nk > 256) throw Error(B2N_ESHAPE, "b200nn conv: kh x kernels exceeds one MMA (N <= 256)");
     if (2 * (2 + 2 * (kh - 1)) * L.nk > 512) throw Error(B2N_ESHAPE, "b200nn conv: accumulators exceed TMEM");
-    ct_tile_shape(p.OH, p.OW, L.nk, kh, p.R, p.Wt);
+    ct_tile_shape(B, p.OH, p.OW, L.nk, kh, p.R, p.Wt);
+    for (;;) {  // the tallest tile whose 2 halo stages (hi + lo) fit next to the weights / staging
+        const int P_ = p.Wt + kw - 1, HR_ = p.R + kh - 1, G_ = Cp / 4;
+        const int hb = (HR_ * G_ * P_ * 16 + (kw + 129) * 16 + 127) & ~127;
+        const int ks = G_ >= 2 ? kw * ((G_ + 1) / 2) : (kw + 1) / 2;
+        int zb = 0;
+        if (z) {
+            DZSrc zz = *z;
+            zz.bh = z->pool ? HR_ / 2 + 1 : HR_;
+            zz.bw = ((z->pool ? P_ / 2 + 1 : P_) + 6) & ~3;
+            zb = (zs_bytes(zz) + 127) & ~127;
+        }
+        const int need = 2 * (2 * hb) + 2 * (ks * 2 * kh * L.nk * 16) + 1024 + 256 + ks * 16 + 128 + 2 * zb;
+        if (need <= 227 * 1024 || p.R <= 2) break;
+        p.R -= 2;
+    }
     p.P = p.Wt + kw - 1;
     p.HR = p.R + kh - 1;
     p.slots = p.HR + kh - 1;

@@ -31,7 +31,8 @@ METRICS = {
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1, "nsecond": 1e-3, "msecond": 1e3}
 
 RBM_STEP = ["rbm.hidden+sample", "rbm.visible+recon", "rbm.neg_hidden", "rbm.dW+update"]
-CIFAR_CONV = None  # labelled from the template's mode argument
+# launch order of the halo-tile conv kernels in one ImageNet-shape step (capture.sh)
+IMAGENET_CONV = [f"conv{i}.fwd" for i in range(5)] + [x for i in (4, 3, 2, 1) for x in (f"conv{i}.dgrad", f"conv{i}.wgrad")] + ["conv0.wgrad"]
 
 
 def raw_rows(rep: Path):
@@ -76,31 +77,29 @@ def main(tag: str):
              "(cold-cache, serialised): compare SHARES with bench.py's live CUDA-event timings, not absolutes.", ""]
     traffic = {}
     for rep, names, title in [(OUT / f"{tag}_rbm_full.ncu-rep", RBM_STEP, "RBM CD-1 step (headline), 4 GEMM launches"),
-                              (OUT / f"{tag}_cifar_conv_full.ncu-rep", CIFAR_CONV, "CIFAR CNN conv kernels")]:
+                              (OUT / f"{tag}_imagenet_conv_full.ncu-rep", IMAGENET_CONV,
+                               "ImageNet-shape CNN (batch 128): halo-tile conv kernels of one step")]:
         if not rep.exists():
             continue
         rows = raw_rows(rep)
         lines += [f"## {title}", "", "| op | kernel | us | DRAM rd+wr MB | DRAM % | tensor-pipe % | SM % | regs | grid |",
                   "|---|---|---|---|---|---|---|---|---|"]
         for i, d in enumerate(rows):
-            if names is None:
-                mode = d["kernel"].split("<")[1].split(",")[1].strip() if "<" in d["kernel"] else "?"
-                op = {"0": "conv.fwd+act+pool", "1": "conv.dgrad", "2": "conv.wgrad"}.get(mode, "?") + f" (grid {d.get('grid', 0):.0f})"
-            else:
-                op = names[i] if i < len(names) else "?"
+            op = names[i] if i < len(names) else "?"
             tb = (d.get("dram_read") or 0) + (d.get("dram_write") or 0)
             traffic.setdefault(op, tb)
             lines.append(f"| {op} | `{d['kernel'][:60]}` | {d.get('dur_us', 0):.2f} | {tb / 1e6:.3f} | "
                          f"{d.get('dram_pct', 0):.1f} | {d.get('tensor_pct', 0):.1f} | {d.get('sm_pct', 0):.1f} | "
                          f"{d.get('regs', 0):.0f} | {d.get('grid', 0):.0f} |")
         lines.append("")
-    for c in ["rbm", "mlp", "mnist_cnn", "cifar_cnn"]:
+    for c in ["rbm", "mlp", "mnist_cnn", "cifar_cnn", "imagenet_cnn"]:
         p = OUT / f"{tag}_launches_{c}.csv"
         if not p.exists():
             continue
         agg = launch_share(p)
         tot = sum(v[1] for v in agg.values())
-        lines += [f"## launch list: `bench.py --profile-only --config {c}`", "", "| kernel | launches | total us | share |",
+        lines += [f"## launch list: `bench.py --profile-only --config {c}` (warm-up + 1 step)", "",
+                  "| kernel | launches | total us | share |",
                   "|---|---|---|---|"]
         for k, (n, t) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
             lines.append(f"| `{k[:70]}` | {n} | {t:.1f} | {t / tot:.1%} |")
@@ -109,11 +108,13 @@ def main(tag: str):
     if lib.exists():
         sass = subprocess.run(["cuobjdump", "-sass", str(lib)], capture_output=True, text=True).stdout
         import re
-        counts = {m: len(re.findall(r"\b" + m + r"\b", sass)) for m in ["UTCHMMA", "UTMALDG", "LDTM", "UTCBAR", "HMMA"]}
+        counts = {m: len(re.findall(r"\b" + m + r"\b", sass)) for m in ["UTCHMMA", "UTMALDG", "UBLKCP", "LDTM", "STTM", "UTCBAR", "HMMA"]}
         lines += ["## SASS evidence (cuobjdump -sass libb200nn.so)", "",
                   "| mnemonic | count | meaning |", "|---|---|---|",
                   f"| UTCHMMA | {counts['UTCHMMA']} | tcgen05.mma (kind::tf32) |",
                   f"| UTMALDG | {counts['UTMALDG']} | TMA tensor loads |",
+                  f"| UBLKCP | {counts['UBLKCP']} | cp.async.bulk (conv halo rows) |",
+                  f"| STTM | {counts['STTM']} | tcgen05.st (conv accumulator re-zeroing) |",
                   f"| LDTM | {counts['LDTM']} | tcgen05.ld (TMEM -> registers) |",
                   f"| UTCBAR | {counts['UTCBAR']} | tcgen05.commit -> mbarrier |",
                   f"| HMMA | {counts['HMMA']} | legacy mma.sync (none expected) |", ""]
