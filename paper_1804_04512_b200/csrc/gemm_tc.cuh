@@ -147,110 +147,142 @@ __device__ __forceinline__ bool vec_ok(const void* base, long long ld, int n, in
     return n + 3 < N && (ld & 3) == 0 && ((reinterpret_cast<uintptr_t>(base) & 15) == 0);
 }
 
+// Epilogue inputs of 4 columns [n, n+4) of row m that do not depend on the product.
+struct EpiIn {
+    float4 a, b;  // aux / C / V rows
+    double u[4];  // RBM sampling uniforms
+};
+constexpr int kEpiPrefetch = 4;  // iterations whose inputs are loaded before the split-K exchange
+
+__device__ __forceinline__ float4 ld4(const float* base, long long ld, int m, int n, int N) {
+    const long long o = (long long)m * ld + n;
+    if (vec_ok(base, ld, n, N)) return *reinterpret_cast<const float4*>(base + o);
+    float t[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int i = 0; i < 4 && n + i < N; ++i) t[i] = base[o + i];
+    return make_float4(t[0], t[1], t[2], t[3]);
+}
+
+// bias of the thread's 4 columns (constant over its tile rows)
+template <int EPI>
+__device__ __forceinline__ void epi_bias(const GemmParams& p, int n, float (&b)[4]) {
+    const EpiParams& e = p.ep;
+    if (EPI == EPI_BIAS_ACT || EPI == EPI_RBM_HID || EPI == EPI_RBM_VIS || EPI == EPI_RBM_NEGHID)
+        for (int i = 0; i < 4; ++i) b[i] = n + i < p.N ? e.bias[(long long)(n + i) * e.bias_stride] : 0.0f;
+}
+
+template <int EPI>
+__device__ __forceinline__ void epi_load(const GemmParams& p, int m, int n, EpiIn& in) {
+    const EpiParams& e = p.ep;
+    switch (EPI) {
+        case EPI_DACT: in.a = ld4(e.aux, e.ld_aux, m, n, p.N); break;
+        case EPI_SGD: in.a = ld4(e.C, e.ldc, m, n, p.N); in.b = ld4(e.V, e.ldv, m, n, p.N); break;
+        case EPI_AXPY: in.a = ld4(e.C, e.ldc, m, n, p.N); break;
+        case EPI_RBM_VIS: in.a = ld4(e.aux, e.ld_aux, m, n, p.N); break;
+        case EPI_RBM_HID:
+            for (int i = 0; i < 4; ++i) in.u[i] = n + i < p.N ? e.u[(long long)m * e.ldu + n + i] : 2.0;
+            break;
+        default: break;
+    }
+}
+
 // elementwise epilogue on 4 columns [n, n+4) of row m (values v); returns the row partial for RBM_VIS
 template <int EPI>
-__device__ __forceinline__ double epi4(const GemmParams& p, int m, int n, const float (&v)[4]) {
+__device__ __forceinline__ double epi_apply(const GemmParams& p, int m, int n, const float (&v)[4],
+                                            const float (&bias)[4], const EpiIn& in) {
     const EpiParams& e = p.ep;
     const int cnt = p.N - n < 4 ? p.N - n : 4;
     const long long row = (long long)m * e.ldc;
     double part = 0.0;
+    auto st4 = [&](float* base, long long ld, const float (&o)[4]) {
+        if (vec_ok(base, ld, n, p.N))
+            *reinterpret_cast<float4*>(base + (long long)m * ld + n) = make_float4(o[0], o[1], o[2], o[3]);
+        else
+            for (int i = 0; i < cnt; ++i) base[(long long)m * ld + n + i] = o[i];
+    };
+    const float a[4] = {in.a.x, in.a.y, in.a.z, in.a.w}, b[4] = {in.b.x, in.b.y, in.b.z, in.b.w};
     switch (EPI) {
         case EPI_STORE: {
-            if (vec_ok(e.C, e.ldc, n, p.N)) {
-                *reinterpret_cast<float4*>(e.C + row + n) =
-                    make_float4(e.alpha * v[0], e.alpha * v[1], e.alpha * v[2], e.alpha * v[3]);
-            } else {
-                for (int i = 0; i < cnt; ++i) e.C[row + n + i] = e.alpha * v[i];
-            }
+            const float o[4] = {e.alpha * v[0], e.alpha * v[1], e.alpha * v[2], e.alpha * v[3]};
+            st4(e.C, e.ldc, o);
             break;
         }
-        case EPI_BIAS_ACT: {
-            float o[4] = {0, 0, 0, 0};
-            for (int i = 0; i < cnt; ++i) o[i] = apply_act(e.act, v[i] + e.bias[(long long)(n + i) * e.bias_stride]);
-            if (vec_ok(e.C, e.ldc, n, p.N))
-                *reinterpret_cast<float4*>(e.C + row + n) = make_float4(o[0], o[1], o[2], o[3]);
-            else
-                for (int i = 0; i < cnt; ++i) e.C[row + n + i] = o[i];
+        case EPI_BIAS_ACT: {  // dense_forward + activation_apply
+            float o[4];
+            for (int i = 0; i < 4; ++i) o[i] = apply_act(e.act, v[i] + bias[i]);
+            st4(e.C, e.ldc, o);
             break;
         }
-        case EPI_DACT: {
-            float y[4] = {0, 0, 0, 0}, o[4] = {0, 0, 0, 0};
-            const long long ar = (long long)m * e.ld_aux + n;
-            if (vec_ok(e.aux, e.ld_aux, n, p.N)) {
-                const float4 t = *reinterpret_cast<const float4*>(e.aux + ar);
-                y[0] = t.x, y[1] = t.y, y[2] = t.z, y[3] = t.w;
-            } else {
-                for (int i = 0; i < cnt; ++i) y[i] = e.aux[ar + i];
-            }
-            for (int i = 0; i < cnt; ++i)  // layers.hpp:294 order: dy * y * (1 - y)
-                o[i] = e.act == ACT_SIGMOID ? v[i] * y[i] * (1.0f - y[i]) : (y[i] > 0.0f ? v[i] : 0.0f);
-            if (vec_ok(e.C, e.ldc, n, p.N))
-                *reinterpret_cast<float4*>(e.C + row + n) = make_float4(o[0], o[1], o[2], o[3]);
-            else
-                for (int i = 0; i < cnt; ++i) e.C[row + n + i] = o[i];
+        case EPI_DACT: {  // layers.hpp:294 order: dy * y * (1 - y)
+            float o[4];
+            for (int i = 0; i < 4; ++i)
+                o[i] = e.act == ACT_SIGMOID ? v[i] * a[i] * (1.0f - a[i]) : (a[i] > 0.0f ? v[i] : 0.0f);
+            st4(e.C, e.ldc, o);
             break;
         }
         case EPI_SGD: {  // optim.hpp:75-78 on (w | b) tiles
-            float pp[4] = {0, 0, 0, 0}, vv[4] = {0, 0, 0, 0};
-            const long long vr = (long long)m * e.ldv + n;
-            const bool vec = vec_ok(e.C, e.ldc, n, p.N) && vec_ok(e.V, e.ldv, n, p.N);
-            if (vec) {
-                const float4 a = *reinterpret_cast<const float4*>(e.C + row + n);
-                const float4 b = *reinterpret_cast<const float4*>(e.V + vr);
-                pp[0] = a.x, pp[1] = a.y, pp[2] = a.z, pp[3] = a.w;
-                vv[0] = b.x, vv[1] = b.y, vv[2] = b.z, vv[3] = b.w;
-            } else {
-                for (int i = 0; i < cnt; ++i) pp[i] = e.C[row + n + i], vv[i] = e.V[vr + i];
+            float pp[4], vv[4];
+            for (int i = 0; i < 4; ++i) {
+                const float g = v[i] + e.wd * a[i];
+                vv[i] = e.mom * b[i] - e.lr * g;
+                pp[i] = a[i] + vv[i];
             }
-            for (int i = 0; i < cnt; ++i) {
-                const float g = v[i] + e.wd * pp[i];
-                vv[i] = e.mom * vv[i] - e.lr * g;
-                pp[i] = pp[i] + vv[i];
-            }
-            if (vec) {
-                *reinterpret_cast<float4*>(e.C + row + n) = make_float4(pp[0], pp[1], pp[2], pp[3]);
-                *reinterpret_cast<float4*>(e.V + vr) = make_float4(vv[0], vv[1], vv[2], vv[3]);
-            } else {
-                for (int i = 0; i < cnt; ++i) e.C[row + n + i] = pp[i], e.V[vr + i] = vv[i];
-            }
+            st4(e.C, e.ldc, pp);
+            st4(e.V, e.ldv, vv);
             break;
         }
         case EPI_RBM_HID: {  // energy.hpp:101-110 + unit_sample_inplace :59-61
-            for (int i = 0; i < cnt; ++i) {
-                const float pr = sigmoid_ref(v[i] + e.bias[(long long)(n + i) * e.bias_stride]);
-                e.C[row + n + i] = pr;
-                e.C2[(long long)m * e.ldc2 + n + i] = (e.u[(long long)m * e.ldu + n + i] < (double)pr) ? 1.0f : 0.0f;
+            float pr[4], hs[4];
+            for (int i = 0; i < 4; ++i) {
+                pr[i] = sigmoid_ref(v[i] + bias[i]);
+                hs[i] = (in.u[i] < (double)pr[i]) ? 1.0f : 0.0f;
             }
+            st4(e.C, e.ldc, pr);
+            st4(e.C2, e.ldc2, hs);
             break;
         }
         case EPI_RBM_VIS: {
+            float pr[4];
+            for (int i = 0; i < 4; ++i) pr[i] = sigmoid_ref(v[i] + bias[i]);
             for (int i = 0; i < cnt; ++i) {
-                const float pr = sigmoid_ref(v[i] + e.bias[(long long)(n + i) * e.bias_stride]);
-                e.C[row + n + i] = pr;
-                const double d = (double)e.aux[(long long)m * e.ld_aux + n + i] - (double)pr;
+                const double d = (double)a[i] - (double)pr[i];
                 part += d * d;
             }
+            st4(e.C, e.ldc, pr);
             break;
         }
-        case EPI_RBM_NEGHID:
-            for (int i = 0; i < cnt; ++i) e.C[row + n + i] = -sigmoid_ref(v[i] + e.bias[(long long)(n + i) * e.bias_stride]);
+        case EPI_RBM_NEGHID: {
+            float o[4];
+            for (int i = 0; i < 4; ++i) o[i] = -sigmoid_ref(v[i] + bias[i]);
+            st4(e.C, e.ldc, o);
             break;
+        }
         case EPI_AXPY: {
-            if (vec_ok(e.C, e.ldc, n, p.N)) {
-                float4 a = *reinterpret_cast<const float4*>(e.C + row + n);
-                a.x += e.alpha * v[0];
-                a.y += e.alpha * v[1];
-                a.z += e.alpha * v[2];
-                a.w += e.alpha * v[3];
-                *reinterpret_cast<float4*>(e.C + row + n) = a;
-            } else {
-                for (int i = 0; i < cnt; ++i) e.C[row + n + i] = e.C[row + n + i] + e.alpha * v[i];
-            }
+            float o[4];
+            for (int i = 0; i < 4; ++i) o[i] = a[i] + e.alpha * v[i];
+            st4(e.C, e.ldc, o);
             break;
         }
         default: break;
     }
+    (void)row;
     return part;
+}
+
+// smem tile row store of a reduced float4
+__device__ __forceinline__ void red_buf_store(float* tile, int r, int c, int TP, const float4& v) {
+    *reinterpret_cast<float4*>(tile + r * TP + c) = v;
+}
+// distributed shared memory: address of the same smem offset in cluster CTA `rank`, and a 16 B load
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+__device__ __forceinline__ float4 ld_dsmem4(uint32_t addr) {
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr)
+                 : "memory");
+    return v;
 }
 
 // softmax (layers.hpp:301-320) + softmax_cross_entropy (network.hpp:410-437) of one full row held
@@ -480,39 +512,55 @@ __global__ void __launch_bounds__(kThreads, 1)
     pdl_wait();  // global writes (and epilogue reads) only after the preceding kernel completed
     if (threadIdx.x == 0) B2N_TRACE(53);
 
-    // ---------------- split-K reduction across the cluster (fixed split order: deterministic)
+    // rows of the tile this CTA finishes: all of them, or (split-K) one slice per cluster rank
     int r_lo = 0, r_hi = kBM;
+    const int rank = p.splits > 1 ? (int)cluster_rank() : 0;
     if (p.splits > 1) {
-        const long long tile_id = (long long)blockIdx.y * gridDim.x + blockIdx.x;
-        float* ws = p.ws + tile_id * p.splits * (long long)(kBM * BN);
-        float* mine = ws + (long long)split * kBM * BN;
-        for (int idx = threadIdx.x; idx < kBM * BN / 4; idx += kThreads) {
-            const int r = idx / (BN / 4), c = (idx % (BN / 4)) * 4;
-            if (m0 + r < p.M)
-                *reinterpret_cast<float4*>(mine + r * BN + c) = *reinterpret_cast<const float4*>(tile + r * TP + c);
-        }
-        if (threadIdx.x == 0) B2N_TRACE(54);
-        cluster_sync_all();  // release our partial / acquire everyone's
-        if (threadIdx.x == 0) B2N_TRACE(55);
-        const int rank = (int)cluster_rank();
         const int rows = (kBM + p.splits - 1) / p.splits;
         r_lo = min(kBM, rank * rows);
         r_hi = min(kBM, r_lo + rows);
+    }
+    // epilogue inputs that do not depend on the product (bias, u, aux, C, V) are loaded now, so their
+    // latency overlaps the split-K exchange instead of following it
+    constexpr int G = BN / 4;  // threads per tile row (kThreads % G == 0: a thread keeps its columns)
+    const int total = (r_hi - r_lo) * G;
+    const int iters = (total + kThreads - 1) / kThreads;
+    const int ccol = (threadIdx.x % G) * 4;
+    float bias4[4] = {0.f, 0.f, 0.f, 0.f};
+    EpiIn pre[kEpiPrefetch];
+    if constexpr (EPI != EPI_SOFTMAX_XENT) {
+        epi_bias<EPI>(p, n0 + ccol, bias4);
+#pragma unroll
+        for (int it = 0; it < kEpiPrefetch; ++it) {
+            const int idx = it * kThreads + threadIdx.x;
+            const int m = m0 + r_lo + idx / G, n = n0 + ccol;
+            if (it < iters && idx < total && m < p.M && n < p.N) epi_load<EPI>(p, m, n, pre[it]);
+        }
+    }
+
+    // ---------------- split-K reduction across the cluster through distributed shared memory: every
+    // CTA's partial tile stays in its own smem; rank z sums its row slice over the peers in fixed split
+    // order (deterministic), then a second cluster barrier keeps the peers' smem alive until all read
+    if (p.splits > 1) {
+        if (threadIdx.x == 0) B2N_TRACE(54);
+        cluster_sync_all();  // release our partial / acquire everyone's
+        if (threadIdx.x == 0) B2N_TRACE(55);
+        const uint32_t tl = smem_u32(tile);
         for (int idx = threadIdx.x; idx < (r_hi - r_lo) * (BN / 4); idx += kThreads) {
             const int r = r_lo + idx / (BN / 4), c = (idx % (BN / 4)) * 4;
-            if (m0 + r >= p.M) continue;
-            float4 acc = *reinterpret_cast<const float4*>(ws + r * BN + c);
+            const uint32_t off = (uint32_t)((r * TP + c) * 4);
+            float4 acc = ld_dsmem4(mapa_u32(tl + off, 0));
             for (int z = 1; z < p.splits; ++z) {
-                const float4 t = *reinterpret_cast<const float4*>(ws + (long long)z * kBM * BN + r * BN + c);
+                const float4 t = ld_dsmem4(mapa_u32(tl + off, (uint32_t)z));
                 acc.x += t.x;
                 acc.y += t.y;
                 acc.z += t.z;
                 acc.w += t.w;
             }
-            *reinterpret_cast<float4*>(tile + r * TP + c) = acc;
+            red_buf_store(tile, r, c, TP, acc);
         }
         if (threadIdx.x == 0) B2N_TRACE(58);
-        __syncthreads();
+        cluster_sync_all();  // every peer has read our partial: slices may now be overwritten
         if (threadIdx.x == 0) B2N_TRACE(56);
     }
 
@@ -522,18 +570,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int r = r_lo + threadIdx.x; r < r_hi; r += kThreads)
             if (m0 + r < p.M) softmax_row(p, tile + r * TP, m0 + r);
     } else {
-        constexpr int G = BN / 4;  // threads per row
-        const int total = (r_hi - r_lo) * G;
-        const int iters = (total + kThreads - 1) / kThreads;
-        for (int it = 0; it < iters; ++it) {
+        auto body = [&](int it, const EpiIn& in) {
             const int idx = it * kThreads + threadIdx.x;
-            const int r = r_lo + idx / G, c = (idx % G) * 4;
+            const int r = r_lo + idx / G, c = ccol;
             const int m = m0 + r, n = n0 + c;
             double part = 0.0;
             if (idx < total && m < p.M && n < p.N) {
                 const float4 t = *reinterpret_cast<const float4*>(tile + r * TP + c);
                 const float v[4] = {t.x, t.y, t.z, t.w};
-                part = epi4<EPI>(p, m, n, v);
+                part = epi_apply<EPI>(p, m, n, v, bias4, in);
             }
             if constexpr (G <= 32 && EPI == EPI_RBM_VIS) {  // row partial over this CTA's BN columns
 #pragma unroll
@@ -541,6 +586,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (idx < total && (idx % G) == 0 && m < p.M)
                     p.ep.row_part[(long long)blockIdx.x * p.ep.ld_part + m] = part;
             }
+        };
+#pragma unroll
+        for (int it = 0; it < kEpiPrefetch; ++it)
+            if (it < iters) body(it, pre[it]);
+        for (int it = kEpiPrefetch; it < iters; ++it) {
+            EpiIn in;
+            const int idx = it * kThreads + threadIdx.x;
+            const int m = m0 + r_lo + idx / G, n = n0 + ccol;
+            if (idx < total && m < p.M && n < p.N) epi_load<EPI>(p, m, n, in);
+            body(it, in);
         }
     }
 
