@@ -295,6 +295,9 @@ int b2n_debug_gemm_trace(const float* A, long long lda, int ta, const float* B, 
 }
 
 // bring-up: copy the B2N_TRACE=1 registry (regions x 512 CTAs x 64 u64 stamps); returns regions used
+int b2n_debug_rbm_trace(b2n_rbm* r, unsigned long long* host) {
+    return guard([&] { r->impl.read_trace(host); });
+}
 int b2n_debug_trace_read(unsigned long long* host, long long max_u64, int* regions) {
     return guard([&] {
         auto& r = b2n::TraceRegistry::get();

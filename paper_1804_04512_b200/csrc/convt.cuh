@@ -451,8 +451,9 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int S = p.stages;
     const int bufcols = p.slots * NK;
-    uint32_t tcols = 32;
-    while (tcols < (uint32_t)(2 * bufcols)) tcols <<= 1;
+    // one CTA per SM (shared memory): it takes all of TMEM, whose base is then column 0 -- a compile-time
+    // constant, so the MMA warp's accumulator addresses stay in uniform registers
+    constexpr uint32_t tcols = 512;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
@@ -497,7 +498,8 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem_base = *tslot;
+    if (*tslot != 0u) __trap();  // the MMA issue below assumes TMEM base column 0
+    constexpr uint32_t tmem_base = 0u;
 
     if (warp == 0) {
         if (MODE == CT_FWD) {  // ---------------- halo producer (bulk copies + edge zeros)

@@ -11,10 +11,12 @@
 //   [0:H, 0:V] = pos - neg,  [0:H, V] = sum(h0 - h1),  [H, 0:V] = sum(v0 - v1)
 // i.e. the reference's weight update and both bias updates (energy.hpp:148-169) in one pass.
 #pragma once
+#include <cstdio>
 #include <random>
 
 #include "nccl_dyn.cuh"
 #include "network.cuh"
+#include "rbm_fused.cuh"
 
 namespace b2n {
 
@@ -173,7 +175,99 @@ class Rbm {
         return *plans_.back();
     }
 
+    // the fused single-kernel CD-1 step (rbm_fused.cuh) covers k = 1, 3xTF32, single GPU, B <= 128,
+    // H < 512, V < 1024, when all its clusters can be co-resident (grid barrier); B2N_RBM_FUSED=0 opts out
+    bool fused_ok(const Plan& pl) const {
+        const char* e = std::getenv("B2N_RBM_FUSED");
+        if (e && e[0] == '0') return false;
+        const int jt = (int)((H_ + 1 + kRfTileH - 1) / kRfTileH);
+        if (pl.k != 1 || dp_ || !x3_ || pl.B > 128 || pl.B > 16LL * jt || jt > 8 || V_ + 1 > kRfSlices * kRfSliceW)
+            return false;
+        static int clusters = [] {
+            B2N_CUDA(cudaFuncSetAttribute(rbm_cd1_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRfSmem));
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(kRfSlices, 8);
+            cfg.blockDim = dim3(kRfThreads);
+            cfg.dynamicSmemBytes = kRfSmem;
+            cudaLaunchAttribute at;
+            at.id = cudaLaunchAttributeClusterDimension;
+            at.val.clusterDim.x = kRfSlices;
+            at.val.clusterDim.y = 1;
+            at.val.clusterDim.z = 1;
+            cfg.attrs = &at;
+            cfg.numAttrs = 1;
+            int n = 0;
+            if (cudaOccupancyMaxActiveClusters(&n, rbm_cd1_fused_kernel, &cfg) != cudaSuccess) {
+                cudaGetLastError();
+                cfg.numAttrs = 0;  // compile-time cluster dims only
+                if (cudaOccupancyMaxActiveClusters(&n, rbm_cd1_fused_kernel, &cfg) != cudaSuccess) n = 0;
+            }
+            cudaGetLastError();
+            return n;
+        }();
+        if (std::getenv("B2N_RBM_FUSED_VERBOSE"))
+            std::fprintf(stderr, "b2n: fused CD-1 needs %d co-resident clusters of %d, device reports %d\n", jt, kRfSlices,
+                         clusters);
+        return clusters >= jt;
+    }
+
+    void build_fused(Plan& pl) {
+        const int B = (int)pl.B, H = (int)H_, V = (int)V_;
+        const int jt = (H + 1 + kRfTileH - 1) / kRfTileH;
+        float* W = W_.as<float>();
+        float* Vc = Vcat_.as<float>();
+        float* Hc = Hcat_.as<float>();
+        if (!fused_ws_.p) {
+            fused_ws_.alloc((size_t)8 * 128 * kRfSlices * kRfSliceW * 4 + (size_t)8 * kRfSlices * 128 * kRfTileH * 4);
+            gbar_.alloc(256);
+        }
+        RbmFusedParams rp;
+        std::memset(&rp, 0, sizeof(rp));
+        rp.B = B;
+        rp.H = H;
+        rp.V = V;
+        rp.ldw = ldw_;
+        rp.ldv = ldv_;
+        rp.ldh = ldh_;
+        rp.ldhs = ldhs_;
+        rp.W = W;
+        rp.Vcat = Vc;
+        rp.Hcat = Hc;
+        rp.HS = HS_.as<float>();
+        rp.u = U_.as<double>();
+        rp.row_part = recon_.as<double>();
+        rp.cap = cap_;
+        rp.ws2 = fused_ws_.as<float>();
+        rp.ws1 = rp.ws2 + (size_t)8 * 128 * kRfSlices * kRfSliceW;
+        rp.gbar = gbar_.as<unsigned>();
+        rp.alpha = pl.lr / static_cast<float>(pl.Bg);
+        rp.jt = jt;
+        if (std::getenv("B2N_RBM_TRACE")) {
+            if (!trace_.p) trace_.alloc(256 * 8);
+            rp.trace = trace_.as<unsigned long long>();
+        }
+        // TMA maps: K-major operands of phases 1-3, MN-major ones of phases 2 and 4 (see rbm_fused.cuh)
+        const CUtensorMap mVk = make_map_2d(Vc, V, 2 * B, ldv_, 32, 128);
+        const CUtensorMap mWk = make_map_2d(W, V, H, ldw_, 32, kRfTileH);
+        const CUtensorMap mHSk = make_map_2d(HS_.as<float>(), H, B, ldhs_, 32, 128);
+        const CUtensorMap mWmn = make_map_2d(W, V, H, ldw_, 32, 32, true);
+        const CUtensorMap mVmn = make_map_2d(Vc, V + 1, 2 * B, ldv_, 32, 32, true);
+        const CUtensorMap mHmn = make_map_2d(Hc, H + 1, 2 * B, ldh_, 32, 32, true);
+        const double flops = 2.0 * B * H * V * 4, bytes = 4.0 * ((double)H * V * 4 + (double)B * (V + H) * 6);
+        pl.ops.push_back(Op([=](cudaStream_t st) {
+            launch_ex(rbm_cd1_fused_kernel, dim3(kRfSlices, jt), dim3(kRfThreads), (size_t)kRfSmem, st, 1u, mVk, mWk,
+                      mHSk, mWmn, mVmn, mHmn, rp);
+        }, "rbm.cd1_fused", flops, bytes));
+        pl.recon_tiles = kRfSlices;
+        pl.nk = 1;
+        last_kernels_ = 1;
+    }
+
     void build(Plan& pl) {
+        if (fused_ok(pl)) {
+            build_fused(pl);
+            return;
+        }
         const int B = (int)pl.B;
         float* W = W_.as<float>();
         float* G = G_.as<float>();
@@ -286,6 +380,13 @@ class Rbm {
     long long cap_ = 0;
     int kcap_ = 0;
     DevMem W_, G_, Vcat_, Hcat_, HS_, U_, recon_;
+    DevMem fused_ws_, gbar_, trace_;
+  public:
+    void read_trace(unsigned long long* h) {
+        B2N_CUDA(cudaDeviceSynchronize());
+        if (trace_.p) B2N_CUDA(cudaMemcpy(h, trace_.p, 256 * 8, cudaMemcpyDeviceToHost));
+    }
+  private:  // fused CD-1 kernel: phase-2 partials, grid-barrier counters
     HostPinned h_recon_;
     long long staged_B_ = 0, last_B_ = 0, last_Bg_ = 0;
     int staged_k_ = 1;

@@ -1,0 +1,418 @@
+// rbm_fused.cuh -- one CD-1 step of a binary RBM (cd_k_update, energy.hpp:131-171) as ONE persistent
+// kernel: the four dependent products of the step are separated by grid barriers instead of kernel
+// boundaries, and every CTA keeps a fixed piece of the problem.
+//
+// 64 CTAs = 8 hidden tiles j (64 units) x 8 visible slices s (128 units), clusters of the 8 slices of
+// a hidden tile (a B200 holds 15 co-resident clusters of 8 at this shared-memory size, measured). W_aug is (H+1) x ldw with bh in column V and bv in row H (rbm.cuh).
+//   phase 1  h0 = sigmoid(v0 W^T + bh), hs = (u < h0)   CTA (j,s): v0[:, s] . W[j, s]^T over its 128
+//            visible units (K), partials of the 8 slices summed through distributed shared memory
+//   phase 2  v1 = sigmoid(hs W + bv), recon rows        CTA (j,s): hs[:, j] . W[j, s] (K = 32 hidden);
+//            the 8 hidden-tile partials meet in an L2 workspace, each CTA finishes 16 batch rows of its
+//            slice: sigmoid, (v0 - v1)^2 row partials
+//   phase 3  -h1 = -sigmoid(v1 W^T + bh)                 as phase 1
+//   phase 4  W_aug[j, s] += lr/B * (Hcat^T Vcat)^T       K = 2B over [h0; -h1] x [v0; v1] with the +-1 /
+//            ones columns: dW, dbh and dbv of energy.hpp:148-169 in one product, written by the owner
+// 3xTF32 everywhere (tcgen05.mma kind::tf32; the TMA-landed tile is the hi part, lo split by all threads).
+// Reductions are in fixed order (deterministic); the grid barrier is a generation counter in global
+// memory (all 128 CTAs are co-resident: one per SM).
+#pragma once
+#include "gemm_tc.cuh"
+#include "runtime.cuh"
+
+namespace b2n {
+
+constexpr int kRfThreads = 256;
+constexpr int kRfSlices = 8;                  // visible slices = cluster size
+constexpr int kRfSliceW = 128;                // visible units per slice
+constexpr int kRfTileH = 64;                  // hidden units per tile
+constexpr int kRfStage = 64 * 1024;           // operand stage: A hi | B hi | A lo | B lo
+constexpr int kRfStages = 3;
+constexpr int kRfTileP = 66;                  // padded pitch of the [128][64] reduction tile (8 B aligned rows)
+constexpr int kRfSmem = kRfStages * kRfStage + 128 * kRfTileP * 4 + 1024 + 512;
+
+struct RbmFusedParams {
+    int B, H, V;
+    long long ldw, ldv, ldh, ldhs;
+    float* W;          // W_aug
+    float* Vcat;       // [v0; v1] (+ ones column V)
+    float* Hcat;       // [h0; -h1] (+ +-1 column H)
+    float* HS;         // samples
+    const double* u;   // uniforms [B][H]
+    double* row_part;  // recon partials [slice][cap]
+    long long cap;
+    float* ws2;        // phase-2 partials [jt tiles][128 rows][8*128 cols]
+    float* ws1;        // phase-1/3 partials [jt tiles][8 slices][128 rows][64]
+    unsigned* gbar;    // slice barriers: [slice][count, generation]
+    unsigned long long* trace;  // bring-up: phase timestamps (clock64) of CTA (0,0) and (7,7), null normally
+    float alpha;       // lr / B_global
+    int jt;            // hidden tiles
+};
+
+// barrier over the nblocks CTAs that share the counter pair gbar = [count, generation]
+__device__ __forceinline__ void rf_grid_sync(unsigned* gbar, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* gen = gbar + 1;
+        const unsigned g = *gen;
+        asm volatile("fence.proxy.async.global;" ::: "memory");  // our generic writes -> later TMA reads
+        __threadfence();
+        if (atomicInc(gbar, nblocks - 1) == nblocks - 1) {
+            __threadfence();
+            *gen = g + 1;
+        } else {
+            // all CTAs are co-resident (checked on the host); the watchdog turns a broken invariant into
+            // a launch error instead of a hung GPU
+            unsigned long long spins = 0;
+            while (*gen == g) {
+                __nanosleep(20);
+                if (++spins > (1ull << 26)) __trap();
+            }
+        }
+        __threadfence();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+    }
+    __syncthreads();
+}
+
+// one 3xTF32 product of this phase into TMEM columns [0, N): nkb K-blocks of 32, operands by TMA into a
+// ring of ns stages of 2*(a_bytes + b_bytes) (hi | lo) carved for this phase, with this phase's own
+// full / empty barriers (fresh parity). load(kb, a_dst, b_dst, bar) issues the TMA boxes of K-block kb
+// (thread 0); tph = running TMEM-barrier phase.
+template <class Load>
+__device__ __forceinline__ void rf_product(uint8_t* ring, uint64_t* full, uint64_t* empty, uint64_t* tbar, int& tph,
+                                           int ns, int nkb, int a_bytes, int b_bytes, bool a_mn, bool b_mn,
+                                           uint32_t idesc, uint32_t idesc2, Load load) {
+    // stage = A hi | B hi | B lo | A lo: B hi and B lo are adjacent along N, so ONE MMA with N doubled
+    // (idesc2) computes a_hi.b_hi into columns [0, N) and a_hi.b_lo into [N, 2N); a second MMA adds
+    // a_lo.b_hi into [0, N). Two MMAs per K step instead of three; rf_tmem_to_smem folds the halves.
+    const int warp = threadIdx.x >> 5;
+    const int sb = 2 * (a_bytes + b_bytes);
+    auto slot = [&](int g) { return ring + (g % ns) * sb; };
+    if (threadIdx.x == 0)
+        for (int i = 0; i < nkb && i < ns; ++i) {
+            mbar_arrive_expect_tx(&full[i], (uint32_t)(a_bytes + b_bytes));
+            load(i, slot(i), slot(i) + a_bytes, &full[i]);
+        }
+    for (int i = 0; i < nkb; ++i) {
+        const int s = i % ns;
+        uint8_t* st = slot(i);
+        mbar_wait(&full[s], (i / ns) & 1);
+        split_lo(st + a_bytes, st + a_bytes + b_bytes, b_bytes, threadIdx.x, kRfThreads);
+        split_lo(st, st + a_bytes + 2 * b_bytes, a_bytes, threadIdx.x, kRfThreads);
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (warp == 1) {
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(st), b0 = a0 + (uint32_t)a_bytes;
+            const uint64_t a_lo = (uint64_t)((a_bytes + 2 * b_bytes) >> 4);
+            uint64_t da = a_mn ? desc_mnmajor(a0, 0) : desc_kmajor(a0, 0);
+            uint64_t db = b_mn ? desc_mnmajor(b0, 0) : desc_kmajor(b0, 0);
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk, da += a_mn ? 64 : 2, db += b_mn ? 64 : 2) {
+                mma_tf32_warp(0u, da, db, idesc2, (i | kk) != 0);
+                mma_tf32_warp(0u, da + a_lo, db, idesc, 1);
+            }
+            mma_commit_warp(&empty[s]);
+            if (i == nkb - 1) mma_commit_warp(tbar);
+        }
+        // refill the PREVIOUS block's slot (its MMAs have had this block's split to retire) with the block
+        // ns - 1 ahead; waiting on the slot just issued would serialise TMA behind every MMA batch
+        if (threadIdx.x == 0 && i >= 1 && i - 1 + ns < nkb) {
+            const int ip = i - 1, sp = ip % ns, i2 = ip + ns;
+            mbar_wait(&empty[sp], (ip / ns) & 1);
+            mbar_arrive_expect_tx(&full[sp], (uint32_t)(a_bytes + b_bytes));
+            load(i2, slot(i2), slot(i2) + a_bytes, &full[sp]);
+        }
+    }
+    mbar_wait(tbar, tph & 1);
+    ++tph;
+    tc_fence_after();
+}
+
+// TMEM [128 lanes][2*ncols] -> smem tile (pitch tp floats) as cols[c] + cols[c + ncols] (the hi.lo half);
+// warps w and w+4 share lane quadrant w%4
+__device__ __forceinline__ void rf_tmem_to_smem(float* tile, int tp, int ncols) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int q = warp & 3, half = warp >> 2;
+    const int row = 32 * q + lane;
+    const int per = ncols / 2;
+    for (int c = half * per; c < (half + 1) * per; c += 16) {
+        float v[16], w[16];
+        tmem_ld16(((uint32_t)(32 * q) << 16) + (uint32_t)c, v);
+        tmem_ld16(((uint32_t)(32 * q) << 16) + (uint32_t)(c + ncols), w);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) tile[row * tp + c + i] = v[i] + w[i];
+    }
+    tc_fence_before();
+}
+
+__global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 1)
+    rbm_cd1_fused_kernel(const __grid_constant__ CUtensorMap mVk, const __grid_constant__ CUtensorMap mWk,
+                         const __grid_constant__ CUtensorMap mHSk, const __grid_constant__ CUtensorMap mWmn,
+                         const __grid_constant__ CUtensorMap mVmn, const __grid_constant__ CUtensorMap mHmn,
+                         const RbmFusedParams p) {
+    extern __shared__ uint8_t smem_raw[];
+    if (p.trace && threadIdx.x == 0) {  // bring-up: entry time of every CTA (globaltimer, ns)
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        p.trace[64 + blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+    uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    float* tile = reinterpret_cast<float*>(ring + kRfStages * kRfStage);  // [128][kRfTileP]
+    uint64_t* full = reinterpret_cast<uint64_t*>(tile + 128 * kRfTileP);  // [phase][4]
+    uint64_t* empty = full + 16;
+    uint64_t* tbar = empty + 16;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(tbar + 1);
+
+    const int s = blockIdx.x, j = blockIdx.y;  // visible slice (= cluster rank), hidden tile
+    const int warp = threadIdx.x >> 5;
+    const int B = p.B, H = p.H, V = p.V;
+    const int v0c = s * kRfSliceW, h0c = j * kRfTileH;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 16; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(tbar, 1);
+        fence_barrier_init();
+        tma_prefetch(&mVk);
+        tma_prefetch(&mWk);
+        tma_prefetch(&mHSk);
+        tma_prefetch(&mWmn);
+        tma_prefetch(&mVmn);
+        tma_prefetch(&mHmn);
+    }
+    if (warp == 1) tmem_alloc(tslot, 256);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (*tslot != 0u) __trap();  // TMEM base column 0 (one CTA per SM)
+    pdl_wait();
+    int tph = 0;
+    int tev = 0;
+    auto mark = [&]() {
+        if (p.trace && threadIdx.x == 0 && (blockIdx.x + blockIdx.y == 0 || (blockIdx.x == 7 && blockIdx.y == 7)))
+            p.trace[(blockIdx.x ? 32 : 0) + tev] = clock64();
+        ++tev;
+    };
+    mark();
+    if (p.trace && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        p.trace[128 + blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+    const uint32_t id_h = umma_idesc_tf32(128, kRfTileH, 0, 0);   // [batch x hidden], both K-major
+    const uint32_t id_v = umma_idesc_tf32(128, kRfSliceW, 0, 1);  // [batch x visible], W MN-major
+    const uint32_t id_w = umma_idesc_tf32(128, kRfTileH, 1, 1);   // [visible x hidden], both MN-major
+    const uint32_t id_h2 = umma_idesc_tf32(128, 2 * kRfTileH, 0, 0), id_v2 = umma_idesc_tf32(128, 2 * kRfSliceW, 0, 1),
+                   id_w2 = umma_idesc_tf32(128, 2 * kRfTileH, 1, 1);
+
+    // ---- phases 1 and 3: [batch x 32 hidden] over this slice's 128 visible units, summed over the slices
+    auto hidden_phase = [&](int vrow0, bool first) {
+        const int ph = first ? 0 : 2;  // all 4 K-blocks in flight at once (4 stages of 48 KB)
+        rf_product(ring, full + 4 * ph, empty + 4 * ph, tbar, tph, 4, kRfSliceW / 32, 128 * 32 * 4, kRfTileH * 32 * 4,
+                   false, false, id_h, id_h2, [&](int kb, uint8_t* a, uint8_t* b, uint64_t* bar) {
+                       tma_load_2d(a, &mVk, bar, v0c + kb * 32, vrow0);
+                       tma_load_2d(b, &mWk, bar, v0c + kb * 32, h0c);
+                   });
+        mark();
+        rf_tmem_to_smem(tile, kRfTileP, kRfTileH);
+        __syncthreads();
+        {  // partial [B rows][64] of this slice -> L2 workspace (coalesced float4 rows)
+            float* dst = p.ws1 + ((long long)j * kRfSlices + s) * 128 * kRfTileH;
+            for (int idx = threadIdx.x; idx < B * (kRfTileH / 4); idx += kRfThreads) {
+                const int rr = idx / (kRfTileH / 4), cc = (idx % (kRfTileH / 4)) * 4;
+                const float* t = tile + rr * kRfTileP + cc;
+                *reinterpret_cast<float4*>(dst + rr * kRfTileH + cc) = make_float4(t[0], t[1], t[2], t[3]);
+            }
+        }
+        __threadfence();
+        cluster_sync_all();  // partials of the 8 slices visible cluster-wide
+        mark();
+        // rank s finishes batch rows [16 s, 16 s + 16): sum over the slices in fixed order, all loads first
+        const int r = 16 * s + (threadIdx.x >> 4), c = (threadIdx.x & 15) * 4;
+        float4 x[kRfSlices];
+#pragma unroll
+        for (int z = 0; z < kRfSlices; ++z)
+            x[z] = r < B ? __ldcg(reinterpret_cast<const float4*>(p.ws1 + (((long long)j * kRfSlices + z) * 128 + r) *
+                                                                              kRfTileH + c))
+                         : make_float4(0.f, 0.f, 0.f, 0.f);
+        float av[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int z = 0; z < kRfSlices; ++z) {
+            av[0] += x[z].x;
+            av[1] += x[z].y;
+            av[2] += x[z].z;
+            av[3] += x[z].w;
+        }
+        mark();
+        if (r < B) {
+            float bh[4];
+            double uu[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int h = h0c + c + i;
+                bh[i] = h < H ? p.W[(long long)h * p.ldw + V] : 0.0f;
+                uu[i] = first && h < H ? p.u[(long long)r * H + h] : 2.0;
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int h = h0c + c + i;
+                if (h >= H) continue;
+                const float pr = sigmoid_ref(av[i] + bh[i]);  // + bh
+                if (first) {  // energy.hpp:101-110 + unit_sample_inplace :59-61
+                    p.Hcat[(long long)r * p.ldh + h] = pr;
+                    p.HS[(long long)r * p.ldhs + h] = (uu[i] < (double)pr) ? 1.0f : 0.0f;
+                } else {
+                    p.Hcat[(long long)(B + r) * p.ldh + h] = -pr;  // stored negated for phase 4
+                }
+            }
+        }
+    };
+
+    // dependencies are narrower than the grid: phase 2 of (j, s) reads hs[:, tile j] (written by the 8
+    // CTAs of cluster j), the phase-2 reduction of slice s reads the partials of the 8 CTAs (., s), and
+    // phase 3 / 4 of (j, s) read v1[:, slice s] (written by (., s)) and -h1[:, tile j] (cluster j): so
+    // cluster barriers plus 8-CTA slice barriers (global counters) replace every grid-wide barrier
+    unsigned* sbar = p.gbar + 2 * s;
+    hidden_phase(0, true);
+    mark();
+    __threadfence();
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    cluster_sync_all();
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    mark();
+
+    // ---- phase 2: [batch x 128 visible] over this tile's 32 hidden units; tiles meet in L2
+    rf_product(ring, full + 4, empty + 4, tbar, tph, 2, kRfTileH / 32, 128 * 32 * 4, kRfSliceW * 32 * 4, false, true,
+               id_v, id_v2,
+               [&](int kb, uint8_t* a, uint8_t* b, uint64_t* bar) {
+                   tma_load_2d(a, &mHSk, bar, h0c + 32 * kb, 0);
+                   for (int q = 0; q < kRfSliceW / 32; ++q)
+                       tma_load_2d(b + q * 4096, &mWmn, bar, v0c + 32 * q, h0c + 32 * kb);
+               });
+    mark();
+    {
+        float* stg = reinterpret_cast<float*>(ring);  // [128][132], the operand ring is idle now
+        rf_tmem_to_smem(stg, kRfSliceW + 4, kRfSliceW);
+        __syncthreads();
+        float* dst = p.ws2 + (long long)j * 128 * (kRfSlices * kRfSliceW) + v0c;
+        for (int idx = threadIdx.x; idx < B * (kRfSliceW / 4); idx += kRfThreads) {
+            const int r = idx / (kRfSliceW / 4), c = (idx % (kRfSliceW / 4)) * 4;
+            *reinterpret_cast<float4*>(dst + (long long)r * (kRfSlices * kRfSliceW) + c) =
+                *reinterpret_cast<const float4*>(stg + r * (kRfSliceW + 4) + c);
+        }
+    }
+    mark();
+    rf_grid_sync(sbar, gridDim.y);
+    mark();
+    // CTA (j, s) finishes batch rows [16 j, 16 j + 16) of slice s: one warp per row (two rows per warp),
+    // 4 columns per lane; every load of both rows is issued before the first use
+    {
+        const int c = v0c + (threadIdx.x & 31) * 4;
+        float4 part[2][8], vz[2];
+        int rows[2];
+        const float4 bv = c < V ? *reinterpret_cast<const float4*>(p.W + (long long)H * p.ldw + c)
+                                : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            const int r = 16 * j + 8 * rr + warp;
+            rows[rr] = r;
+            if (r < B) {
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                    part[rr][t] = t < p.jt ? *reinterpret_cast<const float4*>(
+                                                 p.ws2 + ((long long)t * 128 + r) * (kRfSlices * kRfSliceW) + c)
+                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+                vz[rr] = *reinterpret_cast<const float4*>(p.Vcat + (long long)r * p.ldv + c);
+            }
+        }
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            const int r = rows[rr];
+            double pd = 0.0;
+            if (r < B) {
+                float4 acc = part[rr][0];
+#pragma unroll
+                for (int t = 1; t < 8; ++t) {
+                    acc.x += part[rr][t].x;
+                    acc.y += part[rr][t].y;
+                    acc.z += part[rr][t].z;
+                    acc.w += part[rr][t].w;
+                }
+                const float av[4] = {acc.x, acc.y, acc.z, acc.w}, bb[4] = {bv.x, bv.y, bv.z, bv.w};
+                const float v0v[4] = {vz[rr].x, vz[rr].y, vz[rr].z, vz[rr].w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int v = c + i;
+                    if (v >= V) continue;
+                    const float pr = sigmoid_ref(av[i] + bb[i]);  // + bv
+                    p.Vcat[(long long)(B + r) * p.ldv + v] = pr;
+                    const double d = (double)v0v[i] - (double)pr;  // energy.hpp:84-96
+                    pd += d * d;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) pd += __shfl_xor_sync(0xffffffffu, pd, o);
+            if (r < B && (threadIdx.x & 31) == 0) p.row_part[(long long)s * p.cap + r] = pd;
+        }
+    }
+    mark();
+    rf_grid_sync(sbar, gridDim.y);
+    mark();
+
+    // ---- phase 3
+    hidden_phase(B, false);
+    mark();
+    __threadfence();
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    cluster_sync_all();
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+    mark();
+
+    // ---- phase 4: [128 visible x 64 hidden] over K = 2B batch rows, then W_aug[j, s] += alpha * D^T.
+    // The W tile is read into registers before the product (nothing else writes it) so the update is
+    // a pure store after the MMAs: W, the bh column (v == V) and the bv row (h == H)
+    constexpr int kPer = kRfTileH * kRfSliceW / kRfThreads;
+    float wv[kPer];
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+        const int idx = i * kRfThreads + threadIdx.x;
+        const int n = idx / kRfSliceW, m = idx % kRfSliceW;  // hidden row n of W, visible column m
+        const int h = h0c + n, v = v0c + m;
+        wv[i] = (h <= H && v <= V) ? p.W[(long long)h * p.ldw + v] : 0.0f;
+    }
+    rf_product(ring, full + 12, empty + 12, tbar, tph, 4, (2 * B + 31) / 32, 128 * 32 * 4, kRfTileH * 32 * 4, true,
+               true, id_w, id_w2, [&](int kb, uint8_t* a, uint8_t* b, uint64_t* bar) {
+                   for (int q = 0; q < 4; ++q) tma_load_2d(a + q * 4096, &mVmn, bar, v0c + 32 * q, kb * 32);
+                   for (int q = 0; q < kRfTileH / 32; ++q) tma_load_2d(b + q * 4096, &mHmn, bar, h0c + 32 * q, kb * 32);
+               });
+    mark();
+    rf_tmem_to_smem(tile, kRfTileP, kRfTileH);
+    __syncthreads();
+    {
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            const int idx = i * kRfThreads + threadIdx.x;
+            const int n = idx / kRfSliceW, m = idx % kRfSliceW;
+            const int h = h0c + n, v = v0c + m;
+            if (h <= H && v <= V) p.W[(long long)h * p.ldw + v] = wv[i] + p.alpha * tile[m * kRfTileP + n];
+        }
+    }
+    __syncthreads();
+    mark();
+    if (p.trace && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        p.trace[192 + blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+    pdl_trigger();
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(0u, 256);
+    }
+}
+
+}  // namespace b2n
