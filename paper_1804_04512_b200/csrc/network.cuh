@@ -817,7 +817,7 @@ inline void Net::stage_inputs(const float* x, const int* labels, long long B) {
 
 inline double Net::read_loss(long long B) {
     B2N_CUDA(cudaMemcpyAsync(h_loss_.p, row_loss_, B * 8, cudaMemcpyDeviceToHost, stream_));
-    B2N_CUDA(cudaStreamSynchronize(stream_));
+    spin_sync(stream_);
     double loss = 0.0;  // network.hpp:433-435: sequential over rows, then / batch
     const double* rl = h_loss_.as<double>();
     for (long long r = 0; r < B; ++r) loss += rl[r];

@@ -91,8 +91,9 @@ class Rbm {
     }
     double recon() {  // sum of the per-(tile,row) partials / batch_global
         const long long nt = recon_tiles_;
-        B2N_CUDA(cudaMemcpyAsync(h_recon_.p, recon_.p, nt * last_B_ * 8, cudaMemcpyDeviceToHost, stream_));
-        B2N_CUDA(cudaStreamSynchronize(stream_));
+        // partials are [tile][cap_]: copy through the last tile's rows
+        B2N_CUDA(cudaMemcpyAsync(h_recon_.p, recon_.p, ((nt - 1) * cap_ + last_B_) * 8, cudaMemcpyDeviceToHost, stream_));
+        spin_sync(stream_);
         const double* r = h_recon_.as<double>();
         double acc = 0.0;
         for (long long b = 0; b < last_B_; ++b)

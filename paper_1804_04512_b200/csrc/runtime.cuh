@@ -89,6 +89,26 @@ inline CUtensorMap make_map_2d(const float* base, uint64_t inner, uint64_t outer
     return m;
 }
 
+// Low-latency host wait for the step result: record an event behind the work and busy-poll it (a
+// blocking cudaStreamSynchronize may sleep and wake the host thread several microseconds late; the
+// step itself is tens of microseconds). One event per thread, reused.
+inline void spin_sync(cudaStream_t st) {
+    thread_local cudaEvent_t ev = [] {
+        cudaEvent_t e = nullptr;
+        if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) e = nullptr;
+        return e;
+    }();
+    if (!ev) {
+        B2N_CUDA(cudaStreamSynchronize(st));
+        return;
+    }
+    B2N_CUDA(cudaEventRecord(ev, st));
+    cudaError_t e;
+    while ((e = cudaEventQuery(ev)) == cudaErrorNotReady) {
+    }
+    B2N_CUDA(e);
+}
+
 struct DevMem {
     void* p = nullptr;
     size_t bytes = 0;

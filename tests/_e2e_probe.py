@@ -30,3 +30,12 @@ t = time.perf_counter()
 lib = F._lib.load()
 for _ in range(n): lib.b2n_version()
 print("ctypes call overhead us %.2f" % ((time.perf_counter() - t) / n * 1e6))
+# component timings of the public call
+rbm.stage(v0, u); torch.cuda.synchronize()
+t = time.perf_counter()
+for _ in range(n): rbm.stage(v0, u)
+print("stage (H2D + sync) us %.1f" % ((time.perf_counter() - t) / n * 1e6))
+t = time.perf_counter()
+for _ in range(n):
+    rbm.run_staged(1, 0.1, B); rbm.recon()
+print("run_staged + recon (launch, D2H, sync) us %.1f" % ((time.perf_counter() - t) / n * 1e6))

@@ -46,5 +46,7 @@ def test_nccl_rbm_matches_single(gpu):
     b.run_staged(2, 0.1, 100)
     wa, bva, bha = a.get()
     wb, bvb, bhb = b.get()
-    assert norm_err(wb, wa) < 1e-6 and norm_err(bvb, bva) < 1e-6 and norm_err(bhb, bha) < 1e-6
-    assert abs(a.recon() - b.recon()) < 1e-9 * a.recon()
+    # the single-GPU step runs the fused CD-1 kernel, the data-parallel one the split GEMMs + allreduce:
+    # same math, different (deterministic) summation orders -> agreement at the 3xTF32 level
+    assert norm_err(wb, wa) < 1e-5 and norm_err(bvb, bva) < 1e-5 and norm_err(bhb, bha) < 1e-5
+    assert abs(a.recon() - b.recon()) < 1e-6 * a.recon()
