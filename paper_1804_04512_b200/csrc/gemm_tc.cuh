@@ -101,7 +101,11 @@ struct GemmCfg {
     static constexpr int STAGE_BYTES = (A_BYTES + B_BYTES) * (X3 ? 2 : 1);
     static constexpr int STAGES_FIT = (200 * 1024) / STAGE_BYTES;
     static constexpr int STAGES = STAGES_FIT > 6 ? 6 : STAGES_FIT;
-    static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+    // 3xTF32 with BN <= 128 stacks B hi | B lo along N: one MMA (N = 2 BN) gives a_hi.b_hi in columns
+    // [0, BN) and a_hi.b_lo in [BN, 2 BN), a second adds a_lo.b_hi to [0, BN): 2 MMAs per K step, not 3
+    static constexpr bool STACK = X3 && BN <= 128;
+    static constexpr int ACC_COLS = STACK ? 2 * BN : BN;
+    static constexpr int TMEM_COLS = ACC_COLS <= 32 ? 32 : ACC_COLS <= 64 ? 64 : ACC_COLS <= 128 ? 128 : 256;
     static constexpr int TP = BN + 4;  // padded smem tile pitch (floats): conflict-free row writes
     static constexpr int TILE_BYTES = kBM * TP * 4;
     static constexpr int MAIN_BYTES = STAGES * STAGE_BYTES > TILE_BYTES ? STAGES * STAGE_BYTES : TILE_BYTES;
@@ -435,6 +439,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // descriptors advance by running adds on the 14-bit start-address field: a K-major kk step is
         // 32 B (SW128 rows), an MN-major one 1024 B (8 K-rows of 128 B); stages STAGE_BYTES apart
         const uint32_t idesc = umma_idesc_tf32(kBM, BN, p.a_mn, p.b_mn);
+        const uint32_t idesc2 = umma_idesc_tf32(kBM, Cfg::STACK ? 2 * BN : BN, p.a_mn, p.b_mn);
         const uint32_t a0 = smem_u32(smem), b0 = a0 + Cfg::A_BYTES;
         const uint64_t da0 = p.a_mn ? desc_mnmajor(a0, 0) : desc_kmajor(a0, 0);
         const uint64_t db0 = p.b_mn ? desc_mnmajor(b0, 0) : desc_kmajor(b0, 0);
@@ -450,7 +455,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint64_t dah = da0 + st, dbh = db0 + st;
 #pragma unroll
             for (int kk = 0; kk < kBK / 8; ++kk, dah += a_kk, dbh += b_kk) {
-                if (X3) {
+                if (Cfg::STACK) {  // stage: A hi | B hi | B lo | A lo
+                    mma_tf32_warp(tmem_base, dah, dbh, idesc2, (i | kk) != 0);
+                    mma_tf32_warp(tmem_base, dah + (uint64_t)((Cfg::A_BYTES + 2 * Cfg::B_BYTES) >> 4), dbh, idesc, 1);
+                } else if (X3) {
                     mma_tf32_warp(tmem_base, dah + lo_add, dbh, idesc, (i | kk) != 0);
                     mma_tf32_warp(tmem_base, dah, dbh + lo_add, idesc, 1);
                     mma_tf32_warp(tmem_base, dah, dbh, idesc, 1);
@@ -472,7 +480,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&full[s], ph);
                 if (ct == 0 && i < 16) B2N_TRACE(18 + i);
                 uint8_t* a = smem + s * Cfg::STAGE_BYTES;
-                split_lo(a, a + Cfg::A_BYTES + Cfg::B_BYTES, Cfg::A_BYTES + Cfg::B_BYTES, ct, 32 * kEpiWarps);
+                if (Cfg::STACK) {
+                    split_lo(a + Cfg::A_BYTES, a + Cfg::A_BYTES + Cfg::B_BYTES, Cfg::B_BYTES, ct, 32 * kEpiWarps);
+                    split_lo(a, a + Cfg::A_BYTES + 2 * Cfg::B_BYTES, Cfg::A_BYTES, ct, 32 * kEpiWarps);
+                } else {
+                    split_lo(a, a + Cfg::A_BYTES + Cfg::B_BYTES, Cfg::A_BYTES + Cfg::B_BYTES, ct, 32 * kEpiWarps);
+                }
                 fence_proxy_async_smem();
                 mbar_arrive(&ready[s]);
             }
@@ -494,6 +507,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int c = half * (BN / 2); c < (half + 1) * (BN / 2); c += 16) {
                 float v[16];
                 tmem_ld16(trow + c, v);
+                if (Cfg::STACK) {  // fold the a_hi.b_lo half
+                    float w[16];
+                    tmem_ld16(trow + c + BN, w);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) v[i] += w[i];
+                }
 #pragma unroll
                 for (int i = 0; i < 16; i += 4)
                     *reinterpret_cast<float4*>(dst + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
@@ -501,6 +520,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         } else {
             float v[8];
             tmem_ld8(trow + half * 8, v);
+            if (Cfg::STACK) {
+                float w[8];
+                tmem_ld8(trow + half * 8 + BN, w);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) v[i] += w[i];
+            }
 #pragma unroll
             for (int i = 0; i < 8; i += 4)
                 *reinterpret_cast<float4*>(dst + half * 8 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
