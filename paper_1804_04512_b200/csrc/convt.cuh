@@ -416,6 +416,23 @@ __device__ __forceinline__ void ct_epilogue(const ConvTParams& p, uint32_t tmem_
     }
 }
 
+// the K steps of one halo row, unrolled: KW taps x GP quad pairs (GP = 0: one quad, tap pairs)
+template <int KW, int GP, bool X3>
+__device__ __forceinline__ void ct_mma_row(uint32_t tacc, uint64_t a_row, uint64_t b_base, uint64_t b_step,
+                                           uint64_t two_p, uint64_t a_lo_add, uint64_t b_lo_add, uint32_t idesc) {
+    constexpr int NS = GP ? KW * GP : (KW + 1) / 2;
+#pragma unroll
+    for (int ks = 0; ks < NS; ++ks) {
+        const uint64_t dah = a_row + (GP ? (uint64_t)(ks / GP) + (uint64_t)(ks % GP) * two_p : (uint64_t)(2 * ks));
+        const uint64_t dbh = b_base + (uint64_t)ks * b_step;
+        if (X3) {
+            mma_tf32_elect(tacc, dah + a_lo_add, dbh, idesc);
+            mma_tf32_elect(tacc, dah, dbh + b_lo_add, idesc);
+        }
+        mma_tf32_elect(tacc, dah, dbh, idesc);
+    }
+}
+
 // Correlation over row-blocked halo tiles on the tensor cores (3xTF32: a.b = ah.bh + ah.bl + al.bh with
 // the hardware's tf32 truncation making the raw value the hi part, fp32 accumulate, ~1e-7 relative). Per tile (R output rows x Wt columns) and per halo row
 // h, each MMA reads the halo row ONCE and multiplies it with all kh filter rows stacked along N
@@ -553,7 +570,21 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
                 // halo row h feeds output rows h - di (di = 0..kh-1) = row slots HR-1-h .. HR-1-h+kh-1
                 const uint32_t tacc = tmem_base + (uint32_t)(buf * bufcols + (p.HR - 1 - h) * NK);
                 uint64_t dbh = b_base;
-                if (p.G >= 2) {
+                const uint64_t two_p = (uint64_t)(2 * p.P);
+                // the common shapes run fully unrolled (independent descriptor adds interleave)
+                if (p.kw == 3 && p.G == 4) {
+                    ct_mma_row<3, 2, X3>(tacc, a_row, b_base, b_step, two_p, a_lo_add, b_lo_add, idesc);
+                } else if (p.kw == 3 && p.G == 1) {
+                    ct_mma_row<3, 0, X3>(tacc, a_row, b_base, b_step, two_p, a_lo_add, b_lo_add, idesc);
+                } else if (p.kw == 5 && p.G == 1) {
+                    ct_mma_row<5, 0, X3>(tacc, a_row, b_base, b_step, two_p, a_lo_add, b_lo_add, idesc);
+                } else if (p.kw == 5 && (p.G == 3 || p.G == 4)) {
+                    ct_mma_row<5, 2, X3>(tacc, a_row, b_base, b_step, two_p, a_lo_add, b_lo_add, idesc);
+                } else if (p.kw == 5 && p.G == 2) {
+                    ct_mma_row<5, 1, X3>(tacc, a_row, b_base, b_step, two_p, a_lo_add, b_lo_add, idesc);
+                } else if (p.kw == 3 && p.G == 2) {
+                    ct_mma_row<3, 1, X3>(tacc, a_row, b_base, b_step, two_p, a_lo_add, b_lo_add, idesc);
+                } else if (p.G >= 2) {
                     const int GP = (p.G + 1) >> 1;
                     for (int dj = 0; dj < p.kw; ++dj) {
                         uint64_t dah = a_row + (uint64_t)dj;
