@@ -166,6 +166,7 @@ class RbmWork:
         self.u_h = pinned(u.shape, np.float64)
         self.u_h[:] = u
         self.F = F
+        self.dist = dist
         self.config = {"workload": "mnist_rbm_cd1", "model": "RBM 784-500 binary, CD-1", "global_batch": self.Bg,
                        "local_batch": self.B, "parallelism": f"dp{dist.world}", "lr": self.lr,
                        "sampling": "supplied generate_canonical<double,53> uniforms (bit-exact Bernoulli)"}
@@ -179,6 +180,10 @@ class RbmWork:
         self.rbm.run_staged(n, self.lr, self.Bg)
 
     def e2e_step(self):
+        if self.dist.world > 1:  # data-parallel: stage the shard (H2D), one step, read the recon partials
+            self.rbm.stage(self.v0_h, self.u_h)
+            self.rbm.run_staged(1, self.lr, self.Bg)
+            return self.rbm.recon()
         return self.F.cd_k_update(self.rbm, self.v0_h, 1, self.lr, self.u_h, self.Bg)
 
     def kernels_per_step(self):
@@ -188,7 +193,10 @@ class RbmWork:
         return _profile(self.F._lib, "b2n_rbm_profile", self.rbm.handle, steps, self.lr, self.Bg)
 
     def d2h_bytes(self):
-        return self.B * 8 * 25  # per-(tile,row) reconstruction partials read back
+        # per-(slice,row) reconstruction partials read back: 8 slices for the fused step, one per
+        # 64-column tile of the visible GEMM on the split path
+        tiles = 8 if self.kernels_per_step() == 1 else (self.V + 63) // 64
+        return self.B * 8 * tiles
 
 
 class NetWork:

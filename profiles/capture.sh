@@ -8,9 +8,11 @@ for c in rbm mlp mnist_cnn cifar_cnn imagenet_cnn; do
       --log-file gpurun_out/${R}_launches_${c}.csv \
       python bench.py --profile-only --config $c --steps 1 --warmup 1 > /dev/null 2>&1
 done
-# one full step of the headline workload (RBM CD-1: 4 GEMM launches), full metric set
-ncu --set full --clock-control none --import-source on -k regex:gemm_tc -s 4 -c 4 \
+# one step of the headline workload: the fused CD-1 kernel, and the 4-GEMM split path it replaced
+ncu --set full --clock-control none --import-source on -k regex:rbm_cd1 -s 1 -c 1 \
     -o gpurun_out/${R}_rbm_full python bench.py --profile-only --config rbm --steps 1 --warmup 1 > /dev/null 2>&1
+B2N_RBM_FUSED=0 ncu --set full --clock-control none --import-source on -k regex:gemm_tc -s 4 -c 4 \
+    -o gpurun_out/${R}_rbm_split_full python bench.py --profile-only --config rbm --steps 1 --warmup 1 > /dev/null 2>&1
 # the halo-tile conv kernels of one ImageNet-shape step (5 fwd, 4 dgrad, 5 wgrad)
 ncu --set full --clock-control none --import-source on -k regex:"convt_(mma|wgrad)_kernel" -c 14 \
     -o gpurun_out/${R}_imagenet_conv_full python bench.py --profile-only --config imagenet_cnn --steps 1 --warmup 0 > /dev/null 2>&1

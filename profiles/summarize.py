@@ -76,7 +76,10 @@ def main(tag: str):
              "Captured with `profiles/capture.sh` under gpurun; numbers from single-kernel replay",
              "(cold-cache, serialised): compare SHARES with bench.py's live CUDA-event timings, not absolutes.", ""]
     traffic = {}
-    for rep, names, title in [(OUT / f"{tag}_rbm_full.ncu-rep", RBM_STEP, "RBM CD-1 step (headline), 4 GEMM launches"),
+    for rep, names, title in [(OUT / f"{tag}_rbm_full.ncu-rep", ["rbm.cd1_fused"],
+                               "RBM CD-1 step (headline): the fused single-kernel step"),
+                              (OUT / f"{tag}_rbm_split_full.ncu-rep", RBM_STEP,
+                               "RBM CD-1 step, split path (4 GEMM launches; data-parallel mode, B2N_RBM_FUSED=0)"),
                               (OUT / f"{tag}_imagenet_conv_full.ncu-rep", IMAGENET_CONV,
                                "ImageNet-shape CNN (batch 128): halo-tile conv kernels of one step")]:
         if not rep.exists():
@@ -87,7 +90,7 @@ def main(tag: str):
         for i, d in enumerate(rows):
             op = names[i] if i < len(names) else "?"
             tb = (d.get("dram_read") or 0) + (d.get("dram_write") or 0)
-            traffic.setdefault(op, tb)
+            traffic.setdefault(op, tb)  # per launch: bench.py's roofline `traffic`
             lines.append(f"| {op} | `{d['kernel'][:60]}` | {d.get('dur_us', 0):.2f} | {tb / 1e6:.3f} | "
                          f"{d.get('dram_pct', 0):.1f} | {d.get('tensor_pct', 0):.1f} | {d.get('sm_pct', 0):.1f} | "
                          f"{d.get('regs', 0):.0f} | {d.get('grid', 0):.0f} |")
@@ -108,7 +111,8 @@ def main(tag: str):
     if lib.exists():
         sass = subprocess.run(["cuobjdump", "-sass", str(lib)], capture_output=True, text=True).stdout
         import re
-        counts = {m: len(re.findall(r"\b" + m + r"\b", sass)) for m in ["UTCHMMA", "UTMALDG", "UBLKCP", "LDTM", "STTM", "UTCBAR", "HMMA"]}
+        counts = {m: len(re.findall(r"\b" + m + r"\b", sass))
+                  for m in ["UTCHMMA", "UTMALDG", "UBLKCP", "LDTM", "STTM", "UTCBAR", "HMMA"]}
         lines += ["## SASS evidence (cuobjdump -sass libb200nn.so)", "",
                   "| mnemonic | count | meaning |", "|---|---|---|",
                   f"| UTCHMMA | {counts['UTCHMMA']} | tcgen05.mma (kind::tf32) |",
