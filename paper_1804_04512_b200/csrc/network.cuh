@@ -362,9 +362,15 @@ inline Net::Net(const b2n_network_spec& spec, int device, int precision)
     {  // the halo-tile conv kernels cover 3x3 / 5x5 filters with <= 32 channels and kernels
         const char* e = std::getenv("B2N_CONV_LEGACY");
         tconv_ = !(e && e[0] == '1');
-        for (const Layer& L : layers_)
-            if (L.kind == B2N_CONV && !(L.g.kh == L.g.kw && (L.g.kh == 3 || L.g.kh == 5) && L.g.k <= 32 && L.g.c <= 32))
-                tconv_ = false;
+        auto nk = [](int n) { return n <= 8 ? 8 : n <= 16 ? 16 : 32; };
+        for (const Layer& L : layers_) {
+            if (L.kind != B2N_CONV) continue;
+            const bool shape_ok = L.g.kh == L.g.kw && (L.g.kh == 3 || L.g.kh == 5) && L.g.k <= 32 && L.g.c <= 32;
+            // two TMEM buffers of >= 2 + 2(kh-1) row slots of NK columns (fwd: NK(k), dgrad: NK(c))
+            const int slots = 2 + 2 * (L.g.kh - 1);
+            const bool tmem_ok = 2 * slots * nk(L.g.k) <= 512 && 2 * slots * nk(L.g.c) <= 512;
+            if (!shape_ok || !tmem_ok) tconv_ = false;
+        }
     }
 
     // packed parameter layout, trainable() order

@@ -308,6 +308,11 @@ class Rbm:
         _lib.call("b2n_rbm_get", self._h, _f(w), _f(bv), _f(bh))
         return w, bv, bh
 
+    def kernels_per_step(self) -> int:
+        n = C.c_int()
+        _lib.call("b2n_rbm_kernels_per_step", self._h, C.byref(n))
+        return n.value
+
     def last_states(self, batch: int):
         h0 = np.zeros((batch, self.hidden), np.float32)
         hs = np.zeros_like(h0)
