@@ -147,6 +147,7 @@ struct ConvTParams {
     int halo_bytes;             // fp32 halo [HR][G][P][4]
     int h_bytes;                // one halo buffer incl. the slack MMA rows past the tile read
     int stage_bytes, w_bytes;       // smem carve-up (host-computed)
+    int stack;                      // 3xTF32 with B hi|lo interleaved along N: 2 MMAs per K step (below)
     const float* x;     // FWD input, row-blocked [b][y][G][Win][4]
     long long x_bstride;
     // epilogue
@@ -319,10 +320,14 @@ __device__ __forceinline__ void ct_epilogue(const ConvTParams& p, uint32_t tmem_
     const int c_lo = hsel * NH;
     const int L = 32 * q + lane;
     const uint32_t tq = tmem_base + ((uint32_t)(32 * q) << 16) + (uint32_t)c_lo;
+    const int SW = p.stack ? 2 * NK : NK;  // row-slot width: [a.b_hi + a_lo.b_hi | a_hi.b_lo] when stacked
     // output row r of buffer buf accumulates in row slot HR-1-r (see convt_mma_kernel); zero the real
     // slots of both buffers once, then after every drain
     auto zero_rows = [&](int buf) {
-        for (int r = 0; r < p.R; ++r) tmem_zeron<NH>(tq + (uint32_t)(buf * bufcols + (p.HR - 1 - r) * NK));
+        for (int r = 0; r < p.R; ++r) {
+            tmem_zeron<NH>(tq + (uint32_t)(buf * bufcols + (p.HR - 1 - r) * SW));
+            if (p.stack) tmem_zeron<NH>(tq + (uint32_t)(buf * bufcols + (p.HR - 1 - r) * SW + NK));
+        }
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     };
     zero_rows(0);
@@ -346,12 +351,22 @@ __device__ __forceinline__ void ct_epilogue(const ConvTParams& p, uint32_t tmem_
         ct_tile(p, t, b, y0, x0);
         const int x = x0 + L;
         const bool xok = L < p.Wt && x < p.OW;
-        const uint32_t tcol = tq + (uint32_t)(buf * bufcols + (p.HR - 1) * NK);  // slot of row 0; row r at -r*NK
+        const uint32_t tcol = tq + (uint32_t)(buf * bufcols + (p.HR - 1) * SW);  // slot of row 0; row r at -r*SW
         float* ob = p.out.p + (long long)b * p.out.bstride;
         for (int r = 0; r < (p.dbg & 2 ? 0 : p.R); r += POOL ? 2 : 1) {
             float v0[NH], v1[NH];
-            tmem_ldn<NH>(tcol - r * NK, v0);
-            if (POOL) tmem_ldn<NH>(tcol - (r + 1) * NK, v1);
+            tmem_ldn<NH>(tcol - r * SW, v0);
+            if (POOL) tmem_ldn<NH>(tcol - (r + 1) * SW, v1);
+            if (p.stack) {  // fold the a_hi.b_lo half of each slot
+                float w0[NH], w1[NH];
+                tmem_ldn<NH>(tcol - r * SW + NK, w0);
+                if (POOL) tmem_ldn<NH>(tcol - (r + 1) * SW + NK, w1);
+#pragma unroll
+                for (int j = 0; j < NH; ++j) {
+                    v0[j] += w0[j];
+                    if (POOL) v1[j] += w1[j];
+                }
+            }
             const int y = y0 + r;
 #pragma unroll
             for (int j = 0; j < NH; ++j) {
@@ -419,12 +434,18 @@ __device__ __forceinline__ void ct_epilogue(const ConvTParams& p, uint32_t tmem_
 // the K steps of one halo row, unrolled: KW taps x GP quad pairs (GP = 0: one quad, tap pairs)
 template <int KW, int GP, bool X3>
 __device__ __forceinline__ void ct_mma_row(uint32_t tacc, uint64_t a_row, uint64_t b_base, uint64_t b_step,
-                                           uint64_t two_p, uint64_t a_lo_add, uint64_t b_lo_add, uint32_t idesc) {
+                                           uint64_t two_p, uint64_t a_lo_add, uint64_t b_lo_add, uint32_t idesc,
+                                           bool stk) {
     constexpr int NS = GP ? KW * GP : (KW + 1) / 2;
 #pragma unroll
     for (int ks = 0; ks < NS; ++ks) {
         const uint64_t dah = a_row + (GP ? (uint64_t)(ks / GP) + (uint64_t)(ks % GP) * two_p : (uint64_t)(2 * ks));
         const uint64_t dbh = b_base + (uint64_t)ks * b_step;
+        if (X3 && stk) {  // B1 = [hi | lo], B2 = [hi | 0] per filter row: a_hi.B1 + a_lo.B2
+            mma_tf32_elect(tacc, dah, dbh, idesc);
+            mma_tf32_elect(tacc, dah + a_lo_add, dbh + b_lo_add, idesc);
+            continue;
+        }
         if (X3) {
             mma_tf32_elect(tacc, dah + a_lo_add, dbh, idesc);
             mma_tf32_elect(tacc, dah, dbh + b_lo_add, idesc);
@@ -467,7 +488,7 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int S = p.stages;
-    const int bufcols = p.slots * NK;
+    const int bufcols = p.slots * (p.stack ? 2 * NK : NK);
     // one CTA per SM (shared memory): it takes all of TMEM, whose base is then column 0 -- a compile-time
     // constant, so the MMA warp's accumulator addresses stay in uniform registers
     constexpr uint32_t tcols = 512;
@@ -491,12 +512,14 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
     for (int i = threadIdx.x; i < S * p.stage_bytes / 16; i += blockDim.x)
         reinterpret_cast<uint4*>(smem)[i] = make_uint4(0u, 0u, 0u, 0u);
     pdl_wait();  // weights and inputs are written by earlier kernels of the step
-    {  // weights, K-major no-swizzle: [kstep][kc][n = di*NK + k][4]
-        const int NN = p.kh * NK;
+    {  // weights, K-major no-swizzle: [kstep][kc][n][4] with n = di*NK + k, or (stacked) di*2NK + part*NK + k:
+        // array 1 = hi | lo, array 2 = hi | 0 (the lo part of array 1 takes the place of array 2's zeros)
+        const int SWb = p.stack ? 2 * NK : NK;
+        const int NN = p.kh * SWb;
         const int total = p.ksteps * 2 * NN * 4;
         for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
             const int j = idx & 3, n = (idx >> 2) % NN, kc = (idx / (4 * NN)) & 1, s = idx / (8 * NN);
-            const int di = n / NK, nn = n - di * NK;
+            const int di = n / SWb, part = (n - di * SWb) / NK, nn = n - di * SWb - part * NK;
             int cin, dj;
             float v = 0.0f;
             if (ct_kdecode(p, s, kc, j, cin, dj) && nn < p.N) {
@@ -507,8 +530,13 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
                 }
             }
             const int off = s * (2 * NN * 16) + kc * (NN * 16) + n * 16 + j * 4;
-            *reinterpret_cast<float*>(wsm + off) = v;
-            *reinterpret_cast<float*>(wsm + p.w_bytes + off) = split_lo1(v);
+            if (p.stack) {
+                *reinterpret_cast<float*>(wsm + off) = part ? split_lo1(v) : v;
+                *reinterpret_cast<float*>(wsm + p.w_bytes + off) = part ? 0.0f : v;
+            } else {
+                *reinterpret_cast<float*>(wsm + off) = v;
+                *reinterpret_cast<float*>(wsm + p.w_bytes + off) = split_lo1(v);
+            }
         }
     }
     fence_proxy_async_smem();
@@ -549,12 +577,13 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
         }
     } else if (warp == 1) {  // ---------------- MMA issue (whole warp, elected lane)
         // descriptor arithmetic only touches the 14-bit start-address field (smem < 256 KB)
-        const uint32_t idesc = umma_idesc_tf32(128, p.kh * NK, 0, 0);
+        const int SWm = p.stack ? 2 * NK : NK;
+        const uint32_t idesc = umma_idesc_tf32(128, p.kh * SWm, 0, 0);
         const uint64_t a_lo_add = (uint64_t)(p.h_bytes >> 4), b_lo_add = (uint64_t)(p.w_bytes >> 4);
         const uint64_t row_add = (uint64_t)((p.G * p.P * 16) >> 4);
         const uint64_t a_base = desc_none(smem_u32(smem), p.G >= 2 ? (uint32_t)p.P * 16 : 16u);
-        const uint64_t b_base = desc_none(smem_u32(wsm), (uint32_t)(p.kh * NK * 16));
-        const uint64_t b_step = (uint64_t)((2 * p.kh * NK * 16) >> 4);
+        const uint64_t b_base = desc_none(smem_u32(wsm), (uint32_t)(p.kh * SWm * 16));
+        const uint64_t b_step = (uint64_t)((2 * p.kh * SWm * 16) >> 4);
         int it = 0;
         for (int t = blockIdx.x; t < p.ntiles; t += gridDim.x, ++it) {
             const int s = it % S, buf = it & 1;
@@ -568,27 +597,32 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
             uint64_t a_row = a_base + (uint64_t)((s * p.stage_bytes) >> 4);
             for (int h = 0; h < p.HR; ++h, a_row += row_add) {
                 // halo row h feeds output rows h - di (di = 0..kh-1) = row slots HR-1-h .. HR-1-h+kh-1
-                const uint32_t tacc = tmem_base + (uint32_t)(buf * bufcols + (p.HR - 1 - h) * NK);
+                const uint32_t tacc = tmem_base + (uint32_t)(buf * bufcols + (p.HR - 1 - h) * SWm);
                 uint64_t dbh = b_base;
                 const uint64_t two_p = (uint64_t)(2 * p.P);
                 // the common shapes run fully unrolled (independent descriptor adds interleave)
                 if (p.kw == 3 && p.G == 4) {
-                    ct_mma_row<3, 2, X3>(tacc, a_row, b_base, b_step, two_p, a_lo_add, b_lo_add, idesc);
+                    ct_mma_row<3, 2, X3>(tacc, a_row, b_base, b_step, two_p, a_lo_add, b_lo_add, idesc, p.stack != 0);
                 } else if (p.kw == 3 && p.G == 1) {
-                    ct_mma_row<3, 0, X3>(tacc, a_row, b_base, b_step, two_p, a_lo_add, b_lo_add, idesc);
+                    ct_mma_row<3, 0, X3>(tacc, a_row, b_base, b_step, two_p, a_lo_add, b_lo_add, idesc, p.stack != 0);
                 } else if (p.kw == 5 && p.G == 1) {
-                    ct_mma_row<5, 0, X3>(tacc, a_row, b_base, b_step, two_p, a_lo_add, b_lo_add, idesc);
+                    ct_mma_row<5, 0, X3>(tacc, a_row, b_base, b_step, two_p, a_lo_add, b_lo_add, idesc, p.stack != 0);
                 } else if (p.kw == 5 && (p.G == 3 || p.G == 4)) {
-                    ct_mma_row<5, 2, X3>(tacc, a_row, b_base, b_step, two_p, a_lo_add, b_lo_add, idesc);
+                    ct_mma_row<5, 2, X3>(tacc, a_row, b_base, b_step, two_p, a_lo_add, b_lo_add, idesc, p.stack != 0);
                 } else if (p.kw == 5 && p.G == 2) {
-                    ct_mma_row<5, 1, X3>(tacc, a_row, b_base, b_step, two_p, a_lo_add, b_lo_add, idesc);
+                    ct_mma_row<5, 1, X3>(tacc, a_row, b_base, b_step, two_p, a_lo_add, b_lo_add, idesc, p.stack != 0);
                 } else if (p.kw == 3 && p.G == 2) {
-                    ct_mma_row<3, 1, X3>(tacc, a_row, b_base, b_step, two_p, a_lo_add, b_lo_add, idesc);
+                    ct_mma_row<3, 1, X3>(tacc, a_row, b_base, b_step, two_p, a_lo_add, b_lo_add, idesc, p.stack != 0);
                 } else if (p.G >= 2) {
                     const int GP = (p.G + 1) >> 1;
                     for (int dj = 0; dj < p.kw; ++dj) {
                         uint64_t dah = a_row + (uint64_t)dj;
                         for (int gp = 0; gp < GP; ++gp, dah += (uint64_t)(2 * p.P), dbh += b_step) {
+                            if (X3 && p.stack) {
+                                mma_tf32_elect(tacc, dah, dbh, idesc);
+                                mma_tf32_elect(tacc, dah + a_lo_add, dbh + b_lo_add, idesc);
+                                continue;
+                            }
                             if (X3) {
                                 mma_tf32_elect(tacc, dah + a_lo_add, dbh, idesc);
                                 mma_tf32_elect(tacc, dah, dbh + b_lo_add, idesc);
@@ -599,6 +633,11 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
                 } else {
                     uint64_t dah = a_row;
                     for (int ks = 0; ks < p.ksteps; ++ks, dah += 2, dbh += b_step) {
+                        if (X3 && p.stack) {
+                            mma_tf32_elect(tacc, dah, dbh, idesc);
+                            mma_tf32_elect(tacc, dah + a_lo_add, dbh + b_lo_add, idesc);
+                            continue;
+                        }
                         if (X3) {
                             mma_tf32_elect(tacc, dah + a_lo_add, dbh, idesc);
                             mma_tf32_elect(tacc, dah, dbh + b_lo_add, idesc);
@@ -1041,7 +1080,12 @@ inline ConvTLaunch plan_convt(int mode, int B, int Cp, int Hin, int Win, int kh,
     p.N = N;
     if (kh * L.nk > 256) throw Error(B2N_ESHAPE, "b200nn conv: kh x kernels exceeds one MMA (N <= 256)");
     if (2 * (2 + 2 * (kh - 1)) * L.nk > 512) throw Error(B2N_ESHAPE, "b200nn conv: accumulators exceed TMEM");
-    ct_tile_shape(B, p.OH, p.OW, L.nk, kh, p.R, p.Wt);
+    // 3x3 / <= 16 kernels: B hi|lo interleaved along N (2 MMAs per K step, double-width row slots) when
+    // a tile of >= 4 rows (or the whole map) still fits shared memory with the doubled weights
+    p.stack = x3 && kh == 3 && L.nk <= 16 && !std::getenv("B2N_CT_NOSTACK");
+    for (int attempt = 0; attempt < 2; ++attempt) {
+    ct_tile_shape(B, p.OH, p.OW, p.stack ? 2 * L.nk : L.nk, kh, p.R, p.Wt);
+    bool fits = true;
     for (;;) {  // the tallest tile whose 2 halo stages (hi + lo) fit next to the weights / staging
         const int P_ = p.Wt + kw - 1, HR_ = p.R + kh - 1, G_ = Cp / 4;
         const int hb = (HR_ * G_ * P_ * 16 + (kw + 129) * 16 + 127) & ~127;
@@ -1053,9 +1097,17 @@ inline ConvTLaunch plan_convt(int mode, int B, int Cp, int Hin, int Win, int kh,
             zz.bw = ((z->pool ? P_ / 2 + 1 : P_) + 6) & ~3;
             zb = (zs_bytes(zz) + 127) & ~127;
         }
-        const int need = 2 * (2 * hb) + 2 * (ks * 2 * kh * L.nk * 16) + 1024 + 256 + ks * 16 + 128 + 2 * zb;
-        if (need <= 227 * 1024 || p.R <= 2) break;
+        const int need = 2 * (2 * hb) + 2 * (ks * 2 * kh * (p.stack ? 2 : 1) * L.nk * 16) + 1024 + 256 + ks * 16 + 128 + 2 * zb;
+        if (need <= 227 * 1024) break;
+        if (p.R <= 2) {
+            fits = false;
+            break;
+        }
         p.R -= 2;
+    }
+    const int ohe = (p.OH + 1) & ~1;
+    if (!p.stack || (fits && (p.R >= 4 || p.R >= ohe))) break;
+    p.stack = 0;  // fall back to 3 MMAs per K step with single-width slots
     }
     p.P = p.Wt + kw - 1;
     p.HR = p.R + kh - 1;
@@ -1069,7 +1121,7 @@ inline ConvTLaunch plan_convt(int mode, int B, int Cp, int Hin, int Win, int kh,
     // MMA rows past the tile width read at most (kw + 128) * 16 bytes beyond the halo (ct_aoff)
     p.h_bytes = (p.halo_bytes + (kw + 129) * 16 + 127) & ~127;
     p.stage_bytes = 2 * p.h_bytes;
-    p.w_bytes = p.ksteps * 2 * kh * L.nk * 16;
+    p.w_bytes = p.ksteps * 2 * kh * (p.stack ? 2 : 1) * L.nk * 16;
     std::memset(L.zmaps, 0, sizeof(L.zmaps));
     if (z) {  // DGRAD: pooled window covering the dZ halo rows / cols of a tile
         p.z = *z;
