@@ -461,6 +461,11 @@ def main():
     rl = roofline(prof, a.precision)
     prof_step = sum(o["ms"] for o in prof)
     rl["share_of_step"] = round(max(o["ms"] for o in prof) / prof_step, 4) if prof_step else None
+    # the B=100 steps sit far below the HBM roofline, so the step is also set against a
+    # launch floor: dependent kernels x the measured single-kernel graph-launch latency
+    # (tools/launch_probe.cu: 4.2 us on this pool's B200s)
+    rl["launch_floor_us"] = round(work.kernels_per_step() * 4.2, 2)
+    rl["step_us"] = round(step_ms * 1e3, 2)
     line = {"metric": "train samples/s", "value": round(value, 2), "unit": "samples/s", "n_gpus": dist.world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(step_ms, 5), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32 (3xTF32 tensor-core GEMMs)" if
