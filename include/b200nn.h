@@ -127,6 +127,20 @@ int b2n_net_run_staged(b2n_net* net, int steps, long long batch_global);
 int b2n_net_loss(b2n_net* net, double* loss);
 int b2n_net_stream(b2n_net* net, void** cuda_stream);
 int b2n_net_kernels_per_step(b2n_net* net, long long batch, int* n);
+/* fit (network.hpp:488-511) over a dataset held in device memory: images (n x prod(input)),
+ * int class ids (validated like data.hpp:257-260, ELABEL). Batches follow BatchIterator's order
+ * (data.hpp:224-238: std::shuffle with mt19937(net seed), reshuffled with seed + epoch) and are
+ * gathered on the device; one host synchronisation per epoch. Per epoch: loss (mean row loss),
+ * accuracy (evaluate over the training set) and the batch-loop wall time. Arrays hold `epochs`
+ * entries. */
+int b2n_net_fit(b2n_net* net, const float* images_host, const int* labels_host, long long n, int epochs,
+                double* loss_out, double* accuracy_out, double* seconds_out);
+/* evaluate (network.hpp:474-484): fraction of rows whose first-max class equals the label,
+ * forward_batch in net.batch_size chunks in dataset order */
+int b2n_net_evaluate(b2n_net* net, const float* images_host, const int* labels_host, long long n,
+                     double* accuracy);
+/* BatchIterator's sample order for epoch `epoch` (0 = construction shuffle) */
+int b2n_batch_order(long long n, unsigned seed, int epoch, long long* order_out);
 /* Per-op device time of the planned step (un-graphed launches, CUDA events between ops), averaged
  * over `steps`: stats[i*4 + {0,1,2,3}] = {ms, algorithmic FLOPs, algorithmic HBM bytes, kernels};
  * names gets the op names, newline-separated. */

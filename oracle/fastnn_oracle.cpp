@@ -511,6 +511,63 @@ void orc_net_forward(void* h, const float* x, long long B, float* probs, int* ar
         }
 }
 
+// ---------------------------------------------------------------------------- epoch level
+// BatchIterator order (data.hpp:224-238): iota, std::shuffle with mt19937(seed) at construction,
+// then mt19937(seed + e) over the current order for epoch e > 0 (network.hpp:495)
+void orc_batch_order(long long N, unsigned seed, int epoch, long long* out) {
+    std::vector<size_t> o((size_t)N);
+    for (size_t i = 0; i < o.size(); ++i) o[i] = i;
+    for (int e = 0; e <= epoch; ++e) {
+        std::mt19937 rng(e == 0 ? seed : seed + (unsigned)e);
+        std::shuffle(o.begin(), o.end(), rng);
+    }
+    for (size_t i = 0; i < o.size(); ++i) out[i] = (long long)o[i];
+}
+
+// evaluate (network.hpp:474-484): argmax over forward_batch chunks of `batch` in dataset order
+double orc_net_evaluate(void* h, const float* images, const int* labels, long long N, long long batch) {
+    Net& net = *static_cast<Net*>(h);
+    size_t per = 1;
+    for (size_t e : net.input) per *= e;
+    std::vector<int> am((size_t)batch);
+    size_t correct = 0;
+    for (long long lo = 0; lo < N; lo += batch) {
+        const long long n = std::min(batch, N - lo);
+        orc_net_forward(h, images + (size_t)lo * per, n, nullptr, am.data());
+        for (long long r = 0; r < n; ++r) correct += am[(size_t)r] == labels[lo + r];
+    }
+    return (double)correct / (double)N;
+}
+
+// fit (network.hpp:488-511): per epoch, loss_sum += train_minibatch * count over the shuffled
+// batches, loss = loss_sum / N, accuracy = evaluate(train)
+void orc_net_fit(void* h, const float* images, const int* labels, long long N, long long batch, unsigned seed,
+                 int epochs, double* loss_out, double* acc_out) {
+    Net& net = *static_cast<Net*>(h);
+    size_t per = 1;
+    for (size_t e : net.input) per *= e;
+    std::vector<long long> order((size_t)N);
+    std::vector<float> x;
+    std::vector<int> y;
+    for (int e = 0; e < epochs; ++e) {
+        orc_batch_order(N, seed, e, order.data());
+        double loss_sum = 0.0;
+        for (long long pos = 0; pos < N; pos += batch) {
+            const long long n = std::min(batch, N - pos);
+            x.resize((size_t)n * per);
+            y.resize((size_t)n);
+            for (long long r = 0; r < n; ++r) {
+                const long long src = order[(size_t)(pos + r)];
+                std::memcpy(x.data() + (size_t)r * per, images + (size_t)src * per, per * sizeof(float));
+                y[(size_t)r] = labels[src];
+            }
+            loss_sum += orc_net_train_minibatch(h, x.data(), y.data(), n) * (double)n;
+        }
+        loss_out[e] = loss_sum / (double)N;
+        acc_out[e] = orc_net_evaluate(h, images, labels, N, batch);
+    }
+}
+
 // ---------------------------------------------------------------------------- op level
 // gemm (gemm.hpp:225-229): C = op(A) . op(B), dense row-major operands
 void orc_gemm(int ta, int tb, const float* A, const float* B, float* C, long long M, long long N, long long K) {

@@ -71,6 +71,11 @@ def _declare(lib: C.CDLL, prefix: str) -> None:
     g = getattr(lib, f"{p}_gemm")
     g.argtypes = [C.c_int, C.c_int, _F, _F, _F, C.c_longlong, C.c_longlong, C.c_longlong]
     getattr(lib, f"{p}_sgd_momentum_step").argtypes = [_F, _F, _F, C.c_longlong, C.c_float, C.c_float, C.c_float]
+    getattr(lib, f"{p}_batch_order").argtypes = [C.c_longlong, C.c_uint, C.c_int, _LL]
+    getattr(lib, f"{p}_net_fit").argtypes = [C.c_void_p, _F, _I, C.c_longlong, C.c_longlong, C.c_uint, C.c_int,
+                                             _D, _D]
+    getattr(lib, f"{p}_net_evaluate").argtypes = [C.c_void_p, _F, _I, C.c_longlong, C.c_longlong]
+    getattr(lib, f"{p}_net_evaluate").restype = C.c_double
     getattr(lib, f"{p}_rbm_init").argtypes = [C.c_longlong, C.c_longlong, C.c_uint, _F]
     if p == "orc":
         lib.orc_net_set_hparams.argtypes = [C.c_void_p, C.c_float, C.c_float, C.c_float]
@@ -222,6 +227,30 @@ class Net:
         am = np.zeros(B, np.int32)
         getattr(self.lib, f"{self.p}_net_forward")(self.h, fptr(x), B, fptr(probs), iptr(am))
         return probs, am
+
+
+    def fit(self, x: np.ndarray, labels: np.ndarray, batch: int, seed: int, epochs: int):
+        """fit (network.hpp:488-511): per-epoch (loss, train accuracy)"""
+        x = np.ascontiguousarray(x, np.float32)
+        labels = np.ascontiguousarray(labels, np.int32)
+        loss = np.zeros(epochs, np.float64)
+        acc = np.zeros(epochs, np.float64)
+        getattr(self.lib, f"{self.p}_net_fit")(self.h, fptr(x), iptr(labels), labels.shape[0], batch, seed, epochs,
+                                               dptr(loss), dptr(acc))
+        return loss, acc
+
+    def evaluate(self, x: np.ndarray, labels: np.ndarray, batch: int) -> float:
+        x = np.ascontiguousarray(x, np.float32)
+        labels = np.ascontiguousarray(labels, np.int32)
+        return getattr(self.lib, f"{self.p}_net_evaluate")(self.h, fptr(x), iptr(labels), labels.shape[0], batch)
+
+
+def batch_order(n: int, seed: int, epoch: int, which: str = "oracle") -> np.ndarray:
+    """BatchIterator's sample order (data.hpp:224-238) for epoch `epoch`"""
+    lib = load(which)
+    out = np.zeros(n, np.int64)
+    getattr(lib, f"{'orc' if which == 'oracle' else 'ref'}_batch_order")(n, seed, epoch, out.ctypes.data_as(_LL))
+    return out
 
 
 def gemm(ta: bool, tb: bool, a: np.ndarray, b: np.ndarray, which: str = "oracle") -> np.ndarray:

@@ -229,6 +229,19 @@ bool build_composite(RefNet& rn, const std::vector<long long>& input, const orc_
     return true;
 }
 
+Dataset make_dataset(const RefNet& rn, const float* images, const int* labels, long long N) {
+    Dataset ds;
+    const std::vector<long long>& in = rn.net.input;
+    std::vector<long long> dims{N};
+    if (in.size() == 1) dims.insert(dims.end(), {1, 1, in[0]});
+    else dims.insert(dims.end(), in.begin(), in.end());
+    ds.images = make_tensor(dims);
+    copy_in(ds.images, images);
+    ds.labels.assign(labels, labels + N);
+    ds.num_classes = (size_t)rn.classes;
+    return ds;
+}
+
 }  // namespace
 
 extern "C" {
@@ -349,6 +362,36 @@ void ref_free_batch(void* b) { delete static_cast<std::pair<Tensor, Tensor>*>(b)
 double ref_net_train_prepared(void* h, void* batch) {
     auto* pair = static_cast<std::pair<Tensor, Tensor>*>(batch);
     return train_minibatch(static_cast<RefNet*>(h)->net, pair->first, pair->second);
+}
+
+// BatchIterator::order() after construction (epoch 0) and `epoch` reshuffles (data.hpp:224-238)
+void ref_batch_order(long long N, unsigned seed, int epoch, long long* out) {
+    Dataset ds;
+    ds.images = make_tensor({N, 1, 1, 1});
+    ds.labels.assign((size_t)N, 0);
+    BatchIterator it(ds, 1, seed);
+    for (int e = 1; e <= epoch; ++e) it.reshuffle(seed + (unsigned)e);
+    for (size_t i = 0; i < it.order().size(); ++i) out[i] = (long long)it.order()[i];
+}
+
+// the reference's own fit (network.hpp:488-511) with the net's batch size / seed overridden
+void ref_net_fit(void* h, const float* images, const int* labels, long long N, long long batch, unsigned seed,
+                 int epochs, double* loss_out, double* acc_out) {
+    RefNet& rn = *static_cast<RefNet*>(h);
+    rn.net.batch_size = (size_t)batch;
+    rn.net.seed = seed;
+    Dataset ds = make_dataset(rn, images, labels, N);
+    TrainReport rep = fit(rn.net, ds, (size_t)epochs);
+    for (int e = 0; e < epochs; ++e) {
+        loss_out[e] = rep.epochs[(size_t)e].loss;
+        acc_out[e] = rep.epochs[(size_t)e].accuracy;
+    }
+}
+
+double ref_net_evaluate(void* h, const float* images, const int* labels, long long N, long long batch) {
+    RefNet& rn = *static_cast<RefNet*>(h);
+    rn.net.batch_size = (size_t)batch;
+    return evaluate(rn.net, make_dataset(rn, images, labels, N));
 }
 
 void ref_net_forward(void* h, const float* x, long long B, float* probs, int* argmax) {

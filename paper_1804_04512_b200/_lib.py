@@ -90,6 +90,9 @@ _SIGS = {
     "b2n_net_stage": ([_VP, _F, _I, C.c_longlong], C.c_int),
     "b2n_net_run_staged": ([_VP, C.c_int, C.c_longlong], C.c_int),
     "b2n_net_loss": ([_VP, _D], C.c_int),
+    "b2n_net_fit": ([_VP, _F, _I, C.c_longlong, C.c_int, _D, _D, _D], C.c_int),
+    "b2n_net_evaluate": ([_VP, _F, _I, C.c_longlong, _D], C.c_int),
+    "b2n_batch_order": ([C.c_longlong, C.c_uint, C.c_int, _LL], C.c_int),
     "b2n_net_stream": ([_VP, C.POINTER(_VP)], C.c_int),
     "b2n_net_kernels_per_step": ([_VP, C.c_longlong, _I], C.c_int),
     "b2n_net_profile": ([_VP, C.c_longlong, C.c_int, C.c_int, _D, C.c_char_p, C.c_int, _I], C.c_int),

@@ -152,6 +152,28 @@ int b2n_net_stage(b2n_net* net, const float* x, const int* labels, long long bat
 int b2n_net_run_staged(b2n_net* net, int steps, long long batch_global) {
     return guard([&] { net->impl.run_staged(steps, batch_global); });
 }
+int b2n_net_fit(b2n_net* net, const float* images, const int* labels, long long n, int epochs, double* loss_out,
+                double* accuracy_out, double* seconds_out) {
+    return guard([&] {
+        auto st = net->impl.fit(images, labels, n, epochs);
+        for (size_t e = 0; e < st.size(); ++e) {
+            if (loss_out) loss_out[e] = st[e].loss;
+            if (accuracy_out) accuracy_out[e] = st[e].accuracy;
+            if (seconds_out) seconds_out[e] = st[e].seconds;
+        }
+    });
+}
+int b2n_net_evaluate(b2n_net* net, const float* images, const int* labels, long long n, double* accuracy) {
+    return guard([&] { *accuracy = net->impl.evaluate(images, labels, n); });
+}
+int b2n_batch_order(long long n, unsigned seed, int epoch, long long* order_out) {
+    return guard([&] {
+        if (n < 1) throw b2n::Error(B2N_EPARAM, "batch_iterator: empty dataset");
+        std::vector<long long> o;
+        b2n::batch_order(o, n, seed, epoch);
+        std::copy(o.begin(), o.end(), order_out);
+    });
+}
 int b2n_net_loss(b2n_net* net, double* loss) {
     return guard([&] { *loss = net->impl.loss(); });
 }

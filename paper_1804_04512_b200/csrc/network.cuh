@@ -14,6 +14,8 @@
 // mirror that layout, which makes the data-parallel allreduce a single NCCL call and the optimizer
 // one vectorised pass.
 #pragma once
+#include <algorithm>
+#include <chrono>
 #include <functional>
 #include <string>
 #include <map>
@@ -122,6 +124,70 @@ inline long long numel(const std::vector<long long>& s) {
     return n;
 }
 
+// ---- device-resident epoch loop (fit / evaluate, network.hpp:474-511, data.hpp:243-266): the dataset
+// lives in HBM, each batch is gathered on the device in the shuffled order, and a device-side batch
+// cursor lets one CUDA graph (gather + step + loss / accuracy accumulation) be relaunched per batch
+// with no host synchronisation inside an epoch.
+struct FitState {
+    long long pos;          // first order index of the next batch
+    double loss_sum;        // sum of per-row losses of the epoch (network.hpp:500)
+    unsigned long long correct;  // evaluate(): rows whose argmax equals the label
+};
+
+static __global__ void fit_gather_kernel(const float* __restrict__ ds, long long per, const int* __restrict__ ds_y,
+                                         const int* __restrict__ order, const FitState* st, int count,
+                                         float* __restrict__ X, long long ldx, int* __restrict__ labels) {
+    pdl_wait();
+    const long long pos = st->pos;
+    const bool vec = (per & 3) == 0 && (ldx & 3) == 0;
+    const long long n = (long long)count * (vec ? per / 4 : per);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        if (vec) {
+            const long long r = i / (per / 4), c = i - r * (per / 4);
+            const long long src = order[pos + r];
+            reinterpret_cast<float4*>(X + r * ldx)[c] = __ldg(reinterpret_cast<const float4*>(ds + src * per) + c);
+        } else {
+            const long long r = i / per, c = i - r * per;
+            X[r * ldx + c] = __ldg(ds + order[pos + r] * per + c);
+        }
+    }
+    if (blockIdx.x == 0)
+        for (int r = threadIdx.x; r < count; r += blockDim.x) labels[r] = ds_y[order[pos + r]];
+}
+
+// after a training step: loss_sum += sum of the batch's row losses in row order; advance the cursor
+static __global__ void fit_advance_kernel(const double* __restrict__ row_loss, int count, FitState* st, int eval,
+                                          const int* __restrict__ argmax, const int* __restrict__ labels) {
+    pdl_wait();
+    if (threadIdx.x != 0) return;
+    if (eval) {
+        unsigned long long c = 0;
+        for (int r = 0; r < count; ++r) c += argmax[r] == labels[r];
+        st->correct += c;
+    } else {
+        double s = 0.0;
+        for (int r = 0; r < count; ++r) s += row_loss[r];
+        st->loss_sum += s;
+    }
+    st->pos += count;
+}
+
+// BatchIterator's order (data.hpp:224-238): iota, then std::shuffle with mt19937(seed) at construction
+// and mt19937(seed + epoch) on the current order for every later epoch (network.hpp:495)
+inline void batch_order(std::vector<long long>& order, long long N, unsigned seed, int epoch) {
+    std::vector<std::size_t> o((size_t)N);
+    for (long long i = 0; i < N; ++i) o[(size_t)i] = (std::size_t)i;
+    {
+        std::mt19937 rng(seed);
+        std::shuffle(o.begin(), o.end(), rng);
+    }
+    for (int e = 1; e <= epoch; ++e) {
+        std::mt19937 rng(seed + (unsigned)e);
+        std::shuffle(o.begin(), o.end(), rng);
+    }
+    order.assign(o.begin(), o.end());
+}
+
 class Net {
   public:
     struct Layer {
@@ -170,6 +236,13 @@ class Net {
     void apply_update();
     void forward(const float* x, long long B, float* probs, int* argmax);
     void stage(const float* x, const int* labels, long long B);
+    struct FitEpoch {
+        double loss, accuracy, seconds;
+    };
+    // fit (network.hpp:488-511): `epochs` shuffled passes over a dataset of N samples held in HBM;
+    // per-epoch mean loss, train accuracy (evaluate) and batch-loop wall time
+    std::vector<FitEpoch> fit(const float* images, const int* labels, long long N, int epochs);
+    double evaluate(const float* images, const int* labels, long long N);  // network.hpp:474-484
     void run_staged(int steps, long long Bg);
     double loss();
     int kernels_per_step(long long B);
@@ -190,12 +263,12 @@ class Net {
     long long packed_floats() const { return n_packed_; }
 
   private:
-    enum Mode { FUSED = 0, SPLIT = 1, FWD = 2, SPLIT_APPLY = 3 };
+    enum Mode { FUSED = 0, SPLIT = 1, FWD = 2, SPLIT_APPLY = 3, FIT = 4, EVAL = 5 };
     struct Plan {
         long long B = 0, Bg = 0;
-        std::vector<Op> ops[4];
-        cudaGraphExec_t graph[4] = {nullptr, nullptr, nullptr, nullptr};
-        int nkernels[4] = {0, 0, 0, 0};
+        std::vector<Op> ops[6];
+        cudaGraphExec_t graph[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+        int nkernels[6] = {0, 0, 0, 0, 0, 0};
         ~Plan() {
             for (auto& g : graph)
                 if (g) cudaGraphExecDestroy(g);
@@ -238,6 +311,13 @@ class Net {
     std::unique_ptr<DpComm> dp_;
     DevMem loss_sum_;  // dp: double partial loss
     bool tconv_ = false;     // conv layers on the halo-tile kernels (convt.cuh) instead of conv.cuh
+    DevMem ds_x_, ds_y_, ds_order_, fit_state_;  // device-resident dataset, order, cursor / sums
+    long long ds_n_ = 0;
+    unsigned seed_ = 0;
+    long long batch_size_ = 1;
+    void upload_dataset(const float* images, const int* labels, long long N);
+    void build_fit_ops(Plan& pl, int mode);
+    double run_epoch_eval(long long N);
     float* Xb_ = nullptr;    // row-blocked copy of a conv network's input
     long long xb_bstride_ = 0;
     TLayout out_layout(const Layer& L, float* p, long long ld) const {
@@ -255,6 +335,8 @@ class Net {
 // --------------------------------------------------------------------------- construction
 inline Net::Net(const b2n_network_spec& spec, int device, int precision)
     : device_(device), x3_(precision == B2N_TF32X3), lr_(spec.lr), mom_(spec.momentum), wd_(spec.weight_decay) {
+    seed_ = spec.seed;
+    batch_size_ = spec.batch_size;
     // validation mirrors build_network (network.hpp:285-300, :303-367)
     if (spec.n_layers < 1 || !spec.layers) throw Error(B2N_ESPEC, "network spec has no layers");
     if (spec.input_rank != 1 && spec.input_rank != 3)
@@ -903,6 +985,126 @@ inline double Net::loss() { return read_loss(last_B_) / (double)(last_Bg_ ? last
 inline int Net::kernels_per_step(long long B) {
     Plan& pl = plan_for(B, B);
     return dp_ ? pl.nkernels[SPLIT] + pl.nkernels[SPLIT_APPLY] : pl.nkernels[lr_ != 0.0f ? FUSED : SPLIT];
+}
+
+// --------------------------------------------------------------------------- fit / evaluate
+inline void Net::upload_dataset(const float* images, const int* labels, long long N) {
+    const long long per = numel(input_);
+    for (long long r = 0; r < N; ++r)  // data.hpp:257-260 (BatchIterator::next)
+        if (labels[r] < 0 || labels[r] >= classes_)
+            throw Error(B2N_ELABEL, "batch_iterator: label " + std::to_string(labels[r]) + " outside [0, " +
+                                        std::to_string(classes_) + ")");
+    bool moved = false;  // the FIT / EVAL graphs bake these addresses in
+    if (ds_x_.bytes < (size_t)(N * per * 4)) ds_x_.alloc((size_t)(N * per * 4)), moved = true;
+    if (ds_y_.bytes < (size_t)(N * 4)) ds_y_.alloc((size_t)(N * 4)), moved = true;
+    if (ds_order_.bytes < (size_t)(N * 4)) ds_order_.alloc((size_t)(N * 4)), moved = true;
+    if (!fit_state_.p) fit_state_.alloc(sizeof(FitState)), moved = true;
+    if (moved)
+        for (auto& kv : plans_)
+            for (int m : {FIT, EVAL}) {
+                kv.second->ops[m].clear();
+                if (kv.second->graph[m]) cudaGraphExecDestroy(kv.second->graph[m]);
+                kv.second->graph[m] = nullptr;
+            }
+    B2N_CUDA(cudaMemcpyAsync(ds_x_.p, images, (size_t)(N * per * 4), cudaMemcpyHostToDevice, stream_));
+    B2N_CUDA(cudaMemcpyAsync(ds_y_.p, labels, (size_t)(N * 4), cudaMemcpyHostToDevice, stream_));
+    ds_n_ = N;
+}
+
+// FIT: gather -> training step -> loss sum + cursor; EVAL: gather -> forward -> correct count + cursor
+inline void Net::build_fit_ops(Plan& pl, int mode) {
+    const int count = (int)pl.B;
+    const long long per = numel(input_);
+    const float* ds = ds_x_.as<float>();
+    const int* dy = ds_y_.as<int>();
+    const int* ord = ds_order_.as<int>();
+    FitState* st = fit_state_.as<FitState>();
+    float* X = X_;
+    long long ldx = ldx_;
+    int* lab = labels_;
+    std::vector<Op> ops;
+    ops.push_back(Op([=](cudaStream_t s) {
+        const long long n = (long long)count * per / 4 + 1;
+        launch_ex(fit_gather_kernel, dim3(grid_for(n)), dim3(256), 0, s, 1u, ds, per, dy, ord, (const FitState*)st, count,
+                  X, ldx, lab);
+    }, "fit.gather", 0.0, (double)count * per * 8));
+    const std::vector<Op>& body = pl.ops[mode == FIT ? (lr_ != 0.0f ? FUSED : SPLIT) : FWD];
+    ops.insert(ops.end(), body.begin(), body.end());
+    const double* rl = row_loss_;
+    const int* am = argmax_;
+    const int eval = mode == EVAL;
+    ops.push_back(Op([=](cudaStream_t s) {
+        launch_ex(fit_advance_kernel, dim3(1), dim3(32), 0, s, 1u, rl, count, st, eval, am, (const int*)lab);
+    }, "fit.advance", 0.0, (double)count * 16));
+    assign_prefetch(ops);
+    pl.ops[mode] = ops;
+    int n = 0;
+    for (const Op& o : ops) n += o.kernels;
+    pl.nkernels[mode] = n;
+}
+
+inline double Net::run_epoch_eval(long long N) {
+    B2N_CUDA(cudaMemsetAsync(fit_state_.p, 0, sizeof(FitState), stream_));
+    const long long B = batch_size_;  // network.hpp:477
+    for (long long pos = 0; pos < N; pos += B) {
+        const long long count = std::min(B, N - pos);
+        Plan& pl = plan_for(count, count);
+        if (pl.ops[EVAL].empty()) build_fit_ops(pl, EVAL);
+        launch(pl, EVAL);
+    }
+    FitState h;
+    B2N_CUDA(cudaMemcpyAsync(&h, fit_state_.p, sizeof(FitState), cudaMemcpyDeviceToHost, stream_));
+    spin_sync(stream_);
+    return (double)h.correct / (double)N;
+}
+
+inline std::vector<Net::FitEpoch> Net::fit(const float* images, const int* labels, long long N, int epochs) {
+    const unsigned seed = seed_;  // BatchIterator(train, net.batch_size, net.seed)
+    if (N < 1) throw Error(B2N_EPARAM, "fit: empty dataset");
+    if (epochs < 1) throw Error(B2N_EPARAM, "fit: epochs must be >= 1");
+    if (dp_) throw Error(B2N_EPARAM, "fit: data-parallel nets step through forward_backward + apply_update");
+    check_train_params();
+    const long long B = batch_size_;  // network.hpp:494
+    ensure_capacity(B);
+    upload_dataset(images, labels, N);
+    std::vector<long long> order;
+    std::vector<int> order32((size_t)N);
+    std::vector<FitEpoch> out;
+    for (int e = 0; e < epochs; ++e) {
+        batch_order(order, N, seed, e);
+        for (long long i = 0; i < N; ++i) order32[(size_t)i] = (int)order[(size_t)i];
+        B2N_CUDA(cudaMemcpyAsync(ds_order_.p, order32.data(), (size_t)N * 4, cudaMemcpyHostToDevice, stream_));
+        B2N_CUDA(cudaMemsetAsync(fit_state_.p, 0, sizeof(FitState), stream_));
+        spin_sync(stream_);  // the order buffer is a pageable host copy: complete before it changes
+        const auto t0 = std::chrono::steady_clock::now();
+        for (long long pos = 0; pos < N; pos += B) {
+            const long long count = std::min(B, N - pos);
+            Plan& pl = plan_for(count, count);
+            if (pl.ops[FIT].empty()) build_fit_ops(pl, FIT);
+            launch(pl, FIT);
+        }
+        FitState h;
+        B2N_CUDA(cudaMemcpyAsync(&h, fit_state_.p, sizeof(FitState), cudaMemcpyDeviceToHost, stream_));
+        spin_sync(stream_);
+        const auto t1 = std::chrono::steady_clock::now();
+        FitEpoch fe;
+        fe.loss = h.loss_sum / (double)N;
+        fe.seconds = std::chrono::duration<double>(t1 - t0).count();
+        fe.accuracy = run_epoch_eval(N);  // evaluate(net, train) over the same resident data, in order
+        out.push_back(fe);
+    }
+    return out;
+}
+
+inline double Net::evaluate(const float* images, const int* labels, long long N) {
+    if (N < 1) throw Error(B2N_EPARAM, "evaluate: empty dataset");
+    ensure_capacity(batch_size_);
+    upload_dataset(images, labels, N);
+    std::vector<int> iota((size_t)N);
+    for (long long i = 0; i < N; ++i) iota[(size_t)i] = (int)i;
+    B2N_CUDA(cudaMemcpyAsync(ds_order_.p, iota.data(), (size_t)N * 4, cudaMemcpyHostToDevice, stream_));
+    spin_sync(stream_);
+    return run_epoch_eval(N);
 }
 
 // --------------------------------------------------------------------------- params

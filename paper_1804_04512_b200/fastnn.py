@@ -9,6 +9,7 @@ Same names, argument meaning and error types as the reference, backed by the B20
     loss = train_minibatch(net, x, y_onehot)       # network.hpp:463
     probs = forward_batch(net, x)                  # network.hpp:402
     acc = evaluate(net, images, labels)            # network.hpp:474
+    report = fit(net, images, labels, epochs)      # network.hpp:488
     rbm = Rbm(500, 784); rbm.init(seed)            # energy.hpp:16-32
     recon = cd_k_update(rbm, v0, 1, lr, uniforms)  # energy.hpp:131
 """
@@ -257,18 +258,64 @@ def forward_batch(net: Network, x, return_argmax: bool = False):
     return (probs, am) if return_argmax else probs
 
 
+def _dataset(net: Network, images, labels):
+    x = _flat_batch(net, images)
+    lab = np.ascontiguousarray(labels, np.int32)
+    if lab.ndim != 1 or lab.shape[0] != x.shape[0]:
+        raise ShapeError("dataset: need one label per image")
+    if x.shape[0] == 0:
+        raise Error("empty dataset")
+    return x, lab
+
+
 def evaluate(net: Network, images, labels) -> float:
-    """fastnn::evaluate (network.hpp:474-484): batched inference, first-max argmax accuracy."""
-    images = np.asarray(images, np.float32)
-    labels = np.asarray(labels)
-    if images.shape[0] == 0:
-        raise Error("evaluate: empty dataset")
-    correct = 0
-    for lo in range(0, images.shape[0], net.batch_size):
-        hi = min(lo + net.batch_size, images.shape[0])
-        _, am = forward_batch(net, images[lo:hi], return_argmax=True)
-        correct += int((am == labels[lo:hi]).sum())
-    return correct / images.shape[0]
+    """fastnn::evaluate (network.hpp:474-484): forward_batch in net.batch_size chunks over the
+    device-resident dataset, first-max argmax accuracy counted on the device."""
+    x, lab = _dataset(net, images, labels)
+    out = C.c_double()
+    _lib.call("b2n_net_evaluate", net.handle, _f(x), _i(lab), x.shape[0], C.byref(out))
+    return out.value
+
+
+@dataclass
+class EpochStats:
+    """fastnn::EpochStats (network.hpp:255-259)"""
+    loss: float = 0.0
+    accuracy: float = 0.0
+    seconds: float = 0.0
+
+
+@dataclass
+class TrainReport:
+    """fastnn::TrainReport (network.hpp:261-265)"""
+    epochs: list = field(default_factory=list)
+    test_accuracy: float = -1.0
+    total_batches: int = 0
+
+
+def fit(net: Network, images, labels, epochs: int, test=None) -> TrainReport:
+    """fastnn::fit (network.hpp:488-511): `epochs` passes in BatchIterator order (net.seed,
+    reshuffled with seed + epoch), the dataset resident in HBM and each batch gathered on the
+    device; per-epoch mean loss, train accuracy and batch-loop seconds. `test` = (images, labels)."""
+    x, lab = _dataset(net, images, labels)
+    if epochs < 1:
+        raise ParamError("fit: epochs must be >= 1")
+    loss = np.zeros(epochs)
+    acc = np.zeros(epochs)
+    sec = np.zeros(epochs)
+    _lib.call("b2n_net_fit", net.handle, _f(x), _i(lab), x.shape[0], epochs, _d(loss), _d(acc), _d(sec))
+    rep = TrainReport([EpochStats(float(a), float(b), float(c)) for a, b, c in zip(loss, acc, sec)])
+    rep.total_batches = epochs * -(-x.shape[0] // net.batch_size)
+    if test is not None:
+        rep.test_accuracy = evaluate(net, *test)
+    return rep
+
+
+def batch_order(n: int, seed: int, epoch: int = 0) -> np.ndarray:
+    """BatchIterator's sample order (data.hpp:224-238) for epoch `epoch` of fit()."""
+    out = np.zeros(n, np.int64)
+    _lib.call("b2n_batch_order", n, seed, epoch, out.ctypes.data_as(C.POINTER(C.c_longlong)))
+    return out
 
 
 class Rbm:

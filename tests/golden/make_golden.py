@@ -7,6 +7,7 @@ oracle/ref_shim.cpp): build_network / train_minibatch (network.hpp:284, :463), g
 padded ImageNet-shaped net, the SURVEY 8(c) composite of reference primitives.
 
     python tests/golden/make_golden.py        # writes tests/golden/*.npz and full_size.json
+    python tests/golden/make_golden.py fit    # only fit.npz (fit / evaluate / batch order)
 """
 from __future__ import annotations
 
@@ -68,7 +69,39 @@ def net_case(spec, B, steps=2):
     return out
 
 
+FIT_CASES = {  # name -> (small spec, dataset size, batch size, epochs); N % batch != 0 on purpose
+    "mlp_small": (250, 32, 3),
+    "mnist_cnn_small": (90, 20, 2),
+}
+
+
+def fit_cases():
+    """fit / evaluate / BatchIterator order (network.hpp:474-511, data.hpp:224-266) from the reference."""
+    out = {}
+    for N, seed in [(250, 42), (90, 7), (1000, 3)]:
+        for e in range(3):
+            out[f"order_{N}_{seed}_{e}"] = O.batch_order(N, seed, e, "ref")
+    specs = small_specs()
+    for name, (N, B, epochs) in FIT_CASES.items():
+        spec = specs[name][0]
+        per = int(np.prod(spec["input"]))
+        x = O.uniform_f32(201, N * per).reshape([N] + spec["input"])
+        lab = O.uniform_int(202, 0, 9, N)
+        ref = O.Net(spec, "ref")
+        out[f"{name}_x"], out[f"{name}_labels"] = x, lab
+        out[f"{name}_acc0"] = np.array([ref.evaluate(x, lab, B)])
+        loss, acc = ref.fit(x, lab, B, spec["seed"], epochs)
+        out[f"{name}_loss"], out[f"{name}_acc"] = loss, acc
+        for i in range(ref.num_params()):
+            out[f"{name}_final{i}"] = ref.get(i)
+    np.savez_compressed(HERE / "fit.npz", **out)
+
+
 def main():
+    if sys.argv[1:] == ["fit"]:
+        fit_cases()
+        print("fit fixtures written to", HERE)
+        return
     assert O.ref_available(), "build oracle/_ref first (make -C oracle) -- needs /root/reference"
     meta = {}
     rng = np.random.default_rng(2024)
@@ -129,6 +162,7 @@ def main():
                    "bv_sum": float(np.sum(bv1.astype(np.float64))), "bh_sum": float(np.sum(bh1.astype(np.float64)))}
     (HERE / "full_size.json").write_text(json.dumps(full, indent=1))
     (HERE / "meta.json").write_text(json.dumps(meta, indent=1))
+    fit_cases()
     print("golden fixtures written to", HERE)
 
 
