@@ -406,6 +406,34 @@ def cpu_reference(name: str, budget_s: float, min_steps: int = 2, max_steps: int
 
 
 # ----------------------------------------------------------------------------- main
+def fit_epochs(dev, precision):
+    """SURVEY 8(f)1-2: one fastnn::fit epoch (network.hpp:488-511) over a synthetic dataset of the
+    real dataset's size held in HBM (MNIST 60000, CIFAR-10 50000), through the public fit() API;
+    samples/s from the epoch's batch-loop seconds as the reference reports them, plus the
+    evaluate() pass fit runs afterwards."""
+    from paper_1804_04512_b200 import configs as CF, fastnn as F
+    out = {}
+    for name, N in [("mlp", 60000), ("mnist_cnn", 60000), ("cifar_cnn", 50000)]:
+        try:
+            spec = CF.NET_CONFIGS[name]()
+            rng = np.random.default_rng(3)
+            x = rng.random((N, *spec["input"]), dtype=np.float32)
+            lab = rng.integers(0, 10, N).astype(np.int32)
+            net = F.build_network(spec, device=dev, precision=precision)
+            F.fit(net, x[:spec["batch_size"] * 4], lab[:spec["batch_size"] * 4], 1)  # plans + graphs
+            t0 = time.perf_counter()
+            rep = F.fit(net, x, lab, 2)
+            wall = time.perf_counter() - t0
+            ep = rep.epochs[-1]
+            out[name] = {"samples": N, "batch": spec["batch_size"], "epoch_s": round(ep.seconds, 5),
+                         "samples_per_s": round(N / ep.seconds, 1), "loss": round(ep.loss, 5),
+                         "train_accuracy": ep.accuracy, "fit_wall_s_2_epochs_incl_upload_and_eval": round(wall, 4)}
+            del net
+        except Exception as ex:
+            out[name] = {"unavailable": f"{type(ex).__name__}: {ex}"[:200]}
+    return out
+
+
 def main():
     a = parse()
     dist = Dist()
@@ -497,6 +525,8 @@ def main():
             except Exception as ex:  # a config the build does not cover yet is reported, not hidden
                 others[name] = {"unavailable": f"{type(ex).__name__}: {ex}"[:200]}
         line["other_configs"] = others
+    if dist.world == 1 and not a.no_others:
+        line["fit_epoch"] = fit_epochs(dev, precision)
     if dist.rank == 0 and dist.world == 1:
         v, info = cpu_reference(a.config, a.cpu_budget)
         line["cpu_baseline"] = {"value": round(v, 2), "unit": "samples/s", "cores": info["cores"],
