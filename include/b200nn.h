@@ -32,7 +32,12 @@ enum {
     B2N_EOOM = 6,    /* device allocation failure */
     B2N_ESPEC = 7,   /* SpecError    */
     B2N_EBOUNDS = 8, /* BoundsError  */
-    B2N_EINTERNAL = 9
+    B2N_EINTERNAL = 9,
+    B2N_EFORMAT = 10, /* FormatError: malformed / mismatched checkpoint */
+    B2N_ELENGTH = 11, /* LengthError: checkpoint truncated */
+    B2N_EIO = 12,     /* DataMissingError: file cannot be opened / written */
+    B2N_ECONSISTENCY = 13, /* ConsistencyError: e.g. a dataset label outside [0, classes) */
+    B2N_EDATA = 14         /* DataError: e.g. an empty dataset */
 };
 
 /* fastnn::LayerDesc::Kind numbering (network.hpp:195) */
@@ -128,7 +133,7 @@ int b2n_net_loss(b2n_net* net, double* loss);
 int b2n_net_stream(b2n_net* net, void** cuda_stream);
 int b2n_net_kernels_per_step(b2n_net* net, long long batch, int* n);
 /* fit (network.hpp:488-511) over a dataset held in device memory: images (n x prod(input)),
- * int class ids (validated like data.hpp:257-260, ELABEL). Batches follow BatchIterator's order
+ * int class ids (validated like data.hpp:257-260, ECONSISTENCY; empty dataset EDATA). Batches follow BatchIterator's order
  * (data.hpp:224-238: std::shuffle with mt19937(net seed), reshuffled with seed + epoch) and are
  * gathered on the device; one host synchronisation per epoch. Per epoch: loss (mean row loss),
  * accuracy (evaluate over the training set) and the batch-loop wall time. Arrays hold `epochs`
@@ -141,6 +146,13 @@ int b2n_net_evaluate(b2n_net* net, const float* images_host, const int* labels_h
                      double* accuracy);
 /* BatchIterator's sample order for epoch `epoch` (0 = construction shuffle) */
 int b2n_batch_order(long long n, unsigned seed, int epoch, long long* order_out);
+/* save_network / load_network (network.hpp:552-607): the reference's FNN1 byte format, written
+ * from / read into the device-resident parameters (one packed D2H / H2D copy). with_state != 0
+ * also writes / reads the sidecar `<path>.state` holding momentum velocities and hyper-parameters
+ * for an exact resume (the reference has no such file). Errors: EIO (cannot open), ELENGTH
+ * (truncated), EFORMAT (magic, layer count, tag, tensor count / rank / extent mismatch). */
+int b2n_save_network(b2n_net* net, const char* path, int with_state);
+int b2n_load_network(b2n_net* net, const char* path, int with_state);
 /* Per-op device time of the planned step (un-graphed launches, CUDA events between ops), averaged
  * over `steps`: stats[i*4 + {0,1,2,3}] = {ms, algorithmic FLOPs, algorithmic HBM bytes, kernels};
  * names gets the op names, newline-separated. */

@@ -104,6 +104,8 @@ def _declare(lib: C.CDLL, prefix: str) -> None:
         lib.ref_rbm_step.argtypes = [C.c_void_p, C.c_float]
         lib.ref_rbm_step.restype = C.c_double
         lib.ref_rbm_destroy.argtypes = [C.c_void_p]
+        lib.ref_save_network.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int]
+        lib.ref_load_network.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int]
         lib.ref_set_threads.argtypes = [C.c_int]
         lib.ref_thread_count.restype = C.c_int
 
@@ -243,6 +245,14 @@ class Net:
         x = np.ascontiguousarray(x, np.float32)
         labels = np.ascontiguousarray(labels, np.int32)
         return getattr(self.lib, f"{self.p}_net_evaluate")(self.h, fptr(x), iptr(labels), labels.shape[0], batch)
+
+
+def ref_checkpoint(net: "Net", path: str, load: bool = False) -> str:
+    """the reference's save_network / load_network on a 'ref' net; returns '' or the error text"""
+    assert net.which == "ref"
+    err = C.create_string_buffer(512)
+    fn = net.lib.ref_load_network if load else net.lib.ref_save_network
+    return "" if fn(net.h, str(path).encode(), err, 512) == 0 else err.value.decode()
 
 
 def batch_order(n: int, seed: int, epoch: int, which: str = "oracle") -> np.ndarray:

@@ -394,6 +394,28 @@ double ref_net_evaluate(void* h, const float* images, const int* labels, long lo
     return evaluate(rn.net, make_dataset(rn, images, labels, N));
 }
 
+// the reference's own checkpoint I/O (network.hpp:552-607); returns 0 or the error text length
+int ref_save_network(void* h, const char* path, char* err, int errlen) {
+    try {
+        save_network(static_cast<RefNet*>(h)->net, path);
+    } catch (const std::exception& e) {
+        std::strncpy(err, e.what(), (size_t)errlen - 1);
+        err[errlen - 1] = 0;
+        return 1;
+    }
+    return 0;
+}
+int ref_load_network(void* h, const char* path, char* err, int errlen) {
+    try {
+        load_network(static_cast<RefNet*>(h)->net, path);
+    } catch (const std::exception& e) {
+        std::strncpy(err, e.what(), (size_t)errlen - 1);
+        err[errlen - 1] = 0;
+        return 1;
+    }
+    return 0;
+}
+
 void ref_net_forward(void* h, const float* x, long long B, float* probs, int* argmax) {
     RefNet& rn = *static_cast<RefNet*>(h);
     Tensor pred = forward_batch(rn.net, make_batch(x, B, rn.net.input));

@@ -47,8 +47,29 @@ class OutOfMemory(Error):
     pass
 
 
+class FormatError(Error):
+    """fastnn::FormatError (config.hpp): malformed or mismatched checkpoint."""
+
+
+class LengthError(Error):
+    """fastnn::LengthError (config.hpp): checkpoint truncated."""
+
+
+class DataMissingError(Error):
+    """fastnn::DataMissingError (config.hpp): a file cannot be opened or written."""
+
+
+class ConsistencyError(Error):
+    """fastnn::ConsistencyError (config.hpp): mutually inconsistent inputs."""
+
+
+class DataError(Error):
+    """fastnn::DataError (config.hpp): unusable dataset (e.g. empty)."""
+
+
 _ERRORS = {1: ShapeError, 2: ParamError, 3: LabelError, 4: CudaError, 5: NcclError, 6: OutOfMemory, 7: SpecError,
-           8: BoundsError, 9: Error}
+           8: BoundsError, 9: Error, 10: FormatError, 11: LengthError, 12: DataMissingError,
+           13: ConsistencyError, 14: DataError}
 
 _F = C.POINTER(C.c_float)
 _D = C.POINTER(C.c_double)
@@ -92,6 +113,8 @@ _SIGS = {
     "b2n_net_loss": ([_VP, _D], C.c_int),
     "b2n_net_fit": ([_VP, _F, _I, C.c_longlong, C.c_int, _D, _D, _D], C.c_int),
     "b2n_net_evaluate": ([_VP, _F, _I, C.c_longlong, _D], C.c_int),
+    "b2n_save_network": ([_VP, C.c_char_p, C.c_int], C.c_int),
+    "b2n_load_network": ([_VP, C.c_char_p, C.c_int], C.c_int),
     "b2n_batch_order": ([C.c_longlong, C.c_uint, C.c_int, _LL], C.c_int),
     "b2n_net_stream": ([_VP, C.POINTER(_VP)], C.c_int),
     "b2n_net_kernels_per_step": ([_VP, C.c_longlong, _I], C.c_int),

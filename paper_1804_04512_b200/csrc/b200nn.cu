@@ -166,6 +166,18 @@ int b2n_net_fit(b2n_net* net, const float* images, const int* labels, long long 
 int b2n_net_evaluate(b2n_net* net, const float* images, const int* labels, long long n, double* accuracy) {
     return guard([&] { *accuracy = net->impl.evaluate(images, labels, n); });
 }
+int b2n_save_network(b2n_net* net, const char* path, int with_state) {
+    return guard([&] {
+        if (!path) throw b2n::Error(B2N_EIO, "save_network: cannot open (null path)");
+        net->impl.save(path, with_state != 0);
+    });
+}
+int b2n_load_network(b2n_net* net, const char* path, int with_state) {
+    return guard([&] {
+        if (!path) throw b2n::Error(B2N_EIO, "load_network: cannot open (null path)");
+        net->impl.load(path, with_state != 0);
+    });
+}
 int b2n_batch_order(long long n, unsigned seed, int epoch, long long* order_out) {
     return guard([&] {
         if (n < 1) throw b2n::Error(B2N_EPARAM, "batch_iterator: empty dataset");

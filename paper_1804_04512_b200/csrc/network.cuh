@@ -23,6 +23,7 @@
 #include <random>
 
 #include "conv.cuh"
+#include "checkpoint.cuh"
 #include "convt.cuh"
 #include "nccl_dyn.cuh"
 #include "runtime.cuh"
@@ -243,6 +244,8 @@ class Net {
     // per-epoch mean loss, train accuracy (evaluate) and batch-loop wall time
     std::vector<FitEpoch> fit(const float* images, const int* labels, long long N, int epochs);
     double evaluate(const float* images, const int* labels, long long N);  // network.hpp:474-484
+    void save(const std::string& path, bool with_state);  // network.hpp:552-573 (+ sidecar)
+    void load(const std::string& path, bool with_state);  // network.hpp:575-607 (+ sidecar)
     void run_staged(int steps, long long Bg);
     double loss();
     int kernels_per_step(long long B);
@@ -315,6 +318,9 @@ class Net {
     long long ds_n_ = 0;
     unsigned seed_ = 0;
     long long batch_size_ = 1;
+    std::vector<int> spec_kinds_;  // the spec's layer list (checkpoint tags, network.hpp:560)
+    void gather_params(const std::vector<float>& packed, int idx, float* out) const;
+    void scatter_params(std::vector<float>& packed, int idx, const float* in) const;
     void upload_dataset(const float* images, const int* labels, long long N);
     void build_fit_ops(Plan& pl, int mode);
     double run_epoch_eval(long long N);
@@ -361,6 +367,10 @@ inline Net::Net(const b2n_network_spec& spec, int device, int precision)
     for (int i = 0; i < spec.n_layers; ++i) {
         const b2n_layer_desc& d = spec.layers[i];
         const int idx = i + 1;
+        // the reference's node list (checkpoint layer count / tags): an implicit FlattenNode before a
+        // dense layer that follows feature maps (network.hpp:309-312)
+        if (d.kind == B2N_DENSE && cur.size() == 3) spec_kinds_.push_back(B2N_FLATTEN);
+        spec_kinds_.push_back(d.kind);
         switch (d.kind) {
             case B2N_DENSE: {
                 if (cur.size() == 3) cur = {cur[0] * cur[1] * cur[2]};  // implicit flatten (network.hpp:309-312)
@@ -992,7 +1002,7 @@ inline void Net::upload_dataset(const float* images, const int* labels, long lon
     const long long per = numel(input_);
     for (long long r = 0; r < N; ++r)  // data.hpp:257-260 (BatchIterator::next)
         if (labels[r] < 0 || labels[r] >= classes_)
-            throw Error(B2N_ELABEL, "batch_iterator: label " + std::to_string(labels[r]) + " outside [0, " +
+            throw Error(B2N_ECONSISTENCY, "batch_iterator: label " + std::to_string(labels[r]) + " outside [0, " +
                                         std::to_string(classes_) + ")");
     bool moved = false;  // the FIT / EVAL graphs bake these addresses in
     if (ds_x_.bytes < (size_t)(N * per * 4)) ds_x_.alloc((size_t)(N * per * 4)), moved = true;
@@ -1060,7 +1070,7 @@ inline double Net::run_epoch_eval(long long N) {
 
 inline std::vector<Net::FitEpoch> Net::fit(const float* images, const int* labels, long long N, int epochs) {
     const unsigned seed = seed_;  // BatchIterator(train, net.batch_size, net.seed)
-    if (N < 1) throw Error(B2N_EPARAM, "fit: empty dataset");
+    if (N < 1) throw Error(B2N_EDATA, "fit: empty dataset");
     if (epochs < 1) throw Error(B2N_EPARAM, "fit: epochs must be >= 1");
     if (dp_) throw Error(B2N_EPARAM, "fit: data-parallel nets step through forward_backward + apply_update");
     check_train_params();
@@ -1097,7 +1107,7 @@ inline std::vector<Net::FitEpoch> Net::fit(const float* images, const int* label
 }
 
 inline double Net::evaluate(const float* images, const int* labels, long long N) {
-    if (N < 1) throw Error(B2N_EPARAM, "evaluate: empty dataset");
+    if (N < 1) throw Error(B2N_EDATA, "evaluate: empty dataset");
     ensure_capacity(batch_size_);
     upload_dataset(images, labels, N);
     std::vector<int> iota((size_t)N);
@@ -1105,6 +1115,113 @@ inline double Net::evaluate(const float* images, const int* labels, long long N)
     B2N_CUDA(cudaMemcpyAsync(ds_order_.p, iota.data(), (size_t)N * 4, cudaMemcpyHostToDevice, stream_));
     spin_sync(stream_);
     return run_epoch_eval(N);
+}
+
+// --------------------------------------------------------------------------- checkpoint
+inline void Net::gather_params(const std::vector<float>& packed, int idx, float* out) const {
+    const ParamView& v = params_[idx];
+    for (long long r = 0; r < v.rows; ++r)
+        for (long long c = 0; c < v.cols; ++c) out[r * v.cols + c] = packed[(size_t)(v.off + r * v.pitch + c)];
+}
+inline void Net::scatter_params(std::vector<float>& packed, int idx, const float* in) const {
+    const ParamView& v = params_[idx];
+    for (long long r = 0; r < v.rows; ++r)
+        for (long long c = 0; c < v.cols; ++c) packed[(size_t)(v.off + r * v.pitch + c)] = in[r * v.cols + c];
+}
+
+inline void Net::save(const std::string& path, bool with_state) {
+    std::vector<float> packed((size_t)n_packed_), tmp;
+    B2N_CUDA(cudaMemcpyAsync(packed.data(), P_.p, (size_t)n_packed_ * 4, cudaMemcpyDeviceToHost, stream_));
+    B2N_CUDA(cudaStreamSynchronize(stream_));
+    std::string o;
+    o.append("FNN1", 4);
+    ckpt::put_u32(o, (uint32_t)spec_kinds_.size());
+    int pi = 0;
+    auto put_tensor = [&](const std::vector<float>& src, int idx) {
+        const ParamView& v = params_[idx];
+        ckpt::put_u32(o, (uint32_t)v.dims.size());
+        for (long long e : v.dims) ckpt::put_u64(o, (uint64_t)e);
+        tmp.resize((size_t)numel(v.dims));
+        gather_params(src, idx, tmp.data());
+        ckpt::put_f32s(o, tmp.data(), tmp.size());
+    };
+    for (int kind : spec_kinds_) {
+        const std::string tag = ckpt::tag_of(kind);
+        ckpt::put_u32(o, (uint32_t)tag.size());
+        o.append(tag);
+        const int n = kind == B2N_DENSE || kind == B2N_CONV ? 2 : 0;
+        ckpt::put_u32(o, (uint32_t)n);
+        for (int t = 0; t < n; ++t) put_tensor(packed, pi++);
+    }
+    ckpt::write_file(path, o, "save_network");
+    if (!with_state) return;
+    B2N_CUDA(cudaMemcpyAsync(packed.data(), V_.p, (size_t)n_packed_ * 4, cudaMemcpyDeviceToHost, stream_));
+    B2N_CUDA(cudaStreamSynchronize(stream_));
+    o.clear();
+    o.append("B2NS", 4);
+    ckpt::put_u32(o, 1);
+    ckpt::put_u32(o, (uint32_t)params_.size());
+    for (int i = 0; i < (int)params_.size(); ++i) put_tensor(packed, i);
+    const float hp[3] = {lr_, mom_, wd_};
+    ckpt::put_f32s(o, hp, 3);
+    ckpt::write_file(path + ".state", o, "save_network");
+}
+
+inline void Net::load(const std::string& path, bool with_state) {
+    ckpt::Reader rd;
+    rd.buf = ckpt::read_file(path, "load_network");
+    if (rd.bytes(4) != "FNN1") throw Error(B2N_EFORMAT, "load_network: bad magic; expected FNN1");
+    const uint32_t nl = rd.u32();
+    if (nl != spec_kinds_.size())
+        throw Error(B2N_EFORMAT, "load_network: checkpoint has " + std::to_string(nl) + " layers; network has " +
+                                     std::to_string(spec_kinds_.size()));
+    // parse everything before touching the device: a failed load leaves the parameters unchanged
+    std::vector<float> packed((size_t)n_packed_), tmp;
+    B2N_CUDA(cudaMemcpyAsync(packed.data(), P_.p, (size_t)n_packed_ * 4, cudaMemcpyDeviceToHost, stream_));
+    B2N_CUDA(cudaStreamSynchronize(stream_));
+    auto get_tensor = [&](ckpt::Reader& r, std::vector<float>& dst, int idx, const std::string& tag) {
+        const ParamView& v = params_[idx];
+        const uint32_t rank = r.u32();
+        if (rank != v.dims.size())
+            throw Error(B2N_EFORMAT, "load_network: tensor rank mismatch in layer '" + tag + "'");
+        for (size_t d = 0; d < rank; ++d)
+            if (r.u64() != (uint64_t)v.dims[d])
+                throw Error(B2N_EFORMAT, "load_network: tensor extent mismatch in layer '" + tag + "'");
+        tmp.resize((size_t)numel(v.dims));
+        r.f32s(tmp.data(), tmp.size());
+        scatter_params(dst, idx, tmp.data());
+    };
+    int pi = 0;
+    for (int kind : spec_kinds_) {
+        const uint32_t taglen = rd.u32();
+        if (taglen > 64) throw Error(B2N_EFORMAT, "load_network: implausible tag length");
+        const std::string tag = rd.bytes(taglen);
+        const std::string want = ckpt::tag_of(kind);
+        if (tag != want)
+            throw Error(B2N_EFORMAT,
+                        "load_network: layer tag mismatch; checkpoint '" + tag + "' vs network '" + want + "'");
+        const uint32_t count = rd.u32();
+        const uint32_t n = kind == B2N_DENSE || kind == B2N_CONV ? 2 : 0;
+        if (count != n) throw Error(B2N_EFORMAT, "load_network: tensor count mismatch in layer '" + tag + "'");
+        for (uint32_t t = 0; t < n; ++t) get_tensor(rd, packed, pi++, tag);
+    }
+    std::vector<float> vel;
+    float hp[3] = {lr_, mom_, wd_};
+    if (with_state) {
+        ckpt::Reader sr;
+        sr.buf = ckpt::read_file(path + ".state", "load_network");
+        if (sr.bytes(4) != "B2NS" || sr.u32() != 1) throw Error(B2N_EFORMAT, "load_network: bad state sidecar");
+        if (sr.u32() != params_.size()) throw Error(B2N_EFORMAT, "load_network: state tensor count mismatch");
+        vel.assign((size_t)n_packed_, 0.0f);
+        for (int i = 0; i < (int)params_.size(); ++i) get_tensor(sr, vel, i, "state");
+        sr.f32s(hp, 3);
+    }
+    B2N_CUDA(cudaMemcpyAsync(P_.p, packed.data(), (size_t)n_packed_ * 4, cudaMemcpyHostToDevice, stream_));
+    if (with_state) {
+        B2N_CUDA(cudaMemcpyAsync(V_.p, vel.data(), (size_t)n_packed_ * 4, cudaMemcpyHostToDevice, stream_));
+        if (hp[0] != lr_ || hp[1] != mom_ || hp[2] != wd_) set_hparams(hp[0], hp[1], hp[2]);
+    }
+    B2N_CUDA(cudaStreamSynchronize(stream_));
 }
 
 // --------------------------------------------------------------------------- params

@@ -21,8 +21,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from ._lib import (BoundsError, CudaError, Error, LabelError, NcclError, ParamError, ShapeError,  # noqa: F401
-                   SpecError)
+from ._lib import (BoundsError, ConsistencyError, CudaError, DataError, DataMissingError, Error,  # noqa: F401
+                   FormatError, LabelError, LengthError, NcclError, ParamError, ShapeError, SpecError)
 
 DENSE, CONV, MAXPOOL, SIGMOID, RELU, SOFTMAX, DROPOUT, BATCHNORM, FLATTEN = range(9)
 TF32X3, TF32 = 0, 1
@@ -264,7 +264,7 @@ def _dataset(net: Network, images, labels):
     if lab.ndim != 1 or lab.shape[0] != x.shape[0]:
         raise ShapeError("dataset: need one label per image")
     if x.shape[0] == 0:
-        raise Error("empty dataset")
+        raise DataError("empty dataset")
     return x, lab
 
 
@@ -309,6 +309,17 @@ def fit(net: Network, images, labels, epochs: int, test=None) -> TrainReport:
     if test is not None:
         rep.test_accuracy = evaluate(net, *test)
     return rep
+
+
+def save_network(net: Network, path: str, with_state: bool = False) -> None:
+    """fastnn::save_network (network.hpp:552-573): the reference's FNN1 bytes; with_state also
+    writes `<path>.state` (momentum velocities + hyper-parameters) for an exact resume."""
+    _lib.call("b2n_save_network", net.handle, str(path).encode(), int(with_state))
+
+
+def load_network(net: Network, path: str, with_state: bool = False) -> None:
+    """fastnn::load_network (network.hpp:575-607), same checks and error types."""
+    _lib.call("b2n_load_network", net.handle, str(path).encode(), int(with_state))
 
 
 def batch_order(n: int, seed: int, epoch: int = 0) -> np.ndarray:

@@ -8,6 +8,7 @@ padded ImageNet-shaped net, the SURVEY 8(c) composite of reference primitives.
 
     python tests/golden/make_golden.py        # writes tests/golden/*.npz and full_size.json
     python tests/golden/make_golden.py fit    # only fit.npz (fit / evaluate / batch order)
+    python tests/golden/make_golden.py checkpoint  # only *.fnn1 + checkpoint_errors.json
 """
 from __future__ import annotations
 
@@ -97,10 +98,39 @@ def fit_cases():
     np.savez_compressed(HERE / "fit.npz", **out)
 
 
+def checkpoint_cases():
+    """save_network bytes (network.hpp:552-573) of each small net after its two golden steps, plus
+    the reference's error texts for malformed files (network.hpp:575-607)."""
+    errs = {}
+    for name in ["mlp_small", "mnist_cnn_small", "cifar_cnn_small"]:
+        spec, _ = small_specs()[name]
+        g = np.load(HERE / f"{name}.npz")
+        ref = O.Net(spec, "ref")
+        for _ in range(2):
+            ref.train_minibatch(g["x"], g["labels"])
+        path = HERE / f"{name}.fnn1"
+        assert O.ref_checkpoint(ref, path) == ""
+        data = path.read_bytes()
+        cases = {"bad_magic": b"FNN2" + data[4:], "truncated": data[:-3], "empty": b"",
+                 "layer_count": data[:4] + (99).to_bytes(4, "little") + data[8:],
+                 "tag": data[:12] + b"x" + data[13:]}
+        for case, blob in cases.items():
+            tmp = HERE / "_tmp.fnn1"
+            tmp.write_bytes(blob)
+            errs[f"{name}:{case}"] = O.ref_checkpoint(ref, tmp, load=True)
+            tmp.unlink()
+        errs[f"{name}:missing"] = O.ref_checkpoint(ref, HERE / "_does_not_exist.fnn1", load=True)
+    (HERE / "checkpoint_errors.json").write_text(json.dumps(errs, indent=1))
+
+
 def main():
     if sys.argv[1:] == ["fit"]:
         fit_cases()
         print("fit fixtures written to", HERE)
+        return
+    if sys.argv[1:] == ["checkpoint"]:
+        checkpoint_cases()
+        print("checkpoint fixtures written to", HERE)
         return
     assert O.ref_available(), "build oracle/_ref first (make -C oracle) -- needs /root/reference"
     meta = {}
@@ -163,6 +193,7 @@ def main():
     (HERE / "full_size.json").write_text(json.dumps(full, indent=1))
     (HERE / "meta.json").write_text(json.dumps(meta, indent=1))
     fit_cases()
+    checkpoint_cases()
     print("golden fixtures written to", HERE)
 
 

@@ -80,9 +80,9 @@ def test_fit_errors(gpu):
     from paper_1804_04512_b200 import fastnn as F
     net = F.build_network(dict(META["mlp_small"]["spec"], batch_size=8))
     x = np.zeros((10, 64), np.float32)
-    with pytest.raises(F.LabelError):
+    with pytest.raises(F.ConsistencyError):  # data.hpp:257-260
         F.fit(net, x, np.full(10, 10, np.int32), 1)
     with pytest.raises(F.ParamError):
         F.fit(net, x, np.zeros(10, np.int32), 0)
-    with pytest.raises(F.Error):
+    with pytest.raises(F.DataError):
         F.evaluate(net, x[:0], np.zeros(0, np.int32))
