@@ -50,6 +50,21 @@ struct CudaError : Error {
 struct NcclError : Error {
     using Error::Error;
 };
+struct FormatError : Error {
+    using Error::Error;
+};
+struct LengthError : Error {
+    using Error::Error;
+};
+struct DataMissingError : Error {
+    using Error::Error;
+};
+struct ConsistencyError : Error {
+    using Error::Error;
+};
+struct DataError : Error {
+    using Error::Error;
+};
 
 inline void check(int status) {
     if (status == B2N_OK) return;
@@ -62,6 +77,11 @@ inline void check(int status) {
         case B2N_EBOUNDS: throw BoundsError(msg);
         case B2N_ECUDA: throw CudaError(msg);
         case B2N_ENCCL: throw NcclError(msg);
+        case B2N_EFORMAT: throw FormatError(msg);
+        case B2N_ELENGTH: throw LengthError(msg);
+        case B2N_EIO: throw DataMissingError(msg);
+        case B2N_ECONSISTENCY: throw ConsistencyError(msg);
+        case B2N_EDATA: throw DataError(msg);
         default: throw Error(msg);
     }
 }
@@ -196,22 +216,40 @@ std::vector<float> forward_batch(Network& net, const T& x, std::vector<int>* arg
     return probs;
 }
 
-// evaluate (network.hpp:474-484) over a dataset of `n` packed samples and int labels
+// evaluate (network.hpp:474-484) over a dataset of `n` packed samples and int labels, held in
+// device memory for the pass
 inline double evaluate(Network& net, const float* images, const int* labels, std::size_t n) {
-    if (n == 0) throw Error("evaluate: empty dataset");
-    const long long per = net.input_size();
-    std::size_t correct = 0;
-    std::vector<float> probs;
-    std::vector<int> am;
-    for (std::size_t lo = 0; lo < n; lo += net.batch_size) {
-        const std::size_t hi = std::min(lo + net.batch_size, n);
-        const long long B = (long long)(hi - lo);
-        probs.resize((std::size_t)(B * net.classes()));
-        am.resize((std::size_t)B);
-        check(b2n_forward_batch(net.handle(), images + lo * per, B, probs.data(), am.data()));
-        for (long long r = 0; r < B; ++r) correct += am[(std::size_t)r] == labels[lo + (std::size_t)r];
-    }
-    return (double)correct / (double)n;
+    double acc = 0.0;
+    check(b2n_net_evaluate(net.handle(), images, labels, (long long)n, &acc));
+    return acc;
+}
+
+// EpochStats / TrainReport / fit (network.hpp:255-265, :488-511): BatchIterator order from the
+// net's seed, dataset resident in device memory, batches gathered on the device
+struct EpochStats {
+    double loss = 0.0, accuracy = 0.0, seconds = 0.0;
+};
+struct TrainReport {
+    std::vector<EpochStats> epochs;
+    double test_accuracy = -1.0;
+    std::size_t total_batches = 0;
+};
+inline TrainReport fit(Network& net, const float* images, const int* labels, std::size_t n, std::size_t epochs) {
+    std::vector<double> loss(epochs), acc(epochs), sec(epochs);
+    check(b2n_net_fit(net.handle(), images, labels, (long long)n, (int)epochs, loss.data(), acc.data(), sec.data()));
+    TrainReport r;
+    for (std::size_t e = 0; e < epochs; ++e) r.epochs.push_back({loss[e], acc[e], sec[e]});
+    r.total_batches = epochs * ((n + net.batch_size - 1) / net.batch_size);
+    return r;
+}
+
+// save_network / load_network (network.hpp:552-607): the reference's FNN1 file; with_state adds
+// the `<path>.state` sidecar (velocities, hyper-parameters) for an exact resume
+inline void save_network(Network& net, const std::string& path, bool with_state = false) {
+    check(b2n_save_network(net.handle(), path.c_str(), with_state ? 1 : 0));
+}
+inline void load_network(Network& net, const std::string& path, bool with_state = false) {
+    check(b2n_load_network(net.handle(), path.c_str(), with_state ? 1 : 0));
 }
 
 // Rbm (energy.hpp:16-32), binary units

@@ -5,6 +5,9 @@
 // run by tests/test_gpu_cpp.py on a GPU box.
 #include <cmath>
 #include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <iterator>
 #include <random>
 #include <string>
 
@@ -67,6 +70,61 @@ bool net_criterion(const char* name, const std::vector<long long>& input,
     return ok;
 }
 
+std::string slurp(const std::string& path) {
+    std::ifstream is(path, std::ios::binary);
+    return std::string((std::istreambuf_iterator<char>(is)), std::istreambuf_iterator<char>());
+}
+
+// fit (network.hpp:488-511) on both sides over the same Dataset, then save_network on both sides
+bool fit_checkpoint_criterion() {
+    using FL = fastnn::LayerDesc;
+    using BL = b200nn::LayerDesc;
+    fastnn::NetworkSpec fs;
+    fs.input = {1, 28, 28};
+    fs.layers = {FL::conv(8, 5, 5), FL::sigmoid(), FL::maxpool(), FL::conv(8, 5, 5), FL::sigmoid(), FL::maxpool(),
+                 FL::dense(128, 150), FL::sigmoid(), FL::dense(150, 10), FL::softmax()};
+    b200nn::NetworkSpec bs;
+    bs.input = fs.input;
+    bs.layers = {BL::conv(8, 5, 5), BL::sigmoid(), BL::maxpool(), BL::conv(8, 5, 5), BL::sigmoid(), BL::maxpool(),
+                 BL::dense(128, 150), BL::sigmoid(), BL::dense(150, 10), BL::softmax()};
+    fastnn::Network ref = fastnn::build_network(fs);
+    b200nn::Network dev = b200nn::build_network(bs);
+    const std::size_t n = 450;  // 4 full batches of 100 and a partial one
+    fastnn::Dataset ds;
+    ds.images = random_batch({(long long)n, 1, 28, 28}, 7);
+    std::mt19937 lr_rng(8);
+    for (std::size_t i = 0; i < n; ++i) ds.labels.push_back((int)(lr_rng() % 10));
+    std::vector<float> flat(n * 784);
+    for (std::size_t r = 0; r < ds.images.rows_total(); ++r)
+        std::memcpy(flat.data() + r * 28, ds.images.row_ptr(r), 28 * sizeof(float));
+    const fastnn::TrainReport rf = fastnn::fit(ref, ds, 2);
+    const b200nn::TrainReport rd = b200nn::fit(dev, flat.data(), ds.labels.data(), n, 2);
+    double dloss = 0, dacc = 0;
+    for (int e = 0; e < 2; ++e) {
+        dloss = std::max(dloss, std::fabs(rf.epochs[e].loss - rd.epochs[e].loss) / rf.epochs[e].loss);
+        dacc = std::max(dacc, std::fabs(rf.epochs[e].accuracy - rd.epochs[e].accuracy));
+    }
+    double worst = 0;
+    auto tp = ref.trainable();
+    for (int i = 0; i < dev.num_params(); ++i) worst = std::max(worst, norm_err(dev.param(i), *tp[i].value));
+    // the reference's bytes for the device net's parameters: copy them in, save from both sides
+    for (int i = 0; i < dev.num_params(); ++i) {
+        const std::vector<float> v = dev.param(i);
+        std::size_t k = 0;
+        for (std::size_t r = 0; r < tp[i].value->rows_total(); ++r)
+            for (std::size_t j = 0; j < tp[i].value->last_dim(); ++j) tp[i].value->row_ptr(r)[j] = v[k++];
+    }
+    fastnn::save_network(ref, "/tmp/b2n_drop_in_ref.fnn1");
+    b200nn::save_network(dev, "/tmp/b2n_drop_in_dev.fnn1");
+    const bool same = slurp("/tmp/b2n_drop_in_ref.fnn1") == slurp("/tmp/b2n_drop_in_dev.fnn1");
+    const bool ok = dloss < 1e-4 && dacc <= 1.0 / n + 1e-12 && worst < 1e-3 && same &&
+                    rd.total_batches == rf.total_batches;
+    std::printf("criterion fit+checkpoint: %s -- 2 epochs x 450 samples, loss rel err %.2e, accuracy diff %.4f, "
+                "worst param norm err %.2e, FNN1 bytes %s\n",
+                ok ? "PASS" : "FAIL", dloss, dacc, worst, same ? "identical" : "DIFFER");
+    return ok;
+}
+
 }  // namespace
 
 int main() {
@@ -112,5 +170,6 @@ int main() {
                     rf, ew, ev, eh);
         ok &= r_ok;
     }
+    ok &= fit_checkpoint_criterion();
     return ok ? 0 : 1;
 }
