@@ -57,7 +57,13 @@ enum {
 enum { B2N_TF32X3 = 0, B2N_TF32 = 1 };
 
 /* parameter views for get/set */
-enum { B2N_VALUE = 0, B2N_GRAD = 1, B2N_VELOCITY = 2 };
+enum {
+    B2N_VALUE = 0,
+    B2N_GRAD = 1,
+    B2N_VELOCITY = 2,    /* SGD-momentum velocity */
+    B2N_OPT_STATE1 = 3,  /* Adagrad / Adadelta acc, Adam m (optim.hpp:25-26) */
+    B2N_OPT_STATE2 = 4   /* Adadelta acc_update, Adam v */
+};
 
 /* == fastnn::LayerDesc (network.hpp:194-223) plus a conv zero-padding field (`pad`) that the
  *    reference's ConvShape has (conv.hpp:21) but its LayerDesc cannot set. */
@@ -75,7 +81,7 @@ typedef struct b2n_network_spec {
     long long input[3];
     const b2n_layer_desc* layers;
     int n_layers;
-    int optimizer; /* 0 = SgdMomentum (optim.hpp:11); others ESPEC */
+    int optimizer; /* OptimizerKind (optim.hpp:11): 0 SgdMomentum, 1 Adagrad, 2 Adadelta, 3 Adam */
     float lr, momentum, weight_decay;
     long long batch_size;
     unsigned seed;

@@ -159,6 +159,7 @@ struct Layer {
     // dense: w (out,in), conv: kernels (k,c,kh,kw); b per unit
     size_t out = 0, in = 0, k = 0, c = 0, kh = 0, kw = 0, h = 0, w = 0, pad = 0;
     std::vector<float> wv, bv, gw, gb, vw, vb;
+    std::vector<float> s1w, s1b, s2w, s2b;  // adagrad/adadelta acc + acc_update, adam m + v (optim.hpp:23-27)
     std::vector<float> x_cache, y_cache, argmax;
 };
 
@@ -172,6 +173,9 @@ struct Net {
     std::vector<Layer> layers;
     std::vector<size_t> input;
     float lr = 0.1f, mom = 0.9f, wd = 0.0f;
+    int opt = 0;  // OptimizerKind (optim.hpp:11): 0 SgdMomentum, 1 Adagrad, 2 Adadelta, 3 Adam
+    float eps = 1e-8f, beta1 = 0.9f, beta2 = 0.999f, rho = 0.95f;  // OptimizerState defaults (optim.hpp:14-21)
+    long long t = 0;  // adam step counter (every slot steps together)
     std::string err;
 };
 
@@ -327,13 +331,68 @@ void sgd(std::vector<float>& p, std::vector<float>& v, const std::vector<float>&
     }
 }
 
+// adagrad_step optim.hpp:83-94
+void adagrad(std::vector<float>& p, std::vector<float>& acc, const std::vector<float>& grad, float lr, float eps) {
+    for (size_t i = 0; i < p.size(); ++i) {
+        float* a = &acc[i];
+        const float g = grad[i];
+        *a += g * g;
+        p[i] -= lr * g / (std::sqrt(*a) + eps);
+    }
+}
+
+// adadelta_step optim.hpp:96-110
+void adadelta(std::vector<float>& p, std::vector<float>& eg_, std::vector<float>& ex_, const std::vector<float>& grad,
+              float rho, float eps) {
+    for (size_t i = 0; i < p.size(); ++i) {
+        float* eg = &eg_[i];
+        float* ex = &ex_[i];
+        const float g = grad[i];
+        *eg = rho * *eg + (1.0f - rho) * g * g;
+        const float delta = -std::sqrt(*ex + eps) / std::sqrt(*eg + eps) * g;
+        *ex = rho * *ex + (1.0f - rho) * delta * delta;
+        p[i] += delta;
+    }
+}
+
+// adam_step optim.hpp:112-127 (c1, c2 from the step counter after its increment)
+void adam(std::vector<float>& p, std::vector<float>& m_, std::vector<float>& v_, const std::vector<float>& grad,
+          float lr, float b1, float b2, float eps, float c1, float c2) {
+    for (size_t i = 0; i < p.size(); ++i) {
+        float* m = &m_[i];
+        float* v = &v_[i];
+        const float g = grad[i];
+        *m = b1 * *m + (1.0f - b1) * g;
+        *v = b2 * *v + (1.0f - b2) * g * g;
+        p[i] -= lr * (*m / c1) / (std::sqrt(*v / c2) + eps);
+    }
+}
+
+void optimizer_step(Net& net, std::vector<float>& p, std::vector<float>& vel, std::vector<float>& s1,
+                    std::vector<float>& s2, const std::vector<float>& g, float c1, float c2) {  // optim.hpp:129-137
+    if (s1.size() != p.size()) s1.assign(p.size(), 0.0f), s2.assign(p.size(), 0.0f);
+    switch (net.opt) {
+        case 0: sgd(p, vel, g, net.lr, net.mom, net.wd); break;
+        case 1: adagrad(p, s1, g, net.lr, net.eps); break;
+        case 2: adadelta(p, s1, s2, g, net.rho, net.eps); break;
+        case 3: adam(p, s1, s2, g, net.lr, net.beta1, net.beta2, net.eps, c1, c2); break;
+    }
+}
+
 void apply(Net& net) {  // network.hpp:468-470
-    if (net.lr != 0.0f)
+    if (net.lr != 0.0f) {
+        float c1 = 1.0f, c2 = 1.0f;
+        if (net.opt == 3) {
+            net.t += 1;
+            c1 = 1.0f - std::pow(net.beta1, static_cast<float>(net.t));
+            c2 = 1.0f - std::pow(net.beta2, static_cast<float>(net.t));
+        }
         for (Layer& L : net.layers)
             if (L.kind == Dense || L.kind == Conv) {
-                sgd(L.wv, L.vw, L.gw, net.lr, net.mom, net.wd);
-                sgd(L.bv, L.vb, L.gb, net.lr, net.mom, net.wd);
+                optimizer_step(net, L.wv, L.vw, L.s1w, L.s2w, L.gw, c1, c2);
+                optimizer_step(net, L.bv, L.vb, L.s1b, L.s2b, L.gb, c1, c2);
             }
+    }
     for (Layer& L : net.layers) {
         std::fill(L.gw.begin(), L.gw.end(), 0.0f);
         std::fill(L.gb.begin(), L.gb.end(), 0.0f);
@@ -344,14 +403,18 @@ struct ParamSlot {
     std::vector<float>* val;
     std::vector<float>* grad;
     std::vector<float>* vel;
+    std::vector<float>* s1;
+    std::vector<float>* s2;
 };
 
 std::vector<ParamSlot> params(Net& net) {  // trainable() order: w then b per layer (network.hpp:83, :100, :244-249)
     std::vector<ParamSlot> out;
     for (Layer& L : net.layers)
         if (L.kind == Dense || L.kind == Conv) {
-            out.push_back({&L.wv, &L.gw, &L.vw});
-            out.push_back({&L.bv, &L.gb, &L.vb});
+            for (auto* v : {&L.s1w, &L.s2w}) v->resize(L.wv.size());
+            for (auto* v : {&L.s1b, &L.s2b}) v->resize(L.bv.size());
+            out.push_back({&L.wv, &L.gw, &L.vw, &L.s1w, &L.s2w});
+            out.push_back({&L.bv, &L.gb, &L.vb, &L.s1b, &L.s2b});
         }
     return out;
 }
@@ -457,18 +520,20 @@ int orc_net_num_params(void* h) { return (int)params(*static_cast<Net*>(h)).size
 
 long long orc_net_param_size(void* h, int idx) { return (long long)params(*static_cast<Net*>(h))[idx].val->size(); }
 
-// which: 0 value, 1 grad, 2 velocity
+// which: 0 value, 1 grad, 2 velocity, 3 acc / adam m, 4 acc_update / adam v
 void orc_net_get(void* h, int idx, int which, float* out) {
     ParamSlot s = params(*static_cast<Net*>(h))[idx];
-    const std::vector<float>* v = which == 0 ? s.val : which == 1 ? s.grad : s.vel;
+    const std::vector<float>* v = which == 0 ? s.val : which == 1 ? s.grad : which == 2 ? s.vel : which == 3 ? s.s1 : s.s2;
     std::memcpy(out, v->data(), v->size() * sizeof(float));
 }
 
 void orc_net_set(void* h, int idx, int which, const float* in) {
     ParamSlot s = params(*static_cast<Net*>(h))[idx];
-    std::vector<float>* v = which == 0 ? s.val : which == 1 ? s.grad : s.vel;
+    std::vector<float>* v = which == 0 ? s.val : which == 1 ? s.grad : which == 2 ? s.vel : which == 3 ? s.s1 : s.s2;
     std::memcpy(v->data(), in, v->size() * sizeof(float));
 }
+
+void orc_net_set_optimizer(void* h, int kind) { static_cast<Net*>(h)->opt = kind; }
 
 void orc_net_set_hparams(void* h, float lr, float mom, float wd) {
     Net* n = static_cast<Net*>(h);

@@ -71,6 +71,7 @@ def _declare(lib: C.CDLL, prefix: str) -> None:
     g = getattr(lib, f"{p}_gemm")
     g.argtypes = [C.c_int, C.c_int, _F, _F, _F, C.c_longlong, C.c_longlong, C.c_longlong]
     getattr(lib, f"{p}_sgd_momentum_step").argtypes = [_F, _F, _F, C.c_longlong, C.c_float, C.c_float, C.c_float]
+    getattr(lib, f"{p}_net_set_optimizer").argtypes = [C.c_void_p, C.c_int]
     getattr(lib, f"{p}_batch_order").argtypes = [C.c_longlong, C.c_uint, C.c_int, _LL]
     getattr(lib, f"{p}_net_fit").argtypes = [C.c_void_p, _F, _I, C.c_longlong, C.c_longlong, C.c_uint, C.c_int,
                                              _D, _D]
@@ -182,6 +183,8 @@ class Net:
         self.h = h
         self.classes = [d for d in spec["layers"] if d["kind"] == DENSE][-1]["out"]
         self.input = list(spec["input"])
+        if spec.get("optimizer", 0):
+            getattr(self.lib, f"{self.p}_net_set_optimizer")(self.h, spec["optimizer"])
 
     def __del__(self):
         if getattr(self, "h", None):

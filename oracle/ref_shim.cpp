@@ -301,7 +301,8 @@ long long ref_net_param_size(void* h, int idx) {
     return (long long)static_cast<RefNet*>(h)->net.trainable()[idx].value->size();
 }
 
-// which: 0 value, 1 grad, 2 velocity (OptimizerState slot keyed by the parameter's storage, optim.hpp:31-34)
+// which: 0 value, 1 grad, 2 velocity, 3 acc (adagrad / adadelta) or m (adam), 4 acc_update or v
+// (OptimizerState slot keyed by the parameter's storage, optim.hpp:23-34)
 void ref_net_get(void* h, int idx, int which, float* out) {
     RefNet& rn = *static_cast<RefNet*>(h);
     ParamRef p = rn.net.trainable()[idx];
@@ -312,8 +313,12 @@ void ref_net_get(void* h, int idx, int which, float* out) {
         std::memset(out, 0, p.value->size() * sizeof(float));
         return;
     }
-    copy_out(it->second.velocity, out);
+    const OptimizerState::Slot& sl = it->second;
+    const bool adam = rn.net.opt.kind == OptimizerKind::Adam;
+    copy_out(which == 2 ? sl.velocity : which == 3 ? (adam ? sl.m : sl.acc) : (adam ? sl.v : sl.acc_update), out);
 }
+
+void ref_net_set_optimizer(void* h, int kind) { static_cast<RefNet*>(h)->net.opt.kind = (OptimizerKind)kind; }
 
 void ref_net_set(void* h, int idx, int which, const float* in) {
     RefNet& rn = *static_cast<RefNet*>(h);

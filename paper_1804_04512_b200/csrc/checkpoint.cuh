@@ -9,9 +9,10 @@
 // written / parsed on the host with the reference's checks and messages.
 //
 // For exact resume the library also writes an optional sidecar `<path>.state` (not read by the
-// reference): "B2NS", u32 version 1, u32 tensor count, then per trainable tensor its rank, extents
-// and momentum velocity (optim.hpp:31-34 OptimizerState.velocity), then f32 lr, momentum,
-// weight_decay.
+// reference): "B2NS", u32 version 2, u32 optimizer kind, u64 adam step count, f32 lr, momentum,
+// weight_decay, u32 buffer count (1 for SGD-momentum / Adagrad, 2 for Adadelta / Adam), then per
+// buffer a u32 tensor count and per trainable tensor its rank, extents and values: the momentum
+// velocity, or acc [+ acc_update], or m + v (optim.hpp:23-27 OptimizerState::Slot).
 #pragma once
 #include <cstdint>
 #include <cstring>

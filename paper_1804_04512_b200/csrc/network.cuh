@@ -252,9 +252,7 @@ class Net {
     std::vector<OpStats> profile(long long B, int steps) {
         ensure_capacity(B);
         Plan& pl = plan_for(B, B);
-        std::vector<Op> ops = pl.ops[dp_ ? SPLIT : (lr_ != 0.0f ? FUSED : SPLIT)];
-        if (dp_) ops.insert(ops.end(), pl.ops[SPLIT_APPLY].begin(), pl.ops[SPLIT_APPLY].end());
-        return profile_ops(ops, steps, stream_);
+        return profile_ops(pl.ops[TRAIN], steps, stream_);
     }
     void dp_init(const char id[128], int rank, int world) {
         dp_ = std::make_unique<DpComm>();
@@ -266,12 +264,15 @@ class Net {
     long long packed_floats() const { return n_packed_; }
 
   private:
-    enum Mode { FUSED = 0, SPLIT = 1, FWD = 2, SPLIT_APPLY = 3, FIT = 4, EVAL = 5 };
+    // TRAIN = the whole training step of this net: FUSED (SGD epilogues in the backward kernels) when
+    // the optimizer is SGD-momentum on one GPU, else SPLIT + SPLIT_APPLY (allreduce and / or the
+    // packed optimizer kernel), SPLIT alone when lr == 0
+    enum Mode { FUSED = 0, SPLIT = 1, FWD = 2, SPLIT_APPLY = 3, FIT = 4, EVAL = 5, TRAIN = 6, NMODES = 7 };
     struct Plan {
         long long B = 0, Bg = 0;
-        std::vector<Op> ops[6];
-        cudaGraphExec_t graph[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
-        int nkernels[6] = {0, 0, 0, 0, 0, 0};
+        std::vector<Op> ops[NMODES];
+        cudaGraphExec_t graph[NMODES] = {};
+        int nkernels[NMODES] = {};
         ~Plan() {
             for (auto& g : graph)
                 if (g) cudaGraphExecDestroy(g);
@@ -319,6 +320,13 @@ class Net {
     unsigned seed_ = 0;
     long long batch_size_ = 1;
     std::vector<int> spec_kinds_;  // the spec's layer list (checkpoint tags, network.hpp:560)
+    int opt_ = 0;                  // OptimizerKind (optim.hpp:11)
+    DevMem S1_, S2_;               // adagrad / adadelta / adam state (packed like P_)
+    DevMem opt_ctab_, opt_cnt_;    // adam bias-correction table + device step counter
+    long long opt_steps_ = 0, opt_ctab_filled_ = 0;  // host view of the adam step count / table fill
+    static constexpr long long kCtabCap = 1ll << 24;
+    void note_opt_step();
+    DevMem& state_buffer(int which);
     void gather_params(const std::vector<float>& packed, int idx, float* out) const;
     void scatter_params(std::vector<float>& packed, int idx, const float* in) const;
     void upload_dataset(const float* images, const int* labels, long long N);
@@ -350,7 +358,8 @@ inline Net::Net(const b2n_network_spec& spec, int device, int precision)
     for (int i = 0; i < spec.input_rank; ++i)
         if (spec.input[i] < 1) throw Error(B2N_ESPEC, "network spec input extents must be positive");
     if (spec.batch_size < 1) throw Error(B2N_ESPEC, "network spec batch_size must be >= 1");
-    if (spec.optimizer != 0) throw Error(B2N_ESPEC, "b200nn: only the SGD-momentum optimizer is on the B200 path");
+    if (spec.optimizer < 0 || spec.optimizer > OPT_ADAM) throw Error(B2N_ESPEC, "unknown optimizer kind");
+    opt_ = spec.optimizer;
     input_.assign(spec.input, spec.input + spec.input_rank);
 
     auto shape_str = [](const std::vector<long long>& s) {
@@ -492,6 +501,12 @@ inline Net::Net(const b2n_network_spec& spec, int device, int precision)
     P_.alloc(n_packed_ * 4);
     V_.alloc(n_packed_ * 4);
     G_.alloc(n_packed_ * 4);
+    if (opt_ != 0) {
+        S1_.alloc(n_packed_ * 4);
+        if (opt_ != OPT_ADAGRAD) S2_.alloc(n_packed_ * 4);
+        opt_cnt_.alloc(sizeof(OptCounter));
+        if (opt_ == OPT_ADAM) opt_ctab_.alloc(kCtabCap * sizeof(float2));
+    }
     loss_sum_.alloc(64);
     // seeded Glorot init in layer order (network.hpp:369-373, layers.hpp:40-48), same draws
     std::mt19937 rng(spec.seed);
@@ -868,21 +883,78 @@ inline void Net::build_plan(Plan& pl) {
     pl.ops[SPLIT].insert(pl.ops[SPLIT].end(), bwd_split.begin(), bwd_split.end());
     pl.nkernels[SPLIT] = nk_fwd + nk_split;
     for (int m : {FWD, FUSED, SPLIT}) assign_prefetch(pl.ops[m]);
-    // data-parallel apply: allreduce(G) then the packed SGD pass
+    // data-parallel apply: allreduce(G) then the packed optimizer pass
     float* Pp = P;
     long long n4 = n_packed_ / 4;
     float lr = lr_, mom = mom_, wd = wd_;
     DpComm* dp = dp_.get();
     long long npk = n_packed_;
+    const int opt = opt_;
+    float* S1 = S1_.as<float>();
+    float* S2 = opt_ == OPT_ADAGRAD ? S1 : S2_.as<float>();
+    const float2* ctab = opt_ctab_.as<float2>();
+    OptCounter* cnt = opt_cnt_.as<OptCounter>();
+    static const char* opt_names[] = {"sgd", "adagrad", "adadelta", "adam"};
+    const double opt_bytes = (double)npk * (opt == 0 ? 20 : opt == OPT_ADAGRAD ? 20 : 28);
     pl.ops[SPLIT_APPLY].push_back(Op([=](cudaStream_t s) {
         if (dp) dp->allreduce_f32(G, (size_t)npk, s);
-        launch_ex(sgd_packed_kernel, dim3(grid_for(n4)), dim3(256), 0, s, 1u, reinterpret_cast<float4*>(Pp),
-                  reinterpret_cast<float4*>(Vv), reinterpret_cast<const float4*>(G), n4, lr, mom, wd);
-    }, dp ? "allreduce+sgd" : "sgd", 0.0, (double)npk * 20));
+        float4* p4 = reinterpret_cast<float4*>(Pp);
+        const float4* g4 = reinterpret_cast<const float4*>(G);
+        float4* a4 = reinterpret_cast<float4*>(S1);
+        float4* b4 = reinterpret_cast<float4*>(S2);
+        // OptimizerState defaults (optim.hpp:18-21): eps 1e-8, beta1 0.9, beta2 0.999, rho 0.95
+        switch (opt) {
+            case 0:
+                launch_ex(sgd_packed_kernel, dim3(grid_for(n4)), dim3(256), 0, s, 1u, p4,
+                          reinterpret_cast<float4*>(Vv), g4, n4, lr, mom, wd);
+                break;
+            case OPT_ADAGRAD:
+                launch_ex(opt_packed_kernel<OPT_ADAGRAD>, dim3(grid_for(n4)), dim3(256), 0, s, 1u, p4, a4, b4, g4, n4,
+                          lr, 1e-8f, 0.95f, 0.9f, 0.999f, ctab, cnt);
+                break;
+            case OPT_ADADELTA:
+                launch_ex(opt_packed_kernel<OPT_ADADELTA>, dim3(grid_for(n4)), dim3(256), 0, s, 1u, p4, a4, b4, g4,
+                          n4, lr, 1e-8f, 0.95f, 0.9f, 0.999f, ctab, cnt);
+                break;
+            default:
+                launch_ex(opt_packed_kernel<OPT_ADAM>, dim3(grid_for(n4)), dim3(256), 0, s, 1u, p4, a4, b4, g4, n4,
+                          lr, 1e-8f, 0.95f, 0.9f, 0.999f, ctab, cnt);
+        }
+    }, std::string(dp ? "allreduce+" : "") + opt_names[opt], 0.0, opt_bytes));
     pl.nkernels[SPLIT_APPLY] = 1;
+    // the whole step
+    if (!dp_ && opt_ == 0 && lr_ != 0.0f) {
+        pl.ops[TRAIN] = pl.ops[FUSED];
+        pl.nkernels[TRAIN] = pl.nkernels[FUSED];
+    } else {
+        pl.ops[TRAIN] = pl.ops[SPLIT];
+        pl.nkernels[TRAIN] = pl.nkernels[SPLIT];
+        if (dp_ || lr_ != 0.0f) {
+            pl.ops[TRAIN].insert(pl.ops[TRAIN].end(), pl.ops[SPLIT_APPLY].begin(), pl.ops[SPLIT_APPLY].end());
+            pl.nkernels[TRAIN] += pl.nkernels[SPLIT_APPLY];
+        }
+    }
+}
+
+// the host's count of adam steps keeps the bias-correction table filled ahead of the device counter
+inline void Net::note_opt_step() {
+    if (opt_ != OPT_ADAM) return;
+    ++opt_steps_;
+    if (opt_steps_ + 1 < opt_ctab_filled_) return;
+    if (opt_steps_ + 2 > kCtabCap) throw Error(B2N_EPARAM, "adam: step counter exceeds the bias-correction table");
+    const long long lo = opt_ctab_filled_, hi = std::min(kCtabCap, std::max(lo + 65536, opt_steps_ + 2));
+    std::vector<float2> c((size_t)(hi - lo));
+    for (long long t = lo; t < hi; ++t)  // adam_step (optim.hpp:118-119)
+        c[(size_t)(t - lo)] = make_float2(1.0f - std::pow(0.9f, static_cast<float>(t)),
+                                          1.0f - std::pow(0.999f, static_cast<float>(t)));
+    B2N_CUDA(cudaMemcpyAsync(opt_ctab_.as<float2>() + lo, c.data(), c.size() * sizeof(float2), cudaMemcpyHostToDevice,
+                             stream_));
+    B2N_CUDA(cudaStreamSynchronize(stream_));
+    opt_ctab_filled_ = hi;
 }
 
 inline void Net::launch(Plan& pl, int mode) {
+    if (opt_ == OPT_ADAM && lr_ != 0.0f && (mode == TRAIN || mode == SPLIT_APPLY || mode == FIT)) note_opt_step();
     if (!pl.graph[mode]) {
         cudaGraph_t graph;
         B2N_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
@@ -932,7 +1004,7 @@ inline double Net::train(const float* x, const int* labels, long long B) {
         throw Error(B2N_EPARAM, "data-parallel nets step through forward_backward + apply_update");
     }
     Plan& pl = plan_for(B, B);
-    launch(pl, lr_ != 0.0f ? FUSED : SPLIT);
+    launch(pl, TRAIN);
     last_B_ = B;
     last_Bg_ = B;
     return read_loss(B) / (double)B;
@@ -980,21 +1052,14 @@ inline void Net::run_staged(int steps, long long Bg) {
     check_train_params();
     Plan& pl = plan_for(last_B_, Bg ? Bg : last_B_);
     last_Bg_ = pl.Bg;
-    for (int s = 0; s < steps; ++s) {
-        if (dp_) {
-            launch(pl, SPLIT);
-            launch(pl, SPLIT_APPLY);
-        } else {
-            launch(pl, lr_ != 0.0f ? FUSED : SPLIT);
-        }
-    }
+    for (int s = 0; s < steps; ++s) launch(pl, TRAIN);
 }
 
 inline double Net::loss() { return read_loss(last_B_) / (double)(last_Bg_ ? last_Bg_ : last_B_); }
 
 inline int Net::kernels_per_step(long long B) {
     Plan& pl = plan_for(B, B);
-    return dp_ ? pl.nkernels[SPLIT] + pl.nkernels[SPLIT_APPLY] : pl.nkernels[lr_ != 0.0f ? FUSED : SPLIT];
+    return pl.nkernels[TRAIN];
 }
 
 // --------------------------------------------------------------------------- fit / evaluate
@@ -1038,7 +1103,7 @@ inline void Net::build_fit_ops(Plan& pl, int mode) {
         launch_ex(fit_gather_kernel, dim3(grid_for(n)), dim3(256), 0, s, 1u, ds, per, dy, ord, (const FitState*)st, count,
                   X, ldx, lab);
     }, "fit.gather", 0.0, (double)count * per * 8));
-    const std::vector<Op>& body = pl.ops[mode == FIT ? (lr_ != 0.0f ? FUSED : SPLIT) : FWD];
+    const std::vector<Op>& body = pl.ops[mode == FIT ? TRAIN : FWD];
     ops.insert(ops.end(), body.begin(), body.end());
     const double* rl = row_loss_;
     const int* am = argmax_;
@@ -1155,15 +1220,25 @@ inline void Net::save(const std::string& path, bool with_state) {
     }
     ckpt::write_file(path, o, "save_network");
     if (!with_state) return;
-    B2N_CUDA(cudaMemcpyAsync(packed.data(), V_.p, (size_t)n_packed_ * 4, cudaMemcpyDeviceToHost, stream_));
-    B2N_CUDA(cudaStreamSynchronize(stream_));
     o.clear();
     o.append("B2NS", 4);
-    ckpt::put_u32(o, 1);
-    ckpt::put_u32(o, (uint32_t)params_.size());
-    for (int i = 0; i < (int)params_.size(); ++i) put_tensor(packed, i);
+    ckpt::put_u32(o, 2);
+    ckpt::put_u32(o, (uint32_t)opt_);
+    OptCounter oc{};
+    if (opt_cnt_.p) B2N_CUDA(cudaMemcpyAsync(&oc, opt_cnt_.p, sizeof(oc), cudaMemcpyDeviceToHost, stream_));
+    B2N_CUDA(cudaStreamSynchronize(stream_));
+    ckpt::put_u64(o, (uint64_t)oc.t);
     const float hp[3] = {lr_, mom_, wd_};
     ckpt::put_f32s(o, hp, 3);
+    const int nbuf = opt_ == 0 ? 1 : opt_ == OPT_ADAGRAD ? 1 : 2;
+    ckpt::put_u32(o, (uint32_t)nbuf);
+    for (int b = 0; b < nbuf; ++b) {  // velocity (sgd) or the optimizer's state buffers
+        DevMem& src = opt_ == 0 ? V_ : b == 0 ? S1_ : S2_;
+        B2N_CUDA(cudaMemcpyAsync(packed.data(), src.p, (size_t)n_packed_ * 4, cudaMemcpyDeviceToHost, stream_));
+        B2N_CUDA(cudaStreamSynchronize(stream_));
+        ckpt::put_u32(o, (uint32_t)params_.size());
+        for (int i = 0; i < (int)params_.size(); ++i) put_tensor(packed, i);
+    }
     ckpt::write_file(path + ".state", o, "save_network");
 }
 
@@ -1205,30 +1280,63 @@ inline void Net::load(const std::string& path, bool with_state) {
         if (count != n) throw Error(B2N_EFORMAT, "load_network: tensor count mismatch in layer '" + tag + "'");
         for (uint32_t t = 0; t < n; ++t) get_tensor(rd, packed, pi++, tag);
     }
-    std::vector<float> vel;
+    std::vector<std::vector<float>> bufs;
     float hp[3] = {lr_, mom_, wd_};
+    uint64_t t = 0;
     if (with_state) {
         ckpt::Reader sr;
         sr.buf = ckpt::read_file(path + ".state", "load_network");
-        if (sr.bytes(4) != "B2NS" || sr.u32() != 1) throw Error(B2N_EFORMAT, "load_network: bad state sidecar");
-        if (sr.u32() != params_.size()) throw Error(B2N_EFORMAT, "load_network: state tensor count mismatch");
-        vel.assign((size_t)n_packed_, 0.0f);
-        for (int i = 0; i < (int)params_.size(); ++i) get_tensor(sr, vel, i, "state");
+        if (sr.bytes(4) != "B2NS" || sr.u32() != 2) throw Error(B2N_EFORMAT, "load_network: bad state sidecar");
+        if ((int)sr.u32() != opt_) throw Error(B2N_EFORMAT, "load_network: state sidecar is for another optimizer");
+        t = sr.u64();
         sr.f32s(hp, 3);
+        const uint32_t nbuf = sr.u32();
+        if (nbuf != (opt_ == 0 || opt_ == OPT_ADAGRAD ? 1u : 2u))
+            throw Error(B2N_EFORMAT, "load_network: state buffer count mismatch");
+        for (uint32_t b = 0; b < nbuf; ++b) {
+            if (sr.u32() != params_.size()) throw Error(B2N_EFORMAT, "load_network: state tensor count mismatch");
+            bufs.emplace_back((size_t)n_packed_, 0.0f);
+            for (int i = 0; i < (int)params_.size(); ++i) get_tensor(sr, bufs.back(), i, "state");
+        }
     }
     B2N_CUDA(cudaMemcpyAsync(P_.p, packed.data(), (size_t)n_packed_ * 4, cudaMemcpyHostToDevice, stream_));
     if (with_state) {
-        B2N_CUDA(cudaMemcpyAsync(V_.p, vel.data(), (size_t)n_packed_ * 4, cudaMemcpyHostToDevice, stream_));
+        for (size_t b = 0; b < bufs.size(); ++b) {
+            DevMem& dst = opt_ == 0 ? V_ : b == 0 ? S1_ : S2_;
+            B2N_CUDA(cudaMemcpyAsync(dst.p, bufs[b].data(), (size_t)n_packed_ * 4, cudaMemcpyHostToDevice, stream_));
+        }
+        if (opt_cnt_.p) {
+            const OptCounter oc{(long long)t, 0u};
+            B2N_CUDA(cudaMemcpyAsync(opt_cnt_.p, &oc, sizeof(oc), cudaMemcpyHostToDevice, stream_));
+            B2N_CUDA(cudaStreamSynchronize(stream_));
+            opt_steps_ = (long long)t - 1;
+            if (opt_ == OPT_ADAM) note_opt_step();  // table filled past t; opt_steps_ back to t
+        }
         if (hp[0] != lr_ || hp[1] != mom_ || hp[2] != wd_) set_hparams(hp[0], hp[1], hp[2]);
     }
     B2N_CUDA(cudaStreamSynchronize(stream_));
 }
 
 // --------------------------------------------------------------------------- params
+inline DevMem& Net::state_buffer(int which) {
+    switch (which) {
+        case B2N_VALUE: return P_;
+        case B2N_GRAD: return G_;
+        case B2N_VELOCITY: return V_;
+        case B2N_OPT_STATE1:
+            if (S1_.p) return S1_;
+            break;
+        case B2N_OPT_STATE2:
+            if (S2_.p) return S2_;
+            break;
+    }
+    throw Error(B2N_EBOUNDS, "parameter view " + std::to_string(which) + " does not exist for this optimizer");
+}
+
 inline void Net::get_param(int idx, int which, float* host) {
     if (idx < 0 || idx >= num_params()) throw Error(B2N_EBOUNDS, "param index out of range");
     const ParamView& v = params_[idx];
-    const float* base = (which == B2N_VALUE ? P_ : which == B2N_GRAD ? G_ : V_).as<float>() + v.off;
+    const float* base = state_buffer(which).as<float>() + v.off;
     B2N_CUDA(cudaMemcpy2DAsync(host, v.cols * 4, base, v.pitch * 4, v.cols * 4, v.rows, cudaMemcpyDeviceToHost,
                                stream_));
     B2N_CUDA(cudaStreamSynchronize(stream_));
@@ -1237,7 +1345,7 @@ inline void Net::get_param(int idx, int which, float* host) {
 inline void Net::set_param(int idx, int which, const float* host) {
     if (idx < 0 || idx >= num_params()) throw Error(B2N_EBOUNDS, "param index out of range");
     const ParamView& v = params_[idx];
-    float* base = (which == B2N_VALUE ? P_ : which == B2N_GRAD ? G_ : V_).as<float>() + v.off;
+    float* base = state_buffer(which).as<float>() + v.off;
     B2N_CUDA(cudaMemcpy2DAsync(base, v.pitch * 4, host, v.cols * 4, v.cols * 4, v.rows, cudaMemcpyHostToDevice,
                                stream_));
     B2N_CUDA(cudaStreamSynchronize(stream_));

@@ -465,6 +465,69 @@ static __global__ void sgd_packed_kernel(float4* __restrict__ p, float4* __restr
     }
 }
 
+// adagrad / adadelta / adam steps (optim.hpp:83-127) over the packed buffers. s1 = acc (adagrad,
+// adadelta) or m (adam); s2 = acc_update (adadelta) or v (adam). Adam's bias corrections come from
+// a host-computed table c[t] = {1 - powf(b1, t), 1 - powf(b2, t)} (the reference's std::pow on
+// floats) indexed by the device step counter, which the last block to finish advances -- so a
+// replayed graph steps t without the host.
+struct OptCounter {
+    long long t;            // completed adam steps
+    unsigned int done;      // blocks finished in the current launch
+};
+constexpr int OPT_ADAGRAD = 1, OPT_ADADELTA = 2, OPT_ADAM = 3;
+
+template <int KIND>
+__device__ __forceinline__ void opt_elem(float& p, float& a, float& b, float g, float lr, float eps, float rho,
+                                         float b1, float b2, float c1, float c2) {
+    if constexpr (KIND == OPT_ADAGRAD) {
+        a += g * g;
+        p -= lr * g / (sqrtf(a) + eps);
+    } else if constexpr (KIND == OPT_ADADELTA) {
+        a = rho * a + (1.0f - rho) * g * g;
+        const float delta = -sqrtf(b + eps) / sqrtf(a + eps) * g;
+        b = rho * b + (1.0f - rho) * delta * delta;
+        p += delta;
+    } else {
+        a = b1 * a + (1.0f - b1) * g;
+        b = b2 * b + (1.0f - b2) * g * g;
+        p -= lr * (a / c1) / (sqrtf(b / c2) + eps);
+    }
+}
+
+template <int KIND>
+static __global__ void opt_packed_kernel(float4* __restrict__ p, float4* __restrict__ s1, float4* __restrict__ s2,
+                                         const float4* __restrict__ g, long long n4, float lr, float eps, float rho,
+                                         float b1, float b2, const float2* __restrict__ ctab, OptCounter* cnt) {
+    pdl_wait();
+    float c1 = 1.0f, c2 = 1.0f;
+    if (KIND == OPT_ADAM) {
+        const float2 c = ctab[cnt->t + 1];
+        c1 = c.x;
+        c2 = c.y;
+    }
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+        float4 pp = p[i], aa = s1[i], bb = KIND == OPT_ADAGRAD ? make_float4(0, 0, 0, 0) : s2[i];
+        const float4 gg = g[i];
+        opt_elem<KIND>(pp.x, aa.x, bb.x, gg.x, lr, eps, rho, b1, b2, c1, c2);
+        opt_elem<KIND>(pp.y, aa.y, bb.y, gg.y, lr, eps, rho, b1, b2, c1, c2);
+        opt_elem<KIND>(pp.z, aa.z, bb.z, gg.z, lr, eps, rho, b1, b2, c1, c2);
+        opt_elem<KIND>(pp.w, aa.w, bb.w, gg.w, lr, eps, rho, b1, b2, c1, c2);
+        p[i] = pp;
+        s1[i] = aa;
+        if (KIND != OPT_ADAGRAD) s2[i] = bb;
+    }
+    if (KIND == OPT_ADAM) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(&cnt->done, 1u) == gridDim.x - 1) {  // every block has read t
+                cnt->t += 1;
+                cnt->done = 0;
+            }
+        }
+    }
+}
+
 static __global__ void fill_kernel(float* __restrict__ p, long long n, float v) {
     pdl_wait();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)

@@ -26,7 +26,8 @@ from ._lib import (BoundsError, ConsistencyError, CudaError, DataError, DataMiss
 
 DENSE, CONV, MAXPOOL, SIGMOID, RELU, SOFTMAX, DROPOUT, BATCHNORM, FLATTEN = range(9)
 TF32X3, TF32 = 0, 1
-VALUE, GRAD, VELOCITY = 0, 1, 2
+VALUE, GRAD, VELOCITY, OPT_STATE1, OPT_STATE2 = 0, 1, 2, 3, 4  # OPT_STATE1/2: acc/acc_update or adam m/v
+SGD_MOMENTUM, ADAGRAD, ADADELTA, ADAM = 0, 1, 2, 3  # OptimizerKind (optim.hpp:11)
 
 
 def _f(a: np.ndarray):
@@ -108,7 +109,7 @@ class NetworkSpec:
         return NetworkSpec(input=list(d["input"]), layers=[LayerDesc.from_dict(x) for x in d["layers"]],
                            lr=d.get("lr", 0.1), momentum=d.get("momentum", 0.9),
                            weight_decay=d.get("weight_decay", 0.0), batch_size=d.get("batch_size", 100),
-                           seed=d.get("seed", 42))
+                           seed=d.get("seed", 42), optimizer=d.get("optimizer", 0))
 
 
 class Network:

@@ -9,6 +9,7 @@ padded ImageNet-shaped net, the SURVEY 8(c) composite of reference primitives.
     python tests/golden/make_golden.py        # writes tests/golden/*.npz and full_size.json
     python tests/golden/make_golden.py fit    # only fit.npz (fit / evaluate / batch order)
     python tests/golden/make_golden.py checkpoint  # only *.fnn1 + checkpoint_errors.json
+    python tests/golden/make_golden.py optim  # only optim.npz (Adagrad / Adadelta / Adam)
 """
 from __future__ import annotations
 
@@ -123,7 +124,26 @@ def checkpoint_cases():
     (HERE / "checkpoint_errors.json").write_text(json.dumps(errs, indent=1))
 
 
+def optim_cases():
+    """Adagrad / Adadelta / Adam (optim.hpp:83-137): 4 reference steps of two small nets, lr 0.01"""
+    out = {}
+    for name in ["mlp_small", "mnist_cnn_small"]:
+        spec, _ = small_specs()[name]
+        g = np.load(HERE / f"{name}.npz")
+        for kind in (1, 2, 3):
+            ref = O.Net(dict(spec, optimizer=kind, lr=0.01), "ref")
+            out[f"{name}_{kind}_losses"] = np.array([ref.train_minibatch(g["x"], g["labels"]) for _ in range(4)])
+            for i in range(ref.num_params()):
+                for w in (0, 3, 4):
+                    out[f"{name}_{kind}_{w}_{i}"] = ref.get(i, w)
+    np.savez_compressed(HERE / "optim.npz", **out)
+
+
 def main():
+    if sys.argv[1:] == ["optim"]:
+        optim_cases()
+        print("optimizer fixtures written to", HERE)
+        return
     if sys.argv[1:] == ["fit"]:
         fit_cases()
         print("fit fixtures written to", HERE)
@@ -194,6 +214,7 @@ def main():
     (HERE / "meta.json").write_text(json.dumps(meta, indent=1))
     fit_cases()
     checkpoint_cases()
+    optim_cases()
     print("golden fixtures written to", HERE)
 
 
