@@ -165,6 +165,11 @@ int b2n_load_network(b2n_net* net, const char* path, int with_state);
 int b2n_net_profile(b2n_net* net, long long batch, int steps, int max_ops, double* stats, char* names, int names_len,
                     int* n_ops);
 
+/* A source of Bernoulli uniforms: writes the next `count` draws of the caller's stream
+ * (std::generate_canonical<double,53> over its std::mt19937 -- what std::bernoulli_distribution
+ * consumes) to `out`. Called on the calling thread, in step order. */
+typedef void (*b2n_uniform_fn)(void* ctx, double* out, long long count);
+
 /* ---- RBM: replaces Rbm (energy.hpp:16-32) and cd_k_update (energy.hpp:131-171) ---- */
 int b2n_rbm_create(long long hidden, long long visible, int device, int precision, b2n_rbm** out);
 int b2n_rbm_destroy(b2n_rbm* rbm);
@@ -185,6 +190,16 @@ int b2n_rbm_stage(b2n_rbm* rbm, const float* v0_host, const double* uniforms_hos
 int b2n_rbm_run_staged(b2n_rbm* rbm, int steps, float lr, long long batch_global);
 int b2n_rbm_recon(b2n_rbm* rbm, double* recon);
 int b2n_rbm_stream(b2n_rbm* rbm, void** cuda_stream);
+/* dbn_pretrain (energy.hpp:208-240): greedy CD-1 training of a stack of `layers` RBMs (layer l's
+ * visible extent == layer l-1's hidden extent; all on one device). `data` (n x visible(0), host)
+ * is uploaded once; each layer trains `epochs` passes of CD-1 over its input in file order,
+ * `batch` rows per step, then its hidden means (rbm_transform_up, energy.hpp:122-126) become the
+ * next layer's input -- on the device. Uniforms: B x H per step from `fill`, layer by layer,
+ * epoch by epoch, batch by batch (the reference's single rng stream). recon_out[layer*epochs + e]
+ * = mean per-step reconstruction error. Errors: EPARAM (empty stack, batch < 1, epochs < 0),
+ * ESHAPE (extent chain, the reference's message). */
+int b2n_dbn_pretrain(b2n_rbm* const* stack, int layers, const float* data_host, long long n, int epochs, float lr,
+                     long long batch, b2n_uniform_fn fill, void* ctx, double* recon_out);
 int b2n_rbm_kernels_per_step(b2n_rbm* rbm, int* n);
 int b2n_rbm_profile(b2n_rbm* rbm, int steps, float lr, long long batch_global, int max_ops, double* stats, char* names,
                     int names_len, int* n_ops);

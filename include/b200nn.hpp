@@ -311,4 +311,30 @@ double cd_k_update(Rbm& rbm, const T& v0, int k, float lr, std::mt19937& rng) {
     return recon;
 }
 
+// dbn_pretrain (energy.hpp:208-240) with the reference's signature: the stack trains on the device
+// (data uploaded once, hidden means passed up on the device); `rng` supplies the Bernoulli
+// uniforms in the reference's order, drawn on this thread while the GPU runs the previous step.
+struct DbnReport {
+    std::vector<std::vector<double>> recon;  // [layer][epoch]
+};
+template <class T>
+DbnReport dbn_pretrain(std::vector<Rbm>& stack, const T& data, std::size_t epochs, float lr, std::size_t batch_size,
+                       std::mt19937& rng) {
+    if (data.rank() != 2) throw ShapeError("dbn_pretrain: data must be (rows, visible)");
+    const std::vector<float> xs = detail::pack_rows(data);
+    std::vector<b2n_rbm*> hs;
+    for (Rbm& r : stack) hs.push_back(r.handle());
+    std::vector<double> rec(std::max<std::size_t>(stack.size() * epochs, 1));
+    auto fill = [](void* ctx, double* out, long long count) {
+        std::mt19937& g = *static_cast<std::mt19937*>(ctx);
+        for (long long i = 0; i < count; ++i) out[i] = std::generate_canonical<double, 53>(g);
+    };
+    check(b2n_dbn_pretrain(hs.data(), (int)hs.size(), xs.data(), (long long)data.dim(0), (int)epochs, lr,
+                           (long long)batch_size, fill, &rng, rec.data()));
+    DbnReport r;
+    for (std::size_t l = 0; l < stack.size(); ++l)
+        r.recon.emplace_back(rec.begin() + (long)(l * epochs), rec.begin() + (long)((l + 1) * epochs));
+    return r;
+}
+
 }  // namespace b200nn

@@ -735,6 +735,15 @@ double orc_rbm_cd1(long long H, long long V, float* W, float* bv, float* bh, con
     return recon / double(B_global);
 }
 
+// rbm_transform_up (energy.hpp:122-126): hidden means of every row, the DBN layer-to-layer map
+void orc_rbm_transform_up(long long H, long long V, const float* W, const float* bh, const float* data, long long N,
+                          float* out) {
+    const size_t h = (size_t)H, vis = (size_t)V, n = (size_t)N;
+    gemm_nt(data, vis, W, vis, out, h, n, h, vis);
+    for (size_t r = 0; r < n; ++r)
+        for (size_t j = 0; j < h; ++j) out[r * h + j] = sigmoidf_ref(out[r * h + j] + bh[j]);
+}
+
 // Rbm::init (energy.hpp:31): glorot on w only, biases zero
 void orc_rbm_init(long long H, long long V, unsigned seed, float* W) {
     std::mt19937 rng(seed);

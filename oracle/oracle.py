@@ -88,6 +88,7 @@ def _declare(lib: C.CDLL, prefix: str) -> None:
         lib.orc_conv_backward.argtypes = [_F, C.c_longlong, C.c_longlong, C.c_longlong, C.c_longlong, _F,
                                           C.c_longlong, C.c_longlong, C.c_longlong, C.c_longlong, _F, _F, _F, _F]
         lib.orc_uniform_f32.argtypes = [C.c_uint, C.c_float, C.c_float, C.c_longlong, _F]
+        lib.orc_rbm_transform_up.argtypes = [C.c_longlong, C.c_longlong, _F, _F, _F, C.c_longlong, _F]
         lib.orc_canonical_f64.argtypes = [C.c_uint, C.c_longlong, _D]
         lib.orc_bernoulli_f32.argtypes = [C.c_uint, C.c_double, C.c_longlong, _F]
         lib.orc_uniform_int.argtypes = [C.c_uint, C.c_int, C.c_int, C.c_longlong, _I]
@@ -107,6 +108,8 @@ def _declare(lib: C.CDLL, prefix: str) -> None:
         lib.ref_rbm_destroy.argtypes = [C.c_void_p]
         lib.ref_save_network.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int]
         lib.ref_load_network.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_int]
+        lib.ref_dbn_pretrain.argtypes = [C.c_int, _LL, _LL, _F, _F, _F, _F, C.c_longlong, C.c_int, C.c_float,
+                                         C.c_longlong, C.c_uint, _D, C.c_char_p, C.c_int]
         lib.ref_set_threads.argtypes = [C.c_int]
         lib.ref_thread_count.restype = C.c_int
 
@@ -248,6 +251,70 @@ class Net:
         x = np.ascontiguousarray(x, np.float32)
         labels = np.ascontiguousarray(labels, np.int32)
         return getattr(self.lib, f"{self.p}_net_evaluate")(self.h, fptr(x), iptr(labels), labels.shape[0], batch)
+
+
+def rbm_transform_up(W, bh, data):
+    """rbm_transform_up (energy.hpp:122-126): sigmoid(data . W^T + bh)"""
+    W = np.ascontiguousarray(W, np.float32)
+    bh = np.ascontiguousarray(bh, np.float32)
+    data = np.ascontiguousarray(data, np.float32)
+    H, V = W.shape
+    out = np.zeros((data.shape[0], H), np.float32)
+    load().orc_rbm_transform_up(H, V, fptr(W), fptr(bh), fptr(data), data.shape[0], fptr(out))
+    return out
+
+
+def dbn_pretrain(stack, data, epochs, lr, batch, seed):
+    """dbn_pretrain (energy.hpp:208-240) restated over the oracle's CD-1: each layer trains with CD-1
+    on the previous layer's hidden means, batches in file order, ONE std::mt19937(seed) stream of
+    generate_canonical<double,53> draws across layers, epochs and batches (B x H per step).
+    stack = [(W, bv, bh)] (copied); returns (trained stack, recon[layer][epoch])."""
+    stack = [(np.array(W, np.float32), np.array(bv, np.float32), np.array(bh, np.float32)) for W, bv, bh in stack]
+    n = data.shape[0]
+    draws = sum(epochs * n * W.shape[0] for W, _, _ in stack)
+    u = canonical_f64(seed, draws)
+    pos = 0
+    cur = np.ascontiguousarray(data, np.float32)
+    recon = []
+    for li, (W, bv, bh) in enumerate(stack):
+        H = W.shape[0]
+        rl = []
+        for _ in range(epochs):
+            total, nb = 0.0, 0
+            for lo in range(0, n, batch):
+                hi = min(lo + batch, n)
+                r, W, bv, bh, _ = rbm_cd1(W, bv, bh, cur[lo:hi], lr, u[pos:pos + (hi - lo) * H].reshape(hi - lo, H))
+                pos += (hi - lo) * H
+                total += r
+                nb += 1
+            rl.append(total / nb)
+        stack[li] = (W, bv, bh)
+        recon.append(rl)
+        if li + 1 < len(stack):
+            cur = rbm_transform_up(W, bh, cur)
+    return stack, recon
+
+
+def ref_dbn_pretrain(stack, data, epochs, lr, batch, seed):
+    """the reference's own dbn_pretrain (needs oracle/_ref); same contract as dbn_pretrain()"""
+    lib = load("ref")
+    vis = np.array([w.shape[1] for w, _, _ in stack], np.int64)
+    hid = np.array([w.shape[0] for w, _, _ in stack], np.int64)
+    W = np.concatenate([np.ravel(w) for w, _, _ in stack]).astype(np.float32)
+    bv = np.concatenate([np.ravel(b) for _, b, _ in stack]).astype(np.float32)
+    bh = np.concatenate([np.ravel(b) for _, _, b in stack]).astype(np.float32)
+    data = np.ascontiguousarray(data, np.float32)
+    rec = np.zeros(len(stack) * epochs, np.float64)
+    err = C.create_string_buffer(512)
+    if lib.ref_dbn_pretrain(len(stack), vis.ctypes.data_as(_LL), hid.ctypes.data_as(_LL), fptr(W), fptr(bv), fptr(bh), fptr(data), data.shape[0],
+                            epochs, lr, batch, seed, dptr(rec), err, 512):
+        raise RuntimeError(err.value.decode())
+    out, ow, ov, oh = [], 0, 0, 0
+    for l in range(len(stack)):
+        V, H = int(vis[l]), int(hid[l])
+        out.append((W[ow:ow + H * V].reshape(H, V), bv[ov:ov + V], bh[oh:oh + H]))
+        ow, ov, oh = ow + H * V, ov + V, oh + H
+    return out, rec.reshape(len(stack), epochs).tolist()
 
 
 def ref_checkpoint(net: "Net", path: str, load: bool = False) -> str:

@@ -421,6 +421,47 @@ int ref_load_network(void* h, const char* path, char* err, int errlen) {
     return 0;
 }
 
+// the reference's dbn_pretrain (energy.hpp:208-240) over a stack of L binary RBMs, layer l being
+// hid[l] x vis[l]; W/bv/bh hold every layer's parameters back to back (in: initial, out: trained);
+// recon_out gets [layer][epoch]. Returns 0 or 1 with the exception text in err.
+int ref_dbn_pretrain(int L, const long long* vis, const long long* hid, float* W, float* bv, float* bh,
+                     const float* data, long long N, int epochs, float lr, long long batch, unsigned seed,
+                     double* recon_out, char* err, int errlen) {
+    try {
+        std::vector<Rbm> stack;
+        std::vector<long long> dims;
+        size_t ow = 0, ov = 0, oh = 0;
+        for (int l = 0; l < L; ++l) {
+            dims = {vis[l], hid[l]};
+            stack.emplace_back((size_t)hid[l], (size_t)vis[l]);
+            copy_in(stack.back().w, W + ow);
+            copy_in(stack.back().bv, bv + ov);
+            copy_in(stack.back().bh, bh + oh);
+            ow += (size_t)(vis[l] * hid[l]);
+            ov += (size_t)vis[l];
+            oh += (size_t)hid[l];
+        }
+        Tensor x = make_batch(data, N, {vis[0]});
+        std::mt19937 rng(seed);
+        DbnReport rep = dbn_pretrain(stack, x, (size_t)epochs, lr, (size_t)batch, rng);
+        ow = ov = oh = 0;
+        for (int l = 0; l < L; ++l) {
+            copy_out(stack[l].w, W + ow);
+            copy_out(stack[l].bv, bv + ov);
+            copy_out(stack[l].bh, bh + oh);
+            ow += (size_t)(vis[l] * hid[l]);
+            ov += (size_t)vis[l];
+            oh += (size_t)hid[l];
+            for (int e = 0; e < epochs; ++e) recon_out[l * epochs + e] = rep.recon[(size_t)l][(size_t)e];
+        }
+    } catch (const std::exception& e) {
+        std::strncpy(err, e.what(), (size_t)errlen - 1);
+        err[errlen - 1] = 0;
+        return 1;
+    }
+    return 0;
+}
+
 void ref_net_forward(void* h, const float* x, long long B, float* probs, int* argmax) {
     RefNet& rn = *static_cast<RefNet*>(h);
     Tensor pred = forward_batch(rn.net, make_batch(x, B, rn.net.input));

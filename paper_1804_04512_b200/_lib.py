@@ -115,6 +115,8 @@ _SIGS = {
     "b2n_net_evaluate": ([_VP, _F, _I, C.c_longlong, _D], C.c_int),
     "b2n_save_network": ([_VP, C.c_char_p, C.c_int], C.c_int),
     "b2n_load_network": ([_VP, C.c_char_p, C.c_int], C.c_int),
+    "b2n_dbn_pretrain": ([C.POINTER(_VP), C.c_int, _F, C.c_longlong, C.c_int, C.c_float, C.c_longlong, _VP, _VP,
+                          _D], C.c_int),
     "b2n_batch_order": ([C.c_longlong, C.c_uint, C.c_int, _LL], C.c_int),
     "b2n_net_stream": ([_VP, C.POINTER(_VP)], C.c_int),
     "b2n_net_kernels_per_step": ([_VP, C.c_longlong, _I], C.c_int),

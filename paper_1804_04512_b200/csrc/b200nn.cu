@@ -178,6 +178,46 @@ int b2n_load_network(b2n_net* net, const char* path, int with_state) {
         net->impl.load(path, with_state != 0);
     });
 }
+int b2n_dbn_pretrain(b2n_rbm* const* stack, int layers, const float* data, long long n, int epochs, float lr,
+                     long long batch, b2n_uniform_fn fill, void* ctx, double* recon_out) {
+    return guard([&] {
+        if (layers < 1 || !stack) throw b2n::Error(B2N_EPARAM, "dbn_pretrain: empty stack");
+        if (batch < 1) throw b2n::Error(B2N_EPARAM, "dbn_pretrain: batch_size must be >= 1");
+        if (epochs < 0) throw b2n::Error(B2N_EPARAM, "dbn_pretrain: epochs must be >= 0");
+        if (!fill) throw b2n::Error(B2N_EPARAM, "dbn_pretrain: no uniform source");
+        long long in = stack[0]->impl.visible();
+        for (int l = 0; l < layers; ++l) {  // energy.hpp:216-224
+            const long long v = stack[l]->impl.visible();
+            if (v != in)
+                throw b2n::Error(B2N_ESHAPE, "dbn_pretrain: layer " + std::to_string(l) + " expects " + std::to_string(v) +
+                                                 " visible units but layer " + std::to_string(l ? l - 1 : 0) +
+                                                 (l ? " provides " : "'s input provides ") + std::to_string(in));
+            in = stack[l]->impl.hidden();
+        }
+        if (n < 1) throw b2n::Error(B2N_EDATA, "dbn_pretrain: empty dataset");
+        b2n::Rbm& r0 = stack[0]->impl;
+        const long long V0 = r0.visible();
+        b2n::DevMem cur, next;
+        cur.alloc((size_t)(n * r0.ld_visible() * 4));
+        B2N_CUDA(cudaMemcpy2DAsync(cur.p, r0.ld_visible() * 4, data, V0 * 4, V0 * 4, n, cudaMemcpyHostToDevice,
+                                   r0.stream()));
+        B2N_CUDA(cudaStreamSynchronize(r0.stream()));
+        for (int l = 0; l < layers; ++l) {
+            b2n::Rbm& r = stack[l]->impl;
+            for (int e = 0; e < epochs; ++e) {
+                const double rc = r.train_epoch(cur.as<float>(), n, batch, lr, fill, ctx);
+                if (recon_out) recon_out[(size_t)l * epochs + e] = rc;
+            }
+            if (l + 1 < layers) {
+                next.alloc((size_t)(n * stack[l + 1]->impl.ld_visible() * 4));
+                r.transform_up(cur.as<float>(), n, next.as<float>());
+                B2N_CUDA(cudaStreamSynchronize(r.stream()));
+                std::swap(cur.p, next.p);  // DevMem is not movable: swap the owned pointers
+                std::swap(cur.bytes, next.bytes);
+            }
+        }
+    });
+}
 int b2n_batch_order(long long n, unsigned seed, int epoch, long long* order_out) {
     return guard([&] {
         if (n < 1) throw b2n::Error(B2N_EPARAM, "batch_iterator: empty dataset");

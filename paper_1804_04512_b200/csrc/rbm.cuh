@@ -20,6 +20,17 @@
 
 namespace b2n {
 
+// dbn_pretrain's per-step reconstruction error: the step's (tile, row) partials summed exactly as
+// Rbm::recon() does (rows outer, tiles inner), / batch, added to the epoch sum (energy.hpp:232)
+static __global__ void recon_accum_kernel(const double* __restrict__ part, int tiles, long long cap, long long B,
+                                          double* acc) {
+    if (threadIdx.x != 0) return;
+    double r = 0.0;
+    for (long long b = 0; b < B; ++b)
+        for (int t = 0; t < tiles; ++t) r += part[t * cap + b];
+    *acc += r / (double)B;
+}
+
 class Rbm {
   public:
     Rbm(long long H, long long V, int device, int precision)
@@ -35,6 +46,8 @@ class Rbm {
     }
     ~Rbm() {
         plans_.clear();
+        for (cudaEvent_t e : uev_)
+            if (e) cudaEventDestroy(e);
         if (stream_) cudaStreamDestroy(stream_);
     }
 
@@ -118,6 +131,65 @@ class Rbm {
         dp_ = std::make_unique<DpComm>();
         dp_->init(id, rank, world);
         plans_.clear();
+    }
+    long long hidden() const { return H_; }
+    long long visible() const { return V_; }
+    long long ld_visible() const { return round_up(V_ + 1, 8); }  // row pitch of a visible-side data matrix
+
+    // One epoch of dbn_pretrain's inner loop (energy.hpp:226-233): CD-1 over rows [0, n) of a
+    // device-resident data matrix (pitch ld_visible()) in file order, `batch` rows per step (the
+    // last step takes the remainder). The Bernoulli uniforms come from `fill` (the caller's
+    // mt19937 stream, B x H per step, in step order) through two pinned buffers so the host
+    // draws step i+1 while the GPU runs step i. The per-step reconstruction errors are summed on
+    // the device in the reference's order; one host synchronisation per epoch.
+    double train_epoch(const float* data, long long n, long long batch, float lr, b2n_uniform_fn fill, void* ctx) {
+        if (dp_) throw Error(B2N_EPARAM, "dbn_pretrain: data-parallel RBMs step through run_staged");
+        ensure_capacity(std::min(batch, n), 1);
+        const long long per = std::min(batch, n) * H_;
+        for (int j = 0; j < 2; ++j) {
+            if (ubuf_[j].bytes < (size_t)per * 8) ubuf_[j].alloc((size_t)per * 8);
+            if (!uev_[j]) B2N_CUDA(cudaEventCreateWithFlags(&uev_[j], cudaEventDisableTiming));
+        }
+        if (!racc_.p) racc_.alloc(16);
+        B2N_CUDA(cudaMemsetAsync(racc_.p, 0, 8, stream_));
+        const long long ldd = ld_visible();
+        long long batches = 0;
+        bool pending[2] = {false, false};
+        for (long long lo = 0; lo < n; lo += batch, ++batches) {
+            const long long B = std::min(batch, n - lo);
+            const int j = (int)(batches & 1);
+            if (pending[j]) B2N_CUDA(cudaEventSynchronize(uev_[j]));  // its previous H2D has drained
+            fill(ctx, ubuf_[j].as<double>(), B * H_);
+            B2N_CUDA(cudaMemcpyAsync(U_.p, ubuf_[j].p, (size_t)(B * H_ * 8), cudaMemcpyHostToDevice, stream_));
+            B2N_CUDA(cudaEventRecord(uev_[j], stream_));
+            pending[j] = true;
+            B2N_CUDA(cudaMemcpy2DAsync(Vcat_.p, ldv_ * 4, data + lo * ldd, ldd * 4, V_ * 4, B, cudaMemcpyDeviceToDevice,
+                                       stream_));
+            Plan& pl = plan_for(B, 1, lr, B);
+            launch(pl);
+            recon_accum_kernel<<<1, 32, 0, stream_>>>(recon_.as<double>(), recon_tiles_, cap_, B, racc_.as<double>());
+            B2N_CUDA(cudaGetLastError());
+        }
+        double acc = 0.0;
+        B2N_CUDA(cudaMemcpyAsync(&acc, racc_.p, 8, cudaMemcpyDeviceToHost, stream_));
+        B2N_CUDA(cudaStreamSynchronize(stream_));
+        last_B_ = 0;
+        return acc / (double)batches;
+    }
+
+    // rbm_transform_up (energy.hpp:122-126): out = sigmoid(data . W^T + bh) for n rows, data pitch
+    // ld_visible(), out pitch round_up(H + 1, 8) (the next layer's ld_visible())
+    void transform_up(const float* data, long long n, float* out) {
+        EpiParams e = epi_default();
+        e.C = out;
+        e.ldc = round_up(H_ + 1, 8);
+        e.bias = W_.as<float>() + V_;
+        e.bias_stride = ldw_;
+        e.act = ACT_SIGMOID;
+        GemmLaunch g = plan_gemm((int)n, (int)H_, (int)V_, {data, ld_visible(), false}, {W_.as<float>(), ldw_, false},
+                                 EPI_BIAS_ACT, e, x3_);
+        g.run(stream_);
+        B2N_CUDA(cudaGetLastError());
     }
     cudaStream_t stream() const { return stream_; }
     int kernels_per_step() const { return last_kernels_; }
@@ -382,6 +454,9 @@ class Rbm {
     int kcap_ = 0;
     DevMem W_, G_, Vcat_, Hcat_, HS_, U_, recon_;
     DevMem fused_ws_, gbar_, trace_;
+    HostPinned ubuf_[2];       // train_epoch: double-buffered uniforms
+    cudaEvent_t uev_[2] = {nullptr, nullptr};
+    DevMem racc_;              // train_epoch: device sum of per-step reconstruction errors
   public:
     void read_trace(unsigned long long* h) {
         B2N_CUDA(cudaDeviceSynchronize());

@@ -112,6 +112,9 @@ inline void spin_sync(cudaStream_t st) {
 struct DevMem {
     void* p = nullptr;
     size_t bytes = 0;
+    DevMem() = default;
+    DevMem(const DevMem&) = delete;  // owns p
+    DevMem& operator=(const DevMem&) = delete;
     void alloc(size_t n) {
         release();
         if (n == 0) return;
@@ -369,12 +372,13 @@ struct TraceRegistry {
     int used = 0;
     bool on = false;
     static TraceRegistry& get() {
-        static TraceRegistry r = [] {
-            TraceRegistry t;
+        static TraceRegistry r;
+        static const bool init = [] {
             const char* e = std::getenv("B2N_TRACE");
-            t.on = e && e[0] == '1';
-            return t;
+            r.on = e && e[0] == '1';
+            return true;
         }();
+        (void)init;
         return r;
     }
     unsigned long long* next() {

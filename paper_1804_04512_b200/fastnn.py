@@ -422,6 +422,49 @@ def cd_k_update(rbm: Rbm, v0, k: int, lr: float, uniforms, batch_global: int | N
     return out.value
 
 
+class Mt19937:
+    """A std::mt19937 stream (numpy's MT19937 with the legacy init_genrand seeding is the same
+    generator) yielding std::generate_canonical<double,53> values: two 32-bit draws per double,
+    (lo + hi * 2^32) / 2^64, clamped below 1 -- exactly what std::bernoulli_distribution consumes."""
+
+    def __init__(self, seed: int):
+        self._rs = np.random.RandomState(seed)
+
+    def canonical(self, n: int) -> np.ndarray:
+        u = self._rs.randint(0, 2 ** 32, size=2 * n, dtype=np.uint64).reshape(n, 2).astype(np.float64)
+        c = (u[:, 0] + u[:, 1] * 4294967296.0) / 18446744073709551616.0
+        return np.where(c >= 1.0, np.nextafter(1.0, 0.0), c)
+
+
+_UNIFORM_FN = C.CFUNCTYPE(None, C.c_void_p, C.POINTER(C.c_double), C.c_longlong)
+
+
+@dataclass
+class DbnReport:
+    """fastnn::DbnReport (energy.hpp:199-201): recon[layer][epoch]"""
+    recon: list = field(default_factory=list)
+
+
+def dbn_pretrain(stack: list, data, epochs: int, lr: float, batch_size: int, rng: Mt19937) -> DbnReport:
+    """fastnn::dbn_pretrain (energy.hpp:208-240): greedy CD-1 over a stack of Rbm on one device,
+    data resident in HBM, each layer's hidden means computed on the device for the next; the
+    Bernoulli uniforms are drawn from `rng` in the reference's order (B x H per step)."""
+    data = np.ascontiguousarray(data, np.float32)
+    if data.ndim != 2:
+        raise ShapeError("dbn_pretrain: data must be (rows, visible)")
+    arr = (C.c_void_p * max(len(stack), 1))(*[r.handle.value if hasattr(r.handle, "value") else r.handle
+                                               for r in stack])
+
+    def fill(_ctx, out, count):
+        np.ctypeslib.as_array(out, shape=(count,))[:] = rng.canonical(count)
+
+    cb = _UNIFORM_FN(fill)
+    rec = np.zeros(max(len(stack) * epochs, 1))
+    _lib.call("b2n_dbn_pretrain", arr, len(stack), _f(data), data.shape[0], epochs, lr, batch_size,
+              C.cast(cb, C.c_void_p), None, _d(rec))
+    return DbnReport([list(rec[l * epochs:(l + 1) * epochs]) for l in range(len(stack))])
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _lib.call("b2n_nccl_unique_id", buf)

@@ -10,6 +10,7 @@ padded ImageNet-shaped net, the SURVEY 8(c) composite of reference primitives.
     python tests/golden/make_golden.py fit    # only fit.npz (fit / evaluate / batch order)
     python tests/golden/make_golden.py checkpoint  # only *.fnn1 + checkpoint_errors.json
     python tests/golden/make_golden.py optim  # only optim.npz (Adagrad / Adadelta / Adam)
+    python tests/golden/make_golden.py dbn    # only dbn.npz (dbn_pretrain)
 """
 from __future__ import annotations
 
@@ -139,7 +140,35 @@ def optim_cases():
     np.savez_compressed(HERE / "optim.npz", **out)
 
 
+DBN_CASE = {"dims": [40, 24, 16], "n": 50, "epochs": 2, "lr": 0.1, "batch": 16, "seed": 5}
+
+
+def dbn_case_inputs():
+    c = DBN_CASE
+    dims = c["dims"]
+    stack = [(O.rbm_init(dims[l + 1], dims[l], 42 + l), O.uniform_f32(9 + l, dims[l], -0.1, 0.1),
+              O.uniform_f32(19 + l, dims[l + 1], -0.1, 0.1)) for l in range(len(dims) - 1)]
+    data = O.bernoulli_f32(3, 0.5, c["n"] * dims[0]).reshape(c["n"], dims[0])
+    return stack, data
+
+
+def dbn_cases():
+    """the reference's dbn_pretrain (energy.hpp:208-240) on a 40-24-16 stack, 50 rows, batch 16
+    (a partial last batch), 2 epochs, one mt19937(5) stream"""
+    c = DBN_CASE
+    stack, data = dbn_case_inputs()
+    out, recon = O.ref_dbn_pretrain(stack, data, c["epochs"], c["lr"], c["batch"], c["seed"])
+    g = {"recon": np.array(recon)}
+    for l, (W, bv, bh) in enumerate(out):
+        g[f"W{l}"], g[f"bv{l}"], g[f"bh{l}"] = W, bv, bh
+    np.savez_compressed(HERE / "dbn.npz", **g)
+
+
 def main():
+    if sys.argv[1:] == ["dbn"]:
+        dbn_cases()
+        print("dbn fixtures written to", HERE)
+        return
     if sys.argv[1:] == ["optim"]:
         optim_cases()
         print("optimizer fixtures written to", HERE)
@@ -215,6 +244,7 @@ def main():
     fit_cases()
     checkpoint_cases()
     optim_cases()
+    dbn_cases()
     print("golden fixtures written to", HERE)
 
 
