@@ -193,10 +193,12 @@ class RbmWork:
         return _profile(self.F._lib, "b2n_rbm_profile", self.rbm.handle, steps, self.lr, self.Bg)
 
     def d2h_bytes(self):
-        # per-(slice,row) reconstruction partials read back: 8 slices for the fused step, one per
-        # 64-column tile of the visible GEMM on the split path
-        tiles = 8 if self.kernels_per_step() == 1 else (self.V + 63) // 64
-        return self.B * 8 * tiles
+        # fused step, single GPU, pinned inputs: the kernel reads v0 and the uniforms from host memory
+        # and stores the finished recon (one double) into host-mapped memory; otherwise the per-
+        # (tile, row) reconstruction partials are copied back (one tile per 64 visible columns)
+        if self.kernels_per_step() == 1 and self.dist.world == 1:
+            return 8
+        return self.B * 8 * ((self.V + 63) // 64)
 
 
 class NetWork:

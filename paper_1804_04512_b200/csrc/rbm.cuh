@@ -20,15 +20,32 @@
 
 namespace b2n {
 
-// dbn_pretrain's per-step reconstruction error: the step's (tile, row) partials summed exactly as
-// Rbm::recon() does (rows outer, tiles inner), / batch, added to the epoch sum (energy.hpp:232)
+// The one summation order of a step's (tile, row) reconstruction partials, shared by the host
+// (Rbm::recon), dbn_pretrain's device accumulator and the fused kernel's in-kernel sum: 32 lanes
+// take rows lane, lane + 32, ... (tiles inner, in order), then the xor butterfly of a warp
+// shuffle reduction (lane 0's result), simulated lane by lane here.
+__host__ __device__ inline double recon_tree_sum(const double* part, int tiles, long long cap, long long B) {
+    double lane[32];
+    for (int l = 0; l < 32; ++l) {
+        double a = 0.0;
+        for (long long r = l; r < B; r += 32)
+            for (int t = 0; t < tiles; ++t) a += part[t * cap + r];
+        lane[l] = a;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        double nx[32];
+        for (int l = 0; l < 32; ++l) nx[l] = lane[l] + lane[l ^ o];
+        for (int l = 0; l < 32; ++l) lane[l] = nx[l];
+    }
+    return lane[0];
+}
+
+// dbn_pretrain's per-step reconstruction error (recon_tree_sum / batch) added to the epoch sum
+// (energy.hpp:232)
 static __global__ void recon_accum_kernel(const double* __restrict__ part, int tiles, long long cap, long long B,
                                           double* acc) {
     if (threadIdx.x != 0) return;
-    double r = 0.0;
-    for (long long b = 0; b < B; ++b)
-        for (int t = 0; t < tiles; ++t) r += part[t * cap + b];
-    *acc += r / (double)B;
+    *acc += recon_tree_sum(part, tiles, cap, B) / (double)B;
 }
 
 class Rbm {
@@ -48,6 +65,7 @@ class Rbm {
         plans_.clear();
         for (cudaEvent_t e : uev_)
             if (e) cudaEventDestroy(e);
+        if (recon_host_) cudaFreeHost(recon_host_);
         if (stream_) cudaStreamDestroy(stream_);
     }
 
@@ -79,9 +97,28 @@ class Rbm {
     double cd_k(const float* v0, long long B, int k, float lr, const double* u, long long Bg) {
         if (k < 1) throw Error(B2N_EPARAM, "cd_k_update: k must be >= 1, got " + std::to_string(k));
         if (B < 1 || Bg < B) throw Error(B2N_ESHAPE, "cd_k_update: need 1 <= batch <= batch_global");
-        stage(v0, u, B, k);
+        ensure_capacity(B, k);
         Plan& pl = plan_for(B, k, lr, Bg);
-        launch(pl);
+        const float* v0d = device_alias(v0);
+        const double* ud = device_alias(u);
+        if (pl.fused && v0d && ud && V_ % 4 == 0) {
+            // pinned caller buffers: the fused kernel reads v0 and the uniforms itself (zero-copy),
+            // launched directly with this call's pointers instead of staging copies + the graph
+            staged_B_ = B;
+            staged_k_ = k;
+            prepare(pl);
+            RbmFusedParams rp = pl.rp;
+            rp.v0_src = v0d;
+            rp.ld_src = V_;
+            rp.u_src = ud;
+            rp.recon_out = recon_host_dev_;
+            recon_mapped_ = true;
+            launch_ex(rbm_cd1_fused_kernel, dim3(kRfSlices, rp.jt), dim3(kRfThreads), (size_t)kRfSmem, stream_, 1u,
+                      pl.maps[0], pl.maps[1], pl.maps[2], pl.maps[3], pl.maps[4], pl.maps[5], rp);
+        } else {
+            stage(v0, u, B, k);
+            launch(pl);
+        }
         if (dp_) throw Error(B2N_EPARAM, "data-parallel RBM steps through run_staged");
         last_B_ = B;
         last_Bg_ = Bg;
@@ -103,15 +140,15 @@ class Rbm {
         last_Bg_ = pl.Bg;
     }
     double recon() {  // sum of the per-(tile,row) partials / batch_global
+        if (recon_mapped_) {  // the fused step already wrote it to host-mapped memory
+            spin_sync(stream_);
+            return *reinterpret_cast<volatile double*>(recon_host_);
+        }
         const long long nt = recon_tiles_;
         // partials are [tile][cap_]: copy through the last tile's rows
         B2N_CUDA(cudaMemcpyAsync(h_recon_.p, recon_.p, ((nt - 1) * cap_ + last_B_) * 8, cudaMemcpyDeviceToHost, stream_));
         spin_sync(stream_);
-        const double* r = h_recon_.as<double>();
-        double acc = 0.0;
-        for (long long b = 0; b < last_B_; ++b)
-            for (long long t = 0; t < nt; ++t) acc += r[t * cap_ + b];
-        return acc / (double)last_Bg_;
+        return recon_tree_sum(h_recon_.as<double>(), (int)nt, cap_, last_B_) / (double)last_Bg_;
     }
     void last_states(float* h0, float* hs, float* v1, float* h1) {
         const long long B = last_B_;
@@ -208,6 +245,9 @@ class Rbm {
         std::vector<Op> ops;
         int nk = 0;
         int recon_tiles = 1;
+        bool fused = false;         // rp / maps describe the single fused launch
+        RbmFusedParams rp;
+        CUtensorMap maps[6];
         cudaGraphExec_t graph = nullptr;
         ~Plan() {
             if (graph) cudaGraphExecDestroy(graph);
@@ -315,6 +355,14 @@ class Rbm {
         rp.gbar = gbar_.as<unsigned>();
         rp.alpha = pl.lr / static_cast<float>(pl.Bg);
         rp.jt = jt;
+        if (!recon_host_) {
+            B2N_CUDA(cudaHostAlloc((void**)&recon_host_, 64, cudaHostAllocMapped));
+            B2N_CUDA(cudaHostGetDevicePointer((void**)&recon_host_dev_, recon_host_, 0));
+            done_.alloc(64);
+        }
+        rp.recon_out = nullptr;  // set per direct (zero-copy) launch: a host-mapped store costs the
+        rp.done = done_.as<unsigned>();  // device-resident step ~3 us at its end
+        rp.bg = (double)pl.Bg;
         if (std::getenv("B2N_RBM_TRACE")) {
             if (!trace_.p) trace_.alloc(256 * 8);
             rp.trace = trace_.as<unsigned long long>();
@@ -331,6 +379,10 @@ class Rbm {
             launch_ex(rbm_cd1_fused_kernel, dim3(kRfSlices, jt), dim3(kRfThreads), (size_t)kRfSmem, st, 1u, mVk, mWk,
                       mHSk, mWmn, mVmn, mHmn, rp);
         }, "rbm.cd1_fused", flops, bytes));
+        pl.fused = true;
+        pl.rp = rp;
+        const CUtensorMap ms[6] = {mVk, mWk, mHSk, mWmn, mVmn, mHmn};
+        std::memcpy(pl.maps, ms, sizeof(ms));
         pl.recon_tiles = kRfSlices;
         pl.nk = 1;
         last_kernels_ = 1;
@@ -419,7 +471,21 @@ class Rbm {
         last_kernels_ = pl.nk;
     }
 
-    void launch(Plan& pl) {
+    // device alias of a host pointer the GPU can read directly (pinned + mapped under UVA), else null
+    static const void* device_alias_v(const void* h) {
+        cudaPointerAttributes a;
+        if (cudaPointerGetAttributes(&a, h) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        return a.type == cudaMemoryTypeHost ? a.devicePointer : nullptr;
+    }
+    template <class T>
+    static const T* device_alias(const T* h) {
+        return static_cast<const T*>(device_alias_v(h));
+    }
+
+    void prepare(Plan& pl) {
         if (hcol_B_ != pl.B) {  // the +1 / -1 column of Hcat for this batch split
             float* Hc = Hcat_.as<float>();
             const long long B = pl.B;
@@ -429,6 +495,11 @@ class Rbm {
             hcol_B_ = pl.B;
         }
         recon_tiles_ = pl.recon_tiles;
+        recon_mapped_ = false;
+    }
+
+    void launch(Plan& pl) {
+        prepare(pl);
         if (!pl.graph) {
             cudaGraph_t graph;
             B2N_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
@@ -468,6 +539,10 @@ class Rbm {
     int staged_k_ = 1;
     int last_kernels_ = 0;
     int recon_tiles_ = 1;
+    bool recon_mapped_ = false;
+    double* recon_host_ = nullptr;      // cudaHostAllocMapped: the fused step's recon
+    double* recon_host_dev_ = nullptr;  // its device alias
+    DevMem done_;
     long long hcol_B_ = -1;
     std::vector<std::unique_ptr<Plan>> plans_;
     std::unique_ptr<DpComm> dp_;

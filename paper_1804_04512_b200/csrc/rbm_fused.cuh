@@ -46,7 +46,17 @@ struct RbmFusedParams {
     unsigned long long* trace;  // bring-up: phase timestamps (clock64) of CTA (0,0) and (7,7), null normally
     float alpha;       // lr / B_global
     int jt;            // hidden tiles
+    double* recon_out;  // host-mapped: the step's reconstruction error, written by the last CTA (or null)
+    unsigned* done;     // CTAs finished (last-CTA election for recon_out)
+    double bg;          // batch_global (the recon divisor, energy.hpp:144)
+    // zero-copy inputs (or null): v0 rows (pitch ld_src floats) and the uniforms [B][H] read straight
+    // from device-accessible host memory (pinned user buffers) -- no staging copies before the step
+    const float* v0_src;
+    long long ld_src;
+    const double* u_src;
 };
+
+__device__ __forceinline__ unsigned* sbar_of(const RbmFusedParams& p, int s) { return p.gbar + 2 * s; }
 
 // barrier over the nblocks CTAs that share the counter pair gbar = [count, generation]
 __device__ __forceinline__ void rf_grid_sync(unsigned* gbar, unsigned nblocks) {
@@ -201,6 +211,30 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
         p.trace[128 + blockIdx.y * gridDim.x + blockIdx.x] = t;
     }
+    if (p.v0_src) {
+        // zero-copy v0: CTA (s, j) moves rows [16 j, 16 j + 16) of visible slice s into Vcat; the 8 CTAs
+        // of slice s then meet at the slice barrier before phase 1 reads the slice by TMA
+        const int vlo = v0c, vhi = min(v0c + kRfSliceW, V);
+        const int w4 = (vhi - vlo) / 4;  // V % 4 == 0 (host-checked)
+        for (int idx = threadIdx.x; idx < 16 * w4; idx += kRfThreads) {
+            const int r = 16 * j + idx / w4, c = vlo + (idx % w4) * 4;
+            if (r < B)
+                *reinterpret_cast<float4*>(p.Vcat + (long long)r * p.ldv + c) =
+                    *reinterpret_cast<const float4*>(p.v0_src + (long long)r * p.ld_src + c);
+        }
+        rf_grid_sync(sbar_of(p, s), gridDim.y);
+    }
+    // the phase-1 sampling uniforms of this thread (rows 16 s + tid / 16, hidden 4 (tid % 16) of tile j),
+    // loaded after v0 (which phase 1 needs first) so a host-memory read overlaps the phase-1 product
+    double upre[4] = {2.0, 2.0, 2.0, 2.0};
+    {
+        const int r = 16 * s + (threadIdx.x >> 4), c = (threadIdx.x & 15) * 4;
+        const double* usrc = p.u_src ? p.u_src : p.u;
+        if (r < B)
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (h0c + c + i < H) upre[i] = usrc[(long long)r * H + h0c + c + i];
+    }
     const uint32_t id_h = umma_idesc_tf32(128, kRfTileH, 0, 0);   // [batch x hidden], both K-major
     const uint32_t id_v = umma_idesc_tf32(128, kRfSliceW, 0, 1);  // [batch x visible], W MN-major
     const uint32_t id_w = umma_idesc_tf32(128, kRfTileH, 1, 1);   // [visible x hidden], both MN-major
@@ -253,7 +287,7 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
             for (int i = 0; i < 4; ++i) {
                 const int h = h0c + c + i;
                 bh[i] = h < H ? p.W[(long long)h * p.ldw + V] : 0.0f;
-                uu[i] = first && h < H ? p.u[(long long)r * H + h] : 2.0;
+                uu[i] = upre[i];
             }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
@@ -401,6 +435,29 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
     }
     __syncthreads();
     mark();
+    // the step's reconstruction error straight into host-mapped memory: the last CTA to finish sums
+    // the (slice, row) partials written in phase 2 (rows over lanes, slices in order, then a fixed
+    // shuffle tree) -- no device-to-host copy behind the step
+    if (p.recon_out) {
+        __shared__ unsigned s_last;
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_last = atomicAdd(p.done, 1u) == gridDim.x * gridDim.y - 1;
+        }
+        __syncthreads();
+        if (s_last && warp == 0) {
+            const int lane = threadIdx.x & 31;
+            double acc = 0.0;
+            for (int r = lane; r < B; r += 32)
+                for (int s2 = 0; s2 < kRfSlices; ++s2) acc += __ldcg(p.row_part + (long long)s2 * p.cap + r);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (lane == 0) {
+                *reinterpret_cast<volatile double*>(p.recon_out) = acc / p.bg;
+                *p.done = 0;
+            }
+        }
+    }
     if (p.trace && threadIdx.x == 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -57,3 +57,31 @@ def test_k_below_one(gpu):
     rbm = F.Rbm(2, 2)
     with pytest.raises(F.ParamError):
         F.cd_k_update(rbm, np.zeros((1, 2), np.float32), 0, 0.1, np.zeros(2))
+
+
+def test_zero_copy_pinned_inputs_match_staged(gpu):
+    """pinned caller buffers take the zero-copy fused launch (the kernel reads v0 and the uniforms
+    from host memory); pageable ones are staged by copies. Same kernel arithmetic: bitwise equal."""
+    import torch
+    from paper_1804_04512_b200 import fastnn as F
+    B, V, H = 100, 784, 500
+    v0 = O.bernoulli_f32(3, 0.5, B * V).reshape(B, V)
+    u = O.canonical_f64(5, B * H).reshape(B, H)
+    v0p = torch.empty((B, V), dtype=torch.float32, pin_memory=True).numpy()
+    up = torch.empty((B, H), dtype=torch.float64, pin_memory=True).numpy()
+    v0p[:] = v0
+    up[:] = u
+    a, b = F.Rbm(H, V), F.Rbm(H, V)
+    a.init(42)
+    b.init(42)
+    for step in range(3):
+        ra = F.cd_k_update(a, v0, 1, 0.1, u)
+        rb = F.cd_k_update(b, v0p, 1, 0.1, up)
+        assert ra == rb, step
+        v0p[:] = (O.bernoulli_f32(10 + step, 0.5, B * V).reshape(B, V))
+        v0[:] = v0p
+    for x, y in zip(a.get(), b.get()):
+        assert np.array_equal(x, y)
+    sa, sb = a.last_states(B), b.last_states(B)
+    for x, y in zip(sa, sb):
+        assert np.array_equal(x, y)
