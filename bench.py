@@ -201,6 +201,53 @@ class RbmWork:
         return self.B * 8 * ((self.V + 63) // 64)
 
 
+class CrbmWork:
+    """CD-1 of the MNIST-shaped convolutional RBM (configs.CRBM), single GPU."""
+    name = "crbm"
+
+    def __init__(self, dist: Dist, precision: int, nccl_id):
+        from oracle import oracle as O  # synthetic-input generators (std::mt19937 streams), not the measured path
+        from paper_1804_04512_b200 import configs as CF, fastnn as F
+        if dist.world > 1:
+            raise RuntimeError("the convolutional RBM step runs on one GPU (no data-parallel build yet)")
+        c = CF.CRBM
+        self.Bg = self.B = c["batch_size"]
+        self.lr = c["lr"]
+        shp = (c["c_in"], c["h"], c["w"])
+        oh, ow = c["h"] - c["kh"] + 1, c["w"] - c["kw"] + 1
+        v0 = O.bernoulli_f32(3, 0.5, self.B * int(np.prod(shp))).reshape((self.B,) + shp)
+        u = O.canonical_f64(5, self.B * c["k"] * oh * ow)
+        self.m = F.Crbm(*shp, c["k"], c["kh"], c["kw"], device=dist.local, precision=precision)
+        self.m.init(c["seed"])
+        self.m.stage(v0, u)
+        self.v0_h = pinned(v0.shape, np.float32)
+        self.v0_h[:] = v0
+        self.u_h = pinned(u.shape, np.float64)
+        self.u_h[:] = u
+        self.F = F
+        self.config = {"workload": "mnist_crbm_cd1", "model": f"CRBM 1x28x28, {c['k']} kernels 5x5, binary, CD-1",
+                       "global_batch": self.B, "local_batch": self.B, "parallelism": "dp1", "lr": self.lr}
+        self.h2d = v0.nbytes + u.nbytes
+
+    def stream(self):
+        return self.m.stream_handle()
+
+    def step(self, n=1):
+        self.m.run_staged(n, self.lr, self.Bg)
+
+    def e2e_step(self):
+        return self.F.crbm_cd_update(self.m, self.v0_h, self.lr, self.u_h)
+
+    def kernels_per_step(self):
+        return _kernels(self.F._lib, "b2n_crbm_kernels_per_step", self.m.handle)
+
+    def profile(self, steps):
+        return _profile(self.F._lib, "b2n_crbm_profile", self.m.handle, steps, self.lr, self.Bg)
+
+    def d2h_bytes(self):
+        return 8
+
+
 class NetWork:
     def __init__(self, name: str, dist: Dist, precision: int, nccl_id):
         from oracle import oracle as O
@@ -282,6 +329,8 @@ def _profile(lib, fn, h, *args):
 
 
 def make_work(name, dist, precision, nccl_id):
+    if name == "crbm":
+        return CrbmWork(dist, precision, nccl_id)
     return RbmWork(dist, precision, nccl_id) if name == "rbm" else NetWork(name, dist, precision, nccl_id)
 
 
@@ -377,6 +426,24 @@ def cpu_reference(name: str, budget_s: float, min_steps: int = 2, max_steps: int
                                            O.dptr(u), None, None, None, None, None, None, None)
             done = lambda: None  # noqa: E731
         what = "cd_k_update(k=1)"
+    elif name == "crbm":
+        c = CF.CRBM
+        B = c["batch_size"]
+        shp = (c["c_in"], c["h"], c["w"], c["k"], c["kh"], c["kw"])
+        v0 = O.bernoulli_f32(3, 0.5, B * c["c_in"] * c["h"] * c["w"])
+        if kind == "reference":
+            h = lib.ref_crbm_create(*shp, c["seed"], O.fptr(v0), B, 5)
+            step = lambda: lib.ref_crbm_step(h, c["lr"])  # noqa: E731
+            done = lambda: lib.ref_crbm_destroy(h)  # noqa: E731
+            what = "crbm_cd_update"
+        else:
+            ker = O.crbm_init(c["c_in"], c["h"], c["w"], c["k"], c["kh"], c["kw"], c["seed"])
+            u = O.canonical_f64(5, B * c["k"] * (c["h"] - c["kh"] + 1) * (c["w"] - c["kw"] + 1))
+            v4 = v0.reshape(B, c["c_in"], c["h"], c["w"])
+            step = lambda: O.crbm_cd1(ker, np.zeros(c["c_in"], np.float32), np.zeros(c["k"], np.float32), v4,  # noqa
+                                      c["lr"], u)
+            done = lambda: None  # noqa: E731
+            what = "oracle crbm_cd1"
     else:
         spec = CF.NET_CONFIGS[name]()
         B = spec["batch_size"]
@@ -451,7 +518,7 @@ def main():
                 "steps": info["steps"], "warmup": 1, "ms_per_step": round(info["seconds"] * 1e3 / info["steps"], 3),
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic", "impl": "reference",
-                "config": {"workload": {"rbm": "mnist_rbm_cd1"}.get(name, name), "global_batch": 100 if name != "imagenet_cnn" else 128,
+                "config": {"workload": {"rbm": "mnist_rbm_cd1", "crbm": "mnist_crbm_cd1"}.get(name, name), "global_batch": 100 if name != "imagenet_cnn" else 128,
                            "host": platform.processor() or platform.machine()},
                 "cpu_baseline": {"value": round(v, 3), "unit": "samples/s", "cores": info["cores"],
                                  "kind": info["kind"], "sample": info["sample"]},
@@ -511,7 +578,7 @@ def main():
             "clocks": clk.summary()}
     if not a.no_others:
         others = {}
-        for name in ["rbm", "mlp", "mnist_cnn", "cifar_cnn", "imagenet_cnn"]:
+        for name in ["rbm", "mlp", "mnist_cnn", "cifar_cnn", "imagenet_cnn", "crbm"]:
             if name == a.config:
                 continue
             try:
@@ -523,6 +590,10 @@ def main():
                                 "ms_per_step": round(ms / n, 5),
                                 "e2e": round(w.Bg * max(n // 2, 5) / (e2 * 1e-3), 2),
                                 "kernels_per_step": w.kernels_per_step()}
+                if name == "crbm" and dist.rank == 0:  # a widening row: its CPU reference beside it
+                    cv, ci = cpu_reference("crbm", 3.0)
+                    others[name]["cpu_baseline"] = {"value": round(cv, 2), "unit": "samples/s",
+                                                    "cores": ci["cores"], "kind": ci["kind"], "sample": ci["sample"]}
                 del w
             except Exception as ex:  # a config the build does not cover yet is reported, not hidden
                 others[name] = {"unavailable": f"{type(ex).__name__}: {ex}"[:200]}

@@ -89,6 +89,7 @@ typedef struct b2n_network_spec {
 
 typedef struct b2n_net b2n_net;
 typedef struct b2n_rbm b2n_rbm;
+typedef struct b2n_crbm b2n_crbm;
 
 const char* b2n_last_error(void);
 int b2n_version(void);
@@ -203,6 +204,32 @@ int b2n_dbn_pretrain(b2n_rbm* const* stack, int layers, const float* data_host, 
 int b2n_rbm_kernels_per_step(b2n_rbm* rbm, int* n);
 int b2n_rbm_profile(b2n_rbm* rbm, int steps, float lr, long long batch_global, int max_ops, double* stats, char* names,
                     int names_len, int* n_ops);
+
+/* ---- convolutional RBM: replaces Crbm (energy.hpp:245-262) and crbm_cd_update
+ * (energy.hpp:333-376), binary units, non-pooled formulation, valid convolutions ----
+ * kernels (k, c_in, kh, kw), bv (c_in), bh (k); visible batches NCHW (batch, c_in, h, w).
+ * Errors: ESHAPE for kh > h or kw > w (the reference's "crbm: kernel extents exceed visible
+ * extents") and outside the tensor-core conv envelope (k, c_in <= 32, c_in*kh*kw <= 320,
+ * k*kh*kw <= 320). */
+int b2n_crbm_create(int c_in, int h, int w, int k, int kh, int kw, int device, int precision, b2n_crbm** out);
+int b2n_crbm_destroy(b2n_crbm* crbm);
+/* Crbm::init (energy.hpp:261): Glorot(c_in*kh*kw, k*kh*kw) on the kernels, std::mt19937(seed) */
+int b2n_crbm_init(b2n_crbm* crbm, unsigned seed);
+int b2n_crbm_set(b2n_crbm* crbm, const float* kernels_host, const float* bv_host, const float* bh_host);
+int b2n_crbm_get(b2n_crbm* crbm, float* kernels_host, float* bv_host, float* bh_host);
+/* crbm_cd_update: uniforms_host holds the batch*k*oh*ow draws unit_sample_inplace consumes
+ * (generate_canonical<double,53>, NCHW order); recon = sum (v0 - v1)^2 / batch_global. */
+int b2n_crbm_cd_update(b2n_crbm* crbm, const float* v0_host, long long batch, float lr,
+                       const double* uniforms_host, long long batch_global, double* recon);
+/* the chain states of the last update (h0 mean, h sample, v1 mean, h1 mean), NCHW */
+int b2n_crbm_last_states(b2n_crbm* crbm, float* h0, float* hs, float* v1, float* h1);
+int b2n_crbm_stage(b2n_crbm* crbm, const float* v0_host, const double* uniforms_host, long long batch);
+int b2n_crbm_run_staged(b2n_crbm* crbm, int steps, float lr, long long batch_global);
+int b2n_crbm_recon(b2n_crbm* crbm, double* recon);
+int b2n_crbm_kernels_per_step(b2n_crbm* crbm, int* n);
+int b2n_crbm_stream(b2n_crbm* crbm, void** cuda_stream);
+int b2n_crbm_profile(b2n_crbm* crbm, int steps, float lr, long long batch_global, int max_ops, double* stats,
+                     char* names, int names_len, int* n_ops);
 
 /* ---- op level (device pointers, async on `stream`; NULL = default stream) ---- */
 /* gemm (gemm.hpp:225-229): C = op(A) . op(B); lda/ldb/ldc are row pitches in floats (multiples

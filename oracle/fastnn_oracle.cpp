@@ -752,6 +752,87 @@ void orc_rbm_init(long long H, long long V, unsigned seed, float* W) {
     std::memcpy(W, w.data(), w.size() * sizeof(float));
 }
 
+// ---------------------------------------------------------------------------- convolutional RBM
+// crbm_cd_update (energy.hpp:333-376) for binary units with the Bernoulli draws supplied
+// (u[B][k][oh][ow], row-major like unit_sample_inplace's serial walk, energy.hpp:53-71):
+//   a0 = conv_valid(v0, K) + bh            crbm_hidden_preact (energy.hpp:267-283)
+//   h0 = sigmoid(a0), hs = (u < (double)h0)
+//   v1 = sigmoid(conv_full(hs, K^T) + bv)  crbm_visible_preact (energy.hpp:285-313)
+//   h1 = sigmoid(conv_valid(v1, K) + bh)
+//   K += lr/B (pos - neg), pos/neg = crbm_corr_stats (energy.hpp:316-329) = add_corr_map per
+//   (f, c) over images; bh / bv += lr/B * (h0 - h1) / (v0 - v1) per element in the reference's
+//   serial loop order (energy.hpp:359-374); recon = sq_diff_per_row(v0, v1) / B.
+// Shard form: statistics over the local images, scaled by lr / B_global. With d* outputs the
+// deltas are written instead of applied (data-parallel reduction checks).
+double orc_crbm_cd1(long long C, long long Hh, long long Ww, long long K, long long KH, long long KW, float* ker,
+                    float* bv, float* bh, const float* v0, long long B, long long B_global, float lr, const double* u,
+                    float* h0_out, float* hs_out, float* v1_out, float* h1_out, float* dker, float* dbh, float* dbv) {
+    const size_t c = (size_t)C, h = (size_t)Hh, w = (size_t)Ww, k = (size_t)K, kh = (size_t)KH, kw = (size_t)KW;
+    const size_t n = (size_t)B, oh = h - kh + 1, ow = w - kw + 1, hp = oh * ow, vp = h * w;
+    std::vector<float> h0(n * k * hp), hs(n * k * hp), v1(n * c * vp), h1(n * k * hp);
+    conv_fwd(v0, {n, c, h, w}, ker, k, kh, kw, 0, h0.data());
+    for (size_t m = 0; m < n * k; ++m)
+        for (size_t p = 0; p < hp; ++p) {
+            const size_t i = m * hp + p;
+            const float a = h0[i] + bh[m % k];
+            const float pr = sigmoidf_ref(a);
+            h0[i] = pr;
+            hs[i] = (u[i] < (double)pr) ? 1.0f : 0.0f;
+        }
+    conv_bwd_data(hs.data(), n, k, oh, ow, ker, c, kh, kw, 0, h, w, v1.data());
+    for (size_t m = 0; m < n * c; ++m)
+        for (size_t p = 0; p < vp; ++p) v1[m * vp + p] = sigmoidf_ref(v1[m * vp + p] + bv[m % c]);
+    double recon = 0.0;  // sq_diff_per_row energy.hpp:84-96
+    for (size_t i = 0; i < n * c * vp; ++i) {
+        const double d = double(v0[i]) - double(v1[i]);
+        recon += d * d;
+    }
+    conv_fwd(v1.data(), {n, c, h, w}, ker, k, kh, kw, 0, h1.data());
+    for (size_t m = 0; m < n * k; ++m)
+        for (size_t p = 0; p < hp; ++p) h1[m * hp + p] = sigmoidf_ref(h1[m * hp + p] + bh[m % k]);
+    const size_t nk = k * c * kh * kw;
+    std::vector<float> pos(nk, 0.0f), neg(nk, 0.0f), gdummy(k, 0.0f);
+    conv_bwd_filter(v0, {n, c, h, w}, h0.data(), k, oh, ow, kh, kw, 0, pos.data(), gdummy.data());
+    conv_bwd_filter(v1.data(), {n, c, h, w}, h1.data(), k, oh, ow, kh, kw, 0, neg.data(), gdummy.data());
+    const float scale = lr / static_cast<float>(B_global);
+    std::vector<float> dbh_l(k, 0.0f), dbv_l(c, 0.0f);
+    float* tbh = dker ? dbh_l.data() : bh;
+    float* tbv = dker ? dbv_l.data() : bv;
+    for (size_t i = 0; i < nk; ++i) {
+        if (dker) dker[i] = scale * (pos[i] - neg[i]);
+        else ker[i] += scale * (pos[i] - neg[i]);
+    }
+    for (size_t img = 0; img < n; ++img) {
+        for (size_t f = 0; f < k; ++f)
+            for (size_t p = 0; p < hp; ++p) {
+                const size_t i = (img * k + f) * hp + p;
+                tbh[f] += scale * (h0[i] - h1[i]);
+            }
+        for (size_t ch = 0; ch < c; ++ch)
+            for (size_t p = 0; p < vp; ++p) {
+                const size_t i = (img * c + ch) * vp + p;
+                tbv[ch] += scale * (v0[i] - v1[i]);
+            }
+    }
+    if (dker) {
+        std::memcpy(dbh, dbh_l.data(), k * sizeof(float));
+        std::memcpy(dbv, dbv_l.data(), c * sizeof(float));
+    }
+    if (h0_out) std::memcpy(h0_out, h0.data(), h0.size() * sizeof(float));
+    if (hs_out) std::memcpy(hs_out, hs.data(), hs.size() * sizeof(float));
+    if (v1_out) std::memcpy(v1_out, v1.data(), v1.size() * sizeof(float));
+    if (h1_out) std::memcpy(h1_out, h1.data(), h1.size() * sizeof(float));
+    return recon / double(B_global);
+}
+
+// Crbm::init (energy.hpp:261): glorot(fan_in = c*kh*kw, fan_out = k*kh*kw) on the kernels only
+void orc_crbm_init(long long C, long long K, long long KH, long long KW, unsigned seed, float* ker) {
+    std::mt19937 rng(seed);
+    std::vector<float> w((size_t)(K * C * KH * KW));
+    glorot(w, (size_t)(C * KH * KW), (size_t)(K * KH * KW), rng);
+    std::memcpy(ker, w.data(), w.size() * sizeof(float));
+}
+
 // ---------------------------------------------------------------------------- synthetic inputs
 // The exact libstdc++ distributions the reference's tests and BASELINE.md use.
 void orc_uniform_f32(unsigned seed, float lo, float hi, long long n, float* out) {

@@ -92,6 +92,10 @@ def _declare(lib: C.CDLL, prefix: str) -> None:
         lib.orc_canonical_f64.argtypes = [C.c_uint, C.c_longlong, _D]
         lib.orc_bernoulli_f32.argtypes = [C.c_uint, C.c_double, C.c_longlong, _F]
         lib.orc_uniform_int.argtypes = [C.c_uint, C.c_int, C.c_int, C.c_longlong, _I]
+        lib.orc_crbm_cd1.argtypes = [C.c_longlong] * 6 + [_F, _F, _F, _F, C.c_longlong, C.c_longlong, C.c_float,
+                                                          _D, _F, _F, _F, _F, _F, _F, _F]
+        lib.orc_crbm_cd1.restype = C.c_double
+        lib.orc_crbm_init.argtypes = [C.c_longlong] * 4 + [C.c_uint, _F]
     else:
         lib.ref_cd_k.argtypes = [C.c_longlong, C.c_longlong, _F, _F, _F, _F, C.c_longlong, C.c_int, C.c_float,
                                  C.c_uint]
@@ -111,6 +115,14 @@ def _declare(lib: C.CDLL, prefix: str) -> None:
         lib.ref_dbn_pretrain.argtypes = [C.c_int, _LL, _LL, _F, _F, _F, _F, C.c_longlong, C.c_int, C.c_float,
                                          C.c_longlong, C.c_uint, _D, C.c_char_p, C.c_int]
         lib.ref_set_threads.argtypes = [C.c_int]
+        lib.ref_crbm_cd.argtypes = [C.c_longlong] * 6 + [_F, _F, _F, _F, C.c_longlong, C.c_float, C.c_uint]
+        lib.ref_crbm_cd.restype = C.c_double
+        lib.ref_crbm_init.argtypes = [C.c_longlong] * 6 + [C.c_uint, _F]
+        lib.ref_crbm_create.argtypes = [C.c_longlong] * 6 + [C.c_uint, _F, C.c_longlong, C.c_uint]
+        lib.ref_crbm_create.restype = C.c_void_p
+        lib.ref_crbm_step.argtypes = [C.c_void_p, C.c_float]
+        lib.ref_crbm_step.restype = C.c_double
+        lib.ref_crbm_destroy.argtypes = [C.c_void_p]
         lib.ref_thread_count.restype = C.c_int
 
 
@@ -385,6 +397,53 @@ def rbm_init(H: int, V: int, seed: int, which: str = "oracle") -> np.ndarray:
     W = np.zeros((H, V), np.float32)
     getattr(lib, "orc_rbm_init" if which == "oracle" else "ref_rbm_init")(H, V, seed, fptr(W))
     return W
+
+
+def crbm_cd1(ker, bv, bh, v0, lr, u, b_global=None, deltas=False):
+    """Oracle CRBM CD-1 (crbm_cd_update, energy.hpp:333-376) with supplied uniforms u[B][k][oh][ow].
+    ker (k,c,kh,kw), v0 (B,c,h,w). Returns (recon, ker, bv, bh, extras)."""
+    lib = load("oracle")
+    ker = np.array(ker, np.float32, copy=True, order="C")
+    bv = np.array(bv, np.float32, copy=True)
+    bh = np.array(bh, np.float32, copy=True)
+    v0 = np.ascontiguousarray(v0, np.float32)
+    u = np.ascontiguousarray(u, np.float64)
+    k, c, kh, kw = ker.shape
+    B, _, h, w = v0.shape
+    oh, ow = h - kh + 1, w - kw + 1
+    h0 = np.zeros((B, k, oh, ow), np.float32)
+    hs, h1 = np.zeros_like(h0), np.zeros_like(h0)
+    v1 = np.zeros_like(v0)
+    dk = np.zeros_like(ker) if deltas else None
+    dbh = np.zeros(k, np.float32) if deltas else None
+    dbv = np.zeros(c, np.float32) if deltas else None
+    recon = lib.orc_crbm_cd1(c, h, w, k, kh, kw, fptr(ker), fptr(bv), fptr(bh), fptr(v0), B, b_global or B, lr,
+                             dptr(u), fptr(h0), fptr(hs), fptr(v1), fptr(h1), fptr(dk) if deltas else None,
+                             fptr(dbh) if deltas else None, fptr(dbv) if deltas else None)
+    return recon, ker, bv, bh, dict(h0=h0, hs=hs, v1=v1, h1=h1, dker=dk, dbh=dbh, dbv=dbv)
+
+
+def ref_crbm_cd(ker, bv, bh, v0, lr, seed):
+    """The reference's own crbm_cd_update with std::mt19937(seed) (oracle/_ref)."""
+    lib = load("ref")
+    ker = np.array(ker, np.float32, copy=True, order="C")
+    bv = np.array(bv, np.float32, copy=True)
+    bh = np.array(bh, np.float32, copy=True)
+    v0 = np.ascontiguousarray(v0, np.float32)
+    k, c, kh, kw = ker.shape
+    B, _, h, w = v0.shape
+    recon = lib.ref_crbm_cd(c, h, w, k, kh, kw, fptr(ker), fptr(bv), fptr(bh), fptr(v0), B, lr, seed)
+    return recon, ker, bv, bh
+
+
+def crbm_init(c: int, h: int, w: int, k: int, kh: int, kw: int, seed: int, which: str = "oracle") -> np.ndarray:
+    lib = load(which)
+    ker = np.zeros((k, c, kh, kw), np.float32)
+    if which == "oracle":
+        lib.orc_crbm_init(c, k, kh, kw, seed, fptr(ker))
+    else:
+        lib.ref_crbm_init(c, h, w, k, kh, kw, seed, fptr(ker))
+    return ker
 
 
 def uniform_f32(seed: int, n: int, lo: float = 0.0, hi: float = 1.0) -> np.ndarray:

@@ -504,6 +504,57 @@ double ref_rbm_step(void* h, float lr) {
 }
 void ref_rbm_destroy(void* h) { delete static_cast<RefRbm*>(h); }
 
+// crbm_cd_update (energy.hpp:333) with its own std::mt19937(rng_seed); kernels (k,c,kh,kw), bv (c), bh (k)
+static ConvShape crbm_shape(long long C, long long Hh, long long Ww, long long K, long long KH, long long KW) {
+    ConvShape s;
+    s.c_in = (std::size_t)C;
+    s.h = (std::size_t)Hh;
+    s.w = (std::size_t)Ww;
+    s.k = (std::size_t)K;
+    s.kh = (std::size_t)KH;
+    s.kw = (std::size_t)KW;
+    return s;
+}
+double ref_crbm_cd(long long C, long long Hh, long long Ww, long long K, long long KH, long long KW, float* ker,
+                   float* bv, float* bh, const float* v0, long long B, float lr, unsigned rng_seed) {
+    Crbm m(crbm_shape(C, Hh, Ww, K, KH, KW));
+    copy_in(m.kernels, ker);
+    copy_in(m.bv, bv);
+    copy_in(m.bh, bh);
+    Tensor v = make_batch(v0, B, {C, Hh, Ww});
+    std::mt19937 rng(rng_seed);
+    const double recon = crbm_cd_update(m, v, lr, rng);
+    copy_out(m.kernels, ker);
+    copy_out(m.bv, bv);
+    copy_out(m.bh, bh);
+    return recon;
+}
+void ref_crbm_init(long long C, long long Hh, long long Ww, long long K, long long KH, long long KW, unsigned seed,
+                   float* ker) {
+    Crbm m(crbm_shape(C, Hh, Ww, K, KH, KW));
+    std::mt19937 rng(seed);
+    m.init(rng);
+    copy_out(m.kernels, ker);
+}
+// persistent CRBM for the CPU baseline timing loop
+struct RefCrbm {
+    Crbm m;
+    Tensor v;
+    std::mt19937 rng;
+};
+void* ref_crbm_create(long long C, long long Hh, long long Ww, long long K, long long KH, long long KW,
+                      unsigned init_seed, const float* v0, long long B, unsigned rng_seed) {
+    auto* r = new RefCrbm{Crbm(crbm_shape(C, Hh, Ww, K, KH, KW)), make_batch(v0, B, {C, Hh, Ww}), std::mt19937(rng_seed)};
+    std::mt19937 init(init_seed);
+    r->m.init(init);
+    return r;
+}
+double ref_crbm_step(void* h, float lr) {
+    RefCrbm* r = static_cast<RefCrbm*>(h);
+    return crbm_cd_update(r->m, r->v, lr, r->rng);
+}
+void ref_crbm_destroy(void* h) { delete static_cast<RefCrbm*>(h); }
+
 void ref_rbm_init(long long H, long long V, unsigned seed, float* W) {
     Rbm rbm((std::size_t)H, (std::size_t)V);
     std::mt19937 rng(seed);

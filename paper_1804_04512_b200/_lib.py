@@ -135,6 +135,19 @@ _SIGS = {
     "b2n_rbm_run_staged": ([_VP, C.c_int, C.c_float, C.c_longlong], C.c_int),
     "b2n_rbm_recon": ([_VP, _D], C.c_int),
     "b2n_rbm_stream": ([_VP, C.POINTER(_VP)], C.c_int),
+    "b2n_crbm_create": ([C.c_int] * 6 + [C.c_int, C.c_int, C.POINTER(_VP)], C.c_int),
+    "b2n_crbm_destroy": ([_VP], C.c_int),
+    "b2n_crbm_init": ([_VP, C.c_uint], C.c_int),
+    "b2n_crbm_set": ([_VP, _F, _F, _F], C.c_int),
+    "b2n_crbm_get": ([_VP, _F, _F, _F], C.c_int),
+    "b2n_crbm_cd_update": ([_VP, _F, C.c_longlong, C.c_float, _D, C.c_longlong, _D], C.c_int),
+    "b2n_crbm_last_states": ([_VP, _F, _F, _F, _F], C.c_int),
+    "b2n_crbm_stage": ([_VP, _F, _D, C.c_longlong], C.c_int),
+    "b2n_crbm_run_staged": ([_VP, C.c_int, C.c_float, C.c_longlong], C.c_int),
+    "b2n_crbm_recon": ([_VP, _D], C.c_int),
+    "b2n_crbm_kernels_per_step": ([_VP, _I], C.c_int),
+    "b2n_crbm_stream": ([_VP, C.POINTER(_VP)], C.c_int),
+    "b2n_crbm_profile": ([_VP, C.c_int, C.c_float, C.c_longlong, C.c_int, _D, C.c_char_p, C.c_int, _I], C.c_int),
     "b2n_gemm": ([_VP, C.c_longlong, C.c_int, _VP, C.c_longlong, C.c_int, _VP, C.c_longlong, C.c_longlong,
                   C.c_longlong, C.c_longlong, C.c_int, _VP], C.c_int),
     "b2n_sgd_momentum_step": ([_VP, _VP, _VP, C.c_longlong, C.c_float, C.c_float, C.c_float, _VP], C.c_int),

@@ -65,6 +65,10 @@ def imagenet_cnn_spec(batch: int = 128, hw: int = 256) -> dict:
 
 
 RBM = {"name": "mnist_rbm", "hidden": 500, "visible": 784, "batch_size": 100, "lr": 0.1, "k": 1, "seed": 42}
+# SURVEY 8(f)4 widening (not a BASELINE config): an MNIST-shaped convolutional RBM (Crbm,
+# energy.hpp:245-376) on the MNIST-CNN's first-layer filter shape, batch 100, CD-1
+CRBM = {"name": "mnist_crbm", "c_in": 1, "h": 28, "w": 28, "k": 12, "kh": 5, "kw": 5, "batch_size": 100, "lr": 0.1,
+        "seed": 42}
 
 NET_CONFIGS = {"mlp": mlp_spec, "mnist_cnn": mnist_cnn_spec, "cifar_cnn": cifar_cnn_spec,
                "imagenet_cnn": imagenet_cnn_spec}

@@ -7,6 +7,7 @@
 #include "../../include/b200nn.h"
 #include "network.cuh"
 #include "probe.cuh"
+#include "crbm.cuh"
 #include "rbm.cuh"
 #include "runtime.cuh"
 
@@ -19,6 +20,12 @@ struct b2n_rbm {
     b2n::Rbm impl;
     template <class... A>
     explicit b2n_rbm(A&&... a) : impl(std::forward<A>(a)...) {}
+};
+
+struct b2n_crbm {
+    b2n::Crbm impl;
+    template <class... A>
+    explicit b2n_crbm(A&&... a) : impl(std::forward<A>(a)...) {}
 };
 
 namespace {
@@ -305,6 +312,53 @@ int b2n_rbm_kernels_per_step(b2n_rbm* r, int* n) {
 }
 int b2n_rbm_stream(b2n_rbm* r, void** s) {
     return guard([&] { *s = r->impl.stream(); });
+}
+
+// ------------------------------------------------------------------ convolutional RBM
+int b2n_crbm_create(int c_in, int h, int w, int k, int kh, int kw, int device, int precision, b2n_crbm** out) {
+    return guard([&] { *out = new b2n_crbm(c_in, h, w, k, kh, kw, device, precision); });
+}
+int b2n_crbm_destroy(b2n_crbm* m) {
+    return guard([&] { delete m; });
+}
+int b2n_crbm_init(b2n_crbm* m, unsigned seed) {
+    return guard([&] { m->impl.init(seed); });
+}
+int b2n_crbm_set(b2n_crbm* m, const float* kernels, const float* bv, const float* bh) {
+    return guard([&] { m->impl.set(kernels, bv, bh); });
+}
+int b2n_crbm_get(b2n_crbm* m, float* kernels, float* bv, float* bh) {
+    return guard([&] { m->impl.get(kernels, bv, bh); });
+}
+int b2n_crbm_cd_update(b2n_crbm* m, const float* v0, long long batch, float lr, const double* u,
+                       long long batch_global, double* recon) {
+    return guard([&] {
+        B2N_REQUIRE(batch >= 1 && (batch_global == 0 || batch_global >= batch), B2N_ESHAPE,
+                    "crbm_cd_update: need 1 <= batch <= batch_global");
+        *recon = m->impl.cd_update(v0, batch, lr, u, batch_global ? batch_global : batch);
+    });
+}
+int b2n_crbm_last_states(b2n_crbm* m, float* h0, float* hs, float* v1, float* h1) {
+    return guard([&] { m->impl.last_states(h0, hs, v1, h1); });
+}
+int b2n_crbm_stage(b2n_crbm* m, const float* v0, const double* u, long long batch) {
+    return guard([&] { m->impl.stage(v0, u, batch); });
+}
+int b2n_crbm_run_staged(b2n_crbm* m, int steps, float lr, long long batch_global) {
+    return guard([&] { m->impl.run_staged(steps, lr, batch_global); });
+}
+int b2n_crbm_recon(b2n_crbm* m, double* recon) {
+    return guard([&] { *recon = m->impl.recon(); });
+}
+int b2n_crbm_kernels_per_step(b2n_crbm* m, int* n) {
+    return guard([&] { *n = m->impl.kernels_per_step(); });
+}
+int b2n_crbm_stream(b2n_crbm* m, void** s) {
+    return guard([&] { *s = m->impl.stream(); });
+}
+int b2n_crbm_profile(b2n_crbm* m, int steps, float lr, long long batch_global, int max_ops, double* stats, char* names,
+                     int names_len, int* n_ops) {
+    return guard([&] { export_stats(m->impl.profile(steps, lr, batch_global), max_ops, stats, names, names_len, n_ops); });
 }
 
 // ------------------------------------------------------------------ op level

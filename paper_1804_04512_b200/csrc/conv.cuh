@@ -58,6 +58,14 @@ struct ConvParams {
     int chunk_px;    // WGRAD: output pixels per item (multiple of 32)
     int chunks;      // WGRAD: pixel chunks
     long long npix;  // rows of the GEMM view (pixels)
+    // convolutional-RBM epilogue extensions (crbm.cuh); zero for the network layers
+    const double* u;       // FWD: Bernoulli uniforms [B][K][OH][OW] -> ys = (u < (double)y)
+    float* ys;             // FWD: sampled hidden states, dense [B][K][OH][OW]
+    int neg_out;           // FWD: store -y (the negative phase of the weight statistics)
+    const float* dg_bias;  // DGRAD: dx = act(acc + dg_bias[c]) (crbm_visible_preact + unit mean)
+    int dg_act;
+    float* vstat_f;        // DGRAD: per (item, warp, channel) sum of (x - dx) (p.x = v0) ...
+    double* vstat_d;       // ... and sum of (x - dx)^2 in double (sq_diff_per_row)
 };
 
 constexpr int kGatherWarps = 8;
@@ -401,16 +409,43 @@ __global__ void __launch_bounds__(kConvThreads, 1) conv_tc_kernel(const ConvPara
                             p.arg[(long long)b * g.k * p.ph * p.pw + pi] = (uint8_t)code;
                         }
                     } else if (ok && n < g.k) {
-                        p.y[(long long)b * p.ldy + ((long long)n * g.oh + oy) * g.ow + ox] = val;
+                        p.y[(long long)b * p.ldy + ((long long)n * g.oh + oy) * g.ow + ox] = p.neg_out ? -val : val;
+                        if (p.u) {  // unit_sample_inplace (energy.hpp:59-61) on the supplied draw
+                            const long long ui = (((long long)b * g.k + n) * g.oh + oy) * g.ow + ox;
+                            p.ys[ui] = p.u[ui] < (double)val ? 1.0f : 0.0f;
+                        }
                     }
                 }
             } else if (MODE == CONV_DGRAD) {
                 const long long row = (long long)item * 128 + r;
-                if (row < p.npix) {
-                    const int b = (int)(row / HW), rem = (int)(row % HW);
+                const bool rok = row < p.npix;
+                const int b = rok ? (int)(row / HW) : 0, rem = rok ? (int)(row % HW) : 0;
 #pragma unroll
-                    for (int n = 0; n < NPAD; ++n)
-                        if (n < g.c) p.dx[(long long)b * p.lddx + (long long)n * HW + rem] = v[n];
+                for (int n = 0; n < NPAD; ++n) {
+                    if (n >= g.c) break;  // uniform
+                    float val = v[n];
+                    if (p.dg_bias) val = apply_act(p.dg_act, val + p.dg_bias[n]);
+                    if (rok) p.dx[(long long)b * p.lddx + (long long)n * HW + rem] = val;
+                    if (p.vstat_f) {  // visible-bias and reconstruction partials of this warp's 32 rows
+                        float d = 0.0f;
+                        double dd = 0.0;
+                        if (rok) {
+                            const float x0 = p.x[(long long)b * p.ldx + (long long)n * HW + rem];
+                            d = x0 - val;
+                            const double e = (double)x0 - (double)val;
+                            dd = e * e;
+                        }
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) {
+                            d += __shfl_xor_sync(0xffffffffu, d, o);
+                            dd += __shfl_xor_sync(0xffffffffu, dd, o);
+                        }
+                        if (lane == 0) {
+                            const long long si = ((long long)item * 4 + q) * g.c + n;
+                            p.vstat_f[si] = d;
+                            p.vstat_d[si] = dd;
+                        }
+                    }
                 }
             } else {  // WGRAD partial tile: rows = patch index, cols = kernels
                 float* dst = p.ws + (long long)item * 128 * 32 + r * 32;

@@ -422,6 +422,100 @@ def cd_k_update(rbm: Rbm, v0, k: int, lr: float, uniforms, batch_global: int | N
     return out.value
 
 
+class Crbm:
+    """fastnn::Crbm (energy.hpp:245-262), binary units, non-pooled, resident on the GPU.
+    kernels (k, c_in, kh, kw), bv (c_in), bh (k); visible batches (n, c_in, h, w)."""
+
+    def __init__(self, c_in: int, h: int, w: int, k: int, kh: int, kw: int, device: int = 0,
+                 precision: int = TF32X3):
+        hd = C.c_void_p()
+        _lib.call("b2n_crbm_create", c_in, h, w, k, kh, kw, device, precision, C.byref(hd))
+        self._h = hd
+        self.c_in, self.h, self.w, self.k, self.kh, self.kw = c_in, h, w, k, kh, kw
+        self.oh, self.ow = h - kh + 1, w - kw + 1
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            _lib.load().b2n_crbm_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def kernel_shape(self):
+        return (self.k, self.c_in, self.kh, self.kw)
+
+    def init(self, seed: int) -> None:
+        _lib.call("b2n_crbm_init", self._h, seed)
+
+    def set(self, kernels, bv, bh) -> None:
+        kernels = np.ascontiguousarray(kernels, np.float32)
+        bv = np.ascontiguousarray(bv, np.float32)
+        bh = np.ascontiguousarray(bh, np.float32)
+        if kernels.shape != self.kernel_shape or bv.shape != (self.c_in,) or bh.shape != (self.k,):
+            raise ShapeError("crbm parameter shapes")
+        _lib.call("b2n_crbm_set", self._h, _f(kernels), _f(bv), _f(bh))
+
+    def get(self):
+        ker = np.zeros(self.kernel_shape, np.float32)
+        bv = np.zeros(self.c_in, np.float32)
+        bh = np.zeros(self.k, np.float32)
+        _lib.call("b2n_crbm_get", self._h, _f(ker), _f(bv), _f(bh))
+        return ker, bv, bh
+
+    def kernels_per_step(self) -> int:
+        n = C.c_int()
+        _lib.call("b2n_crbm_kernels_per_step", self._h, C.byref(n))
+        return n.value
+
+    def last_states(self, batch: int):
+        h0 = np.zeros((batch, self.k, self.oh, self.ow), np.float32)
+        hs, h1 = np.zeros_like(h0), np.zeros_like(h0)
+        v1 = np.zeros((batch, self.c_in, self.h, self.w), np.float32)
+        _lib.call("b2n_crbm_last_states", self._h, _f(h0), _f(hs), _f(v1), _f(h1))
+        return h0, hs, v1, h1
+
+    def stage(self, v0, uniforms) -> None:
+        v0 = np.ascontiguousarray(v0, np.float32)
+        u = np.ascontiguousarray(uniforms, np.float64)
+        if v0.ndim != 4 or v0.shape[1:] != (self.c_in, self.h, self.w) or u.size < v0.shape[0] * self.k * self.oh * self.ow:
+            raise ShapeError("crbm stage: visible batch / uniforms do not match the model")
+        _lib.call("b2n_crbm_stage", self._h, _f(v0), _d(u), v0.shape[0])
+
+    def run_staged(self, steps: int, lr: float, batch_global: int = 0) -> None:
+        _lib.call("b2n_crbm_run_staged", self._h, steps, lr, batch_global)
+
+    def recon(self) -> float:
+        out = C.c_double()
+        _lib.call("b2n_crbm_recon", self._h, C.byref(out))
+        return out.value
+
+    def stream_handle(self) -> int:
+        s = C.c_void_p()
+        _lib.call("b2n_crbm_stream", self._h, C.byref(s))
+        return s.value or 0
+
+
+def crbm_cd_update(m: Crbm, v0, lr: float, uniforms, batch_global: int | None = None) -> float:
+    """fastnn::crbm_cd_update (energy.hpp:333-376) with the Bernoulli uniforms supplied
+    (batch * k * oh * ow generate_canonical<double,53> draws in NCHW order, the stream
+    unit_sample_inplace's std::bernoulli_distribution consumes). Returns the reconstruction error
+    per image."""
+    v0 = np.ascontiguousarray(v0, np.float32)
+    if v0.ndim != 4 or v0.shape[1] != m.c_in or v0.shape[2] != m.h or v0.shape[3] != m.w:
+        raise ShapeError("crbm_cd_update: input does not match the model's visible shape")
+    u = np.ascontiguousarray(uniforms, np.float64).ravel()
+    if u.size < v0.shape[0] * m.k * m.oh * m.ow:
+        raise ShapeError("crbm_cd_update: need batch * k * oh * ow uniforms")
+    out = C.c_double()
+    _lib.call("b2n_crbm_cd_update", m.handle, _f(v0), v0.shape[0], lr, _d(u), batch_global or v0.shape[0],
+              C.byref(out))
+    return out.value
+
+
 class Mt19937:
     """A std::mt19937 stream (numpy's MT19937 with the legacy init_genrand seeding is the same
     generator) yielding std::generate_canonical<double,53> values: two 32-bit draws per double,

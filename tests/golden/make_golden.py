@@ -11,6 +11,7 @@ padded ImageNet-shaped net, the SURVEY 8(c) composite of reference primitives.
     python tests/golden/make_golden.py checkpoint  # only *.fnn1 + checkpoint_errors.json
     python tests/golden/make_golden.py optim  # only optim.npz (Adagrad / Adadelta / Adam)
     python tests/golden/make_golden.py dbn    # only dbn.npz (dbn_pretrain)
+    python tests/golden/make_golden.py crbm   # only crbm.npz (crbm_cd_update)
 """
 from __future__ import annotations
 
@@ -164,7 +165,38 @@ def dbn_cases():
     np.savez_compressed(HERE / "dbn.npz", **g)
 
 
+# CRBM shapes (c, h, w, k, kh, kw, batch): the reference test's 1x4x4 / 3x3 single-kernel case
+# (test_energy.cpp:374-435), the toy-image case (:437-464), the 1x1 dense-degenerate case
+# (:466-503), a multi-channel rectangular case and an MNIST-shaped one
+CRBM_CASES = [(1, 4, 4, 1, 3, 3, 1), (1, 6, 6, 4, 3, 3, 8), (3, 1, 1, 2, 1, 1, 4), (2, 10, 9, 5, 3, 2, 3),
+              (1, 28, 28, 12, 5, 5, 4)]
+
+
+def crbm_case_inputs(i):
+    c, h, w, k, kh, kw, B = CRBM_CASES[i]
+    ker = O.crbm_init(c, h, w, k, kh, kw, 42 + i, "ref")
+    bv = O.uniform_f32(7 + i, c, -0.1, 0.1)
+    bh = O.uniform_f32(8 + i, k, -0.1, 0.1)
+    v0 = O.bernoulli_f32(3 + i, 0.5, B * c * h * w).reshape(B, c, h, w)
+    return ker, bv, bh, v0
+
+
+def crbm_cases():
+    """the reference's crbm_cd_update (energy.hpp:333-376) on CRBM_CASES, std::mt19937(5 + i)"""
+    g = {}
+    for i in range(len(CRBM_CASES)):
+        ker, bv, bh, v0 = crbm_case_inputs(i)
+        recon, k1, bv1, bh1 = O.ref_crbm_cd(ker, bv, bh, v0, 0.1, 5 + i)
+        g.update({f"ker{i}": ker, f"bv{i}": bv, f"bh{i}": bh, f"v0_{i}": v0, f"ker1_{i}": k1, f"bv1_{i}": bv1,
+                  f"bh1_{i}": bh1, f"recon{i}": np.array([recon])})
+    np.savez_compressed(HERE / "crbm.npz", **g)
+
+
 def main():
+    if sys.argv[1:] == ["crbm"]:
+        crbm_cases()
+        print("crbm fixtures written to", HERE)
+        return
     if sys.argv[1:] == ["dbn"]:
         dbn_cases()
         print("dbn fixtures written to", HERE)
@@ -245,6 +277,7 @@ def main():
     checkpoint_cases()
     optim_cases()
     dbn_cases()
+    crbm_cases()
     print("golden fixtures written to", HERE)
 
 
