@@ -311,6 +311,67 @@ double cd_k_update(Rbm& rbm, const T& v0, int k, float lr, std::mt19937& rng) {
     return recon;
 }
 
+// Crbm (energy.hpp:245-262): kernels (k, c_in, kh, kw), bv (c_in), bh (k), binary units. Takes the
+// reference's ConvShape-style extents (c_in, h, w, k, kh, kw); same ShapeError for kh > h / kw > w.
+class Crbm {
+  public:
+    Crbm(std::size_t c_in, std::size_t h, std::size_t w, std::size_t k, std::size_t kh, std::size_t kw,
+         int device = 0, int precision = B2N_TF32X3)
+        : c_(c_in), h_(h), w_(w), k_(k), kh_(kh), kw_(kw) {
+        b2n_crbm* p = nullptr;
+        check(b2n_crbm_create((int)c_in, (int)h, (int)w, (int)k, (int)kh, (int)kw, device, precision, &p));
+        p_.reset(p);
+    }
+    // Crbm::init (energy.hpp:261): glorot_fill(kernels, c_in*kh*kw, k*kh*kw) from the caller's generator
+    void init(std::mt19937& rng) {
+        const float limit = std::sqrt(6.0f / static_cast<float>(c_ * kh_ * kw_ + k_ * kh_ * kw_));
+        std::vector<float> ker(k_ * c_ * kh_ * kw_), bv(c_, 0.0f), bh(k_, 0.0f);
+        for (float& x : ker) {
+            const float u = std::generate_canonical<float, std::numeric_limits<float>::digits>(rng);
+            x = std::fma(u, limit - (-limit), -limit);
+        }
+        set(ker, bv, bh);
+    }
+    void set(const std::vector<float>& kernels, const std::vector<float>& bv, const std::vector<float>& bh) {
+        check(b2n_crbm_set(p_.get(), kernels.data(), bv.data(), bh.data()));
+    }
+    void get(std::vector<float>& kernels, std::vector<float>& bv, std::vector<float>& bh) const {
+        kernels.resize(k_ * c_ * kh_ * kw_);
+        bv.resize(c_);
+        bh.resize(k_);
+        check(b2n_crbm_get(p_.get(), kernels.data(), bv.data(), bh.data()));
+    }
+    std::size_t c_in() const { return c_; }
+    std::size_t height() const { return h_; }
+    std::size_t width() const { return w_; }
+    std::size_t hidden_maps() const { return k_; }
+    std::size_t hidden_pixels() const { return k_ * (h_ - kh_ + 1) * (w_ - kw_ + 1); }
+    b2n_crbm* handle() const { return p_.get(); }
+
+  private:
+    struct Del {
+        void operator()(b2n_crbm* r) const { b2n_crbm_destroy(r); }
+    };
+    std::unique_ptr<b2n_crbm, Del> p_;
+    std::size_t c_, h_, w_, k_, kh_, kw_;
+};
+
+// crbm_cd_update (energy.hpp:333-376): the reference's Bernoulli draws (unit_sample_inplace over
+// the n x k x oh x ow hidden tensor, energy.hpp:53-71) are taken from `rng` on the host in the same
+// order and supplied, so sampling stays bit-exact given the same probabilities.
+template <class T>
+double crbm_cd_update(Crbm& m, const T& v0, float lr, std::mt19937& rng) {
+    if (v0.rank() != 4 || v0.dim(1) != m.c_in() || v0.dim(2) != m.height() || v0.dim(3) != m.width())
+        throw ShapeError("crbm_cd_update: input does not match the model's visible shape");
+    const std::vector<float> vs = detail::pack_rows(v0);
+    const std::size_t B = v0.dim(0);
+    std::vector<double> u(B * m.hidden_pixels());
+    for (double& d : u) d = std::generate_canonical<double, 53>(rng);
+    double recon = 0.0;
+    check(b2n_crbm_cd_update(m.handle(), vs.data(), (long long)B, lr, u.data(), (long long)B, &recon));
+    return recon;
+}
+
 // dbn_pretrain (energy.hpp:208-240) with the reference's signature: the stack trains on the device
 // (data uploaded once, hidden means passed up on the device); `rng` supplies the Bernoulli
 // uniforms in the reference's order, drawn on this thread while the GPU runs the previous step.

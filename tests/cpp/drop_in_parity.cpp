@@ -170,6 +170,38 @@ int main() {
                     rf, ew, ev, eh);
         ok &= r_ok;
     }
+    {  // convolutional RBM CD-1 (crbm_cd_update) with the same generators on both sides
+        fastnn::ConvShape s;
+        s.c_in = 1;
+        s.h = 28;
+        s.w = 28;
+        s.k = 12;
+        s.kh = 5;
+        s.kw = 5;
+        fastnn::Crbm ref(s);
+        b200nn::Crbm dev(1, 28, 28, 12, 5, 5);
+        std::mt19937 ia(42), ib(42);
+        ref.init(ia);
+        dev.init(ib);
+        fastnn::Tensor v0 = fastnn::make_tensor({100, 1, 28, 28});
+        std::mt19937 vr(3);
+        std::bernoulli_distribution bit(0.5);
+        for (std::size_t b = 0; b < 100; ++b)
+            for (std::size_t y = 0; y < 28; ++y)
+                for (std::size_t x = 0; x < 28; ++x) v0.at(b, 0, y, x) = bit(vr) ? 1.0f : 0.0f;
+        std::vector<float> k0, bv0, bh0;
+        dev.get(k0, bv0, bh0);
+        std::mt19937 ra(5), rb(5);
+        const double rf = fastnn::crbm_cd_update(ref, v0, 0.1f, ra);
+        const double rd = b200nn::crbm_cd_update(dev, v0, 0.1f, rb);
+        std::vector<float> kk, bv, bh;
+        dev.get(kk, bv, bh);
+        const double ek = norm_err(kk, ref.kernels), ev = norm_err(bv, ref.bv), eh = norm_err(bh, ref.bh);
+        const bool c_ok = ek < 1e-3 && ev < 1e-3 && eh < 1e-3 && std::fabs(rf - rd) < 1e-3 * rf;
+        std::printf("criterion crbm_cd1: %s -- recon %.9g vs %.9g, kernels %.2e bv %.2e bh %.2e\n",
+                    c_ok ? "PASS" : "FAIL", rd, rf, ek, ev, eh);
+        ok &= c_ok;
+    }
     ok &= fit_checkpoint_criterion();
     return ok ? 0 : 1;
 }

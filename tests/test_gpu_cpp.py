@@ -1,6 +1,6 @@
 """The reference (fastnn) and the B200 build side by side through their C++ APIs
 (tests/cpp/drop_in_parity.cpp; include/b200nn.hpp is the drop-in): MLP, MNIST CNN, CIFAR CNN
-3-step training, RBM CD-1, and fit + save_network driven by identical fastnn::Tensor inputs and std::mt19937 streams."""
+3-step training, RBM CD-1, CRBM CD-1, and fit + save_network driven by identical fastnn::Tensor inputs and std::mt19937 streams."""
 import subprocess
 from pathlib import Path
 
@@ -15,4 +15,4 @@ def test_cpp_drop_in_parity(gpu):
     r = subprocess.run([str(BIN)], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("PASS") == 5
+    assert r.stdout.count("PASS") == 6
