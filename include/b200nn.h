@@ -221,7 +221,10 @@ int b2n_crbm_get(b2n_crbm* crbm, float* kernels_host, float* bv_host, float* bh_
  * (generate_canonical<double,53>, NCHW order); recon = sum (v0 - v1)^2 / batch_global. */
 int b2n_crbm_cd_update(b2n_crbm* crbm, const float* v0_host, long long batch, float lr,
                        const double* uniforms_host, long long batch_global, double* recon);
-/* the chain states of the last update (h0 mean, h sample, v1 mean, h1 mean), NCHW */
+/* the chain states of the last update (h0 mean, h sample, v1 mean, h1 mean), NCHW; the fused
+ * one-launch step keeps them in shared memory unless keep_states was enabled before the step
+ * (EPARAM otherwise) */
+int b2n_crbm_keep_states(b2n_crbm* crbm, int on);
 int b2n_crbm_last_states(b2n_crbm* crbm, float* h0, float* hs, float* v1, float* h1);
 int b2n_crbm_stage(b2n_crbm* crbm, const float* v0_host, const double* uniforms_host, long long batch);
 int b2n_crbm_run_staged(b2n_crbm* crbm, int steps, float lr, long long batch_global);

@@ -341,6 +341,9 @@ int b2n_crbm_cd_update(b2n_crbm* m, const float* v0, long long batch, float lr, 
 int b2n_crbm_last_states(b2n_crbm* m, float* h0, float* hs, float* v1, float* h1) {
     return guard([&] { m->impl.last_states(h0, hs, v1, h1); });
 }
+int b2n_crbm_keep_states(b2n_crbm* m, int on) {
+    return guard([&] { m->impl.keep_states(on != 0); });
+}
 int b2n_crbm_stage(b2n_crbm* m, const float* v0, const double* u, long long batch) {
     return guard([&] { m->impl.stage(v0, u, batch); });
 }

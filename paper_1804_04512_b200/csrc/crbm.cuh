@@ -13,10 +13,16 @@
 //
 // Parameters live in one buffer P = [K (k,c,kh,kw) | bh (k) | bv (c)]. Envelope of the conv
 // kernels: k, c <= 32, c*kh*kw <= 320, k*kh*kw <= 320 (ShapeError outside it -- no fallback).
+//
+// When an image's whole chain fits in shared memory (kw <= 8, <= 200 KB), the step is instead ONE
+// launch of crbm_cd1_fused_kernel (crbm_fused.cuh: a CTA per image, FFMA register strips, last-CTA
+// fixed-order reduction) -- the product path for the few-channel CRBM shapes, where N = c_in makes
+// the tensor-core dgrad mostly padding. B2N_CRBM_FUSED=0 forces the split path.
 #pragma once
 #include <random>
 
 #include "conv.cuh"
+#include "crbm_fused.cuh"
 #include "network.cuh"
 
 namespace b2n {
@@ -151,6 +157,7 @@ class Crbm {
         Plan& pl = plan_for(staged_B_, lr, Bg ? Bg : staged_B_);
         for (int s = 0; s < steps; ++s) launch(pl);
         last_B_ = staged_B_;
+        last_kept_ = pl.fused ? pl.keep : true;
     }
     double recon() {
         double r = 0.0;
@@ -161,6 +168,7 @@ class Crbm {
     }
     // chain states of the last step (h0 mean, h sample, v1 mean, h1 mean), NCHW
     void last_states(float* h0, float* hs, float* v1, float* h1) {
+        if (!last_kept_) throw Error(B2N_EPARAM, "crbm last_states: enable keep_states before the step");
         const long long B = last_B_, hp = hpix(), vp = vpix();
         const float* Hc = Hc_.as<float>();
         const auto D2H = cudaMemcpyDeviceToHost;
@@ -173,7 +181,10 @@ class Crbm {
             for (long long i = 0; i < B * hp; ++i) h1[i] = -h1[i];  // stored negated for the statistics
     }
     cudaStream_t stream() const { return stream_; }
-    int kernels_per_step() const { return 5; }
+    int kernels_per_step() const { return last_kernels_; }
+    // write the chain states of every step (h0, hs, v1, -h1) to HBM for last_states (the fused
+    // step otherwise keeps them in shared memory only)
+    void keep_states(bool on) { keep_states_ = on; }
     std::vector<OpStats> profile(int steps, float lr, long long Bg) {
         if (!staged_B_) throw Error(B2N_EPARAM, "profile before stage");
         Plan& pl = plan_for(staged_B_, lr, Bg ? Bg : staged_B_);
@@ -184,6 +195,7 @@ class Crbm {
     struct Plan {
         long long B, Bg;
         float lr;
+        bool keep = false, fused = false;
         std::vector<Op> ops;
         std::shared_ptr<DevMem> ws, vf, vd;
         cudaGraphExec_t graph = nullptr;
@@ -207,17 +219,95 @@ class Crbm {
 
     Plan& plan_for(long long B, float lr, long long Bg) {
         for (auto& p : plans_)
-            if (p->B == B && p->lr == lr && p->Bg == Bg) return *p;
+            if (p->B == B && p->lr == lr && p->Bg == Bg && p->keep == keep_states_) return *p;
         auto pl = std::make_unique<Plan>();
         pl->B = B;
         pl->lr = lr;
         pl->Bg = Bg;
+        pl->keep = keep_states_;
         build(*pl);
         plans_.push_back(std::move(pl));
         return *plans_.back();
     }
 
+    bool fused_ok() const {
+        const char* e = std::getenv("B2N_CRBM_FUSED");
+        if (e && e[0] == '0') return false;
+        return g_.kw <= 8 && g_.c <= 64 && crbm_fused_smem(g_.c, g_.h, g_.w, g_.k, g_.kh, g_.kw) <= 200 * 1024;
+    }
+
+    template <int KW>
+    void build_fused_kw(Plan& pl) {
+        const ConvGeom& g = g_;
+        const size_t smem = crbm_fused_smem(g.c, g.h, g.w, g.k, g.kh, g.kw);
+        B2N_CUDA(cudaFuncSetAttribute(crbm_cd1_fused_kernel<KW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)smem));
+        int occ = 0;
+        B2N_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, crbm_cd1_fused_kernel<KW>, kCfThreads, smem));
+        const int grid = (int)std::min<long long>(pl.B, (long long)sm_count() * std::max(occ, 1));
+        const long long np = g.k * ckk_ + g.k + g.c;
+        pl.ws = std::make_shared<DevMem>();
+        pl.ws->alloc((size_t)(pl.B * np) * 4);
+        pl.vd = std::make_shared<DevMem>();
+        pl.vd->alloc((size_t)pl.B * 8 + 64);
+        CrbmFusedParams p;
+        std::memset(&p, 0, sizeof(p));
+        p.C = g.c;
+        p.H = g.h;
+        p.W = g.w;
+        p.K = g.k;
+        p.KH = g.kh;
+        p.KW = g.kw;
+        p.OH = g.oh;
+        p.OW = g.ow;
+        p.HP = g.oh + 2 * (g.kh - 1);
+        const CrbmPitches q = crbm_pitches(g.w, g.ow, g.kw);
+        p.VP = q.VP;
+        p.OP = q.OP;
+        p.HPP = q.HPP;
+        p.B = (int)pl.B;
+        p.npart = (int)np;
+        p.v0 = Vc_.as<float>();
+        p.u = U_.as<double>();
+        p.P = P_.as<float>();
+        p.ws = pl.ws->as<float>();
+        p.rws = pl.vd->as<double>();
+        p.ticket = reinterpret_cast<unsigned*>(recon_.as<double>() + 1);
+        p.recon = recon_.as<double>();
+        p.scale = pl.lr / static_cast<float>(pl.Bg);
+        p.inv_bg = 1.0 / (double)pl.Bg;
+        p.stage_floats = (long long)(smem / 4) - round_up(np, 4) - 16;
+        p.trace = TraceRegistry::get().next();
+        if (pl.keep) {
+            p.h0_out = Hc_.as<float>();
+            p.h1_out = Hc_.as<float>() + pl.B * hpix();
+            p.hs_out = HS_.as<float>();
+            p.v1_out = Vc_.as<float>() + pl.B * vpix();
+        }
+        const double fl = 2.0 * pl.B * (3.0 * hpix() * ckk_ + (double)vpix() * g.k * g.kh * g.kw + 2.0 * hpix() * ckk_);
+        const double by = 4.0 * pl.B * vpix() + 8.0 * pl.B * hpix() + 8.0 * np + 4.0 * 2 * pl.B * np;
+        pl.ops.push_back(Op([=](cudaStream_t st) {
+            launch_ex(crbm_cd1_fused_kernel<KW>, dim3(grid), dim3(kCfThreads), smem, st, 1u, p);
+        }, "crbm.cd1_fused", fl, by));
+        pl.fused = true;
+    }
+
     void build(Plan& pl) {
+        if (fused_ok()) {
+            switch (g_.kw) {
+                case 1: build_fused_kw<1>(pl); break;
+                case 2: build_fused_kw<2>(pl); break;
+                case 3: build_fused_kw<3>(pl); break;
+                case 4: build_fused_kw<4>(pl); break;
+                case 5: build_fused_kw<5>(pl); break;
+                case 6: build_fused_kw<6>(pl); break;
+                case 7: build_fused_kw<7>(pl); break;
+                default: build_fused_kw<8>(pl); break;
+            }
+            last_kernels_ = 1;
+            return;
+        }
+        last_kernels_ = 5;
         const int B = (int)pl.B;
         const ConvGeom& g = g_;
         float* P = P_.as<float>();
@@ -345,6 +435,8 @@ class Crbm {
     bool x3_;
     long long ckk_ = 0, nP_ = 0, cap_ = 0;
     long long staged_B_ = 0, last_B_ = 0;
+    bool keep_states_ = false, last_kept_ = false;
+    int last_kernels_ = 1;
     cudaStream_t stream_ = nullptr;
     DevMem P_, Vc_, Hc_, HS_, U_, recon_;
     HostPinned h_recon_;

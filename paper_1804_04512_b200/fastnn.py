@@ -471,6 +471,10 @@ class Crbm:
         _lib.call("b2n_crbm_kernels_per_step", self._h, C.byref(n))
         return n.value
 
+    def keep_states(self, on: bool = True) -> None:
+        """write every step's chain states to HBM so last_states() can read them back"""
+        _lib.call("b2n_crbm_keep_states", self._h, int(on))
+
     def last_states(self, batch: int):
         h0 = np.zeros((batch, self.k, self.oh, self.ow), np.float32)
         hs, h1 = np.zeros_like(h0), np.zeros_like(h0)

@@ -25,6 +25,7 @@ SHAPES = CRBM_CASES + [(1, 28, 28, 12, 5, 5, 100), (3, 32, 32, 8, 5, 5, 16), (16
 def _step(c, h, w, k, kh, kw, B, lr=0.1, seed=0):
     from paper_1804_04512_b200 import fastnn as F
     m = F.Crbm(c, h, w, k, kh, kw)
+    m.keep_states(True)
     ker = O.crbm_init(c, h, w, k, kh, kw, 42 + seed)
     bv = O.uniform_f32(7 + seed, c, -0.1, 0.1)
     bh = O.uniform_f32(8 + seed, k, -0.1, 0.1)
@@ -35,8 +36,16 @@ def _step(c, h, w, k, kh, kw, B, lr=0.1, seed=0):
     return m, (ker, bv, bh), v0, u, recon
 
 
+@pytest.fixture(params=["fused", "split"])
+def crbm_path(request, monkeypatch):
+    """the one-launch per-image step (crbm_fused.cuh) and the tensor-core split path (crbm.cuh)"""
+    if request.param == "split":
+        monkeypatch.setenv("B2N_CRBM_FUSED", "0")
+    return request.param
+
+
 @pytest.mark.parametrize("shape", SHAPES)
-def test_crbm_cd1_step(gpu, shape):
+def test_crbm_cd1_step(gpu, shape, crbm_path):
     c, h, w, k, kh, kw, B = shape
     m, (ker, bv, bh), v0, u, recon_g = _step(*shape)
     h0, hs, v1, h1 = m.last_states(B)
@@ -72,6 +81,7 @@ def test_crbm_init_matches_oracle(gpu):
 def test_crbm_zero_model_hidden_means_one_half(gpu):  # test_energy.cpp:348-363
     from paper_1804_04512_b200 import fastnn as F
     m = F.Crbm(1, 5, 5, 2, 3, 3)
+    m.keep_states(True)
     m.set(np.zeros((2, 1, 3, 3), np.float32), np.zeros(1, np.float32), np.zeros(2, np.float32))
     v0 = O.uniform_f32(19, 50).reshape(2, 1, 5, 5)
     F.crbm_cd_update(m, v0, 0.1, O.canonical_f64(1, 2 * 2 * 9))
@@ -79,7 +89,7 @@ def test_crbm_zero_model_hidden_means_one_half(gpu):  # test_energy.cpp:348-363
     assert np.all(h0 == 0.5)
 
 
-def test_crbm_one_by_one_matches_dense_rbm(gpu):  # test_energy.cpp:466-503
+def test_crbm_one_by_one_matches_dense_rbm(gpu, crbm_path):  # test_energy.cpp:466-503
     from paper_1804_04512_b200 import fastnn as F
     H, V, B = 2, 3, 4
     W = O.rbm_init(H, V, 23)
@@ -107,7 +117,7 @@ def test_crbm_training_reduces_reconstruction(gpu):  # test_energy.cpp:437-464
     assert errs[-1] < errs[0]
 
 
-def test_crbm_staged_steps_match_calls(gpu):
+def test_crbm_staged_steps_match_calls(gpu, crbm_path):
     """run_staged(n) replays the captured step graph: same arithmetic as n cd_update calls"""
     from paper_1804_04512_b200 import fastnn as F
     c, h, w, k, kh, kw, B = 1, 28, 28, 12, 5, 5, 100
@@ -123,6 +133,39 @@ def test_crbm_staged_steps_match_calls(gpu):
     assert b.recon() == ra
     for x, y in zip(a.get(), b.get()):
         np.testing.assert_array_equal(x, y)
+
+
+def test_crbm_fused_is_one_launch_and_matches_split(gpu):
+    """the MNIST-shape CRBM takes the one-launch path; it agrees with the split tensor-core path"""
+    import os
+    from paper_1804_04512_b200 import fastnn as F
+    c, h, w, k, kh, kw, B = 1, 28, 28, 12, 5, 5, 100
+    v0 = O.bernoulli_f32(3, 0.5, B * c * h * w).reshape(B, c, h, w)
+    u = O.canonical_f64(5, B * k * 24 * 24)
+    a = F.Crbm(c, h, w, k, kh, kw)
+    a.init(42)
+    ra = F.crbm_cd_update(a, v0, 0.1, u)
+    assert a.kernels_per_step() == 1
+    os.environ["B2N_CRBM_FUSED"] = "0"
+    try:
+        b = F.Crbm(c, h, w, k, kh, kw)
+        b.init(42)
+        rb = F.crbm_cd_update(b, v0, 0.1, u)
+        assert b.kernels_per_step() == 5
+    finally:
+        del os.environ["B2N_CRBM_FUSED"]
+    ka, kb = a.get()[0], b.get()[0]
+    k0 = O.crbm_init(c, h, w, k, kh, kw, 42)
+    assert norm_err(ka - k0, kb - k0) < 1e-3
+    assert abs(ra - rb) <= 1e-5 * rb
+
+
+def test_crbm_last_states_needs_keep(gpu):
+    from paper_1804_04512_b200 import fastnn as F
+    m = F.Crbm(1, 6, 6, 2, 3, 3)
+    F.crbm_cd_update(m, np.zeros((2, 1, 6, 6), np.float32), 0.1, np.zeros(2 * 2 * 16))
+    with pytest.raises(F.ParamError):
+        m.last_states(2)
 
 
 def test_crbm_shape_errors(gpu):
