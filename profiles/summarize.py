@@ -30,6 +30,7 @@ METRICS = {
 }
 UNIT_SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1, "nsecond": 1e-3, "msecond": 1e3}
 
+CRBM_SPLIT = ["crbm.hidden+sample", "crbm.visible+stats", "crbm.neg_hidden", "crbm.stats", "crbm.update"]
 RBM_STEP = ["rbm.hidden+sample", "rbm.visible+recon", "rbm.neg_hidden", "rbm.dW+update"]
 # launch order of the halo-tile conv kernels in one ImageNet-shape step (capture.sh)
 IMAGENET_CONV = [f"conv{i}.fwd" for i in range(5)] + [x for i in (4, 3, 2, 1) for x in (f"conv{i}.dgrad", f"conv{i}.wgrad")] + ["conv0.wgrad"]
@@ -80,6 +81,10 @@ def main(tag: str):
                                "RBM CD-1 step (headline): the fused single-kernel step"),
                               (OUT / f"{tag}_rbm_split_full.ncu-rep", RBM_STEP,
                                "RBM CD-1 step, split path (4 GEMM launches; data-parallel mode, B2N_RBM_FUSED=0)"),
+                              (OUT / f"{tag}_crbm_full.ncu-rep", ["crbm.cd1_fused"],
+                               "Convolutional RBM CD-1 (SURVEY 8(f)4, MNIST shape): the one-launch step"),
+                              (OUT / f"{tag}_crbm_split_full.ncu-rep", CRBM_SPLIT,
+                               "Convolutional RBM CD-1, split tensor-core path (B2N_CRBM_FUSED=0)"),
                               (OUT / f"{tag}_imagenet_conv_full.ncu-rep", IMAGENET_CONV,
                                "ImageNet-shape CNN (batch 128): halo-tile conv kernels of one step")]:
         if not rep.exists():
@@ -95,7 +100,7 @@ def main(tag: str):
                          f"{d.get('dram_pct', 0):.1f} | {d.get('tensor_pct', 0):.1f} | {d.get('sm_pct', 0):.1f} | "
                          f"{d.get('regs', 0):.0f} | {d.get('grid', 0):.0f} |")
         lines.append("")
-    for c in ["rbm", "mlp", "mnist_cnn", "cifar_cnn", "imagenet_cnn"]:
+    for c in ["rbm", "mlp", "mnist_cnn", "cifar_cnn", "imagenet_cnn", "crbm"]:
         p = OUT / f"{tag}_launches_{c}.csv"
         if not p.exists():
             continue
