@@ -241,6 +241,10 @@ class CrbmWork:
     def kernels_per_step(self):
         return _kernels(self.F._lib, "b2n_crbm_kernels_per_step", self.m.handle)
 
+    @property
+    def dtype(self):
+        return "f32 (FFMA, one-launch step)" if self.kernels_per_step() == 1 else None
+
     def profile(self, steps):
         return _profile(self.F._lib, "b2n_crbm_profile", self.m.handle, steps, self.lr, self.Bg)
 
@@ -565,8 +569,9 @@ def main():
     rl["step_us"] = round(step_ms * 1e3, 2)
     line = {"metric": "train samples/s", "value": round(value, 2), "unit": "samples/s", "n_gpus": dist.world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(step_ms, 5), "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32 (3xTF32 tensor-core GEMMs)" if
-            a.precision == "tf32x3" else "f32 (1xTF32 tensor-core GEMMs)", "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": getattr(work, "dtype", None) or (
+                "f32 (3xTF32 tensor-core GEMMs)" if a.precision == "tf32x3" else "f32 (1xTF32 tensor-core GEMMs)"),
+            "data": "synthetic",
             "config": dict(work.config, l2="flushed between timed steps (512 MiB write)",
                            precision=a.precision),
             "e2e": {"value": round(e2e_val, 2), "unit": "samples/s", "h2d_bytes_per_step": work.h2d,

@@ -247,7 +247,7 @@ class Crbm {
         const int grid = (int)std::min<long long>(pl.B, (long long)sm_count() * std::max(occ, 1));
         const long long np = g.k * ckk_ + g.k + g.c;
         pl.ws = std::make_shared<DevMem>();
-        pl.ws->alloc((size_t)(pl.B * np) * 4);
+        pl.ws->alloc((size_t)(pl.B * round_up(np, 4)) * 4);
         pl.vd = std::make_shared<DevMem>();
         pl.vd->alloc((size_t)pl.B * 8 + 64);
         CrbmFusedParams p;
@@ -277,6 +277,7 @@ class Crbm {
         p.scale = pl.lr / static_cast<float>(pl.Bg);
         p.inv_bg = 1.0 / (double)pl.Bg;
         p.stage_floats = (long long)(smem / 4) - round_up(np, 4) - 16;
+        p.ws_pitch = (int)round_up(np, 4);
         p.trace = TraceRegistry::get().next();
         if (pl.keep) {
             p.h0_out = Hc_.as<float>();

@@ -42,6 +42,7 @@ struct CrbmFusedParams {
     double* recon;       // sum (v0 - v1)^2 / B_global
     float scale;         // lr / B_global
     long long stage_floats;  // smem floats after P available to stage the partials in the last CTA
+    int ws_pitch;            // floats per partial row in ws (npart rounded up to 4)
     double inv_bg;
     // chain states of every image (for last_states / tests); null unless keep_states
     float *h0_out, *hs_out, *v1_out, *h1_out;
@@ -52,30 +53,31 @@ struct CrbmFusedParams {
         if (p.trace && threadIdx.x == 0) p.trace[blockIdx.x * 64 + (slot)] = gtimer();    \
     } while (0)
 
-// Row pitches: every 4-output strip reads its (4 + KW - 1)-wide input window as NV float4s, so a
-// row is padded until the last strip's window fits; pads are zero (written once) and only feed
-// outputs beyond the valid width, which are discarded.
+// Row pitches: every 8-output strip reads its (8 + KW - 1)-wide input window as NV float4s (and
+// the statistics pass 4-wide windows), so a row is padded until the last window fits; pads are zero
+// (written once) and only feed outputs beyond the valid width, which are discarded.
+constexpr int kCfStrip = 8;
 struct CrbmPitches {
     int VP, OP, HPP;
 };
 inline CrbmPitches crbm_pitches(int W, int OW, int KW) {
-    const int NV = (KW + 3 + 3) / 4;
-    const int nsx1 = (OW + 3) / 4, nsx2 = (W + 3) / 4, WP = W + KW - 1;
+    const int NV = (kCfStrip + KW - 1 + 3) / 4, NV4 = (4 + KW - 1 + 3) / 4;
+    const int nsx1 = (OW + kCfStrip - 1) / kCfStrip, nsx2 = (W + kCfStrip - 1) / kCfStrip, WP = W + KW - 1;
     CrbmPitches q;
-    q.VP = (int)round_up(std::max(W, 4 * nsx1 - 4 + 4 * NV), 4);
+    q.VP = (int)round_up(std::max({W, kCfStrip * nsx1 - kCfStrip + 4 * NV, 4 * ((OW + 3) / 4) - 4 + 4 * NV4}), 4);
     q.OP = (int)round_up(OW, 4);
-    q.HPP = (int)round_up(std::max(WP, 4 * nsx2 - 4 + 4 * NV), 4);
+    q.HPP = (int)round_up(std::max(WP, kCfStrip * nsx2 - kCfStrip + 4 * NV), 4);
     return q;
 }
 inline long long crbm_stage_scratch(int C, int K, int KH, int KW) {
-    return std::max<long long>(std::max<long long>(2048, 512LL * KW), (long long)K * C * KH * KW);
+    return std::max<long long>(std::max<long long>(4096, 512LL * KW), (long long)K * C * KH * KW);
 }
 inline size_t crbm_fused_smem(int C, int H, int W, int K, int KH, int KW) {
     const int OH = H - KH + 1, OW = W - KW + 1, HP = OH + 2 * (KH - 1);
     const CrbmPitches q = crbm_pitches(W, OW, KW);
     const long long np = round_up((long long)K * C * KH * KW + K + C, 4);
-    const long long fl = np + 2LL * C * H * q.VP + 2LL * K * OH * q.OP + (long long)K * HP * q.HPP +
-                         crbm_stage_scratch(C, K, KH, KW);
+    const long long fl = np + 2LL * K * C * KH * 8 + 2LL * C * H * q.VP + 2LL * K * OH * q.OP +
+                         (long long)K * HP * q.HPP + crbm_stage_scratch(C, K, KH, KW);
     return (size_t)fl * 4 + 64 * 8;
 }
 
@@ -83,34 +85,41 @@ __device__ __forceinline__ int rup4(int n) { return (n + 3) & ~3; }
 __device__ __forceinline__ float sigmoid_f(float v) { return 1.0f / (1.0f + expf(-v)); }  // energy.hpp:36
 
 // valid correlation of `in` (CI channels x IH rows, row pitch IP, smem) with taps into outputs
-// (f, oy, ox) of F x OHh x OWw; each job owns a strip of 4 consecutive ox (adjacent lanes take
-// adjacent strips: the float4 window loads are conflict-free). FLIP selects the phase-2 form
-// (taps K[ci][f][KH-1-di][KW-1-dj]: flipped, channel-transposed). With G > 1 the ci range is split
-// over G jobs per strip (few-output phases): partial strips go to `part` and the caller runs
-// conv_strips_finish after a barrier. `upre` (phase 1) prefetches the strip's Bernoulli uniforms
-// before the product so their latency hides under it.
-template <int KW, bool FLIP, class Epi>
-__device__ __forceinline__ void conv_strips(const float* __restrict__ in, int IP, int CI, int IH, const float* ker,
-                                            int F, int OHh, int OWw, int KH, int kC, int G, float* part,
-                                            const double* upre, Epi epi) {
-    constexpr int NV = (KW + 3 + 3) / 4;
-    const int nsx = (OWw + 3) >> 2;
+// (f, oy, ox) of F x OHh x OWw; each job owns a strip of 8 consecutive ox (adjacent lanes take
+// adjacent strips: the float4 window loads are conflict-free). taps8 holds the taps of output f,
+// input ci, row di at ((f*CI + ci)*KH + di)*8 (dj padded to 8; the phase-2 copy is already
+// flipped and channel-transposed). With G > 1 the ci range is split over G jobs per strip
+// (few-output phases): partial strips go to `part` and the caller runs conv_strips_finish after a
+// barrier. `upre` (phase 1) prefetches the strip's Bernoulli uniforms before the product so their
+// latency hides under it.
+template <int KW, class Epi>
+__device__ __forceinline__ void conv_strips(const float* __restrict__ in, int IP, int CI, int IH,
+                                            const float* __restrict__ taps8, int F, int OHh, int OWw, int KH, int G,
+                                            float* part, const double* upre, Epi epi) {
+    constexpr int SW = kCfStrip;
+    constexpr int NV = (SW + KW - 1 + 3) / 4;
+    const int nsx = (OWw + SW - 1) / SW;
     const int total = F * OHh * nsx;
     for (int job = threadIdx.x; job < total * G; job += kCfThreads) {
         const int s = job % total, g = job / total;
         const int f = s / (OHh * nsx);
         const int rem = s - f * OHh * nsx;
         const int oy = rem / nsx;
-        const int ox0 = (rem - oy * nsx) * 4;
-        double uu[4] = {0.0, 0.0, 0.0, 0.0};
+        const int ox0 = (rem - oy * nsx) * SW;
+        double uu[SW];
+#pragma unroll
+        for (int t = 0; t < SW; ++t) uu[t] = 0.0;
         if (upre) {
 #pragma unroll
-            for (int t = 0; t < 4; ++t)
+            for (int t = 0; t < SW; ++t)
                 if (ox0 + t < OWw) uu[t] = upre[(f * OHh + oy) * OWw + ox0 + t];
         }
-        float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+        float acc[SW];
+#pragma unroll
+        for (int t = 0; t < SW; ++t) acc[t] = 0.0f;
         const int ci0 = g * CI / G, ci1 = (g + 1) * CI / G;
         for (int ci = ci0; ci < ci1; ++ci) {
+            const float* trow = taps8 + (f * CI + ci) * KH * 8;
             for (int di = 0; di < KH; ++di) {
                 const float4* row = reinterpret_cast<const float4*>(in + (ci * IH + oy + di) * IP + ox0);
                 float win[4 * NV];
@@ -122,37 +131,51 @@ __device__ __forceinline__ void conv_strips(const float* __restrict__ in, int IP
                     win[4 * v + 2] = q.z;
                     win[4 * v + 3] = q.w;
                 }
-                const float* kr = FLIP ? ker + ((ci * kC + f) * KH + (KH - 1 - di)) * KW
-                                       : ker + ((f * CI + ci) * KH + di) * KW;
+                const float4 k0 = *reinterpret_cast<const float4*>(trow + di * 8);
+                const float4 k1 = *reinterpret_cast<const float4*>(trow + di * 8 + 4);
+                const float kw[8] = {k0.x, k0.y, k0.z, k0.w, k1.x, k1.y, k1.z, k1.w};
 #pragma unroll
-                for (int dj = 0; dj < KW; ++dj) {
-                    const float w = FLIP ? kr[KW - 1 - dj] : kr[dj];
+                for (int dj = 0; dj < KW; ++dj)
 #pragma unroll
-                    for (int t = 0; t < 4; ++t) acc[t] = fmaf(w, win[t + dj], acc[t]);
-                }
+                    for (int t = 0; t < SW; ++t) acc[t] = fmaf(kw[dj], win[t + dj], acc[t]);
             }
         }
         if (G > 1) {
-            *reinterpret_cast<float4*>(part + (g * total + s) * 4) = make_float4(acc[0], acc[1], acc[2], acc[3]);
-        } else {
+            float4* o = reinterpret_cast<float4*>(part + (g * total + s) * SW);
 #pragma unroll
-            for (int t = 0; t < 4; ++t)
-                if (ox0 + t < OWw) epi(f, oy, ox0 + t, acc[t], uu[t]);
+            for (int v = 0; v < SW / 4; ++v) o[v] = make_float4(acc[4 * v], acc[4 * v + 1], acc[4 * v + 2], acc[4 * v + 3]);
+        } else {
+            epi(f, oy, ox0, acc, uu, min(SW, OWw - ox0));
         }
     }
 }
-// the G partial strips of every output summed in group order, then the epilogue
+// the G partial strips summed in group order (one thread per strip), then the strip epilogue
 template <class Epi>
 __device__ __forceinline__ void conv_strips_finish(int F, int OHh, int OWw, int G, const float* part, Epi epi) {
-    const int nsx = (OWw + 3) >> 2;
+    constexpr int SW = kCfStrip;
+    const int nsx = (OWw + SW - 1) / SW;
     const int total = F * OHh * nsx;
-    for (int o = threadIdx.x; o < total * 4; o += kCfThreads) {
-        const int s = o >> 2, t = o & 3;
-        const int f = s / (OHh * nsx), rem = s - f * OHh * nsx, oy = rem / nsx, ox = (rem - oy * nsx) * 4 + t;
-        if (ox >= OWw) continue;
-        float a = part[s * 4 + t];
-        for (int g = 1; g < G; ++g) a += part[(g * total + s) * 4 + t];
-        epi(f, oy, ox, a, 0.0);
+    for (int s = threadIdx.x; s < total; s += kCfThreads) {
+        const int f = s / (OHh * nsx), rem = s - f * OHh * nsx, oy = rem / nsx, ox0 = (rem - oy * nsx) * SW;
+        float a[SW];
+        const double uu[SW] = {};
+#pragma unroll
+        for (int t = 0; t < SW; ++t) a[t] = part[s * SW + t];
+        for (int g = 1; g < G; ++g)
+#pragma unroll
+            for (int t = 0; t < SW; ++t) a[t] += part[(g * total + s) * SW + t];
+        epi(f, oy, ox0, a, uu, min(SW, OWw - ox0));
+    }
+}
+
+// n consecutive floats of a strip: two 16-byte stores when the strip is whole and aligned (the
+// scalar form is an 8-way bank conflict: adjacent lanes own strips 8 floats apart)
+__device__ __forceinline__ void store_strip(float* dst, const float* v, int n) {
+    if (n == kCfStrip && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        reinterpret_cast<float4*>(dst)[0] = make_float4(v[0], v[1], v[2], v[3]);
+        reinterpret_cast<float4*>(dst)[1] = make_float4(v[4], v[5], v[6], v[7]);
+    } else {
+        for (int t = 0; t < n; ++t) dst[t] = v[t];
     }
 }
 
@@ -165,7 +188,9 @@ __global__ void __launch_bounds__(kCfThreads, 1) crbm_cd1_fused_kernel(const Crb
     const int CKK = C * KH * KW;
     const int HW = H * W, OHW = OH * OW;
     float* sP = sm;
-    float* sv0 = sP + rup4(p.npart);
+    float* sK8 = sP + rup4(p.npart);       // taps K[f][c][di][0..8) (phases 1, 3)
+    float* sKT8 = sK8 + K * C * KH * 8;    // taps K[k][c][KH-1-di][KW-1-dj] as [c][k][di][0..8) (phase 2)
+    float* sv0 = sKT8 + K * C * KH * 8;
     float* sv1 = sv0 + C * H * VP;
     float* sh0 = sv1 + C * H * VP;
     float* sh1 = sh0 + K * OH * OP;
@@ -184,6 +209,13 @@ __global__ void __launch_bounds__(kCfThreads, 1) crbm_cd1_fused_kernel(const Crb
     }
     pdl_wait();  // P is updated by the previous step's last CTA
     for (int i = tid; i < p.npart; i += kCfThreads) sP[i] = p.P[i];
+    __syncthreads();
+    for (int i = tid; i < K * C * KH * 8; i += kCfThreads) {
+        const int dj = i & 7, r = i >> 3, di = r % KH, fc = r / KH;  // fc = f*C + c
+        sK8[i] = dj < KW ? sP[r * KW + dj] : 0.0f;
+        const int c2 = fc / K, k2 = fc % K;  // sKT8 row (c2, k2, di) <- K[k2][c2][KH-1-di][KW-1-dj]
+        sKT8[i] = dj < KW ? sP[((k2 * C + c2) * KH + (KH - 1 - di)) * KW + (KW - 1 - dj)] : 0.0f;
+    }
     B2N_CF_TRACE(1);
     const float* sbh = sP + K * CKK;
     const float* sbv = sbh + K;
@@ -198,21 +230,31 @@ __global__ void __launch_bounds__(kCfThreads, 1) crbm_cd1_fused_kernel(const Crb
         __syncthreads();
         B2N_CF_TRACE(2);
         // phase 1: hidden means + samples (crbm_hidden_preact + unit_mean / unit_sample)
-        conv_strips<KW, false>(sv0, VP, C, H, sP, K, OH, OW, KH, C, 1, sst, gu,
-                               [&](int f, int oy, int ox, float a, double uv) {
-            const float pr = sigmoid_f(a + sbh[f]);
-            sh0[(f * OH + oy) * OP + ox] = pr;
-            shp[(f * HP + oy + KH - 1) * HPP + ox + KW - 1] = uv < (double)pr ? 1.0f : 0.0f;
+        conv_strips<KW>(sv0, VP, C, H, sK8, K, OH, OW, KH, 1, sst, gu,
+                        [&](int f, int oy, int ox0, const float* a, const double* uv, int n) {
+            float pr[kCfStrip], hs[kCfStrip];
+#pragma unroll
+            for (int t = 0; t < kCfStrip; ++t) {
+                pr[t] = sigmoid_f(a[t] + sbh[f]);
+                hs[t] = uv[t] < (double)pr[t] ? 1.0f : 0.0f;
+            }
+            store_strip(sh0 + (f * OH + oy) * OP + ox0, pr, n);
+            store_strip(shp + (f * HP + oy + KH - 1) * HPP + ox0 + KW - 1, hs, n);
         });
         __syncthreads();
         B2N_CF_TRACE(3);
         // phase 2: visible means from the sample (crbm_visible_preact: full conv, K^T); few
         // outputs, so the hidden-map sum is split over G jobs per strip
         {
-            auto epi2 = [&](int c, int y, int x, float a, double) { sv1[(c * H + y) * VP + x] = sigmoid_f(a + sbv[c]); };
-            const int strips2 = C * H * ((W + 3) >> 2);
+            auto epi2 = [&](int c, int y, int ox0, const float* a, const double*, int n) {
+                float v[kCfStrip];
+#pragma unroll
+                for (int t = 0; t < kCfStrip; ++t) v[t] = sigmoid_f(a[t] + sbv[c]);
+                store_strip(sv1 + (c * H + y) * VP + ox0, v, n);
+            };
+            const int strips2 = C * H * ((W + kCfStrip - 1) / kCfStrip);
             const int G2 = max(1, min(K, kCfThreads / strips2));
-            conv_strips<KW, true>(shp, HPP, K, HP, sP, C, H, W, KH, C, G2, sst, nullptr, epi2);
+            conv_strips<KW>(shp, HPP, K, HP, sKT8, C, H, W, KH, G2, sst, nullptr, epi2);
             if (G2 > 1) {
                 __syncthreads();
                 conv_strips_finish(C, H, W, G2, sst, epi2);
@@ -221,16 +263,19 @@ __global__ void __launch_bounds__(kCfThreads, 1) crbm_cd1_fused_kernel(const Crb
         __syncthreads();
         B2N_CF_TRACE(4);
         // phase 3: hidden means of the reconstruction
-        conv_strips<KW, false>(sv1, VP, C, H, sP, K, OH, OW, KH, C, 1, sst, nullptr,
-                               [&](int f, int oy, int ox, float a, double) {
-            sh1[(f * OH + oy) * OP + ox] = sigmoid_f(a + sbh[f]);
+        conv_strips<KW>(sv1, VP, C, H, sK8, K, OH, OW, KH, 1, sst, nullptr,
+                        [&](int f, int oy, int ox0, const float* a, const double*, int n) {
+            float v[kCfStrip];
+#pragma unroll
+            for (int t = 0; t < kCfStrip; ++t) v[t] = sigmoid_f(a[t] + sbh[f]);
+            store_strip(sh1 + (f * OH + oy) * OP + ox0, v, n);
         });
         __syncthreads();
         B2N_CF_TRACE(5);
         // phase 4a: correlation statistics pos - neg (crbm_corr_stats). Thread = (f, c, di) x a
         // segment of the output rows; KW pos / neg accumulators, the v windows slid along the row
         // (4 outputs per step, zero pads past OW), segments summed in order below.
-        float* wrow = p.ws + (long long)img * p.npart;
+        float* wrow = p.ws + (long long)img * p.ws_pitch;
         {
             const int T = K * C * KH;
             const int S = max(1, min(OH, kCfThreads / T));
@@ -349,23 +394,38 @@ __global__ void __launch_bounds__(kCfThreads, 1) crbm_cd1_fused_kernel(const Crb
     B2N_CF_TRACE(7);
     if (!s_last) return;
     __threadfence();
-    const long long nws = (long long)p.B * p.npart;
+    const long long nws = (long long)p.B * p.ws_pitch;
     if (nws <= p.stage_floats) {
         // stage every image's partial row in shared memory with independent coalesced loads
         // (the image buffers are dead now), then sum each parameter's column in image order
         float* st = sm + rup4(p.npart);
-        for (long long i = tid; i < nws; i += kCfThreads) st[i] = __ldcg(p.ws + i);
+        const int n4 = (int)(nws / 4);  // rows padded to ws_pitch (a multiple of 4)
+        const float4* src = reinterpret_cast<const float4*>(p.ws);
+        float4* dst = reinterpret_cast<float4*>(st);
+        for (int i0 = tid; i0 < n4; i0 += 8 * kCfThreads) {  // 8 independent 16-byte loads in flight
+            float4 t8[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int i = i0 + q * kCfThreads;
+                t8[q] = i < n4 ? __ldcg(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int i = i0 + q * kCfThreads;
+                if (i < n4) dst[i] = t8[q];
+            }
+        }
         __syncthreads();
         B2N_CF_TRACE(8);
         for (int i = tid; i < p.npart; i += kCfThreads) {
             float s = 0.0f;
-            for (int img = 0; img < p.B; ++img) s += st[(long long)img * p.npart + i];
+            for (int img = 0; img < p.B; ++img) s += st[(long long)img * p.ws_pitch + i];
             p.P[i] = sP[i] + p.scale * s;
         }
     } else {
         for (int i = tid; i < p.npart; i += kCfThreads) {
             float s = 0.0f;
-            for (int img = 0; img < p.B; ++img) s += __ldcg(p.ws + (long long)img * p.npart + i);
+            for (int img = 0; img < p.B; ++img) s += __ldcg(p.ws + (long long)img * p.ws_pitch + i);
             p.P[i] = sP[i] + p.scale * s;
         }
     }
