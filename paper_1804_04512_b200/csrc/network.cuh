@@ -36,6 +36,8 @@ struct Op {
     std::string name;
     double flops = 0, bytes = 0;
     int kernels = 1;
+    int branch = 0;  // 1: captured on the side stream after a fork from the main stream (a dense
+                     // wgrad+SGD off the critical path), joined at the end of the graph
     bool is_gemm = false;
     GemmLaunch gemm;  // when is_gemm: launched directly (its PDL prefetch flags are per op list)
     Op() = default;
@@ -59,23 +61,39 @@ inline Op gemm_op(const GemmLaunch& g, const std::string& name) {
     return o;
 }
 // PDL prefetch analysis over one captured op list: a GEMM operand may be loaded before
-// griddepcontrol.wait iff the immediately preceding op does not write it (kernel N-2 has always
-// completed when kernel N launches). Non-GEMM ops count as writing everything.
+// griddepcontrol.wait iff the immediately preceding op OF THE SAME STREAM does not write it (kernel
+// N-2 has always completed when kernel N launches). Non-GEMM ops count as writing everything; ops on
+// the side branch (fork / join through events) never prefetch.
+// B2N_BRANCH=0 keeps every op of the step on one stream (A/B measurement of the fork)
+inline bool branch_wgrad() {
+    static const bool on = [] {
+        const char* e = std::getenv("B2N_BRANCH");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 inline void assign_prefetch(std::vector<Op>& ops) {
+    const Op* prev_main = nullptr;
     for (size_t i = 0; i < ops.size(); ++i) {
-        if (!ops[i].is_gemm) continue;
-        GemmLaunch& g = ops[i].gemm;
-        if (i == 0) {  // first node of a graph: no in-graph predecessor
-            g.p.pre_a = g.p.pre_b = 1;
+        Op& op = ops[i];
+        if (op.branch) {
+            if (op.is_gemm) op.gemm.p.pre_a = op.gemm.p.pre_b = 0;
             continue;
         }
-        const Op& prev = ops[i - 1];
-        if (!prev.is_gemm) {
+        const Op* prev = prev_main;
+        prev_main = &op;
+        if (!op.is_gemm) continue;
+        GemmLaunch& g = op.gemm;
+        if (!prev) {  // first main-stream node of a graph: no in-graph predecessor
+            g.p.pre_a = g.p.pre_b = i == 0 ? 1 : 0;
+            continue;
+        }
+        if (!prev->is_gemm) {
             g.p.pre_a = g.p.pre_b = 0;
             continue;
         }
         bool wa = false, wb = false;
-        for (const auto& w : prev.gemm.writes) {
+        for (const auto& w : prev->gemm.writes) {
             wa = wa || overlaps(w, g.a_rng);
             wb = wb || overlaps(w, g.b_rng);
         }
@@ -292,6 +310,8 @@ class Net {
     int device_;
     bool x3_;
     cudaStream_t stream_ = nullptr;
+    cudaStream_t side_ = nullptr;  // graph-capture side branch (dense wgrad+SGD off the critical path)
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
     std::vector<long long> input_;
     std::vector<Layer> layers_;
     std::vector<ParamView> params_;
@@ -532,6 +552,9 @@ inline Net::Net(const b2n_network_spec& spec, int device, int precision)
 
 inline Net::~Net() {
     plans_.clear();
+    if (ev_fork_) cudaEventDestroy(ev_fork_);
+    if (ev_join_) cudaEventDestroy(ev_join_);
+    if (side_) cudaStreamDestroy(side_);
     if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -788,6 +811,9 @@ inline void Net::build_plan(Plan& pl) {
             GemmLaunch gs = plan_gemm((int)L.out, (int)L.in + 1, B, {L.D, L.ldd, true}, {L.Ain, L.ld_in, true},
                                       EPI_STORE, es, x3_);
             bwd_fused.push_back(gemm_op(gf, "dense" + std::to_string(ii) + ".wgrad+sgd"));
+            // off the critical path: only the next step's forward (after the graph's join) reads the
+            // updated W / V, and this layer's dgrad (which reads W) precedes the fork
+            if (branch_wgrad()) bwd_fused.back().branch = 1;
             bwd_split.push_back(gemm_op(gs, "dense" + std::to_string(ii) + ".wgrad"));
             ++nk_fused;
             ++nk_split;
@@ -871,6 +897,8 @@ inline void Net::build_plan(Plan& pl) {
         for (const Op& o : v) n += o.kernels;
         return n;
     };
+    // the step's last op stays on the main stream (it then runs beside the side chain)
+    if (!bwd_fused.empty()) bwd_fused.back().branch = 0;
     nk_fwd = count(fwd);
     nk_fused = count(bwd_fused);
     nk_split = count(bwd_split);
@@ -957,9 +985,30 @@ inline void Net::launch(Plan& pl, int mode) {
     if (opt_ == OPT_ADAM && lr_ != 0.0f && (mode == TRAIN || mode == SPLIT_APPLY || mode == FIT)) note_opt_step();
     if (!pl.graph[mode]) {
         cudaGraph_t graph;
+        bool branched = false;
+        for (const auto& op : pl.ops[mode]) branched = branched || op.branch;
+        if (branched && !side_) {
+            B2N_CUDA(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+            B2N_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+            B2N_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+        }
         B2N_CUDA(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
         try {
-            for (auto& op : pl.ops[mode]) op(stream_);
+            // side-branch ops fork from the main stream right after the op before them (whose
+            // outputs they read) and run beside the rest of the main chain; one join at the end
+            for (auto& op : pl.ops[mode]) {
+                if (op.branch) {
+                    B2N_CUDA(cudaEventRecord(ev_fork_, stream_));
+                    B2N_CUDA(cudaStreamWaitEvent(side_, ev_fork_, 0));
+                    op(side_);
+                } else {
+                    op(stream_);
+                }
+            }
+            if (branched) {
+                B2N_CUDA(cudaEventRecord(ev_join_, side_));
+                B2N_CUDA(cudaStreamWaitEvent(stream_, ev_join_, 0));
+            }
         } catch (...) {
             cudaStreamEndCapture(stream_, &graph);
             throw;

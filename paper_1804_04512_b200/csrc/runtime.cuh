@@ -337,6 +337,10 @@ inline Tiling pick_tiling(int M, int N, int K, bool b_mn, int epi) {
         if (b_mn && bn < 32) bn = 32;
     } else if (N <= 16 && !b_mn && bn_allowed(epi, 16)) {
         bn = 16;
+    } else if (epi == EPI_SGD && mt * ((N + 31) / 32) <= 148) {
+        // the SGD epilogue reads and writes W and V (16 B per output) -- far more traffic than the
+        // K = batch product: the narrowest tile spreads it over the most SMs (while one wave)
+        bn = 32;
     } else {
         bn = 32;
         for (int c : {128, 64})
