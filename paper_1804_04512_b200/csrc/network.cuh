@@ -865,10 +865,15 @@ inline void Net::build_plan(Plan& pl) {
             const ConvTWLaunch wf = wplan(true), wsp = wplan(false);
             const double fl = wf.flops + (has_d ? d.flops : 0.0), by = wf.bytes + (has_d ? d.bytes : 0.0);
             const int nk = has_d ? 3 : 2;
-            bwd_fused.push_back(Op([d, wf, has_d](cudaStream_t s) {
-                if (has_d) d.run(s);
-                wf.run(s, true);
-            }, "conv" + std::to_string(ii) + ".bwd+sgd", fl, by, nk));
+            // dgrad on the main chain, then the weight gradient + SGD forked onto the side branch:
+            // it must follow this layer's dgrad (which reads the kernels it updates) but nothing
+            // on the main chain below reads its outputs before the graph's join
+            if (has_d)
+                bwd_fused.push_back(Op([d](cudaStream_t s) { d.run(s); }, "conv" + std::to_string(ii) + ".dgrad", d.flops,
+                                       d.bytes, 1));
+            bwd_fused.push_back(Op([wf](cudaStream_t s) { wf.run(s, true); }, "conv" + std::to_string(ii) + ".wgrad+sgd",
+                                   wf.flops, wf.bytes, 2));
+            if (branch_wgrad()) bwd_fused.back().branch = 1;
             bwd_split.push_back(Op([d, wsp, has_d](cudaStream_t s) {
                 if (has_d) d.run(s);
                 wsp.run(s, false);
