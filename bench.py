@@ -186,6 +186,33 @@ class RbmWork:
             return self.rbm.recon()
         return self.F.cd_k_update(self.rbm, self.v0_h, 1, self.lr, self.u_h, self.Bg)
 
+    def e2e_total(self, steps, warmup):
+        """end to end through Rbm.train_stream (the loop of cd_k_update calls over host batches):
+        `steps` distinct host batches (v0 + uniforms, pinned; together larger than L2), every step's
+        H2D inside the timed region (overlapped with the previous step) and every step's recon
+        read back. Returns the device time of the whole call (ms) on the library stream."""
+        if self.dist.world > 1:
+            return None
+        import torch
+        from oracle import oracle as O  # synthetic-input generators (std::mt19937 streams), not the measured path
+        n = steps * self.B
+        if getattr(self, "_sv", None) is None or self._sv.shape[0] < n:
+            self._sv = pinned((n, self.V), np.float32)
+            self._sv[:] = O.bernoulli_f32(11, 0.5, n * self.V).reshape(n, self.V)
+            self._su = pinned((n, self.H), np.float64)
+            self._su[:] = O.canonical_f64(13, n * self.H).reshape(n, self.H)
+        self.rbm.train_stream(self._sv[:max(warmup, 1) * self.B], self._su[:max(warmup, 1) * self.B], self.B, self.lr)
+        s = torch.cuda.ExternalStream(self.stream())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        self.dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(s)
+        self.rbm.train_stream(self._sv[:n], self._su[:n], self.B, self.lr)
+        e1.record(s)
+        torch.cuda.synchronize()
+        self.dist.barrier()
+        return self.dist.max(e0.elapsed_time(e1))
+
     def kernels_per_step(self):
         return _kernels(self.F._lib, "b2n_rbm_kernels_per_step", self.rbm.handle)
 
@@ -554,7 +581,11 @@ def main():
         torch.cuda.synchronize()
     with ClockSampler(dev) as clk:
         total_ms = time_steps(work, a.steps, a.warmup, dist, flush)
-        e2e_ms = time_steps(work, a.steps, max(a.warmup // 2, 3), dist, flush, e2e=True)
+        e2e_ms = work.e2e_total(a.steps, max(a.warmup // 2, 3)) if hasattr(work, "e2e_total") else None
+        e2e_mode = "stream"
+        if e2e_ms is None:
+            e2e_ms = time_steps(work, a.steps, max(a.warmup // 2, 3), dist, flush, e2e=True)
+            e2e_mode = "per-call"
     prof = work.profile(max(min(a.steps, 50), 5))
     step_ms = total_ms / a.steps
     value = work.Bg * a.steps / (total_ms * 1e-3)
@@ -575,7 +606,11 @@ def main():
             "config": dict(work.config, l2="flushed between timed steps (512 MiB write)",
                            precision=a.precision),
             "e2e": {"value": round(e2e_val, 2), "unit": "samples/s", "h2d_bytes_per_step": work.h2d,
-                    "d2h_bytes_per_step": work.d2h_bytes(), "ms_per_step": round(e2e_ms / a.steps, 5)},
+                    "d2h_bytes_per_step": work.d2h_bytes(), "ms_per_step": round(e2e_ms / a.steps, 5),
+                    "api": ("Rbm.train_stream: one call over `steps` distinct pinned host batches (143 MB at 200 "
+                            "steps, > L2), each step's H2D overlapped with the previous step, per-step recon read "
+                            "back" if e2e_mode == "stream" else "one public-API step call per step (H2D, step, "
+                            "result read), L2 flushed between steps")},
             "gpu_launches": work.kernels_per_step() * a.steps,
             "kernels_per_step": work.kernels_per_step(),
             "roofline": rl,

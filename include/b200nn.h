@@ -190,6 +190,12 @@ int b2n_rbm_dp_init(b2n_rbm* rbm, const char id[128], int rank, int world);
 int b2n_rbm_stage(b2n_rbm* rbm, const float* v0_host, const double* uniforms_host, long long batch);
 int b2n_rbm_run_staged(b2n_rbm* rbm, int steps, float lr, long long batch_global);
 int b2n_rbm_recon(b2n_rbm* rbm, double* recon);
+/* `steps` CD-1 updates (k = 1) over consecutive host batches -- the reference's loop of
+ * cd_k_update calls: step i uses rows [i*batch, (i+1)*batch) of v0_host (steps*batch x visible)
+ * and of uniforms_host (steps*batch x hidden). The host->device copy of step i+1 overlaps step i
+ * (double-buffered staging on a copy stream); recon_out[i] = step i's reconstruction error. */
+int b2n_rbm_train_stream(b2n_rbm* rbm, const float* v0_host, const double* uniforms_host, long long steps,
+                         long long batch, float lr, double* recon_out);
 int b2n_rbm_stream(b2n_rbm* rbm, void** cuda_stream);
 /* dbn_pretrain (energy.hpp:208-240): greedy CD-1 training of a stack of `layers` RBMs (layer l's
  * visible extent == layer l-1's hidden extent; all on one device). `data` (n x visible(0), host)

@@ -300,6 +300,10 @@ int b2n_rbm_stage(b2n_rbm* r, const float* v0, const double* u, long long batch)
 int b2n_rbm_run_staged(b2n_rbm* r, int steps, float lr, long long batch_global) {
     return guard([&] { r->impl.run_staged(steps, lr, batch_global); });
 }
+int b2n_rbm_train_stream(b2n_rbm* r, const float* v0, const double* u, long long steps, long long batch, float lr,
+                         double* recon_out) {
+    return guard([&] { r->impl.train_stream(v0, u, steps, batch, lr, recon_out); });
+}
 int b2n_rbm_recon(b2n_rbm* r, double* recon) {
     return guard([&] { *recon = r->impl.recon(); });
 }

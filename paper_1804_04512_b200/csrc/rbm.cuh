@@ -65,6 +65,11 @@ class Rbm {
         plans_.clear();
         for (cudaEvent_t e : uev_)
             if (e) cudaEventDestroy(e);
+        for (int j = 0; j < 2; ++j) {
+            if (ev_copied_[j]) cudaEventDestroy(ev_copied_[j]);
+            if (ev_used_[j]) cudaEventDestroy(ev_used_[j]);
+        }
+        if (copy_stream_) cudaStreamDestroy(copy_stream_);
         if (recon_host_) cudaFreeHost(recon_host_);
         if (stream_) cudaStreamDestroy(stream_);
     }
@@ -212,6 +217,65 @@ class Rbm {
         B2N_CUDA(cudaStreamSynchronize(stream_));
         last_B_ = 0;
         return acc / (double)batches;
+    }
+
+    // A stream of CD-1 steps over host batches (the reference's training loop of cd_k_update calls,
+    // energy.hpp:131): step i takes rows [i B, (i + 1) B) of v0 (pitch V) and of the uniforms
+    // (pitch H). The H2D of step i + 1 runs on a copy stream into the other of two device staging
+    // buffers while step i computes (the fused kernel reads its v0 / uniforms from the staging
+    // buffer it is handed); each step's reconstruction error lands in a device array read back
+    // once. recon_out[i] = step i's cd_k_update return value.
+    void train_stream(const float* v0, const double* u, long long steps, long long B, float lr, double* recon_out) {
+        if (dp_) throw Error(B2N_EPARAM, "train_stream: data-parallel RBMs step through run_staged");
+        if (steps < 1 || B < 1) throw Error(B2N_ESHAPE, "train_stream: need steps >= 1 and batch >= 1");
+        ensure_capacity(B, 1);
+        Plan& pl = plan_for(B, 1, lr, B);
+        if (!pl.fused || V_ % 4 != 0) {  // the split path: staged copies + the step graph, in order
+            for (long long i = 0; i < steps; ++i) {
+                stage(v0 + i * B * V_, u + i * B * H_, B, 1);
+                launch(pl);
+                last_B_ = B;
+                last_Bg_ = B;
+                recon_out[i] = recon();
+            }
+            return;
+        }
+        prepare(pl);
+        for (int j = 0; j < 2; ++j) {
+            if (sv_[j].bytes < (size_t)(B * V_ * 4)) sv_[j].alloc((size_t)(B * V_ * 4));
+            if (su_[j].bytes < (size_t)(B * H_ * 8)) su_[j].alloc((size_t)(B * H_ * 8));
+            if (!ev_copied_[j]) B2N_CUDA(cudaEventCreateWithFlags(&ev_copied_[j], cudaEventDisableTiming));
+            if (!ev_used_[j]) B2N_CUDA(cudaEventCreateWithFlags(&ev_used_[j], cudaEventDisableTiming));
+        }
+        if (!copy_stream_) B2N_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
+        if (rstream_.bytes < (size_t)steps * 8) rstream_.alloc((size_t)steps * 8);
+        B2N_CUDA(cudaEventRecord(ev_used_[0], stream_));  // staging buffers free after prior work
+        B2N_CUDA(cudaEventRecord(ev_used_[1], stream_));
+        for (long long i = 0; i < steps; ++i) {
+            const int j = (int)(i & 1);
+            B2N_CUDA(cudaStreamWaitEvent(copy_stream_, ev_used_[j], 0));  // step i - 2 done with buffer j
+            B2N_CUDA(cudaMemcpyAsync(sv_[j].p, v0 + i * B * V_, (size_t)(B * V_ * 4), cudaMemcpyHostToDevice,
+                                     copy_stream_));
+            B2N_CUDA(cudaMemcpyAsync(su_[j].p, u + i * B * H_, (size_t)(B * H_ * 8), cudaMemcpyHostToDevice,
+                                     copy_stream_));
+            B2N_CUDA(cudaEventRecord(ev_copied_[j], copy_stream_));
+            B2N_CUDA(cudaStreamWaitEvent(stream_, ev_copied_[j], 0));
+            RbmFusedParams rp = pl.rp;
+            rp.v0_src = sv_[j].as<float>();
+            rp.ld_src = V_;
+            rp.u_src = su_[j].as<double>();
+            rp.recon_out = rstream_.as<double>() + i;
+            launch_ex(rbm_cd1_fused_kernel, dim3(kRfSlices, rp.jt), dim3(kRfThreads), (size_t)kRfSmem, stream_, 1u,
+                      pl.maps[0], pl.maps[1], pl.maps[2], pl.maps[3], pl.maps[4], pl.maps[5], rp);
+            B2N_CUDA(cudaEventRecord(ev_used_[j], stream_));
+        }
+        B2N_CUDA(cudaMemcpyAsync(recon_out, rstream_.p, (size_t)steps * 8, cudaMemcpyDeviceToHost, stream_));
+        spin_sync(stream_);
+        staged_B_ = B;
+        staged_k_ = 1;
+        last_B_ = B;
+        last_Bg_ = B;
+        recon_mapped_ = false;
     }
 
     // rbm_transform_up (energy.hpp:122-126): out = sigmoid(data . W^T + bh) for n rows, data pitch
@@ -528,6 +592,10 @@ class Rbm {
     HostPinned ubuf_[2];       // train_epoch: double-buffered uniforms
     cudaEvent_t uev_[2] = {nullptr, nullptr};
     DevMem racc_;              // train_epoch: device sum of per-step reconstruction errors
+    DevMem sv_[2], su_[2];     // train_stream: double-buffered device staging of v0 / uniforms
+    DevMem rstream_;           // train_stream: per-step reconstruction errors
+    cudaEvent_t ev_copied_[2] = {nullptr, nullptr}, ev_used_[2] = {nullptr, nullptr};
+    cudaStream_t copy_stream_ = nullptr;
   public:
     void read_trace(unsigned long long* h) {
         B2N_CUDA(cudaDeviceSynchronize());

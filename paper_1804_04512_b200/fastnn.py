@@ -393,6 +393,20 @@ class Rbm:
         _lib.call("b2n_rbm_recon", self._h, C.byref(out))
         return out.value
 
+    def train_stream(self, v0, uniforms, batch: int, lr: float) -> np.ndarray:
+        """CD-1 over consecutive host batches (rows [i*batch, (i+1)*batch) of v0 / uniforms per
+        step), copies of step i+1 overlapped with step i; returns every step's recon error."""
+        v0 = np.ascontiguousarray(v0, np.float32)
+        u = np.ascontiguousarray(uniforms, np.float64)
+        if v0.ndim != 2 or v0.shape[1] != self.visible or v0.shape[0] % batch:
+            raise ShapeError("train_stream: v0 must be (steps * batch, visible)")
+        steps = v0.shape[0] // batch
+        if u.size < steps * batch * self.hidden:
+            raise ShapeError("train_stream: need steps * batch * hidden uniforms")
+        out = np.zeros(steps, np.float64)
+        _lib.call("b2n_rbm_train_stream", self._h, _f(v0), _d(u), steps, batch, lr, _d(out))
+        return out
+
     def stream_handle(self) -> int:
         s = C.c_void_p()
         _lib.call("b2n_rbm_stream", self._h, C.byref(s))

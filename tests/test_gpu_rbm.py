@@ -85,3 +85,29 @@ def test_zero_copy_pinned_inputs_match_staged(gpu):
     sa, sb = a.last_states(B), b.last_states(B)
     for x, y in zip(sa, sb):
         assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_train_stream_matches_cd_k_calls(gpu, fused, monkeypatch):
+    """train_stream (double-buffered host->device staging overlapped with the steps) runs the same
+    kernel arithmetic as one cd_k_update call per batch: identical per-step recon and weights"""
+    import torch
+    from paper_1804_04512_b200 import fastnn as F
+    monkeypatch.setenv("B2N_RBM_FUSED", fused)
+    S, B, V, H = 5, 100, 784, 500
+    v0 = O.bernoulli_f32(3, 0.5, S * B * V).reshape(S * B, V)
+    u = O.canonical_f64(5, S * B * H).reshape(S * B, H)
+    v0p = torch.empty((S * B, V), dtype=torch.float32, pin_memory=True).numpy()
+    up = torch.empty((S * B, H), dtype=torch.float64, pin_memory=True).numpy()
+    v0p[:] = v0
+    up[:] = u
+    a, b = F.Rbm(H, V), F.Rbm(H, V)
+    a.init(42)
+    b.init(42)
+    ra = [F.cd_k_update(a, v0[i * B:(i + 1) * B], 1, 0.1, u[i * B:(i + 1) * B]) for i in range(S)]
+    rb = b.train_stream(v0p, up, B, 0.1)
+    assert list(rb) == ra
+    for x, y in zip(a.get(), b.get()):
+        np.testing.assert_array_equal(x, y)
+    rc = b.train_stream(v0, u, B, 0.1)  # pageable host buffers: same path, staged copies
+    assert np.all(np.isfinite(rc)) and len(rc) == S
