@@ -118,6 +118,11 @@ int b2n_train_minibatch(b2n_net* net, const float* x_host, const float* y_onehot
 int b2n_train_minibatch_labels(b2n_net* net, const float* x_host, const int* labels_host, long long batch,
                                double* loss);
 /* forward_batch + argmax_row (network.hpp:66-72, :402): probs (batch x classes) and first-max ids */
+/* `steps` train_minibatch_labels calls over consecutive host batches: step i uses rows
+ * [i*batch, (i+1)*batch) of x_host / labels_host; the host->device copy of step i+1 overlaps
+ * step i (double-buffered staging on a copy stream). loss_out[i] = step i's loss. */
+int b2n_net_train_stream(b2n_net* net, const float* x_host, const int* labels_host, long long steps, long long batch,
+                         double* loss_out);
 int b2n_forward_batch(b2n_net* net, const float* x_host, long long batch, float* probs_host, int* argmax_host);
 
 /* Data-parallel pieces. forward_backward leaves the full-batch-scaled gradient

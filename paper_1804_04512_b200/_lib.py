@@ -102,6 +102,7 @@ _SIGS = {
     "b2n_net_set_hparams": ([_VP, C.c_float, C.c_float, C.c_float], C.c_int),
     "b2n_train_minibatch": ([_VP, _F, _F, C.c_longlong, _D], C.c_int),
     "b2n_train_minibatch_labels": ([_VP, _F, _I, C.c_longlong, _D], C.c_int),
+    "b2n_net_train_stream": ([_VP, _F, _I, C.c_longlong, C.c_longlong, _D], C.c_int),
     "b2n_forward_batch": ([_VP, _F, C.c_longlong, _F, _I], C.c_int),
     "b2n_net_forward_backward": ([_VP, _F, _I, C.c_longlong, C.c_longlong, _D], C.c_int),
     "b2n_net_apply_update": ([_VP], C.c_int),

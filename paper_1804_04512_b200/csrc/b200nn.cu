@@ -124,6 +124,10 @@ int b2n_train_minibatch(b2n_net* net, const float* x, const float* y_onehot, lon
         *loss = net->impl.train(x, labels.data(), batch);
     });
 }
+int b2n_net_train_stream(b2n_net* net, const float* x, const int* labels, long long steps, long long batch,
+                         double* loss_out) {
+    return guard([&] { net->impl.train_stream(x, labels, steps, batch, loss_out); });
+}
 int b2n_train_minibatch_labels(b2n_net* net, const float* x, const int* labels, long long batch, double* loss) {
     return guard([&] { *loss = net->impl.train(x, labels, batch); });
 }

@@ -191,6 +191,18 @@ static __global__ void fit_advance_kernel(const double* __restrict__ row_loss, i
     st->pos += count;
 }
 
+// train_stream: the step's loss (row losses summed in row order, network.hpp:433-435) into the
+// next slot of the per-step array
+static __global__ void stream_loss_kernel(const double* __restrict__ row_loss, int count, double* out) {
+    pdl_wait();
+    if (threadIdx.x != 0) return;
+    double s = 0.0;
+    for (int r = 0; r < count; ++r) s += row_loss[r];
+    unsigned long long* idx = reinterpret_cast<unsigned long long*>(out - 1);
+    out[*idx] = s;
+    *idx += 1;
+}
+
 // BatchIterator's order (data.hpp:224-238): iota, then std::shuffle with mt19937(seed) at construction
 // and mt19937(seed + epoch) on the current order for every later epoch (network.hpp:495)
 inline void batch_order(std::vector<long long>& order, long long N, unsigned seed, int epoch) {
@@ -251,6 +263,10 @@ class Net {
     }
 
     double train(const float* x, const int* labels, long long B);
+    // `steps` train_minibatch calls over consecutive host batches (rows [i B, (i + 1) B) of x / labels);
+    // the H2D of step i + 1 runs on a copy stream into the other of two device staging buffers while
+    // step i computes. loss_out[i] = step i's train_minibatch return value.
+    void train_stream(const float* x, const int* labels, long long steps, long long B, double* loss_out);
     double forward_backward(const float* x, const int* labels, long long B, long long Bg);
     void apply_update();
     void forward(const float* x, long long B, float* probs, int* argmax);
@@ -285,7 +301,8 @@ class Net {
     // TRAIN = the whole training step of this net: FUSED (SGD epilogues in the backward kernels) when
     // the optimizer is SGD-momentum on one GPU, else SPLIT + SPLIT_APPLY (allreduce and / or the
     // packed optimizer kernel), SPLIT alone when lr == 0
-    enum Mode { FUSED = 0, SPLIT = 1, FWD = 2, SPLIT_APPLY = 3, FIT = 4, EVAL = 5, TRAIN = 6, NMODES = 7 };
+    enum Mode { FUSED = 0, SPLIT = 1, FWD = 2, SPLIT_APPLY = 3, FIT = 4, EVAL = 5, TRAIN = 6, STREAM0 = 7, STREAM1 = 8,
+                NMODES = 9 };
     struct Plan {
         long long B = 0, Bg = 0;
         std::vector<Op> ops[NMODES];
@@ -303,6 +320,12 @@ class Net {
     void build_plan(Plan& pl);
     void launch(Plan& pl, int mode);
     void stage_inputs(const float* x, const int* labels, long long B);
+    void build_stream_ops(Plan& pl, int j);
+    DevMem sx_[2], sl_[2];   // train_stream: double-buffered device staging of x / labels
+    DevMem sloss_;           // train_stream: per-step loss sums [kStreamChunk] + step counter
+    static constexpr long long kStreamChunk = 4096;
+    cudaEvent_t ev_copied_[2] = {nullptr, nullptr}, ev_used_[2] = {nullptr, nullptr};
+    cudaStream_t copy_stream_ = nullptr;
     double read_loss(long long B);
     void invalidate_plans() { plans_.clear(); }
     void check_train_params() const;
@@ -552,6 +575,11 @@ inline Net::Net(const b2n_network_spec& spec, int device, int precision)
 
 inline Net::~Net() {
     plans_.clear();
+    for (int j = 0; j < 2; ++j) {
+        if (ev_copied_[j]) cudaEventDestroy(ev_copied_[j]);
+        if (ev_used_[j]) cudaEventDestroy(ev_used_[j]);
+    }
+    if (copy_stream_) cudaStreamDestroy(copy_stream_);
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
     if (side_) cudaStreamDestroy(side_);
@@ -987,7 +1015,9 @@ inline void Net::note_opt_step() {
 }
 
 inline void Net::launch(Plan& pl, int mode) {
-    if (opt_ == OPT_ADAM && lr_ != 0.0f && (mode == TRAIN || mode == SPLIT_APPLY || mode == FIT)) note_opt_step();
+    if (opt_ == OPT_ADAM && lr_ != 0.0f && (mode == TRAIN || mode == SPLIT_APPLY || mode == FIT || mode == STREAM0 ||
+                                          mode == STREAM1))
+        note_opt_step();
     if (!pl.graph[mode]) {
         cudaGraph_t graph;
         bool branched = false;
@@ -1062,6 +1092,88 @@ inline double Net::train(const float* x, const int* labels, long long B) {
     last_B_ = B;
     last_Bg_ = B;
     return read_loss(B) / (double)B;
+}
+
+inline void Net::build_stream_ops(Plan& pl, int j) {
+    const long long B = pl.B;
+    const long long per = numel(input_);
+    float* X = X_;
+    const long long ldx = ldx_;
+    int* lab = labels_;
+    const float* sx = sx_[j].as<float>();
+    const int* sl = sl_[j].as<int>();
+    std::vector<Op> ops;
+    ops.push_back(Op([=](cudaStream_t s) {  // staging buffer j -> the step's input / label buffers
+        B2N_CUDA(cudaMemcpy2DAsync(X, ldx * 4, sx, per * 4, per * 4, B, cudaMemcpyDeviceToDevice, s));
+        B2N_CUDA(cudaMemcpyAsync(lab, sl, B * 4, cudaMemcpyDeviceToDevice, s));
+    }, "stream.stage", 0.0, (double)B * (per + 1) * 8, 0));
+    const std::vector<Op>& body = pl.ops[TRAIN];
+    ops.insert(ops.end(), body.begin(), body.end());
+    const double* rl = row_loss_;
+    double* out = sloss_.as<double>() + 1;
+    ops.push_back(Op([=](cudaStream_t s) {
+        launch_ex(stream_loss_kernel, dim3(1), dim3(32), 0, s, 1u, rl, (int)B, out);
+    }, "stream.loss", 0.0, (double)B * 8));
+    assign_prefetch(ops);
+    pl.ops[STREAM0 + j] = ops;
+    int n = 0;
+    for (const Op& o : ops) n += o.kernels;
+    pl.nkernels[STREAM0 + j] = n;
+}
+
+inline void Net::train_stream(const float* x, const int* labels, long long steps, long long B, double* loss_out) {
+    if (B < 1 || steps < 1) throw Error(B2N_ESHAPE, "train_stream: need steps >= 1 and batch >= 1");
+    if (dp_) throw Error(B2N_EPARAM, "data-parallel nets step through forward_backward + apply_update");
+    check_train_params();
+    for (long long r = 0; r < steps * B; ++r)  // softmax_cross_entropy's one-hot check (network.hpp:423-432)
+        if (labels[r] < 0 || labels[r] >= classes_)
+            throw Error(B2N_ELABEL, "softmax_cross_entropy: labels must be one-hot; row " + std::to_string(r % B));
+    ensure_capacity(B);
+    const long long per = numel(input_);
+    if (sx_[0].bytes < (size_t)(cap_ * per * 4) || !sloss_.p) {
+        for (int j = 0; j < 2; ++j) {
+            sx_[j].alloc((size_t)(cap_ * per * 4));
+            sl_[j].alloc((size_t)cap_ * 4);
+        }
+        sloss_.alloc((size_t)(kStreamChunk + 1) * 8);
+        for (auto& kv : plans_)  // stream graphs captured the old staging pointers
+            for (int m : {STREAM0, STREAM1}) {
+                if (kv.second->graph[m]) cudaGraphExecDestroy(kv.second->graph[m]);
+                kv.second->graph[m] = nullptr;
+                kv.second->ops[m].clear();
+            }
+    }
+    for (int j = 0; j < 2; ++j) {
+        if (!ev_copied_[j]) B2N_CUDA(cudaEventCreateWithFlags(&ev_copied_[j], cudaEventDisableTiming));
+        if (!ev_used_[j]) B2N_CUDA(cudaEventCreateWithFlags(&ev_used_[j], cudaEventDisableTiming));
+    }
+    if (!copy_stream_) B2N_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
+    Plan& pl = plan_for(B, B);
+    for (int j = 0; j < 2; ++j)
+        if (pl.ops[STREAM0 + j].empty()) build_stream_ops(pl, j);
+    B2N_CUDA(cudaEventRecord(ev_used_[0], stream_));  // staging buffers free after prior work
+    B2N_CUDA(cudaEventRecord(ev_used_[1], stream_));
+    for (long long c0 = 0; c0 < steps; c0 += kStreamChunk) {
+        const long long n = std::min(kStreamChunk, steps - c0);
+        B2N_CUDA(cudaMemsetAsync(sloss_.p, 0, 8, stream_));  // step counter
+        for (long long i = c0; i < c0 + n; ++i) {
+            const int j = (int)(i & 1);
+            B2N_CUDA(cudaStreamWaitEvent(copy_stream_, ev_used_[j], 0));  // step i - 2 done with buffer j
+            B2N_CUDA(cudaMemcpyAsync(sx_[j].p, x + i * B * per, (size_t)(B * per * 4), cudaMemcpyHostToDevice,
+                                     copy_stream_));
+            B2N_CUDA(cudaMemcpyAsync(sl_[j].p, labels + i * B, (size_t)B * 4, cudaMemcpyHostToDevice, copy_stream_));
+            B2N_CUDA(cudaEventRecord(ev_copied_[j], copy_stream_));
+            B2N_CUDA(cudaStreamWaitEvent(stream_, ev_copied_[j], 0));
+            launch(pl, STREAM0 + j);
+            B2N_CUDA(cudaEventRecord(ev_used_[j], stream_));
+        }
+        std::vector<double> h((size_t)n);
+        B2N_CUDA(cudaMemcpyAsync(h.data(), sloss_.as<double>() + 1, (size_t)n * 8, cudaMemcpyDeviceToHost, stream_));
+        spin_sync(stream_);
+        for (long long i = 0; i < n; ++i) loss_out[c0 + i] = h[(size_t)i] / (double)B;
+    }
+    last_B_ = B;
+    last_Bg_ = B;
 }
 
 inline double Net::forward_backward(const float* x, const int* labels, long long B, long long Bg) {

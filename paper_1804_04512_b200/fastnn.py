@@ -202,6 +202,17 @@ class Network:
     def run_staged(self, steps: int, batch_global: int = 0) -> None:
         _lib.call("b2n_net_run_staged", self._h, steps, batch_global)
 
+    def train_stream(self, x, labels, batch: int) -> np.ndarray:
+        """train_minibatch over consecutive host batches (rows [i*batch, (i+1)*batch) per step),
+        step i+1's host->device copy overlapped with step i; returns every step's loss."""
+        xb = _flat_batch(self, x)
+        lab = np.ascontiguousarray(labels, np.int32)
+        if xb.shape[0] % batch or lab.shape[0] != xb.shape[0]:
+            raise ShapeError("train_stream: x / labels must hold steps * batch rows")
+        out = np.zeros(xb.shape[0] // batch, np.float64)
+        _lib.call("b2n_net_train_stream", self._h, _f(xb), _i(lab), xb.shape[0] // batch, batch, _d(out))
+        return out
+
     def loss(self) -> float:
         out = C.c_double()
         _lib.call("b2n_net_loss", self._h, C.byref(out))

@@ -116,3 +116,29 @@ def test_data_parallel_shards_sum_to_full_batch(gpu):
         acc = g if acc is None else [a + b for a, b in zip(acc, g)]
     for a, b in zip(acc, gfull):
         assert norm_err(a, b) < 1e-5
+
+
+@pytest.mark.parametrize("name", ["mlp", "mnist_cnn"])
+def test_train_stream_matches_train_calls(gpu, name):
+    """Network.train_stream (double-buffered H2D staging overlapped with the steps) runs the same
+    step graph as one train_minibatch call per batch: identical per-step losses and parameters"""
+    import torch
+    from paper_1804_04512_b200 import configs as CF
+    from paper_1804_04512_b200 import fastnn as F
+    S, B = 4, 20
+    spec = CF.NET_CONFIGS[name](B)
+    per = int(np.prod(spec["input"]))
+    x = O.uniform_f32(1, S * B * per).reshape(S * B, per)
+    lab = O.uniform_int(2, 0, 9, S * B)
+    a, b = F.build_network(spec), F.build_network(spec)
+    la = [F.train_minibatch_labels(a, x[i * B:(i + 1) * B], lab[i * B:(i + 1) * B]) for i in range(S)]
+    xp = torch.empty((S * B, per), dtype=torch.float32, pin_memory=True).numpy()
+    lp = torch.empty((S * B,), dtype=torch.int32, pin_memory=True).numpy()
+    xp[:] = x
+    lp[:] = lab
+    lb = b.train_stream(xp, lp, B)
+    assert list(lb) == la
+    for i in range(a.num_params()):
+        np.testing.assert_array_equal(a.get_param(i), b.get_param(i))
+    with pytest.raises(F.LabelError):
+        b.train_stream(xp, np.full(S * B, 10, np.int32), B)
