@@ -216,6 +216,16 @@ std::vector<float> forward_batch(Network& net, const T& x, std::vector<int>* arg
     return probs;
 }
 
+// The reference's training loop -- one train_minibatch per batch -- over `steps` consecutive host
+// batches of packed samples (rows [i*batch, (i+1)*batch) of images / labels), each step's
+// host->device copy overlapped with the previous step. Returns every step's loss.
+inline std::vector<double> train_stream(Network& net, const float* images, const int* labels, std::size_t steps,
+                                        std::size_t batch) {
+    std::vector<double> loss(steps);
+    check(b2n_net_train_stream(net.handle(), images, labels, (long long)steps, (long long)batch, loss.data()));
+    return loss;
+}
+
 // evaluate (network.hpp:474-484) over a dataset of `n` packed samples and int labels, held in
 // device memory for the pass
 inline double evaluate(Network& net, const float* images, const int* labels, std::size_t n) {
@@ -369,6 +379,18 @@ double crbm_cd_update(Crbm& m, const T& v0, float lr, std::mt19937& rng) {
     for (double& d : u) d = std::generate_canonical<double, 53>(rng);
     double recon = 0.0;
     check(b2n_crbm_cd_update(m.handle(), vs.data(), (long long)B, lr, u.data(), (long long)B, &recon));
+    return recon;
+}
+
+// `steps` cd_k_update(rbm, batch_i, 1, lr, rng) calls over consecutive host batches of v0 (rows
+// [i*batch, (i+1)*batch), pitch visible): the Bernoulli draws are taken from `rng` in the
+// reference's order (step by step, row-major), and each step's copies overlap the previous step.
+// Returns every step's reconstruction error.
+inline std::vector<double> cd1_stream(Rbm& rbm, const float* v0, std::size_t steps, std::size_t batch, float lr,
+                                      std::mt19937& rng) {
+    std::vector<double> u(steps * batch * rbm.hidden_units()), recon(steps);
+    for (double& d : u) d = std::generate_canonical<double, 53>(rng);
+    check(b2n_rbm_train_stream(rbm.handle(), v0, u.data(), (long long)steps, (long long)batch, lr, recon.data()));
     return recon;
 }
 
