@@ -235,25 +235,30 @@ class CrbmWork:
     def __init__(self, dist: Dist, precision: int, nccl_id):
         from oracle import oracle as O  # synthetic-input generators (std::mt19937 streams), not the measured path
         from paper_1804_04512_b200 import configs as CF, fastnn as F
-        if dist.world > 1:
-            raise RuntimeError("the convolutional RBM step runs on one GPU (no data-parallel build yet)")
+        from paper_1804_04512_b200.dp import shard_bounds
         c = CF.CRBM
-        self.Bg = self.B = c["batch_size"]
+        self.Bg = c["batch_size"]
+        lo, hi = shard_bounds(self.Bg, dist.world, dist.rank)
+        self.B = hi - lo
         self.lr = c["lr"]
         shp = (c["c_in"], c["h"], c["w"])
         oh, ow = c["h"] - c["kh"] + 1, c["w"] - c["kw"] + 1
-        v0 = O.bernoulli_f32(3, 0.5, self.B * int(np.prod(shp))).reshape((self.B,) + shp)
-        u = O.canonical_f64(5, self.B * c["k"] * oh * ow)
+        v0 = O.bernoulli_f32(3, 0.5, self.Bg * int(np.prod(shp))).reshape((self.Bg,) + shp)[lo:hi]
+        u = O.canonical_f64(5, self.Bg * c["k"] * oh * ow).reshape(self.Bg, -1)[lo:hi]
         self.m = F.Crbm(*shp, c["k"], c["kh"], c["kw"], device=dist.local, precision=precision)
         self.m.init(c["seed"])
+        if dist.world > 1:
+            self.m.dp_init(nccl_id, dist.rank, dist.world)
         self.m.stage(v0, u)
+        self.dist = dist
         self.v0_h = pinned(v0.shape, np.float32)
         self.v0_h[:] = v0
         self.u_h = pinned(u.shape, np.float64)
         self.u_h[:] = u
         self.F = F
         self.config = {"workload": "mnist_crbm_cd1", "model": f"CRBM 1x28x28, {c['k']} kernels 5x5, binary, CD-1",
-                       "global_batch": self.B, "local_batch": self.B, "parallelism": "dp1", "lr": self.lr}
+                       "global_batch": self.Bg, "local_batch": self.B, "parallelism": f"dp{dist.world}",
+                       "lr": self.lr}
         self.h2d = v0.nbytes + u.nbytes
 
     def stream(self):
@@ -263,7 +268,7 @@ class CrbmWork:
         self.m.run_staged(n, self.lr, self.Bg)
 
     def e2e_step(self):
-        return self.F.crbm_cd_update(self.m, self.v0_h, self.lr, self.u_h)
+        return self.F.crbm_cd_update(self.m, self.v0_h, self.lr, self.u_h, self.Bg)
 
     def kernels_per_step(self):
         return _kernels(self.F._lib, "b2n_crbm_kernels_per_step", self.m.handle)

@@ -236,6 +236,10 @@ int b2n_crbm_cd_update(b2n_crbm* crbm, const float* v0_host, long long batch, fl
  * one-launch step keeps them in shared memory unless keep_states was enabled before the step
  * (EPARAM otherwise) */
 int b2n_crbm_keep_states(b2n_crbm* crbm, int on);
+/* data-parallel CRBM (one process per GPU): each rank steps its shard with batch_global = the
+ * global batch; the shards' parameter and reconstruction sums are allreduced (NCCL) before the
+ * identical update on every rank. Needs the one-launch step's shape envelope (EPARAM otherwise). */
+int b2n_crbm_dp_init(b2n_crbm* crbm, const char id[128], int rank, int world);
 int b2n_crbm_last_states(b2n_crbm* crbm, float* h0, float* hs, float* v1, float* h1);
 int b2n_crbm_stage(b2n_crbm* crbm, const float* v0_host, const double* uniforms_host, long long batch);
 int b2n_crbm_run_staged(b2n_crbm* crbm, int steps, float lr, long long batch_global);

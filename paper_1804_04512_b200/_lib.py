@@ -145,6 +145,7 @@ _SIGS = {
     "b2n_crbm_cd_update": ([_VP, _F, C.c_longlong, C.c_float, _D, C.c_longlong, _D], C.c_int),
     "b2n_crbm_last_states": ([_VP, _F, _F, _F, _F], C.c_int),
     "b2n_crbm_keep_states": ([_VP, C.c_int], C.c_int),
+    "b2n_crbm_dp_init": ([_VP, C.c_char_p, C.c_int, C.c_int], C.c_int),
     "b2n_crbm_stage": ([_VP, _F, _D, C.c_longlong], C.c_int),
     "b2n_crbm_run_staged": ([_VP, C.c_int, C.c_float, C.c_longlong], C.c_int),
     "b2n_crbm_recon": ([_VP, _D], C.c_int),

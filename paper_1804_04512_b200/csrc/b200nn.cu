@@ -349,6 +349,9 @@ int b2n_crbm_cd_update(b2n_crbm* m, const float* v0, long long batch, float lr, 
 int b2n_crbm_last_states(b2n_crbm* m, float* h0, float* hs, float* v1, float* h1) {
     return guard([&] { m->impl.last_states(h0, hs, v1, h1); });
 }
+int b2n_crbm_dp_init(b2n_crbm* m, const char id[128], int rank, int world) {
+    return guard([&] { m->impl.dp_init(id, rank, world); });
+}
 int b2n_crbm_keep_states(b2n_crbm* m, int on) {
     return guard([&] { m->impl.keep_states(on != 0); });
 }

@@ -23,6 +23,7 @@
 
 #include "conv.cuh"
 #include "crbm_fused.cuh"
+#include "nccl_dyn.cuh"
 #include "network.cuh"
 
 namespace b2n {
@@ -181,6 +182,11 @@ class Crbm {
             for (long long i = 0; i < B * hp; ++i) h1[i] = -h1[i];  // stored negated for the statistics
     }
     cudaStream_t stream() const { return stream_; }
+    void dp_init(const char id[128], int rank, int world) {
+        dp_ = std::make_unique<DpComm>();
+        dp_->init(id, rank, world);
+        plans_.clear();
+    }
     int kernels_per_step() const { return last_kernels_; }
     // write the chain states of every step (h0, hs, v1, -h1) to HBM for last_states (the fused
     // step otherwise keeps them in shared memory only)
@@ -279,6 +285,12 @@ class Crbm {
         p.stage_floats = (long long)(smem / 4) - round_up(np, 4) - 16;
         p.ws_pitch = (int)round_up(np, 4);
         p.trace = TraceRegistry::get().next();
+        if (dp_) {
+            pl.vf = std::make_shared<DevMem>();  // [G (npart floats) | pad | Gd (double)]
+            pl.vf->alloc((size_t)(round_up(np, 2) * 4 + 64));
+            p.G = pl.vf->as<float>();
+            p.Gd = reinterpret_cast<double*>(p.G + round_up(np, 2));
+        }
         if (pl.keep) {
             p.h0_out = Hc_.as<float>();
             p.h1_out = Hc_.as<float>() + pl.B * hpix();
@@ -290,10 +302,28 @@ class Crbm {
         pl.ops.push_back(Op([=](cudaStream_t st) {
             launch_ex(crbm_cd1_fused_kernel<KW>, dim3(grid), dim3(kCfThreads), smem, st, 1u, p);
         }, "crbm.cd1_fused", fl, by));
+        if (dp_) {  // one exchange step: the shards' parameter sums and recon sums, then the update
+            DpComm* dp = dp_.get();
+            float* G = p.G;
+            double* Gd = p.Gd;
+            float* P = p.P;
+            double* rc = p.recon;
+            const int n = (int)np;
+            const float scale = p.scale;
+            const double inv_bg = p.inv_bg;
+            pl.ops.push_back(Op([=](cudaStream_t st) {
+                dp->allreduce_f32(G, (size_t)n, st);
+                dp->allreduce_f64(Gd, 1, st);
+                launch_ex(crbm_dp_apply_kernel, dim3((n + 255) / 256), dim3(256), 0, st, 1u, P, (const float*)G, n, scale,
+                          (const double*)Gd, rc, inv_bg);
+            }, "allreduce+update", 0.0, 12.0 * np));
+        }
         pl.fused = true;
     }
 
     void build(Plan& pl) {
+        if (dp_ && !fused_ok())
+            throw Error(B2N_EPARAM, "data-parallel CRBM steps need the one-launch kernel's shape envelope");
         if (fused_ok()) {
             switch (g_.kw) {
                 case 1: build_fused_kw<1>(pl); break;
@@ -305,7 +335,7 @@ class Crbm {
                 case 7: build_fused_kw<7>(pl); break;
                 default: build_fused_kw<8>(pl); break;
             }
-            last_kernels_ = 1;
+            last_kernels_ = dp_ ? 2 : 1;
             return;
         }
         last_kernels_ = 5;
@@ -442,6 +472,7 @@ class Crbm {
     DevMem P_, Vc_, Hc_, HS_, U_, recon_;
     HostPinned h_recon_;
     std::vector<std::unique_ptr<Plan>> plans_;
+    std::unique_ptr<DpComm> dp_;
 };
 
 }  // namespace b2n

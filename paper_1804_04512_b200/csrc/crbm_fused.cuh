@@ -47,6 +47,10 @@ struct CrbmFusedParams {
     // chain states of every image (for last_states / tests); null unless keep_states
     float *h0_out, *hs_out, *v1_out, *h1_out;
     unsigned long long* trace;  // bring-up timeline (B2N_TRACE=1, %globaltimer ns), null in production
+    // data-parallel mode (non-null): the last CTA stores this shard's raw parameter sums and recon
+    // sum here instead of updating P; crbm_dp_apply_kernel applies them after the allreduce
+    float* G;
+    double* Gd;
 };
 #define B2N_CF_TRACE(slot)                                                                \
     do {                                                                                  \
@@ -420,13 +424,15 @@ __global__ void __launch_bounds__(kCfThreads, 1) crbm_cd1_fused_kernel(const Crb
         for (int i = tid; i < p.npart; i += kCfThreads) {
             float s = 0.0f;
             for (int img = 0; img < p.B; ++img) s += st[(long long)img * p.ws_pitch + i];
-            p.P[i] = sP[i] + p.scale * s;
+            if (p.G) p.G[i] = s;
+            else p.P[i] = sP[i] + p.scale * s;
         }
     } else {
         for (int i = tid; i < p.npart; i += kCfThreads) {
             float s = 0.0f;
             for (int img = 0; img < p.B; ++img) s += __ldcg(p.ws + (long long)img * p.ws_pitch + i);
-            p.P[i] = sP[i] + p.scale * s;
+            if (p.G) p.G[i] = s;
+            else p.P[i] = sP[i] + p.scale * s;
         }
     }
     if (tid < 32) {  // recon: lane-strided image sums + a fixed butterfly
@@ -435,12 +441,22 @@ __global__ void __launch_bounds__(kCfThreads, 1) crbm_cd1_fused_kernel(const Crb
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
         if (tid == 0) {
-            *p.recon = r * p.inv_bg;
+            if (p.Gd) *p.Gd = r;
+            else *p.recon = r * p.inv_bg;
             *p.ticket = 0u;
         }
     }
     __syncthreads();
     B2N_CF_TRACE(9);
+}
+
+// data-parallel CRBM step: P += lr / B_global * (allreduced parameter sums), recon = sum / B_global
+static __global__ void crbm_dp_apply_kernel(float* __restrict__ P, const float* __restrict__ G, int n, float scale,
+                                            const double* __restrict__ Gd, double* recon, double inv_bg) {
+    pdl_wait();
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) P[i] += scale * G[i];
+    if (i == 0) *recon = *Gd * inv_bg;
 }
 
 }  // namespace b2n

@@ -496,6 +496,9 @@ class Crbm:
         _lib.call("b2n_crbm_kernels_per_step", self._h, C.byref(n))
         return n.value
 
+    def dp_init(self, nccl_id: bytes, rank: int, world: int) -> None:
+        _lib.call("b2n_crbm_dp_init", self._h, nccl_id, rank, world)
+
     def keep_states(self, on: bool = True) -> None:
         """write every step's chain states to HBM so last_states() can read them back"""
         _lib.call("b2n_crbm_keep_states", self._h, int(on))

@@ -50,3 +50,23 @@ def test_nccl_rbm_matches_single(gpu):
     # same math, different (deterministic) summation orders -> agreement at the 3xTF32 level
     assert norm_err(wb, wa) < 1e-5 and norm_err(bvb, bva) < 1e-5 and norm_err(bhb, bha) < 1e-5
     assert abs(a.recon() - b.recon()) < 1e-6 * a.recon()
+
+
+def test_nccl_crbm_matches_single(gpu):
+    """the data-parallel CRBM step (shard sums -> ncclAllReduce -> update) on a 1-rank communicator
+    equals the single-GPU one-launch step"""
+    from paper_1804_04512_b200 import fastnn as F
+    c, h, w, k, kh, kw, B = 1, 28, 28, 12, 5, 5, 40
+    v0 = O.bernoulli_f32(3, 0.5, B * c * h * w).reshape(B, c, h, w)
+    u = O.canonical_f64(5, B * k * 24 * 24)
+    a, b = F.Crbm(c, h, w, k, kh, kw), F.Crbm(c, h, w, k, kh, kw)
+    a.init(42)
+    b.init(42)
+    b.dp_init(F.nccl_unique_id(), 0, 1)
+    for _ in range(2):
+        ra = F.crbm_cd_update(a, v0, 0.1, u)
+        rb = F.crbm_cd_update(b, v0, 0.1, u, batch_global=B)
+        assert abs(ra - rb) <= 1e-9 * ra
+    assert b.kernels_per_step() == 2
+    for x, y in zip(a.get(), b.get()):
+        assert norm_err(y, x) < 1e-6
