@@ -19,7 +19,12 @@ from make_golden import CRBM_CASES  # noqa: E402
 pytestmark = pytest.mark.gpu
 
 SHAPES = CRBM_CASES + [(1, 28, 28, 12, 5, 5, 100), (3, 32, 32, 8, 5, 5, 16), (16, 12, 12, 16, 3, 3, 10),
-                       (1, 28, 28, 32, 3, 3, 7), (2, 5, 40, 3, 1, 7, 5)]
+                       (1, 28, 28, 32, 3, 3, 7), (2, 5, 40, 3, 1, 7, 5),
+                       # more images than co-resident CTAs (a CTA loops over images; the last CTA's
+                       # partial rows no longer fit its shared memory: the global-load reduction)
+                       (1, 28, 28, 12, 5, 5, 400),
+                       # widest register strip template (kw = 8) and a 1-wide kernel on a tall map
+                       (2, 20, 23, 4, 3, 8, 6), (1, 30, 9, 5, 4, 1, 3)]
 
 
 def _step(c, h, w, k, kh, kw, B, lr=0.1, seed=0):
