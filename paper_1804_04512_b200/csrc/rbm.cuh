@@ -249,6 +249,11 @@ class Rbm {
         }
         if (!copy_stream_) B2N_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
         if (rstream_.bytes < (size_t)steps * 8) rstream_.alloc((size_t)steps * 8);
+        // readiness flags: the copy stream stamps step i + 1 into flag j after step i's copies (a
+        // stream memory write, fenced after them); the step kernel polls it, so the compute stream
+        // carries no cross-stream event and consecutive steps keep their programmatic overlap
+        if (!sready_.p) sready_.alloc(64);
+        B2N_CUDA(cudaMemsetAsync(sready_.p, 0, 64, stream_));
         B2N_CUDA(cudaEventRecord(ev_used_[0], stream_));  // staging buffers free after prior work
         B2N_CUDA(cudaEventRecord(ev_used_[1], stream_));
         for (long long i = 0; i < steps; ++i) {
@@ -258,12 +263,14 @@ class Rbm {
                                      copy_stream_));
             B2N_CUDA(cudaMemcpyAsync(su_[j].p, u + i * B * H_, (size_t)(B * H_ * 8), cudaMemcpyHostToDevice,
                                      copy_stream_));
-            B2N_CUDA(cudaEventRecord(ev_copied_[j], copy_stream_));
-            B2N_CUDA(cudaStreamWaitEvent(stream_, ev_copied_[j], 0));
+            unsigned* flag = sready_.as<unsigned>() + j;
+            stream_write_u32(copy_stream_, flag, (unsigned)(i + 1));
             RbmFusedParams rp = pl.rp;
             rp.v0_src = sv_[j].as<float>();
             rp.ld_src = V_;
             rp.u_src = su_[j].as<double>();
+            rp.ready = flag;
+            rp.ready_val = (unsigned)(i + 1);
             rp.recon_out = rstream_.as<double>() + i;
             launch_ex(rbm_cd1_fused_kernel, dim3(kRfSlices, rp.jt), dim3(kRfThreads), (size_t)kRfSmem, stream_, 1u,
                       pl.maps[0], pl.maps[1], pl.maps[2], pl.maps[3], pl.maps[4], pl.maps[5], rp);
@@ -594,6 +601,7 @@ class Rbm {
     DevMem racc_;              // train_epoch: device sum of per-step reconstruction errors
     DevMem sv_[2], su_[2];     // train_stream: double-buffered device staging of v0 / uniforms
     DevMem rstream_;           // train_stream: per-step reconstruction errors
+    DevMem sready_;            // train_stream: staging readiness flags (step index + 1 per buffer)
     cudaEvent_t ev_copied_[2] = {nullptr, nullptr}, ev_used_[2] = {nullptr, nullptr};
     cudaStream_t copy_stream_ = nullptr;
   public:

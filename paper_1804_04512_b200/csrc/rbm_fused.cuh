@@ -54,6 +54,10 @@ struct RbmFusedParams {
     const float* v0_src;
     long long ld_src;
     const double* u_src;
+    // train_stream: the staging buffer holding v0_src / u_src is complete once *ready >= ready_val
+    // (written by the copy stream after its copies); null otherwise
+    const unsigned* ready;
+    unsigned ready_val;
 };
 
 __device__ __forceinline__ unsigned* sbar_of(const RbmFusedParams& p, int s) { return p.gbar + 2 * s; }
@@ -211,6 +215,19 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
         p.trace[128 + blockIdx.y * gridDim.x + blockIdx.x] = t;
     }
+    if (p.ready) {  // train_stream: wait for this step's staging copies (no cross-stream event)
+        if (threadIdx.x == 0) {
+            unsigned long long spins = 0;
+            unsigned v;
+            for (;;) {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.ready) : "memory");
+                if (v >= p.ready_val) break;
+                __nanosleep(64);
+                if (++spins > (1ull << 26)) __trap();  // watchdog: a launch error instead of a hung GPU
+            }
+        }
+        __syncthreads();
+    }
     if (p.v0_src) {
         // zero-copy v0: CTA (s, j) moves rows [16 j, 16 j + 16) of visible slice s into Vcat; the 8 CTAs
         // of slice s then meet at the slice barrier before phase 1 reads the slice by TMA
@@ -220,7 +237,7 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
             const int r = 16 * j + idx / w4, c = vlo + (idx % w4) * 4;
             if (r < B)
                 *reinterpret_cast<float4*>(p.Vcat + (long long)r * p.ldv + c) =
-                    *reinterpret_cast<const float4*>(p.v0_src + (long long)r * p.ld_src + c);
+                    __ldcg(reinterpret_cast<const float4*>(p.v0_src + (long long)r * p.ld_src + c));
         }
         rf_grid_sync(sbar_of(p, s), gridDim.y);
     }
@@ -233,7 +250,7 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
         if (r < B)
 #pragma unroll
             for (int i = 0; i < 4; ++i)
-                if (h0c + c + i < H) upre[i] = usrc[(long long)r * H + h0c + c + i];
+                if (h0c + c + i < H) upre[i] = __ldcg(usrc + (long long)r * H + h0c + c + i);
     }
     const uint32_t id_h = umma_idesc_tf32(128, kRfTileH, 0, 0);   // [batch x hidden], both K-major
     const uint32_t id_v = umma_idesc_tf32(128, kRfSliceW, 0, 1);  // [batch x visible], W MN-major

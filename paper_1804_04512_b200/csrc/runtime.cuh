@@ -68,6 +68,21 @@ inline EncodeTiledFn encode_fn() {
     return fn;
 }
 
+// cuStreamWriteValue32: a stream-ordered 32-bit store, fenced after the stream's earlier work
+// (copies included), for device-side readiness flags
+inline void stream_write_u32(cudaStream_t st, unsigned* addr, unsigned v) {
+    typedef CUresult (*WriteFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+    static WriteFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        B2N_CUDA(cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) throw Error(B2N_ECUDA, "cuStreamWriteValue32 unavailable");
+        return reinterpret_cast<WriteFn>(p);
+    }();
+    const CUresult r = fn(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(addr), v, 0);
+    if (r != CUDA_SUCCESS) throw Error(B2N_ECUDA, "cuStreamWriteValue32 failed (" + std::to_string((int)r) + ")");
+}
+
 // 2-D fp32 map over a row-major matrix of `outer` rows x `inner` logical columns with row pitch
 // `ld` elements; 128 B-swizzled boxes of box_inner (32) x box_outer (16 B atoms for K-major operands,
 // 32 B atoms for MN-major ones); out-of-bounds reads fill zero.
