@@ -142,3 +142,21 @@ def test_train_stream_matches_train_calls(gpu, name):
         np.testing.assert_array_equal(a.get_param(i), b.get_param(i))
     with pytest.raises(F.LabelError):
         b.train_stream(xp, np.full(S * B, 10, np.int32), B)
+
+
+def test_train_stream_adam_and_single_step(gpu):
+    """train_stream on the split step (Adam: packed optimizer kernel, device step counter) and with
+    one step: same losses / parameters as per-batch calls"""
+    import torch
+    from paper_1804_04512_b200 import configs as CF
+    from paper_1804_04512_b200 import fastnn as F
+    S, B = 3, 16
+    spec = dict(CF.NET_CONFIGS["mlp"](B), optimizer=3, lr=0.001)
+    x = O.uniform_f32(4, S * B * 784).reshape(S * B, 784)
+    lab = O.uniform_int(5, 0, 9, S * B)
+    a, b, c = F.build_network(spec), F.build_network(spec), F.build_network(spec)
+    la = [F.train_minibatch_labels(a, x[i * B:(i + 1) * B], lab[i * B:(i + 1) * B]) for i in range(S)]
+    assert list(b.train_stream(x, lab, B)) == la
+    for i in range(a.num_params()):
+        np.testing.assert_array_equal(a.get_param(i), b.get_param(i))
+    assert list(c.train_stream(x[:B], lab[:B], B)) == la[:1]
