@@ -66,7 +66,6 @@ class Rbm {
         for (cudaEvent_t e : uev_)
             if (e) cudaEventDestroy(e);
         for (int j = 0; j < 2; ++j) {
-            if (ev_copied_[j]) cudaEventDestroy(ev_copied_[j]);
             if (ev_used_[j]) cudaEventDestroy(ev_used_[j]);
         }
         if (copy_stream_) cudaStreamDestroy(copy_stream_);
@@ -244,7 +243,6 @@ class Rbm {
         for (int j = 0; j < 2; ++j) {
             if (sv_[j].bytes < (size_t)(B * V_ * 4)) sv_[j].alloc((size_t)(B * V_ * 4));
             if (su_[j].bytes < (size_t)(B * H_ * 8)) su_[j].alloc((size_t)(B * H_ * 8));
-            if (!ev_copied_[j]) B2N_CUDA(cudaEventCreateWithFlags(&ev_copied_[j], cudaEventDisableTiming));
             if (!ev_used_[j]) B2N_CUDA(cudaEventCreateWithFlags(&ev_used_[j], cudaEventDisableTiming));
         }
         if (!copy_stream_) B2N_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
@@ -602,7 +600,7 @@ class Rbm {
     DevMem sv_[2], su_[2];     // train_stream: double-buffered device staging of v0 / uniforms
     DevMem rstream_;           // train_stream: per-step reconstruction errors
     DevMem sready_;            // train_stream: staging readiness flags (step index + 1 per buffer)
-    cudaEvent_t ev_copied_[2] = {nullptr, nullptr}, ev_used_[2] = {nullptr, nullptr};
+    cudaEvent_t ev_used_[2] = {nullptr, nullptr};
     cudaStream_t copy_stream_ = nullptr;
   public:
     void read_trace(unsigned long long* h) {
