@@ -291,17 +291,18 @@ __device__ __forceinline__ float4 ld_dsmem4(uint32_t addr) {
 
 // softmax (layers.hpp:301-320) + softmax_cross_entropy (network.hpp:410-437) of one full row held
 // in the smem tile; sequential in j like the reference.
-__device__ __forceinline__ void softmax_row(const GemmParams& p, const float* trow, int m) {
+__device__ __forceinline__ void softmax_row(const GemmParams& p, const float* trow, int m, const float* sbias) {
     const EpiParams& e = p.ep;
     float mx = -INFINITY;
-    for (int n = 0; n < p.N; ++n) mx = fmaxf(mx, trow[n] + e.bias[(long long)n * e.bias_stride]);
+    auto bias = [&](int n) { return sbias ? sbias[n] : e.bias[(long long)n * e.bias_stride]; };
+    for (int n = 0; n < p.N; ++n) mx = fmaxf(mx, trow[n] + bias(n));
     float sum = 0.0f;
-    for (int n = 0; n < p.N; ++n) sum += expf((trow[n] + e.bias[(long long)n * e.bias_stride]) - mx);
+    for (int n = 0; n < p.N; ++n) sum += expf((trow[n] + bias(n)) - mx);
     const int label = e.labels[m];
     int best = 0;
     float bestp = -1.0f, ptrue = 0.0f;
     for (int n = 0; n < p.N; ++n) {
-        const float q = expf((trow[n] + e.bias[(long long)n * e.bias_stride]) - mx) / sum;
+        const float q = expf((trow[n] + bias(n)) - mx) / sum;
         if (q > bestp) {  // strict >: first maximum wins (network.hpp:69-70)
             bestp = q;
             best = n;
@@ -553,6 +554,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ccol = (threadIdx.x % G) * 4;
     float bias4[4] = {0.f, 0.f, 0.f, 0.f};
     EpiIn pre[kEpiPrefetch];
+    // softmax: the bias row (one strided column of W_aug) staged in the drained operand stages
+    // behind the tile with independent loads now, instead of a serial global load per class later
+    constexpr bool kStageBias = Cfg::MAIN_BYTES >= Cfg::TILE_BYTES + 256 * 4;
+    float* sbias = kStageBias ? tile + kBM * TP : nullptr;
+    if constexpr (EPI == EPI_SOFTMAX_XENT && kStageBias) {
+        for (int i = threadIdx.x; i < p.N; i += kThreads) sbias[i] = p.ep.bias[(long long)i * p.ep.bias_stride];
+        if (p.splits <= 1) __syncthreads();  // (split-K: the cluster barriers below order it)
+    }
     if constexpr (EPI != EPI_SOFTMAX_XENT) {
         epi_bias<EPI>(p, n0 + ccol, bias4);
 #pragma unroll
@@ -593,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) B2N_TRACE(59);
     if constexpr (EPI == EPI_SOFTMAX_XENT) {
         for (int r = r_lo + threadIdx.x; r < r_hi; r += kThreads)
-            if (m0 + r < p.M) softmax_row(p, tile + r * TP, m0 + r);
+            if (m0 + r < p.M) softmax_row(p, tile + r * TP, m0 + r, sbias);
     } else {
         auto body = [&](int it, const EpiIn& in) {
             const int idx = it * kThreads + threadIdx.x;
