@@ -430,6 +430,56 @@ def time_steps(work, steps, warmup, dist, flush, e2e=False):
     return dist.max(total_ms)
 
 
+def host_info() -> dict:
+    """lscpu-style host description for the CPU baseline (model name, logical CPUs)."""
+    model = None
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    import platform
+    return {"cpu_model": model or platform.processor() or platform.machine(), "logical_cpus": os.cpu_count()}
+
+
+_TF32 = {}
+
+
+def measure_tf32_peak(dev: int) -> dict:
+    """the TF32 tensor peak measured on this box (not assumed bf16/2): cuBLAS fp32 GEMM
+    with TF32 math, 8192^3, best of 5 after warm-up (a measurement of the hardware, outside every
+    timed region). 3xTF32 issues three TF32 products per fp32 product, so its peak is /3."""
+    if dev in _TF32:
+        return _TF32[dev]
+    import torch
+    n = 8192
+    prev = torch.backends.cuda.matmul.allow_tf32
+    try:
+        torch.backends.cuda.matmul.allow_tf32 = True
+        a = torch.randn(n, n, device=f"cuda:{dev}")
+        b = torch.randn(n, n, device=f"cuda:{dev}")
+        c = a @ b
+        torch.cuda.synchronize()
+        best = float("inf")
+        for _ in range(5):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b, out=c)
+            e1.record()
+            torch.cuda.synchronize()
+            best = min(best, e0.elapsed_time(e1))
+        tf = 2.0 * n ** 3 / (best * 1e-3) / 1e12
+        del a, b, c
+        torch.cuda.empty_cache()
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    _TF32[dev] = {"tf32_tflops": round(tf, 1), "tf32x3_tflops": round(tf / 3.0, 1),
+                  "how": "cuBLAS fp32 GEMM with TF32 math, 8192^3, best of 5 (CUDA events)"}
+    return _TF32[dev]
+
+
 def peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -438,11 +488,16 @@ def peaks():
     return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
 
 
-def roofline(prof, precision):
+def roofline(prof, precision, tf32_meas=None):
     hbm, bf16, src = peaks()
     top = max(prof, key=lambda o: o["ms"])
-    # tensor peak for the arithmetic in use: tf32 is half the bf16 rate; 3xTF32 issues 3 MMAs
-    tf32 = bf16 / 2.0 / (3.0 if precision == "tf32x3" else 1.0)
+    # tensor peak for the arithmetic in use: the measured TF32 rate (3xTF32 issues 3 products)
+    if tf32_meas:
+        tf32 = tf32_meas["tf32x3_tflops" if precision == "tf32x3" else "tf32_tflops"]
+        tsrc = "measured " + tf32_meas["how"] + (" / 3 (3xTF32)" if precision == "tf32x3" else "")
+    else:
+        tf32 = bf16 / 2.0 / (3.0 if precision == "tf32x3" else 1.0)
+        tsrc = src + f" (bf16 {bf16} TF/s -> tf32 /2" + (", 3xTF32 /3)" if precision == "tf32x3" else ")")
     ridge = tf32 * 1e12 / (hbm * 1e9)
     ai = top["flops"] / top["bytes"] if top["bytes"] else float("inf")
     sec = top["ms"] * 1e-3
@@ -458,19 +513,39 @@ def roofline(prof, precision):
         return {"bound": "hbm", "kernel": top["name"], "achieved": round(ach, 2), "peak": hbm, "unit": "GB/s",
                 "frac": round(ach / hbm, 5), "traffic": traffic, "algorithmic_bytes": top["bytes"],
                 "flops": top["flops"], "avg_launch_us": round(top["ms"] * 1e3, 3), "peak_source": src,
-                "share_of_step": None}
+                "tensor_peak_tflops": round(tf32, 1), "share_of_step": None}
     ach = top["flops"] / sec / 1e12
     return {"bound": "tensor", "kernel": top["name"], "achieved": round(ach, 3), "peak": round(tf32, 1),
             "unit": "TFLOP/s", "frac": round(ach / tf32, 5), "traffic": traffic, "algorithmic_bytes": top["bytes"],
             "flops": top["flops"], "avg_launch_us": round(top["ms"] * 1e3, 3),
-            "peak_source": src + f" (bf16 {bf16} TF/s -> tf32 /2" + (", 3xTF32 /3)" if precision == "tf32x3" else ")"),
-            "share_of_step": None}
+            "peak_source": tsrc, "share_of_step": None}
+
+
+def step_roofline(work, prof, precision, tf32, step_ms):
+    """The dominant kernel's roofline (algorithmic bytes or FLOPs per launch / its event-timed launch
+    duration) plus the whole step's: the planner's algorithmic bytes of every op / the step time,
+    against the measured HBM peak, and the launch floor (dependent kernels x the measured 4.2 us
+    single-kernel graph-launch latency, tools/launch_probe.cu)."""
+    rl = roofline(prof, precision, tf32)
+    prof_step = sum(o["ms"] for o in prof)
+    rl["share_of_step"] = round(max(o["ms"] for o in prof) / prof_step, 4) if prof_step else None
+    hbm = peaks()[0]
+    step_bytes = sum(o["bytes"] for o in prof)
+    rl["step_algorithmic_bytes"] = step_bytes
+    rl["step_hbm_frac"] = round(step_bytes / (step_ms * 1e-3) / 1e9 / hbm, 5)
+    rl["launch_floor_us"] = round(work.kernels_per_step() * 4.2, 2)
+    rl["step_us"] = round(step_ms * 1e3, 2)
+    return rl
 
 
 # ----------------------------------------------------------------------------- CPU reference
-def cpu_reference(name: str, budget_s: float, min_steps: int = 2, max_steps: int | None = None):
+def cpu_reference(name: str, budget_s: float, min_steps: int = 2, max_steps: int | None = None,
+                  warmup_s: float = 0.0, warmup_min: int = 1, exact_steps: int | None = None):
     """Time the reference's own step on this host: oracle/_ref when built (kind 'reference'),
-    else the oracle restatement (kind 'port'). Returns (samples/s, info dict)."""
+    else the oracle restatement (kind 'port'). Warm-up: at least `warmup_min` steps and `warmup_s`
+    seconds (thread pool, page faults, caches at steady state). Then either exactly `exact_steps`
+    timed steps, or steps until `budget_s` seconds (>= min_steps, <= max_steps).
+    Returns (samples/s, info dict)."""
     import ctypes as C
     from oracle import oracle as O
     from paper_1804_04512_b200 import configs as CF
@@ -532,17 +607,23 @@ def cpu_reference(name: str, budget_s: float, min_steps: int = 2, max_steps: int
             step = lambda: net.train_minibatch(x, lab)  # noqa: E731
             done = lambda: None  # noqa: E731
             what = "oracle train_minibatch"
-    step()  # warm-up (thread pool, page faults)
+    nw, t0 = 0, time.perf_counter()
+    while nw < warmup_min or time.perf_counter() - t0 < warmup_s:
+        step()
+        nw += 1
     n, t0 = 0, time.perf_counter()
     while True:
         step()
         n += 1
         el = time.perf_counter() - t0
-        if (el >= budget_s and n >= min_steps) or (max_steps and n >= max_steps):
+        if exact_steps is not None:
+            if n >= exact_steps:
+                break
+        elif (el >= budget_s and n >= min_steps) or (max_steps and n >= max_steps):
             break
     done()
-    return B * n / el, {"kind": kind, "cores": cores, "steps": n, "seconds": round(el, 3),
-                        "sample": f"{n} x {what}, global batch {B}, {cores} host threads"}
+    return B * n / el, {"kind": kind, "cores": cores, "steps": n, "seconds": round(el, 3), "warmup_steps": nw,
+                        "sample": f"{n} x {what}, global batch {B}, {cores} host threads, after {nw} warm-up steps"}
 
 
 # ----------------------------------------------------------------------------- main
@@ -581,16 +662,16 @@ def main():
         if dist.rank != 0:
             return
         name = a.config
-        import platform
-        t_per = []
-        v, info = cpu_reference(name, budget_s=max(a.cpu_budget, 1.0), min_steps=max(a.steps // 20, 2),
-                                max_steps=a.steps)
+        # steady state: >= max(W, 1) warm-up steps and >= 1.5 s of them, then exactly K timed steps
+        v, info = cpu_reference(name, budget_s=0.0, warmup_s=1.5 if name != "imagenet_cnn" else 0.0,
+                                warmup_min=max(a.warmup, 1) if name != "imagenet_cnn" else 1, exact_steps=a.steps)
         line = {"metric": "train samples/s", "value": round(v, 3), "unit": "samples/s", "n_gpus": a.gpus,
-                "steps": info["steps"], "warmup": 1, "ms_per_step": round(info["seconds"] * 1e3 / info["steps"], 3),
+                "steps": info["steps"], "warmup": info["warmup_steps"],
+                "ms_per_step": round(info["seconds"] * 1e3 / info["steps"], 3),
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic", "impl": "reference",
-                "config": {"workload": {"rbm": "mnist_rbm_cd1", "crbm": "mnist_crbm_cd1"}.get(name, name), "global_batch": 100 if name != "imagenet_cnn" else 128,
-                           "host": platform.processor() or platform.machine()},
+                "config": {"workload": {"rbm": "mnist_rbm_cd1", "crbm": "mnist_crbm_cd1"}.get(name, name),
+                           "global_batch": 100 if name != "imagenet_cnn" else 128, "host": host_info()},
                 "cpu_baseline": {"value": round(v, 3), "unit": "samples/s", "cores": info["cores"],
                                  "kind": info["kind"], "sample": info["sample"]},
                 "e2e": {"value": round(v, 3), "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -630,14 +711,8 @@ def main():
     step_ms = total_ms / a.steps
     value = work.Bg * a.steps / (total_ms * 1e-3)
     e2e_val = work.Bg * a.steps / (e2e_ms * 1e-3)
-    rl = roofline(prof, a.precision)
-    prof_step = sum(o["ms"] for o in prof)
-    rl["share_of_step"] = round(max(o["ms"] for o in prof) / prof_step, 4) if prof_step else None
-    # the B=100 steps sit far below the HBM roofline, so the step is also set against a
-    # launch floor: dependent kernels x the measured single-kernel graph-launch latency
-    # (tools/launch_probe.cu: 4.2 us on this pool's B200s)
-    rl["launch_floor_us"] = round(work.kernels_per_step() * 4.2, 2)
-    rl["step_us"] = round(step_ms * 1e3, 2)
+    tf32 = measure_tf32_peak(dev)
+    rl = step_roofline(work, prof, a.precision, tf32, step_ms)
     line = {"metric": "train samples/s", "value": round(value, 2), "unit": "samples/s", "n_gpus": dist.world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(step_ms, 5), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": getattr(work, "dtype", None) or (
@@ -654,6 +729,7 @@ def main():
             "gpu_launches": work.kernels_per_step() * a.steps,
             "kernels_per_step": work.kernels_per_step(),
             "roofline": rl,
+            "tensor_peaks": tf32,
             "step_profile": [{k: (round(v, 5) if isinstance(v, float) else v) for k, v in o.items()} for o in prof],
             "clocks": clk.summary()}
     if not a.no_others:
@@ -668,12 +744,16 @@ def main():
                 e2 = w.e2e_total(max(n // 2, 5), 2) if hasattr(w, "e2e_total") else None
                 if e2 is None:
                     e2 = time_steps(w, max(n // 2, 5), 2, dist, flush, e2e=True)
+                wprof = w.profile(10 if name == "imagenet_cnn" else 30)
                 others[name] = {"value": round(w.Bg * n / (ms * 1e-3), 2), "unit": "samples/s",
                                 "ms_per_step": round(ms / n, 5),
                                 "e2e": round(w.Bg * max(n // 2, 5) / (e2 * 1e-3), 2),
-                                "kernels_per_step": w.kernels_per_step()}
-                if name == "crbm" and dist.rank == 0:  # a widening row: its CPU reference beside it
-                    cv, ci = cpu_reference("crbm", 3.0)
+                                "kernels_per_step": w.kernels_per_step(),
+                                "roofline": step_roofline(w, wprof, a.precision, tf32, ms / n)}
+                if dist.rank == 0 and dist.world == 1:  # the reference's own step beside every config
+                    big = name == "imagenet_cnn"
+                    cv, ci = cpu_reference(name, 0.0 if big else 3.0, min_steps=1 if big else 2,
+                                           warmup_s=0.0 if big else 0.5)
                     others[name]["cpu_baseline"] = {"value": round(cv, 2), "unit": "samples/s",
                                                     "cores": ci["cores"], "kind": ci["kind"], "sample": ci["sample"]}
                 del w
@@ -683,9 +763,9 @@ def main():
     if dist.world == 1 and not a.no_others:
         line["fit_epoch"] = fit_epochs(dev, precision)
     if dist.rank == 0 and dist.world == 1:
-        v, info = cpu_reference(a.config, a.cpu_budget)
+        v, info = cpu_reference(a.config, a.cpu_budget, warmup_s=1.5)
         line["cpu_baseline"] = {"value": round(v, 2), "unit": "samples/s", "cores": info["cores"],
-                                "kind": info["kind"], "sample": info["sample"]}
+                                "kind": info["kind"], "sample": info["sample"], "host": host_info()}
     if dist.rank == 0:
         print(json.dumps(line), flush=True)
     if dist.pg:

@@ -683,56 +683,76 @@ void orc_sgd_momentum_step(float* p, float* v, const float* g, long long n, floa
 // h_s = (u < (double)sigmoid(a)) is exactly bernoulli_distribution(p)(mt19937) when u is the
 // generate_canonical<double,53> stream (random.h:3741-3749). Shard form: statistics over the local
 // rows, scaled by lr / B_global. If d* outputs are given, the deltas are written instead of applied.
-double orc_rbm_cd1(long long H, long long V, float* W, float* bv, float* bh, const float* v0, long long B,
-                   long long B_global, float lr, const double* u, float* h0_out, float* hs_out, float* v1_out,
-                   float* h1_out, float* dW, float* dbh, float* dbv) {
+// cd_k_update (energy.hpp:131-171) for binary units with the Bernoulli draws supplied: u holds
+// k * B * H generate_canonical<double,53> values in the order the reference consumes them (the hs of
+// Gibbs step s is drawn from u[s * B * H ...], row-major, unit_sample_inplace energy.hpp:53-71).
+// hs_out receives the LAST sampled hidden state, v1_out the step-1 visible means (recon), h1_out the
+// negative hidden means hk, vk_out (optional) the final visible means vk.
+double orc_rbm_cdk(long long H, long long V, float* W, float* bv, float* bh, const float* v0, long long B,
+                   long long B_global, int k, float lr, const double* u, float* h0_out, float* hs_out, float* v1_out,
+                   float* h1_out, float* vk_out, float* dW, float* dbh, float* dbv) {
     const size_t h = (size_t)H, vis = (size_t)V, b = (size_t)B;
-    std::vector<float> h0(b * h), hs(b * h), v1(b * vis), h1(b * h);
-    // rbm_hidden_given_visible (energy.hpp:101-110): NT gemm, row bias, unit rule
-    gemm_nt(v0, vis, W, vis, h0.data(), h, b, h, vis);
-    for (size_t r = 0; r < b; ++r)
-        for (size_t j = 0; j < h; ++j) {
-            const float a = h0[r * h + j] + bh[j];
-            const float p = sigmoidf_ref(a);
-            h0[r * h + j] = p;
-            hs[r * h + j] = (u[r * h + j] < (double)p) ? 1.0f : 0.0f;
+    std::vector<float> h0(b * h), hs(b * h), vk(b * vis), v1(b * vis), hk(b * h);
+    // rbm_hidden_given_visible (energy.hpp:101-110): NT gemm, row bias, unit rule (mean or sample)
+    auto hidden = [&](const float* vin, float* out, const double* uu) {
+        gemm_nt(vin, vis, W, vis, out, h, b, h, vis);
+        for (size_t r = 0; r < b; ++r)
+            for (size_t j = 0; j < h; ++j) {
+                const float p = sigmoidf_ref(out[r * h + j] + bh[j]);
+                out[r * h + j] = uu ? ((uu[r * h + j] < (double)p) ? 1.0f : 0.0f) : p;
+            }
+    };
+    hidden(v0, h0.data(), nullptr);
+    hidden(v0, hs.data(), u);  // the reference recomputes the same product for the sample (energy.hpp:137-138)
+    double recon = 0.0;
+    for (int step = 1; step <= k; ++step) {
+        // rbm_visible_given_hidden (energy.hpp:112-120): NN gemm
+        std::fill(vk.begin(), vk.end(), 0.0f);
+        gemm_axpy(false, hs.data(), h, W, vis, vk.data(), vis, b, vis, h);
+        for (size_t r = 0; r < b; ++r)
+            for (size_t j = 0; j < vis; ++j) vk[r * vis + j] = sigmoidf_ref(vk[r * vis + j] + bv[j]);
+        if (step == 1) {  // sq_diff_per_row energy.hpp:84-96
+            for (size_t i = 0; i < b * vis; ++i) {
+                const double d = double(v0[i]) - double(vk[i]);
+                recon += d * d;
+            }
+            v1 = vk;
         }
-    // rbm_visible_given_hidden (energy.hpp:112-120): NN gemm
-    gemm_axpy(false, hs.data(), h, W, vis, v1.data(), vis, b, vis, h);
-    for (size_t r = 0; r < b; ++r)
-        for (size_t j = 0; j < vis; ++j) v1[r * vis + j] = sigmoidf_ref(v1[r * vis + j] + bv[j]);
-    double recon = 0.0;  // sq_diff_per_row energy.hpp:84-96
-    for (size_t i = 0; i < b * vis; ++i) {
-        const double d = double(v0[i]) - double(v1[i]);
-        recon += d * d;
+        if (step < k) hidden(vk.data(), hs.data(), u + (size_t)step * b * h);
     }
-    gemm_nt(v1.data(), vis, W, vis, h1.data(), h, b, h, vis);
-    for (size_t r = 0; r < b; ++r)
-        for (size_t j = 0; j < h; ++j) h1[r * h + j] = sigmoidf_ref(h1[r * h + j] + bh[j]);
+    hidden(vk.data(), hk.data(), nullptr);
     std::vector<float> pos(h * vis), neg(h * vis);
     gemm_axpy(true, h0.data(), h, v0, vis, pos.data(), vis, h, vis, b);
-    gemm_axpy(true, h1.data(), h, v1.data(), vis, neg.data(), vis, h, vis, b);
+    gemm_axpy(true, hk.data(), h, vk.data(), vis, neg.data(), vis, h, vis, b);
     const float scale = lr / static_cast<float>(B_global);
     if (dW) {
         for (size_t i = 0; i < h * vis; ++i) dW[i] = scale * (pos[i] - neg[i]);
         for (size_t j = 0; j < h; ++j) dbh[j] = 0.0f;
         for (size_t j = 0; j < vis; ++j) dbv[j] = 0.0f;
         for (size_t r = 0; r < b; ++r)
-            for (size_t j = 0; j < h; ++j) dbh[j] += scale * (h0[r * h + j] - h1[r * h + j]);
+            for (size_t j = 0; j < h; ++j) dbh[j] += scale * (h0[r * h + j] - hk[r * h + j]);
         for (size_t r = 0; r < b; ++r)
-            for (size_t j = 0; j < vis; ++j) dbv[j] += scale * (v0[r * vis + j] - v1[r * vis + j]);
+            for (size_t j = 0; j < vis; ++j) dbv[j] += scale * (v0[r * vis + j] - vk[r * vis + j]);
     } else {
         for (size_t i = 0; i < h * vis; ++i) W[i] += scale * (pos[i] - neg[i]);
         for (size_t r = 0; r < b; ++r)
-            for (size_t j = 0; j < h; ++j) bh[j] += scale * (h0[r * h + j] - h1[r * h + j]);
+            for (size_t j = 0; j < h; ++j) bh[j] += scale * (h0[r * h + j] - hk[r * h + j]);
         for (size_t r = 0; r < b; ++r)
-            for (size_t j = 0; j < vis; ++j) bv[j] += scale * (v0[r * vis + j] - v1[r * vis + j]);
+            for (size_t j = 0; j < vis; ++j) bv[j] += scale * (v0[r * vis + j] - vk[r * vis + j]);
     }
     if (h0_out) std::memcpy(h0_out, h0.data(), h0.size() * sizeof(float));
     if (hs_out) std::memcpy(hs_out, hs.data(), hs.size() * sizeof(float));
     if (v1_out) std::memcpy(v1_out, v1.data(), v1.size() * sizeof(float));
-    if (h1_out) std::memcpy(h1_out, h1.data(), h1.size() * sizeof(float));
+    if (h1_out) std::memcpy(h1_out, hk.data(), hk.size() * sizeof(float));
+    if (vk_out) std::memcpy(vk_out, vk.data(), vk.size() * sizeof(float));
     return recon / double(B_global);
+}
+
+double orc_rbm_cd1(long long H, long long V, float* W, float* bv, float* bh, const float* v0, long long B,
+                   long long B_global, float lr, const double* u, float* h0_out, float* hs_out, float* v1_out,
+                   float* h1_out, float* dW, float* dbh, float* dbv) {
+    return orc_rbm_cdk(H, V, W, bv, bh, v0, B, B_global, 1, lr, u, h0_out, hs_out, v1_out, h1_out, nullptr, dW, dbh,
+                       dbv);
 }
 
 // rbm_transform_up (energy.hpp:122-126): hidden means of every row, the DBN layer-to-layer map

@@ -83,6 +83,9 @@ def _declare(lib: C.CDLL, prefix: str) -> None:
         lib.orc_rbm_cd1.argtypes = [C.c_longlong, C.c_longlong, _F, _F, _F, _F, C.c_longlong, C.c_longlong,
                                     C.c_float, _D, _F, _F, _F, _F, _F, _F, _F]
         lib.orc_rbm_cd1.restype = C.c_double
+        lib.orc_rbm_cdk.argtypes = [C.c_longlong, C.c_longlong, _F, _F, _F, _F, C.c_longlong, C.c_longlong,
+                                    C.c_int, C.c_float, _D, _F, _F, _F, _F, _F, _F, _F, _F]
+        lib.orc_rbm_cdk.restype = C.c_double
         lib.orc_conv_forward.argtypes = [_F, C.c_longlong, C.c_longlong, C.c_longlong, C.c_longlong, _F, _F,
                                          C.c_longlong, C.c_longlong, C.c_longlong, C.c_longlong, _F]
         lib.orc_conv_backward.argtypes = [_F, C.c_longlong, C.c_longlong, C.c_longlong, C.c_longlong, _F,
@@ -379,6 +382,32 @@ def rbm_cd1(W, bv, bh, v0, lr, u, b_global=None, deltas=False):
                             fptr(dbh) if deltas else None, fptr(dbv) if deltas else None)
     extra = dict(h0=h0, hs=hs, v1=v1, h1=h1, dW=dW, dbh=dbh, dbv=dbv)
     return recon, W, bv, bh, extra
+
+
+def rbm_cdk(W, bv, bh, v0, k, lr, u, b_global=None):
+    """Oracle CD-k (energy.hpp:131-171) with supplied uniforms u[k][B][H] (the draw order of the
+    reference's std::mt19937 stream). Returns (recon, W, bv, bh, extras); extras["hs"] is the LAST
+    sampled hidden state, "v1" the step-1 visible means, "vk" the final ones, "h1" = hk."""
+    lib = load("oracle")
+    W = np.array(W, np.float32, copy=True, order="C")
+    bv = np.array(bv, np.float32, copy=True)
+    bh = np.array(bh, np.float32, copy=True)
+    v0 = np.ascontiguousarray(v0, np.float32)
+    u = np.ascontiguousarray(u, np.float64).ravel()
+    H, V = W.shape
+    B = v0.shape[0]
+    assert u.size >= k * B * H
+    h0, hs, h1 = (np.zeros((B, H), np.float32) for _ in range(3))
+    v1, vk = np.zeros((B, V), np.float32), np.zeros((B, V), np.float32)
+    recon = lib.orc_rbm_cdk(H, V, fptr(W), fptr(bv), fptr(bh), fptr(v0), B, b_global or B, k, lr, dptr(u), fptr(h0),
+                            fptr(hs), fptr(v1), fptr(h1), fptr(vk), None, None, None)
+    return recon, W, bv, bh, dict(h0=h0, hs=hs, v1=v1, h1=h1, vk=vk)
+
+
+def force_samples(u, hs):
+    """uniforms that make `u < p` reproduce the given binary samples for any p in (0, 1]: 0 where
+    hs = 1, 2 where hs = 0 (re-running the oracle on a kernel's own samples)."""
+    return np.where(np.asarray(hs).reshape(np.shape(u)) > 0.5, 0.0, 2.0)
 
 
 def ref_cd_k(W, bv, bh, v0, k, lr, seed):

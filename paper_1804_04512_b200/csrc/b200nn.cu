@@ -6,7 +6,6 @@
 
 #include "../../include/b200nn.h"
 #include "network.cuh"
-#include "probe.cuh"
 #include "crbm.cuh"
 #include "rbm.cuh"
 #include "runtime.cuh"
@@ -401,21 +400,6 @@ int b2n_sgd_momentum_step(float* p, float* v, const float* g, long long n, float
             reinterpret_cast<float4*>(p), reinterpret_cast<float4*>(v), reinterpret_cast<const float4*>(g), n / 4, lr,
             momentum, wd);
         B2N_CUDA(cudaGetLastError());
-    });
-}
-
-// bring-up probe (not part of the documented ABI): A is 128 x 32 (K-major, lda) or 32 x 128
-// (MN-major), B is 32 x 32 (K-major rows of N, or MN-major). smem_out: 5120 floats, d_out: 128x32.
-int b2n_debug_probe(const float* A, long long lda, int a_mn, const float* B, long long ldb, int b_mn, float* smem_out,
-                    float* d_out) {
-    return guard([&] {
-        CUtensorMap ma = a_mn ? b2n::make_map_2d(A, 128, 32, lda, 32, 32, true) : b2n::make_map_2d(A, 32, 128, lda, 32, 128);
-        CUtensorMap mb = b_mn ? b2n::make_map_2d(B, 32, 32, ldb, 32, 32, true) : b2n::make_map_2d(B, 32, 32, ldb, 32, 32);
-        const int smem = 16384 + 4096 + 1024 + 256;
-        B2N_CUDA(cudaFuncSetAttribute(b2n::probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        b2n::probe_kernel<<<1, 192, smem>>>(ma, mb, a_mn, b_mn, smem_out, d_out);
-        B2N_CUDA(cudaGetLastError());
-        B2N_CUDA(cudaDeviceSynchronize());
     });
 }
 

@@ -12,6 +12,7 @@ padded ImageNet-shaped net, the SURVEY 8(c) composite of reference primitives.
     python tests/golden/make_golden.py optim  # only optim.npz (Adagrad / Adadelta / Adam)
     python tests/golden/make_golden.py dbn    # only dbn.npz (dbn_pretrain)
     python tests/golden/make_golden.py crbm   # only crbm.npz (crbm_cd_update)
+    python tests/golden/make_golden.py cdk    # only rbm_cdk.npz (cd_k_update, k = 2 and 3)
 """
 from __future__ import annotations
 
@@ -192,7 +193,29 @@ def crbm_cases():
     np.savez_compressed(HERE / "crbm.npz", **g)
 
 
+CDK_CASES = [(2, 12, 40, 30), (3, 9, 24, 17)]  # (k, batch, hidden, visible)
+
+
+def cdk_cases():
+    """the reference's cd_k_update (energy.hpp:131-171) for k > 1 with std::mt19937(11 + i): the Gibbs
+    chain resamples hs from each intermediate visible mean (k * B * H draws per step)"""
+    g = {}
+    for i, (k, B, H, V) in enumerate(CDK_CASES):
+        W = O.rbm_init(H, V, 42 + i, "ref")
+        bv = O.uniform_f32(7 + i, V, -0.1, 0.1)
+        bh = O.uniform_f32(8 + i, H, -0.1, 0.1)
+        v0 = O.bernoulli_f32(3 + i, 0.5, B * V).reshape(B, V)
+        recon, W1, bv1, bh1 = O.ref_cd_k(W, bv, bh, v0, k, 0.1, 11 + i)
+        g.update({f"W{i}": W, f"bv{i}": bv, f"bh{i}": bh, f"v0_{i}": v0, f"W1_{i}": W1, f"bv1_{i}": bv1,
+                  f"bh1_{i}": bh1, f"recon{i}": np.array([recon]), f"k{i}": np.array([k])})
+    np.savez_compressed(HERE / "rbm_cdk.npz", **g)
+
+
 def main():
+    if sys.argv[1:] == ["cdk"]:
+        cdk_cases()
+        print("cd-k fixtures written to", HERE)
+        return
     if sys.argv[1:] == ["crbm"]:
         crbm_cases()
         print("crbm fixtures written to", HERE)

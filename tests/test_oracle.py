@@ -65,6 +65,26 @@ def test_rbm_cd1_golden():
     assert recon == g["recon"][0]
 
 
+def test_rbm_cdk_golden():
+    """CD-k for k = 2, 3 (energy.hpp:139-144): the reference's chain resamples hs from every
+    intermediate visible mean; the oracle consumes the same mt19937(11 + i) stream as k * B * H
+    supplied uniforms and must match bit for bit."""
+    g = np.load(GOLD / "rbm_cdk.npz")
+    i = 0
+    while f"W{i}" in g:
+        k, B, H = int(g[f"k{i}"][0]), g[f"v0_{i}"].shape[0], g[f"W{i}"].shape[0]
+        u = O.canonical_f64(11 + i, k * B * H)
+        recon, W1, bv1, bh1, _ = O.rbm_cdk(g[f"W{i}"], g[f"bv{i}"], g[f"bh{i}"], g[f"v0_{i}"], k, 0.1, u)
+        assert bitwise(W1, g[f"W1_{i}"]) and bitwise(bv1, g[f"bv1_{i}"]) and bitwise(bh1, g[f"bh1_{i}"]), i
+        assert recon == g[f"recon{i}"][0]
+        # k = 1 of the general routine is the CD-1 restatement
+        r1, Wa, _, _, _ = O.rbm_cdk(g[f"W{i}"], g[f"bv{i}"], g[f"bh{i}"], g[f"v0_{i}"], 1, 0.1, u[:B * H])
+        r2, Wb, _, _, _ = O.rbm_cd1(g[f"W{i}"], g[f"bv{i}"], g[f"bh{i}"], g[f"v0_{i}"], 0.1, u[:B * H].reshape(B, H))
+        assert r1 == r2 and bitwise(Wa, Wb)
+        i += 1
+    assert i == 2
+
+
 def test_sgd_trace_golden():
     """acceptance.cpp:483-555: the 3-step momentum trace with grads {0.3, -0.2, 0.05}."""
     g = np.load(GOLD / "sgd.npz")
