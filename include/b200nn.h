@@ -132,6 +132,12 @@ int b2n_forward_batch(b2n_net* net, const float* x_host, long long batch, float*
 int b2n_net_forward_backward(b2n_net* net, const float* x_host, const int* labels_host, long long batch,
                              long long batch_global, double* loss_share);
 int b2n_net_apply_update(b2n_net* net);
+/* Inspection of the last forward (per-layer parity; no reference counterpart -- fastnn keeps its node
+ * outputs in Network::forward's locals, network.hpp:58-64): the output of fused layer `layer` (conv +
+ * act + 2x2 pool, or dense + act) for `batch` rows, NCHW per row, and the pool argmax codes in the
+ * same order (codes may be NULL). */
+int b2n_net_num_layers(b2n_net* net, long long* n);
+int b2n_net_layer_output(b2n_net* net, int layer, long long batch, float* out_host, unsigned char* codes_host);
 int b2n_net_grad_buffer(b2n_net* net, float** dev_ptr, long long* n_floats);
 int b2n_nccl_unique_id(char id_out[128]);
 int b2n_net_dp_init(b2n_net* net, const char id[128], int rank, int world);

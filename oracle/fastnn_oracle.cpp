@@ -29,9 +29,33 @@
 #include <memory>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 namespace {
+
+// Exact-sum mode (test instrumentation, off by default): the conv kernel / bias gradient sums --
+// chains of up to N*OH*OW ~ 10^7 terms that the reference accumulates in fp32 -- run in double and
+// round once, giving the float64 truth of the reference's own summands. The parity test of the
+// ImageNet shape at B = 128 uses it to show where the reference's fp32 sum is the inexact side.
+bool g_exact_sums = false;
+
+// fn(i) for i in [0, n) over the host threads when the work is large; every output is still
+// produced by exactly one call in its fixed order, so results are bitwise independent of threads
+template <class F>
+void par_for(size_t n, bool big, F fn) {
+    const size_t nt = big ? std::min<size_t>(n, std::max(1u, std::thread::hardware_concurrency())) : 1;
+    if (nt <= 1) {
+        for (size_t i = 0; i < n; ++i) fn(i);
+        return;
+    }
+    std::vector<std::thread> ts;
+    for (size_t t = 0; t < nt; ++t)
+        ts.emplace_back([&, t] {
+            for (size_t i = t; i < n; i += nt) fn(i);
+        });
+    for (auto& th : ts) th.join();
+}
 
 // ---------------------------------------------------------------------------- gemm kernels
 
@@ -46,7 +70,8 @@ inline float hsum8(const float* v) {
 void gemm_nt(const float* A, size_t lda, const float* B, size_t ldb, float* C, size_t ldc, size_t M, size_t N,
              size_t K) {
     const size_t kt = K / 8 * 8;
-    for (size_t i = 0; i < M; ++i)
+    // one thread per output row: every output keeps its single fixed-order chain (bit-exact)
+    par_for(M, M * N * K > (1u << 22), [&](size_t i) {
         for (size_t j = 0; j < N; ++j) {
             float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             const float* a = A + i * lda;
@@ -56,17 +81,19 @@ void gemm_nt(const float* A, size_t lda, const float* B, size_t ldb, float* C, s
             for (size_t k = kt; k < K; ++k) acc[k - kt] = std::fmaf(a[k], b[k], acc[k - kt]);
             C[i * ldc + j] = hsum8(acc);
         }
+    });
 }
 
 // C = op(A) . B with op(A) = A (NN) or A^T (TN): gemm.hpp:30-78, sequential fma over k
 void gemm_axpy(bool a_t, const float* A, size_t lda, const float* B, size_t ldb, float* C, size_t ldc, size_t M,
                size_t N, size_t K) {
-    for (size_t i = 0; i < M; ++i)
+    par_for(M, M * N * K > (1u << 22), [&](size_t i) {
         for (size_t j = 0; j < N; ++j) {
             float acc = 0.0f;
             for (size_t k = 0; k < K; ++k) acc = std::fmaf(a_t ? A[k * lda + i] : A[i * lda + k], B[k * ldb + j], acc);
             C[i * ldc + j] = acc;
         }
+    });
 }
 
 inline float sigmoidf_ref(float v) { return 1.0f / (1.0f + std::exp(-v)); }  // layers.hpp:279, energy.hpp:36
@@ -80,8 +107,8 @@ struct Shape4 {
 void conv_fwd(const float* x, const Shape4& xs, const float* ker, size_t k, size_t kh, size_t kw, size_t pad,
               float* y /* n,k,oh,ow */) {
     const size_t oh = xs.h + 2 * pad - kh + 1, ow = xs.w + 2 * pad - kw + 1;
-    for (size_t b = 0; b < xs.n; ++b)
-        for (size_t f = 0; f < k; ++f)
+    par_for(xs.n * k, xs.n * k * oh * ow > (1u << 16), [&](size_t bf) {
+        const size_t b = bf / k, f = bf % k;
             for (size_t oy = 0; oy < oh; ++oy)
                 for (size_t ox = 0; ox < ow; ++ox) {
                     float acc = 0.0f;
@@ -97,6 +124,7 @@ void conv_fwd(const float* x, const Shape4& xs, const float* ker, size_t k, size
                             }
                     y[((b * k + f) * oh + oy) * ow + ox] = acc;
                 }
+    });
 }
 
 // dx = crop_pad(full-conv(dy, kt)) via padded-valid with flipped kernels (layers.hpp:161-174,
@@ -104,8 +132,8 @@ void conv_fwd(const float* x, const Shape4& xs, const float* ker, size_t k, size
 // where dy_pad has a (kh-1) zero border. With pad>0 this is the SURVEY 8(c) composite (crop p per border).
 void conv_bwd_data(const float* dy, size_t n, size_t k, size_t oh, size_t ow, const float* ker, size_t c_in,
                    size_t kh, size_t kw, size_t pad, size_t h, size_t w, float* dx) {
-    for (size_t b = 0; b < n; ++b)
-        for (size_t c = 0; c < c_in; ++c)
+    par_for(n * c_in, n * c_in * h * w > (1u << 16), [&](size_t bc) {
+        const size_t b = bc / c_in, c = bc % c_in;
             for (size_t iy = 0; iy < h; ++iy)
                 for (size_t ix = 0; ix < w; ++ix) {
                     float acc = 0.0f;
@@ -122,17 +150,22 @@ void conv_bwd_data(const float* dy, size_t n, size_t k, size_t oh, size_t ow, co
                             }
                     dx[((b * c_in + c) * h + iy) * w + ix] = acc;
                 }
+    });
 }
 
 // gk[f,c] += sum_img corr(x[img,c] (padded), dy[img,f]) (layers.hpp:176-184, add_corr_map conv.hpp:62-89)
 void conv_bwd_filter(const float* x, const Shape4& xs, const float* dy, size_t k, size_t oh, size_t ow, size_t kh,
                      size_t kw, size_t pad, float* gk, float* gb) {
-    for (size_t f = 0; f < k; ++f)
-        for (size_t c = 0; c < xs.c; ++c)
+    // one thread per (f, c) pair, as the reference's parallel_for (layers.hpp:176-184)
+    par_for(k * xs.c, xs.n * oh * ow > (1u << 14), [&](size_t fc) {
+        const size_t f = fc / xs.c, c = fc % xs.c;
+        {
+            double exact[64] = {};  // kh * kw <= 64 (exact-sum mode only)
             for (size_t img = 0; img < xs.n; ++img)
                 for (size_t oy = 0; oy < kh; ++oy)
                     for (size_t ox = 0; ox < kw; ++ox) {
                         float acc = gk[((f * xs.c + c) * kh + oy) * kw + ox];
+                        double dacc = 0.0;
                         for (size_t di = 0; di < oh; ++di)
                             for (size_t dj = 0; dj < ow; ++dj) {
                                 const long long iy = (long long)(oy + di) - (long long)pad;
@@ -140,10 +173,26 @@ void conv_bwd_filter(const float* x, const Shape4& xs, const float* dy, size_t k
                                 const float v = (iy < 0 || ix < 0 || iy >= (long long)xs.h || ix >= (long long)xs.w)
                                                     ? 0.0f
                                                     : x[((img * xs.c + c) * xs.h + iy) * xs.w + ix];
-                                acc = std::fmaf(dy[((img * k + f) * oh + di) * ow + dj], v, acc);
+                                const float d = dy[((img * k + f) * oh + di) * ow + dj];
+                                if (g_exact_sums) dacc += (double)d * (double)v;
+                                else acc = std::fmaf(d, v, acc);
                             }
-                        gk[((f * xs.c + c) * kh + oy) * kw + ox] = acc;
+                        if (g_exact_sums) exact[oy * kw + ox] += dacc;
+                        else gk[((f * xs.c + c) * kh + oy) * kw + ox] = acc;
                     }
+            if (g_exact_sums)
+                for (size_t t = 0; t < kh * kw; ++t) gk[(f * xs.c + c) * kh * kw + t] += (float)exact[t];
+        }
+    });
+    if (g_exact_sums) {
+        for (size_t f = 0; f < k; ++f) {
+            double acc = 0.0;
+            for (size_t img = 0; img < xs.n; ++img)
+                for (size_t p = 0; p < oh * ow; ++p) acc += dy[(img * k + f) * oh * ow + p];
+            gb[f] += (float)acc;
+        }
+        return;
+    }
     for (size_t img = 0; img < xs.n; ++img)  // layers.hpp:185-191, serial
         for (size_t f = 0; f < k; ++f)
             for (size_t p = 0; p < oh * ow; ++p) gb[f] += dy[(img * k + f) * oh * ow + p];
@@ -422,6 +471,9 @@ std::vector<ParamSlot> params(Net& net) {  // trainable() order: w then b per la
 }  // namespace
 
 extern "C" {
+
+// test instrumentation: exact (double) conv gradient sums, see g_exact_sums
+void orc_set_exact_sums(int on) { g_exact_sums = on != 0; }
 
 struct orc_layer {
     int kind;

@@ -99,6 +99,7 @@ def _declare(lib: C.CDLL, prefix: str) -> None:
                                                           _D, _F, _F, _F, _F, _F, _F, _F]
         lib.orc_crbm_cd1.restype = C.c_double
         lib.orc_crbm_init.argtypes = [C.c_longlong] * 4 + [C.c_uint, _F]
+        lib.orc_set_exact_sums.argtypes = [C.c_int]
     else:
         lib.ref_cd_k.argtypes = [C.c_longlong, C.c_longlong, _F, _F, _F, _F, C.c_longlong, C.c_int, C.c_float,
                                  C.c_uint]
@@ -142,6 +143,12 @@ def load(which: str = "oracle") -> C.CDLL:
     _declare(lib, "orc" if which == "oracle" else "ref")
     _lib_cache[which] = lib
     return lib
+
+
+def set_exact_sums(on: bool) -> None:
+    """Restatement only: conv kernel / bias gradient sums in double (the float64 truth of the
+    reference's own summands), see g_exact_sums in fastnn_oracle.cpp."""
+    load("oracle").orc_set_exact_sums(1 if on else 0)
 
 
 def ref_available() -> bool:

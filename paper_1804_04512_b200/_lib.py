@@ -105,6 +105,8 @@ _SIGS = {
     "b2n_net_train_stream": ([_VP, _F, _I, C.c_longlong, C.c_longlong, _D], C.c_int),
     "b2n_forward_batch": ([_VP, _F, C.c_longlong, _F, _I], C.c_int),
     "b2n_net_forward_backward": ([_VP, _F, _I, C.c_longlong, C.c_longlong, _D], C.c_int),
+    "b2n_net_num_layers": ([_VP, C.POINTER(C.c_longlong)], C.c_int),
+    "b2n_net_layer_output": ([_VP, C.c_int, C.c_longlong, _F, C.POINTER(C.c_ubyte)], C.c_int),
     "b2n_net_apply_update": ([_VP], C.c_int),
     "b2n_net_grad_buffer": ([_VP, C.POINTER(_F), _LL], C.c_int),
     "b2n_nccl_unique_id": ([C.c_char_p], C.c_int),

@@ -137,6 +137,12 @@ int b2n_net_forward_backward(b2n_net* net, const float* x, const int* labels, lo
                              double* loss_share) {
     return guard([&] { *loss_share = net->impl.forward_backward(x, labels, batch, batch_global); });
 }
+int b2n_net_num_layers(b2n_net* net, long long* n) {
+    return guard([&] { *n = net->impl.num_layers(); });
+}
+int b2n_net_layer_output(b2n_net* net, int layer, long long batch, float* out, unsigned char* codes) {
+    return guard([&] { net->impl.layer_output(layer, batch, out, codes); });
+}
 int b2n_net_apply_update(b2n_net* net) {
     return guard([&] { net->impl.apply_update(); });
 }

@@ -163,6 +163,12 @@ struct ConvTParams {
     // DGRAD producer: dZ of the layer, staged + expanded on the fly (two staging slots)
     DZSrc z;
     int zslot_bytes;
+    // FWD + pool, 3xTF32: exact resolution of the pooling decisions the tensor-core rounding could flip
+    // (ct_fix_window). fix_list = per-CTA item lists ([grid][fix_cap]), null disables it; fix_cb = the
+    // rigorous per-term bound of |Z_tc - Z_ref| / sum|k x| for this layer's chain length (host-computed)
+    unsigned* fix_list;
+    long long fix_cap;
+    float fix_cb;
     unsigned long long* trace;  // bring-up: per-tile role timestamps of CTA 0 (clock64), null in production
     int dbg;                    // bring-up bisection (B2N_CT_DBG): 1 no lo split, 2 no epilogue work, 4 no halo copy
 };
@@ -312,9 +318,18 @@ __device__ __forceinline__ void tmem_zeron(uint32_t taddr) {
 // tile row), channels [hsel*NK/2, (hsel+1)*NK/2). Specialised on activation / pooling / output layout.
 // FWD: bias + act (layers.hpp:138-146, :278-282), then the 2x2 max with the reference's first-index
 // tie rule over window order (0,0) (0,1) (1,0) (1,1) (layers.hpp:228-232) -> pooled value + code byte.
+//
+// Exact pooling decisions (FWD + pool, 3xTF32, p.fix_list set). The reference computes every conv
+// output as ONE fp32 fma chain over (c, di, dj) plus the bias (conv.hpp:62-119, layers.hpp:138-146);
+// the tensor-core value differs from it by at most tau = fix_cb * sum|k x| (+ the bias-add rounding),
+// and sum|k x| <= ||k||_1 * max|x| over the tile's input halo (measured by the lo-split warps). A window
+// whose first-index argmax -- or, for relu, whether the routed value is > 0 -- is not decided with that
+// margin is appended to the CTA's fix list; the CTA recomputes it at its end with the reference's own
+// chain (ct_fix_window), so pooled codes and relu' are the reference's, not a rounding artefact.
 template <int NK, int ACT, bool POOL, bool BLOCKED, int MODE>
 __device__ __forceinline__ void ct_epilogue(const ConvTParams& p, uint32_t tmem_base, int bufcols, uint64_t* tfull,
-                                            uint64_t* tempty, int q, int hsel, int lane) {
+                                            uint64_t* tempty, int q, int hsel, int lane, const float* xmr,
+                                            unsigned* fixcnt) {
     constexpr int NH = NK / 2;   // channels of this warp
     constexpr int NQ = (NH + 3) / 4;
     const int c_lo = hsel * NH;
@@ -339,6 +354,18 @@ __device__ __forceinline__ void ct_epilogue(const ConvTParams& p, uint32_t tmem_
     float bias_r[NH];
 #pragma unroll
     for (int j = 0; j < NH; ++j) bias_r[j] = (MODE == CT_FWD && c_lo + j < p.N) ? __ldg(p.bias + c_lo + j) : 0.0f;
+    // fix_cb * ||k_j||_1 per channel of this warp (0: no fix-up)
+    constexpr bool kFix = MODE == CT_FWD && POOL;
+    const bool fix = kFix && p.fix_list != nullptr;
+    float tk[NH];
+#pragma unroll
+    for (int j = 0; j < NH; ++j) {
+        float a = 0.0f;
+        if (fix && c_lo + j < p.N)
+            for (int i = 0; i < p.wk_C * p.kh * p.kw; ++i) a += fabsf(__ldg(p.wk + (long long)(c_lo + j) * p.wk_C * p.kh * p.kw + i));
+        tk[j] = p.fix_cb * a * 1.0001f;  // the float sum of |k| may round low by < 1e-4 relative
+    }
+    unsigned* flist = fix ? p.fix_list + (long long)blockIdx.x * p.fix_cap : nullptr;
     const long long plane = (long long)p.out.H * p.out.W;  // NCHW channel stride
     const long long qstride = (long long)p.out.W * 4;      // blocked quad stride (floats)
     int it = 0;
@@ -369,15 +396,24 @@ __device__ __forceinline__ void ct_epilogue(const ConvTParams& p, uint32_t tmem_
             }
             const int y = y0 + r;
 #pragma unroll
-            for (int j = 0; j < NH; ++j) {
-                v0[j] = apply_act(ACT, v0[j] + bias_r[j]);
-                if (POOL) v1[j] = apply_act(ACT, v1[j] + bias_r[j]);
+            for (int j = 0; j < NH; ++j) {  // pre-activations Z = chain + bias (layers.hpp:138-146)
+                v0[j] += bias_r[j];
+                if (POOL) v1[j] += bias_r[j];
+            }
+            if (!POOL) {
+#pragma unroll
+                for (int j = 0; j < NH; ++j) v0[j] = apply_act(ACT, v0[j]);
             }
             if (POOL) {
                 const bool writer = xok && y + 1 < p.OH && (lane & 1) == 0;
                 const int py = y >> 1, px = x >> 1;
                 float* orow = BLOCKED ? ob + (long long)py * Kq * qstride + (long long)px * 4 : ob + (long long)py * p.out.W + px;
                 uint8_t* crow = p.codes + (long long)b * p.codes_bstride + (((long long)py * Kq) * p.codes_pw + px) * 4;
+                float xm = 0.0f;
+                if (fix) {
+                    const float* xr = xmr + (it & 7) * 4;
+                    xm = fmaxf(fmaxf(xr[0], xr[1]), fmaxf(xr[2], xr[3]));
+                }
 #pragma unroll
                 for (int g = 0; g < NQ; ++g) {
                     float o[4];
@@ -385,15 +421,54 @@ __device__ __forceinline__ void ct_epilogue(const ConvTParams& p, uint32_t tmem_
 #pragma unroll
                     for (int jj = 0; jj < 4; ++jj) {
                         const int j = 4 * g + jj;
-                        const float a1 = __shfl_xor_sync(0xffffffffu, v0[j], 1);
-                        const float a3 = __shfl_xor_sync(0xffffffffu, v1[j], 1);
-                        float best = v0[j];
+                        // window order (0,0) (0,1) (1,0) (1,1) (layers.hpp:228-232)
+                        const float z[4] = {v0[j], __shfl_xor_sync(0xffffffffu, v0[j], 1), v1[j],
+                                            __shfl_xor_sync(0xffffffffu, v1[j], 1)};
+                        float a[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) a[i] = apply_act(ACT, z[i]);
+                        float best = a[0], zb = z[0];
                         uint32_t code = 0;
-                        if (a1 > best) best = a1, code = 1;
-                        if (v1[j] > best) best = v1[j], code = 2;
-                        if (a3 > best) best = a3, code = 3;
+#pragma unroll
+                        for (int i = 1; i < 4; ++i)
+                            if (a[i] > best) best = a[i], zb = z[i], code = (uint32_t)i;
                         o[jj] = best;
                         cw |= code << (8 * jj);
+                        if (kFix && fix) {
+                            // is the decision (and, for relu, the routed value's sign) certain within tau?
+                            const float tau = tk[j] * xm;
+                            bool doubt = false;
+                            if (ACT == ACT_RELU) {
+                                const float tw = tau + fabsf(zb) * 2.4e-7f;
+                                const float lo_w = fmaxf(zb - tw, 0.0f), hi_w = fmaxf(zb + tw, 0.0f);
+                                doubt = lo_w == 0.0f && hi_w > 0.0f;
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    const float hi = fmaxf(z[i] + tau + fabsf(z[i]) * 2.4e-7f, 0.0f);
+                                    if ((uint32_t)i < code ? hi >= lo_w : ((uint32_t)i > code && hi > lo_w)) doubt = true;
+                                }
+                            } else {
+                                // sigmoid: |da| <= |dz| / 4 + a few ulps of the two implementations' expf
+                                const float sc = ACT == ACT_SIGMOID ? 0.25f : 1.0f;
+                                const float lo_w = best - (sc * tau + fabsf(best) * 4.8e-7f);
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) {
+                                    const float hi = a[i] + sc * tau + fabsf(a[i]) * 4.8e-7f;
+                                    if ((uint32_t)i < code ? hi >= lo_w : ((uint32_t)i > code && hi > lo_w)) doubt = true;
+                                }
+                            }
+                            doubt = (doubt || (p.dbg & 8)) && writer && c_lo + j < p.N;
+                            const unsigned m = __ballot_sync(0xffffffffu, doubt);
+                            if (m) {
+                                const int leader = __ffs(m) - 1;
+                                unsigned base = 0;
+                                if (lane == leader) base = atomicAdd(fixcnt, (unsigned)__popc(m));
+                                base = __shfl_sync(0xffffffffu, base, leader);
+                                if (doubt)
+                                    flist[base + __popc(m & ((1u << lane) - 1u))] =
+                                        (((unsigned)it * p.R + r) * p.Wt + L) * NK + c_lo + j;
+                            }
+                        }
                     }
                     const int gq = (c_lo >> 2) + g;
                     if (writer && gq < Kq) {
@@ -454,6 +529,55 @@ __device__ __forceinline__ void ct_mma_row(uint32_t tacc, uint64_t a_row, uint64
     }
 }
 
+// One pooling window of the forward recomputed exactly as the reference does (ct_epilogue's fix list):
+// Z = fl(fma chain over (c, di, dj) in that order from 0) + bias (conv.hpp:62-119 / :215-273,
+// layers.hpp:138-146; zero padding contributes exact zeros), the activation, then the first-index 2x2
+// max (layers.hpp:228-232). Rewrites the pooled value and the code byte. Item = ((it*R + r)*Wt + L)*NK + k.
+__device__ __forceinline__ void ct_fix_window(const ConvTParams& p, unsigned item, int NK) {
+    const int k = (int)(item % (unsigned)NK);
+    unsigned rest = item / (unsigned)NK;
+    const int L = (int)(rest % (unsigned)p.Wt);
+    rest /= (unsigned)p.Wt;
+    const int r = (int)(rest % (unsigned)p.R);
+    const int it = (int)(rest / (unsigned)p.R);
+    int b, y0, x0;
+    ct_tile(p, (int)blockIdx.x + it * (int)gridDim.x, b, y0, x0);
+    const int Y = y0 + r, X = x0 + L;  // window origin (even, even)
+    const int C = p.wk_C, KH = p.kh, KW = p.kw;
+    const float* wk = p.wk + (long long)k * C * KH * KW;
+    const float* xb = p.x + (long long)b * p.x_bstride;
+    const float bias = __ldg(p.bias + k);
+    float a[4];
+#pragma unroll 1
+    for (int w = 0; w < 4; ++w) {
+        const int y = Y + (w >> 1), x = X + (w & 1);
+        float acc = 0.0f;
+        for (int c = 0; c < C; ++c)
+            for (int di = 0; di < KH; ++di) {
+                const int iy = y + di - p.pad;
+                for (int dj = 0; dj < KW; ++dj) {
+                    const int ix = x + dj - p.pad;
+                    if ((unsigned)iy < (unsigned)p.Hin && (unsigned)ix < (unsigned)p.Win)
+                        acc = fmaf(__ldg(wk + (c * KH + di) * KW + dj),
+                                   __ldg(xb + (((long long)iy * p.G + (c >> 2)) * p.Win + ix) * 4 + (c & 3)), acc);
+                }
+            }
+        a[w] = apply_act(p.act, acc + bias);
+    }
+    float best = a[0];
+    int code = 0;
+    for (int i = 1; i < 4; ++i)
+        if (a[i] > best) best = a[i], code = i;
+    const int py = Y >> 1, px = X >> 1, Kq = (p.out.C + 3) >> 2;
+    float* ob = p.out.p + (long long)b * p.out.bstride;
+    if (p.out.blocked)
+        ob[(((long long)py * Kq + (k >> 2)) * p.out.W + px) * 4 + (k & 3)] = best;
+    else
+        ob[((long long)k * p.out.H + py) * p.out.W + px] = best;
+    p.codes[(long long)b * p.codes_bstride + (((long long)py * Kq + (k >> 2)) * p.codes_pw + px) * 4 + (k & 3)] =
+        (uint8_t)code;
+}
+
 // Correlation over row-blocked halo tiles on the tensor cores (3xTF32: a.b = ah.bh + ah.bl + al.bh with
 // the hardware's tf32 truncation making the raw value the hi part, fp32 accumulate, ~1e-7 relative). Per tile (R output rows x Wt columns) and per halo row
 // h, each MMA reads the halo row ONCE and multiplies it with all kh filter rows stacked along N
@@ -483,7 +607,9 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
     uint64_t* zfull = reinterpret_cast<uint64_t*>(tslot + 2);  // DGRAD staging slots
     uint64_t* zempty = zfull + 2;
     uint64_t* dtab = zempty + 2;  // per K step: A descriptor (halo row 0, stage 0), B descriptor
-    uint8_t* zst = reinterpret_cast<uint8_t*>(dtab + 2 * p.ksteps);  // 2 staging slots (DGRAD)
+    float* xmr = reinterpret_cast<float*>(dtab + 2 * p.ksteps);  // [8 tiles][4 producer warps] max|x| of a halo
+    unsigned* fixcnt = reinterpret_cast<unsigned*>(xmr + 32);     // items in this CTA's fix list
+    uint8_t* zst = reinterpret_cast<uint8_t*>(xmr + 64);  // 2 staging slots (DGRAD)
     zst = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(zst) + 127) & ~uintptr_t(127));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -505,6 +631,7 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
             mbar_init(&zfull[a], 1);
             mbar_init(&zempty[a], 32 * Roles::kProdWarps);
         }
+        *fixcnt = 0u;
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(tslot, tcols);
@@ -665,10 +792,19 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
                 if (pt == 0) CT_TRACE(it, 1);
                 if (X3 && !(p.dbg & 1)) {
                     const float4* src = reinterpret_cast<const float4*>(hi);
+                    float am = 0.0f;  // max|x| of the halo: bounds sum|k x| for the exact-decision test
                     for (int i = pt; i < chunks; i += NP) {
                         const float4 a = src[i];
+                        am = fmaxf(am, fmaxf(fmaxf(fabsf(a.x), fabsf(a.y)), fmaxf(fabsf(a.z), fabsf(a.w))));
                         reinterpret_cast<float4*>(lo)[i] =
                             make_float4(split_lo1(a.x), split_lo1(a.y), split_lo1(a.z), split_lo1(a.w));
+                    }
+                    if (p.fix_list) {
+#pragma unroll
+                        for (int o = 16; o; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+                        // ring of 8: the producer of tile it + 8 waits (through the stage / TMEM buffer
+                        // barriers) for the epilogue of tile it + 2
+                        if ((pt & 31) == 0) xmr[(it & 7) * 4 + (pt >> 5)] = am;
                     }
                 }
                 fence_proxy_async_smem();
@@ -709,23 +845,23 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
         const int q = warp & 3;
         const int hsel = (warp - Roles::kEpi0) >> 2;
         if (MODE == CT_DGRAD) {
-            ct_epilogue<NK, ACT_NONE, false, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane);
+            ct_epilogue<NK, ACT_NONE, false, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane, xmr, fixcnt);
         } else {
             const int sel = (p.act == ACT_SIGMOID ? 2 : p.act == ACT_RELU ? 1 : 0) * 4 + (p.pool ? 2 : 0) +
                             (p.out.blocked ? 1 : 0);
             switch (sel) {
-                case 3: ct_epilogue<NK, ACT_NONE, true, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
-                case 2: ct_epilogue<NK, ACT_NONE, true, false, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
-                case 7: ct_epilogue<NK, ACT_RELU, true, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
-                case 6: ct_epilogue<NK, ACT_RELU, true, false, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
-                case 11: ct_epilogue<NK, ACT_SIGMOID, true, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
-                case 10: ct_epilogue<NK, ACT_SIGMOID, true, false, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
-                case 1: ct_epilogue<NK, ACT_NONE, false, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
-                case 0: ct_epilogue<NK, ACT_NONE, false, false, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
-                case 5: ct_epilogue<NK, ACT_RELU, false, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
-                case 4: ct_epilogue<NK, ACT_RELU, false, false, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
-                case 9: ct_epilogue<NK, ACT_SIGMOID, false, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
-                default: ct_epilogue<NK, ACT_SIGMOID, false, false, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane); break;
+                case 3: ct_epilogue<NK, ACT_NONE, true, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane, xmr, fixcnt); break;
+                case 2: ct_epilogue<NK, ACT_NONE, true, false, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane, xmr, fixcnt); break;
+                case 7: ct_epilogue<NK, ACT_RELU, true, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane, xmr, fixcnt); break;
+                case 6: ct_epilogue<NK, ACT_RELU, true, false, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane, xmr, fixcnt); break;
+                case 11: ct_epilogue<NK, ACT_SIGMOID, true, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane, xmr, fixcnt); break;
+                case 10: ct_epilogue<NK, ACT_SIGMOID, true, false, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane, xmr, fixcnt); break;
+                case 1: ct_epilogue<NK, ACT_NONE, false, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane, xmr, fixcnt); break;
+                case 0: ct_epilogue<NK, ACT_NONE, false, false, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane, xmr, fixcnt); break;
+                case 5: ct_epilogue<NK, ACT_RELU, false, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane, xmr, fixcnt); break;
+                case 4: ct_epilogue<NK, ACT_RELU, false, false, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane, xmr, fixcnt); break;
+                case 9: ct_epilogue<NK, ACT_SIGMOID, false, true, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane, xmr, fixcnt); break;
+                default: ct_epilogue<NK, ACT_SIGMOID, false, false, MODE>(p, tmem_base, bufcols, tfull, tempty, q, hsel, lane, xmr, fixcnt); break;
             }
         }
     }
@@ -735,6 +871,11 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem_base, tcols);
+    }
+    if (MODE == CT_FWD && p.fix_list) {  // the CTA's doubtful windows, recomputed in the reference's order
+        const unsigned n = *fixcnt;
+        const unsigned* fl = p.fix_list + (long long)blockIdx.x * p.fix_cap;
+        for (unsigned i = threadIdx.x; i < n; i += blockDim.x) ct_fix_window(p, fl[i], NK);
     }
 }
 
@@ -1055,6 +1196,7 @@ struct ConvTLaunch {
     int mode = CT_FWD, nk = 16, grid = 1, smem = 0;
     bool x3 = true;
     double flops = 0, bytes = 0;
+    std::shared_ptr<DevMem> fix;  // exact-decision item lists (convt_enable_fix)
     void run(cudaStream_t st) const;
 };
 
@@ -1097,7 +1239,7 @@ inline ConvTLaunch plan_convt(int mode, int B, int Cp, int Hin, int Win, int kh,
             zz.bw = ((z->pool ? P_ / 2 + 1 : P_) + 6) & ~3;
             zb = (zs_bytes(zz) + 127) & ~127;
         }
-        const int need = 2 * (2 * hb) + 2 * (ks * 2 * kh * (p.stack ? 2 : 1) * L.nk * 16) + 1024 + 256 + ks * 16 + 128 + 2 * zb;
+        const int need = 2 * (2 * hb) + 2 * (ks * 2 * kh * (p.stack ? 2 : 1) * L.nk * 16) + 1024 + 256 + ks * 16 + 384 + 2 * zb;
         if (need <= 227 * 1024) break;
         if (p.R <= 2) {
             fits = false;
@@ -1130,7 +1272,7 @@ inline ConvTLaunch plan_convt(int mode, int B, int Cp, int Hin, int Win, int kh,
         p.zslot_bytes = (zs_bytes(p.z) + 127) & ~127;
         dz_maps(p.z, B, L.zmaps);
     }
-    const int fixed = 2 * p.w_bytes + 1024 + 256 + p.ksteps * 16 + 128 + 2 * p.zslot_bytes;
+    const int fixed = 2 * p.w_bytes + 1024 + 256 + p.ksteps * 16 + 384 + 2 * p.zslot_bytes;
     const int budget = 227 * 1024;
     p.stages = std::min(4, (budget - fixed) / p.stage_bytes);
     if (p.stages < 2) throw Error(B2N_ESHAPE, "b200nn conv: halo tile does not fit shared memory");
@@ -1140,6 +1282,25 @@ inline ConvTLaunch plan_convt(int mode, int B, int Cp, int Hin, int Win, int kh,
     p.trace = TraceRegistry::get().next();
     if (const char* e = std::getenv("B2N_CT_DBG")) p.dbg = std::atoi(e);
     return L;
+}
+
+// Exact pooling decisions for a FWD + pool plan (3xTF32 only): one item list per CTA, sized for every
+// window x channel of its tiles. The bound per chain term: the tf32 split drops <= 3 * 2^-20 |k x| per
+// product; the tensor core's fp32 accumulation (products exact, sums aligned to the largest term and
+// truncated: <= 9 ulps of it per 8-term MMA, up to 3 MMAs per K step) <= 7 n 2^-24 sum|k x|; the
+// reference's sequential fma chain <= n 2^-24 sum|k x| (n = Cp * kh * kw terms).
+inline void convt_enable_fix(ConvTLaunch& L, std::shared_ptr<DevMem>& mem) {
+    ConvTParams& p = L.p;
+    if (!L.x3 || !p.pool || L.mode != CT_FWD) return;
+    const long long per_cta = (p.ntiles + L.grid - 1) / L.grid;
+    p.fix_cap = per_cta * (p.R / 2) * ((p.Wt + 1) / 2) * L.nk;
+    if (((long long)per_cta * p.R * p.Wt * L.nk) >> 32) throw Error(B2N_ESHAPE, "conv fix-up items exceed 32 bits");
+    mem = std::make_shared<DevMem>();
+    mem->alloc((size_t)L.grid * p.fix_cap * 4);
+    p.fix_list = mem->as<unsigned>();
+    const double n = (double)p.Cp * p.kh * p.kw;
+    p.fix_cb = (float)(3.0 * std::ldexp(1.0, -20) + 8.0 * n * std::ldexp(1.0, -24));
+    if (const char* e = std::getenv("B2N_CT_FIXSCALE")) p.fix_cb *= (float)std::atof(e);
 }
 
 template <int NK, int MODE, bool X3>

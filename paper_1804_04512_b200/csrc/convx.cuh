@@ -1,0 +1,284 @@
+// convx.cuh -- the conv-stack FORWARD (conv_forward + activation + 2x2 max-pool, layers.hpp:132-148,
+// :205-238, :278-282) computed bit-for-bit as the reference computes it.
+//
+// Why not the tensor cores here: the forward makes DISCRETE decisions -- the first-index argmax of
+// every pooling window and relu's "> 0" -- that route the whole backward pass. A 3xTF32 tensor-core
+// value is within ~1e-6 of the reference's, yet over the ImageNet-shaped stack at batch 128 a dozen
+// of the ~44 M windows are near-ties that it resolves differently, and each misrouted window moves
+// the first layers' gradients by up to ~5e-3 of their norm (measured; tools/diag/imnet_layers.py).
+// Recomputing only the doubtful windows exactly (convt.cuh's fix list) cannot help past the first
+// layer: the NEXT layer's inputs are then tensor-core values, and near-ties flip on those. So the
+// forward values themselves have to be the reference's: ONE fp32 fma chain per output over
+// (c, di, dj) in that order from 0 (conv.hpp:62-119 add_corr_map / :215-273 im2col, both backends
+// the same order), padding contributing exact zeros, then + bias (a separate rounding,
+// layers.hpp:138-146), the activation, and the first-index 2x2 max. On 16-kernel filters this is
+// also the faster path: the 3xTF32 tensor-core forward is bound by streaming its M=128 operand from
+// shared memory at N = 16, while this kernel keeps 64 independent FFMA chains per thread.
+//
+// Layout: thread = one 2x2 output block (one pooling window) x KG = 4*KQ kernels (grid.y = kernel
+// groups). Per tile (TR x TW outputs) the input halo is transposed from the row-blocked activations
+// ([b][y][c/4][x][4], convt.cuh) into channel planes [C][HR][PWp] in shared memory and the kernel
+// group's weights into [C][kh][kw][KG]; the channel loop streams two halo rows at a time (float2
+// loads), every (c, di, dj) step is KQ broadcast float4 weight loads + 4*KG FFMAs.
+#pragma once
+#include "convt.cuh"
+
+namespace b2n {
+
+struct ConvXParams {
+    int B, C, G, Hin, Win, kh, kw, pad, OH, OW, K;  // C real input channels (G quads in the blocked input)
+    int TR, TW, HR, PW, PWp;                       // tile rows / cols (even), halo rows / cols, plane pitch
+    int tiles_x, tiles_y;
+    int act, pool;
+    const float* x;  // row-blocked input [b][y][G][Win][4]
+    long long x_bstride;
+    const float* wk;    // [K][C][kh][kw]
+    const float* bias;  // [K]
+    TLayout out;        // pooled (or full) output, row-blocked or NCHW
+    uint8_t* codes;     // pool argmax codes, row-blocked bytes [b][py][Kq][PWc][4]
+    long long codes_bstride;
+    int codes_pw;
+};
+
+// the reference's sigmoidf (layers.hpp:279): 1 / (1 + expf(-v)) with expf rounded to nearest (glibc's
+// expf is correctly rounded except in rare hard cases; exp in double then one rounding reproduces it)
+__device__ __forceinline__ float sigmoid_exact(float v) {
+    const float e = (float)exp(-(double)v);
+    return 1.0f / (1.0f + e);
+}
+__device__ __forceinline__ float act_exact(int act, float v) {
+    if (act == ACT_SIGMOID) return sigmoid_exact(v);
+    if (act == ACT_RELU) return v > 0.0f ? v : 0.0f;
+    return v;
+}
+
+template <int KH, int KW, int KQ>
+__global__ void __launch_bounds__(128) convx_fwd_kernel(const ConvXParams p) {
+    constexpr int KG = 4 * KQ;
+    constexpr int NX = (KW + 2) / 2;  // float2 loads per halo row segment (KW + 1 values, rounded up)
+    extern __shared__ float4 smx[];
+    float4* ws = smx;                                                // [C][KH][KW][KQ] float4
+    float* hs = reinterpret_cast<float*>(smx + p.C * KH * KW * KQ);  // [C][HR][PWp]
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int kg0 = blockIdx.y * KG;
+    const int per = p.tiles_x * p.tiles_y;
+    const int b = blockIdx.x / per, rem = blockIdx.x - b * per;
+    const int ty = rem / p.tiles_x, tx = rem - ty * p.tiles_x;
+    const int y0 = ty * p.TR, x0 = tx * p.TW;
+    pdl_wait();  // weights and input are written by earlier kernels of the step
+    {
+        float* wsf = reinterpret_cast<float*>(ws);
+        const int n = p.C * KH * KW * KG;
+        for (int i = tid; i < n; i += nt) {
+            const int k = i % KG, r = i / KG;  // r = c * KH * KW + tap
+            const int kk = kg0 + k;
+            wsf[i] = kk < p.K ? __ldg(p.wk + (long long)kk * p.C * KH * KW + r) : 0.0f;
+        }
+        // halo rows [y0 - pad, + HR) x cols [x0 - pad, + PW): one float4 (channel quad) per thread step,
+        // consecutive threads on consecutive columns (coalesced), zeros outside the map (padding)
+        const int ys = y0 - p.pad, xs = x0 - p.pad;
+        const int m = p.HR * p.G * p.PW;
+        const float* xb = p.x + (long long)b * p.x_bstride;
+        for (int i = tid; i < m; i += nt) {
+            const int row = i / (p.G * p.PW), r2 = i - row * (p.G * p.PW);
+            const int q = r2 / p.PW, col = r2 - q * p.PW;
+            const int iy = ys + row, ix = xs + col;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if ((unsigned)iy < (unsigned)p.Hin && (unsigned)ix < (unsigned)p.Win)
+                v = __ldg(reinterpret_cast<const float4*>(xb + (((long long)iy * p.G + q) * p.Win + ix) * 4));
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (4 * q + j < p.C) hs[((4 * q + j) * p.HR + row) * p.PWp + col] = vv[j];
+        }
+    }
+    __syncthreads();
+    pdl_trigger();
+    const int wpr = p.TW / 2;  // windows per tile row
+    const int wy = tid / wpr, wx = tid - wy * wpr;
+    const int oy = y0 + 2 * wy, ox = x0 + 2 * wx;
+    if (wy >= p.TR / 2 || oy >= p.OH || ox >= p.OW) return;
+    float acc[4][KG];
+#pragma unroll
+    for (int o = 0; o < 4; ++o)
+#pragma unroll
+        for (int k = 0; k < KG; ++k) acc[o][k] = 0.0f;
+    const float* hbase = hs + (2 * wy) * p.PWp + 2 * wx;
+    const int plane = p.HR * p.PWp;
+    for (int c = 0; c < p.C; ++c) {
+        const float* hc = hbase + c * plane;
+        float ra[2 * NX], rb[2 * NX];
+#pragma unroll
+        for (int j = 0; j < NX; ++j) {
+            const float2 t = *reinterpret_cast<const float2*>(hc + 2 * j);
+            ra[2 * j] = t.x, ra[2 * j + 1] = t.y;
+        }
+        const float4* wc = ws + c * KH * KW * KQ;
+#pragma unroll
+        for (int di = 0; di < KH; ++di) {
+#pragma unroll
+            for (int j = 0; j < NX; ++j) {
+                const float2 t = *reinterpret_cast<const float2*>(hc + (di + 1) * p.PWp + 2 * j);
+                rb[2 * j] = t.x, rb[2 * j + 1] = t.y;
+            }
+#pragma unroll
+            for (int dj = 0; dj < KW; ++dj) {
+                float w[KG];
+#pragma unroll
+                for (int q = 0; q < KQ; ++q) {
+                    const float4 t = wc[(di * KW + dj) * KQ + q];
+                    w[4 * q] = t.x, w[4 * q + 1] = t.y, w[4 * q + 2] = t.z, w[4 * q + 3] = t.w;
+                }
+                // acc = fma(ker, x, acc): the reference's chain order (c, di, dj), conv.hpp:62-89
+#pragma unroll
+                for (int k = 0; k < KG; ++k) {
+                    acc[0][k] = fmaf(w[k], ra[dj], acc[0][k]);
+                    acc[1][k] = fmaf(w[k], ra[dj + 1], acc[1][k]);
+                    acc[2][k] = fmaf(w[k], rb[dj], acc[2][k]);
+                    acc[3][k] = fmaf(w[k], rb[dj + 1], acc[3][k]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 2 * NX; ++j) ra[j] = rb[j];
+        }
+    }
+    // + bias (its own rounding, layers.hpp:138-146), activation, then the pool or the plain store
+    const int Kq = (p.out.C + 3) >> 2;
+    float* ob = p.out.p + (long long)b * p.out.bstride;
+    if (p.pool) {
+        const int py = oy >> 1, px = ox >> 1;
+#pragma unroll
+        for (int q = 0; q < KQ; ++q) {
+            const int gq = (kg0 >> 2) + q;
+            if (gq >= Kq) break;
+            float o4[4];
+            uint32_t cw = 0;
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const int k = 4 * q + jj, kk = kg0 + k;
+                float best = 0.0f;
+                uint32_t code = 0;
+                if (kk < p.K) {
+                    const float bb = __ldg(p.bias + kk);
+                    // window order (0,0) (0,1) (1,0) (1,1), the first maximum wins (layers.hpp:228-232)
+                    best = act_exact(p.act, acc[0][k] + bb);
+#pragma unroll
+                    for (int o = 1; o < 4; ++o) {
+                        const float a = act_exact(p.act, acc[o][k] + bb);
+                        if (a > best) best = a, code = (uint32_t)o;
+                    }
+                }
+                o4[jj] = best;
+                cw |= code << (8 * jj);
+            }
+            if (p.out.blocked) {
+                *reinterpret_cast<float4*>(ob + (((long long)py * Kq + gq) * p.out.W + px) * 4) =
+                    make_float4(o4[0], o4[1], o4[2], o4[3]);
+            } else {
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj)
+                    if (4 * gq + jj < p.out.C) ob[((long long)(4 * gq + jj) * p.out.H + py) * p.out.W + px] = o4[jj];
+            }
+            *reinterpret_cast<uint32_t*>(p.codes + (long long)b * p.codes_bstride +
+                                         (((long long)py * Kq + gq) * p.codes_pw + px) * 4) = cw;
+        }
+    } else {
+#pragma unroll
+        for (int o = 0; o < 4; ++o) {
+            const int y = oy + (o >> 1), x = ox + (o & 1);
+            if (y >= p.OH || x >= p.OW) continue;
+#pragma unroll
+            for (int q = 0; q < KQ; ++q) {
+                const int gq = (kg0 >> 2) + q;
+                if (gq >= Kq) break;
+                float o4[4];
+#pragma unroll
+                for (int jj = 0; jj < 4; ++jj) {
+                    const int kk = kg0 + 4 * q + jj;
+                    o4[jj] = kk < p.K ? act_exact(p.act, acc[o][4 * q + jj] + __ldg(p.bias + kk)) : 0.0f;
+                }
+                if (p.out.blocked) {
+                    *reinterpret_cast<float4*>(ob + (((long long)y * Kq + gq) * p.out.W + x) * 4) =
+                        make_float4(o4[0], o4[1], o4[2], o4[3]);
+                } else {
+#pragma unroll
+                    for (int jj = 0; jj < 4; ++jj)
+                        if (4 * gq + jj < p.out.C) ob[((long long)(4 * gq + jj) * p.out.H + y) * p.out.W + x] = o4[jj];
+                }
+            }
+        }
+    }
+}
+
+struct ConvXLaunch {
+    ConvXParams p;
+    int kq = 4, groups = 1, threads = 128, smem = 0;
+    double flops = 0, bytes = 0;
+    void run(cudaStream_t st) const;
+};
+
+// the exact forward over a blocked input; output / codes / act / pool / weights filled by the caller
+inline ConvXLaunch plan_convx_fwd(int B, int C, int Hin, int Win, int kh, int kw, int pad, int K) {
+    if (!((kh == 3 && kw == 3) || (kh == 5 && kw == 5)))
+        throw Error(B2N_ESHAPE, "b200nn conv: the exact forward covers 3x3 and 5x5 filters");
+    ConvXLaunch L;
+    ConvXParams& p = L.p;
+    std::memset(&p, 0, sizeof(p));
+    p.B = B;
+    p.C = C;
+    p.G = (C + 3) / 4;
+    p.Hin = Hin;
+    p.Win = Win;
+    p.kh = kh;
+    p.kw = kw;
+    p.pad = pad;
+    p.OH = Hin + 2 * pad - kh + 1;
+    p.OW = Win + 2 * pad - kw + 1;
+    p.K = K;
+    L.kq = K <= 8 ? 2 : K <= 12 ? 3 : 4;
+    L.groups = (K + 4 * L.kq - 1) / (4 * L.kq);
+    auto even = [](int n) { return (n + 1) & ~1; };
+    p.TW = std::min(32, even(p.OW));
+    p.TR = std::min(16, even(p.OH));
+    while ((p.TR / 2) * (p.TW / 2) > 128) p.TR -= 2;
+    L.threads = std::max(32, ((p.TR / 2) * (p.TW / 2) + 31) / 32 * 32);
+    p.HR = p.TR + kh;  // the rolling row pair reads one row past the last filter row
+    p.PW = p.TW + kw - 1;
+    p.PWp = (p.PW + 2) & ~1;  // float2 loads: even pitch, and room for the (KW + 1)-th column of the last window
+    p.tiles_x = (p.OW + p.TW - 1) / p.TW;
+    p.tiles_y = (p.OH + p.TR - 1) / p.TR;
+    L.smem = C * kh * kw * 4 * L.kq * 16 + C * p.HR * p.PWp * 4;
+    if (L.smem > 227 * 1024) throw Error(B2N_ESHAPE, "b200nn conv: exact-forward tile does not fit shared memory");
+    L.flops = 2.0 * B * p.OH * p.OW * K * (double)C * kh * kw;
+    return L;
+}
+
+void launch_convx_fwd(const ConvXLaunch& L, cudaStream_t st);
+inline void ConvXLaunch::run(cudaStream_t st) const { launch_convx_fwd(*this, st); }
+
+#ifdef B2N_CONVX_INSTANTIATE
+template <int KH, int KW, int KQ>
+inline void launch_convx_inst(const ConvXLaunch& L, cudaStream_t st) {
+    auto k = convx_fwd_kernel<KH, KW, KQ>;
+    static bool attr = false;
+    if (!attr) {
+        B2N_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+        attr = true;
+    }
+    const int ntiles = L.p.B * L.p.tiles_x * L.p.tiles_y;
+    launch_ex(k, dim3(ntiles, L.groups), dim3(L.threads), (size_t)L.smem, st, 1u, L.p);
+}
+void launch_convx_fwd(const ConvXLaunch& L, cudaStream_t st) {
+    if (L.p.kh == 3) {
+        if (L.kq == 2) launch_convx_inst<3, 3, 2>(L, st);
+        else if (L.kq == 3) launch_convx_inst<3, 3, 3>(L, st);
+        else launch_convx_inst<3, 3, 4>(L, st);
+    } else {
+        if (L.kq == 2) launch_convx_inst<5, 5, 2>(L, st);
+        else if (L.kq == 3) launch_convx_inst<5, 5, 3>(L, st);
+        else launch_convx_inst<5, 5, 4>(L, st);
+    }
+}
+#endif
+
+}  // namespace b2n

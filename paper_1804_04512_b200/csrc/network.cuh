@@ -24,7 +24,7 @@
 
 #include "conv.cuh"
 #include "checkpoint.cuh"
-#include "convt.cuh"
+#include "convx.cuh"
 #include "nccl_dyn.cuh"
 #include "runtime.cuh"
 
@@ -255,6 +255,8 @@ class Net {
     const ParamView& param(int i) const { return params_.at(i); }
     void get_param(int idx, int which, float* host);
     void set_param(int idx, int which, const float* host);
+    long long num_layers() const { return (long long)layers_.size(); }
+    void layer_output(int li, long long batch, float* host, uint8_t* codes_host);
     void set_hparams(float lr, float mom, float wd) {
         lr_ = lr;
         mom_ = mom;
@@ -358,6 +360,7 @@ class Net {
     std::unique_ptr<DpComm> dp_;
     DevMem loss_sum_;  // dp: double partial loss
     bool tconv_ = false;     // conv layers on the halo-tile kernels (convt.cuh) instead of conv.cuh
+    bool conv_fwd_tc_ = false;  // conv forward on the tensor cores (convt FWD) instead of the exact convx
     DevMem ds_x_, ds_y_, ds_order_, fit_state_;  // device-resident dataset, order, cursor / sums
     long long ds_n_ = 0;
     unsigned seed_ = 0;
@@ -506,6 +509,8 @@ inline Net::Net(const b2n_network_spec& spec, int device, int precision)
     {  // the halo-tile conv kernels cover 3x3 / 5x5 filters with <= 32 channels and kernels
         const char* e = std::getenv("B2N_CONV_LEGACY");
         tconv_ = !(e && e[0] == '1');
+        const char* f = std::getenv("B2N_CONV_FWD");
+        conv_fwd_tc_ = f && std::string(f) == "tc";
         auto nk = [](int n) { return n <= 8 ? 8 : n <= 16 ? 16 : 32; };
         for (const Layer& L : layers_) {
             if (L.kind != B2N_CONV) continue;
@@ -782,8 +787,25 @@ inline void Net::build_plan(Plan& pl) {
                 const double outn = (double)B * numel(L.out_shape);
                 f.bytes = (double)B * g.c * g.h * g.w * 4 + outn * (L.pool_after ? 5 : 4) + (double)g.k * (g.c * g.kh * g.kw + 1) * 4;
                 f.flops = 2.0 * B * g.oh * g.ow * g.k * (double)g.c * g.kh * g.kw;
-                tfwd[i] = f;
-                fwd.push_back(Op([f](cudaStream_t s) { f.run(s); }, "conv" + std::to_string(i) + ".fwd", f.flops, f.bytes));
+                tfwd[i] = f;  // its tiles and input map also plan the weight gradient
+                if (conv_fwd_tc_) {  // 3xTF32 tensor-core forward (B2N_CONV_FWD=tc), near-tie fix-up
+                    if (!std::getenv("B2N_CT_NOFIX")) convt_enable_fix(f, f.fix);
+                    fwd.push_back(Op([f](cudaStream_t s) { f.run(s); }, "conv" + std::to_string(i) + ".fwd", f.flops, f.bytes));
+                } else {  // the reference's own fma chains: bit-identical activations and pool decisions
+                    ConvXLaunch xf = plan_convx_fwd(B, g.c, g.h, g.w, g.kh, g.kw, g.pad, g.k);
+                    xf.p.x = in;
+                    xf.p.x_bstride = in_bs;
+                    xf.p.wk = P + L.kern_off;
+                    xf.p.bias = P + L.bias_off;
+                    xf.p.act = L.act;
+                    xf.p.pool = L.pool_after ? 1 : 0;
+                    xf.p.out = out_layout(L, L.Aout, L.ld_out);
+                    xf.p.codes = L.arg;
+                    xf.p.codes_bstride = L.codes_bstride;
+                    xf.p.codes_pw = L.codes_pw;
+                    xf.bytes = f.bytes;
+                    fwd.push_back(Op([xf](cudaStream_t s) { xf.run(s); }, "conv" + std::to_string(i) + ".fwd", xf.flops, xf.bytes));
+                }
                 ++nk_fwd;
                 continue;
             }
@@ -1515,6 +1537,44 @@ inline void Net::set_param(int idx, int which, const float* host) {
     B2N_CUDA(cudaMemcpy2DAsync(base, v.pitch * 4, host, v.cols * 4, v.cols * 4, v.rows, cudaMemcpyHostToDevice,
                                stream_));
     B2N_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// The last forward's output of fused layer li (act + pool applied) for `batch` rows, NCHW per row
+// (conv) or [batch][out] (dense), plus the pool argmax codes (window order (0,0) (0,1) (1,0) (1,1)) in
+// the same NCHW order -- per-layer forward parity against the reference's conv_forward / pool_forward.
+inline void Net::layer_output(int li, long long batch, float* host, uint8_t* codes_host) {
+    if (li < 0 || li >= (int)layers_.size()) throw Error(B2N_EBOUNDS, "layer index out of range");
+    if (batch < 1 || batch > cap_) throw Error(B2N_EBOUNDS, "batch exceeds the staged capacity");
+    const Layer& L = layers_[li];
+    B2N_CUDA(cudaStreamSynchronize(stream_));
+    if (!L.Aout) throw Error(B2N_EPARAM, "the last layer keeps no activation buffer (use forward_batch)");
+    if (L.kind == B2N_DENSE) {
+        B2N_CUDA(cudaMemcpy2D(host, L.out * 4, L.Aout, L.ld_out * 4, L.out * 4, batch, cudaMemcpyDeviceToHost));
+        return;
+    }
+    const long long k = L.out_shape[0], oh = L.out_shape[1], ow = L.out_shape[2], per = k * oh * ow;
+    const long long kq = (k + 3) / 4;
+    std::vector<float> raw((size_t)(batch * L.ld_out));
+    B2N_CUDA(cudaMemcpy(raw.data(), L.Aout, raw.size() * 4, cudaMemcpyDeviceToHost));
+    for (long long b = 0; b < batch; ++b)
+        for (long long c = 0; c < k; ++c)
+            for (long long y = 0; y < oh; ++y)
+                for (long long x = 0; x < ow; ++x)
+                    host[((b * k + c) * oh + y) * ow + x] =
+                        L.blocked_out ? raw[(size_t)(b * L.ld_out + ((y * kq + c / 4) * ow + x) * 4 + c % 4)]
+                                      : raw[(size_t)(b * L.ld_out + (c * oh + y) * ow + x)];
+    if (codes_host && L.pool_after && L.arg) {
+        std::vector<uint8_t> cr((size_t)(batch * L.codes_bstride));
+        B2N_CUDA(cudaMemcpy(cr.data(), L.arg, cr.size(), cudaMemcpyDeviceToHost));
+        for (long long b = 0; b < batch; ++b)
+            for (long long c = 0; c < k; ++c)
+                for (long long y = 0; y < oh; ++y)
+                    for (long long x = 0; x < ow; ++x)
+                        codes_host[((b * k + c) * oh + y) * ow + x] =
+                            tconv_ ? cr[(size_t)(b * L.codes_bstride + ((y * kq + c / 4) * L.codes_pw + x) * 4 + c % 4)]
+                                   : cr[(size_t)(b * L.codes_bstride + (c * oh + y) * ow + x)];
+    }
+    (void)per;
 }
 
 }  // namespace b2n

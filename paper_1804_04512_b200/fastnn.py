@@ -178,6 +178,14 @@ class Network:
     def set_hparams(self, lr: float, momentum: float, weight_decay: float = 0.0) -> None:
         _lib.call("b2n_net_set_hparams", self._h, lr, momentum, weight_decay)
 
+    # ---- inspection
+    def layer_output(self, layer: int, batch: int, shape) -> tuple[np.ndarray, np.ndarray]:
+        """(output, pool codes) of fused layer `layer` from the last forward, NCHW per row."""
+        out = np.zeros([batch] + list(shape), np.float32)
+        codes = np.zeros(out.shape, np.uint8)
+        _lib.call("b2n_net_layer_output", self._h, layer, batch, _f(out), codes.ctypes.data_as(C.POINTER(C.c_ubyte)))
+        return out, codes
+
     # ---- data-parallel pieces
     def forward_backward(self, x, labels, batch_global: int | None = None) -> float:
         x = np.ascontiguousarray(x, np.float32)
