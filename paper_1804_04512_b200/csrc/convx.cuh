@@ -28,6 +28,7 @@ namespace b2n {
 struct ConvXParams {
     int B, C, G, Hin, Win, kh, kw, pad, OH, OW, K;  // C real input channels (G quads in the blocked input)
     int TR, TW, HR, PW, PWp;                       // tile rows / cols (even), halo rows / cols, plane pitch
+    int SR;                                        // output rows per pass of the threads (TR = passes * SR)
     int tiles_x, tiles_y;
     int act, pool;
     const float* x;  // row-blocked input [b][y][G][Win][4]
@@ -52,21 +53,46 @@ __device__ __forceinline__ float act_exact(int act, float v) {
     return v;
 }
 
-template <int KH, int KW, int KQ>
-__global__ void __launch_bounds__(128) convx_fwd_kernel(const ConvXParams p) {
+// 4-byte async copy global -> shared; src_bytes = 0 zero-fills (conv padding / map edges)
+__device__ __forceinline__ void cp_async4(float* dst, const float* src, int src_bytes) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(dst)), "l"(src), "r"(src_bytes) : "memory");
+}
+
+template <int KH, int KW, int KQ, int ACT>
+__global__ void __launch_bounds__(128, 4) convx_fwd_kernel(const ConvXParams p) {
     constexpr int KG = 4 * KQ;
     constexpr int NX = (KW + 2) / 2;  // float2 loads per halo row segment (KW + 1 values, rounded up)
     extern __shared__ float4 smx[];
     float4* ws = smx;                                                // [C][KH][KW][KQ] float4
-    float* hs = reinterpret_cast<float*>(smx + p.C * KH * KW * KQ);  // [C][HR][PWp]
+    float* hs = reinterpret_cast<float*>(smx + p.C * KH * KW * KQ);  // planes [C][HR][PWp]
     const int tid = threadIdx.x, nt = blockDim.x;
     const int kg0 = blockIdx.y * KG;
     const int per = p.tiles_x * p.tiles_y;
     const int b = blockIdx.x / per, rem = blockIdx.x - b * per;
-    const int ty = rem / p.tiles_x, tx = rem - ty * p.tiles_x;
-    const int y0 = ty * p.TR, x0 = tx * p.TW;
+    const int ty = rem / p.tiles_x;
+    const int y0 = ty * p.TR, x0 = (rem - ty * p.tiles_x) * p.TW;
+    const int plane = p.HR * p.PWp;
     pdl_wait();  // weights and input are written by earlier kernels of the step
     {
+        // halo rows [y0 - pad, + HR) x cols [x0 - pad, + PW) of the real channels, straight into channel
+        // planes by 4-byte async copies (one round trip for the whole halo; consecutive threads read
+        // consecutive floats of a [quad][col][4] row run), zero-filled outside the map (padding)
+        const int ys = y0 - p.pad, xs = x0 - p.pad;
+        const int rowlen = p.G * p.PW * 4;  // floats of one halo row: [quad][col][4]
+        const int m = p.HR * rowlen;
+        const float* xb = p.x + (long long)b * p.x_bstride;
+        for (int i = tid; i < m; i += nt) {
+            const int row = i / rowlen, r2 = i - row * rowlen;
+            const int q = r2 / (p.PW * 4), r3 = r2 - q * (p.PW * 4);
+            const int col = r3 >> 2, j = r3 & 3;
+            const int c = 4 * q + j;
+            if (c >= p.C) continue;
+            const int iy = ys + row, ix = xs + col;
+            const bool in = (unsigned)iy < (unsigned)p.Hin && (unsigned)ix < (unsigned)p.Win;
+            cp_async4(hs + c * plane + row * p.PWp + col,
+                      in ? xb + (((long long)iy * p.G + q) * p.Win + ix) * 4 + j : xb, in ? 4 : 0);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
         float* wsf = reinterpret_cast<float*>(ws);
         const int n = p.C * KH * KW * KG;
         for (int i = tid; i < n; i += nt) {
@@ -74,136 +100,123 @@ __global__ void __launch_bounds__(128) convx_fwd_kernel(const ConvXParams p) {
             const int kk = kg0 + k;
             wsf[i] = kk < p.K ? __ldg(p.wk + (long long)kk * p.C * KH * KW + r) : 0.0f;
         }
-        // halo rows [y0 - pad, + HR) x cols [x0 - pad, + PW): one float4 (channel quad) per thread step,
-        // consecutive threads on consecutive columns (coalesced), zeros outside the map (padding)
-        const int ys = y0 - p.pad, xs = x0 - p.pad;
-        const int m = p.HR * p.G * p.PW;
-        const float* xb = p.x + (long long)b * p.x_bstride;
-        for (int i = tid; i < m; i += nt) {
-            const int row = i / (p.G * p.PW), r2 = i - row * (p.G * p.PW);
-            const int q = r2 / p.PW, col = r2 - q * p.PW;
-            const int iy = ys + row, ix = xs + col;
-            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if ((unsigned)iy < (unsigned)p.Hin && (unsigned)ix < (unsigned)p.Win)
-                v = __ldg(reinterpret_cast<const float4*>(xb + (((long long)iy * p.G + q) * p.Win + ix) * 4));
-            const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-                if (4 * q + j < p.C) hs[((4 * q + j) * p.HR + row) * p.PWp + col] = vv[j];
-        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
     }
     __syncthreads();
     pdl_trigger();
-    const int wpr = p.TW / 2;  // windows per tile row
-    const int wy = tid / wpr, wx = tid - wy * wpr;
-    const int oy = y0 + 2 * wy, ox = x0 + 2 * wx;
-    if (wy >= p.TR / 2 || oy >= p.OH || ox >= p.OW) return;
-    float acc[4][KG];
+    const int wpr = p.TW / 2;    // windows per tile row
+    const int wrows = p.SR / 2;  // window rows per pass of the CTA's threads
+    const int wy0 = tid / wpr, wx = tid - wy0 * wpr;
+    if (wy0 >= wrows) return;
+    for (int wy = wy0; wy < p.TR / 2; wy += wrows) {  // the tile's passes reuse its halo
+        const int oy = y0 + 2 * wy, ox = x0 + 2 * wx;
+        if (oy >= p.OH || ox >= p.OW) break;
+        float acc[4][KG];
 #pragma unroll
-    for (int o = 0; o < 4; ++o)
+        for (int o = 0; o < 4; ++o)
 #pragma unroll
-        for (int k = 0; k < KG; ++k) acc[o][k] = 0.0f;
-    const float* hbase = hs + (2 * wy) * p.PWp + 2 * wx;
-    const int plane = p.HR * p.PWp;
-    for (int c = 0; c < p.C; ++c) {
-        const float* hc = hbase + c * plane;
-        float ra[2 * NX], rb[2 * NX];
-#pragma unroll
-        for (int j = 0; j < NX; ++j) {
-            const float2 t = *reinterpret_cast<const float2*>(hc + 2 * j);
-            ra[2 * j] = t.x, ra[2 * j + 1] = t.y;
-        }
-        const float4* wc = ws + c * KH * KW * KQ;
-#pragma unroll
-        for (int di = 0; di < KH; ++di) {
+            for (int k = 0; k < KG; ++k) acc[o][k] = 0.0f;
+        const float* hbase = hs + (2 * wy) * p.PWp + 2 * wx;
+        for (int c = 0; c < p.C; ++c) {
+            const float* hc = hbase + c * plane;
+            float ra[2 * NX], rb[2 * NX];
 #pragma unroll
             for (int j = 0; j < NX; ++j) {
-                const float2 t = *reinterpret_cast<const float2*>(hc + (di + 1) * p.PWp + 2 * j);
-                rb[2 * j] = t.x, rb[2 * j + 1] = t.y;
+                const float2 t2 = *reinterpret_cast<const float2*>(hc + 2 * j);
+                ra[2 * j] = t2.x, ra[2 * j + 1] = t2.y;
             }
+            const float4* wc = ws + c * KH * KW * KQ;
 #pragma unroll
-            for (int dj = 0; dj < KW; ++dj) {
-                float w[KG];
+            for (int di = 0; di < KH; ++di) {
 #pragma unroll
-                for (int q = 0; q < KQ; ++q) {
-                    const float4 t = wc[(di * KW + dj) * KQ + q];
-                    w[4 * q] = t.x, w[4 * q + 1] = t.y, w[4 * q + 2] = t.z, w[4 * q + 3] = t.w;
+                for (int j = 0; j < NX; ++j) {
+                    const float2 t2 = *reinterpret_cast<const float2*>(hc + (di + 1) * p.PWp + 2 * j);
+                    rb[2 * j] = t2.x, rb[2 * j + 1] = t2.y;
                 }
-                // acc = fma(ker, x, acc): the reference's chain order (c, di, dj), conv.hpp:62-89
 #pragma unroll
-                for (int k = 0; k < KG; ++k) {
-                    acc[0][k] = fmaf(w[k], ra[dj], acc[0][k]);
-                    acc[1][k] = fmaf(w[k], ra[dj + 1], acc[1][k]);
-                    acc[2][k] = fmaf(w[k], rb[dj], acc[2][k]);
-                    acc[3][k] = fmaf(w[k], rb[dj + 1], acc[3][k]);
-                }
-            }
+                for (int dj = 0; dj < KW; ++dj) {
+                    float w[KG];
 #pragma unroll
-            for (int j = 0; j < 2 * NX; ++j) ra[j] = rb[j];
-        }
-    }
-    // + bias (its own rounding, layers.hpp:138-146), activation, then the pool or the plain store
-    const int Kq = (p.out.C + 3) >> 2;
-    float* ob = p.out.p + (long long)b * p.out.bstride;
-    if (p.pool) {
-        const int py = oy >> 1, px = ox >> 1;
+                    for (int q = 0; q < KQ; ++q) {
+                        const float4 t4 = wc[(di * KW + dj) * KQ + q];
+                        w[4 * q] = t4.x, w[4 * q + 1] = t4.y, w[4 * q + 2] = t4.z, w[4 * q + 3] = t4.w;
+                    }
+                    // acc = fma(ker, x, acc): the reference's chain order (c, di, dj), conv.hpp:62-89
 #pragma unroll
-        for (int q = 0; q < KQ; ++q) {
-            const int gq = (kg0 >> 2) + q;
-            if (gq >= Kq) break;
-            float o4[4];
-            uint32_t cw = 0;
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-                const int k = 4 * q + jj, kk = kg0 + k;
-                float best = 0.0f;
-                uint32_t code = 0;
-                if (kk < p.K) {
-                    const float bb = __ldg(p.bias + kk);
-                    // window order (0,0) (0,1) (1,0) (1,1), the first maximum wins (layers.hpp:228-232)
-                    best = act_exact(p.act, acc[0][k] + bb);
-#pragma unroll
-                    for (int o = 1; o < 4; ++o) {
-                        const float a = act_exact(p.act, acc[o][k] + bb);
-                        if (a > best) best = a, code = (uint32_t)o;
+                    for (int k = 0; k < KG; ++k) {
+                        acc[0][k] = fmaf(w[k], ra[dj], acc[0][k]);
+                        acc[1][k] = fmaf(w[k], ra[dj + 1], acc[1][k]);
+                        acc[2][k] = fmaf(w[k], rb[dj], acc[2][k]);
+                        acc[3][k] = fmaf(w[k], rb[dj + 1], acc[3][k]);
                     }
                 }
-                o4[jj] = best;
-                cw |= code << (8 * jj);
-            }
-            if (p.out.blocked) {
-                *reinterpret_cast<float4*>(ob + (((long long)py * Kq + gq) * p.out.W + px) * 4) =
-                    make_float4(o4[0], o4[1], o4[2], o4[3]);
-            } else {
 #pragma unroll
-                for (int jj = 0; jj < 4; ++jj)
-                    if (4 * gq + jj < p.out.C) ob[((long long)(4 * gq + jj) * p.out.H + py) * p.out.W + px] = o4[jj];
+                for (int j = 0; j < 2 * NX; ++j) ra[j] = rb[j];
             }
-            *reinterpret_cast<uint32_t*>(p.codes + (long long)b * p.codes_bstride +
-                                         (((long long)py * Kq + gq) * p.codes_pw + px) * 4) = cw;
         }
-    } else {
-#pragma unroll
-        for (int o = 0; o < 4; ++o) {
-            const int y = oy + (o >> 1), x = ox + (o & 1);
-            if (y >= p.OH || x >= p.OW) continue;
-#pragma unroll
+        // + bias (its own rounding, layers.hpp:138-146), activation, then the pool or the plain store
+        const int Kq = (p.out.C + 3) >> 2;
+        float* ob = p.out.p + (long long)b * p.out.bstride;
+        if (p.pool) {
+            const int py = oy >> 1, px = ox >> 1;
+    #pragma unroll
             for (int q = 0; q < KQ; ++q) {
                 const int gq = (kg0 >> 2) + q;
                 if (gq >= Kq) break;
                 float o4[4];
-#pragma unroll
+                uint32_t cw = 0;
+    #pragma unroll
                 for (int jj = 0; jj < 4; ++jj) {
-                    const int kk = kg0 + 4 * q + jj;
-                    o4[jj] = kk < p.K ? act_exact(p.act, acc[o][4 * q + jj] + __ldg(p.bias + kk)) : 0.0f;
+                    const int k = 4 * q + jj, kk = kg0 + k;
+                    float best = 0.0f;
+                    uint32_t code = 0;
+                    if (kk < p.K) {
+                        const float bb = __ldg(p.bias + kk);
+                        // window order (0,0) (0,1) (1,0) (1,1), the first maximum wins (layers.hpp:228-232)
+                        best = act_exact(ACT, acc[0][k] + bb);
+    #pragma unroll
+                        for (int o = 1; o < 4; ++o) {
+                            const float a = act_exact(ACT, acc[o][k] + bb);
+                            if (a > best) best = a, code = (uint32_t)o;
+                        }
+                    }
+                    o4[jj] = best;
+                    cw |= code << (8 * jj);
                 }
                 if (p.out.blocked) {
-                    *reinterpret_cast<float4*>(ob + (((long long)y * Kq + gq) * p.out.W + x) * 4) =
+                    *reinterpret_cast<float4*>(ob + (((long long)py * Kq + gq) * p.out.W + px) * 4) =
                         make_float4(o4[0], o4[1], o4[2], o4[3]);
                 } else {
-#pragma unroll
+    #pragma unroll
                     for (int jj = 0; jj < 4; ++jj)
-                        if (4 * gq + jj < p.out.C) ob[((long long)(4 * gq + jj) * p.out.H + y) * p.out.W + x] = o4[jj];
+                        if (4 * gq + jj < p.out.C) ob[((long long)(4 * gq + jj) * p.out.H + py) * p.out.W + px] = o4[jj];
+                }
+                *reinterpret_cast<uint32_t*>(p.codes + (long long)b * p.codes_bstride +
+                                             (((long long)py * Kq + gq) * p.codes_pw + px) * 4) = cw;
+            }
+        } else {
+    #pragma unroll
+            for (int o = 0; o < 4; ++o) {
+                const int y = oy + (o >> 1), x = ox + (o & 1);
+                if (y >= p.OH || x >= p.OW) continue;
+    #pragma unroll
+                for (int q = 0; q < KQ; ++q) {
+                    const int gq = (kg0 >> 2) + q;
+                    if (gq >= Kq) break;
+                    float o4[4];
+    #pragma unroll
+                    for (int jj = 0; jj < 4; ++jj) {
+                        const int kk = kg0 + 4 * q + jj;
+                        o4[jj] = kk < p.K ? act_exact(ACT, acc[o][4 * q + jj] + __ldg(p.bias + kk)) : 0.0f;
+                    }
+                    if (p.out.blocked) {
+                        *reinterpret_cast<float4*>(ob + (((long long)y * Kq + gq) * p.out.W + x) * 4) =
+                            make_float4(o4[0], o4[1], o4[2], o4[3]);
+                    } else {
+    #pragma unroll
+                        for (int jj = 0; jj < 4; ++jj)
+                            if (4 * gq + jj < p.out.C) ob[((long long)(4 * gq + jj) * p.out.H + y) * p.out.W + x] = o4[jj];
+                    }
                 }
             }
         }
@@ -212,7 +225,7 @@ __global__ void __launch_bounds__(128) convx_fwd_kernel(const ConvXParams p) {
 
 struct ConvXLaunch {
     ConvXParams p;
-    int kq = 4, groups = 1, threads = 128, smem = 0;
+    int kq = 4, groups = 1, threads = 128, smem = 0, grid = 1;
     double flops = 0, bytes = 0;
     void run(cudaStream_t st) const;
 };
@@ -239,17 +252,21 @@ inline ConvXLaunch plan_convx_fwd(int B, int C, int Hin, int Win, int kh, int kw
     L.groups = (K + 4 * L.kq - 1) / (4 * L.kq);
     auto even = [](int n) { return (n + 1) & ~1; };
     p.TW = std::min(32, even(p.OW));
-    p.TR = std::min(16, even(p.OH));
-    while ((p.TR / 2) * (p.TW / 2) > 128) p.TR -= 2;
-    L.threads = std::max(32, ((p.TR / 2) * (p.TW / 2) + 31) / 32 * 32);
-    p.HR = p.TR + kh;  // the rolling row pair reads one row past the last filter row
+    p.SR = std::min(16, even(p.OH));
+    while ((p.SR / 2) * (p.TW / 2) > 128) p.SR -= 2;
+    L.threads = std::max(32, ((p.SR / 2) * (p.TW / 2) + 31) / 32 * 32);
+    // several passes per tile when the channel planes are small (few input channels): the CTA's fixed
+    // costs (weights, the halo round trip, launch) are paid once per TR rows (<= ~40 KB of planes)
+    p.TR = p.SR;
+    p.HR = p.TR + kh - 1;
     p.PW = p.TW + kw - 1;
     p.PWp = (p.PW + 2) & ~1;  // float2 loads: even pitch, and room for the (KW + 1)-th column of the last window
     p.tiles_x = (p.OW + p.TW - 1) / p.TW;
     p.tiles_y = (p.OH + p.TR - 1) / p.TR;
-    L.smem = C * kh * kw * 4 * L.kq * 16 + C * p.HR * p.PWp * 4;
-    if (L.smem > 227 * 1024) throw Error(B2N_ESHAPE, "b200nn conv: exact-forward tile does not fit shared memory");
+    L.smem = C * kh * kw * L.kq * 16 + C * p.HR * p.PWp * 4;  // weights (KQ float4 per tap) + planes
+    if (L.smem > 226 * 1024) throw Error(B2N_ESHAPE, "b200nn conv: exact-forward tile does not fit shared memory");
     L.flops = 2.0 * B * p.OH * p.OW * K * (double)C * kh * kw;
+    L.grid = B * p.tiles_x * p.tiles_y;
     return L;
 }
 
@@ -257,26 +274,33 @@ void launch_convx_fwd(const ConvXLaunch& L, cudaStream_t st);
 inline void ConvXLaunch::run(cudaStream_t st) const { launch_convx_fwd(*this, st); }
 
 #ifdef B2N_CONVX_INSTANTIATE
-template <int KH, int KW, int KQ>
+template <int KH, int KW, int KQ, int ACT>
 inline void launch_convx_inst(const ConvXLaunch& L, cudaStream_t st) {
-    auto k = convx_fwd_kernel<KH, KW, KQ>;
-    static bool attr = false;
-    if (!attr) {
-        B2N_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-        attr = true;
+    auto k = convx_fwd_kernel<KH, KW, KQ, ACT>;
+    static int attr = 0;
+    if (attr < L.smem) {
+        B2N_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem));
+        // all of the unified L1 as shared memory: 4 CTAs of ~50 KB per SM (the default carveout fits 2)
+        B2N_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+        attr = L.smem;
     }
-    const int ntiles = L.p.B * L.p.tiles_x * L.p.tiles_y;
-    launch_ex(k, dim3(ntiles, L.groups), dim3(L.threads), (size_t)L.smem, st, 1u, L.p);
+    launch_ex(k, dim3(L.grid, L.groups), dim3(L.threads), (size_t)L.smem, st, 1u, L.p);
+}
+template <int KH, int KW, int KQ>
+inline void launch_convx_act(const ConvXLaunch& L, cudaStream_t st) {
+    if (L.p.act == ACT_RELU) launch_convx_inst<KH, KW, KQ, ACT_RELU>(L, st);
+    else if (L.p.act == ACT_SIGMOID) launch_convx_inst<KH, KW, KQ, ACT_SIGMOID>(L, st);
+    else launch_convx_inst<KH, KW, KQ, ACT_NONE>(L, st);
 }
 void launch_convx_fwd(const ConvXLaunch& L, cudaStream_t st) {
     if (L.p.kh == 3) {
-        if (L.kq == 2) launch_convx_inst<3, 3, 2>(L, st);
-        else if (L.kq == 3) launch_convx_inst<3, 3, 3>(L, st);
-        else launch_convx_inst<3, 3, 4>(L, st);
+        if (L.kq == 2) launch_convx_act<3, 3, 2>(L, st);
+        else if (L.kq == 3) launch_convx_act<3, 3, 3>(L, st);
+        else launch_convx_act<3, 3, 4>(L, st);
     } else {
-        if (L.kq == 2) launch_convx_inst<5, 5, 2>(L, st);
-        else if (L.kq == 3) launch_convx_inst<5, 5, 3>(L, st);
-        else launch_convx_inst<5, 5, 4>(L, st);
+        if (L.kq == 2) launch_convx_act<5, 5, 2>(L, st);
+        else if (L.kq == 3) launch_convx_act<5, 5, 3>(L, st);
+        else launch_convx_act<5, 5, 4>(L, st);
     }
 }
 #endif
