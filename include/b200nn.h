@@ -198,6 +198,15 @@ int b2n_cd_k_update(b2n_rbm* rbm, const float* v0_host, long long batch, int k, 
 /* the chain states of the last update (h0 mean, h sample, v1 mean, h1 mean), batch-major */
 int b2n_rbm_last_states(b2n_rbm* rbm, float* h0, float* hs, float* v1, float* h1);
 int b2n_rbm_dp_init(b2n_rbm* rbm, const char id[128], int rank, int world);
+/* Data parallelism driven by the caller (no NCCL; e.g. a gloo / MPI allreduce): with grad_only on,
+ * b2n_cd_k_update(..., batch_global) leaves the parameters alone and keeps this shard's raw sums
+ * dW = h0^T v0 - h1^T v1, dbh = sum(h0 - h1), dbv = sum(v0 - v1) (energy.hpp:148-169 before the
+ * lr / batch scale); get_grad / set_grad move them (w: hidden x visible), apply_update adds
+ * lr / batch_global * (the summed sums) -- the same arithmetic the NCCL mode runs in its step. */
+int b2n_rbm_set_grad_only(b2n_rbm* rbm, int on);
+int b2n_rbm_get_grad(b2n_rbm* rbm, float* w_host, float* bv_host, float* bh_host);
+int b2n_rbm_set_grad(b2n_rbm* rbm, const float* w_host, const float* bv_host, const float* bh_host);
+int b2n_rbm_apply_update(b2n_rbm* rbm, float lr, long long batch_global);
 int b2n_rbm_stage(b2n_rbm* rbm, const float* v0_host, const double* uniforms_host, long long batch);
 int b2n_rbm_run_staged(b2n_rbm* rbm, int steps, float lr, long long batch_global);
 int b2n_rbm_recon(b2n_rbm* rbm, double* recon);

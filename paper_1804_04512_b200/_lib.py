@@ -137,6 +137,10 @@ _SIGS = {
     "b2n_rbm_stage": ([_VP, _F, _D, C.c_longlong], C.c_int),
     "b2n_rbm_run_staged": ([_VP, C.c_int, C.c_float, C.c_longlong], C.c_int),
     "b2n_rbm_recon": ([_VP, _D], C.c_int),
+    "b2n_rbm_set_grad_only": ([_VP, C.c_int], C.c_int),
+    "b2n_rbm_get_grad": ([_VP, _F, _F, _F], C.c_int),
+    "b2n_rbm_set_grad": ([_VP, _F, _F, _F], C.c_int),
+    "b2n_rbm_apply_update": ([_VP, C.c_float, C.c_longlong], C.c_int),
     "b2n_rbm_train_stream": ([_VP, _F, _D, C.c_longlong, C.c_longlong, C.c_float, _D], C.c_int),
     "b2n_rbm_stream": ([_VP, C.POINTER(_VP)], C.c_int),
     "b2n_crbm_create": ([C.c_int] * 6 + [C.c_int, C.c_int, C.POINTER(_VP)], C.c_int),

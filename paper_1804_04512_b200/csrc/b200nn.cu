@@ -313,6 +313,18 @@ int b2n_rbm_train_stream(b2n_rbm* r, const float* v0, const double* u, long long
                          double* recon_out) {
     return guard([&] { r->impl.train_stream(v0, u, steps, batch, lr, recon_out); });
 }
+int b2n_rbm_set_grad_only(b2n_rbm* r, int on) {
+    return guard([&] { r->impl.set_grad_only(on != 0); });
+}
+int b2n_rbm_get_grad(b2n_rbm* r, float* w, float* bv, float* bh) {
+    return guard([&] { r->impl.get_grad(w, bv, bh); });
+}
+int b2n_rbm_set_grad(b2n_rbm* r, const float* w, const float* bv, const float* bh) {
+    return guard([&] { r->impl.set_grad(w, bv, bh); });
+}
+int b2n_rbm_apply_update(b2n_rbm* r, float lr, long long batch_global) {
+    return guard([&] { r->impl.apply_update(lr, batch_global); });
+}
 int b2n_rbm_recon(b2n_rbm* r, double* recon) {
     return guard([&] { *recon = r->impl.recon(); });
 }

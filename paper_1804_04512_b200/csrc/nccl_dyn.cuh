@@ -5,6 +5,9 @@
 #include <dlfcn.h>
 #include <nccl.h>
 
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
 #include <string>
 
 #include "runtime.cuh"
@@ -17,6 +20,8 @@ struct NcclApi {
     ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*commGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+    ncclResult_t (*commAbort)(ncclComm_t) = nullptr;
     const char* (*errStr)(ncclResult_t) = nullptr;
 };
 
@@ -31,6 +36,8 @@ inline NcclApi& nccl() {
         a.allReduce = reinterpret_cast<decltype(a.allReduce)>(dlsym(h, "ncclAllReduce"));
         a.commDestroy = reinterpret_cast<decltype(a.commDestroy)>(dlsym(h, "ncclCommDestroy"));
         a.errStr = reinterpret_cast<decltype(a.errStr)>(dlsym(h, "ncclGetErrorString"));
+        a.commGetAsyncError = reinterpret_cast<decltype(a.commGetAsyncError)>(dlsym(h, "ncclCommGetAsyncError"));
+        a.commAbort = reinterpret_cast<decltype(a.commAbort)>(dlsym(h, "ncclCommAbort"));
         if (!a.getUniqueId || !a.commInitRank || !a.allReduce || !a.commDestroy)
             throw Error(B2N_ENCCL, "libnccl.so.2 lacks a required symbol");
         return a;
@@ -43,10 +50,15 @@ inline void nccl_check(ncclResult_t r, const char* what) {
         throw Error(B2N_ENCCL, std::string(what) + ": " + (nccl().errStr ? nccl().errStr(r) : "nccl error"));
 }
 
-// one communicator per replica (one process per GPU, rank = process rank)
-struct DpComm {
+// one communicator per replica (one process per GPU, rank = process rank). While the host waits on
+// a step (spin_sync) the communicator is polled: ncclCommGetAsyncError reporting an error, or a wait
+// longer than B2N_NCCL_TIMEOUT seconds (default 600), aborts it (ncclCommAbort releases the kernels
+// blocked in the collective) and throws B2N_ENCCL -- a dead peer fails the step instead of hanging it.
+struct DpComm : WaitWatch {
     ncclComm_t comm = nullptr;
     int rank = 0, world = 1;
+    double timeout_s = 600.0;
+    bool aborted = false;
     void init(const char id[128], int r, int w) {
         ncclUniqueId uid;
         static_assert(sizeof(uid.internal) == 128, "ncclUniqueId size");
@@ -54,8 +66,24 @@ struct DpComm {
         nccl_check(nccl().commInitRank(&comm, w, uid, r), "ncclCommInitRank");
         rank = r;
         world = w;
+        if (const char* e = std::getenv("B2N_NCCL_TIMEOUT")) timeout_s = std::atof(e);
+        wait_watches().push_back(this);
+    }
+    void poll(double waited_s) override {
+        if (!comm || aborted) return;
+        ncclResult_t st = ncclSuccess;
+        if (nccl().commGetAsyncError && nccl().commGetAsyncError(comm, &st) != ncclSuccess) st = ncclSystemError;
+        const bool err = st != ncclSuccess && st != ncclInProgress;
+        if (!err && !(timeout_s > 0 && waited_s > timeout_s)) return;
+        if (nccl().commAbort) nccl().commAbort(comm);
+        aborted = true;
+        comm = nullptr;
+        throw Error(B2N_ENCCL, err ? std::string("NCCL asynchronous error: ") + (nccl().errStr ? nccl().errStr(st) : "?")
+                                   : "NCCL collective exceeded B2N_NCCL_TIMEOUT; communicator aborted");
     }
     ~DpComm() {
+        auto& w = wait_watches();
+        w.erase(std::remove(w.begin(), w.end(), static_cast<WaitWatch*>(this)), w.end());
         if (comm) nccl().commDestroy(comm);
     }
     void allreduce_f32(float* buf, size_t n, cudaStream_t st) const {

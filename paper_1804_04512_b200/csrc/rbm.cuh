@@ -173,6 +173,34 @@ class Rbm {
         dp_->init(id, rank, world);
         plans_.clear();
     }
+    // gradient-only steps (the caller reduces the shards): cd_k_update leaves W alone and keeps this
+    // shard's raw sums dW_aug = (Hcat^T Vcat)^T in G; apply_update then adds lr / batch_global * G
+    void set_grad_only(bool on) {
+        if (on != grad_only_) plans_.clear();
+        grad_only_ = on;
+    }
+    void get_grad(float* w, float* bv, float* bh) {
+        const float* G = G_.as<float>();
+        if (w) B2N_CUDA(cudaMemcpy2DAsync(w, V_ * 4, G, ldw_ * 4, V_ * 4, H_, cudaMemcpyDeviceToHost, stream_));
+        if (bh) B2N_CUDA(cudaMemcpy2DAsync(bh, 4, G + V_, ldw_ * 4, 4, H_, cudaMemcpyDeviceToHost, stream_));
+        if (bv) B2N_CUDA(cudaMemcpyAsync(bv, G + H_ * ldw_, V_ * 4, cudaMemcpyDeviceToHost, stream_));
+        B2N_CUDA(cudaStreamSynchronize(stream_));
+    }
+    void set_grad(const float* w, const float* bv, const float* bh) {
+        float* G = G_.as<float>();
+        B2N_CUDA(cudaMemsetAsync(G, 0, nW_ * 4, stream_));
+        B2N_CUDA(cudaMemcpy2DAsync(G, ldw_ * 4, w, V_ * 4, V_ * 4, H_, cudaMemcpyHostToDevice, stream_));
+        B2N_CUDA(cudaMemcpy2DAsync(G + V_, ldw_ * 4, bh, 4, 4, H_, cudaMemcpyHostToDevice, stream_));
+        B2N_CUDA(cudaMemcpyAsync(G + H_ * ldw_, bv, V_ * 4, cudaMemcpyHostToDevice, stream_));
+        B2N_CUDA(cudaStreamSynchronize(stream_));
+    }
+    void apply_update(float lr, long long Bg) {  // energy.hpp:148-169 with the shards' summed G
+        if (Bg < 1) throw Error(B2N_EPARAM, "apply_update: batch_global must be >= 1");
+        const long long n = nW_;
+        launch_ex(axpy_kernel, dim3(grid_for(n / 4)), dim3(256), 0, stream_, 1u, reinterpret_cast<float4*>(W_.as<float>()),
+                  reinterpret_cast<const float4*>(G_.as<float>()), n / 4, lr / static_cast<float>(Bg));
+        B2N_CUDA(cudaStreamSynchronize(stream_));
+    }
     long long hidden() const { return H_; }
     long long visible() const { return V_; }
     long long ld_visible() const { return round_up(V_ + 1, 8); }  // row pitch of a visible-side data matrix
@@ -363,7 +391,7 @@ class Rbm {
         const char* e = std::getenv("B2N_RBM_FUSED");
         if (e && e[0] == '0') return false;
         const int jt = (int)((H_ + 1 + kRfTileH - 1) / kRfTileH);
-        if (pl.k != 1 || dp_ || !x3_ || pl.B > 128 || pl.B > 16LL * jt || jt > 8 || V_ + 1 > kRfSlices * kRfSliceW)
+        if (pl.k != 1 || !x3_ || pl.B > 128 || pl.B > 16LL * jt || jt > 8 || V_ + 1 > kRfSlices * kRfSliceW)
             return false;
         static int clusters = [] {
             B2N_CUDA(cudaFuncSetAttribute(rbm_cd1_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kRfSmem));
@@ -432,6 +460,8 @@ class Rbm {
         rp.recon_out = nullptr;  // set per direct (zero-copy) launch: a host-mapped store costs the
         rp.done = done_.as<unsigned>();  // device-resident step ~3 us at its end
         rp.bg = (double)pl.Bg;
+        rp.G = G_.as<float>();
+        rp.grad_only = (dp_ || grad_only_) ? 1 : 0;
         if (std::getenv("B2N_RBM_TRACE")) {
             if (!trace_.p) trace_.alloc(256 * 8);
             rp.trace = trace_.as<unsigned long long>();
@@ -447,14 +477,25 @@ class Rbm {
         pl.ops.push_back(Op([=](cudaStream_t st) {
             launch_ex(rbm_cd1_fused_kernel, dim3(kRfSlices, jt), dim3(kRfThreads), (size_t)kRfSmem, st, 1u, mVk, mWk,
                       mHSk, mWmn, mVmn, mHmn, rp);
-        }, "rbm.cd1_fused", flops, bytes));
+        }, dp_ || grad_only_ ? "rbm.cd1_fused(grad)" : "rbm.cd1_fused", flops, bytes));
+        if (dp_) {  // sum the shards' raw dW / dbh / dbv, then the same update on every replica
+            DpComm* dp = dp_.get();
+            float* G = G_.as<float>();
+            const long long n = nW_;
+            const float scale = pl.lr / static_cast<float>(pl.Bg);
+            pl.ops.push_back(Op([=](cudaStream_t s) {
+                dp->allreduce_f32(G, (size_t)n, s);
+                launch_ex(axpy_kernel, dim3(grid_for(n / 4)), dim3(256), 0, s, 1u, reinterpret_cast<float4*>(W),
+                          reinterpret_cast<const float4*>(G), n / 4, scale);
+            }, "allreduce+update", 0.0, (double)n * 12));
+        }
         pl.fused = true;
         pl.rp = rp;
         const CUtensorMap ms[6] = {mVk, mWk, mHSk, mWmn, mVmn, mHmn};
         std::memcpy(pl.maps, ms, sizeof(ms));
         pl.recon_tiles = kRfSlices;
-        pl.nk = 1;
-        last_kernels_ = 1;
+        pl.nk = dp_ ? 2 : 1;
+        last_kernels_ = pl.nk;
     }
 
     void build(Plan& pl) {
@@ -513,7 +554,7 @@ class Rbm {
         // dW / dbh / dbv in one GEMM over K = 2B
         const float scale = pl.lr / static_cast<float>(pl.Bg);
         EpiParams e = epi_default();
-        if (dp_) {
+        if (dp_ || grad_only_) {
             e.C = G;
             e.ldc = ldw_;
             e.alpha = 1.0f;
@@ -522,9 +563,10 @@ class Rbm {
             e.ldc = ldw_;
             e.alpha = scale;
         }
-        GemmLaunch g = plan_gemm(H + 1, V + 1, 2 * B, {Hc, ldh_, true}, {Vc, ldv_, true}, dp_ ? EPI_STORE : EPI_AXPY, e,
+        const bool go = dp_ || grad_only_;
+        GemmLaunch g = plan_gemm(H + 1, V + 1, 2 * B, {Hc, ldh_, true}, {Vc, ldv_, true}, go ? EPI_STORE : EPI_AXPY, e,
                                  x3_);
-        pl.ops.push_back(gemm_op(g, dp_ ? "rbm.dW" : "rbm.dW+update"));
+        pl.ops.push_back(gemm_op(g, go ? "rbm.dW" : "rbm.dW+update"));
         ++pl.nk;
         if (dp_) {
             DpComm* dp = dp_.get();
@@ -620,6 +662,7 @@ class Rbm {
     long long hcol_B_ = -1;
     std::vector<std::unique_ptr<Plan>> plans_;
     std::unique_ptr<DpComm> dp_;
+    bool grad_only_ = false;
 };
 
 }  // namespace b2n

@@ -58,6 +58,11 @@ struct RbmFusedParams {
     // (written by the copy stream after its copies); null otherwise
     const unsigned* ready;
     unsigned ready_val;
+    // data-parallel shard / gradient-only step: phase 4 stores the raw sums (Hcat^T Vcat)^T of this
+    // shard into G (W_aug layout) and leaves W alone; the update W += lr / B_global * sum_ranks G
+    // follows the allreduce (NCCL inside the step graph, or the caller's for b2n_rbm_set_grad_only)
+    float* G;
+    int grad_only;
 };
 
 __device__ __forceinline__ unsigned* sbar_of(const RbmFusedParams& p, int s) { return p.gbar + 2 * s; }
@@ -431,7 +436,7 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
         const int idx = i * kRfThreads + threadIdx.x;
         const int n = idx / kRfSliceW, m = idx % kRfSliceW;  // hidden row n of W, visible column m
         const int h = h0c + n, v = v0c + m;
-        wv[i] = (h <= H && v <= V) ? p.W[(long long)h * p.ldw + v] : 0.0f;
+        wv[i] = (!p.grad_only && h <= H && v <= V) ? p.W[(long long)h * p.ldw + v] : 0.0f;
     }
     rf_product(ring, full + 12, empty + 12, tbar, tph, 4, (2 * B + 31) / 32, 128 * 32 * 4, kRfTileH * 32 * 4, true,
                true, id_w, id_w2, [&](int kb, uint8_t* a, uint8_t* b, uint64_t* bar) {
@@ -447,7 +452,12 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
             const int idx = i * kRfThreads + threadIdx.x;
             const int n = idx / kRfSliceW, m = idx % kRfSliceW;
             const int h = h0c + n, v = v0c + m;
-            if (h <= H && v <= V) p.W[(long long)h * p.ldw + v] = wv[i] + p.alpha * tile[m * kRfTileP + n];
+            if (h <= H && v <= V) {
+                if (p.grad_only)
+                    p.G[(long long)h * p.ldw + v] = tile[m * kRfTileP + n];
+                else
+                    p.W[(long long)h * p.ldw + v] = wv[i] + p.alpha * tile[m * kRfTileP + n];
+            }
         }
     }
     __syncthreads();

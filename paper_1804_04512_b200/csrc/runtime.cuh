@@ -14,6 +14,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
+#include <chrono>
 #include <string>
 #include <memory>
 #include <vector>
@@ -107,6 +108,18 @@ inline CUtensorMap make_map_2d(const float* base, uint64_t inner, uint64_t outer
 // Low-latency host wait for the step result: record an event behind the work and busy-poll it (a
 // blocking cudaStreamSynchronize may sleep and wake the host thread several microseconds late; the
 // step itself is tens of microseconds). One event per thread, reused.
+// While a host thread waits, the live NCCL communicators are polled (failure detection):
+// an asynchronous NCCL error or a wait beyond the communicator's timeout aborts it and throws
+// B2N_ENCCL instead of hanging the process behind a dead peer (nccl_dyn.cuh, DpComm::poll).
+struct WaitWatch {
+    virtual void poll(double waited_s) = 0;
+    virtual ~WaitWatch() = default;
+};
+inline std::vector<WaitWatch*>& wait_watches() {
+    static std::vector<WaitWatch*> v;
+    return v;
+}
+
 inline void spin_sync(cudaStream_t st) {
     thread_local cudaEvent_t ev = [] {
         cudaEvent_t e = nullptr;
@@ -119,7 +132,14 @@ inline void spin_sync(cudaStream_t st) {
     }
     B2N_CUDA(cudaEventRecord(ev, st));
     cudaError_t e;
+    unsigned long long spins = 0;
+    std::chrono::steady_clock::time_point t0;
     while ((e = cudaEventQuery(ev)) == cudaErrorNotReady) {
+        if (!wait_watches().empty() && (++spins & 0x3FFF) == 0) {  // every few ms of waiting
+            if (spins == 0x4000) t0 = std::chrono::steady_clock::now();
+            const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            for (WaitWatch* w : wait_watches()) w->poll(waited);
+        }
     }
     B2N_CUDA(e);
 }

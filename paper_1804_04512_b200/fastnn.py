@@ -412,6 +412,26 @@ class Rbm:
         _lib.call("b2n_rbm_recon", self._h, C.byref(out))
         return out.value
 
+    # ---- data parallelism driven by the caller (b2n_rbm_set_grad_only)
+    def set_grad_only(self, on: bool) -> None:
+        _lib.call("b2n_rbm_set_grad_only", self._h, 1 if on else 0)
+
+    def get_grad(self):
+        w = np.zeros((self.hidden, self.visible), np.float32)
+        bv = np.zeros(self.visible, np.float32)
+        bh = np.zeros(self.hidden, np.float32)
+        _lib.call("b2n_rbm_get_grad", self._h, _f(w), _f(bv), _f(bh))
+        return w, bv, bh
+
+    def set_grad(self, w, bv, bh) -> None:
+        w = np.ascontiguousarray(w, np.float32)
+        bv = np.ascontiguousarray(bv, np.float32)
+        bh = np.ascontiguousarray(bh, np.float32)
+        _lib.call("b2n_rbm_set_grad", self._h, _f(w), _f(bv), _f(bh))
+
+    def apply_update(self, lr: float, batch_global: int) -> None:
+        _lib.call("b2n_rbm_apply_update", self._h, lr, batch_global)
+
     def train_stream(self, v0, uniforms, batch: int, lr: float) -> np.ndarray:
         """CD-1 over consecutive host batches (rows [i*batch, (i+1)*batch) of v0 / uniforms per
         step), copies of step i+1 overlapped with step i; returns every step's recon error."""

@@ -46,9 +46,10 @@ def test_nccl_rbm_matches_single(gpu):
     b.run_staged(2, 0.1, 100)
     wa, bva, bha = a.get()
     wb, bvb, bhb = b.get()
-    # the single-GPU step runs the fused CD-1 kernel, the data-parallel one the split GEMMs + allreduce:
-    # same math, different (deterministic) summation orders -> agreement at the 3xTF32 level
-    assert norm_err(wb, wa) < 1e-5 and norm_err(bvb, bva) < 1e-5 and norm_err(bhb, bha) < 1e-5
+    # both run the fused CD-1 kernel; in data-parallel mode it stores the raw sums, NCCL sums them over
+    # the ranks and one axpy applies lr / B_global -- the same products, so agreement to rounding
+    assert b.kernels_per_step() == 2 and a.kernels_per_step() == 1
+    assert norm_err(wb, wa) < 1e-6 and norm_err(bvb, bva) < 1e-6 and norm_err(bhb, bha) < 1e-6
     assert abs(a.recon() - b.recon()) < 1e-6 * a.recon()
 
 
