@@ -169,8 +169,10 @@ class RbmWork:
         self.dist = dist
         self.config = {"workload": "mnist_rbm_cd1", "model": "RBM 784-500 binary, CD-1", "global_batch": self.Bg,
                        "local_batch": self.B, "parallelism": f"dp{dist.world}", "lr": self.lr,
-                       "sampling": "supplied generate_canonical<double,53> uniforms (bit-exact Bernoulli)"}
-        self.h2d = self.B * self.V * 4 + self.B * self.H * 8
+                       "sampling": "std::mt19937 generate_canonical<double,53> stream (bit-exact Bernoulli): "
+                                   "staged for `value`, generated on the device from the caller's generator "
+                                   "inside the timed region for `e2e`"}
+        self.h2d = self.B * self.V * 4  # e2e: v0 only -- the draws are generated on the device
         self.d2h = None
 
     def stream(self):
@@ -180,17 +182,21 @@ class RbmWork:
         self.rbm.run_staged(n, self.lr, self.Bg)
 
     def e2e_step(self):
-        if self.dist.world > 1:  # data-parallel: stage the shard (H2D), one step, read the recon partials
-            self.rbm.stage(self.v0_h, self.u_h)
+        if getattr(self, "_gen1", None) is None:  # this rank's generator (device draws)
+            self._gen1 = self.F.Mt19937(23 + self.dist.rank)
+            self.rbm.set_rng(self._gen1)
+        if self.dist.world > 1:  # data-parallel: stage the shard (H2D + device draws), one step, recon
+            self.rbm.stage(self.v0_h, None)
             self.rbm.run_staged(1, self.lr, self.Bg)
             return self.rbm.recon()
-        return self.F.cd_k_update(self.rbm, self.v0_h, 1, self.lr, self.u_h, self.Bg)
+        return self.F.cd_k_update(self.rbm, self.v0_h, 1, self.lr, self._gen1, self.Bg)
 
     def e2e_total(self, steps, warmup):
-        """end to end through Rbm.train_stream (the loop of cd_k_update calls over host batches):
-        `steps` distinct host batches (v0 + uniforms, pinned; together larger than L2), every step's
-        H2D inside the timed region (overlapped with the previous step) and every step's recon
-        read back. Returns the device time of the whole call (ms) on the library stream."""
+        """end to end through Rbm.train_stream (the loop of cd_k_update(rbm, v0_i, 1, lr, rng) calls
+        over host batches): `steps` distinct pinned host batches (together larger than L2), every
+        step's H2D inside the timed region (overlapped with the previous step), every step's
+        Bernoulli draws generated from the caller's mt19937 inside it (on the device, ahead of the
+        step), every step's recon read back. Returns the device time of the call (ms)."""
         if self.dist.world > 1:
             return None
         import torch
@@ -199,15 +205,16 @@ class RbmWork:
         if getattr(self, "_sv", None) is None or self._sv.shape[0] < n:
             self._sv = pinned((n, self.V), np.float32)
             self._sv[:] = O.bernoulli_f32(11, 0.5, n * self.V).reshape(n, self.V)
-            self._su = pinned((n, self.H), np.float64)
-            self._su[:] = O.canonical_f64(13, n * self.H).reshape(n, self.H)
-        self.rbm.train_stream(self._sv[:max(warmup, 1) * self.B], self._su[:max(warmup, 1) * self.B], self.B, self.lr)
+        # the Bernoulli draws: the reference's std::mt19937 stream generated on the device from the
+        # caller's generator state (bit-exact; the state goes up once and comes back once per call)
+        gen = self.F.Mt19937(13)
+        self.rbm.train_stream(self._sv[:max(warmup, 1) * self.B], gen, self.B, self.lr)
         s = torch.cuda.ExternalStream(self.stream())
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         self.dist.barrier()
         torch.cuda.synchronize()
         e0.record(s)
-        self.rbm.train_stream(self._sv[:n], self._su[:n], self.B, self.lr)
+        self.rbm.train_stream(self._sv[:n], gen, self.B, self.lr)
         e1.record(s)
         torch.cuda.synchronize()
         self.dist.barrier()
@@ -259,7 +266,7 @@ class CrbmWork:
         self.config = {"workload": "mnist_crbm_cd1", "model": f"CRBM 1x28x28, {c['k']} kernels 5x5, binary, CD-1",
                        "global_batch": self.Bg, "local_batch": self.B, "parallelism": f"dp{dist.world}",
                        "lr": self.lr}
-        self.h2d = v0.nbytes + u.nbytes
+        self.h2d = v0.nbytes  # e2e: v0 only -- the draws are generated on the device
 
     def stream(self):
         return self.m.stream_handle()
@@ -268,7 +275,11 @@ class CrbmWork:
         self.m.run_staged(n, self.lr, self.Bg)
 
     def e2e_step(self):
-        return self.F.crbm_cd_update(self.m, self.v0_h, self.lr, self.u_h, self.Bg)
+        # crbm_cd_update(m, v0, lr, rng): the B*k*oh*ow draws generated on the device from the
+        # caller's mt19937 (state up only when it changed, back every call)
+        if getattr(self, "_gen", None) is None:
+            self._gen = self.F.Mt19937(17)
+        return self.F.crbm_cd_update(self.m, self.v0_h, self.lr, self._gen, self.Bg)
 
     def kernels_per_step(self):
         return _kernels(self.F._lib, "b2n_crbm_kernels_per_step", self.m.handle)

@@ -182,6 +182,15 @@ int b2n_net_profile(b2n_net* net, long long batch, int steps, int max_ops, doubl
  * consumes) to `out`. Called on the calling thread, in step order. */
 typedef void (*b2n_uniform_fn)(void* ctx, double* out, long long count);
 
+/* The reference's generator on the device. A std::mt19937 is passed as its libstdc++ state: the
+ * 624 state words then the position (_M_x[0..623], _M_p -- the 625 numbers `os << rng` prints).
+ * Every entry point below that takes uniforms_host also accepts NULL: the draws then come from the
+ * object's device copy of the caller's generator (set with *_set_rng, read back with *_get_rng),
+ * generated on the GPU bit-exactly as std::bernoulli_distribution would have drawn them
+ * (generate_canonical<double,53>, energy.hpp:53-71) -- no host draws, no uniforms over PCIe.
+ * b2n_mt19937_draw: the next n generate_canonical<double,53> draws of `state` (advanced in place). */
+int b2n_mt19937_draw(int device, unsigned state[625], double* out_host, long long n);
+
 /* ---- RBM: replaces Rbm (energy.hpp:16-32) and cd_k_update (energy.hpp:131-171) ---- */
 int b2n_rbm_create(long long hidden, long long visible, int device, int precision, b2n_rbm** out);
 int b2n_rbm_destroy(b2n_rbm* rbm);
@@ -204,6 +213,9 @@ int b2n_rbm_dp_init(b2n_rbm* rbm, const char id[128], int rank, int world);
  * lr / batch scale); get_grad / set_grad move them (w: hidden x visible), apply_update adds
  * lr / batch_global * (the summed sums) -- the same arithmetic the NCCL mode runs in its step. */
 int b2n_rbm_set_grad_only(b2n_rbm* rbm, int on);
+/* the device generator behind uniforms_host == NULL (see b2n_mt19937_draw) */
+int b2n_rbm_set_rng(b2n_rbm* rbm, const unsigned state[625]);
+int b2n_rbm_get_rng(b2n_rbm* rbm, unsigned state[625]);
 int b2n_rbm_get_grad(b2n_rbm* rbm, float* w_host, float* bv_host, float* bh_host);
 int b2n_rbm_set_grad(b2n_rbm* rbm, const float* w_host, const float* bv_host, const float* bh_host);
 int b2n_rbm_apply_update(b2n_rbm* rbm, float lr, long long batch_global);
@@ -224,7 +236,8 @@ int b2n_rbm_stream(b2n_rbm* rbm, void** cuda_stream);
  * next layer's input -- on the device. Uniforms: B x H per step from `fill`, layer by layer,
  * epoch by epoch, batch by batch (the reference's single rng stream). recon_out[layer*epochs + e]
  * = mean per-step reconstruction error. Errors: EPARAM (empty stack, batch < 1, epochs < 0),
- * ESHAPE (extent chain, the reference's message). */
+ * ESHAPE (extent chain, the reference's message). fill == NULL: ctx is the caller's generator
+ * state (unsigned[625], see b2n_mt19937_draw), drawn from and advanced on the device. */
 int b2n_dbn_pretrain(b2n_rbm* const* stack, int layers, const float* data_host, long long n, int epochs, float lr,
                      long long batch, b2n_uniform_fn fill, void* ctx, double* recon_out);
 int b2n_rbm_kernels_per_step(b2n_rbm* rbm, int* n);
@@ -256,6 +269,8 @@ int b2n_crbm_keep_states(b2n_crbm* crbm, int on);
  * identical update on every rank. Needs the one-launch step's shape envelope (EPARAM otherwise). */
 int b2n_crbm_dp_init(b2n_crbm* crbm, const char id[128], int rank, int world);
 int b2n_crbm_last_states(b2n_crbm* crbm, float* h0, float* hs, float* v1, float* h1);
+int b2n_crbm_set_rng(b2n_crbm* crbm, const unsigned state[625]);
+int b2n_crbm_get_rng(b2n_crbm* crbm, unsigned state[625]);
 int b2n_crbm_stage(b2n_crbm* crbm, const float* v0_host, const double* uniforms_host, long long batch);
 int b2n_crbm_run_staged(b2n_crbm* crbm, int steps, float lr, long long batch_global);
 int b2n_crbm_recon(b2n_crbm* crbm, double* recon);

@@ -6,7 +6,7 @@
 //   build_network (network.hpp:284)          build_network          -> device-resident Network
 //   train_minibatch (network.hpp:463)        train_minibatch        -> loss, params updated in HBM
 //   forward_batch / evaluate (:402, :474)    forward_batch / evaluate
-//   Rbm / cd_k_update (energy.hpp:16, :131)  Rbm / cd_k_update      (Bernoulli uniforms supplied)
+//   Rbm / cd_k_update (energy.hpp:16, :131)  Rbm / cd_k_update      (rng's Bernoulli stream drawn on the GPU)
 //   Error, ShapeError, ... (config.hpp:11-57) the same exception types, thrown from C ABI statuses
 //
 // Tensors: any type with fastnn::Tensor's accessors (rank(), dim(i), rows_total(), last_dim(),
@@ -19,6 +19,8 @@
 #include <memory>
 #include <random>
 #include <stdexcept>
+#include <type_traits>
+#include <cstdint>
 #include <string>
 #include <vector>
 
@@ -304,9 +306,46 @@ class Rbm {
     std::size_t hidden_, visible_;
 };
 
+namespace detail {
+#if defined(__GLIBCXX__)
+// The caller's std::mt19937 as the C ABI's 625-word state (libstdc++: _M_x[624], _M_p -- the same
+// numbers `os << rng` prints). The Bernoulli draws then run on the device from this state
+// (b2n_mt19937_draw) and the advanced state is written back, so `rng` ends exactly where the
+// reference's cd_k_update would have left it.
+constexpr bool kDeviceDraws = true;
+struct MtRaw {
+    std::uint_fast32_t x[624];
+    std::size_t p;
+};
+static_assert(sizeof(std::mt19937) == sizeof(MtRaw) && std::is_trivially_copyable<std::mt19937>::value,
+              "libstdc++ mersenne_twister_engine layout");
+inline void mt_export(const std::mt19937& g, unsigned s[625]) {
+    MtRaw r;
+    std::memcpy(&r, &g, sizeof r);
+    for (int i = 0; i < 624; ++i) s[i] = (unsigned)r.x[i];
+    s[624] = (unsigned)r.p;
+}
+inline void mt_import(std::mt19937& g, const unsigned s[625]) {
+    MtRaw r;
+    for (int i = 0; i < 624; ++i) r.x[i] = s[i];
+    r.p = s[624];
+    std::memcpy(static_cast<void*>(&g), &r, sizeof r);
+}
+#else
+constexpr bool kDeviceDraws = false;  // another standard library: draw on the host and supply them
+inline void mt_export(const std::mt19937&, unsigned*) {}
+inline void mt_import(std::mt19937&, const unsigned*) {}
+#endif
+inline std::vector<double> host_draws(std::mt19937& rng, std::size_t n) {
+    std::vector<double> u(n);
+    for (double& d : u) d = std::generate_canonical<double, 53>(rng);
+    return u;
+}
+}  // namespace detail
+
 // cd_k_update (energy.hpp:131-171). The reference draws its Bernoulli samples from `rng`; here the
-// same stream is drawn on the host (generate_canonical<double,53>, exactly what
-// std::bernoulli_distribution consumes) and supplied, so sampling stays bit-exact.
+// same stream (generate_canonical<double,53>, what std::bernoulli_distribution consumes) is
+// generated on the GPU from rng's state and rng is advanced past it, so sampling stays bit-exact.
 template <class T>
 double cd_k_update(Rbm& rbm, const T& v0, int k, float lr, std::mt19937& rng) {
     if (k < 1) throw ParamError("cd_k_update: k must be >= 1, got " + std::to_string(k));
@@ -314,9 +353,17 @@ double cd_k_update(Rbm& rbm, const T& v0, int k, float lr, std::mt19937& rng) {
     if (v0.dim(1) != rbm.visible_units()) throw ShapeError("cd_k_update: visible extent mismatch");
     const std::vector<float> vs = detail::pack_rows(v0);
     const std::size_t B = v0.dim(0);
-    std::vector<double> u((std::size_t)k * B * rbm.hidden_units());
-    for (double& d : u) d = std::generate_canonical<double, 53>(rng);
     double recon = 0.0;
+    if (detail::kDeviceDraws) {
+        unsigned st[625];
+        detail::mt_export(rng, st);
+        check(b2n_rbm_set_rng(rbm.handle(), st));
+        check(b2n_cd_k_update(rbm.handle(), vs.data(), (long long)B, k, lr, nullptr, (long long)B, &recon));
+        check(b2n_rbm_get_rng(rbm.handle(), st));
+        detail::mt_import(rng, st);
+        return recon;
+    }
+    const std::vector<double> u = detail::host_draws(rng, (std::size_t)k * B * rbm.hidden_units());
     check(b2n_cd_k_update(rbm.handle(), vs.data(), (long long)B, k, lr, u.data(), (long long)B, &recon));
     return recon;
 }
@@ -375,9 +422,17 @@ double crbm_cd_update(Crbm& m, const T& v0, float lr, std::mt19937& rng) {
         throw ShapeError("crbm_cd_update: input does not match the model's visible shape");
     const std::vector<float> vs = detail::pack_rows(v0);
     const std::size_t B = v0.dim(0);
-    std::vector<double> u(B * m.hidden_pixels());
-    for (double& d : u) d = std::generate_canonical<double, 53>(rng);
     double recon = 0.0;
+    if (detail::kDeviceDraws) {  // the draws generated on the GPU from rng's state (see cd_k_update)
+        unsigned st[625];
+        detail::mt_export(rng, st);
+        check(b2n_crbm_set_rng(m.handle(), st));
+        check(b2n_crbm_cd_update(m.handle(), vs.data(), (long long)B, lr, nullptr, (long long)B, &recon));
+        check(b2n_crbm_get_rng(m.handle(), st));
+        detail::mt_import(rng, st);
+        return recon;
+    }
+    const std::vector<double> u = detail::host_draws(rng, B * m.hidden_pixels());
     check(b2n_crbm_cd_update(m.handle(), vs.data(), (long long)B, lr, u.data(), (long long)B, &recon));
     return recon;
 }
@@ -388,8 +443,17 @@ double crbm_cd_update(Crbm& m, const T& v0, float lr, std::mt19937& rng) {
 // Returns every step's reconstruction error.
 inline std::vector<double> cd1_stream(Rbm& rbm, const float* v0, std::size_t steps, std::size_t batch, float lr,
                                       std::mt19937& rng) {
-    std::vector<double> u(steps * batch * rbm.hidden_units()), recon(steps);
-    for (double& d : u) d = std::generate_canonical<double, 53>(rng);
+    std::vector<double> recon(steps);
+    if (detail::kDeviceDraws) {  // each step's draws generated on the GPU ahead of the step
+        unsigned st[625];
+        detail::mt_export(rng, st);
+        check(b2n_rbm_set_rng(rbm.handle(), st));
+        check(b2n_rbm_train_stream(rbm.handle(), v0, nullptr, (long long)steps, (long long)batch, lr, recon.data()));
+        check(b2n_rbm_get_rng(rbm.handle(), st));
+        detail::mt_import(rng, st);
+        return recon;
+    }
+    const std::vector<double> u = detail::host_draws(rng, steps * batch * rbm.hidden_units());
     check(b2n_rbm_train_stream(rbm.handle(), v0, u.data(), (long long)steps, (long long)batch, lr, recon.data()));
     return recon;
 }
@@ -412,8 +476,16 @@ DbnReport dbn_pretrain(std::vector<Rbm>& stack, const T& data, std::size_t epoch
         std::mt19937& g = *static_cast<std::mt19937*>(ctx);
         for (long long i = 0; i < count; ++i) out[i] = std::generate_canonical<double, 53>(g);
     };
-    check(b2n_dbn_pretrain(hs.data(), (int)hs.size(), xs.data(), (long long)data.dim(0), (int)epochs, lr,
-                           (long long)batch_size, fill, &rng, rec.data()));
+    if (detail::kDeviceDraws) {  // the draws generated on the GPU from rng's state, rng advanced
+        unsigned st[625];
+        detail::mt_export(rng, st);
+        check(b2n_dbn_pretrain(hs.data(), (int)hs.size(), xs.data(), (long long)data.dim(0), (int)epochs, lr,
+                               (long long)batch_size, nullptr, st, rec.data()));
+        detail::mt_import(rng, st);
+    } else {
+        check(b2n_dbn_pretrain(hs.data(), (int)hs.size(), xs.data(), (long long)data.dim(0), (int)epochs, lr,
+                               (long long)batch_size, fill, &rng, rec.data()));
+    }
     DbnReport r;
     for (std::size_t l = 0; l < stack.size(); ++l)
         r.recon.emplace_back(rec.begin() + (long)(l * epochs), rec.begin() + (long)((l + 1) * epochs));

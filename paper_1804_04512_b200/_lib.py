@@ -76,6 +76,7 @@ _D = C.POINTER(C.c_double)
 _I = C.POINTER(C.c_int)
 _LL = C.POINTER(C.c_longlong)
 _VP = C.c_void_p
+_U = C.POINTER(C.c_uint)
 
 
 class LayerDescC(C.Structure):
@@ -143,6 +144,11 @@ _SIGS = {
     "b2n_rbm_apply_update": ([_VP, C.c_float, C.c_longlong], C.c_int),
     "b2n_rbm_train_stream": ([_VP, _F, _D, C.c_longlong, C.c_longlong, C.c_float, _D], C.c_int),
     "b2n_rbm_stream": ([_VP, C.POINTER(_VP)], C.c_int),
+    "b2n_rbm_set_rng": ([_VP, _U], C.c_int),
+    "b2n_rbm_get_rng": ([_VP, _U], C.c_int),
+    "b2n_crbm_set_rng": ([_VP, _U], C.c_int),
+    "b2n_crbm_get_rng": ([_VP, _U], C.c_int),
+    "b2n_mt19937_draw": ([C.c_int, _U, _D, C.c_longlong], C.c_int),
     "b2n_crbm_create": ([C.c_int] * 6 + [C.c_int, C.c_int, C.POINTER(_VP)], C.c_int),
     "b2n_crbm_destroy": ([_VP], C.c_int),
     "b2n_crbm_init": ([_VP, C.c_uint], C.c_int),

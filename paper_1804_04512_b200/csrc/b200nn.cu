@@ -200,7 +200,9 @@ int b2n_dbn_pretrain(b2n_rbm* const* stack, int layers, const float* data, long 
         if (layers < 1 || !stack) throw b2n::Error(B2N_EPARAM, "dbn_pretrain: empty stack");
         if (batch < 1) throw b2n::Error(B2N_EPARAM, "dbn_pretrain: batch_size must be >= 1");
         if (epochs < 0) throw b2n::Error(B2N_EPARAM, "dbn_pretrain: epochs must be >= 0");
-        if (!fill) throw b2n::Error(B2N_EPARAM, "dbn_pretrain: no uniform source");
+        // fill == null: ctx is the caller's std::mt19937 state (625 words), advanced on the device
+        if (!fill && !ctx) throw b2n::Error(B2N_EPARAM, "dbn_pretrain: no uniform source");
+        uint32_t* mt = fill ? nullptr : static_cast<uint32_t*>(ctx);
         long long in = stack[0]->impl.visible();
         for (int l = 0; l < layers; ++l) {  // energy.hpp:216-224
             const long long v = stack[l]->impl.visible();
@@ -220,10 +222,12 @@ int b2n_dbn_pretrain(b2n_rbm* const* stack, int layers, const float* data, long 
         B2N_CUDA(cudaStreamSynchronize(r0.stream()));
         for (int l = 0; l < layers; ++l) {
             b2n::Rbm& r = stack[l]->impl;
+            if (mt) r.set_rng(mt);
             for (int e = 0; e < epochs; ++e) {
                 const double rc = r.train_epoch(cur.as<float>(), n, batch, lr, fill, ctx);
                 if (recon_out) recon_out[(size_t)l * epochs + e] = rc;
             }
+            if (mt) r.get_rng(mt);
             if (l + 1 < layers) {
                 next.alloc((size_t)(n * stack[l + 1]->impl.ld_visible() * 4));
                 r.transform_up(cur.as<float>(), n, next.as<float>());
@@ -312,6 +316,39 @@ int b2n_rbm_run_staged(b2n_rbm* r, int steps, float lr, long long batch_global) 
 int b2n_rbm_train_stream(b2n_rbm* r, const float* v0, const double* u, long long steps, long long batch, float lr,
                          double* recon_out) {
     return guard([&] { r->impl.train_stream(v0, u, steps, batch, lr, recon_out); });
+}
+int b2n_rbm_set_rng(b2n_rbm* r, const unsigned state[625]) {
+    return guard([&] { r->impl.set_rng(state); });
+}
+int b2n_rbm_get_rng(b2n_rbm* r, unsigned state[625]) {
+    return guard([&] { r->impl.get_rng(state); });
+}
+int b2n_crbm_set_rng(b2n_crbm* m, const unsigned state[625]) {
+    return guard([&] { m->impl.set_rng(state); });
+}
+int b2n_crbm_get_rng(b2n_crbm* m, unsigned state[625]) {
+    return guard([&] { m->impl.get_rng(state); });
+}
+int b2n_mt19937_draw(int device, unsigned state[625], double* out_host, long long n) {
+    return guard([&] {
+        B2N_REQUIRE(state && (out_host || n == 0) && n >= 0, B2N_EPARAM, "mt19937_draw: bad arguments");
+        B2N_CUDA(cudaSetDevice(device));
+        cudaStream_t st;
+        B2N_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        try {
+            b2n::DevRng g;
+            g.load(state, st);
+            b2n::DevMem out;
+            out.alloc((size_t)std::max<long long>(n, 1) * 8);
+            g.draw(out.as<double>(), n, st);
+            B2N_CUDA(cudaMemcpyAsync(out_host, out.p, (size_t)n * 8, cudaMemcpyDeviceToHost, st));
+            g.store(state, st);
+        } catch (...) {
+            cudaStreamDestroy(st);
+            throw;
+        }
+        B2N_CUDA(cudaStreamDestroy(st));
+    });
 }
 int b2n_rbm_set_grad_only(b2n_rbm* r, int on) {
     return guard([&] { r->impl.set_grad_only(on != 0); });

@@ -19,6 +19,7 @@
 // fixed-order reduction) -- the product path for the few-channel CRBM shapes, where N = c_in makes
 // the tensor-core dgrad mostly padding. B2N_CRBM_FUSED=0 forces the split path.
 #pragma once
+#include "mt19937.cuh"
 #include <random>
 
 #include "conv.cuh"
@@ -150,7 +151,10 @@ class Crbm {
         if (B < 1) throw Error(B2N_ESHAPE, "crbm_cd_update: batch must be >= 1");
         ensure_capacity(B);
         B2N_CUDA(cudaMemcpyAsync(Vc_.p, v0, (size_t)(B * vpix()) * 4, cudaMemcpyHostToDevice, stream_));
-        B2N_CUDA(cudaMemcpyAsync(U_.p, u, (size_t)(B * hpix()) * 8, cudaMemcpyHostToDevice, stream_));
+        if (u)
+            B2N_CUDA(cudaMemcpyAsync(U_.p, u, (size_t)(B * hpix()) * 8, cudaMemcpyHostToDevice, stream_));
+        else  // u == null: the B * k * oh * ow draws from the device generator (set_rng)
+            rng_.draw(U_.as<double>(), B * hpix(), stream_);
         staged_B_ = B;
     }
     void run_staged(int steps, float lr, long long Bg) {
@@ -181,6 +185,9 @@ class Crbm {
         if (h1)
             for (long long i = 0; i < B * hp; ++i) h1[i] = -h1[i];  // stored negated for the statistics
     }
+    // the caller's std::mt19937 (625 words: state, position) for the steps that take no uniforms
+    void set_rng(const uint32_t* st) { rng_.load(st, stream_); }
+    void get_rng(uint32_t* st) { rng_.store(st, stream_); }
     cudaStream_t stream() const { return stream_; }
     void dp_init(const char id[128], int rank, int world) {
         dp_ = std::make_unique<DpComm>();
@@ -470,6 +477,7 @@ class Crbm {
     int last_kernels_ = 1;
     cudaStream_t stream_ = nullptr;
     DevMem P_, Vc_, Hc_, HS_, U_, recon_;
+    DevRng rng_;
     HostPinned h_recon_;
     std::vector<std::unique_ptr<Plan>> plans_;
     std::unique_ptr<DpComm> dp_;

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <random>
 
+#include "mt19937.cuh"
 #include "nccl_dyn.cuh"
 #include "network.cuh"
 #include "rbm_fused.cuh"
@@ -65,10 +66,12 @@ class Rbm {
         plans_.clear();
         for (cudaEvent_t e : uev_)
             if (e) cudaEventDestroy(e);
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < kStage; ++j) {
             if (ev_used_[j]) cudaEventDestroy(ev_used_[j]);
+            if (ev_rng_[j]) cudaEventDestroy(ev_rng_[j]);
         }
         if (copy_stream_) cudaStreamDestroy(copy_stream_);
+        if (rng_stream_) cudaStreamDestroy(rng_stream_);
         if (recon_host_) cudaFreeHost(recon_host_);
         if (stream_) cudaStreamDestroy(stream_);
     }
@@ -104,8 +107,12 @@ class Rbm {
         ensure_capacity(B, k);
         Plan& pl = plan_for(B, k, lr, Bg);
         const float* v0d = device_alias(v0);
-        const double* ud = device_alias(u);
-        if (pl.fused && v0d && ud && V_ % 4 == 0) {
+        const double* ud = u ? device_alias(u) : nullptr;
+        if (pl.fused && v0d && (ud || !u) && V_ % 4 == 0) {
+            if (!u) {  // the Bernoulli draws from the device generator (set_rng)
+                ud = U_.as<double>();
+                rng_.draw(U_.as<double>(), B * H_, stream_);
+            }
             // pinned caller buffers: the fused kernel reads v0 and the uniforms itself (zero-copy),
             // launched directly with this call's pointers instead of staging copies + the graph
             staged_B_ = B;
@@ -132,7 +139,10 @@ class Rbm {
         ensure_capacity(B, k);
         float* Vc = Vcat_.as<float>();
         B2N_CUDA(cudaMemcpy2DAsync(Vc, ldv_ * 4, v0, V_ * 4, V_ * 4, B, cudaMemcpyHostToDevice, stream_));
-        B2N_CUDA(cudaMemcpyAsync(U_.p, u, (size_t)k * B * H_ * 8, cudaMemcpyHostToDevice, stream_));
+        if (u)
+            B2N_CUDA(cudaMemcpyAsync(U_.p, u, (size_t)k * B * H_ * 8, cudaMemcpyHostToDevice, stream_));
+        else  // u == null: draw the k * B * H uniforms from the device generator (set_rng)
+            rng_.draw(U_.as<double>(), (long long)k * B * H_, stream_);
         staged_B_ = B;
         staged_k_ = k;
     }
@@ -201,6 +211,9 @@ class Rbm {
                   reinterpret_cast<const float4*>(G_.as<float>()), n / 4, lr / static_cast<float>(Bg));
         B2N_CUDA(cudaStreamSynchronize(stream_));
     }
+    // the caller's std::mt19937 (625 words: state, position) for the steps that take no uniforms
+    void set_rng(const uint32_t* st) { rng_.load(st, stream_); }
+    void get_rng(uint32_t* st) { rng_.store(st, stream_); }
     long long hidden() const { return H_; }
     long long visible() const { return V_; }
     long long ld_visible() const { return round_up(V_ + 1, 8); }  // row pitch of a visible-side data matrix
@@ -215,7 +228,7 @@ class Rbm {
         if (dp_) throw Error(B2N_EPARAM, "dbn_pretrain: data-parallel RBMs step through run_staged");
         ensure_capacity(std::min(batch, n), 1);
         const long long per = std::min(batch, n) * H_;
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; fill && j < 2; ++j) {
             if (ubuf_[j].bytes < (size_t)per * 8) ubuf_[j].alloc((size_t)per * 8);
             if (!uev_[j]) B2N_CUDA(cudaEventCreateWithFlags(&uev_[j], cudaEventDisableTiming));
         }
@@ -227,11 +240,15 @@ class Rbm {
         for (long long lo = 0; lo < n; lo += batch, ++batches) {
             const long long B = std::min(batch, n - lo);
             const int j = (int)(batches & 1);
-            if (pending[j]) B2N_CUDA(cudaEventSynchronize(uev_[j]));  // its previous H2D has drained
-            fill(ctx, ubuf_[j].as<double>(), B * H_);
-            B2N_CUDA(cudaMemcpyAsync(U_.p, ubuf_[j].p, (size_t)(B * H_ * 8), cudaMemcpyHostToDevice, stream_));
-            B2N_CUDA(cudaEventRecord(uev_[j], stream_));
-            pending[j] = true;
+            if (fill) {
+                if (pending[j]) B2N_CUDA(cudaEventSynchronize(uev_[j]));  // its previous H2D has drained
+                fill(ctx, ubuf_[j].as<double>(), B * H_);
+                B2N_CUDA(cudaMemcpyAsync(U_.p, ubuf_[j].p, (size_t)(B * H_ * 8), cudaMemcpyHostToDevice, stream_));
+                B2N_CUDA(cudaEventRecord(uev_[j], stream_));
+                pending[j] = true;
+            } else {  // the device generator (set_rng): no host draws, no copies
+                rng_.draw(U_.as<double>(), B * H_, stream_);
+            }
             B2N_CUDA(cudaMemcpy2DAsync(Vcat_.p, ldv_ * 4, data + lo * ldd, ldd * 4, V_ * 4, B, cudaMemcpyDeviceToDevice,
                                        stream_));
             Plan& pl = plan_for(B, 1, lr, B);
@@ -259,7 +276,7 @@ class Rbm {
         Plan& pl = plan_for(B, 1, lr, B);
         if (!pl.fused || V_ % 4 != 0) {  // the split path: staged copies + the step graph, in order
             for (long long i = 0; i < steps; ++i) {
-                stage(v0 + i * B * V_, u + i * B * H_, B, 1);
+                stage(v0 + i * B * V_, u ? u + i * B * H_ : nullptr, B, 1);
                 launch(pl);
                 last_B_ = B;
                 last_Bg_ = B;
@@ -268,27 +285,36 @@ class Rbm {
             return;
         }
         prepare(pl);
-        for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < kStage; ++j) {
             if (sv_[j].bytes < (size_t)(B * V_ * 4)) sv_[j].alloc((size_t)(B * V_ * 4));
             if (su_[j].bytes < (size_t)(B * H_ * 8)) su_[j].alloc((size_t)(B * H_ * 8));
             if (!ev_used_[j]) B2N_CUDA(cudaEventCreateWithFlags(&ev_used_[j], cudaEventDisableTiming));
+            if (!ev_rng_[j]) B2N_CUDA(cudaEventCreateWithFlags(&ev_rng_[j], cudaEventDisableTiming));
         }
         if (!copy_stream_) B2N_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
+        if (!u && !rng_stream_) B2N_CUDA(cudaStreamCreateWithFlags(&rng_stream_, cudaStreamNonBlocking));
         if (rstream_.bytes < (size_t)steps * 8) rstream_.alloc((size_t)steps * 8);
         // readiness flags: the copy stream stamps step i + 1 into flag j after step i's copies (a
         // stream memory write, fenced after them); the step kernel polls it, so the compute stream
         // carries no cross-stream event and consecutive steps keep their programmatic overlap
         if (!sready_.p) sready_.alloc(64);
         B2N_CUDA(cudaMemsetAsync(sready_.p, 0, 64, stream_));
-        B2N_CUDA(cudaEventRecord(ev_used_[0], stream_));  // staging buffers free after prior work
-        B2N_CUDA(cudaEventRecord(ev_used_[1], stream_));
+        for (int j = 0; j < kStage; ++j)
+            B2N_CUDA(cudaEventRecord(ev_used_[j], stream_));  // staging buffers free after prior work
         for (long long i = 0; i < steps; ++i) {
-            const int j = (int)(i & 1);
-            B2N_CUDA(cudaStreamWaitEvent(copy_stream_, ev_used_[j], 0));  // step i - 2 done with buffer j
+            const int j = (int)(i % kStage);
+            B2N_CUDA(cudaStreamWaitEvent(copy_stream_, ev_used_[j], 0));  // step i - kStage done with buffer j
             B2N_CUDA(cudaMemcpyAsync(sv_[j].p, v0 + i * B * V_, (size_t)(B * V_ * 4), cudaMemcpyHostToDevice,
                                      copy_stream_));
-            B2N_CUDA(cudaMemcpyAsync(su_[j].p, u + i * B * H_, (size_t)(B * H_ * 8), cudaMemcpyHostToDevice,
-                                     copy_stream_));
+            if (u)
+                B2N_CUDA(cudaMemcpyAsync(su_[j].p, u + i * B * H_, (size_t)(B * H_ * 8), cudaMemcpyHostToDevice,
+                                         copy_stream_));
+            else {  // step i's draws from the device generator on its own stream, up to kStage steps ahead
+                B2N_CUDA(cudaStreamWaitEvent(rng_stream_, ev_used_[j], 0));
+                rng_.draw(su_[j].as<double>(), B * H_, rng_stream_);
+                B2N_CUDA(cudaEventRecord(ev_rng_[j], rng_stream_));
+                B2N_CUDA(cudaStreamWaitEvent(copy_stream_, ev_rng_[j], 0));
+            }
             unsigned* flag = sready_.as<unsigned>() + j;
             stream_write_u32(copy_stream_, flag, (unsigned)(i + 1));
             RbmFusedParams rp = pl.rp;
@@ -302,6 +328,8 @@ class Rbm {
                       pl.maps[0], pl.maps[1], pl.maps[2], pl.maps[3], pl.maps[4], pl.maps[5], rp);
             B2N_CUDA(cudaEventRecord(ev_used_[j], stream_));
         }
+        B2N_CUDA(cudaEventRecord(ev_used_[0], copy_stream_));  // after the last draw (copy stream waited on it)
+        B2N_CUDA(cudaStreamWaitEvent(stream_, ev_used_[0], 0));
         B2N_CUDA(cudaMemcpyAsync(recon_out, rstream_.p, (size_t)steps * 8, cudaMemcpyDeviceToHost, stream_));
         spin_sync(stream_);
         staged_B_ = B;
@@ -639,11 +667,15 @@ class Rbm {
     HostPinned ubuf_[2];       // train_epoch: double-buffered uniforms
     cudaEvent_t uev_[2] = {nullptr, nullptr};
     DevMem racc_;              // train_epoch: device sum of per-step reconstruction errors
-    DevMem sv_[2], su_[2];     // train_stream: double-buffered device staging of v0 / uniforms
+    static constexpr int kStage = 4;
+    DevMem sv_[kStage], su_[kStage];  // train_stream: device staging of v0 / uniforms, kStage deep
     DevMem rstream_;           // train_stream: per-step reconstruction errors
     DevMem sready_;            // train_stream: staging readiness flags (step index + 1 per buffer)
-    cudaEvent_t ev_used_[2] = {nullptr, nullptr};
+    cudaEvent_t ev_used_[kStage] = {};
+    cudaEvent_t ev_rng_[kStage] = {};
     cudaStream_t copy_stream_ = nullptr;
+    cudaStream_t rng_stream_ = nullptr;  // train_stream: the device generator runs ahead of the steps here
+    DevRng rng_;               // the device copy of the caller's std::mt19937 (u == null steps)
   public:
     void read_trace(unsigned long long* h) {
         B2N_CUDA(cudaDeviceSynchronize());

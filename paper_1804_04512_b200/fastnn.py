@@ -399,8 +399,23 @@ class Rbm:
         _lib.call("b2n_rbm_last_states", self._h, _f(h0), _f(hs), _f(v1), _f(h1))
         return h0, hs, v1, h1
 
+    def set_rng(self, rng: "Mt19937") -> None:
+        """load the caller's generator into the device generator (steps given no uniforms draw from it)"""
+        st = rng.state()
+        _lib.call("b2n_rbm_set_rng", self._h, st.ctypes.data_as(C.POINTER(C.c_uint)))
+
+    def get_rng(self, rng: "Mt19937") -> None:
+        """advance the caller's generator to the device generator's state"""
+        st = np.zeros(625, np.uint32)
+        _lib.call("b2n_rbm_get_rng", self._h, st.ctypes.data_as(C.POINTER(C.c_uint)))
+        rng.set_state(st)
+
     def stage(self, v0, uniforms) -> None:
+        """stage v0 and the uniforms (an array, or None: the device generator draws them)"""
         v0 = np.ascontiguousarray(v0, np.float32)
+        if uniforms is None:
+            _lib.call("b2n_rbm_stage", self._h, _f(v0), None, v0.shape[0])
+            return
         u = np.ascontiguousarray(uniforms, np.float64)
         _lib.call("b2n_rbm_stage", self._h, _f(v0), _d(u), v0.shape[0])
 
@@ -436,13 +451,18 @@ class Rbm:
         """CD-1 over consecutive host batches (rows [i*batch, (i+1)*batch) of v0 / uniforms per
         step), copies of step i+1 overlapped with step i; returns every step's recon error."""
         v0 = np.ascontiguousarray(v0, np.float32)
-        u = np.ascontiguousarray(uniforms, np.float64)
         if v0.ndim != 2 or v0.shape[1] != self.visible or v0.shape[0] % batch:
             raise ShapeError("train_stream: v0 must be (steps * batch, visible)")
         steps = v0.shape[0] // batch
+        out = np.zeros(steps, np.float64)
+        if isinstance(uniforms, Mt19937):  # each step's draws generated on the device ahead of it
+            self.set_rng(uniforms)
+            _lib.call("b2n_rbm_train_stream", self._h, _f(v0), None, steps, batch, lr, _d(out))
+            self.get_rng(uniforms)
+            return out
+        u = np.ascontiguousarray(uniforms, np.float64)
         if u.size < steps * batch * self.hidden:
             raise ShapeError("train_stream: need steps * batch * hidden uniforms")
-        out = np.zeros(steps, np.float64)
         _lib.call("b2n_rbm_train_stream", self._h, _f(v0), _d(u), steps, batch, lr, _d(out))
         return out
 
@@ -466,10 +486,16 @@ def cd_k_update(rbm: Rbm, v0, k: int, lr: float, uniforms, batch_global: int | N
         raise ShapeError("cd_k_update: expected a rank-2 tensor")
     if v0.shape[1] != rbm.visible:
         raise ShapeError("cd_k_update: visible extent mismatch")
+    out = C.c_double()
+    if isinstance(uniforms, Mt19937):  # the draws on the device from the caller's generator
+        rbm.set_rng(uniforms)
+        _lib.call("b2n_cd_k_update", rbm.handle, _f(v0), v0.shape[0], k, lr, None, batch_global or v0.shape[0],
+                  C.byref(out))
+        rbm.get_rng(uniforms)
+        return out.value
     u = np.ascontiguousarray(uniforms, np.float64).ravel()
     if u.size < k * v0.shape[0] * rbm.hidden:
         raise ShapeError("cd_k_update: need k * batch * hidden uniforms")
-    out = C.c_double()
     _lib.call("b2n_cd_k_update", rbm.handle, _f(v0), v0.shape[0], k, lr, _d(u), batch_global or v0.shape[0],
               C.byref(out))
     return out.value
@@ -538,8 +564,23 @@ class Crbm:
         _lib.call("b2n_crbm_last_states", self._h, _f(h0), _f(hs), _f(v1), _f(h1))
         return h0, hs, v1, h1
 
+    def set_rng(self, rng: "Mt19937") -> None:
+        st = rng.state()
+        _lib.call("b2n_crbm_set_rng", self._h, st.ctypes.data_as(C.POINTER(C.c_uint)))
+
+    def get_rng(self, rng: "Mt19937") -> None:
+        st = np.zeros(625, np.uint32)
+        _lib.call("b2n_crbm_get_rng", self._h, st.ctypes.data_as(C.POINTER(C.c_uint)))
+        rng.set_state(st)
+
     def stage(self, v0, uniforms) -> None:
+        """stage v0 and the uniforms (an array, or None: the device generator draws them)"""
         v0 = np.ascontiguousarray(v0, np.float32)
+        if uniforms is None:
+            if v0.ndim != 4 or v0.shape[1:] != (self.c_in, self.h, self.w):
+                raise ShapeError("crbm stage: visible batch does not match the model")
+            _lib.call("b2n_crbm_stage", self._h, _f(v0), None, v0.shape[0])
+            return
         u = np.ascontiguousarray(uniforms, np.float64)
         if v0.ndim != 4 or v0.shape[1:] != (self.c_in, self.h, self.w) or u.size < v0.shape[0] * self.k * self.oh * self.ow:
             raise ShapeError("crbm stage: visible batch / uniforms do not match the model")
@@ -567,10 +608,16 @@ def crbm_cd_update(m: Crbm, v0, lr: float, uniforms, batch_global: int | None = 
     v0 = np.ascontiguousarray(v0, np.float32)
     if v0.ndim != 4 or v0.shape[1] != m.c_in or v0.shape[2] != m.h or v0.shape[3] != m.w:
         raise ShapeError("crbm_cd_update: input does not match the model's visible shape")
+    out = C.c_double()
+    if isinstance(uniforms, Mt19937):  # the draws on the device from the caller's generator
+        m.set_rng(uniforms)
+        _lib.call("b2n_crbm_cd_update", m.handle, _f(v0), v0.shape[0], lr, None, batch_global or v0.shape[0],
+                  C.byref(out))
+        m.get_rng(uniforms)
+        return out.value
     u = np.ascontiguousarray(uniforms, np.float64).ravel()
     if u.size < v0.shape[0] * m.k * m.oh * m.ow:
         raise ShapeError("crbm_cd_update: need batch * k * oh * ow uniforms")
-    out = C.c_double()
     _lib.call("b2n_crbm_cd_update", m.handle, _f(v0), v0.shape[0], lr, _d(u), batch_global or v0.shape[0],
               C.byref(out))
     return out.value
@@ -583,6 +630,15 @@ class Mt19937:
 
     def __init__(self, seed: int):
         self._rs = np.random.RandomState(seed)
+
+    def state(self) -> np.ndarray:
+        """the libstdc++ state (_M_x[624], _M_p) as 625 uint32 -- what the device generator takes"""
+        _, key, pos, _, _ = self._rs.get_state(legacy=True)
+        return np.concatenate([np.asarray(key, np.uint32), np.asarray([pos], np.uint32)])
+
+    def set_state(self, st) -> None:
+        st = np.asarray(st, np.uint32)
+        self._rs.set_state(("MT19937", st[:624].copy(), int(st[624]), 0, 0.0))
 
     def canonical(self, n: int) -> np.ndarray:
         u = self._rs.randint(0, 2 ** 32, size=2 * n, dtype=np.uint64).reshape(n, 2).astype(np.float64)
@@ -599,15 +655,25 @@ class DbnReport:
     recon: list = field(default_factory=list)
 
 
-def dbn_pretrain(stack: list, data, epochs: int, lr: float, batch_size: int, rng: Mt19937) -> DbnReport:
+def dbn_pretrain(stack: list, data, epochs: int, lr: float, batch_size: int, rng: Mt19937,
+                 host_draws: bool = False) -> DbnReport:
     """fastnn::dbn_pretrain (energy.hpp:208-240): greedy CD-1 over a stack of Rbm on one device,
     data resident in HBM, each layer's hidden means computed on the device for the next; the
-    Bernoulli uniforms are drawn from `rng` in the reference's order (B x H per step)."""
+    Bernoulli uniforms are drawn from `rng` in the reference's order (B x H per step) -- on the
+    device (default; `rng` is advanced to match), or on the host through a callback."""
     data = np.ascontiguousarray(data, np.float32)
     if data.ndim != 2:
         raise ShapeError("dbn_pretrain: data must be (rows, visible)")
     arr = (C.c_void_p * max(len(stack), 1))(*[r.handle.value if hasattr(r.handle, "value") else r.handle
                                                for r in stack])
+
+    if not host_draws:
+        st = rng.state()
+        rec = np.zeros(max(len(stack) * epochs, 1))
+        _lib.call("b2n_dbn_pretrain", arr, len(stack), _f(data), data.shape[0], epochs, lr, batch_size, None,
+                  st.ctypes.data_as(C.c_void_p), _d(rec))
+        rng.set_state(st)
+        return DbnReport([list(rec[l * epochs:(l + 1) * epochs]) for l in range(len(stack))])
 
     def fill(_ctx, out, count):
         np.ctypeslib.as_array(out, shape=(count,))[:] = rng.canonical(count)
@@ -617,6 +683,15 @@ def dbn_pretrain(stack: list, data, epochs: int, lr: float, batch_size: int, rng
     _lib.call("b2n_dbn_pretrain", arr, len(stack), _f(data), data.shape[0], epochs, lr, batch_size,
               C.cast(cb, C.c_void_p), None, _d(rec))
     return DbnReport([list(rec[l * epochs:(l + 1) * epochs]) for l in range(len(stack))])
+
+
+def mt19937_draw(rng: Mt19937, n: int, device: int = 0) -> np.ndarray:
+    """the next n generate_canonical<double,53> draws of `rng`, generated on the GPU (rng advanced)"""
+    st = rng.state()
+    out = np.zeros(max(n, 1), np.float64)
+    _lib.call("b2n_mt19937_draw", device, st.ctypes.data_as(C.POINTER(C.c_uint)), _d(out), n)
+    rng.set_state(st)
+    return out[:n]
 
 
 def nccl_unique_id() -> bytes:

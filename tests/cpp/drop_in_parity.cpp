@@ -5,6 +5,7 @@
 // run by tests/test_gpu_cpp.py on a GPU box.
 #include <cmath>
 #include <cstdio>
+#include <sstream>
 #include <cstring>
 #include <fstream>
 #include <iterator>
@@ -127,6 +128,59 @@ bool fit_checkpoint_criterion() {
 
 }  // namespace
 
+// the device generator against std::mt19937 + generate_canonical<double,53>: the state layout the
+// header reads (against libstdc++'s own `os << rng`), 10^6 draws bit for bit from a mid-block
+// position, the advanced state, and a 5-step cd1_stream whose generator must end where five
+// reference cd_k_update calls leave theirs
+static bool device_rng_criterion() {
+    std::mt19937 g(1234);
+    for (int i = 0; i < 77; ++i) g();  // position 77 of the first block
+    unsigned st[625];
+    b200nn::detail::mt_export(g, st);
+    std::ostringstream a, b;
+    a << g;
+    for (int i = 0; i < 624; ++i) b << st[i] << ' ';
+    b << st[624];
+    bool ok = a.str() == b.str();
+    const long long n = 1000003;
+    std::vector<double> dev((size_t)n);
+    b200nn::check(b2n_mt19937_draw(0, st, dev.data(), n));
+    long long bad = 0;
+    for (long long i = 0; i < n; ++i) bad += dev[(size_t)i] != std::generate_canonical<double, 53>(g);
+    std::mt19937 back;
+    b200nn::detail::mt_import(back, st);
+    const bool state_ok = back == g;
+    // cd1_stream vs five cd_k_update calls of the reference
+    fastnn::Rbm ref(64, 96);
+    b200nn::Rbm dev_rbm(64, 96);
+    std::mt19937 ia(7), ib(7);
+    ref.init(ia);
+    dev_rbm.init(ib);
+    const std::size_t steps = 5, batch = 20;
+    std::vector<float> v(steps * batch * 96);
+    std::mt19937 vr(9);
+    std::bernoulli_distribution bit(0.3);
+    for (float& x : v) x = bit(vr) ? 1.0f : 0.0f;
+    std::mt19937 ra(11), rb(11);
+    std::vector<double> rr;
+    for (std::size_t i = 0; i < steps; ++i) {
+        fastnn::Tensor t = fastnn::make_tensor({batch, 96});
+        for (std::size_t r = 0; r < batch; ++r)
+            for (std::size_t j = 0; j < 96; ++j) t.at(r, j) = v[(i * batch + r) * 96 + j];
+        rr.push_back(fastnn::cd_k_update(ref, t, 1, 0.05f, ra));
+    }
+    const std::vector<double> rd = b200nn::cd1_stream(dev_rbm, v.data(), steps, batch, 0.05f, rb);
+    double rec_err = 0.0;
+    for (std::size_t i = 0; i < steps; ++i) rec_err = std::max(rec_err, std::fabs(rr[i] - rd[i]) / rr[i]);
+    const bool stream_ok = ra == rb && rec_err < 1e-3;
+    ok = ok && bad == 0 && state_ok && stream_ok;
+    std::printf("criterion device_rng: %s -- layout %s, %lld of %lld draws differ, state %s, cd1_stream rng %s "
+                "(recon rel err %.2e)\n",
+                ok ? "PASS" : "FAIL", a.str() == b.str() ? "ok" : "DIFFERS", bad, n, state_ok ? "equal" : "DIFFERS",
+                ra == rb ? "equal" : "DIFFERS", rec_err);
+    return ok;
+}
+
 int main() {
     using FL = fastnn::LayerDesc;
     using BL = b200nn::LayerDesc;
@@ -165,9 +219,11 @@ int main() {
         std::vector<float> w, bv, bh;
         dev.get(w, bv, bh);
         const double ew = norm_err(w, ref.w), ev = norm_err(bv, ref.bv), eh = norm_err(bh, ref.bh);
-        const bool r_ok = ew < 1e-3 && ev < 1e-3 && eh < 1e-3 && std::fabs(rf - rd) < 1e-3 * rf;
-        std::printf("criterion rbm_cd1: %s -- recon %.9g vs %.9g, W %.2e bv %.2e bh %.2e\n", r_ok ? "PASS" : "FAIL", rd,
-                    rf, ew, ev, eh);
+        // the device drew the Bernoulli stream from rb's state: both generators end in the same state
+        const bool same_rng = ra == rb;
+        const bool r_ok = ew < 1e-3 && ev < 1e-3 && eh < 1e-3 && std::fabs(rf - rd) < 1e-3 * rf && same_rng;
+        std::printf("criterion rbm_cd1: %s -- recon %.9g vs %.9g, W %.2e bv %.2e bh %.2e, rng states %s\n",
+                    r_ok ? "PASS" : "FAIL", rd, rf, ew, ev, eh, same_rng ? "equal" : "DIFFER");
         ok &= r_ok;
     }
     {  // convolutional RBM CD-1 (crbm_cd_update) with the same generators on both sides
@@ -197,11 +253,13 @@ int main() {
         std::vector<float> kk, bv, bh;
         dev.get(kk, bv, bh);
         const double ek = norm_err(kk, ref.kernels), ev = norm_err(bv, ref.bv), eh = norm_err(bh, ref.bh);
-        const bool c_ok = ek < 1e-3 && ev < 1e-3 && eh < 1e-3 && std::fabs(rf - rd) < 1e-3 * rf;
-        std::printf("criterion crbm_cd1: %s -- recon %.9g vs %.9g, kernels %.2e bv %.2e bh %.2e\n",
-                    c_ok ? "PASS" : "FAIL", rd, rf, ek, ev, eh);
+        const bool same_rng = ra == rb;
+        const bool c_ok = ek < 1e-3 && ev < 1e-3 && eh < 1e-3 && std::fabs(rf - rd) < 1e-3 * rf && same_rng;
+        std::printf("criterion crbm_cd1: %s -- recon %.9g vs %.9g, kernels %.2e bv %.2e bh %.2e, rng states %s\n",
+                    c_ok ? "PASS" : "FAIL", rd, rf, ek, ev, eh, same_rng ? "equal" : "DIFFER");
         ok &= c_ok;
     }
     ok &= fit_checkpoint_criterion();
+    ok &= device_rng_criterion();
     return ok ? 0 : 1;
 }
