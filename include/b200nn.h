@@ -225,7 +225,8 @@ int b2n_rbm_recon(b2n_rbm* rbm, double* recon);
 /* `steps` CD-1 updates (k = 1) over consecutive host batches -- the reference's loop of
  * cd_k_update calls: step i uses rows [i*batch, (i+1)*batch) of v0_host (steps*batch x visible)
  * and of uniforms_host (steps*batch x hidden). The host->device copy of step i+1 overlaps step i
- * (double-buffered staging on a copy stream); recon_out[i] = step i's reconstruction error. */
+ * (staged up to 4 steps ahead on a copy stream); recon_out[i] = step i's reconstruction error.
+ * v0_host / uniforms_host may also be device pointers (device-resident batches). */
 int b2n_rbm_train_stream(b2n_rbm* rbm, const float* v0_host, const double* uniforms_host, long long steps,
                          long long batch, float lr, double* recon_out);
 int b2n_rbm_stream(b2n_rbm* rbm, void** cuda_stream);

@@ -49,8 +49,32 @@ static __global__ void recon_accum_kernel(const double* __restrict__ part, int t
     *acc += recon_tree_sum(part, tiles, cap, B) / (double)B;
 }
 
+// lo = x - trunc_tf32(x), the 3xTF32 correction operand of W kept next to W for the fused step
+static __global__ void tf32_lo_kernel(const float4* __restrict__ x, float4* __restrict__ lo, long long n4) {
+    pdl_wait();
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+        const float4 v = x[i];
+        lo[i] = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+    }
+}
+
+// v0 rows into a visible staging buffer (pitch ldd) plus their tf32 lo parts (copy == 0: already there)
+static __global__ void stage_rows_kernel(const float* __restrict__ src, long long lds, float* __restrict__ dst,
+                                         float* __restrict__ dlo, long long ldd, int B, int V, int copy) {
+    pdl_wait();
+    const int v4 = V / 4;  // V % 4 == 0 (the fused step's envelope)
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)B * v4;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / v4, c = (i % v4) * 4;
+        const float4 x = *reinterpret_cast<const float4*>(src + r * lds + c);
+        if (copy) *reinterpret_cast<float4*>(dst + r * ldd + c) = x;
+        *reinterpret_cast<float4*>(dlo + r * ldd + c) = make_float4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w));
+    }
+}
+
 class Rbm {
   public:
+    static constexpr int kStage = 4;  // visible-side buffers: train_stream stages up to 4 steps ahead
     Rbm(long long H, long long V, int device, int precision)
         : H_(H), V_(V), device_(device), x3_(precision == B2N_TF32X3) {
         if (H < 1 || V < 1) throw Error(B2N_ESHAPE, "rbm extents must be positive");
@@ -59,6 +83,7 @@ class Rbm {
         ldw_ = round_up(V + 1, 8);
         nW_ = round_up((H + 1) * ldw_, 32);
         W_.alloc(nW_ * 4);
+        Wlo_.alloc(nW_ * 4);
         G_.alloc(nW_ * 4);
         h_recon_.alloc(8 * 1024);
     }
@@ -86,6 +111,7 @@ class Rbm {
         set(w.data(), zv.data(), zh.data());
     }
     void set(const float* w, const float* bv, const float* bh) {
+        wlo_valid_ = false;
         float* W = W_.as<float>();
         B2N_CUDA(cudaMemsetAsync(W, 0, nW_ * 4, stream_));
         B2N_CUDA(cudaMemcpy2DAsync(W, ldw_ * 4, w, V_ * 4, V_ * 4, H_, cudaMemcpyHostToDevice, stream_));
@@ -125,7 +151,8 @@ class Rbm {
             rp.recon_out = recon_host_dev_;
             recon_mapped_ = true;
             launch_ex(rbm_cd1_fused_kernel, dim3(kRfSlices, rp.jt), dim3(kRfThreads), (size_t)kRfSmem, stream_, 1u,
-                      pl.maps[0], pl.maps[1], pl.maps[2], pl.maps[3], pl.maps[4], pl.maps[5], rp);
+                      pl.maps[0], rp);
+            vb_ = 0;
         } else {
             stage(v0, u, B, k);
             launch(pl);
@@ -137,8 +164,10 @@ class Rbm {
     }
     void stage(const float* v0, const double* u, long long B, int k = 1) {
         ensure_capacity(B, k);
-        float* Vc = Vcat_.as<float>();
+        float* Vc = Vcat_[0].as<float>();
         B2N_CUDA(cudaMemcpy2DAsync(Vc, ldv_ * 4, v0, V_ * 4, V_ * 4, B, cudaMemcpyHostToDevice, stream_));
+        stage_lo(0, B, stream_);
+        vb_ = 0;
         if (u)
             B2N_CUDA(cudaMemcpyAsync(U_.p, u, (size_t)k * B * H_ * 8, cudaMemcpyHostToDevice, stream_));
         else  // u == null: draw the k * B * H uniforms from the device generator (set_rng)
@@ -167,7 +196,7 @@ class Rbm {
     void last_states(float* h0, float* hs, float* v1, float* h1) {
         const long long B = last_B_;
         const float* Hc = Hcat_.as<float>();
-        const float* Vc = Vcat_.as<float>();
+        const float* Vc = Vcat_[vb_].as<float>();
         const auto D2H = cudaMemcpyDeviceToHost;
         if (h0) B2N_CUDA(cudaMemcpy2DAsync(h0, H_ * 4, Hc, ldh_ * 4, H_ * 4, B, D2H, stream_));
         if (hs) B2N_CUDA(cudaMemcpy2DAsync(hs, H_ * 4, HS_.p, ldhs_ * 4, H_ * 4, B, D2H, stream_));
@@ -209,6 +238,7 @@ class Rbm {
         const long long n = nW_;
         launch_ex(axpy_kernel, dim3(grid_for(n / 4)), dim3(256), 0, stream_, 1u, reinterpret_cast<float4*>(W_.as<float>()),
                   reinterpret_cast<const float4*>(G_.as<float>()), n / 4, lr / static_cast<float>(Bg));
+        wlo_valid_ = false;
         B2N_CUDA(cudaStreamSynchronize(stream_));
     }
     // the caller's std::mt19937 (625 words: state, position) for the steps that take no uniforms
@@ -249,8 +279,10 @@ class Rbm {
             } else {  // the device generator (set_rng): no host draws, no copies
                 rng_.draw(U_.as<double>(), B * H_, stream_);
             }
-            B2N_CUDA(cudaMemcpy2DAsync(Vcat_.p, ldv_ * 4, data + lo * ldd, ldd * 4, V_ * 4, B, cudaMemcpyDeviceToDevice,
-                                       stream_));
+            B2N_CUDA(cudaMemcpy2DAsync(Vcat_[0].p, ldv_ * 4, data + lo * ldd, ldd * 4, V_ * 4, B,
+                                       cudaMemcpyDeviceToDevice, stream_));
+            stage_lo(0, B, stream_);
+            vb_ = 0;
             Plan& pl = plan_for(B, 1, lr, B);
             launch(pl);
             recon_accum_kernel<<<1, 32, 0, stream_>>>(recon_.as<double>(), recon_tiles_, cap_, B, racc_.as<double>());
@@ -265,9 +297,10 @@ class Rbm {
 
     // A stream of CD-1 steps over host batches (the reference's training loop of cd_k_update calls,
     // energy.hpp:131): step i takes rows [i B, (i + 1) B) of v0 (pitch V) and of the uniforms
-    // (pitch H). The H2D of step i + 1 runs on a copy stream into the other of two device staging
-    // buffers while step i computes (the fused kernel reads its v0 / uniforms from the staging
-    // buffer it is handed); each step's reconstruction error lands in a device array read back
+    // (pitch H, or null: drawn on the device). Up to kStage steps ahead of the compute stream, a copy
+    // stream lands step i's v0 in visible buffer i % kStage (+ its tf32 lo parts) and the device
+    // generator draws its uniforms on a third stream; the step kernel polls a readiness flag instead
+    // of a cross-stream event. Each step's reconstruction error lands in a device array read back
     // once. recon_out[i] = step i's cd_k_update return value.
     void train_stream(const float* v0, const double* u, long long steps, long long B, float lr, double* recon_out) {
         if (dp_) throw Error(B2N_EPARAM, "train_stream: data-parallel RBMs step through run_staged");
@@ -286,7 +319,6 @@ class Rbm {
         }
         prepare(pl);
         for (int j = 0; j < kStage; ++j) {
-            if (sv_[j].bytes < (size_t)(B * V_ * 4)) sv_[j].alloc((size_t)(B * V_ * 4));
             if (su_[j].bytes < (size_t)(B * H_ * 8)) su_[j].alloc((size_t)(B * H_ * 8));
             if (!ev_used_[j]) B2N_CUDA(cudaEventCreateWithFlags(&ev_used_[j], cudaEventDisableTiming));
             if (!ev_rng_[j]) B2N_CUDA(cudaEventCreateWithFlags(&ev_rng_[j], cudaEventDisableTiming));
@@ -304,10 +336,11 @@ class Rbm {
         for (long long i = 0; i < steps; ++i) {
             const int j = (int)(i % kStage);
             B2N_CUDA(cudaStreamWaitEvent(copy_stream_, ev_used_[j], 0));  // step i - kStage done with buffer j
-            B2N_CUDA(cudaMemcpyAsync(sv_[j].p, v0 + i * B * V_, (size_t)(B * V_ * 4), cudaMemcpyHostToDevice,
-                                     copy_stream_));
+            B2N_CUDA(cudaMemcpy2DAsync(Vcat_[j].p, ldv_ * 4, v0 + i * B * V_, V_ * 4, V_ * 4, B, cudaMemcpyDefault,
+                                       copy_stream_));  // host (pinned or not) or device-resident batches
+            stage_lo(j, B, copy_stream_);
             if (u)
-                B2N_CUDA(cudaMemcpyAsync(su_[j].p, u + i * B * H_, (size_t)(B * H_ * 8), cudaMemcpyHostToDevice,
+                B2N_CUDA(cudaMemcpyAsync(su_[j].p, u + i * B * H_, (size_t)(B * H_ * 8), cudaMemcpyDefault,
                                          copy_stream_));
             else {  // step i's draws from the device generator on its own stream, up to kStage steps ahead
                 B2N_CUDA(cudaStreamWaitEvent(rng_stream_, ev_used_[j], 0));
@@ -318,15 +351,16 @@ class Rbm {
             unsigned* flag = sready_.as<unsigned>() + j;
             stream_write_u32(copy_stream_, flag, (unsigned)(i + 1));
             RbmFusedParams rp = pl.rp;
-            rp.v0_src = sv_[j].as<float>();
-            rp.ld_src = V_;
+            rp.Vcat = Vcat_[j].as<float>();
+            rp.Vlo = Vlo_[j].as<float>();
             rp.u_src = su_[j].as<double>();
             rp.ready = flag;
             rp.ready_val = (unsigned)(i + 1);
             rp.recon_out = rstream_.as<double>() + i;
             launch_ex(rbm_cd1_fused_kernel, dim3(kRfSlices, rp.jt), dim3(kRfThreads), (size_t)kRfSmem, stream_, 1u,
-                      pl.maps[0], pl.maps[1], pl.maps[2], pl.maps[3], pl.maps[4], pl.maps[5], rp);
+                      pl.maps[j], rp);
             B2N_CUDA(cudaEventRecord(ev_used_[j], stream_));
+            vb_ = j;
         }
         B2N_CUDA(cudaEventRecord(ev_used_[0], copy_stream_));  // after the last draw (copy stream waited on it)
         B2N_CUDA(cudaStreamWaitEvent(stream_, ev_used_[0], 0));
@@ -358,7 +392,8 @@ class Rbm {
     std::vector<OpStats> profile(int steps, float lr, long long Bg) {
         if (!staged_B_) throw Error(B2N_EPARAM, "profile before stage");
         Plan& pl = plan_for(staged_B_, staged_k_, lr, Bg ? Bg : staged_B_);
-        if (hcol_B_ != pl.B) launch(pl);  // sets the +1/-1 column
+        prepare(pl);  // the +1/-1 column, W's lo companion
+        if (hcol_B_ != pl.B) launch(pl);
         return profile_ops(pl.ops, steps, stream_);
     }
 
@@ -372,7 +407,7 @@ class Rbm {
         int recon_tiles = 1;
         bool fused = false;         // rp / maps describe the single fused launch
         RbmFusedParams rp;
-        CUtensorMap maps[6];
+        RbmMaps maps[kStage];
         cudaGraphExec_t graph = nullptr;
         ~Plan() {
             if (graph) cudaGraphExecDestroy(graph);
@@ -389,13 +424,18 @@ class Rbm {
         ldv_ = round_up(V_ + 1, 8);
         ldh_ = round_up(H_ + 1, 8);
         ldhs_ = round_up(H_, 8);
-        Vcat_.alloc(2 * cap_ * ldv_ * 4);
+        for (int k = 0; k < kStage; ++k) {
+            Vcat_[k].alloc(2 * cap_ * ldv_ * 4);
+            Vlo_[k].alloc(2 * cap_ * ldv_ * 4);
+        }
         Hcat_.alloc(2 * cap_ * ldh_ * 4);
+        Hlo_.alloc(2 * cap_ * ldh_ * 4);
         HS_.alloc(cap_ * ldhs_ * 4);
         U_.alloc((size_t)kcap_ * cap_ * H_ * 8);
         recon_.alloc((size_t)cap_ * 64 * 8);
         if (h_recon_.bytes < (size_t)cap_ * 64 * 8) h_recon_.alloc((size_t)cap_ * 64 * 8);
-        set_column_kernel<<<grid_for(2 * cap_), 256, 0, stream_>>>(Vcat_.as<float>(), 2 * cap_, ldv_, V_, 1.0f);
+        for (int k = 0; k < kStage; ++k)
+            set_column_kernel<<<grid_for(2 * cap_), 256, 0, stream_>>>(Vcat_[k].as<float>(), 2 * cap_, ldv_, V_, 1.0f);
         B2N_CUDA(cudaGetLastError());
         B2N_CUDA(cudaStreamSynchronize(stream_));
     }
@@ -453,7 +493,7 @@ class Rbm {
         const int B = (int)pl.B, H = (int)H_, V = (int)V_;
         const int jt = (H + 1 + kRfTileH - 1) / kRfTileH;
         float* W = W_.as<float>();
-        float* Vc = Vcat_.as<float>();
+        float* Vc = Vcat_[0].as<float>();
         float* Hc = Hcat_.as<float>();
         if (!fused_ws_.p) {
             fused_ws_.alloc((size_t)8 * 128 * kRfSlices * kRfSliceW * 4 + (size_t)8 * kRfSlices * 128 * kRfTileH * 4);
@@ -471,6 +511,9 @@ class Rbm {
         rp.W = W;
         rp.Vcat = Vc;
         rp.Hcat = Hc;
+        rp.Wlo = Wlo_.as<float>();
+        rp.Vlo = Vlo_[0].as<float>();
+        rp.Hlo = Hlo_.as<float>();
         rp.HS = HS_.as<float>();
         rp.u = U_.as<double>();
         rp.row_part = recon_.as<double>();
@@ -494,33 +537,50 @@ class Rbm {
             if (!trace_.p) trace_.alloc(256 * 8);
             rp.trace = trace_.as<unsigned long long>();
         }
-        // TMA maps: K-major operands of phases 1-3, MN-major ones of phases 2 and 4 (see rbm_fused.cuh)
-        const CUtensorMap mVk = make_map_2d(Vc, V, 2 * B, ldv_, 32, 128);
-        const CUtensorMap mWk = make_map_2d(W, V, H, ldw_, 32, kRfTileH);
-        const CUtensorMap mHSk = make_map_2d(HS_.as<float>(), H, B, ldhs_, 32, 128);
-        const CUtensorMap mWmn = make_map_2d(W, V, H, ldw_, 32, 32, true);
-        const CUtensorMap mVmn = make_map_2d(Vc, V + 1, 2 * B, ldv_, 32, 32, true);
-        const CUtensorMap mHmn = make_map_2d(Hc, H + 1, 2 * B, ldh_, 32, 32, true);
+        // TMA maps: K-major operands of phases 1-3, MN-major ones of phases 2 and 4 (see rbm_fused.cuh),
+        // each with its tf32 lo companion
+        RbmMaps mp;
+        const float* Wl = Wlo_.as<float>();
+        const float* Vl = Vlo_[0].as<float>();
+        const float* Hl = Hlo_.as<float>();
+        mp.vk = make_map_2d(Vc, V, 2 * B, ldv_, 32, 128);
+        mp.wk = make_map_2d(W, V, H, ldw_, 32, kRfTileH);
+        mp.hsk = make_map_2d(HS_.as<float>(), H, B, ldhs_, 32, 128);
+        mp.wmn = make_map_2d(W, V, H, ldw_, 32, 32, true);
+        mp.vmn = make_map_2d(Vc, V + 1, 2 * B, ldv_, 32, 32, true);
+        mp.hmn = make_map_2d(Hc, H + 1, 2 * B, ldh_, 32, 32, true);
+        mp.vk_lo = make_map_2d(Vl, V, 2 * B, ldv_, 32, 128);
+        mp.wk_lo = make_map_2d(Wl, V, H, ldw_, 32, kRfTileH);
+        mp.wmn_lo = make_map_2d(Wl, V, H, ldw_, 32, 32, true);
+        mp.vmn_lo = make_map_2d(Vl, V + 1, 2 * B, ldv_, 32, 32, true);
+        mp.hmn_lo = make_map_2d(Hl, H + 1, 2 * B, ldh_, 32, 32, true);
         const double flops = 2.0 * B * H * V * 4, bytes = 4.0 * ((double)H * V * 4 + (double)B * (V + H) * 6);
         pl.ops.push_back(Op([=](cudaStream_t st) {
-            launch_ex(rbm_cd1_fused_kernel, dim3(kRfSlices, jt), dim3(kRfThreads), (size_t)kRfSmem, st, 1u, mVk, mWk,
-                      mHSk, mWmn, mVmn, mHmn, rp);
+            launch_ex(rbm_cd1_fused_kernel, dim3(kRfSlices, jt), dim3(kRfThreads), (size_t)kRfSmem, st, 1u, mp, rp);
         }, dp_ || grad_only_ ? "rbm.cd1_fused(grad)" : "rbm.cd1_fused", flops, bytes));
         if (dp_) {  // sum the shards' raw dW / dbh / dbv, then the same update on every replica
             DpComm* dp = dp_.get();
             float* G = G_.as<float>();
             const long long n = nW_;
             const float scale = pl.lr / static_cast<float>(pl.Bg);
+            float* Wl2 = Wlo_.as<float>();
             pl.ops.push_back(Op([=](cudaStream_t s) {
                 dp->allreduce_f32(G, (size_t)n, s);
                 launch_ex(axpy_kernel, dim3(grid_for(n / 4)), dim3(256), 0, s, 1u, reinterpret_cast<float4*>(W),
                           reinterpret_cast<const float4*>(G), n / 4, scale);
+                launch_ex(tf32_lo_kernel, dim3(grid_for(n / 4)), dim3(256), 0, s, 1u, reinterpret_cast<const float4*>(W),
+                          reinterpret_cast<float4*>(Wl2), n / 4);
             }, "allreduce+update", 0.0, (double)n * 12));
         }
         pl.fused = true;
         pl.rp = rp;
-        const CUtensorMap ms[6] = {mVk, mWk, mHSk, mWmn, mVmn, mHmn};
-        std::memcpy(pl.maps, ms, sizeof(ms));
+        for (int k = 0; k < kStage; ++k) {  // one map set per visible staging buffer
+            pl.maps[k] = mp;
+            pl.maps[k].vk = make_map_2d(Vcat_[k].as<float>(), V, 2 * B, ldv_, 32, 128);
+            pl.maps[k].vmn = make_map_2d(Vcat_[k].as<float>(), V + 1, 2 * B, ldv_, 32, 32, true);
+            pl.maps[k].vk_lo = make_map_2d(Vlo_[k].as<float>(), V, 2 * B, ldv_, 32, 128);
+            pl.maps[k].vmn_lo = make_map_2d(Vlo_[k].as<float>(), V + 1, 2 * B, ldv_, 32, 32, true);
+        }
         pl.recon_tiles = kRfSlices;
         pl.nk = dp_ ? 2 : 1;
         last_kernels_ = pl.nk;
@@ -534,7 +594,7 @@ class Rbm {
         const int B = (int)pl.B;
         float* W = W_.as<float>();
         float* G = G_.as<float>();
-        float* Vc = Vcat_.as<float>();
+        float* Vc = Vcat_[0].as<float>();
         float* Hc = Hcat_.as<float>();
         float* HSp = HS_.as<float>();
         double* U = U_.as<double>();
@@ -635,6 +695,22 @@ class Rbm {
         }
         recon_tiles_ = pl.recon_tiles;
         recon_mapped_ = false;
+        if (!pl.fused) {
+            wlo_valid_ = false;  // the split path updates W without its lo companion
+        } else if (!wlo_valid_) {
+            const long long n = nW_;
+            launch_ex(tf32_lo_kernel, dim3(grid_for(n / 4)), dim3(256), 0, stream_, 1u,
+                      reinterpret_cast<const float4*>(W_.as<float>()), reinterpret_cast<float4*>(Wlo_.as<float>()), n / 4);
+            wlo_valid_ = true;
+        }
+    }
+
+    // the tf32 lo parts of v0 rows [0, B) of visible buffer k (after their copy into Vcat_[k])
+    void stage_lo(int k, long long B, cudaStream_t st) {
+        if (V_ % 4) return;  // the fused step (the only reader) needs V % 4 == 0
+        const float* Vc = Vcat_[k].as<float>();
+        launch_ex(stage_rows_kernel, dim3(grid_for(B * V_ / 4)), dim3(256), 0, st, 1u, Vc, ldv_, (float*)nullptr,
+                  Vlo_[k].as<float>(), ldv_, (int)B, (int)V_, 0);
     }
 
     void launch(Plan& pl) {
@@ -662,13 +738,16 @@ class Rbm {
     long long ldw_ = 0, nW_ = 0, ldv_ = 0, ldh_ = 0, ldhs_ = 0;
     long long cap_ = 0;
     int kcap_ = 0;
-    DevMem W_, G_, Vcat_, Hcat_, HS_, U_, recon_;
+    DevMem W_, G_, Hcat_, HS_, U_, recon_;
+    DevMem Vcat_[kStage];      // [v0; v1] (+ ones column): buffer 0 for every path, 0..3 in rotation for train_stream
+    DevMem Wlo_, Vlo_[kStage], Hlo_;  // tf32 lo parts of W_aug / Vcat / Hcat (the fused step's 3xTF32 operands)
+    int vb_ = 0;               // the Vcat buffer of the last step
+    bool wlo_valid_ = false;   // Wlo_ matches W_ (kept by the fused step; anything else that writes W clears it)
     DevMem fused_ws_, gbar_, trace_;
     HostPinned ubuf_[2];       // train_epoch: double-buffered uniforms
     cudaEvent_t uev_[2] = {nullptr, nullptr};
     DevMem racc_;              // train_epoch: device sum of per-step reconstruction errors
-    static constexpr int kStage = 4;
-    DevMem sv_[kStage], su_[kStage];  // train_stream: device staging of v0 / uniforms, kStage deep
+    DevMem su_[kStage];        // train_stream: device staging of the uniforms, kStage deep
     DevMem rstream_;           // train_stream: per-step reconstruction errors
     DevMem sready_;            // train_stream: staging readiness flags (step index + 1 per buffer)
     cudaEvent_t ev_used_[kStage] = {};

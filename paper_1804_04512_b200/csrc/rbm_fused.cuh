@@ -63,6 +63,18 @@ struct RbmFusedParams {
     // follows the allreduce (NCCL inside the step graph, or the caller's for b2n_rbm_set_grad_only)
     float* G;
     int grad_only;
+    // tf32 lo parts (x - trunc_tf32(x)) of W_aug, Vcat and Hcat, same layouts: written next to every
+    // store of the operand, read by TMA as the 3xTF32 correction terms (the 0/1 samples need none)
+    float* Wlo;
+    float* Vlo;
+    float* Hlo;
+};
+
+// the step's TMA maps (hi operand, lo companion): K-major operands of phases 1-3, MN-major ones of
+// phases 2 and 4
+struct alignas(64) RbmMaps {
+    CUtensorMap vk, wk, hsk, wmn, vmn, hmn;
+    CUtensorMap vk_lo, wk_lo, wmn_lo, vmn_lo, hmn_lo;
 };
 
 __device__ __forceinline__ unsigned* sbar_of(const RbmFusedParams& p, int s) { return p.gbar + 2 * s; }
@@ -94,59 +106,57 @@ __device__ __forceinline__ void rf_grid_sync(unsigned* gbar, unsigned nblocks) {
 }
 
 // one 3xTF32 product of this phase into TMEM columns [0, N): nkb K-blocks of 32, operands by TMA into a
-// ring of ns stages of 2*(a_bytes + b_bytes) (hi | lo) carved for this phase, with this phase's own
-// full / empty barriers (fresh parity). load(kb, a_dst, b_dst, bar) issues the TMA boxes of K-block kb
-// (thread 0); tph = running TMEM-barrier phase.
+// ring of ns stages carved for this phase, with this phase's own full / empty barriers (fresh parity).
+// Every operand arrives PRE-SPLIT: its tf32 lo part (x - trunc_tf32(x)) lives in a companion array
+// written by the producer of the operand (the phase epilogues, the v0 staging, the W update), so the
+// loop is a pure TMA -> MMA pipeline: thread 0 streams the K-blocks as slots drain, warp 1 issues the
+// MMAs, nobody else touches the ring (no per-block split pass, no per-block CTA barrier).
+// load(kb, a_hi, b_hi, b_lo, a_lo, bar) issues the boxes of K-block kb (a_lo == null when a_lo_bytes
+// == 0: an operand exact in tf32, e.g. the 0/1 hidden samples); tph = running TMEM-barrier phase.
 template <class Load>
 __device__ __forceinline__ void rf_product(uint8_t* ring, uint64_t* full, uint64_t* empty, uint64_t* tbar, int& tph,
-                                           int ns, int nkb, int a_bytes, int b_bytes, bool a_mn, bool b_mn,
-                                           uint32_t idesc, uint32_t idesc2, Load load) {
+                                           int ns, int nkb, int a_bytes, int b_bytes, bool a_lo, bool a_mn,
+                                           bool b_mn, uint32_t idesc, uint32_t idesc2, Load load) {
     // stage = A hi | B hi | B lo | A lo: B hi and B lo are adjacent along N, so ONE MMA with N doubled
     // (idesc2) computes a_hi.b_hi into columns [0, N) and a_hi.b_lo into [N, 2N); a second MMA adds
-    // a_lo.b_hi into [0, N). Two MMAs per K step instead of three; rf_tmem_to_smem folds the halves.
+    // a_lo.b_hi into [0, N). rf_tmem_to_smem folds the halves.
     const int warp = threadIdx.x >> 5;
     const int sb = 2 * (a_bytes + b_bytes);
+    const uint32_t tx = (uint32_t)(a_bytes + 2 * b_bytes + (a_lo ? a_bytes : 0));
     auto slot = [&](int g) { return ring + (g % ns) * sb; };
-    if (threadIdx.x == 0)
-        for (int i = 0; i < nkb && i < ns; ++i) {
-            mbar_arrive_expect_tx(&full[i], (uint32_t)(a_bytes + b_bytes));
-            load(i, slot(i), slot(i) + a_bytes, &full[i]);
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < nkb; ++i) {
+            const int st = i % ns;
+            if (i >= ns) mbar_wait(&empty[st], ((i / ns) - 1) & 1);
+            uint8_t* d = slot(i);
+            mbar_arrive_expect_tx(&full[st], tx);
+            load(i, d, d + a_bytes, d + a_bytes + b_bytes, a_lo ? d + a_bytes + 2 * b_bytes : nullptr, &full[st]);
         }
-    for (int i = 0; i < nkb; ++i) {
-        const int s = i % ns;
-        uint8_t* st = slot(i);
-        mbar_wait(&full[s], (i / ns) & 1);
-        split_lo(st + a_bytes, st + a_bytes + b_bytes, b_bytes, threadIdx.x, kRfThreads);
-        split_lo(st, st + a_bytes + 2 * b_bytes, a_bytes, threadIdx.x, kRfThreads);
-        fence_proxy_async_smem();
-        __syncthreads();
-        if (warp == 1) {
+    } else if (warp == 1) {
+        const uint64_t a_lo_off = (uint64_t)((a_bytes + 2 * b_bytes) >> 4);
+        for (int i = 0; i < nkb; ++i) {
+            const int st = i % ns;
+            mbar_wait(&full[st], (i / ns) & 1);
             tc_fence_after();
-            const uint32_t a0 = smem_u32(st), b0 = a0 + (uint32_t)a_bytes;
-            const uint64_t a_lo = (uint64_t)((a_bytes + 2 * b_bytes) >> 4);
+            const uint32_t a0 = smem_u32(slot(i)), b0 = a0 + (uint32_t)a_bytes;
             uint64_t da = a_mn ? desc_mnmajor(a0, 0) : desc_kmajor(a0, 0);
             uint64_t db = b_mn ? desc_mnmajor(b0, 0) : desc_kmajor(b0, 0);
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk, da += a_mn ? 64 : 2, db += b_mn ? 64 : 2) {
                 mma_tf32_warp(0u, da, db, idesc2, (i | kk) != 0);
-                mma_tf32_warp(0u, da + a_lo, db, idesc, 1);
+                if (a_lo) mma_tf32_warp(0u, da + a_lo_off, db, idesc, 1);
             }
-            mma_commit_warp(&empty[s]);
+            mma_commit_warp(&empty[st]);
             if (i == nkb - 1) mma_commit_warp(tbar);
-        }
-        // refill the PREVIOUS block's slot (its MMAs have had this block's split to retire) with the block
-        // ns - 1 ahead; waiting on the slot just issued would serialise TMA behind every MMA batch
-        if (threadIdx.x == 0 && i >= 1 && i - 1 + ns < nkb) {
-            const int ip = i - 1, sp = ip % ns, i2 = ip + ns;
-            mbar_wait(&empty[sp], (ip / ns) & 1);
-            mbar_arrive_expect_tx(&full[sp], (uint32_t)(a_bytes + b_bytes));
-            load(i2, slot(i2), slot(i2) + a_bytes, &full[sp]);
         }
     }
     mbar_wait(tbar, tph & 1);
     ++tph;
     tc_fence_after();
 }
+
+// x - trunc_tf32(x): the tf32 lo part the tensor core's truncation leaves behind (3xTF32)
+__device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 // TMEM [128 lanes][2*ncols] -> smem tile (pitch tp floats) as cols[c] + cols[c + ncols] (the hi.lo half);
 // warps w and w+4 share lane quadrant w%4
@@ -166,10 +176,7 @@ __device__ __forceinline__ void rf_tmem_to_smem(float* tile, int tp, int ncols) 
 }
 
 __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 1)
-    rbm_cd1_fused_kernel(const __grid_constant__ CUtensorMap mVk, const __grid_constant__ CUtensorMap mWk,
-                         const __grid_constant__ CUtensorMap mHSk, const __grid_constant__ CUtensorMap mWmn,
-                         const __grid_constant__ CUtensorMap mVmn, const __grid_constant__ CUtensorMap mHmn,
-                         const RbmFusedParams p) {
+    rbm_cd1_fused_kernel(const __grid_constant__ RbmMaps m, const RbmFusedParams p) {
     extern __shared__ uint8_t smem_raw[];
     if (p.trace && threadIdx.x == 0) {  // bring-up: entry time of every CTA (globaltimer, ns)
         unsigned long long t;
@@ -194,12 +201,17 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
         }
         mbar_init(tbar, 1);
         fence_barrier_init();
-        tma_prefetch(&mVk);
-        tma_prefetch(&mWk);
-        tma_prefetch(&mHSk);
-        tma_prefetch(&mWmn);
-        tma_prefetch(&mVmn);
-        tma_prefetch(&mHmn);
+        tma_prefetch(&m.vk);
+        tma_prefetch(&m.wk);
+        tma_prefetch(&m.hsk);
+        tma_prefetch(&m.wmn);
+        tma_prefetch(&m.vmn);
+        tma_prefetch(&m.hmn);
+        tma_prefetch(&m.vk_lo);
+        tma_prefetch(&m.wk_lo);
+        tma_prefetch(&m.wmn_lo);
+        tma_prefetch(&m.vmn_lo);
+        tma_prefetch(&m.hmn_lo);
     }
     if (warp == 1) tmem_alloc(tslot, 256);
     tc_fence_before();
@@ -234,15 +246,22 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
         __syncthreads();
     }
     if (p.v0_src) {
-        // zero-copy v0: CTA (s, j) moves rows [16 j, 16 j + 16) of visible slice s into Vcat; the 8 CTAs
-        // of slice s then meet at the slice barrier before phase 1 reads the slice by TMA
+        // zero-copy v0 (a direct call on the caller's pinned buffer): CTA (s, j) moves rows [16 j, 16 j + 16)
+        // of visible slice s into Vcat with their tf32 lo parts; the 8 CTAs of slice s then meet at the
+        // slice barrier before phase 1 reads the slice by TMA. Staged / streamed steps find v0 and its lo
+        // parts already in place (stage_rows_kernel on the copy stream) and skip this barrier.
+        const float* src = p.v0_src;
+        const long long lds = p.ld_src;
         const int vlo = v0c, vhi = min(v0c + kRfSliceW, V);
         const int w4 = (vhi - vlo) / 4;  // V % 4 == 0 (host-checked)
         for (int idx = threadIdx.x; idx < 16 * w4; idx += kRfThreads) {
             const int r = 16 * j + idx / w4, c = vlo + (idx % w4) * 4;
-            if (r < B)
-                *reinterpret_cast<float4*>(p.Vcat + (long long)r * p.ldv + c) =
-                    __ldcg(reinterpret_cast<const float4*>(p.v0_src + (long long)r * p.ld_src + c));
+            if (r < B) {
+                const float4 x = __ldcg(reinterpret_cast<const float4*>(src + (long long)r * lds + c));
+                *reinterpret_cast<float4*>(p.Vcat + (long long)r * p.ldv + c) = x;
+                *reinterpret_cast<float4*>(p.Vlo + (long long)r * p.ldv + c) =
+                    make_float4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w));
+            }
         }
         rf_grid_sync(sbar_of(p, s), gridDim.y);
     }
@@ -267,9 +286,12 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
     auto hidden_phase = [&](int vrow0, bool first) {
         const int ph = first ? 0 : 2;  // all 4 K-blocks in flight at once (4 stages of 48 KB)
         rf_product(ring, full + 4 * ph, empty + 4 * ph, tbar, tph, 4, kRfSliceW / 32, 128 * 32 * 4, kRfTileH * 32 * 4,
-                   false, false, id_h, id_h2, [&](int kb, uint8_t* a, uint8_t* b, uint64_t* bar) {
-                       tma_load_2d(a, &mVk, bar, v0c + kb * 32, vrow0);
-                       tma_load_2d(b, &mWk, bar, v0c + kb * 32, h0c);
+                   true, false, false, id_h, id_h2,
+                   [&](int kb, uint8_t* ah, uint8_t* bh, uint8_t* bl, uint8_t* al, uint64_t* bar) {
+                       tma_load_2d(ah, &m.vk, bar, v0c + kb * 32, vrow0);
+                       tma_load_2d(bh, &m.wk, bar, v0c + kb * 32, h0c);
+                       tma_load_2d(bl, &m.wk_lo, bar, v0c + kb * 32, h0c);
+                       tma_load_2d(al, &m.vk_lo, bar, v0c + kb * 32, vrow0);
                    });
         mark();
         rf_tmem_to_smem(tile, kRfTileP, kRfTileH);
@@ -318,9 +340,11 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
                 const float pr = sigmoid_ref(av[i] + bh[i]);  // + bh
                 if (first) {  // energy.hpp:101-110 + unit_sample_inplace :59-61
                     p.Hcat[(long long)r * p.ldh + h] = pr;
+                    p.Hlo[(long long)r * p.ldh + h] = tf32_lo(pr);
                     p.HS[(long long)r * p.ldhs + h] = (uu[i] < (double)pr) ? 1.0f : 0.0f;
                 } else {
                     p.Hcat[(long long)(B + r) * p.ldh + h] = -pr;  // stored negated for phase 4
+                    p.Hlo[(long long)(B + r) * p.ldh + h] = tf32_lo(-pr);
                 }
             }
         }
@@ -340,12 +364,15 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
     mark();
 
     // ---- phase 2: [batch x 128 visible] over this tile's 32 hidden units; tiles meet in L2
-    rf_product(ring, full + 4, empty + 4, tbar, tph, 2, kRfTileH / 32, 128 * 32 * 4, kRfSliceW * 32 * 4, false, true,
-               id_v, id_v2,
-               [&](int kb, uint8_t* a, uint8_t* b, uint64_t* bar) {
-                   tma_load_2d(a, &mHSk, bar, h0c + 32 * kb, 0);
-                   for (int q = 0; q < kRfSliceW / 32; ++q)
-                       tma_load_2d(b + q * 4096, &mWmn, bar, v0c + 32 * q, h0c + 32 * kb);
+    // A = the 0/1 samples: exact in tf32, no lo part -- one MMA per K step
+    rf_product(ring, full + 4, empty + 4, tbar, tph, 2, kRfTileH / 32, 128 * 32 * 4, kRfSliceW * 32 * 4, false, false,
+               true, id_v, id_v2,
+               [&](int kb, uint8_t* ah, uint8_t* bh, uint8_t* bl, uint8_t*, uint64_t* bar) {
+                   tma_load_2d(ah, &m.hsk, bar, h0c + 32 * kb, 0);
+                   for (int q = 0; q < kRfSliceW / 32; ++q) {
+                       tma_load_2d(bh + q * 4096, &m.wmn, bar, v0c + 32 * q, h0c + 32 * kb);
+                       tma_load_2d(bl + q * 4096, &m.wmn_lo, bar, v0c + 32 * q, h0c + 32 * kb);
+                   }
                });
     mark();
     {
@@ -404,6 +431,7 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
                     if (v >= V) continue;
                     const float pr = sigmoid_ref(av[i] + bb[i]);  // + bv
                     p.Vcat[(long long)(B + r) * p.ldv + v] = pr;
+                    p.Vlo[(long long)(B + r) * p.ldv + v] = tf32_lo(pr);
                     const double d = (double)v0v[i] - (double)pr;  // energy.hpp:84-96
                     pd += d * d;
                 }
@@ -434,14 +462,20 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
         const int idx = i * kRfThreads + threadIdx.x;
-        const int n = idx / kRfSliceW, m = idx % kRfSliceW;  // hidden row n of W, visible column m
-        const int h = h0c + n, v = v0c + m;
+        const int n = idx / kRfSliceW, mc = idx % kRfSliceW;  // hidden row n of W, visible column mc
+        const int h = h0c + n, v = v0c + mc;
         wv[i] = (!p.grad_only && h <= H && v <= V) ? p.W[(long long)h * p.ldw + v] : 0.0f;
     }
     rf_product(ring, full + 12, empty + 12, tbar, tph, 4, (2 * B + 31) / 32, 128 * 32 * 4, kRfTileH * 32 * 4, true,
-               true, id_w, id_w2, [&](int kb, uint8_t* a, uint8_t* b, uint64_t* bar) {
-                   for (int q = 0; q < 4; ++q) tma_load_2d(a + q * 4096, &mVmn, bar, v0c + 32 * q, kb * 32);
-                   for (int q = 0; q < kRfTileH / 32; ++q) tma_load_2d(b + q * 4096, &mHmn, bar, h0c + 32 * q, kb * 32);
+               true, true, id_w, id_w2, [&](int kb, uint8_t* ah, uint8_t* bh, uint8_t* bl, uint8_t* al, uint64_t* bar) {
+                   for (int q = 0; q < 4; ++q) {
+                       tma_load_2d(ah + q * 4096, &m.vmn, bar, v0c + 32 * q, kb * 32);
+                       tma_load_2d(al + q * 4096, &m.vmn_lo, bar, v0c + 32 * q, kb * 32);
+                   }
+                   for (int q = 0; q < kRfTileH / 32; ++q) {
+                       tma_load_2d(bh + q * 4096, &m.hmn, bar, h0c + 32 * q, kb * 32);
+                       tma_load_2d(bl + q * 4096, &m.hmn_lo, bar, h0c + 32 * q, kb * 32);
+                   }
                });
     mark();
     rf_tmem_to_smem(tile, kRfTileP, kRfTileH);
@@ -450,13 +484,16 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
 #pragma unroll
         for (int i = 0; i < kPer; ++i) {
             const int idx = i * kRfThreads + threadIdx.x;
-            const int n = idx / kRfSliceW, m = idx % kRfSliceW;
-            const int h = h0c + n, v = v0c + m;
+            const int n = idx / kRfSliceW, mc = idx % kRfSliceW;
+            const int h = h0c + n, v = v0c + mc;
             if (h <= H && v <= V) {
                 if (p.grad_only)
-                    p.G[(long long)h * p.ldw + v] = tile[m * kRfTileP + n];
-                else
-                    p.W[(long long)h * p.ldw + v] = wv[i] + p.alpha * tile[m * kRfTileP + n];
+                    p.G[(long long)h * p.ldw + v] = tile[mc * kRfTileP + n];
+                else {
+                    const float w = wv[i] + p.alpha * tile[mc * kRfTileP + n];
+                    p.W[(long long)h * p.ldw + v] = w;
+                    p.Wlo[(long long)h * p.ldw + v] = tf32_lo(w);
+                }
             }
         }
     }

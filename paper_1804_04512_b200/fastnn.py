@@ -466,6 +466,14 @@ class Rbm:
         _lib.call("b2n_rbm_train_stream", self._h, _f(v0), _d(u), steps, batch, lr, _d(out))
         return out
 
+    def train_stream_ptr(self, v0_ptr: int, u_ptr: int, steps: int, batch: int, lr: float) -> np.ndarray:
+        """train_stream over device-resident batches: v0 (steps*batch x visible f32) and uniforms
+        (steps*batch x hidden f64) at raw device addresses (e.g. torch tensors' data_ptr())"""
+        out = np.zeros(steps, np.float64)
+        _lib.call("b2n_rbm_train_stream", self._h, C.cast(C.c_void_p(v0_ptr), C.POINTER(C.c_float)), C.cast(C.c_void_p(u_ptr), C.POINTER(C.c_double)),
+                  steps, batch, lr, _d(out))
+        return out
+
     def stream_handle(self) -> int:
         s = C.c_void_p()
         _lib.call("b2n_rbm_stream", self._h, C.byref(s))
