@@ -62,13 +62,12 @@ static __global__ void tf32_lo_kernel(const float4* __restrict__ x, float4* __re
 static __global__ void stage_rows_kernel(const float* __restrict__ src, long long lds, float* __restrict__ dst,
                                          float* __restrict__ dlo, long long ldd, int B, int V, int copy) {
     pdl_wait();
-    const int v4 = V / 4;  // V % 4 == 0 (the fused step's envelope)
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)B * v4;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)B * V;
          i += (long long)gridDim.x * blockDim.x) {
-        const long long r = i / v4, c = (i % v4) * 4;
-        const float4 x = *reinterpret_cast<const float4*>(src + r * lds + c);
-        if (copy) *reinterpret_cast<float4*>(dst + r * ldd + c) = x;
-        *reinterpret_cast<float4*>(dlo + r * ldd + c) = make_float4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w));
+        const long long r = i / V, c = i % V;
+        const float x = src[r * lds + c];
+        if (copy) dst[r * ldd + c] = x;
+        dlo[r * ldd + c] = tf32_lo(x);
     }
 }
 
@@ -497,7 +496,7 @@ class Rbm {
         float* Hc = Hcat_.as<float>();
         if (!fused_ws_.p) {
             fused_ws_.alloc((size_t)8 * 128 * kRfSlices * kRfSliceW * 4 + (size_t)8 * kRfSlices * 128 * kRfTileH * 4);
-            gbar_.alloc(256);
+            gbar_.alloc(8 * 128 + 256);  // 8 slice counters, 128 B apart
         }
         RbmFusedParams rp;
         std::memset(&rp, 0, sizeof(rp));
@@ -707,9 +706,8 @@ class Rbm {
 
     // the tf32 lo parts of v0 rows [0, B) of visible buffer k (after their copy into Vcat_[k])
     void stage_lo(int k, long long B, cudaStream_t st) {
-        if (V_ % 4) return;  // the fused step (the only reader) needs V % 4 == 0
         const float* Vc = Vcat_[k].as<float>();
-        launch_ex(stage_rows_kernel, dim3(grid_for(B * V_ / 4)), dim3(256), 0, st, 1u, Vc, ldv_, (float*)nullptr,
+        launch_ex(stage_rows_kernel, dim3(grid_for(B * V_)), dim3(256), 0, st, 1u, Vc, ldv_, (float*)nullptr,
                   Vlo_[k].as<float>(), ldv_, (int)B, (int)V_, 0);
     }
 

@@ -42,7 +42,7 @@ struct RbmFusedParams {
     long long cap;
     float* ws2;        // phase-2 partials [jt tiles][128 rows][8*128 cols]
     float* ws1;        // phase-1/3 partials [jt tiles][8 slices][128 rows][64]
-    unsigned* gbar;    // slice barriers: [slice][count, generation]
+    unsigned* gbar;    // slice barriers: a 64-bit arrival counter per slice, 128 B apart
     unsigned long long* trace;  // bring-up: phase timestamps (clock64) of CTA (0,0) and (7,7), null normally
     float alpha;       // lr / B_global
     int jt;            // hidden tiles
@@ -77,29 +77,32 @@ struct alignas(64) RbmMaps {
     CUtensorMap vk_lo, wk_lo, wmn_lo, vmn_lo, hmn_lo;
 };
 
-__device__ __forceinline__ unsigned* sbar_of(const RbmFusedParams& p, int s) { return p.gbar + 2 * s; }
+// slice barrier counters: one monotonically increasing 64-bit arrival count per slice, 128 B apart
+__device__ __forceinline__ unsigned long long* sbar_of(const RbmFusedParams& p, int s) {
+    return reinterpret_cast<unsigned long long*>(p.gbar) + 16 * s;
+}
 
-// barrier over the nblocks CTAs that share the counter pair gbar = [count, generation]
-__device__ __forceinline__ void rf_grid_sync(unsigned* gbar, unsigned nblocks) {
+// barrier over the nblocks CTAs that share the arrival counter: one release-add (cumulative over the
+// CTA's writes, ordered by the preceding bar.sync), then acquire-polls until the count reaches the end
+// of this barrier instance -- (old / nblocks + 1) * nblocks, so no generation word has to be read
+// first and no reset is needed between launches. Generic-proxy writes are fenced for the async proxy
+// (later TMA reads) on both sides.
+__device__ __forceinline__ void rf_grid_sync(unsigned long long* ctr, unsigned nblocks) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned* gen = gbar + 1;
-        const unsigned g = *gen;
-        asm volatile("fence.proxy.async.global;" ::: "memory");  // our generic writes -> later TMA reads
-        __threadfence();
-        if (atomicInc(gbar, nblocks - 1) == nblocks - 1) {
-            __threadfence();
-            *gen = g + 1;
-        } else {
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        unsigned long long old, v;
+        asm volatile("atom.add.release.gpu.global.u64 %0, [%1], 1;" : "=l"(old) : "l"(ctr) : "memory");
+        const unsigned long long target = (old / nblocks + 1) * nblocks;
+        unsigned long long spins = 0;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+            if (v >= target) break;
             // all CTAs are co-resident (checked on the host); the watchdog turns a broken invariant into
             // a launch error instead of a hung GPU
-            unsigned long long spins = 0;
-            while (*gen == g) {
-                __nanosleep(20);
-                if (++spins > (1ull << 26)) __trap();
-            }
+            if (++spins > 64) __nanosleep(32);
+            if (spins > (1ull << 26)) __trap();
         }
-        __threadfence();
         asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     __syncthreads();
@@ -183,7 +186,9 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
         p.trace[64 + blockIdx.y * gridDim.x + blockIdx.x] = t;
     }
-    uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1 KB-aligned ring by offsetting the __shared__ array itself (not via an integer round trip), so
+    // every pointer derived from it stays in the shared address space (LDS/STS, not generic LD/ST)
+    uint8_t* ring = smem_raw + (((smem_u32(smem_raw) + 1023u) & ~1023u) - smem_u32(smem_raw));
     float* tile = reinterpret_cast<float*>(ring + kRfStages * kRfStage);  // [128][kRfTileP]
     uint64_t* full = reinterpret_cast<uint64_t*>(tile + 128 * kRfTileP);  // [phase][4]
     uint64_t* empty = full + 16;
@@ -277,10 +282,9 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
                 if (h0c + c + i < H) upre[i] = __ldcg(usrc + (long long)r * H + h0c + c + i);
     }
     const uint32_t id_h = umma_idesc_tf32(128, kRfTileH, 0, 0);   // [batch x hidden], both K-major
-    const uint32_t id_v = umma_idesc_tf32(128, kRfSliceW, 0, 1);  // [batch x visible], W MN-major
     const uint32_t id_w = umma_idesc_tf32(128, kRfTileH, 1, 1);   // [visible x hidden], both MN-major
-    const uint32_t id_h2 = umma_idesc_tf32(128, 2 * kRfTileH, 0, 0), id_v2 = umma_idesc_tf32(128, 2 * kRfSliceW, 0, 1),
-                   id_w2 = umma_idesc_tf32(128, 2 * kRfTileH, 1, 1);
+    const uint32_t id_h2 = umma_idesc_tf32(128, 2 * kRfTileH, 0, 0), id_w2 = umma_idesc_tf32(128, 2 * kRfTileH, 1, 1);
+    const uint32_t id_v = umma_idesc_tf32(128, kRfSliceW, 0, 1), id_v2 = umma_idesc_tf32(128, 2 * kRfSliceW, 0, 1);
 
     // ---- phases 1 and 3: [batch x 32 hidden] over this slice's 128 visible units, summed over the slices
     auto hidden_phase = [&](int vrow0, bool first) {
@@ -304,8 +308,7 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
                 *reinterpret_cast<float4*>(dst + rr * kRfTileH + cc) = make_float4(t[0], t[1], t[2], t[3]);
             }
         }
-        __threadfence();
-        cluster_sync_all();  // partials of the 8 slices visible cluster-wide
+        cluster_sync_all();  // partials of the 8 slices visible cluster-wide (release / acquire at cluster scope)
         mark();
         // rank s finishes batch rows [16 s, 16 s + 16): sum over the slices in fixed order, all loads first
         const int r = 16 * s + (threadIdx.x >> 4), c = (threadIdx.x & 15) * 4;
@@ -354,16 +357,17 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
     // CTAs of cluster j), the phase-2 reduction of slice s reads the partials of the 8 CTAs (., s), and
     // phase 3 / 4 of (j, s) read v1[:, slice s] (written by (., s)) and -h1[:, tile j] (cluster j): so
     // cluster barriers plus 8-CTA slice barriers (global counters) replace every grid-wide barrier
-    unsigned* sbar = p.gbar + 2 * s;
+    unsigned long long* sbar = sbar_of(p, s);
     hidden_phase(0, true);
     mark();
-    __threadfence();
     asm volatile("fence.proxy.async.global;" ::: "memory");
     cluster_sync_all();
     asm volatile("fence.proxy.async.global;" ::: "memory");
     mark();
 
-    // ---- phase 2: [batch x 128 visible] over this tile's 32 hidden units; tiles meet in L2
+    // ---- phase 2: [batch x 128 visible] over this tile's 64 hidden units; tiles meet in L2.
+    // (Measured alternative: no split of K -- one CTA per 32-column tile over all 500 hidden units --
+    // is slower: a single SM streams its operands from L2 at ~100 GB/s, 3.7 us for the product alone.)
     // A = the 0/1 samples: exact in tf32, no lo part -- one MMA per K step
     rf_product(ring, full + 4, empty + 4, tbar, tph, 2, kRfTileH / 32, 128 * 32 * 4, kRfSliceW * 32 * 4, false, false,
                true, id_v, id_v2,
@@ -448,7 +452,6 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
     // ---- phase 3
     hidden_phase(B, false);
     mark();
-    __threadfence();
     asm volatile("fence.proxy.async.global;" ::: "memory");
     cluster_sync_all();
     asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -457,14 +460,21 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
     // ---- phase 4: [128 visible x 64 hidden] over K = 2B batch rows, then W_aug[j, s] += alpha * D^T.
     // The W tile is read into registers before the product (nothing else writes it) so the update is
     // a pure store after the MMAs: W, the bh column (v == V) and the bv row (h == H)
+    // thread = visible column mc of the tile, rows n = 2 i + r0 (32 per thread); one base pointer per
+    // array and a 32-bit row stride, predicated rather than branched per element
     constexpr int kPer = kRfTileH * kRfSliceW / kRfThreads;
+    static_assert(kRfThreads == 2 * kRfSliceW, "two tile rows per pass");
+    const int mc4 = threadIdx.x % kRfSliceW, r04 = threadIdx.x / kRfSliceW;
+    const bool col_ok = v0c + mc4 <= V;
+    const int nrows = min(kRfTileH, H + 1 - h0c);  // W rows + the bv row (h == H)
+    const long long base4 = (long long)(h0c + r04) * p.ldw + v0c + mc4;
+    const int rstride = 2 * (int)p.ldw;
     float wv[kPer];
+    {
+        const float* wsrc = p.W + base4;
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-        const int idx = i * kRfThreads + threadIdx.x;
-        const int n = idx / kRfSliceW, mc = idx % kRfSliceW;  // hidden row n of W, visible column mc
-        const int h = h0c + n, v = v0c + mc;
-        wv[i] = (!p.grad_only && h <= H && v <= V) ? p.W[(long long)h * p.ldw + v] : 0.0f;
+        for (int i = 0; i < kPer; ++i)
+            wv[i] = (!p.grad_only && col_ok && 2 * i + r04 < nrows) ? __ldcg(wsrc + i * rstride) : 0.0f;
     }
     rf_product(ring, full + 12, empty + 12, tbar, tph, 4, (2 * B + 31) / 32, 128 * 32 * 4, kRfTileH * 32 * 4, true,
                true, true, id_w, id_w2, [&](int kb, uint8_t* ah, uint8_t* bh, uint8_t* bl, uint8_t* al, uint64_t* bar) {
@@ -480,19 +490,28 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
     mark();
     rf_tmem_to_smem(tile, kRfTileP, kRfTileH);
     __syncthreads();
-    {
+    mark();
+    {  // all tile reads first, then the stores (no load -> store chain per element)
+        float d[kPer];
+        const float* trow = tile + mc4 * kRfTileP + r04;
 #pragma unroll
-        for (int i = 0; i < kPer; ++i) {
-            const int idx = i * kRfThreads + threadIdx.x;
-            const int n = idx / kRfSliceW, mc = idx % kRfSliceW;
-            const int h = h0c + n, v = v0c + mc;
-            if (h <= H && v <= V) {
-                if (p.grad_only)
-                    p.G[(long long)h * p.ldw + v] = tile[mc * kRfTileP + n];
-                else {
-                    const float w = wv[i] + p.alpha * tile[mc * kRfTileP + n];
-                    p.W[(long long)h * p.ldw + v] = w;
-                    p.Wlo[(long long)h * p.ldw + v] = tf32_lo(w);
+        for (int i = 0; i < kPer; ++i) d[i] = trow[2 * i];
+        if (col_ok) {
+            if (p.grad_only) {
+                float* g = p.G + base4;
+#pragma unroll
+                for (int i = 0; i < kPer; ++i)
+                    if (2 * i + r04 < nrows) g[i * rstride] = d[i];
+            } else {
+                float* w = p.W + base4;
+                float* wl = p.Wlo + base4;
+#pragma unroll
+                for (int i = 0; i < kPer; ++i) {
+                    const float x = wv[i] + p.alpha * d[i];
+                    if (2 * i + r04 < nrows) {
+                        w[i * rstride] = x;
+                        wl[i * rstride] = tf32_lo(x);
+                    }
                 }
             }
         }
