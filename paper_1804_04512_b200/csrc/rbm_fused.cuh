@@ -288,6 +288,15 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
 
     // ---- phases 1 and 3: [batch x 32 hidden] over this slice's 128 visible units, summed over the slices
     auto hidden_phase = [&](int vrow0, bool first) {
+        float bhp[4];  // this thread's 4 hidden biases (column V of W_aug), loaded before the product
+        {
+            const int c = (threadIdx.x & 15) * 4;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int h = h0c + c + i;
+                bhp[i] = h < H ? __ldcg(p.W + (long long)h * p.ldw + V) : 0.0f;
+            }
+        }
         const int ph = first ? 0 : 2;  // all 4 K-blocks in flight at once (4 stages of 48 KB)
         rf_product(ring, full + 4 * ph, empty + 4 * ph, tbar, tph, 4, kRfSliceW / 32, 128 * 32 * 4, kRfTileH * 32 * 4,
                    true, false, false, id_h, id_h2,
@@ -333,7 +342,7 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
                 const int h = h0c + c + i;
-                bh[i] = h < H ? p.W[(long long)h * p.ldw + V] : 0.0f;
+                bh[i] = bhp[i];
                 uu[i] = upre[i];
             }
 #pragma unroll
@@ -393,8 +402,9 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
     mark();
     rf_grid_sync(sbar, gridDim.y);
     mark();
-    // CTA (j, s) finishes batch rows [16 j, 16 j + 16) of slice s: one warp per row (two rows per warp),
-    // 4 columns per lane; every load of both rows is issued before the first use
+    // CTA (j, s) finishes batch rows j, j + jt, j + 2 jt, ... of slice s (interleaved: every CTA gets
+    // ~B/jt rows): one warp per row (two rows per warp), 4 columns per lane; every load of both rows
+    // is issued before the first use
     {
         const int c = v0c + (threadIdx.x & 31) * 4;
         float4 part[2][8], vz[2];
@@ -403,7 +413,7 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
                                 : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
         for (int rr = 0; rr < 2; ++rr) {
-            const int r = 16 * j + 8 * rr + warp;
+            const int r = j + (int)gridDim.y * (warp + 8 * rr);  // B <= 16 jt (host-checked)
             rows[rr] = r;
             if (r < B) {
 #pragma unroll
