@@ -38,6 +38,8 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 // ------------------------------------------------------------------ programmatic dependent launch
 // wait until the preceding grid of the stream has completed and its writes are visible (a no-op
 // when the kernel was launched without the programmatic-serialization attribute)
+// x - trunc_tf32(x): the tf32 lo part the tensor core's truncation leaves behind (3xTF32)
+__device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 // allow the next grid to launch (its CTAs then run their prologue and block in pdl_wait)
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }

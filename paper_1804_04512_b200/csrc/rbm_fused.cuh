@@ -158,8 +158,6 @@ __device__ __forceinline__ void rf_product(uint8_t* ring, uint64_t* full, uint64
     tc_fence_after();
 }
 
-// x - trunc_tf32(x): the tf32 lo part the tensor core's truncation leaves behind (3xTF32)
-__device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 // TMEM [128 lanes][2*ncols] -> smem tile (pitch tp floats) as cols[c] + cols[c + ncols] (the hi.lo half);
 // warps w and w+4 share lane quadrant w%4
