@@ -285,6 +285,37 @@ int b2n_crbm_profile(b2n_crbm* crbm, int steps, float lr, long long batch_global
  * of 4, 16-byte aligned bases -- every fastnn tensor satisfies this, tensor.hpp:142) */
 int b2n_gemm(const float* A, long long lda, int transpose_a, const float* B, long long ldb, int transpose_b,
              float* C, long long ldc, long long M, long long N, long long K, int precision, void* stream);
+/* ---- the reference's op-level layer API (layers.hpp:124-320, network.hpp:410-437) on host tensors,
+ * bit-identical to fastnn's (each op computes in the reference's own order; ops.cu). For programs that
+ * call the layer functions directly; the training step itself runs the fused kernels above. ---- */
+typedef struct b2n_conv_shape {  /* fastnn::ConvShape (conv.hpp:20) */
+    long long n, c_in, k, kh, kw, h, w, pad;
+} b2n_conv_shape;
+/* conv_forward (layers.hpp:132): y (n, k, oh, ow) = valid conv of x (n, c_in, h, w) padded by pad with
+ * kernels (k, c_in, kh, kw), + bias (k) */
+int b2n_op_conv_forward(int device, const b2n_conv_shape* shape, const float* x, const float* kernels,
+                        const float* bias, float* y);
+/* conv_backward (layers.hpp:152): dx (n, c_in, h, w); gk (k, c_in, kh, kw) and gb (k) ACCUMULATE into
+ * their incoming values, as the layer's gradient tensors do. ESHAPE for pad != 0 (the reference's
+ * "padded forward has no backward pass"); EPARAM for kernels above 5x5 (the reference's FFT backend). */
+int b2n_op_conv_backward(int device, const b2n_conv_shape* shape, const float* x, const float* kernels,
+                         const float* dy, float* gk, float* gb, float* dx);
+/* pool_forward / pool_backward (layers.hpp:205, :240): mode 0 = max (argmax = in-window index 0..3 as
+ * float, ties keep the first), 1 = avg; maps = product of the leading extents */
+int b2n_op_pool_forward(int device, int mode, long long maps, long long h, long long w, const float* x, float* y,
+                        float* argmax);
+int b2n_op_pool_backward(int device, int mode, long long maps, long long oh, long long ow, const float* dy,
+                         const float* argmax, float* dx);
+/* activation_apply / activation_gradient (layers.hpp:278-299): kind 0 = sigmoid, 1 = relu; the gradient
+ * takes the forward output y */
+int b2n_op_activation_apply(int device, int kind, long long n, const float* x, float* y);
+int b2n_op_activation_gradient(int device, int kind, long long n, const float* y, const float* dy, float* dx);
+/* softmax (layers.hpp:301), softmax_cross_entropy (network.hpp:410): LABEL for labels that are not
+ * one-hot (the reference's message) */
+int b2n_op_softmax(int device, long long rows, long long cols, const float* x, float* y);
+int b2n_op_softmax_cross_entropy(int device, long long rows, long long cols, const float* predictions,
+                                 const float* labels, float* dlogits, double* loss);
+
 /* sgd_momentum_step (optim.hpp:69-80) over n contiguous floats (n % 4 == 0, 16-byte aligned) */
 int b2n_sgd_momentum_step(float* p, float* v, const float* g, long long n, float lr, float momentum,
                           float weight_decay, void* stream);

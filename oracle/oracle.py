@@ -128,6 +128,18 @@ def _declare(lib: C.CDLL, prefix: str) -> None:
         lib.ref_crbm_step.restype = C.c_double
         lib.ref_crbm_destroy.argtypes = [C.c_void_p]
         lib.ref_thread_count.restype = C.c_int
+        # the reference's op-level layer API (b2n_op_* parity)
+        LL = C.c_longlong
+        lib.ref_conv_forward.argtypes = [LL] * 8 + [_F, _F, _F, _F]
+        lib.ref_conv_backward.argtypes = [LL] * 8 + [_F, _F, _F, _F, _F, _F, C.c_char_p, C.c_int]
+        lib.ref_conv_backward.restype = C.c_int
+        lib.ref_pool_forward.argtypes = [C.c_int, LL, LL, LL, _F, _F, _F]
+        lib.ref_pool_backward.argtypes = [C.c_int, LL, LL, LL, _F, _F, _F]
+        lib.ref_softmax.argtypes = [LL, LL, _F, _F]
+        lib.ref_softmax_cross_entropy.argtypes = [LL, LL, _F, _F, _F, _D, C.c_char_p, C.c_int]
+        lib.ref_softmax_cross_entropy.restype = C.c_int
+        lib.ref_activation_apply.argtypes = [C.c_int, LL, _F, _F]
+        lib.ref_activation_gradient.argtypes = [C.c_int, LL, _F, _F, _F]
 
 
 def load(which: str = "oracle") -> C.CDLL:

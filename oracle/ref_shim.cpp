@@ -12,6 +12,7 @@
 // layers.hpp:159 rejects a padded backward), so pad > 0 networks run the SURVEY 8(c) composite of
 // reference primitives: conv_forward with ConvShape.pad, dx = crop(conv_full(dy, kt)),
 // gk += sum_img add_corr_map(pad_spatial(x), dy).
+#include <cstdio>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -582,6 +583,88 @@ void ref_sgd_momentum_step(float* p, float* v, const float* g, long long n, floa
     sgd_momentum_step(st, pt, gt);
     copy_out(pt, p);
     copy_out(st.slot_for(pt).velocity, v);
+}
+
+// ----- the reference's op-level layer API (layers.hpp / network.hpp), for the b2n_op_* parity tests -----
+void ref_conv_forward(long long n, long long c, long long h, long long w, long long k, long long kh, long long kw,
+                      long long pad, const float* x, const float* ker, const float* bias, float* y) {
+    ConvShape s;
+    s.n = n, s.c_in = c, s.h = h, s.w = w, s.k = k, s.kh = kh, s.kw = kw, s.pad = pad;
+    ConvLayer L(s);
+    copy_in(L.kernels, ker);
+    copy_in(L.b, bias);
+    Tensor xt = make_tensor({n, c, h, w});
+    copy_in(xt, x);
+    copy_out(conv_forward(L, xt), y);
+}
+// dx = conv_backward(layer, x, dy); gk / gb accumulate from their incoming values
+int ref_conv_backward(long long n, long long c, long long h, long long w, long long k, long long kh, long long kw,
+                      long long pad, const float* x, const float* ker, const float* dy, float* gk, float* gb, float* dx,
+                      char* err, int errlen) {
+    try {
+        ConvShape s;
+        s.n = n, s.c_in = c, s.h = h, s.w = w, s.k = k, s.kh = kh, s.kw = kw, s.pad = pad;
+        ConvLayer L(s);
+        copy_in(L.kernels, ker);
+        copy_in(L.gk, gk);
+        copy_in(L.gb, gb);
+        const long long oh = h + 2 * pad - kh + 1, ow = w + 2 * pad - kw + 1;
+        Tensor xt = make_tensor({n, c, h, w}), dyt = make_tensor({n, k, oh, ow});
+        copy_in(xt, x);
+        copy_in(dyt, dy);
+        copy_out(conv_backward(L, xt, dyt), dx);
+        copy_out(L.gk, gk);
+        copy_out(L.gb, gb);
+        return 0;
+    } catch (const std::exception& e) {
+        std::snprintf(err, (size_t)errlen, "%s", e.what());
+        return 1;
+    }
+}
+void ref_pool_forward(int mode, long long maps, long long h, long long w, const float* x, float* y, float* argmax) {
+    Tensor xt = make_tensor({maps, h, w});
+    copy_in(xt, x);
+    PoolResult r = pool_forward(mode ? PoolMode::Avg : PoolMode::Max, xt);
+    copy_out(r.y, y);
+    if (!mode) copy_out(r.argmax, argmax);
+}
+void ref_pool_backward(int mode, long long maps, long long oh, long long ow, const float* dy, const float* argmax,
+                       float* dx) {
+    Tensor dyt = make_tensor({maps, oh, ow}), at = make_tensor({maps, oh, ow});
+    copy_in(dyt, dy);
+    if (!mode) copy_in(at, argmax);
+    copy_out(pool_backward(mode ? PoolMode::Avg : PoolMode::Max, dyt, at), dx);
+}
+void ref_softmax(long long rows, long long cols, const float* x, float* y) {
+    Tensor xt = make_tensor({rows, cols});
+    copy_in(xt, x);
+    copy_out(softmax(xt), y);
+}
+int ref_softmax_cross_entropy(long long rows, long long cols, const float* pred, const float* labels, float* dlogits,
+                              double* loss, char* err, int errlen) {
+    try {
+        Tensor p = make_tensor({rows, cols}), l = make_tensor({rows, cols});
+        copy_in(p, pred);
+        copy_in(l, labels);
+        LossGrad g = softmax_cross_entropy(p, l);
+        copy_out(g.dlogits, dlogits);
+        *loss = g.loss;
+        return 0;
+    } catch (const std::exception& e) {
+        std::snprintf(err, (size_t)errlen, "%s", e.what());
+        return 1;
+    }
+}
+void ref_activation_apply(int kind, long long n, const float* x, float* y) {
+    Tensor xt = make_tensor({n});
+    copy_in(xt, x);
+    copy_out(activation_apply(kind ? Activation::Relu : Activation::Sigmoid, xt), y);
+}
+void ref_activation_gradient(int kind, long long n, const float* y, const float* dy, float* dx) {
+    Tensor yt = make_tensor({n}), gt = make_tensor({n});
+    copy_in(yt, y);
+    copy_in(gt, dy);
+    copy_out(activation_gradient(kind ? Activation::Relu : Activation::Sigmoid, yt, gt), dx);
 }
 
 void ref_set_threads(int n) { set_thread_count(n); }

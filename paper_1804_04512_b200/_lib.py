@@ -144,6 +144,14 @@ _SIGS = {
     "b2n_rbm_apply_update": ([_VP, C.c_float, C.c_longlong], C.c_int),
     "b2n_rbm_train_stream": ([_VP, _F, _D, C.c_longlong, C.c_longlong, C.c_float, _D], C.c_int),
     "b2n_rbm_stream": ([_VP, C.POINTER(_VP)], C.c_int),
+    "b2n_op_conv_forward": ([C.c_int, _VP, _F, _F, _F, _F], C.c_int),
+    "b2n_op_conv_backward": ([C.c_int, _VP, _F, _F, _F, _F, _F, _F], C.c_int),
+    "b2n_op_pool_forward": ([C.c_int, C.c_int, C.c_longlong, C.c_longlong, C.c_longlong, _F, _F, _F], C.c_int),
+    "b2n_op_pool_backward": ([C.c_int, C.c_int, C.c_longlong, C.c_longlong, C.c_longlong, _F, _F, _F], C.c_int),
+    "b2n_op_activation_apply": ([C.c_int, C.c_int, C.c_longlong, _F, _F], C.c_int),
+    "b2n_op_activation_gradient": ([C.c_int, C.c_int, C.c_longlong, _F, _F, _F], C.c_int),
+    "b2n_op_softmax": ([C.c_int, C.c_longlong, C.c_longlong, _F, _F], C.c_int),
+    "b2n_op_softmax_cross_entropy": ([C.c_int, C.c_longlong, C.c_longlong, _F, _F, _F, _D], C.c_int),
     "b2n_rbm_set_rng": ([_VP, _U], C.c_int),
     "b2n_rbm_get_rng": ([_VP, _U], C.c_int),
     "b2n_crbm_set_rng": ([_VP, _U], C.c_int),

@@ -56,6 +56,10 @@ int guard(F&& f) {
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 }  // namespace
 
+namespace b2n {
+void set_last_error(const char* msg) { g_last_error = msg; }  // ops.cu's guard
+}
+
 extern "C" {
 
 const char* b2n_last_error(void) { return g_last_error.c_str(); }

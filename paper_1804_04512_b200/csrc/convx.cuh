@@ -41,12 +41,8 @@ struct ConvXParams {
     int codes_pw;
 };
 
-// the reference's sigmoidf (layers.hpp:279): 1 / (1 + expf(-v)) with expf rounded to nearest (glibc's
-// expf is correctly rounded except in rare hard cases; exp in double then one rounding reproduces it)
-__device__ __forceinline__ float sigmoid_exact(float v) {
-    const float e = (float)exp(-(double)v);
-    return 1.0f / (1.0f + e);
-}
+// the reference's sigmoidf (layers.hpp:279): 1 / (1 + expf(-v)) with glibc's expf, bit for bit (ptx.cuh)
+__device__ __forceinline__ float sigmoid_exact(float v) { return 1.0f / (1.0f + glibc_expf(-v)); }
 __device__ __forceinline__ float act_exact(int act, float v) {
     if (act == ACT_SIGMOID) return sigmoid_exact(v);
     if (act == ACT_RELU) return v > 0.0f ? v : 0.0f;

@@ -702,6 +702,126 @@ def mt19937_draw(rng: Mt19937, n: int, device: int = 0) -> np.ndarray:
     return out[:n]
 
 
+# ---------------------------------------------------------------- the reference's op-level layer API
+# (layers.hpp:124-320, network.hpp:410-437) on the GPU, bit-identical to fastnn's: host arrays in / out.
+SIGMOID, RELU = 0, 1      # Activation (layers.hpp:276)
+POOL_MAX, POOL_AVG = 0, 1  # PoolMode (layers.hpp:197)
+
+
+class _ConvShapeC(C.Structure):
+    _fields_ = [(n, C.c_longlong) for n in ("n", "c_in", "k", "kh", "kw", "h", "w", "pad")]
+
+
+def _conv_shape(x, kernels, pad):
+    n, c, h, w = x.shape
+    k, c2, kh, kw = kernels.shape
+    if c2 != c:
+        raise ShapeError("conv: input channels do not match the kernels")
+    return _ConvShapeC(n, c, k, kh, kw, h, w, pad)
+
+
+def conv_forward(kernels, bias, x, pad: int = 0, device: int = 0) -> np.ndarray:
+    """fastnn::conv_forward (layers.hpp:132): x (n, c_in, h, w), kernels (k, c_in, kh, kw), bias (k)"""
+    x = np.ascontiguousarray(x, np.float32)
+    kernels = np.ascontiguousarray(kernels, np.float32)
+    bias = np.ascontiguousarray(bias, np.float32)
+    if x.ndim != 4:
+        raise ShapeError("conv_forward: expected a rank-4 input")
+    s = _conv_shape(x, kernels, pad)
+    y = np.zeros((s.n, s.k, s.h + 2 * pad - s.kh + 1, s.w + 2 * pad - s.kw + 1), np.float32)
+    _lib.call("b2n_op_conv_forward", device, C.addressof(s), _f(x), _f(kernels), _f(bias), _f(y))
+    return y
+
+
+def conv_backward(kernels, x, dy, gk, gb, device: int = 0) -> np.ndarray:
+    """fastnn::conv_backward (layers.hpp:152): returns dx; gk (k, c_in, kh, kw) and gb (k) are float32
+    arrays that accumulate in place, as the layer's gradient tensors do"""
+    x = np.ascontiguousarray(x, np.float32)
+    dy = np.ascontiguousarray(dy, np.float32)
+    kernels = np.ascontiguousarray(kernels, np.float32)
+    if x.ndim != 4 or dy.ndim != 4:
+        raise ShapeError("conv_backward: expected rank-4 tensors")
+    if gk.dtype != np.float32 or gb.dtype != np.float32 or not gk.flags.c_contiguous or not gb.flags.c_contiguous:
+        raise ParamError("conv_backward: gk / gb must be contiguous float32 arrays (updated in place)")
+    s = _conv_shape(x, kernels, 0)
+    if dy.shape != (s.n, s.k, s.h - s.kh + 1, s.w - s.kw + 1):
+        raise ShapeError("conv_backward: dy does not match the forward output shape")
+    dx = np.zeros_like(x)
+    _lib.call("b2n_op_conv_backward", device, C.addressof(s), _f(x), _f(kernels), _f(dy), _f(gk), _f(gb), _f(dx))
+    return dx
+
+
+def pool_forward(mode: int, x, device: int = 0):
+    """fastnn::pool_forward (layers.hpp:205): 2x2 windows over the last two axes; returns (y, argmax)
+    (argmax None in avg mode)"""
+    x = np.ascontiguousarray(x, np.float32)
+    if x.ndim < 2:
+        raise ShapeError("pool_forward: expected rank >= 2")
+    h, w = x.shape[-2:]
+    maps = int(np.prod(x.shape[:-2])) if x.ndim > 2 else 1
+    oshape = x.shape[:-2] + (h // 2, w // 2)
+    y = np.zeros(oshape, np.float32)
+    a = np.zeros(oshape, np.float32) if mode == POOL_MAX else None
+    _lib.call("b2n_op_pool_forward", device, mode, maps, h, w, _f(x), _f(y), _f(a) if a is not None else None)
+    return y, a
+
+
+def pool_backward(mode: int, dy, argmax=None, device: int = 0) -> np.ndarray:
+    """fastnn::pool_backward (layers.hpp:240)"""
+    dy = np.ascontiguousarray(dy, np.float32)
+    if dy.ndim < 2:
+        raise ShapeError("pool_backward: expected rank >= 2")
+    if mode == POOL_MAX and (argmax is None or np.shape(argmax) != dy.shape):
+        raise ShapeError("pool_backward: dy/argmax shape mismatch")
+    oh, ow = dy.shape[-2:]
+    maps = int(np.prod(dy.shape[:-2])) if dy.ndim > 2 else 1
+    dx = np.zeros(dy.shape[:-2] + (2 * oh, 2 * ow), np.float32)
+    a = np.ascontiguousarray(argmax, np.float32) if mode == POOL_MAX else None
+    _lib.call("b2n_op_pool_backward", device, mode, maps, oh, ow, _f(dy), _f(a) if a is not None else None, _f(dx))
+    return dx
+
+
+def activation_apply(kind: int, x, device: int = 0) -> np.ndarray:
+    """fastnn::activation_apply (layers.hpp:278)"""
+    x = np.ascontiguousarray(x, np.float32)
+    y = np.zeros_like(x)
+    _lib.call("b2n_op_activation_apply", device, kind, x.size, _f(x), _f(y))
+    return y
+
+
+def activation_gradient(kind: int, y, dy, device: int = 0) -> np.ndarray:
+    """fastnn::activation_gradient (layers.hpp:284), through the forward output y"""
+    y = np.ascontiguousarray(y, np.float32)
+    dy = np.ascontiguousarray(dy, np.float32)
+    if y.shape != dy.shape:
+        raise ShapeError("activation_gradient: shape mismatch")
+    dx = np.zeros_like(y)
+    _lib.call("b2n_op_activation_gradient", device, kind, y.size, _f(y), _f(dy), _f(dx))
+    return dx
+
+
+def softmax(x, device: int = 0) -> np.ndarray:
+    """fastnn::softmax (layers.hpp:301)"""
+    x = np.ascontiguousarray(x, np.float32)
+    if x.ndim != 2:
+        raise ShapeError(f"softmax: expected a rank-2 tensor, got rank {x.ndim}")
+    y = np.zeros_like(x)
+    _lib.call("b2n_op_softmax", device, x.shape[0], x.shape[1], _f(x), _f(y))
+    return y
+
+
+def softmax_cross_entropy(predictions, labels, device: int = 0):
+    """fastnn::softmax_cross_entropy (network.hpp:410): returns (loss, dlogits)"""
+    p = np.ascontiguousarray(predictions, np.float32)
+    y = np.ascontiguousarray(labels, np.float32)
+    if p.ndim != 2 or y.ndim != 2 or p.shape != y.shape:
+        raise ShapeError("softmax_cross_entropy: predictions and labels must both be (batch, classes)")
+    g = np.zeros_like(p)
+    loss = C.c_double()
+    _lib.call("b2n_op_softmax_cross_entropy", device, p.shape[0], p.shape[1], _f(p), _f(y), _f(g), C.byref(loss))
+    return loss.value, g
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     _lib.call("b2n_nccl_unique_id", buf)
