@@ -19,7 +19,7 @@ ncu --set full --clock-control none --import-source on -k regex:"mt_(words|canon
 ncu --set full --clock-control none --import-source on -k regex:crbm_cd1_fused -s 2 -c 1 \
     -o gpurun_out/${R}_crbm_full python bench.py --profile-only --config crbm --steps 1 --warmup 2 > /dev/null 2>&1
 # the conv kernels of one ImageNet-shaped step: exact forward (convx), tcgen05 dgrad, FFMA wgrad
-ncu --set full --clock-control none --import-source on -k regex:"conv(x|t)_(fwd|mma|wgrad)" -c 14 \
+ncu --set full --clock-control none --import-source on -k regex:"conv(x|t)_(fwd|mma|wgrad)" -c 19 \
     -o gpurun_out/${R}_imagenet_conv_full python bench.py --profile-only --config imagenet_cnn --steps 1 --warmup 0 > /dev/null 2>&1
 # the bandwidth kernels north_star names: softmax-xent rows (1000 classes), wgrad reduce + SGD, repack,
 # the packed SGD / Adam passes (data-parallel apply and the split optimizer path)
@@ -27,4 +27,9 @@ ncu --set full --clock-control none -k regex:"softmax_xent_rows|convt_wgrad_redu
     -o gpurun_out/${R}_bw_imagenet python bench.py --profile-only --config imagenet_cnn --steps 1 --warmup 0 > /dev/null 2>&1
 ncu --set full --clock-control none -k regex:"sgd_packed|opt_packed" -c 6 \
     -o gpurun_out/${R}_bw_optim python -m pytest -q -m gpu -p no:cacheprovider tests/test_gpu_optim.py tests/test_gpu_dp.py > /dev/null 2>&1
+# raw pages exported on the box; large reports dropped (gpurun brings back <= 64 MiB)
+for r in gpurun_out/${R}_*.ncu-rep; do
+  ncu -i "$r" --page raw --csv > "${r%.ncu-rep}.raw.csv" 2>/dev/null
+  if [ $(stat -c %s "$r") -gt 12000000 ]; then rm -f "$r"; fi
+done
 ls -la gpurun_out

@@ -37,7 +37,11 @@ IMAGENET_CONV = [f"conv{i}.fwd" for i in range(5)] + [x for i in (4, 3, 2, 1) fo
 
 
 def raw_rows(rep: Path):
-    txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    csvp = rep.with_suffix(".raw.csv")  # capture.sh exports the raw page on the box (reports are large)
+    if csvp.exists():
+        txt = csvp.read_text()
+    else:
+        txt = subprocess.run(["ncu", "-i", str(rep), "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     head, units = rows[0], rows[1]
     out = []
@@ -61,8 +65,11 @@ def launch_share(csv_path: Path):
     rows = [r for r in csv.reader(open(csv_path)) if r and not r[0].startswith("==")]
     head = rows[0]
     ki, vi, ui = head.index("Kernel Name"), head.index("Metric Value"), head.index("Metric Unit")
+    mi = head.index("Metric Name") if "Metric Name" in head else None
     agg = {}
     for r in rows[1:]:
+        if mi is not None and r[mi] != "gpu__time_duration.sum":
+            continue
         v = float(r[vi].replace(",", ""))
         t = v * {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}.get(r[ui], 1.0)
         name = r[ki].split("(")[0]
@@ -86,17 +93,41 @@ def main(tag: str):
                               (OUT / f"{tag}_crbm_split_full.ncu-rep", CRBM_SPLIT,
                                "Convolutional RBM CD-1, split tensor-core path (B2N_CRBM_FUSED=0)"),
                               (OUT / f"{tag}_imagenet_conv_full.ncu-rep", IMAGENET_CONV,
-                               "ImageNet-shape CNN (batch 128): halo-tile conv kernels of one step")]:
-        if not rep.exists():
+                               "ImageNet-shape CNN (batch 128): conv kernels of one step (convx forward, "
+                               "tcgen05 dgrad, FFMA wgrad)"),
+                              (OUT / f"{tag}_mt_full.ncu-rep", ["mt.words", "mt.canonical"],
+                               "Device std::mt19937 stream: words (one-CTA wavefront) + canonical (grid)"),
+                              (OUT / f"{tag}_bw_imagenet.ncu-rep", ["bw"] * 6,
+                               "Bandwidth kernels of the ImageNet-shape step (softmax-xent rows, wgrad reduce + SGD, repack)"),
+                              (OUT / f"{tag}_bw_optim.ncu-rep", ["bw"] * 6,
+                               "Packed optimizer passes (SGD in data-parallel mode, Adam/Adagrad/Adadelta)")]:
+        if not rep.exists() and not rep.with_suffix(".raw.csv").exists():
             continue
         rows = raw_rows(rep)
-        lines += [f"## {title}", "", "| op | kernel | us | DRAM rd+wr MB | DRAM % | tensor-pipe % | SM % | regs | grid |",
-                  "|---|---|---|---|---|---|---|---|---|"]
+        if names is IMAGENET_CONV:  # label by kernel kind, layers in launch order (fwd 0..4, bwd 4..0)
+            names, fwd, bwd = [], 0, [4, 4, 4]
+            for d in rows:
+                k = d["kernel"]
+                if k.startswith("void convx_fwd"):
+                    names.append(f"conv{fwd}.fwd")
+                    fwd += 1
+                elif "convt_mma_kernel" in k:
+                    names.append(f"conv{bwd[0]}.dgrad")
+                    bwd[0] -= 1
+                elif "convt_wgrad_kernel" in k:
+                    names.append(f"conv{bwd[1]}.wgrad")
+                    bwd[1] -= 1
+                else:
+                    names.append(f"conv{bwd[2]}.wgrad_reduce+sgd")
+                    bwd[2] -= 1
+        lines += [f"## {title}", "", "| op | kernel | us | DRAM rd+wr MB | DRAM GB/s | DRAM % | tensor-pipe % | SM % | regs | grid |",
+                  "|---|---|---|---|---|---|---|---|---|---|"]
         for i, d in enumerate(rows):
             op = names[i] if i < len(names) else "?"
             tb = (d.get("dram_read") or 0) + (d.get("dram_write") or 0)
             traffic.setdefault(op, tb)  # per launch: bench.py's roofline `traffic`
-            lines.append(f"| {op} | `{d['kernel'][:60]}` | {d.get('dur_us', 0):.2f} | {tb / 1e6:.3f} | "
+            gbs = tb / (d.get('dur_us') or 1e9) / 1e3
+            lines.append(f"| {op} | `{d['kernel'][:60]}` | {d.get('dur_us', 0):.2f} | {tb / 1e6:.3f} | {gbs:.0f} | "
                          f"{d.get('dram_pct', 0):.1f} | {d.get('tensor_pct', 0):.1f} | {d.get('sm_pct', 0):.1f} | "
                          f"{d.get('regs', 0):.0f} | {d.get('grid', 0):.0f} |")
         lines.append("")
