@@ -86,7 +86,7 @@ inline size_t crbm_fused_smem(int C, int H, int W, int K, int KH, int KW) {
 }
 
 __device__ __forceinline__ int rup4(int n) { return (n + 3) & ~3; }
-__device__ __forceinline__ float sigmoid_f(float v) { return 1.0f / (1.0f + glibc_expf(-v)); }  // energy.hpp:36
+__device__ __forceinline__ float sigmoid_f(float v) { return 1.0f / (1.0f + expf(-v)); }  // energy.hpp:36
 
 // valid correlation of `in` (CI channels x IH rows, row pitch IP, smem) with taps into outputs
 // (f, oy, ox) of F x OHh x OWw; each job owns a strip of 8 consecutive ox (adjacent lanes take

@@ -113,7 +113,10 @@ struct GemmCfg {
     static_assert(STAGES >= 2, "tile too large");
 };
 
-__device__ __forceinline__ float sigmoid_ref(float v) { return 1.0f / (1.0f + glibc_expf(-v)); }  // layers.hpp:279
+// layers.hpp:279. The tensor-core products feeding it differ from the reference's fp32 sums at ~1e-6,
+// so CUDA's expf (<= 2 ulp) costs nothing in accuracy here; the bit-exact paths (convx.cuh forward,
+// ops.cu) use glibc_expf
+__device__ __forceinline__ float sigmoid_ref(float v) { return 1.0f / (1.0f + expf(-v)); }
 
 __device__ __forceinline__ float apply_act(int act, float v) {
     if (act == ACT_SIGMOID) return sigmoid_ref(v);
@@ -297,12 +300,12 @@ __device__ __forceinline__ void softmax_row(const GemmParams& p, const float* tr
     auto bias = [&](int n) { return sbias ? sbias[n] : e.bias[(long long)n * e.bias_stride]; };
     for (int n = 0; n < p.N; ++n) mx = fmaxf(mx, trow[n] + bias(n));
     float sum = 0.0f;
-    for (int n = 0; n < p.N; ++n) sum += glibc_expf((trow[n] + bias(n)) - mx);
+    for (int n = 0; n < p.N; ++n) sum += expf((trow[n] + bias(n)) - mx);
     const int label = e.labels[m];
     int best = 0;
     float bestp = -1.0f, ptrue = 0.0f;
     for (int n = 0; n < p.N; ++n) {
-        const float q = glibc_expf((trow[n] + bias(n)) - mx) / sum;
+        const float q = expf((trow[n] + bias(n)) - mx) / sum;
         if (q > bestp) {  // strict >: first maximum wins (network.hpp:69-70)
             bestp = q;
             best = n;

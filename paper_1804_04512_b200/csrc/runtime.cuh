@@ -614,7 +614,7 @@ static __global__ void softmax_xent_rows_kernel(const float* __restrict__ logits
     for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
     // exp terms in parallel, then the sequential sum (layers.hpp:312-315 order)
     float* dl = dlogits + (long long)warp * ldd;
-    for (int j = lane; j < cols; j += 32) dl[j] = glibc_expf(z[j] - mx);
+    for (int j = lane; j < cols; j += 32) dl[j] = expf(z[j] - mx);
     __syncwarp();
     if (lane == 0) {
         float sum = 0.0f;
