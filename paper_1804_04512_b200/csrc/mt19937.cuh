@@ -92,7 +92,7 @@ static __global__ void __launch_bounds__(256, 1) mt_words_kernel(uint32_t* st, u
     if (t < 160) {  // 5 warps: lanes 0..154 carry the wavefront, all 160 take the named barrier
         uint4* wb = reinterpret_cast<uint4*>(wbuf);
         int A = (1080 + 4 * t) & M;  // ring slot of this thread's first word
-        uint32_t own0 = ring[(1080 + 4 * t - 620) & M];  // X[q - 620]
+        uint32_t own0 = t < kMtW / 4 ? ring[(1080 + 4 * t - 620) & M] : 0u;  // X[q - 620] (lanes that compute)
         for (long long s = 1080; s < end; s += kMtW) {
             const long long q = s + 4 * t;
             if (t < kMtW / 4 && q < end) {

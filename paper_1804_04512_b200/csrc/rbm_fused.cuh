@@ -419,7 +419,8 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
                     part[rr][t] = t < p.jt ? *reinterpret_cast<const float4*>(
                                                  p.ws2 + ((long long)t * 128 + r) * (kRfSlices * kRfSliceW) + c)
                                            : make_float4(0.f, 0.f, 0.f, 0.f);
-                vz[rr] = *reinterpret_cast<const float4*>(p.Vcat + (long long)r * p.ldv + c);
+                vz[rr] = c < V ? *reinterpret_cast<const float4*>(p.Vcat + (long long)r * p.ldv + c)
+                               : make_float4(0.f, 0.f, 0.f, 0.f);  // slices past V: nothing to read
             }
         }
 #pragma unroll
