@@ -23,11 +23,11 @@
 // libstdc++'s (_M_x, _M_p) after the same draws. One CTA is issue/latency bound at ~1 barrier per
 // 620 words; the step kernels never wait for it where it runs on the copy stream ahead of them.
 #pragma once
+#include "mt_jump.cuh"
 #include "runtime.cuh"
 
 namespace b2n {
 
-constexpr int kMtN = 624;
 
 __device__ __forceinline__ uint32_t mt_twist(uint32_t a, uint32_t b) {
     return (((a & 0x80000000u) | (b & 0x7fffffffu)) >> 1) ^ ((b & 1u) ? 0x9908b0dfu : 0u);
@@ -53,23 +53,26 @@ __host__ __device__ __forceinline__ double mt_canonical(uint32_t w0, uint32_t w1
 // 4-word group is an immediate offset from one register, never a wrapped index.
 constexpr int kMtR = 2048;         // ring words (> 1080 behind + 620 ahead)
 constexpr int kMtW = 620;          // main-wavefront width: 155 threads x 4 words, <= 623
-static __global__ void __launch_bounds__(256, 1) mt_words_kernel(uint32_t* st, uint32_t* __restrict__ wbuf,
-                                                                 long long* meta, long long n) {
+// st_in -> st_out may alias (all of st_in is read first); st_out null: the state is not written back.
+// prefix != 0: just the first kMtPrefix words of the sequence from st_in's block (for mt_jump.cuh).
+static __global__ void __launch_bounds__(256, 1) mt_words_kernel(const uint32_t* st_in, uint32_t* st_out,
+                                                                 uint32_t* __restrict__ wbuf, long long* meta,
+                                                                 long long n, int prefix) {
     pdl_wait();
     __shared__ __align__(16) uint32_t ring[2 * kMtR];
     constexpr int M = kMtR - 1;
     const int t = threadIdx.x;
-    const long long p = st[kMtN];
-    const long long E = p + 2 * n;
-    const long long blk = n > 0 ? (E - 1) / kMtN : 0;
+    const long long p = prefix ? 0 : st_in[kMtN];
+    const long long E = prefix ? kMtPrefix : p + 2 * n;
+    const long long blk = E > p ? (E - 1) / kMtN : 0;
     const long long end = kMtN * (blk + 1);
     for (int i = t; i < kMtN; i += blockDim.x) {
-        const uint32_t x = st[i];
+        const uint32_t x = st_in[i];
         ring[i] = x;
         ring[i + kMtR] = x;
         wbuf[i] = x;
     }
-    if (t == 0) meta[0] = p;
+    if (t == 0 && !prefix) meta[0] = p;
     __syncthreads();
     // bootstrap with the plain recurrence X[q] = X[q-227] ^ T(X[q-624], X[q-623]): [624, 851),
     // [851, 1078), [1078, 1080) -- after which the main wavefront starts 4-word aligned
@@ -124,8 +127,9 @@ static __global__ void __launch_bounds__(256, 1) mt_words_kernel(uint32_t* st, u
         }
     }
     __syncthreads();
-    for (int i = t; i < kMtN; i += blockDim.x) st[i] = ring[(kMtN * blk + i) & M];
-    if (t == 0) st[kMtN] = (uint32_t)(E - kMtN * blk);
+    if (!st_out) return;
+    for (int i = t; i < kMtN; i += blockDim.x) st_out[i] = ring[(kMtN * blk + i) & M];
+    if (t == 0) st_out[kMtN] = (uint32_t)(E - kMtN * blk);
 }
 
 // out[j] = generate_canonical<double, 53> of the words X[p + 2j], X[p + 2j + 1]
@@ -156,6 +160,7 @@ class DevRng {
         B2N_CUDA(cudaStreamSynchronize(st));  // host_ is reused by store()
         std::memcpy(shadow_, s, sizeof(shadow_));
         valid_ = true;
+        p_ = s[kMtN];
     }
     void draw(double* out, long long n, cudaStream_t st) {
         if (!valid_) throw Error(B2N_EPARAM, "device generator used before its state was set");
@@ -165,12 +170,102 @@ class DevRng {
             B2N_CUDA(cudaStreamSynchronize(st));  // a pending draw may still read the old buffer
             wbuf_.alloc(words * 4);
         }
-        launch_ex(mt_words_kernel, dim3(1), dim3(256), 0, st, 1u, st_.as<uint32_t>(), wbuf_.as<uint32_t>(),
-                  reinterpret_cast<long long*>(st_.as<uint8_t>() + kMtN * 4 + 16), n);
+        launch_ex(mt_words_kernel, dim3(1), dim3(256), 0, st, 1u, (const uint32_t*)st_.as<uint32_t>(), st_.as<uint32_t>(),
+                  wbuf_.as<uint32_t>(), reinterpret_cast<long long*>(st_.as<uint8_t>() + kMtN * 4 + 16), n, 0);
         const int g = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
         launch_ex(mt_canonical_kernel, dim3(g), dim3(256), 0, st, 1u, (const uint32_t*)wbuf_.as<uint32_t>(),
                   (const long long*)(st_.as<uint8_t>() + kMtN * 4 + 16), out, n);
         dirty_ = true;
+        p_ = advance(p_, n);
+    }
+
+    // ---- consecutive draws of n doubles each, pipelined (train_stream): a chain stream computes every
+    // step's starting state by jump-ahead (prefix words -> XOR of windows -> block), kGen generator
+    // streams produce the steps' draws concurrently. Bit-identical to draw() called step after step.
+    void stream_begin(long long n, cudaStream_t base) {
+        if (!valid_) throw Error(B2N_EPARAM, "device generator used before its state was set");
+        if (!sm_.slots.p) {
+            sm_.slots.alloc((size_t)kSlots * kSlotBytes);
+            sm_.prefix.alloc((size_t)(kMtN * 34) * 4);
+            sm_.part.alloc((size_t)kMtJumpCtas * kMtN * 4);
+            for (int g = 0; g < kGen; ++g) {
+                sm_.gmeta[g].alloc(64);
+                B2N_CUDA(cudaStreamCreateWithFlags(&sm_.gen[g], cudaStreamNonBlocking));
+            }
+            B2N_CUDA(cudaStreamCreateWithFlags(&sm_.chain, cudaStreamNonBlocking));
+            for (int k = 0; k < kSlots; ++k) {
+                B2N_CUDA(cudaEventCreateWithFlags(&sm_.ev_state[k], cudaEventDisableTiming));
+                B2N_CUDA(cudaEventCreateWithFlags(&sm_.ev_gen[k], cudaEventDisableTiming));
+            }
+            B2N_CUDA(cudaEventCreateWithFlags(&sm_.ev_base, cudaEventDisableTiming));
+        }
+        const size_t words = (size_t)(2 * n + 2 * kMtN + 16);
+        for (int g = 0; g < kGen; ++g)
+            if (sm_.gwbuf[g].bytes < words * 4) {
+                B2N_CUDA(cudaDeviceSynchronize());
+                sm_.gwbuf[g].alloc(words * 4);
+            }
+        sm_.n = n;
+        sm_.p.assign(1, p_);
+        B2N_CUDA(cudaEventRecord(sm_.ev_base, base));
+        B2N_CUDA(cudaStreamWaitEvent(sm_.chain, sm_.ev_base, 0));
+        for (int g = 0; g < kGen; ++g) B2N_CUDA(cudaStreamWaitEvent(sm_.gen[g], sm_.ev_base, 0));
+        B2N_CUDA(cudaMemcpyAsync(slot(0), st_.p, (kMtN + 1) * 4, cudaMemcpyDeviceToDevice, sm_.chain));
+        B2N_CUDA(cudaEventRecord(sm_.ev_state[0], sm_.chain));
+        for (int k = 0; k < kSlots; ++k) B2N_CUDA(cudaEventRecord(sm_.ev_gen[k], sm_.chain));
+    }
+    // step i of `steps`: its draws into out once `out_free` has fired; `out_ready` is recorded after them
+    void stream_step(int i, int steps, double* out, cudaEvent_t out_free, cudaEvent_t out_ready) {
+        const long long n = sm_.n;
+        const int si = i % kSlots, g = i % kGen;
+        cudaStream_t gs = sm_.gen[g];
+        B2N_CUDA(cudaStreamWaitEvent(gs, sm_.ev_state[si], 0));
+        B2N_CUDA(cudaStreamWaitEvent(gs, out_free, 0));
+        uint32_t* fin = i == steps - 1 ? st_.as<uint32_t>() : nullptr;  // the last step hands the state back
+        long long* meta = sm_.gmeta[g].as<long long>();
+        launch_ex(mt_words_kernel, dim3(1), dim3(256), 0, gs, 1u, (const uint32_t*)slot(si), fin,
+                  sm_.gwbuf[g].as<uint32_t>(), meta, n, 0);
+        const int grid = (int)std::min<long long>((n + 255) / 256, 148LL * 8);
+        launch_ex(mt_canonical_kernel, dim3(grid), dim3(256), 0, gs, 1u, (const uint32_t*)sm_.gwbuf[g].as<uint32_t>(),
+                  (const long long*)meta, out, n);
+        B2N_CUDA(cudaEventRecord(out_ready, gs));
+        B2N_CUDA(cudaEventRecord(sm_.ev_gen[si], gs));
+        const long long pi = sm_.p.back(), E = pi + 2 * n, blk = (E - 1) / kMtN;
+        sm_.p.push_back(E - kMtN * blk);
+        sm_.p_host[(size_t)(i + 1) % kSlots] = (unsigned)sm_.p.back();
+        if (i + 1 >= steps) return;
+        // the next step's block: jump blk blocks ahead from this step's block (slot free once its last
+        // generator is done)
+        const int sn = (i + 1) % kSlots;
+        B2N_CUDA(cudaStreamWaitEvent(sm_.chain, sm_.ev_gen[sn], 0));
+        if (blk == 0) {  // the draws stayed inside the block: same block, new position
+            B2N_CUDA(cudaMemcpyAsync(slot(sn), slot(si), kMtN * 4, cudaMemcpyDeviceToDevice, sm_.chain));
+            B2N_CUDA(cudaMemcpyAsync(slot(sn) + kMtN, &sm_.p_host[(size_t)(i + 1) % kSlots], 4, cudaMemcpyHostToDevice,
+                                     sm_.chain));
+            B2N_CUDA(cudaEventRecord(sm_.ev_state[sn], sm_.chain));
+            return;
+        }
+        const JumpPoly& jp = jump_poly(kMtN * blk - 1);
+        launch_ex(mt_words_kernel, dim3(1), dim3(256), 0, sm_.chain, 1u, (const uint32_t*)slot(si), (uint32_t*)nullptr,
+                  sm_.prefix.as<uint32_t>(), (long long*)nullptr, 0LL, 1);
+        launch_ex(mt_jump_kernel, dim3(kMtJumpCtas), dim3(640), 0, sm_.chain, 1u, (const uint32_t*)sm_.prefix.as<uint32_t>(),
+                  (const int*)jp.terms.as<int>(), (const int*)jp.off.as<int>(), sm_.part.as<uint32_t>());
+        launch_ex(mt_jump_finish_kernel, dim3(1), dim3(640), 0, sm_.chain, 1u, (const uint32_t*)sm_.part.as<uint32_t>(),
+                  slot(sn), (unsigned)sm_.p.back());
+        B2N_CUDA(cudaEventRecord(sm_.ev_state[sn], sm_.chain));
+    }
+    // base waits for the whole stream; the generator state is the last step's
+    void stream_end(int steps, cudaStream_t base) {
+        B2N_CUDA(cudaEventRecord(sm_.ev_base, sm_.chain));
+        B2N_CUDA(cudaStreamWaitEvent(base, sm_.ev_base, 0));
+        for (int g = 0; g < kGen; ++g) {
+            B2N_CUDA(cudaEventRecord(sm_.ev_base, sm_.gen[g]));
+            B2N_CUDA(cudaStreamWaitEvent(base, sm_.ev_base, 0));
+        }
+        if (steps > 0) {
+            dirty_ = true;
+            p_ = sm_.p[(size_t)steps];
+        }
     }
     // copy the device state back (synchronises st); s may be null to just refresh the shadow
     void store(uint32_t* s, cudaStream_t st) {
@@ -180,12 +275,58 @@ class DevRng {
             spin_sync(st);
             std::memcpy(shadow_, host_.p, sizeof(shadow_));
             dirty_ = false;
+            if (shadow_[kMtN] != (uint32_t)p_) throw Error(B2N_EINTERNAL, "device generator position out of sync");
         }
         if (s) std::memcpy(s, shadow_, sizeof(shadow_));
     }
     bool valid() const { return valid_; }
 
+    ~DevRng() {
+        if (sm_.chain) cudaStreamDestroy(sm_.chain);
+        for (int g = 0; g < kGen; ++g)
+            if (sm_.gen[g]) cudaStreamDestroy(sm_.gen[g]);
+        for (int k = 0; k < kSlots; ++k) {
+            if (sm_.ev_state[k]) cudaEventDestroy(sm_.ev_state[k]);
+            if (sm_.ev_gen[k]) cudaEventDestroy(sm_.ev_gen[k]);
+        }
+        if (sm_.ev_base) cudaEventDestroy(sm_.ev_base);
+    }
+
   private:
+    static constexpr int kSlots = 8, kGen = 3, kSlotBytes = 4096;
+    struct JumpPoly {
+        DevMem terms, off;
+    };
+    // x^m mod phi as per-CTA term lists (host Berlekamp-Massey / powmod once per m, mt_jump.cuh)
+    const JumpPoly& jump_poly(long long m) {
+        auto it = jumps_.find(m);
+        if (it != jumps_.end()) return *it->second;
+        const std::vector<int> t = mtpoly::jump_terms(m);
+        std::vector<int> off(kMtJumpCtas + 1, 0);
+        for (int v : t) ++off[(size_t)(v / 623 + 1)];
+        for (int c = 0; c < kMtJumpCtas; ++c) off[(size_t)c + 1] += off[(size_t)c];
+        auto jp = std::make_unique<JumpPoly>();
+        jp->terms.alloc(std::max<size_t>(t.size(), 1) * 4);
+        jp->off.alloc(off.size() * 4);
+        B2N_CUDA(cudaMemcpy(jp->terms.p, t.data(), t.size() * 4, cudaMemcpyHostToDevice));
+        B2N_CUDA(cudaMemcpy(jp->off.p, off.data(), off.size() * 4, cudaMemcpyHostToDevice));
+        return *(jumps_[m] = std::move(jp));
+    }
+    uint32_t* slot(int k) { return reinterpret_cast<uint32_t*>(sm_.slots.as<uint8_t>() + (size_t)k * kSlotBytes); }
+    static long long advance(long long p, long long n) {
+        const long long E = p + 2 * n, blk = n > 0 ? (E - 1) / kMtN : 0;
+        return E - kMtN * blk;
+    }
+    struct StreamRes {
+        DevMem slots, prefix, part, gwbuf[kGen], gmeta[kGen];
+        cudaStream_t chain = nullptr, gen[kGen] = {};
+        cudaEvent_t ev_state[kSlots] = {}, ev_gen[kSlots] = {}, ev_base = nullptr;
+        long long n = 0;
+        std::vector<long long> p;  // position before each step of the stream in flight
+        unsigned p_host[kSlots] = {};  // pinned-free staging of a position for the blk == 0 copy
+    } sm_;
+    std::map<long long, std::unique_ptr<JumpPoly>> jumps_;
+    long long p_ = 0;  // the state's position, tracked on the host
     DevMem st_;    // [624 words, p] + the draw's starting position (read by the canonical kernel)
     DevMem wbuf_;  // the raw words of the draw in flight
     HostPinned host_;

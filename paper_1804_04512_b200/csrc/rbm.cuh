@@ -95,7 +95,6 @@ class Rbm {
             if (ev_rng_[j]) cudaEventDestroy(ev_rng_[j]);
         }
         if (copy_stream_) cudaStreamDestroy(copy_stream_);
-        if (rng_stream_) cudaStreamDestroy(rng_stream_);
         if (recon_host_) cudaFreeHost(recon_host_);
         if (stream_) cudaStreamDestroy(stream_);
     }
@@ -323,7 +322,6 @@ class Rbm {
             if (!ev_rng_[j]) B2N_CUDA(cudaEventCreateWithFlags(&ev_rng_[j], cudaEventDisableTiming));
         }
         if (!copy_stream_) B2N_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
-        if (!u && !rng_stream_) B2N_CUDA(cudaStreamCreateWithFlags(&rng_stream_, cudaStreamNonBlocking));
         if (rstream_.bytes < (size_t)steps * 8) rstream_.alloc((size_t)steps * 8);
         // readiness flags: the copy stream stamps step i + 1 into flag j after step i's copies (a
         // stream memory write, fenced after them); the step kernel polls it, so the compute stream
@@ -332,6 +330,7 @@ class Rbm {
         B2N_CUDA(cudaMemsetAsync(sready_.p, 0, 64, stream_));
         for (int j = 0; j < kStage; ++j)
             B2N_CUDA(cudaEventRecord(ev_used_[j], stream_));  // staging buffers free after prior work
+        if (!u) rng_.stream_begin(B * H_, stream_);
         for (long long i = 0; i < steps; ++i) {
             const int j = (int)(i % kStage);
             B2N_CUDA(cudaStreamWaitEvent(copy_stream_, ev_used_[j], 0));  // step i - kStage done with buffer j
@@ -341,10 +340,8 @@ class Rbm {
             if (u)
                 B2N_CUDA(cudaMemcpyAsync(su_[j].p, u + i * B * H_, (size_t)(B * H_ * 8), cudaMemcpyDefault,
                                          copy_stream_));
-            else {  // step i's draws from the device generator on its own stream, up to kStage steps ahead
-                B2N_CUDA(cudaStreamWaitEvent(rng_stream_, ev_used_[j], 0));
-                rng_.draw(su_[j].as<double>(), B * H_, rng_stream_);
-                B2N_CUDA(cudaEventRecord(ev_rng_[j], rng_stream_));
+            else {  // step i's draws from the device generator (jump-ahead pipelined), up to kStage steps ahead
+                rng_.stream_step((int)i, (int)steps, su_[j].as<double>(), ev_used_[j], ev_rng_[j]);
                 B2N_CUDA(cudaStreamWaitEvent(copy_stream_, ev_rng_[j], 0));
             }
             unsigned* flag = sready_.as<unsigned>() + j;
@@ -363,6 +360,7 @@ class Rbm {
         }
         B2N_CUDA(cudaEventRecord(ev_used_[0], copy_stream_));  // after the last draw (copy stream waited on it)
         B2N_CUDA(cudaStreamWaitEvent(stream_, ev_used_[0], 0));
+        if (!u) rng_.stream_end((int)steps, stream_);
         B2N_CUDA(cudaMemcpyAsync(recon_out, rstream_.p, (size_t)steps * 8, cudaMemcpyDeviceToHost, stream_));
         spin_sync(stream_);
         staged_B_ = B;
@@ -751,7 +749,6 @@ class Rbm {
     cudaEvent_t ev_used_[kStage] = {};
     cudaEvent_t ev_rng_[kStage] = {};
     cudaStream_t copy_stream_ = nullptr;
-    cudaStream_t rng_stream_ = nullptr;  // train_stream: the device generator runs ahead of the steps here
     DevRng rng_;               // the device copy of the caller's std::mt19937 (u == null steps)
   public:
     void read_trace(unsigned long long* h) {

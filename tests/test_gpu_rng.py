@@ -86,10 +86,13 @@ def test_cd1_pinned_direct_path_device_draws(gpu):
     np.testing.assert_array_equal(ga.state(), gb.state())
 
 
-@pytest.mark.parametrize("steps,B", [(7, 100), (1, 100), (4, 13)])
-def test_train_stream_device_draws(gpu, steps, B):
+@pytest.mark.parametrize("steps,B,H,V", [(7, 100, 500, 784), (1, 100, 500, 784), (4, 13, 500, 784),
+                                         (37, 100, 500, 784), (25, 4, 8, 16), (12, 7, 40, 24)])
+def test_train_stream_device_draws(gpu, steps, B, H, V):
+    """train_stream generates each step's draws with its start state found by jump-ahead (several steps
+    in flight): every recon, the parameters and the final generator state equal host draws supplied in
+    order -- including long streams and steps whose draws stay inside one 624-word block"""
     F = _F()
-    H, V = 500, 784
     r1, r2 = F.Rbm(H, V), F.Rbm(H, V)
     r1.init(3)
     r2.init(3)
