@@ -299,6 +299,31 @@ class CrbmWork:
     def step(self, n=1):
         self.m.run_staged(n, self.lr, self.Bg)
 
+    def e2e_total(self, steps, warmup):
+        """end to end through Crbm.train_stream (the loop of crbm_cd_update(m, v0_i, lr, rng) calls over
+        host batches): `steps` distinct pinned host batches, each step's H2D and its 691,200 Bernoulli
+        draws (generated on the device from the caller's mt19937, 16 steps in flight by jump-ahead)
+        inside the timed region, every recon read back. Device time of the call (ms)."""
+        if self.dist.world > 1:
+            return None
+        import torch
+        from oracle import oracle as O  # synthetic-input generators (std::mt19937 streams), not the measured path
+        n = steps * self.B
+        shp = self.v0_h.shape[1:]
+        if getattr(self, "_sv", None) is None or self._sv.shape[0] < n:
+            self._sv = pinned((n,) + shp, np.float32)
+            self._sv[:] = O.bernoulli_f32(11, 0.5, n * int(np.prod(shp))).reshape((n,) + shp)
+        gen = self.F.Mt19937(19)
+        self.m.train_stream(self._sv[:max(warmup, 1) * self.B], gen, self.B, self.lr)
+        s = torch.cuda.ExternalStream(self.stream())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(s)
+        self.m.train_stream(self._sv[:n], gen, self.B, self.lr)
+        e1.record(s)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
     def e2e_step(self):
         # crbm_cd_update(m, v0, lr, rng): the B*k*oh*ow draws generated on the device from the
         # caller's mt19937 (state up only when it changed, back every call)

@@ -270,6 +270,12 @@ int b2n_crbm_keep_states(b2n_crbm* crbm, int on);
  * identical update on every rank. Needs the one-launch step's shape envelope (EPARAM otherwise). */
 int b2n_crbm_dp_init(b2n_crbm* crbm, const char id[128], int rank, int world);
 int b2n_crbm_last_states(b2n_crbm* crbm, float* h0, float* hs, float* v1, float* h1);
+/* `steps` crbm_cd_update calls over consecutive host batches of v0_host (steps*batch images, NCHW):
+ * uniforms_host (steps*batch*k*oh*ow) or NULL (the device generator, several steps generated
+ * concurrently by jump-ahead); the next steps' copies overlap the current one; recon_out[i] = step i's
+ * reconstruction error. v0_host / uniforms_host may be device pointers. */
+int b2n_crbm_train_stream(b2n_crbm* crbm, const float* v0_host, const double* uniforms_host, long long steps,
+                          long long batch, float lr, double* recon_out);
 int b2n_crbm_set_rng(b2n_crbm* crbm, const unsigned state[625]);
 int b2n_crbm_get_rng(b2n_crbm* crbm, unsigned state[625]);
 int b2n_crbm_stage(b2n_crbm* crbm, const float* v0_host, const double* uniforms_host, long long batch);

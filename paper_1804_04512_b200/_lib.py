@@ -155,6 +155,7 @@ _SIGS = {
     "b2n_rbm_set_rng": ([_VP, _U], C.c_int),
     "b2n_rbm_get_rng": ([_VP, _U], C.c_int),
     "b2n_crbm_set_rng": ([_VP, _U], C.c_int),
+    "b2n_crbm_train_stream": ([_VP, _F, _D, C.c_longlong, C.c_longlong, C.c_float, _D], C.c_int),
     "b2n_crbm_get_rng": ([_VP, _U], C.c_int),
     "b2n_mt19937_draw": ([C.c_int, _U, _D, C.c_longlong], C.c_int),
     "b2n_crbm_create": ([C.c_int] * 6 + [C.c_int, C.c_int, C.POINTER(_VP)], C.c_int),

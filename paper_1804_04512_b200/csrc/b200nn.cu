@@ -404,6 +404,10 @@ int b2n_crbm_cd_update(b2n_crbm* m, const float* v0, long long batch, float lr, 
         *recon = m->impl.cd_update(v0, batch, lr, u, batch_global ? batch_global : batch);
     });
 }
+int b2n_crbm_train_stream(b2n_crbm* m, const float* v0, const double* u, long long steps, long long batch, float lr,
+                          double* recon_out) {
+    return guard([&] { m->impl.train_stream(v0, u, steps, batch, lr, recon_out); });
+}
 int b2n_crbm_last_states(b2n_crbm* m, float* h0, float* hs, float* v1, float* h1) {
     return guard([&] { m->impl.last_states(h0, hs, v1, h1); });
 }

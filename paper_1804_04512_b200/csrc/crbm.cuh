@@ -111,6 +111,10 @@ class Crbm {
     }
     ~Crbm() {
         plans_.clear();
+        for (int j = 0; j < kCrbmStage; ++j)
+            for (cudaEvent_t e : {ev_used_[j], ev_rng_[j], ev_ready_[j]})
+                if (e) cudaEventDestroy(e);
+        if (copy_stream_) cudaStreamDestroy(copy_stream_);
         if (stream_) cudaStreamDestroy(stream_);
     }
 
@@ -139,6 +143,62 @@ class Crbm {
         if (bh) B2N_CUDA(cudaMemcpyAsync(bh, P + nk, (size_t)g_.k * 4, cudaMemcpyDeviceToHost, stream_));
         if (bv) B2N_CUDA(cudaMemcpyAsync(bv, P + nk + g_.k, (size_t)g_.c * 4, cudaMemcpyDeviceToHost, stream_));
         B2N_CUDA(cudaStreamSynchronize(stream_));
+    }
+
+    // A stream of crbm_cd_update steps over host batches (the caller's loop, energy.hpp:333): step i
+    // takes images [i B, (i + 1) B) of v0 and, with u == null, its draws from the device generator --
+    // generated `gens` steps ahead with jump-ahead start states (mt19937.cuh), the 691,200 draws of a
+    // MNIST-shape step taking ~450 us on one SM. The H2D of the next steps overlaps the current one.
+    void train_stream(const float* v0, const double* u, long long steps, long long B, float lr, double* recon_out) {
+        if (dp_) throw Error(B2N_EPARAM, "train_stream: data-parallel CRBMs step through run_staged");
+        if (steps < 1 || B < 1) throw Error(B2N_ESHAPE, "train_stream: need steps >= 1 and batch >= 1");
+        ensure_capacity(B);
+        Plan& pl = plan_for(B, lr, B);
+        if (!pl.fused || pl.keep) {  // the split path: staged copies + the step graph, in order
+            for (long long i = 0; i < steps; ++i) {
+                stage(v0 + i * B * vpix(), u ? u + i * B * hpix() : nullptr, B);
+                run_staged(1, lr, B);
+                recon_out[i] = recon();
+            }
+            return;
+        }
+        constexpr int kS = kCrbmStage;  // as deep as the generators in flight (one step's draws: ~450 us)
+        for (int j = 0; j < kS; ++j) {
+            if (sv_[j].bytes < (size_t)(B * vpix() * 4)) sv_[j].alloc((size_t)(B * vpix() * 4));
+            if (su_[j].bytes < (size_t)(B * hpix() * 8)) su_[j].alloc((size_t)(B * hpix() * 8));
+            for (cudaEvent_t* e : {&ev_used_[j], &ev_rng_[j], &ev_ready_[j]})
+                if (!*e) B2N_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+        }
+        if (!copy_stream_) B2N_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
+        if (rstream_.bytes < (size_t)steps * 8) rstream_.alloc((size_t)steps * 8);
+        for (int j = 0; j < kS; ++j) B2N_CUDA(cudaEventRecord(ev_used_[j], stream_));
+        if (!u) rng_.stream_begin(B * hpix(), stream_, 16);
+        for (long long i = 0; i < steps; ++i) {
+            const int j = (int)(i % kS);
+            B2N_CUDA(cudaStreamWaitEvent(copy_stream_, ev_used_[j], 0));
+            B2N_CUDA(cudaMemcpyAsync(sv_[j].p, v0 + i * B * vpix(), (size_t)(B * vpix() * 4), cudaMemcpyDefault,
+                                     copy_stream_));
+            if (u)
+                B2N_CUDA(cudaMemcpyAsync(su_[j].p, u + i * B * hpix(), (size_t)(B * hpix() * 8), cudaMemcpyDefault,
+                                         copy_stream_));
+            else {
+                rng_.stream_step((int)i, (int)steps, su_[j].as<double>(), ev_used_[j], ev_rng_[j]);
+                B2N_CUDA(cudaStreamWaitEvent(copy_stream_, ev_rng_[j], 0));
+            }
+            B2N_CUDA(cudaEventRecord(ev_ready_[j], copy_stream_));
+            B2N_CUDA(cudaStreamWaitEvent(stream_, ev_ready_[j], 0));
+            CrbmFusedParams fp = pl.fp;
+            fp.v0 = sv_[j].as<float>();
+            fp.u = su_[j].as<double>();
+            fp.recon = rstream_.as<double>() + i;
+            launch_ex(pl.fkern, dim3(pl.fgrid), dim3(kCfThreads), pl.fsmem, stream_, 1u, fp);
+            B2N_CUDA(cudaEventRecord(ev_used_[j], stream_));
+        }
+        if (!u) rng_.stream_end((int)steps, stream_);
+        B2N_CUDA(cudaMemcpyAsync(recon_out, rstream_.p, (size_t)steps * 8, cudaMemcpyDeviceToHost, stream_));
+        spin_sync(stream_);
+        last_B_ = B;
+        last_kept_ = false;
     }
 
     // crbm_cd_update (energy.hpp:333) with the uniforms supplied: u[B][k][oh][ow]
@@ -212,6 +272,10 @@ class Crbm {
         std::vector<Op> ops;
         std::shared_ptr<DevMem> ws, vf, vd;
         cudaGraphExec_t graph = nullptr;
+        CrbmFusedParams fp;  // the one-launch step (fused plans)
+        int fgrid = 0;
+        size_t fsmem = 0;
+        void (*fkern)(CrbmFusedParams) = nullptr;
         ~Plan() {
             if (graph) cudaGraphExecDestroy(graph);
         }
@@ -309,6 +373,10 @@ class Crbm {
         pl.ops.push_back(Op([=](cudaStream_t st) {
             launch_ex(crbm_cd1_fused_kernel<KW>, dim3(grid), dim3(kCfThreads), smem, st, 1u, p);
         }, "crbm.cd1_fused", fl, by));
+        pl.fp = p;  // train_stream relaunches it with each step's buffers
+        pl.fgrid = grid;
+        pl.fsmem = smem;
+        pl.fkern = crbm_cd1_fused_kernel<KW>;
         if (dp_) {  // one exchange step: the shards' parameter sums and recon sums, then the update
             DpComm* dp = dp_.get();
             float* G = p.G;
@@ -478,6 +546,10 @@ class Crbm {
     cudaStream_t stream_ = nullptr;
     DevMem P_, Vc_, Hc_, HS_, U_, recon_;
     DevRng rng_;
+    static constexpr int kCrbmStage = 16;
+    DevMem sv_[kCrbmStage], su_[kCrbmStage], rstream_;  // train_stream: rotating v0 / draw buffers, per-step recon
+    cudaEvent_t ev_used_[kCrbmStage] = {}, ev_rng_[kCrbmStage] = {}, ev_ready_[kCrbmStage] = {};
+    cudaStream_t copy_stream_ = nullptr;
     HostPinned h_recon_;
     std::vector<std::unique_ptr<Plan>> plans_;
     std::unique_ptr<DpComm> dp_;

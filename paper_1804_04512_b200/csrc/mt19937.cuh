@@ -182,7 +182,7 @@ class DevRng {
     // ---- consecutive draws of n doubles each, pipelined (train_stream): a chain stream computes every
     // step's starting state by jump-ahead (prefix words -> XOR of windows -> block), kGen generator
     // streams produce the steps' draws concurrently. Bit-identical to draw() called step after step.
-    void stream_begin(long long n, cudaStream_t base) {
+    void stream_begin(long long n, cudaStream_t base, int gens = 3) {
         if (!valid_) throw Error(B2N_EPARAM, "device generator used before its state was set");
         if (!sm_.slots.p) {
             sm_.slots.alloc((size_t)kSlots * kSlotBytes);
@@ -191,7 +191,7 @@ class DevRng {
             for (int g = 0; g < kGen; ++g) {
                 sm_.gmeta[g].alloc(64);
                 B2N_CUDA(cudaStreamCreateWithFlags(&sm_.gen[g], cudaStreamNonBlocking));
-            }
+            }  // (one generator CTA per stream; kGen streams exist, sm_.ngen of them are used)
             B2N_CUDA(cudaStreamCreateWithFlags(&sm_.chain, cudaStreamNonBlocking));
             for (int k = 0; k < kSlots; ++k) {
                 B2N_CUDA(cudaEventCreateWithFlags(&sm_.ev_state[k], cudaEventDisableTiming));
@@ -199,8 +199,9 @@ class DevRng {
             }
             B2N_CUDA(cudaEventCreateWithFlags(&sm_.ev_base, cudaEventDisableTiming));
         }
+        sm_.ngen = std::max(1, std::min(gens, kGen));
         const size_t words = (size_t)(2 * n + 2 * kMtN + 16);
-        for (int g = 0; g < kGen; ++g)
+        for (int g = 0; g < sm_.ngen; ++g)
             if (sm_.gwbuf[g].bytes < words * 4) {
                 B2N_CUDA(cudaDeviceSynchronize());
                 sm_.gwbuf[g].alloc(words * 4);
@@ -209,7 +210,7 @@ class DevRng {
         sm_.p.assign(1, p_);
         B2N_CUDA(cudaEventRecord(sm_.ev_base, base));
         B2N_CUDA(cudaStreamWaitEvent(sm_.chain, sm_.ev_base, 0));
-        for (int g = 0; g < kGen; ++g) B2N_CUDA(cudaStreamWaitEvent(sm_.gen[g], sm_.ev_base, 0));
+        for (int g = 0; g < sm_.ngen; ++g) B2N_CUDA(cudaStreamWaitEvent(sm_.gen[g], sm_.ev_base, 0));
         B2N_CUDA(cudaMemcpyAsync(slot(0), st_.p, (kMtN + 1) * 4, cudaMemcpyDeviceToDevice, sm_.chain));
         B2N_CUDA(cudaEventRecord(sm_.ev_state[0], sm_.chain));
         for (int k = 0; k < kSlots; ++k) B2N_CUDA(cudaEventRecord(sm_.ev_gen[k], sm_.chain));
@@ -217,7 +218,7 @@ class DevRng {
     // step i of `steps`: its draws into out once `out_free` has fired; `out_ready` is recorded after them
     void stream_step(int i, int steps, double* out, cudaEvent_t out_free, cudaEvent_t out_ready) {
         const long long n = sm_.n;
-        const int si = i % kSlots, g = i % kGen;
+        const int si = i % kSlots, g = i % sm_.ngen;
         cudaStream_t gs = sm_.gen[g];
         B2N_CUDA(cudaStreamWaitEvent(gs, sm_.ev_state[si], 0));
         B2N_CUDA(cudaStreamWaitEvent(gs, out_free, 0));
@@ -258,7 +259,7 @@ class DevRng {
     void stream_end(int steps, cudaStream_t base) {
         B2N_CUDA(cudaEventRecord(sm_.ev_base, sm_.chain));
         B2N_CUDA(cudaStreamWaitEvent(base, sm_.ev_base, 0));
-        for (int g = 0; g < kGen; ++g) {
+        for (int g = 0; g < sm_.ngen; ++g) {
             B2N_CUDA(cudaEventRecord(sm_.ev_base, sm_.gen[g]));
             B2N_CUDA(cudaStreamWaitEvent(base, sm_.ev_base, 0));
         }
@@ -293,7 +294,7 @@ class DevRng {
     }
 
   private:
-    static constexpr int kSlots = 8, kGen = 3, kSlotBytes = 4096;
+    static constexpr int kSlots = 24, kGen = 16, kSlotBytes = 4096;
     struct JumpPoly {
         DevMem terms, off;
     };
@@ -322,6 +323,7 @@ class DevRng {
         cudaStream_t chain = nullptr, gen[kGen] = {};
         cudaEvent_t ev_state[kSlots] = {}, ev_gen[kSlots] = {}, ev_base = nullptr;
         long long n = 0;
+        int ngen = 3;
         std::vector<long long> p;  // position before each step of the stream in flight
         unsigned p_host[kSlots] = {};  // pinned-free staging of a position for the blk == 0 copy
     } sm_;

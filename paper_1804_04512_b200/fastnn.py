@@ -581,6 +581,26 @@ class Crbm:
         _lib.call("b2n_crbm_get_rng", self._h, st.ctypes.data_as(C.POINTER(C.c_uint)))
         rng.set_state(st)
 
+    def train_stream(self, v0, uniforms, batch: int, lr: float) -> np.ndarray:
+        """crbm_cd_update over consecutive host batches of v0 (steps*batch images); uniforms = an array
+        (steps*batch*k*oh*ow) or an Mt19937 (the draws generated on the device, rng advanced);
+        returns every step's reconstruction error"""
+        v0 = np.ascontiguousarray(v0, np.float32)
+        if v0.ndim != 4 or v0.shape[1:] != (self.c_in, self.h, self.w) or v0.shape[0] % batch:
+            raise ShapeError("train_stream: v0 must be (steps * batch, c_in, h, w)")
+        steps = v0.shape[0] // batch
+        out = np.zeros(steps, np.float64)
+        if isinstance(uniforms, Mt19937):
+            self.set_rng(uniforms)
+            _lib.call("b2n_crbm_train_stream", self._h, _f(v0), None, steps, batch, lr, _d(out))
+            self.get_rng(uniforms)
+            return out
+        u = np.ascontiguousarray(uniforms, np.float64)
+        if u.size < steps * batch * self.k * self.oh * self.ow:
+            raise ShapeError("train_stream: need steps * batch * k * oh * ow uniforms")
+        _lib.call("b2n_crbm_train_stream", self._h, _f(v0), _d(u), steps, batch, lr, _d(out))
+        return out
+
     def stage(self, v0, uniforms) -> None:
         """stage v0 and the uniforms (an array, or None: the device generator draws them)"""
         v0 = np.ascontiguousarray(v0, np.float32)

@@ -125,6 +125,23 @@ def test_crbm_device_draws_equal_supplied(gpu):
     np.testing.assert_array_equal(ga.state(), gb.state())
 
 
+@pytest.mark.parametrize("steps,B", [(6, 100), (1, 100), (5, 17)])
+def test_crbm_train_stream_device_draws(gpu, steps, B):
+    """the CRBM's streamed loop with 16 generators in flight (jump-ahead start states) equals the
+    per-call loop with the host's draws: every recon, the parameters, the generator state"""
+    F = _F()
+    m1, m2 = F.Crbm(1, 28, 28, 12, 5, 5), F.Crbm(1, 28, 28, 12, 5, 5)
+    m1.init(4)
+    m2.init(4)
+    v = O.bernoulli_f32(12, 0.5, steps * B * 784).reshape(steps * B, 1, 28, 28)
+    ga, gb = F.Mt19937(31), F.Mt19937(31)
+    rec = m1.train_stream(v, ga, B, 0.1)
+    want = [F.crbm_cd_update(m2, v[i * B:(i + 1) * B], 0.1, gb.canonical(B * 12 * 24 * 24)) for i in range(steps)]
+    np.testing.assert_array_equal(rec, np.array(want))
+    _same_params(m1, m2)
+    np.testing.assert_array_equal(ga.state(), gb.state())
+
+
 def test_dbn_device_draws_equal_host(gpu):
     F = _F()
     data = O.bernoulli_f32(2, 0.5, 250 * 64).reshape(250, 64)
