@@ -73,7 +73,7 @@ static __global__ void stage_rows_kernel(const float* __restrict__ src, long lon
 
 class Rbm {
   public:
-    static constexpr int kStage = 4;  // visible-side buffers: train_stream stages up to 4 steps ahead
+    static constexpr int kStage = 8;  // visible-side buffers: train_stream stages up to 8 steps ahead
     Rbm(long long H, long long V, int device, int precision)
         : H_(H), V_(V), device_(device), x3_(precision == B2N_TF32X3) {
         if (H < 1 || V < 1) throw Error(B2N_ESHAPE, "rbm extents must be positive");
@@ -330,7 +330,7 @@ class Rbm {
         B2N_CUDA(cudaMemsetAsync(sready_.p, 0, 64, stream_));
         for (int j = 0; j < kStage; ++j)
             B2N_CUDA(cudaEventRecord(ev_used_[j], stream_));  // staging buffers free after prior work
-        if (!u) rng_.stream_begin(B * H_, stream_);
+        if (!u) rng_.stream_begin(B * H_, stream_, 4);
         for (long long i = 0; i < steps; ++i) {
             const int j = (int)(i % kStage);
             B2N_CUDA(cudaStreamWaitEvent(copy_stream_, ev_used_[j], 0));  // step i - kStage done with buffer j
