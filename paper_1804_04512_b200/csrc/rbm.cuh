@@ -59,15 +59,19 @@ static __global__ void tf32_lo_kernel(const float4* __restrict__ x, float4* __re
 }
 
 // v0 rows into a visible staging buffer (pitch ldd) plus their tf32 lo parts (copy == 0: already there)
+// (and flags[c / 128] |= 1 for every 128-column slice holding a value that is not exact in tf32)
 static __global__ void stage_rows_kernel(const float* __restrict__ src, long long lds, float* __restrict__ dst,
-                                         float* __restrict__ dlo, long long ldd, int B, int V, int copy) {
+                                         float* __restrict__ dlo, long long ldd, int B, int V, int copy,
+                                         unsigned* flags) {
     pdl_wait();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)B * V;
          i += (long long)gridDim.x * blockDim.x) {
         const long long r = i / V, c = i % V;
         const float x = src[r * lds + c];
         if (copy) dst[r * ldd + c] = x;
-        dlo[r * ldd + c] = tf32_lo(x);
+        const float lo = tf32_lo(x);
+        dlo[r * ldd + c] = lo;
+        if (lo != 0.0f && flags[c / 128] == 0u) atomicOr(flags + c / 128, 1u);
     }
 }
 
@@ -145,6 +149,7 @@ class Rbm {
             RbmFusedParams rp = pl.rp;
             rp.v0_src = v0d;
             rp.ld_src = V_;
+            rp.v0_inexact = nullptr;  // staged in-kernel: exactness unknown, full 3xTF32
             rp.u_src = ud;
             rp.recon_out = recon_host_dev_;
             recon_mapped_ = true;
@@ -349,6 +354,7 @@ class Rbm {
             RbmFusedParams rp = pl.rp;
             rp.Vcat = Vcat_[j].as<float>();
             rp.Vlo = Vlo_[j].as<float>();
+            rp.v0_inexact = vflags_.as<unsigned>() + 16 * j;
             rp.u_src = su_[j].as<double>();
             rp.ready = flag;
             rp.ready_val = (unsigned)(i + 1);
@@ -427,6 +433,7 @@ class Rbm {
         }
         Hcat_.alloc(2 * cap_ * ldh_ * 4);
         Hlo_.alloc(2 * cap_ * ldh_ * 4);
+        vflags_.alloc((size_t)kStage * 64);
         HS_.alloc(cap_ * ldhs_ * 4);
         U_.alloc((size_t)kcap_ * cap_ * H_ * 8);
         recon_.alloc((size_t)cap_ * 64 * 8);
@@ -510,6 +517,7 @@ class Rbm {
         rp.Hcat = Hc;
         rp.Wlo = Wlo_.as<float>();
         rp.Vlo = Vlo_[0].as<float>();
+        rp.v0_inexact = vflags_.as<unsigned>();
         rp.Hlo = Hlo_.as<float>();
         rp.HS = HS_.as<float>();
         rp.u = U_.as<double>();
@@ -705,8 +713,10 @@ class Rbm {
     // the tf32 lo parts of v0 rows [0, B) of visible buffer k (after their copy into Vcat_[k])
     void stage_lo(int k, long long B, cudaStream_t st) {
         const float* Vc = Vcat_[k].as<float>();
+        unsigned* fl = vflags_.as<unsigned>() + 16 * k;
+        B2N_CUDA(cudaMemsetAsync(fl, 0, 64, st));
         launch_ex(stage_rows_kernel, dim3(grid_for(B * V_)), dim3(256), 0, st, 1u, Vc, ldv_, (float*)nullptr,
-                  Vlo_[k].as<float>(), ldv_, (int)B, (int)V_, 0);
+                  Vlo_[k].as<float>(), ldv_, (int)B, (int)V_, 0, fl);
     }
 
     void launch(Plan& pl) {
@@ -738,6 +748,7 @@ class Rbm {
     DevMem Vcat_[kStage];      // [v0; v1] (+ ones column): buffer 0 for every path, 0..3 in rotation for train_stream
     DevMem Wlo_, Vlo_[kStage], Hlo_;  // tf32 lo parts of W_aug / Vcat / Hcat (the fused step's 3xTF32 operands)
     int vb_ = 0;               // the Vcat buffer of the last step
+    DevMem vflags_;            // per visible buffer: 16 slice flags "v0 not exact in tf32" (stage_rows_kernel)
     bool wlo_valid_ = false;   // Wlo_ matches W_ (kept by the fused step; anything else that writes W clears it)
     DevMem fused_ws_, gbar_, trace_;
     HostPinned ubuf_[2];       // train_epoch: double-buffered uniforms

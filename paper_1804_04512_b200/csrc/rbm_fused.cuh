@@ -68,6 +68,7 @@ struct RbmFusedParams {
     float* Wlo;
     float* Vlo;
     float* Hlo;
+    const unsigned* v0_inexact;  // per visible slice: nonzero when some v0 of the slice has a tf32 lo part
 };
 
 // the step's TMA maps (hi operand, lo companion): K-major operands of phases 1-3, MN-major ones of
@@ -114,26 +115,26 @@ __device__ __forceinline__ void rf_grid_sync(unsigned long long* ctr, unsigned n
 // written by the producer of the operand (the phase epilogues, the v0 staging, the W update), so the
 // loop is a pure TMA -> MMA pipeline: thread 0 streams the K-blocks as slots drain, warp 1 issues the
 // MMAs, nobody else touches the ring (no per-block split pass, no per-block CTA barrier).
-// load(kb, a_hi, b_hi, b_lo, a_lo, bar) issues the boxes of K-block kb (a_lo == null when a_lo_bytes
-// == 0: an operand exact in tf32, e.g. the 0/1 hidden samples); tph = running TMEM-barrier phase.
+// load(kb, a_hi, b_hi, b_lo, a_lo, bar) issues the boxes of K-block kb (a_lo == null for the K-blocks
+// before lo_from, whose A is exact in tf32: the 0/1 samples, binary v0); tph = running TMEM-barrier phase.
 template <class Load>
 __device__ __forceinline__ void rf_product(uint8_t* ring, uint64_t* full, uint64_t* empty, uint64_t* tbar, int& tph,
-                                           int ns, int nkb, int a_bytes, int b_bytes, bool a_lo, bool a_mn,
+                                           int ns, int nkb, int a_bytes, int b_bytes, int lo_from, bool a_mn,
                                            bool b_mn, uint32_t idesc, uint32_t idesc2, Load load) {
     // stage = A hi | B hi | B lo | A lo: B hi and B lo are adjacent along N, so ONE MMA with N doubled
     // (idesc2) computes a_hi.b_hi into columns [0, N) and a_hi.b_lo into [N, 2N); a second MMA adds
     // a_lo.b_hi into [0, N). rf_tmem_to_smem folds the halves.
     const int warp = threadIdx.x >> 5;
     const int sb = 2 * (a_bytes + b_bytes);
-    const uint32_t tx = (uint32_t)(a_bytes + 2 * b_bytes + (a_lo ? a_bytes : 0));
     auto slot = [&](int g) { return ring + (g % ns) * sb; };
     if (threadIdx.x == 0) {
         for (int i = 0; i < nkb; ++i) {
             const int st = i % ns;
             if (i >= ns) mbar_wait(&empty[st], ((i / ns) - 1) & 1);
             uint8_t* d = slot(i);
-            mbar_arrive_expect_tx(&full[st], tx);
-            load(i, d, d + a_bytes, d + a_bytes + b_bytes, a_lo ? d + a_bytes + 2 * b_bytes : nullptr, &full[st]);
+            const bool lo = i >= lo_from;
+            mbar_arrive_expect_tx(&full[st], (uint32_t)(a_bytes + 2 * b_bytes + (lo ? a_bytes : 0)));
+            load(i, d, d + a_bytes, d + a_bytes + b_bytes, lo ? d + a_bytes + 2 * b_bytes : nullptr, &full[st]);
         }
     } else if (warp == 1) {
         const uint64_t a_lo_off = (uint64_t)((a_bytes + 2 * b_bytes) >> 4);
@@ -147,7 +148,7 @@ __device__ __forceinline__ void rf_product(uint8_t* ring, uint64_t* full, uint64
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk, da += a_mn ? 64 : 2, db += b_mn ? 64 : 2) {
                 mma_tf32_warp(0u, da, db, idesc2, (i | kk) != 0);
-                if (a_lo) mma_tf32_warp(0u, da + a_lo_off, db, idesc, 1);
+                if (i >= lo_from) mma_tf32_warp(0u, da + a_lo_off, db, idesc, 1);
             }
             mma_commit_warp(&empty[st]);
             if (i == nkb - 1) mma_commit_warp(tbar);
@@ -268,6 +269,9 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
         }
         rf_grid_sync(sbar_of(p, s), gridDim.y);
     }
+    // v0 of this slice exact in tf32 (all its lo parts zero: e.g. binary data), flagged by the staging
+    // kernel; unknown (the zero-copy path) counts as inexact
+    const bool v0_exact = p.v0_inexact && __ldcg(p.v0_inexact + s) == 0u;
     // the phase-1 sampling uniforms of this thread (rows 16 s + tid / 16, hidden 4 (tid % 16) of tile j),
     // loaded after v0 (which phase 1 needs first) so a host-memory read overlaps the phase-1 product
     double upre[4] = {2.0, 2.0, 2.0, 2.0};
@@ -296,13 +300,14 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
             }
         }
         const int ph = first ? 0 : 2;  // all 4 K-blocks in flight at once (4 stages of 48 KB)
+        // phase 1's A is v0: exact in tf32 when the whole slice is (binary data) -- no lo loads or MMAs
         rf_product(ring, full + 4 * ph, empty + 4 * ph, tbar, tph, 4, kRfSliceW / 32, 128 * 32 * 4, kRfTileH * 32 * 4,
-                   true, false, false, id_h, id_h2,
+                   first && v0_exact ? kRfSliceW / 32 : 0, false, false, id_h, id_h2,
                    [&](int kb, uint8_t* ah, uint8_t* bh, uint8_t* bl, uint8_t* al, uint64_t* bar) {
                        tma_load_2d(ah, &m.vk, bar, v0c + kb * 32, vrow0);
                        tma_load_2d(bh, &m.wk, bar, v0c + kb * 32, h0c);
                        tma_load_2d(bl, &m.wk_lo, bar, v0c + kb * 32, h0c);
-                       tma_load_2d(al, &m.vk_lo, bar, v0c + kb * 32, vrow0);
+                       if (al) tma_load_2d(al, &m.vk_lo, bar, v0c + kb * 32, vrow0);
                    });
         mark();
         rf_tmem_to_smem(tile, kRfTileP, kRfTileH);
@@ -376,8 +381,8 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
     // (Measured alternative: no split of K -- one CTA per 32-column tile over all 500 hidden units --
     // is slower: a single SM streams its operands from L2 at ~100 GB/s, 3.7 us for the product alone.)
     // A = the 0/1 samples: exact in tf32, no lo part -- one MMA per K step
-    rf_product(ring, full + 4, empty + 4, tbar, tph, 2, kRfTileH / 32, 128 * 32 * 4, kRfSliceW * 32 * 4, false, false,
-               true, id_v, id_v2,
+    rf_product(ring, full + 4, empty + 4, tbar, tph, 2, kRfTileH / 32, 128 * 32 * 4, kRfSliceW * 32 * 4, kRfTileH / 32,
+               false, true, id_v, id_v2,
                [&](int kb, uint8_t* ah, uint8_t* bh, uint8_t* bl, uint8_t*, uint64_t* bar) {
                    tma_load_2d(ah, &m.hsk, bar, h0c + 32 * kb, 0);
                    for (int q = 0; q < kRfSliceW / 32; ++q) {
@@ -485,11 +490,13 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
         for (int i = 0; i < kPer; ++i)
             wv[i] = (!p.grad_only && col_ok && 2 * i + r04 < nrows) ? __ldcg(wsrc + i * rstride) : 0.0f;
     }
-    rf_product(ring, full + 12, empty + 12, tbar, tph, 4, (2 * B + 31) / 32, 128 * 32 * 4, kRfTileH * 32 * 4, true,
-               true, true, id_w, id_w2, [&](int kb, uint8_t* ah, uint8_t* bh, uint8_t* bl, uint8_t* al, uint64_t* bar) {
+    // K-blocks of v0 rows only (kb < B / 32) need no A lo when the slice's v0 is exact in tf32
+    rf_product(ring, full + 12, empty + 12, tbar, tph, 4, (2 * B + 31) / 32, 128 * 32 * 4, kRfTileH * 32 * 4,
+               v0_exact ? B / 32 : 0, true, true, id_w, id_w2,
+               [&](int kb, uint8_t* ah, uint8_t* bh, uint8_t* bl, uint8_t* al, uint64_t* bar) {
                    for (int q = 0; q < 4; ++q) {
                        tma_load_2d(ah + q * 4096, &m.vmn, bar, v0c + 32 * q, kb * 32);
-                       tma_load_2d(al + q * 4096, &m.vmn_lo, bar, v0c + 32 * q, kb * 32);
+                       if (al) tma_load_2d(al + q * 4096, &m.vmn_lo, bar, v0c + 32 * q, kb * 32);
                    }
                    for (int q = 0; q < kRfTileH / 32; ++q) {
                        tma_load_2d(bh + q * 4096, &m.hmn, bar, h0c + 32 * q, kb * 32);
