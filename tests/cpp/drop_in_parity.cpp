@@ -181,6 +181,65 @@ static bool device_rng_criterion() {
     return ok;
 }
 
+// the op-level layer API: fastnn's conv_forward / conv_backward / pool_forward / pool_backward /
+// softmax / softmax_cross_entropy and the b2n_op_* calls on the same fastnn::Tensors, bit for bit
+static bool ops_criterion() {
+    using b200nn::detail::pack_rows;
+    auto same = [](const std::vector<float>& a, const fastnn::Tensor& t) {
+        const std::vector<float> b = pack_rows(t);
+        return a.size() == b.size() && std::memcmp(a.data(), b.data(), a.size() * 4) == 0;
+    };
+    std::mt19937 g(17);
+    std::uniform_real_distribution<float> d(-1.0f, 1.0f);
+    auto fill = [&](fastnn::Tensor& t) {
+        for (std::size_t r = 0; r < t.rows_total(); ++r)
+            for (std::size_t j = 0; j < t.last_dim(); ++j) t.row_ptr(r)[j] = d(g);
+    };
+    fastnn::ConvShape s;
+    s.n = 3, s.c_in = 4, s.k = 6, s.kh = 3, s.kw = 3, s.h = 12, s.w = 10, s.pad = 0;
+    fastnn::ConvLayer L(s);
+    fill(L.kernels);
+    fill(L.b);
+    fastnn::Tensor x = fastnn::make_tensor({3, 4, 12, 10});
+    fill(x);
+    b2n_conv_shape cs{3, 4, 6, 3, 3, 12, 10, 0};
+    const fastnn::Tensor y = fastnn::conv_forward(L, x);
+    std::vector<float> yb(pack_rows(y).size());
+    b200nn::check(b2n_op_conv_forward(0, &cs, pack_rows(x).data(), pack_rows(L.kernels).data(), pack_rows(L.b).data(),
+                                      yb.data()));
+    bool ok = same(yb, y);
+    fastnn::Tensor dy = fastnn::make_tensor({3, 6, 10, 8});
+    fill(dy);
+    std::vector<float> gk = pack_rows(L.gk), gb = pack_rows(L.gb), dxb(pack_rows(x).size());
+    const fastnn::Tensor dx = fastnn::conv_backward(L, x, dy);
+    b200nn::check(b2n_op_conv_backward(0, &cs, pack_rows(x).data(), pack_rows(L.kernels).data(), pack_rows(dy).data(),
+                                       gk.data(), gb.data(), dxb.data()));
+    ok = ok && same(dxb, dx) && same(gk, L.gk) && same(gb, L.gb);
+    const fastnn::PoolResult pr = fastnn::pool_forward(fastnn::PoolMode::Max, y);
+    std::vector<float> py(pack_rows(pr.y).size()), pa(py.size());
+    b200nn::check(b2n_op_pool_forward(0, 0, 3 * 6, 10, 8, yb.data(), py.data(), pa.data()));
+    ok = ok && same(py, pr.y) && same(pa, pr.argmax);
+    const fastnn::Tensor pdx = fastnn::pool_backward(fastnn::PoolMode::Max, pr.y, pr.argmax);
+    std::vector<float> pdxb(pack_rows(pdx).size());
+    b200nn::check(b2n_op_pool_backward(0, 0, 3 * 6, 5, 4, py.data(), pa.data(), pdxb.data()));
+    ok = ok && same(pdxb, pdx);
+    fastnn::Tensor z = fastnn::make_tensor({7, 10});
+    fill(z);
+    const fastnn::Tensor pz = fastnn::softmax(z);
+    std::vector<float> pzb(70);
+    b200nn::check(b2n_op_softmax(0, 7, 10, pack_rows(z).data(), pzb.data()));
+    fastnn::Tensor lab = fastnn::make_tensor({7, 10});
+    for (int r = 0; r < 7; ++r) lab.at(r, (r * 3) % 10) = 1.0f;
+    const fastnn::LossGrad lg = fastnn::softmax_cross_entropy(pz, lab);
+    std::vector<float> dl(70);
+    double loss = 0.0;
+    b200nn::check(b2n_op_softmax_cross_entropy(0, 7, 10, pzb.data(), pack_rows(lab).data(), dl.data(), &loss));
+    ok = ok && same(pzb, pz) && same(dl, lg.dlogits) && std::fabs(loss - lg.loss) <= 1e-13 * std::fabs(lg.loss);
+    std::printf("criterion op_level_api: %s -- conv_forward, conv_backward (dx, gk, gb), pool_forward / backward, "
+                "softmax, softmax_cross_entropy bit-identical\n", ok ? "PASS" : "FAIL");
+    return ok;
+}
+
 int main() {
     using FL = fastnn::LayerDesc;
     using BL = b200nn::LayerDesc;
@@ -261,5 +320,6 @@ int main() {
     }
     ok &= fit_checkpoint_criterion();
     ok &= device_rng_criterion();
+    ok &= ops_criterion();
     return ok ? 0 : 1;
 }

@@ -15,4 +15,4 @@ def test_cpp_drop_in_parity(gpu):
     r = subprocess.run([str(BIN)], capture_output=True, text=True, timeout=600)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
-    assert r.stdout.count("PASS") == 7
+    assert r.stdout.count("PASS") == 8
