@@ -894,11 +894,11 @@ struct ConvTWParams {
 };
 
 constexpr int kWgChunk = 16;  // output columns per sliding-window run
-// thread count / kernels per thread of the weight-gradient kernel for a filter size
+// kernels per thread of the weight-gradient kernel for a filter size (the thread count NT is a
+// template parameter: 512 = one CTA per SM, 256 = two; 5x5 runs 256 threads, one CTA per SM)
 template <int KH, int KW>
 struct WgCfg {
-    static constexpr int KG = KH * KW <= 9 ? 8 : 4;           // kernels per thread (register accumulators)
-    static constexpr int NT = KH * KW <= 9 ? 512 : 256;       // threads
+    static constexpr int KG = KH * KW <= 9 ? 8 : 4;  // register accumulators
 };
 
 // Thread (stream st, channel c, kernel group kg) owns dW[KG*kg .. KG*kg+KG)[c][.][.] over the pixel runs
@@ -907,12 +907,12 @@ struct WgCfg {
 // into a double-buffered slot (the next tile's loads fly while this one computes); dZ is expanded from
 // the slot into smem, and the bias gradient (sum of dZ) is accumulated there, per thread in a fixed
 // quad, reduced in fixed order at the end.
-template <int KH, int KW>
-__global__ void __launch_bounds__(WgCfg<KH, KW>::NT, 1)
+template <int KH, int KW, int NT>
+__global__ void __launch_bounds__(NT, NT <= 256 && KH * KW <= 9 ? 2 : 1)
     convt_wgrad_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapZdP,
                        const __grid_constant__ CUtensorMap mapZP, const __grid_constant__ CUtensorMap mapZc,
                        const ConvTWParams p) {
-    constexpr int KG = WgCfg<KH, KW>::KG, NT = WgCfg<KH, KW>::NT, T = KH * KW;
+    constexpr int KG = WgCfg<KH, KW>::KG, T = KH * KW;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* slots[2] = {smem, smem + p.slot_bytes};  // [X halo | dZ staging]
@@ -973,14 +973,18 @@ __global__ void __launch_bounds__(WgCfg<KH, KW>::NT, 1)
         tile_of(t, b, y0, x0);
         const int sy0 = p.z.pool ? y0 >> 1 : y0, sx0 = (p.z.pool ? x0 >> 1 : x0) & ~3;
         uint8_t* zslot = slots[sl] + hb;
+        // the other slot was released by the previous tile's closing barrier: its next fill flies
+        // during this whole tile (dZ expansion + FMAs)
+        if (threadIdx.x < 32 && t + (int)gridDim.x < p.ntiles) issue(t + gridDim.x, sl ^ 1);
         mbar_wait(&full[sl], (it >> 1) & 1);
         if (!p.z.tma) {
             zs_load_sync(p.z, zslot, b, sy0, sx0, threadIdx.x, NT);
             __syncthreads();
         }
-        if (threadIdx.x < (NT / Kq) * Kq)
-            for (int pi = threadIdx.x / Kq; pi < npx; pi += NT / Kq) {  // dZ of the tile, quad bq
-                const int r = pi / p.Wt, xx = pi - r * p.Wt;
+        if (threadIdx.x < (NT / Kq) * Kq) {
+            const int step = NT / Kq;
+            int r = (threadIdx.x / Kq) / p.Wt, xx = threadIdx.x / Kq - r * p.Wt;
+            for (int pi = threadIdx.x / Kq; pi < npx; pi += step) {  // dZ of the tile, quad bq
                 const int Y = y0 + r, X = x0 + xx;
                 float4 d = make_float4(0.f, 0.f, 0.f, 0.f);
                 if (Y < p.OH && X < p.OW) d = zs_dz(p.z, zslot, sy0, sx0, bq, Y, X);
@@ -989,9 +993,10 @@ __global__ void __launch_bounds__(WgCfg<KH, KW>::NT, 1)
                 bsum.y += d.y;
                 bsum.z += d.z;
                 bsum.w += d.w;
+                for (xx += step; xx >= p.Wt; xx -= p.Wt) ++r;
             }
-        __syncthreads();  // dz ready; the other slot (previous tile) is free
-        if (threadIdx.x < 32 && t + (int)gridDim.x < p.ntiles) issue(t + gridDim.x, sl ^ 1);
+        }
+        __syncthreads();  // dz ready
         if (active) {
             const float* hx = reinterpret_cast<const float*>(slots[sl]);
             const int cq = c >> 2, cj = c & 3;
@@ -1340,7 +1345,7 @@ struct ConvTWLaunch {
     ConvTWParams p;
     CUtensorMap map;
     CUtensorMap zmaps[3];
-    int grid = 1, smem = 0;
+    int grid = 1, smem = 0, nt = 512;  // nt: threads per CTA (256 -> two CTAs per SM)
     std::shared_ptr<DevMem> ws;
     float *kern = nullptr, *kvel = nullptr, *bias = nullptr, *bvel = nullptr, *gk = nullptr, *gb = nullptr;
     float lr = 0, mom = 0, wd = 0;
@@ -1379,22 +1384,35 @@ inline ConvTWLaunch plan_convt_wgrad(const ConvTLaunch& f, int K, int C, const D
     if (!((p.kh == 3 && p.kw == 3) || (p.kh == 5 && p.kw == 5)))
         throw Error(B2N_EINTERNAL, "convt wgrad: only 3x3 and 5x5 filters are instantiated");
     const int T = p.kh * p.kw;
-    const int KG = T <= 9 ? 8 : 4, NT = T <= 9 ? 512 : 256;  // WgCfg
+    const int KG = T <= 9 ? 8 : 4;  // WgCfg
     const int TPS = C * ((p.Kp + KG - 1) / KG);
+    int NT = T <= 9 ? 512 : 256;
     if (TPS > NT) throw Error(B2N_ESHAPE, "convt wgrad: channels x kernel groups exceed one CTA");
-    const int streams = NT / TPS;
-    // its own tile height: as many output rows as fit (compute per tile must hide the next tile's loads)
-    const int red_bytes = streams * TPS * KG * T * 4 + NT * 16;
-    auto smem_for = [&](int R) {
+    auto smem_for = [&](int R, int nt) {
         DZSrc zz = p.z;
         zz.bh = z0.pool ? R / 2 : R;
         const int halo = (R + p.kh - 1) * p.G * p.P * 16;
         const int slot = (((halo + 127) & ~127) + zs_bytes(zz) + 1023) & ~1023;
+        const int red_bytes = (nt / TPS) * TPS * KG * T * 4 + nt * 16;
         return 1024 + std::max(2 * slot + R * p.Kp * p.Wt * 4 + 64, red_bytes);
     };
-    const int ohe = (p.OH + 1) & ~1;
-    p.R = std::min(std::max(2, ohe), 16);
-    while (p.R > 2 && smem_for(p.R) > 200 * 1024) p.R -= 2;
+    // its own tile height: as many output rows as fit (compute per tile must hide the next tile's loads)
+    auto rows_for = [&](int nt, int cap) {
+        int R = std::min(std::max(2, (p.OH + 1) & ~1), 16);
+        while (R > 2 && smem_for(R, nt) > cap) R -= 2;
+        return R;
+    };
+    p.R = rows_for(NT, 200 * 1024);
+    // 3x3 filters: two 256-thread CTAs per SM when a tile of >= 4 rows fits half the shared memory --
+    // one CTA's per-tile barrier and dZ expansion overlap the other's FMAs
+    if (T <= 9 && TPS <= 256 && !std::getenv("B2N_CONVT_WG_WIDE")) {
+        const int R2 = rows_for(256, 112 * 1024);
+        if (R2 >= 4 && smem_for(R2, 256) <= 112 * 1024) {
+            NT = 256;
+            p.R = R2;
+        }
+    }
+    const int streams = NT / TPS;
     p.HR = p.R + p.kh - 1;
     p.tiles_y = (p.OH + p.R - 1) / p.R;
     p.ntiles = p.B * p.tiles_x * p.tiles_y;
@@ -1405,8 +1423,9 @@ inline ConvTWLaunch plan_convt_wgrad(const ConvTLaunch& f, int K, int C, const D
     p.slot_bytes = (((p.halo_bytes + 127) & ~127) + zs_bytes(p.z) + 1023) & ~1023;
     L.map = f.map;
     dz_maps(p.z, p.B, L.zmaps);
-    L.grid = std::min(p.ntiles, sm_count());
-    L.smem = smem_for(p.R);
+    L.nt = NT;
+    L.grid = std::min(p.ntiles, (NT <= 256 && T <= 9 ? 2 : 1) * sm_count());
+    L.smem = smem_for(p.R, NT);
     if (L.smem > 227 * 1024) throw Error(B2N_ESHAPE, "convt wgrad: tile does not fit shared memory");
     L.ws = std::make_shared<DevMem>();
     L.ws->alloc((size_t)L.grid * p.ws_stride * 4);

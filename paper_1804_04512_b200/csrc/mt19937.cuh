@@ -208,6 +208,12 @@ class DevRng {
             }
         sm_.n = n;
         sm_.p.assign(1, p_);
+        // every jump distance this step size can need (a step starting at position p covers
+        // (p + 2n - 1) / 624 blocks: two or three values over p in [0, 624]), prepared here so no
+        // later step of this or a following stream stops for the host-side polynomial work
+        if (n > 0)
+            for (long long blk = (2 * n - 1) / kMtN; blk <= (2 * n + kMtN - 1) / kMtN; ++blk)
+                if (blk > 0) jump_poly(kMtN * blk - 1);
         B2N_CUDA(cudaEventRecord(sm_.ev_base, base));
         B2N_CUDA(cudaStreamWaitEvent(sm_.chain, sm_.ev_base, 0));
         for (int g = 0; g < sm_.ngen; ++g) B2N_CUDA(cudaStreamWaitEvent(sm_.gen[g], sm_.ev_base, 0));

@@ -658,15 +658,31 @@ class Mt19937:
 
     def __init__(self, seed: int):
         self._rs = np.random.RandomState(seed)
+        self._st = None  # the libstdc++ state when it is newer than _rs (set by the device generator)
+
+    @property
+    def _rs(self):
+        if self._st is not None:  # bring the host generator up to the state the device left
+            self.__rs.set_state(("MT19937", self._st[:624].copy(), int(self._st[624]), 0, 0.0))
+            self._st = None
+        return self.__rs
+
+    @_rs.setter
+    def _rs(self, rs):
+        self.__rs = rs
+        self._st = None
 
     def state(self) -> np.ndarray:
         """the libstdc++ state (_M_x[624], _M_p) as 625 uint32 -- what the device generator takes"""
-        _, key, pos, _, _ = self._rs.get_state(legacy=True)
+        if self._st is not None:
+            return self._st.copy()
+        _, key, pos, _, _ = self.__rs.get_state(legacy=True)
         return np.concatenate([np.asarray(key, np.uint32), np.asarray([pos], np.uint32)])
 
     def set_state(self, st) -> None:
-        st = np.asarray(st, np.uint32)
-        self._rs.set_state(("MT19937", st[:624].copy(), int(st[624]), 0, 0.0))
+        """(kept as the 625 words; numpy's generator is re-seeded from them only when the host draws
+        next -- a loop of device-drawn steps never pays for the conversion)"""
+        self._st = np.array(st, np.uint32).reshape(625)
 
     def canonical(self, n: int) -> np.ndarray:
         u = self._rs.randint(0, 2 ** 32, size=2 * n, dtype=np.uint64).reshape(n, 2).astype(np.float64)
