@@ -134,6 +134,32 @@ __device__ __forceinline__ float4 zs_dz(const DZSrc& z, const uint8_t* slot, int
     return make_float4(d[0], d[1], d[2], d[3]);
 }
 
+// the same for the two conv-output rows Ye (even) and Ye + 1 of one pooled row at column X: one
+// read of the pooled cell (dP, P, codes) and one act' per channel feed both (pooled layers only)
+__device__ __forceinline__ void zs_dz2(const DZSrc& z, const uint8_t* slot, int sy0, int sx0, int q, int Ye, int X,
+                                       float4& d0, float4& d1) {
+    d0 = d1 = make_float4(0.f, 0.f, 0.f, 0.f);
+    const bool vx = (unsigned)X < (unsigned)z.OWz;
+    const bool v0 = vx && (unsigned)Ye < (unsigned)z.OHz, v1 = vx && (unsigned)(Ye + 1) < (unsigned)z.OHz;
+    if (!(v0 || v1)) return;
+    const int idx = (((Ye >> 1) - sy0) * z.Kq + q) * z.bw + ((X >> 1) - sx0);
+    const float4 g = reinterpret_cast<const float4*>(slot)[idx];
+    const float4 y = reinterpret_cast<const float4*>(slot + zs_off_p(z))[idx];
+    const uint32_t cw = reinterpret_cast<const uint32_t*>(slot + 2 * zs_off_p(z))[idx];
+    const float a[4] = {act_grad(z.act, g.x, y.x), act_grad(z.act, g.y, y.y), act_grad(z.act, g.z, y.z),
+                        act_grad(z.act, g.w, y.w)};
+    const uint32_t w0 = (uint32_t)(X & 1), w1 = w0 + 2u;
+    float e0[4], e1[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint32_t c = (cw >> (8 * j)) & 0xFFu;
+        e0[j] = v0 && c == w0 ? a[j] : 0.0f;
+        e1[j] = v1 && c == w1 ? a[j] : 0.0f;
+    }
+    d0 = make_float4(e0[0], e0[1], e0[2], e0[3]);
+    d1 = make_float4(e1[0], e1[1], e1[2], e1[3]);
+}
+
 enum ConvTMode : int { CT_FWD = 0, CT_DGRAD = 1 };
 constexpr int kCtMaxKSteps = 16;  // K steps per halo row: kw * ceil(quads / 2) (or ceil(kw / 2) for one quad)
 
@@ -824,14 +850,30 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
                     asm volatile("bar.sync 1, %0;" ::"r"(NP) : "memory");
                 }
                 mbar_wait_sleep(&empty[s], ((it / S) & 1) ^ 1);
-                for (int i = pt; i < chunks; i += NP) {
-                    const int row = i / (p.G * p.P), rem = i - row * (p.G * p.P);
-                    const int q = rem / p.P, col = rem - q * p.P;
-                    const float4 d = zs_dz(p.z, slot, sy0, sx0, q, Y0 + row, X0 + col);
+                auto put = [&](int i, const float4& d) {
                     reinterpret_cast<float4*>(hi)[i] = d;
                     if (X3)
                         reinterpret_cast<float4*>(lo)[i] =
                             make_float4(split_lo1(d.x), split_lo1(d.y), split_lo1(d.z), split_lo1(d.w));
+                };
+                const int GP = p.G * p.P;
+                if (p.z.pool) {  // by pooled row: both conv rows of a pooled cell from one read of it
+                    const int pr0 = Y0 >> 1;  // floor (Y0 = -pad on the top tile)
+                    const int items = (((Y0 + p.HR - 1) >> 1) - pr0 + 1) * GP;
+                    for (int i = pt; i < items; i += NP) {
+                        const int a = i / GP, rem = i - a * GP;
+                        const int Ye = 2 * (pr0 + a), r0 = Ye - Y0;  // halo rows r0 (may be -1), r0 + 1
+                        float4 d0, d1;
+                        zs_dz2(p.z, slot, sy0, sx0, rem / p.P, Ye, X0 + rem % p.P, d0, d1);
+                        if (r0 >= 0) put(r0 * GP + rem, d0);
+                        if (r0 + 1 < p.HR) put((r0 + 1) * GP + rem, d1);
+                    }
+                } else {
+                    for (int i = pt; i < chunks; i += NP) {
+                        const int row = i / GP, rem = i - row * GP;
+                        const int q = rem / p.P, col = rem - q * p.P;
+                        put(i, zs_dz(p.z, slot, sy0, sx0, q, Y0 + row, X0 + col));
+                    }
                 }
                 fence_proxy_async_smem();
                 mbar_arrive(&full[s]);
@@ -981,7 +1023,21 @@ __global__ void __launch_bounds__(NT, NT <= 256 && KH * KW <= 9 ? 2 : 1)
             zs_load_sync(p.z, zslot, b, sy0, sx0, threadIdx.x, NT);
             __syncthreads();
         }
-        if (threadIdx.x < (NT / Kq) * Kq) {
+        if (threadIdx.x < (NT / Kq) * Kq && p.z.pool) {  // pooled: rows in pairs, one read per pooled cell
+            const int step = NT / Kq;
+            int a = (threadIdx.x / Kq) / p.Wt, xx = threadIdx.x / Kq - a * p.Wt;
+            for (int pi = threadIdx.x / Kq; pi < npx / 2; pi += step) {
+                float4 d0, d1;
+                zs_dz2(p.z, zslot, sy0, sx0, bq, y0 + 2 * a, x0 + xx, d0, d1);
+                reinterpret_cast<float4*>(dz)[(2 * a * Kq + bq) * p.Wt + xx] = d0;
+                reinterpret_cast<float4*>(dz)[((2 * a + 1) * Kq + bq) * p.Wt + xx] = d1;
+                bsum.x += d0.x + d1.x;
+                bsum.y += d0.y + d1.y;
+                bsum.z += d0.z + d1.z;
+                bsum.w += d0.w + d1.w;
+                for (xx += step; xx >= p.Wt; xx -= p.Wt) ++a;
+            }
+        } else if (threadIdx.x < (NT / Kq) * Kq) {
             const int step = NT / Kq;
             int r = (threadIdx.x / Kq) / p.Wt, xx = threadIdx.x / Kq - r * p.Wt;
             for (int pi = threadIdx.x / Kq; pi < npx; pi += step) {  // dZ of the tile, quad bq

@@ -359,6 +359,7 @@ class Rbm {
             rp.ready = flag;
             rp.ready_val = (unsigned)(i + 1);
             rp.recon_out = rstream_.as<double>() + i;
+            if (rp.trace) rp.trace += 256 * (i & 1);  // bring-up: consecutive steps in separate halves
             launch_ex(rbm_cd1_fused_kernel, dim3(kRfSlices, rp.jt), dim3(kRfThreads), (size_t)kRfSmem, stream_, 1u,
                       pl.maps[j], rp);
             B2N_CUDA(cudaEventRecord(ev_used_[j], stream_));
@@ -539,7 +540,7 @@ class Rbm {
         rp.G = G_.as<float>();
         rp.grad_only = (dp_ || grad_only_) ? 1 : 0;
         if (std::getenv("B2N_RBM_TRACE")) {
-            if (!trace_.p) trace_.alloc(256 * 8);
+            if (!trace_.p) trace_.alloc(512 * 8);  // two steps (train_stream alternates)
             rp.trace = trace_.as<unsigned long long>();
         }
         // TMA maps: K-major operands of phases 1-3, MN-major ones of phases 2 and 4 (see rbm_fused.cuh),
@@ -764,7 +765,7 @@ class Rbm {
   public:
     void read_trace(unsigned long long* h) {
         B2N_CUDA(cudaDeviceSynchronize());
-        if (trace_.p) B2N_CUDA(cudaMemcpy(h, trace_.p, 256 * 8, cudaMemcpyDeviceToHost));
+        if (trace_.p) B2N_CUDA(cudaMemcpy(h, trace_.p, 512 * 8, cudaMemcpyDeviceToHost));
     }
   private:  // fused CD-1 kernel: phase-2 partials, grid-barrier counters
     HostPinned h_recon_;

@@ -535,8 +535,9 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
     __syncthreads();
     mark();
     // the step's reconstruction error straight into host-mapped memory: the last CTA to finish sums
-    // the (slice, row) partials written in phase 2 (rows over lanes, slices in order, then a fixed
-    // shuffle tree) -- no device-to-host copy behind the step
+    // the (slice, row) partials written in phase 2 in recon_tree_sum's order (rows over lanes, slices
+    // in order, then a fixed shuffle tree), every load issued before the first add (B <= 128: one
+    // round trip) -- no device-to-host copy behind the step
     if (p.recon_out) {
         __shared__ unsigned s_last;
         if (threadIdx.x == 0) {
@@ -546,9 +547,17 @@ __global__ void __cluster_dims__(kRfSlices, 1, 1) __launch_bounds__(kRfThreads, 
         __syncthreads();
         if (s_last && warp == 0) {
             const int lane = threadIdx.x & 31;
-            double acc = 0.0;
-            for (int r = lane; r < B; r += 32)
-                for (int s2 = 0; s2 < kRfSlices; ++s2) acc += __ldcg(p.row_part + (long long)s2 * p.cap + r);
+            double v[4][kRfSlices], acc = 0.0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int s2 = 0; s2 < kRfSlices; ++s2)
+                    v[i][s2] = lane + 32 * i < B ? __ldcg(p.row_part + (long long)s2 * p.cap + lane + 32 * i) : 0.0;
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                if (lane + 32 * i < B)
+#pragma unroll
+                    for (int s2 = 0; s2 < kRfSlices; ++s2) acc += v[i][s2];
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
             if (lane == 0) {

@@ -9,7 +9,7 @@ lib = _lib.load()
 rbm = F.Rbm(500, 784); rbm.init(42)
 rbm.stage(O.bernoulli_f32(3, 0.5, 100 * 784).reshape(100, 784), O.canonical_f64(5, 100 * 500).reshape(100, 500))
 rbm.run_staged(5, 0.1, 100)
-buf = np.zeros(256, np.uint64)
+buf = np.zeros(512, np.uint64)
 lib.b2n_debug_rbm_trace(rbm.handle, buf.ctypes.data_as(C.c_void_p))
 names = ["start", "p1.mma", "p1.cbar", "p1.red", "p1.end", "bar1", "p2.mma", "p2.wr", "bar2", "p2.red", "bar3",
          "p3.mma", "p3.cbar", "p3.red", "p3.end", "bar4", "p4.mma", "p4.ts", "p4.end"]
