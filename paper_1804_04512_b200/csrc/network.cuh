@@ -745,9 +745,18 @@ inline void Net::build_plan(Plan& pl) {
                 int* am = argmax_;
                 float* pr = probs_;
                 float bd = (float)pl.Bg;
+                // one CTA per row, the row staged in shared memory
+                const size_t smem = (size_t)((C + 3) & ~3LL) * 4;
+                if (smem > 200 * 1024) throw Error(B2N_ESHAPE, "softmax: more than 51,200 classes");
+                static bool sx_attr = [] {
+                    B2N_CUDA(cudaFuncSetAttribute(softmax_xent_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                  200 * 1024));
+                    return true;
+                }();
+                (void)sx_attr;
                 fwd.push_back(Op([=](cudaStream_t s) {
-                    launch_ex(softmax_xent_rows_kernel, dim3((B * 32 + 255) / 256), dim3(256), 0, s, 1u,
-                              (const float*)lg, ldl, B, (int)C, (const int*)lab, bd, D, ldd, rl, am, pr, C);
+                    launch_ex(softmax_xent_rows_kernel, dim3(B), dim3(kSxThreads), smem, s, 1u, (const float*)lg, ldl, B,
+                              (int)C, (const int*)lab, bd, D, ldd, rl, am, pr, C);
                 }, "softmax_xent", 0.0, (double)B * C * 16));
                 ++nk_fwd;
                 if (ldd < C + 1) throw Error(B2N_EINTERNAL, "dlogits pitch");

@@ -601,42 +601,79 @@ static __global__ void axpy_kernel(float4* __restrict__ w, const float4* __restr
 // softmax + softmax_cross_entropy for class counts beyond one tensor-core tile: one warp per row,
 // the max / exp-sum / normalise passes run in the reference's sequential order by lane 0 after a
 // warp-parallel max (max is order-independent), so dlogits and loss follow network.hpp:410-437.
-static __global__ void softmax_xent_rows_kernel(const float* __restrict__ logits, long long ld, int rows, int cols,
-                                         const int* __restrict__ labels, float batch_div, float* __restrict__ dlogits,
-                                         long long ldd, double* __restrict__ row_loss, int* __restrict__ argmax,
-                                         float* __restrict__ probs, long long ldp) {
+// softmax + cross-entropy over rows of > 256 classes (layers.hpp:301-320, network.hpp:423-437): one CTA
+// of kSxThreads per row, the row staged once in shared memory (float4 loads, all in flight). The exp
+// terms are computed in parallel; ONE thread sums them in the reference's sequential order (the fp32
+// add chain, 4 clk per class, is the floor of the row); then every thread finishes its share of the
+// row: probs, loss, gradient (q - onehot) / batch written once, and the first-max argmax of q (fixed
+// tree: lowest index on equal q).
+constexpr int kSxThreads = 128;
+static __global__ void __launch_bounds__(kSxThreads) softmax_xent_rows_kernel(
+    const float* __restrict__ logits, long long ld, int rows, int cols, const int* __restrict__ labels, float batch_div,
+    float* __restrict__ dlogits, long long ldd, double* __restrict__ row_loss, int* __restrict__ argmax,
+    float* __restrict__ probs, long long ldp) {
+    extern __shared__ __align__(16) float e[];  // [cols rounded up to 4]
+    __shared__ float s_red[kSxThreads / 32];
+    __shared__ int s_idx[kSxThreads / 32];
+    __shared__ float s_sum;
     pdl_wait();
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (warp >= rows) return;
-    const float* z = logits + (long long)warp * ld;
+    const int row = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (row >= rows) return;
+    const float* z = logits + (long long)row * ld;
+    float* dl = dlogits + (long long)row * ldd;
     float mx = -INFINITY;
-    for (int j = lane; j < cols; j += 32) mx = fmaxf(mx, z[j]);
-    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    // exp terms in parallel, then the sequential sum (layers.hpp:312-315 order)
-    float* dl = dlogits + (long long)warp * ldd;
-    for (int j = lane; j < cols; j += 32) dl[j] = expf(z[j] - mx);
-    __syncwarp();
-    if (lane == 0) {
-        float sum = 0.0f;
-        for (int j = 0; j < cols; ++j) sum += dl[j];
-        dl[cols] = sum;  // ldd >= cols + 1 guaranteed by the planner
+    const int c4 = (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(logits) & 15) == 0 ? cols >> 2 : 0;
+#pragma unroll 4
+    for (int i = tid; i < c4; i += kSxThreads) {
+        const float4 v = *reinterpret_cast<const float4*>(z + 4 * i);
+        *reinterpret_cast<float4*>(e + 4 * i) = v;
+        mx = fmaxf(mx, fmaxf(fmaxf(v.x, v.y), fmaxf(v.z, v.w)));
     }
-    __syncwarp();
-    const float sum = dl[cols];
-    const int label = labels[warp];
+    for (int j = 4 * c4 + tid; j < cols; j += kSxThreads) {
+        const float v = z[j];
+        e[j] = v;
+        mx = fmaxf(mx, v);
+    }
+    for (int o = 16; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) s_red[w] = mx;
+    __syncthreads();
+    mx = s_red[0];
+#pragma unroll
+    for (int i = 1; i < kSxThreads / 32; ++i) mx = fmaxf(mx, s_red[i]);
+#pragma unroll 4
+    for (int j = tid; j < cols; j += kSxThreads) e[j] = expf(e[j] - mx);
+    __syncthreads();
+    if (tid == 0) {  // sequential, layers.hpp:312-315 order
+        float sum = 0.0f;
+        int j = 0;
+#pragma unroll 8
+        for (; j + 4 <= cols; j += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(e + j);
+            sum += v.x;
+            sum += v.y;
+            sum += v.z;
+            sum += v.w;
+        }
+        for (; j < cols; ++j) sum += e[j];
+        s_sum = sum;
+    }
+    __syncthreads();
+    const float sum = s_sum;
+    const int label = labels[row];
     float bestp = -1.0f;
     int best = 0;
-    for (int j = lane; j < cols; j += 32) {
-        const float q = dl[j] / sum;
+#pragma unroll 4
+    for (int j = tid; j < cols; j += kSxThreads) {
+        const float q = e[j] / sum;
         if (q > bestp) {
             bestp = q;
             best = j;
         }
-        if (probs) probs[(long long)warp * ldp + j] = q;
-        if (j == label) row_loss[warp] = -log(fmax((double)q, 1e-300));
+        if (probs) probs[(long long)row * ldp + j] = q;
+        if (j == label) row_loss[row] = -log(fmax((double)q, 1e-300));
         dl[j] = (q - (j == label ? 1.0f : 0.0f)) / batch_div;
     }
-    for (int o = 16; o; o >>= 1) {  // first-max argmax across lanes
+    for (int o = 16; o; o >>= 1) {  // first-max argmax: lanes, then warps
         const float bp = __shfl_xor_sync(0xffffffffu, bestp, o);
         const int bi = __shfl_xor_sync(0xffffffffu, best, o);
         if (bp > bestp || (bp == bestp && bi < best)) {
@@ -644,10 +681,20 @@ static __global__ void softmax_xent_rows_kernel(const float* __restrict__ logits
             best = bi;
         }
     }
-    __syncwarp();
+    __syncthreads();  // s_red reused
     if (lane == 0) {
-        dl[cols] = 0.0f;
-        if (argmax) argmax[warp] = best;
+        s_red[w] = bestp;
+        s_idx[w] = best;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int i = 1; i < kSxThreads / 32; ++i)
+            if (s_red[i] > bestp || (s_red[i] == bestp && s_idx[i] < best)) {
+                bestp = s_red[i];
+                best = s_idx[i];
+            }
+        dl[cols] = 0.0f;  // the ones column of the next dW product
+        if (argmax) argmax[row] = best;
     }
 }
 
