@@ -38,6 +38,8 @@ CASES = [
     ((16, 12, 12), [(32, 3, 1, True)], 4, CF.relu),                       # 4 quads -> 32 kernels
     ((1, 17, 17), [(9, 3, 0, False), (4, 5, 1, False)], 2, CF.sigmoid),   # odd widths, 1 channel
     ((3, 36, 36), [(12, 5, 0, True), (12, 5, 0, True)], 2, CF.relu),      # CIFAR-like, 3 quads
+    ((4, 14, 10), [(8, 3, 1, True), (16, 3, 1, False)], 3, CF.relu),      # pooled maps of odd extent (7x5)
+    ((3, 64, 64), [(16, 3, 1, True), (16, 3, 1, True)], 2, CF.sigmoid),   # ImageNet-like 3x3 pad 1, tall tiles
 ]
 
 

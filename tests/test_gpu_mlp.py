@@ -157,3 +157,37 @@ def test_train_stream_adam_and_single_step(gpu):
     for i in range(a.num_params()):
         np.testing.assert_array_equal(a.get_param(i), b.get_param(i))
     assert list(c.train_stream(x[:B], lab[:B], B)) == la[:1]
+
+
+@pytest.mark.parametrize("classes,B", [(257, 37), (1003, 19), (1000, 128), (4099, 5)])
+def test_wide_softmax_rows(gpu, classes, B):
+    """more than 256 classes: the row-per-CTA softmax-cross-entropy kernel (the reference's sequential
+    exp sum, layers.hpp:312-315) -- ragged class counts, unaligned rows, the ImageNet head's 1000 x 128;
+    loss, gradients, probabilities and argmax against the oracle, then two SGD steps"""
+    from paper_1804_04512_b200 import fastnn as F
+    spec = {"name": "wide", "input": [30], "layers": [CF.dense(30, 40), CF.sigmoid(), CF.dense(40, classes),
+                                                      CF.softmax()],
+            "lr": 0.1, "momentum": 0.9, "weight_decay": 0.0, "batch_size": B, "seed": 5}
+    net = F.build_network(spec)
+    orc = O.Net(spec)
+    x, lab = inputs(spec, B, seed=3)
+    lg = net.forward_backward(x, lab)
+    lo = orc.forward_backward(x, lab)
+    assert abs(lg - lo) / abs(lo) < TOL, (lg, lo)
+    for i in range(net.num_params()):
+        assert norm_err(net.get_param(i, F.GRAD).ravel(), orc.get(i, 1)) < 1e-4, i
+    probs, am = F.forward_batch(net, x, return_argmax=True)
+    op, oa = orc.forward(x)
+    assert norm_err(probs, op) < 1e-5
+    check_argmax(am, probs, op, oa)
+    y = np.zeros((B, classes), np.float32)
+    y[np.arange(B), lab] = 1
+    # fresh nets: the shim's forward_backward leaves the reference's accumulated gradients behind
+    # (layers accumulate; train_minibatch zeroes only at its end, network.hpp:463-471)
+    net, orc = F.build_network(spec), O.Net(spec)
+    for step in range(2):
+        lg = F.train_minibatch(net, x, y)
+        lo = orc.train_minibatch(x, lab)
+        assert abs(lg - lo) / abs(lo) < TOL, (step, lg, lo)
+    for i in range(net.num_params()):
+        assert norm_err(net.get_param(i).ravel(), orc.get(i)) < TOL, i
