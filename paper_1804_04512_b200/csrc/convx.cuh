@@ -74,19 +74,25 @@ __global__ void __launch_bounds__(128, 4) convx_fwd_kernel(const ConvXParams p) 
         // planes by 4-byte async copies (one round trip for the whole halo; consecutive threads read
         // consecutive floats of a [quad][col][4] row run), zero-filled outside the map (padding)
         const int ys = y0 - p.pad, xs = x0 - p.pad;
+        // a thread keeps its (quad, col, j) positions of a halo row and walks the rows (no per-element
+        // index division)
         const int rowlen = p.G * p.PW * 4;  // floats of one halo row: [quad][col][4]
-        const int m = p.HR * rowlen;
         const float* xb = p.x + (long long)b * p.x_bstride;
-        for (int i = tid; i < m; i += nt) {
-            const int row = i / rowlen, r2 = i - row * rowlen;
+        const long long ystride = (long long)p.G * p.Win * 4;
+        for (int r2 = tid; r2 < rowlen; r2 += nt) {
             const int q = r2 / (p.PW * 4), r3 = r2 - q * (p.PW * 4);
             const int col = r3 >> 2, j = r3 & 3;
             const int c = 4 * q + j;
             if (c >= p.C) continue;
-            const int iy = ys + row, ix = xs + col;
-            const bool in = (unsigned)iy < (unsigned)p.Hin && (unsigned)ix < (unsigned)p.Win;
-            cp_async4(hs + c * plane + row * p.PWp + col,
-                      in ? xb + (((long long)iy * p.G + q) * p.Win + ix) * 4 + j : xb, in ? 4 : 0);
+            const int ix = xs + col;
+            const bool inx = (unsigned)ix < (unsigned)p.Win;
+            float* dst = hs + c * plane + col;
+            const float* src = xb + ((long long)q * p.Win + ix) * 4 + j;
+            for (int row = 0; row < p.HR; ++row) {
+                const int iy = ys + row;
+                const bool in = inx && (unsigned)iy < (unsigned)p.Hin;
+                cp_async4(dst + row * p.PWp, in ? src + iy * ystride : xb, in ? 4 : 0);
+            }
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
         float* wsf = reinterpret_cast<float*>(ws);
