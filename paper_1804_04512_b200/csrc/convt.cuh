@@ -859,14 +859,16 @@ __global__ void __launch_bounds__(CtRoles<MODE, X3>::kThreads, 1)
                 const int GP = p.G * p.P;
                 if (p.z.pool) {  // by pooled row: both conv rows of a pooled cell from one read of it
                     const int pr0 = Y0 >> 1;  // floor (Y0 = -pad on the top tile)
-                    const int items = (((Y0 + p.HR - 1) >> 1) - pr0 + 1) * GP;
-                    for (int i = pt; i < items; i += NP) {
-                        const int a = i / GP, rem = i - a * GP;
-                        const int Ye = 2 * (pr0 + a), r0 = Ye - Y0;  // halo rows r0 (may be -1), r0 + 1
-                        float4 d0, d1;
-                        zs_dz2(p.z, slot, sy0, sx0, rem / p.P, Ye, X0 + rem % p.P, d0, d1);
-                        if (r0 >= 0) put(r0 * GP + rem, d0);
-                        if (r0 + 1 < p.HR) put((r0 + 1) * GP + rem, d1);
+                    const int prn = ((Y0 + p.HR - 1) >> 1) - pr0 + 1;
+                    for (int rem = pt; rem < GP; rem += NP) {  // (quad, col) fixed per thread, walk the rows
+                        const int q = rem / p.P, X = X0 + rem - q * p.P;
+                        for (int a = 0; a < prn; ++a) {
+                            const int Ye = 2 * (pr0 + a), r0 = Ye - Y0;  // halo rows r0 (may be -1), r0 + 1
+                            float4 d0, d1;
+                            zs_dz2(p.z, slot, sy0, sx0, q, Ye, X, d0, d1);
+                            if (r0 >= 0) put(r0 * GP + rem, d0);
+                            if (r0 + 1 < p.HR) put((r0 + 1) * GP + rem, d1);
+                        }
                     }
                 } else {
                     for (int i = pt; i < chunks; i += NP) {
