@@ -1167,22 +1167,49 @@ static __global__ void convt_wgrad_reduce_kernel(const float* __restrict__ ws, i
 // NCHW (C real channels, per-image pitch ld) -> row-blocked [b][y][Cp/4][x][4], zero channels past C
 static __global__ void convt_repack_kernel(const float* __restrict__ x, long long ld, int B, int C, int H, int W,
                                            float* __restrict__ out, long long obstride) {
+    // NCHW -> row-blocked quads. Vector path: a thread takes 4 consecutive pixels of one image row (one
+    // float4 load per plane, a 4x4 transpose, 4 float4 stores); the CTA covers blockDim / (W / 4) rows
+    // per iteration. Index math once per thread, not per element.
     pdl_wait();
     const int G = (C + 3) >> 2;
-    const long long n = (long long)B * H * G * W;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-        const int xx = (int)(i % W);
-        long long r = i / W;
-        const int q = (int)(r % G);
-        r /= G;
-        const int y = (int)(r % H);
-        const int b = (int)(r / H);
-        const float* src = x + (long long)b * ld + (long long)y * W + xx;
-        float v[4];
+    const long long plane = (long long)H * W;
+    const long long rows = (long long)B * H;
+    const bool vec = (W & 3) == 0 && (ld & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0 &&
+                     W / 4 <= (int)blockDim.x;
+    if (vec) {
+        const int w4 = W / 4, per = blockDim.x / w4;
+        const int x4 = threadIdx.x % w4, sub = threadIdx.x / w4;
+        if (sub >= per) return;
+        for (long long row = (long long)blockIdx.x * per + sub; row < rows; row += (long long)gridDim.x * per) {
+            const int b = (int)(row / H), y = (int)(row - (long long)b * H);
+            const float* src = x + (long long)b * ld + (long long)y * W;
+            float* dst = out + (long long)b * obstride + (long long)y * G * W * 4;
+            for (int q = 0; q < G; ++q) {
+                float4 v[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = 4 * q + j < C ? __ldg(src + (long long)(4 * q + j) * H * W) : 0.0f;
-        *reinterpret_cast<float4*>(out + (long long)b * obstride + ((long long)(y * G + q) * W + xx) * 4) =
-            make_float4(v[0], v[1], v[2], v[3]);
+                for (int j = 0; j < 4; ++j)
+                    v[j] = 4 * q + j < C ? __ldg(reinterpret_cast<const float4*>(src + (4 * q + j) * plane) + x4)
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+                float4* d = reinterpret_cast<float4*>(dst + ((long long)q * W + 4 * x4) * 4);
+                d[0] = make_float4(v[0].x, v[1].x, v[2].x, v[3].x);
+                d[1] = make_float4(v[0].y, v[1].y, v[2].y, v[3].y);
+                d[2] = make_float4(v[0].z, v[1].z, v[2].z, v[3].z);
+                d[3] = make_float4(v[0].w, v[1].w, v[2].w, v[3].w);
+            }
+        }
+        return;
+    }
+    for (long long row = blockIdx.x; row < rows; row += gridDim.x) {
+        const int b = (int)(row / H), y = (int)(row - (long long)b * H);
+        const float* src = x + (long long)b * ld + (long long)y * W;
+        float* dst = out + (long long)b * obstride + (long long)y * G * W * 4;
+        for (int q = 0; q < G; ++q)
+            for (int xx = threadIdx.x; xx < W; xx += blockDim.x) {
+                float v[4];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) v[j] = 4 * q + j < C ? __ldg(src + (4 * q + j) * plane + xx) : 0.0f;
+                *reinterpret_cast<float4*>(dst + ((long long)q * W + xx) * 4) = make_float4(v[0], v[1], v[2], v[3]);
+            }
     }
 }
 
