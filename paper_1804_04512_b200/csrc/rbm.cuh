@@ -58,21 +58,47 @@ static __global__ void tf32_lo_kernel(const float4* __restrict__ x, float4* __re
     }
 }
 
-// v0 rows into a visible staging buffer (pitch ldd) plus their tf32 lo parts (copy == 0: already there)
-// (and flags[c / 128] |= 1 for every 128-column slice holding a value that is not exact in tf32)
+// v0 rows into a visible staging buffer (pitch ldd) plus their tf32 lo parts (copy == 0: already there),
+// and flags[s] = 1 iff 128-column slice s holds a value that is not exact in tf32 (0 otherwise, every
+// one of the 16 flags written -- no memset before). CTA s owns slice s over all B rows: lanes take
+// float4 columns, the warps take rows.
 static __global__ void stage_rows_kernel(const float* __restrict__ src, long long lds, float* __restrict__ dst,
                                          float* __restrict__ dlo, long long ldd, int B, int V, int copy,
                                          unsigned* flags) {
     pdl_wait();
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < (long long)B * V;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long r = i / V, c = i % V;
-        const float x = src[r * lds + c];
-        if (copy) dst[r * ldd + c] = x;
-        const float lo = tf32_lo(x);
-        dlo[r * ldd + c] = lo;
-        if (lo != 0.0f && flags[c / 128] == 0u) atomicOr(flags + c / 128, 1u);
+    const int s = blockIdx.x, c0 = 128 * s, c1 = min(V, c0 + 128);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const bool vec = (V & 3) == 0 && ((lds | ldd) & 3) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+                     (reinterpret_cast<uintptr_t>(dlo) & 15) == 0 && (!copy || (reinterpret_cast<uintptr_t>(dst) & 15) == 0);
+    int inexact = 0;
+#pragma unroll 4
+    for (int r = w; r < B; r += nw) {
+        const float* sr = src + (long long)r * lds;
+        float* dr = dst + (long long)r * ldd;
+        float* lr = dlo + (long long)r * ldd;
+        if (vec) {
+            const int c = c0 + 4 * lane;
+            if (c < c1) {
+                const float4 x = *reinterpret_cast<const float4*>(sr + c);
+                if (copy) *reinterpret_cast<float4*>(dr + c) = x;
+                const float4 lo = make_float4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w));
+                *reinterpret_cast<float4*>(lr + c) = lo;
+                inexact |= lo.x != 0.0f || lo.y != 0.0f || lo.z != 0.0f || lo.w != 0.0f;
+            }
+        } else {
+            for (int c = c0 + lane; c < c1; c += 32) {
+                const float x = sr[c];
+                if (copy) dr[c] = x;
+                const float lo = tf32_lo(x);
+                lr[c] = lo;
+                inexact |= lo != 0.0f;
+            }
+        }
     }
+    inexact = __syncthreads_or(inexact);
+    if (threadIdx.x == 0 && s < 16) flags[s] = inexact ? 1u : 0u;  // (only the fused step's slices are read)
+    if (s == 0)
+        for (int t = gridDim.x + threadIdx.x; t < 16; t += blockDim.x) flags[t] = 0u;
 }
 
 class Rbm {
@@ -715,8 +741,7 @@ class Rbm {
     void stage_lo(int k, long long B, cudaStream_t st) {
         const float* Vc = Vcat_[k].as<float>();
         unsigned* fl = vflags_.as<unsigned>() + 16 * k;
-        B2N_CUDA(cudaMemsetAsync(fl, 0, 64, st));
-        launch_ex(stage_rows_kernel, dim3(grid_for(B * V_)), dim3(256), 0, st, 1u, Vc, ldv_, (float*)nullptr,
+        launch_ex(stage_rows_kernel, dim3((unsigned)((V_ + 127) / 128)), dim3(1024), 0, st, 1u, Vc, ldv_, (float*)nullptr,
                   Vlo_[k].as<float>(), ldv_, (int)B, (int)V_, 0, fl);
     }
 
