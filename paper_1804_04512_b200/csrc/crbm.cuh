@@ -162,7 +162,7 @@ class Crbm {
             }
             return;
         }
-        constexpr int kS = kCrbmStage;  // as deep as the generators in flight (one step's draws: ~450 us)
+        constexpr int kS = kCrbmStage;  // as deep as the generators in flight (one step's draws: ~550 us)
         for (int j = 0; j < kS; ++j) {
             if (sv_[j].bytes < (size_t)(B * vpix() * 4)) sv_[j].alloc((size_t)(B * vpix() * 4));
             if (su_[j].bytes < (size_t)(B * hpix() * 8)) su_[j].alloc((size_t)(B * hpix() * 8));
@@ -172,7 +172,7 @@ class Crbm {
         if (!copy_stream_) B2N_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
         if (rstream_.bytes < (size_t)steps * 8) rstream_.alloc((size_t)steps * 8);
         for (int j = 0; j < kS; ++j) B2N_CUDA(cudaEventRecord(ev_used_[j], stream_));
-        if (!u) rng_.stream_begin(B * hpix(), stream_, 16);
+        if (!u) rng_.stream_begin(B * hpix(), stream_, 24);
         for (long long i = 0; i < steps; ++i) {
             const int j = (int)(i % kS);
             B2N_CUDA(cudaStreamWaitEvent(copy_stream_, ev_used_[j], 0));
@@ -546,7 +546,7 @@ class Crbm {
     cudaStream_t stream_ = nullptr;
     DevMem P_, Vc_, Hc_, HS_, U_, recon_;
     DevRng rng_;
-    static constexpr int kCrbmStage = 16;
+    static constexpr int kCrbmStage = 24;
     DevMem sv_[kCrbmStage], su_[kCrbmStage], rstream_;  // train_stream: rotating v0 / draw buffers, per-step recon
     cudaEvent_t ev_used_[kCrbmStage] = {}, ev_rng_[kCrbmStage] = {}, ev_ready_[kCrbmStage] = {};
     cudaStream_t copy_stream_ = nullptr;

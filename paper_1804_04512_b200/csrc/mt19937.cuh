@@ -300,7 +300,7 @@ class DevRng {
     }
 
   private:
-    static constexpr int kSlots = 24, kGen = 16, kSlotBytes = 4096;
+    static constexpr int kSlots = 40, kGen = 32, kSlotBytes = 4096;
     struct JumpPoly {
         DevMem terms, off;
     };
