@@ -9,7 +9,7 @@
 set -u
 cd "$(dirname "$0")/.."
 CS=${CS:-/usr/local/cuda/bin/compute-sanitizer}
-SEL=${SEL:-"tests/test_gpu_rbm.py::test_cd1_step tests/test_gpu_gemm.py tests/test_gpu_convt_shapes.py tests/test_gpu_crbm.py::test_crbm_cd1_step tests/test_gpu_rng.py"}
+SEL=${SEL:-"tests/test_gpu_rbm.py::test_cd1_step tests/test_gpu_gemm.py tests/test_gpu_convt_shapes.py tests/test_gpu_crbm.py::test_crbm_cd1_step tests/test_gpu_rng.py tests/test_gpu_mlp.py::test_wide_softmax_rows"}
 status=0
 for tool in memcheck racecheck synccheck initcheck; do
     echo "=== compute-sanitizer --tool $tool"
