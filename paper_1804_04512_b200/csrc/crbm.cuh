@@ -170,7 +170,8 @@ class Crbm {
                 if (!*e) B2N_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         }
         if (!copy_stream_) B2N_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
-        if (rstream_.bytes < (size_t)steps * 8) rstream_.alloc((size_t)steps * 8);
+        // per-step recon slots, grown geometrically (no allocation inside a later, longer stream)
+        if (rstream_.bytes < (size_t)steps * 8) rstream_.alloc(std::max<size_t>((size_t)steps * 8 * 2, 8192));
         for (int j = 0; j < kS; ++j) B2N_CUDA(cudaEventRecord(ev_used_[j], stream_));
         if (!u) rng_.stream_begin(B * hpix(), stream_, 24);
         for (long long i = 0; i < steps; ++i) {

@@ -353,7 +353,8 @@ class Rbm {
             if (!ev_rng_[j]) B2N_CUDA(cudaEventCreateWithFlags(&ev_rng_[j], cudaEventDisableTiming));
         }
         if (!copy_stream_) B2N_CUDA(cudaStreamCreateWithFlags(&copy_stream_, cudaStreamNonBlocking));
-        if (rstream_.bytes < (size_t)steps * 8) rstream_.alloc((size_t)steps * 8);
+        // per-step recon slots, grown geometrically (no allocation inside a later, longer stream)
+        if (rstream_.bytes < (size_t)steps * 8) rstream_.alloc(std::max<size_t>((size_t)steps * 8 * 2, 8192));
         // readiness flags: the copy stream stamps step i + 1 into flag j after step i's copies (a
         // stream memory write, fenced after them); the step kernel polls it, so the compute stream
         // carries no cross-stream event and consecutive steps keep their programmatic overlap
