@@ -1488,11 +1488,13 @@ inline ConvTWLaunch plan_convt_wgrad(const ConvTLaunch& f, int K, int C, const D
         return R;
     };
     p.R = rows_for(NT, 200 * 1024);
-    // 3x3 filters: two 256-thread CTAs per SM when a tile of >= 4 rows fits half the shared memory --
+    // 3x3 filters: two 256-thread CTAs per SM when a tile fits half the shared memory (B2N_CONVT_WG_R2MIN:
+    // the least tile height taken, default 2; B2N_CONVT_WG_WIDE: always one 512-thread CTA) --
     // one CTA's per-tile barrier and dZ expansion overlap the other's FMAs
     if (T <= 9 && TPS <= 256 && !std::getenv("B2N_CONVT_WG_WIDE")) {
         const int R2 = rows_for(256, 112 * 1024);
-        if (R2 >= 4 && smem_for(R2, 256) <= 112 * 1024) {
+        static const int r2min = std::getenv("B2N_CONVT_WG_R2MIN") ? std::atoi(std::getenv("B2N_CONVT_WG_R2MIN")) : 2;
+        if (R2 >= r2min && smem_for(R2, 256) <= 112 * 1024) {
             NT = 256;
             p.R = R2;
         }
