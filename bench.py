@@ -549,7 +549,7 @@ def peaks():
     return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
 
 
-def roofline(prof, precision, tf32_meas=None):
+def roofline(prof, precision, tf32_meas=None, config=None):
     hbm, bf16, src = peaks()
     top = max(prof, key=lambda o: o["ms"])
     # tensor peak for the arithmetic in use: the measured TF32 rate (3xTF32 issues 3 products)
@@ -564,9 +564,9 @@ def roofline(prof, precision, tf32_meas=None):
     sec = top["ms"] * 1e-3
     traffic = None
     tp = ROOT / "profiles" / "ncu_traffic.json"
-    if tp.exists():
-        try:
-            traffic = json.loads(tp.read_text()).get(top["name"])
+    if tp.exists() and config:
+        try:  # keyed "<config>/<op>" (profiles/summarize.py); null when that config's op was not captured
+            traffic = json.loads(tp.read_text()).get(f"{config}/{top['name']}")
         except Exception:
             traffic = None
     if ai < ridge:
@@ -582,12 +582,12 @@ def roofline(prof, precision, tf32_meas=None):
             "peak_source": tsrc, "share_of_step": None}
 
 
-def step_roofline(work, prof, precision, tf32, step_ms):
+def step_roofline(work, prof, precision, tf32, step_ms, config=None):
     """The dominant kernel's roofline (algorithmic bytes or FLOPs per launch / its event-timed launch
     duration) plus the whole step's: the planner's algorithmic bytes of every op / the step time,
     against the measured HBM peak, and the launch floor (dependent kernels x the measured 4.2 us
     single-kernel graph-launch latency, tools/launch_probe.cu)."""
-    rl = roofline(prof, precision, tf32)
+    rl = roofline(prof, precision, tf32, config)
     prof_step = sum(o["ms"] for o in prof)
     rl["share_of_step"] = round(max(o["ms"] for o in prof) / prof_step, 4) if prof_step else None
     hbm = peaks()[0]
@@ -777,7 +777,7 @@ def main():
     value = work.Bg * a.steps / (total_ms * 1e-3)
     e2e_val = work.Bg * a.steps / (e2e_ms * 1e-3)
     tf32 = measure_tf32_peak(dev)
-    rl = step_roofline(work, prof, a.precision, tf32, step_ms)
+    rl = step_roofline(work, prof, a.precision, tf32, step_ms, a.config)
     line = {"metric": "train samples/s", "value": round(value, 2), "unit": "samples/s", "n_gpus": dist.world,
             "steps": a.steps, "warmup": a.warmup, "ms_per_step": round(step_ms, 5), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": getattr(work, "dtype", None) or (
@@ -819,7 +819,7 @@ def main():
                                 "ms_per_step": round(ms / n, 5),
                                 "e2e": round(w.Bg * max(n // 2, 5) / (e2 * 1e-3), 2),
                                 "kernels_per_step": w.kernels_per_step(),
-                                "roofline": step_roofline(w, wprof, a.precision, tf32, ms / n)}
+                                "roofline": step_roofline(w, wprof, a.precision, tf32, ms / n, name)}
                 if dist.rank == 0 and dist.world == 1:  # the reference's own step beside every config
                     big = name == "imagenet_cnn"
                     cv, ci = cpu_reference(name, 0.0 if big else 3.0, min_steps=1 if big else 2,

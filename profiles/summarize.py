@@ -79,28 +79,46 @@ def launch_share(csv_path: Path):
     return agg
 
 
+def launch_bytes(csv_path: Path):
+    """[(kernel name, DRAM read + write bytes)] per launch, in launch order"""
+    rows = [r for r in csv.reader(open(csv_path)) if r and not r[0].startswith("==")]
+    head = rows[0]
+    ki, vi, mi, ii = head.index("Kernel Name"), head.index("Metric Value"), head.index("Metric Name"), head.index("ID")
+    ui = head.index("Metric Unit")
+    acc, order = {}, []
+    for r in rows[1:]:
+        if r[mi] not in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            continue
+        v = float(r[vi].replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(r[ui], 1)
+        if r[ii] not in acc:
+            acc[r[ii]] = [r[ki], 0.0]
+            order.append(r[ii])
+        acc[r[ii]][1] += v
+    return [tuple(acc[i]) for i in order]
+
+
 def main(tag: str):
     lines = [f"# ncu summary, round tag `{tag}` (B200, `--clock-control none`)", "",
              "Captured with `profiles/capture.sh` under gpurun; numbers from single-kernel replay",
              "(cold-cache, serialised): compare SHARES with bench.py's live CUDA-event timings, not absolutes.", ""]
     traffic = {}
-    for rep, names, title in [(OUT / f"{tag}_rbm_full.ncu-rep", ["rbm.cd1_fused"],
-                               "RBM CD-1 step (headline): the fused single-kernel step"),
+    for rep, names, title, cfg in [(OUT / f"{tag}_rbm_full.ncu-rep", ["rbm.cd1_fused"],
+                               "RBM CD-1 step (headline): the fused single-kernel step", "rbm"),
                               (OUT / f"{tag}_rbm_split_full.ncu-rep", RBM_STEP,
-                               "RBM CD-1 step, split path (4 GEMM launches; data-parallel mode, B2N_RBM_FUSED=0)"),
+                               "RBM CD-1 step, split path (4 GEMM launches; data-parallel mode, B2N_RBM_FUSED=0)", None),
                               (OUT / f"{tag}_crbm_full.ncu-rep", ["crbm.cd1_fused"],
-                               "Convolutional RBM CD-1 (SURVEY 8(f)4, MNIST shape): the one-launch step"),
+                               "Convolutional RBM CD-1 (SURVEY 8(f)4, MNIST shape): the one-launch step", "crbm"),
                               (OUT / f"{tag}_crbm_split_full.ncu-rep", CRBM_SPLIT,
-                               "Convolutional RBM CD-1, split tensor-core path (B2N_CRBM_FUSED=0)"),
+                               "Convolutional RBM CD-1, split tensor-core path (B2N_CRBM_FUSED=0)", None),
                               (OUT / f"{tag}_imagenet_conv_full.ncu-rep", IMAGENET_CONV,
                                "ImageNet-shape CNN (batch 128): conv kernels of one step (convx forward, "
-                               "tcgen05 dgrad, FFMA wgrad)"),
+                               "tcgen05 dgrad, FFMA wgrad)", "imagenet_cnn"),
                               (OUT / f"{tag}_mt_full.ncu-rep", ["mt.words", "mt.canonical"],
-                               "Device std::mt19937 stream: words (one-CTA wavefront) + canonical (grid)"),
+                               "Device std::mt19937 stream: words (one-CTA wavefront) + canonical (grid)", "rng"),
                               (OUT / f"{tag}_bw_imagenet.ncu-rep", ["bw"] * 6,
-                               "Bandwidth kernels of the ImageNet-shape step (softmax-xent rows, wgrad reduce + SGD, repack)"),
+                               "Bandwidth kernels of the ImageNet-shape step (softmax-xent rows, wgrad reduce + SGD, repack)", None),
                               (OUT / f"{tag}_bw_optim.ncu-rep", ["bw"] * 6,
-                               "Packed optimizer passes (SGD in data-parallel mode, Adam/Adagrad/Adadelta)")]:
+                               "Packed optimizer passes (SGD in data-parallel mode, Adam/Adagrad/Adadelta)", None)]:
         if not rep.exists() and not rep.with_suffix(".raw.csv").exists():
             continue
         rows = raw_rows(rep)
@@ -125,7 +143,10 @@ def main(tag: str):
         for i, d in enumerate(rows):
             op = names[i] if i < len(names) else "?"
             tb = (d.get("dram_read") or 0) + (d.get("dram_write") or 0)
-            traffic.setdefault(op, tb)  # per launch: bench.py's roofline `traffic`
+            # per launch, keyed "<config>/<op>" as bench.py's roofline `traffic` looks it up (the same op
+            # name, e.g. conv1.dgrad, names different kernels in different configs)
+            if cfg and op not in ("bw", "?"):
+                traffic.setdefault(f"{cfg}/{op}", tb)
             gbs = tb / (d.get('dur_us') or 1e9) / 1e3
             lines.append(f"| {op} | `{d['kernel'][:60]}` | {d.get('dur_us', 0):.2f} | {tb / 1e6:.3f} | {gbs:.0f} | "
                          f"{d.get('dram_pct', 0):.1f} | {d.get('tensor_pct', 0):.1f} | {d.get('sm_pct', 0):.1f} | "
@@ -159,6 +180,22 @@ def main(tag: str):
                   f"| UTCBAR | {counts['UTCBAR']} | tcgen05.commit -> mbarrier |",
                   f"| HMMA | {counts['HMMA']} | legacy mma.sync (none expected) |", ""]
     (PROF / f"{tag}_ncu_summary.md").write_text("\n".join(lines) + "\n")
+    # the dominant op of the small configs from their launch lists (DRAM bytes per launch, last step):
+    # the one tcgen05 dgrad of the MNIST / CIFAR step (conv1.dgrad) and the MLP's first GEMM (dense0)
+    for cfg, pick in [("mnist_cnn", ("conv1.dgrad", "convt_mma_kernel", -1)),
+                      ("cifar_cnn", ("conv1.dgrad", "convt_mma_kernel", -1)),
+                      ("mlp", ("dense0.fwd+act", "gemm_tc_kernel", -8))]:
+        p = OUT / f"{tag}_launches_{cfg}.csv"
+        if not p.exists():
+            continue
+        launches = launch_bytes(p)
+        sel = [b for k, b in launches if pick[1] in k]
+        if len(sel) >= -pick[2]:
+            traffic[f"{cfg}/{pick[0]}"] = sel[pick[2]]
+    # bench.py's ops that are two launches: the FFMA weight gradient + its reduce/SGD pass
+    for k in list(traffic):
+        if k.endswith(".wgrad") and k + "_reduce+sgd" in traffic:
+            traffic[k + "+sgd"] = traffic[k] + traffic[k + "_reduce+sgd"]
     (PROF / "ncu_traffic.json").write_text(json.dumps(traffic, indent=1) + "\n")
     print("\n".join(lines))
 
