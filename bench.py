@@ -250,6 +250,9 @@ class RbmWork:
     def kernels_per_step(self):
         return _kernels(self.F._lib, "b2n_rbm_kernels_per_step", self.rbm.handle)
 
+    def stream_launches_per_step(self):  # train_stream: the fused step + stage_rows_kernel (tf32 lo of v0)
+        return self.kernels_per_step() + 1
+
     def profile(self, steps):
         return _profile(self.F._lib, "b2n_rbm_profile", self.rbm.handle, steps, self.lr, self.Bg)
 
@@ -799,7 +802,9 @@ def main():
                             "steps, > L2) / Network.train_stream, each step's H2D overlapped with the previous "
                             "step, per-step result read back" if e2e_mode == "stream" else "one public-API step call per step (H2D, step, "
                             "result read), L2 flushed between steps")},
-            "gpu_launches": work.kernels_per_step() * a.steps,
+            # the `value` region's launches: the step kernels (+ the streamed loop's v0 staging kernel per step)
+            "gpu_launches": (work.stream_launches_per_step() if value_mode == "stream" and
+                             hasattr(work, "stream_launches_per_step") else work.kernels_per_step()) * a.steps,
             "kernels_per_step": work.kernels_per_step(),
             "roofline": rl,
             "tensor_peaks": tf32,
