@@ -259,11 +259,19 @@ inline ConvXLaunch plan_convx_fwd(int B, int C, int Hin, int Win, int kh, int kw
     L.threads = std::max(32, ((p.SR / 2) * (p.TW / 2) + 31) / 32 * 32);
     // several passes per tile when the channel planes are small (few input channels): the CTA's fixed
     // costs (weights, the halo round trip, launch) are paid once per TR rows (<= ~40 KB of planes)
-    p.TR = p.SR;
-    p.HR = p.TR + kh - 1;
     p.PW = p.TW + kw - 1;
     p.PWp = (p.PW + 2) & ~1;  // float2 loads: even pitch, and room for the (KW + 1)-th column of the last window
     p.tiles_x = (p.OW + p.TW - 1) / p.TW;
+    p.TR = p.SR;
+    {  // taller tiles while the planes stay small and the grid keeps >= 8 CTAs per SM
+        static const int maxpass = std::getenv("B2N_CONVX_PASSES") ? std::atoi(std::getenv("B2N_CONVX_PASSES")) : 4;
+        auto planes = [&](int tr) { return (long long)C * (tr + kh - 1) * p.PWp * 4; };
+        auto ctas = [&](int tr) { return (long long)B * p.tiles_x * ((p.OH + tr - 1) / tr); };
+        while (p.TR + p.SR <= ((p.OH + 1) & ~1) && p.TR < maxpass * p.SR && planes(p.TR + p.SR) <= 40 * 1024 &&
+               ctas(p.TR + p.SR) >= 8LL * sm_count())
+            p.TR += p.SR;
+    }
+    p.HR = p.TR + kh - 1;
     p.tiles_y = (p.OH + p.TR - 1) / p.TR;
     L.smem = C * kh * kw * L.kq * 16 + C * p.HR * p.PWp * 4;  // weights (KQ float4 per tap) + planes
     if (L.smem > 226 * 1024) throw Error(B2N_ESHAPE, "b200nn conv: exact-forward tile does not fit shared memory");
