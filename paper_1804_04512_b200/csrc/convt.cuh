@@ -1267,9 +1267,12 @@ inline void ct_tile_shape(int B, int OH, int OW, int NK, int kh, int& R, int& Wt
     R = std::min(R, std::max(2, ohe));
     // two TMEM buffers of (R + 2(kh-1)) row slots of NK columns
     while (2 * (R + 2 * (kh - 1)) * NK > 512 && R > 2) R -= 2;
-    // small maps: keep >= 2 tiles per SM so every SM has a pipeline to run
+    // small maps: optionally shrink R until there are per_sm tiles per SM (B2N_CT_TILES_PER_SM). Off by
+    // default: measured, the taller tiles win (MNIST / CIFAR conv1 dgrad 28.7 / 55.0 -> 24.7 / 48.8 us)
+    // -- a tile's pipeline latency, not the SM count, bounds these small layers
     const long long tx = (OW + Wt - 1) / Wt;
-    while (R > 2 && (long long)B * tx * ((OH + R - 1) / R) < 2LL * sm_count()) R -= 2;
+    static const int per_sm = std::getenv("B2N_CT_TILES_PER_SM") ? std::atoi(std::getenv("B2N_CT_TILES_PER_SM")) : 0;
+    while (R > 2 && (long long)B * tx * ((OH + R - 1) / R) < (long long)per_sm * sm_count()) R -= 2;
 }
 
 inline int ct_nk(int n) {
