@@ -192,6 +192,12 @@ def main(tag: str):
         sel = [b for k, b in launches if pick[1] in k]
         if len(sel) >= -pick[2]:
             traffic[f"{cfg}/{pick[0]}"] = sel[pick[2]]
+        if cfg != "mlp":  # the two conv weight gradients (+ reduce / SGD), conv1 then conv0 in the backward
+            wg = [b for k, b in launches if "convt_wgrad_kernel" in k]
+            rd = [b for k, b in launches if "convt_wgrad_reduce_kernel" in k]
+            if len(wg) >= 2 and len(rd) >= 2:
+                traffic[f"{cfg}/conv1.wgrad+sgd"] = wg[-2] + rd[-2]
+                traffic[f"{cfg}/conv0.wgrad+sgd"] = wg[-1] + rd[-1]
     # bench.py's ops that are two launches: the FFMA weight gradient + its reduce/SGD pass
     for k in list(traffic):
         if k.endswith(".wgrad") and k + "_reduce+sgd" in traffic:
