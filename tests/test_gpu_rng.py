@@ -160,3 +160,23 @@ def test_dbn_device_draws_equal_host(gpu):
     for a, b in zip(s1, s2):
         _same_params(a, b)
     np.testing.assert_array_equal(ga.state(), gb.state())
+
+
+@pytest.mark.parametrize("skip", [77, 623, 1])
+def test_crbm_train_stream_mid_block(gpu, skip):
+    """the CRBM's streamed loop (691,200 draws per step, 24 generators from jumps) started mid-block --
+    odd and last-word positions -- equals the host's draws in order"""
+    F = _F()
+    B, steps = 100, 3
+    m1, m2 = F.Crbm(1, 28, 28, 12, 5, 5), F.Crbm(1, 28, 28, 12, 5, 5)
+    m1.init(8)
+    m2.init(8)
+    v = O.bernoulli_f32(14, 0.5, steps * B * 784).reshape(steps * B, 1, 28, 28)
+    ga, gb = F.Mt19937(41), F.Mt19937(41)
+    ga._rs.randint(0, 2 ** 32, size=skip, dtype=np.uint64)
+    gb._rs.randint(0, 2 ** 32, size=skip, dtype=np.uint64)
+    rec = m1.train_stream(v, ga, B, 0.1)
+    want = [F.crbm_cd_update(m2, v[i * B:(i + 1) * B], 0.1, gb.canonical(B * 12 * 24 * 24)) for i in range(steps)]
+    np.testing.assert_array_equal(rec, np.array(want))
+    _same_params(m1, m2)
+    np.testing.assert_array_equal(ga.state(), gb.state())
