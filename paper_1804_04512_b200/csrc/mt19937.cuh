@@ -156,6 +156,7 @@ class DevRng {
         if (valid_ && !dirty_ && std::memcmp(s, shadow_, sizeof(shadow_)) == 0) return;
         if (s[kMtN] > (uint32_t)kMtN) throw Error(B2N_EPARAM, "mt19937 state: position must be <= 624");
         std::memcpy(host_.p, s, sizeof(shadow_));
+        host_pending_ = false;
         B2N_CUDA(cudaMemcpyAsync(st_.p, host_.p, sizeof(shadow_), cudaMemcpyHostToDevice, st));
         B2N_CUDA(cudaStreamSynchronize(st));  // host_ is reused by store()
         std::memcpy(shadow_, s, sizeof(shadow_));
@@ -176,6 +177,7 @@ class DevRng {
         launch_ex(mt_canonical_kernel, dim3(g), dim3(256), 0, st, 1u, (const uint32_t*)wbuf_.as<uint32_t>(),
                   (const long long*)(st_.as<uint8_t>() + kMtN * 4 + 16), out, n);
         dirty_ = true;
+        host_pending_ = false;  // host_ (if a stream left it) is older than this draw
         p_ = advance(p_, n);
     }
 
@@ -184,6 +186,7 @@ class DevRng {
     // streams produce the steps' draws concurrently. Bit-identical to draw() called step after step.
     void stream_begin(long long n, cudaStream_t base, int gens = 3) {
         if (!valid_) throw Error(B2N_EPARAM, "device generator used before its state was set");
+        host_pending_ = false;
         if (!sm_.slots.p) {
             sm_.slots.alloc((size_t)kSlots * kSlotBytes);
             sm_.prefix.alloc((size_t)(kMtN * 34) * 4);
@@ -272,14 +275,19 @@ class DevRng {
         if (steps > 0) {
             dirty_ = true;
             p_ = sm_.p[(size_t)steps];
+            // the advanced state comes back with the stream (the caller's sync covers it): store() then
+            // needs no round trip of its own
+            B2N_CUDA(cudaMemcpyAsync(host_.p, st_.p, sizeof(shadow_), cudaMemcpyDeviceToHost, base));
+            host_pending_ = true;
         }
     }
     // copy the device state back (synchronises st); s may be null to just refresh the shadow
     void store(uint32_t* s, cudaStream_t st) {
         if (!valid_) throw Error(B2N_EPARAM, "device generator read before its state was set");
         if (dirty_) {
-            B2N_CUDA(cudaMemcpyAsync(host_.p, st_.p, sizeof(shadow_), cudaMemcpyDeviceToHost, st));
+            if (!host_pending_) B2N_CUDA(cudaMemcpyAsync(host_.p, st_.p, sizeof(shadow_), cudaMemcpyDeviceToHost, st));
             spin_sync(st);
+            host_pending_ = false;
             std::memcpy(shadow_, host_.p, sizeof(shadow_));
             dirty_ = false;
             if (shadow_[kMtN] != (uint32_t)p_) throw Error(B2N_EINTERNAL, "device generator position out of sync");
@@ -341,6 +349,7 @@ class DevRng {
     uint32_t shadow_[kMtN + 1];
     bool valid_ = false;
     bool dirty_ = false;
+    bool host_pending_ = false;  // host_ receives the state at the end of a stream (stream_end)
 };
 
 }  // namespace b2n
